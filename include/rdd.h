@@ -1,0 +1,155 @@
+/*
+ * rdd.h — C ABI of the B200 solve pipeline for the RaNN + overlapping-Schwarz method
+ * (arXiv 2412.19207). The reference library `rannddm` is header-only C++ with Eigen value
+ * types (proj/include/rannddm, *.hpp); it exports no symbols, so this ABI is
+ * the drop-in boundary a reference maintainer binds. Every entry point
+ * names the reference function it replaces.
+ *
+ * Conventions
+ *   - One context per host thread; one CUDA stream per context; calls are synchronous.
+ *   - All pointer arguments are HOST pointers, caller-owned, copied in/out.
+ *   - Dense matrices are column-major (Eigen's default storage order).
+ *   - Return value: RDD_OK or an error class mirroring the reference's exception types;
+ *     rdd_last_error() carries the reference's message text.
+ */
+#ifndef RDD_H
+#define RDD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes: the reference's exception classes */
+#define RDD_OK 0
+#define RDD_INVALID_ARGUMENT 1 /* std::invalid_argument */
+#define RDD_RUNTIME_ERROR 2    /* std::runtime_error    */
+#define RDD_DOMAIN_ERROR 3     /* std::domain_error     */
+#define RDD_CUDA_ERROR 4       /* device failure (no reference analogue) */
+
+/* problems (problems.hpp:43-173 built-ins, plus the BASELINE.json configs) */
+#define RDD_PROBLEM_EXAMPLE1 1   /* problems.hpp:43  -Δu=f, multiscale sines, tanh-ramp L   */
+#define RDD_PROBLEM_EXAMPLE2 2   /* problems.hpp:91  advection-diffusion space-time (no exact) */
+#define RDD_PROBLEM_EXAMPLE3 3   /* problems.hpp:110 3-component -Δu+u=f on the cube          */
+#define RDD_PROBLEM_POISSON 10   /* C1/C5: -Δu=f, u=Π sin(πx_a) on [0,1]^d                   */
+#define RDD_PROBLEM_MULTISCALE 11/* C2: u=sin2πx sin2πy + 0.1 sin50πx sin50πy                 */
+#define RDD_PROBLEM_HEAT 12      /* C3: u_t = 0.1Δu, space-time (x,y,t)                       */
+#define RDD_PROBLEM_ADVECTION 13 /* C4: u_t + 2u_x = 0 on [0,2]x[0,1]                          */
+
+/* decomposition kinds */
+#define RDD_DECOMP_REFERENCE 0 /* geometry.hpp:109 build_decomposition(domain, counts, delta)      */
+#define RDD_DECOMP_CELL 1      /* cell-centred boxes extended by `delta` x width per side (§8d)   */
+
+/* tau modes (reduction.hpp:89 truncate; relative mode = BASELINE's σ/σmax > τ) */
+#define RDD_TAU_OFF 0
+#define RDD_TAU_ABSOLUTE 1
+#define RDD_TAU_RELATIVE 2
+
+#define RDD_PCA_PSI 0        /* reduction.hpp:30 build_sample_matrix           */
+#define RDD_PCA_OP_APPLIED 1 /* reduction.hpp:53 build_operator_sample_matrix  */
+
+/* krylov.hpp:16 SolverKind */
+#define RDD_SOLVER_QR 0
+#define RDD_SOLVER_CG 1
+#define RDD_SOLVER_CGS 2
+#define RDD_SOLVER_BICG 3
+#define RDD_SOLVER_GMRES 4
+
+/* schwarz.hpp:18 SchwarzKind; -1 = none */
+#define RDD_PRECOND_NONE (-1)
+#define RDD_PRECOND_AS 0
+#define RDD_PRECOND_SAS 1
+#define RDD_PRECOND_RAS 2
+
+/* normal-operator formulation used by the Krylov loop */
+#define RDD_OPERATOR_TWO_PASS 0 /* Hᵀ(H·w), runner.hpp:232-234 (reference semantics) */
+#define RDD_OPERATOR_NORMAL 1   /* block-sparse HᵀH from the normal blocks           */
+
+/* Mirrors rannddm::RunConfig (config.hpp:23-68) plus the BASELINE extensions. */
+typedef struct rdd_config {
+  int problem;      /* RDD_PROBLEM_*                                   */
+  int n;            /* example1 complexity (config.hpp:27)             */
+  int dim;          /* filled from the problem when 0                  */
+  int counts[4];    /* subdomains per axis                             */
+  int decomposition;/* RDD_DECOMP_*                                    */
+  double delta;     /* overlap ratio (REFERENCE) or extension (CELL)   */
+  int m;            /* hidden width                                    */
+  int activation;   /* 0 tanh, 1 sin (basis.hpp:14)                    */
+  uint64_t seed;
+  int colloc[4];    /* collocation grid per axis                       */
+  int boundary_per_edge; /* extra cell-centred points per domain edge (2-D, C1) */
+  int test[4];      /* test grid per axis                              */
+  int tau_mode;     /* RDD_TAU_*                                       */
+  double tau;
+  int pca_matrix;   /* RDD_PCA_*                                       */
+  int solver;       /* RDD_SOLVER_*                                    */
+  int precond;      /* RDD_PRECOND_*                                   */
+  double rel_tol;
+  int max_iter;     /* 0 = 10 * DoF (krylov.hpp:78-81)                 */
+  int gmres_restart;/* 0 = full                                        */
+  int op_form;      /* RDD_OPERATOR_* (product only; oracle ignores)   */
+  int true_residual;/* GMRES: diagnostic true residual each step (krylov.hpp:360-367); 1 = as reference */
+} rdd_config;
+
+/* Mirrors rannddm::RunSummary (runner.hpp:147-156) + device phase split. */
+typedef struct rdd_summary {
+  uint64_t seed;
+  int J, DoF, N, p;
+  int iterations;
+  int converged;
+  int breakdown;
+  double e_l2, e_l1n;
+  double t_assemble, t_precond, t_solve, t_evaluate; /* seconds */
+  double t_pca;        /* part of t_assemble (instance build incl. PCA) */
+  double final_residual;
+} rdd_summary;
+
+typedef struct rdd_ctx rdd_ctx;
+
+/* ---- lifecycle ---------------------------------------------------------------------- */
+int rdd_create(rdd_ctx** out, int device);
+void rdd_destroy(rdd_ctx* ctx);
+const char* rdd_last_error(const rdd_ctx* ctx);
+const char* rdd_version(void);
+
+/* ---- pipeline (runner.hpp) ---------------------------------------------------------- */
+/* runner.hpp:40-70 build_instance(cfg, seed): decomposition, collocation grid, random bases
+ * (host SplitMix64, bit-exact), then per-subdomain PCA on the device. */
+int rdd_build_instance(rdd_ctx* ctx, const rdd_config* cfg, uint64_t seed);
+/* runner.hpp:89-101 assemble_equilibrated → assembly.hpp:41-108 assemble, :186-204 column_norms/scale_columns */
+int rdd_assemble(rdd_ctx* ctx, int equilibrate);
+/* assembly.hpp:148-183 normal_blocks + schwarz.hpp:39-61 build_index_sets + :93-148 build_preconditioner */
+int rdd_build_preconditioner(rdd_ctx* ctx, int kind);
+/* runner.hpp:232-251: b = Hᵀ F_c, solve_with (krylov.hpp:391), W ./= scales */
+int rdd_solve(rdd_ctx* ctx, int solver, double rel_tol, int max_iter, int gmres_restart);
+/* runner.hpp:253-256 evaluate_solution + exact_values + compute_errors (problems.hpp:294) */
+int rdd_evaluate(rdd_ctx* ctx, const int* test_res);
+/* runner.hpp:202-275 run_single */
+int rdd_run_single(rdd_ctx* ctx, const rdd_config* cfg, uint64_t seed, rdd_summary* out);
+int rdd_get_summary(rdd_ctx* ctx, rdd_summary* out);
+
+/* ---- operators (pluggable into the reference's LinearMap, krylov.hpp:42-52) ---------- */
+int rdd_matvec(rdd_ctx* ctx, const double* w, double* y);            /* assembly.hpp:110 */
+int rdd_matvec_transpose(rdd_ctx* ctx, const double* r, double* out);/* assembly.hpp:123 */
+int rdd_normal_apply(rdd_ctx* ctx, const double* w, double* out);    /* runner.hpp:233   */
+int rdd_precond_apply(rdd_ctx* ctx, const double* v, double* z, int transpose); /* schwarz.hpp:153/189 */
+
+/* ---- exports (parity tooling; assembly.hpp:206-256 densify/export analogues) --------- */
+/* Returns the element count (or <0 on error). With out == NULL only the count is returned.
+ * Names: see DESIGN.md §ABI (e.g. "rows" j, "p_j", "col_off", "H" j, "F", "scales",
+ * "sigma" j, "V" j, "S" j, "nb" k, "nb_pairs", "local_rank", "W" c, "hist" c, ...). */
+int64_t rdd_get_i(rdd_ctx* ctx, const char* what, int index, int32_t* out, int64_t cap);
+int64_t rdd_get_d(rdd_ctx* ctx, const char* what, int index, double* out, int64_t cap);
+
+/* ---- timing / instrumentation -------------------------------------------------------- */
+/* Device time (ms) of the last call of a named kernel family and its launch count since reset. */
+int rdd_kernel_stats(rdd_ctx* ctx, const char* family, double* ms_total, int64_t* launches);
+int rdd_reset_stats(rdd_ctx* ctx);
+/* Time `reps` calls of the normal operator on device-resident vectors (CUDA events). */
+int rdd_bench_operator(rdd_ctx* ctx, int op_form, int reps, double* ms_per_call, double* bytes_per_call);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RDD_H */

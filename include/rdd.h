@@ -112,6 +112,8 @@ int rdd_create(rdd_ctx** out, int device);
 void rdd_destroy(rdd_ctx* ctx);
 const char* rdd_last_error(const rdd_ctx* ctx);
 const char* rdd_version(void);
+/* ABI self-check: sizeof(rdd_config), sizeof(rdd_summary) as compiled into the library */
+int rdd_abi_sizes(int32_t* config_size, int32_t* summary_size);
 
 /* ---- pipeline (runner.hpp) ---------------------------------------------------------- */
 /* runner.hpp:40-70 build_instance(cfg, seed): decomposition, collocation grid, random bases
@@ -146,6 +148,7 @@ int64_t rdd_get_d(rdd_ctx* ctx, const char* what, int index, double* out, int64_
 /* Device time (ms) of the last call of a named kernel family and its launch count since reset. */
 int rdd_kernel_stats(rdd_ctx* ctx, const char* family, double* ms_total, int64_t* launches);
 int rdd_reset_stats(rdd_ctx* ctx);
+int rdd_set_timing(rdd_ctx* ctx, int on);  /* per-family CUDA-event timing (adds syncs) */
 /* Time `reps` calls of the normal operator on device-resident vectors (CUDA events). */
 int rdd_bench_operator(rdd_ctx* ctx, int op_form, int reps, double* ms_per_call, double* bytes_per_call);
 

@@ -1,0 +1,484 @@
+// api.cu — the C ABI (include/rdd.h) and the run_single orchestration (runner.hpp:202-275).
+//
+// Error mapping mirrors the reference's exception classes: std::invalid_argument -> 1,
+// std::runtime_error -> 2, std::domain_error -> 3, CUDA failures -> 4; the message text is the
+// reference's where the reference has one. There is no CPU fallback: without a CUDA device
+// rdd_create fails and every call reports it.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "ctx.hpp"
+
+struct rdd_ctx {
+  rdd::Ctx c;
+};
+
+namespace rdd {
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void upload_inputs(Ctx& c) {
+  c.pts.upload(c.h_pts, c.stream);
+  std::vector<double> box(static_cast<size_t>(c.J) * 16, 0.0);
+  for (int j = 0; j < c.J; ++j)
+    for (int a = 0; a < 4; ++a) {
+      box[j * 16 + a] = c.box_lo[j * 4 + a];
+      box[j * 16 + 4 + a] = c.box_hi[j * 4 + a];
+      box[j * 16 + 8 + a] = c.box_c[j * 4 + a];
+      box[j * 16 + 12 + a] = c.box_h[j * 4 + a];
+    }
+  c.dbox.upload(box, c.stream);
+  c.dnbr_ptr.upload(c.nbr_ptr, c.stream);
+  c.dnbr_idx.upload(c.nbr_idx, c.stream);
+  c.R.upload(c.h_R, c.stream);
+  c.bvec.upload(c.h_b, c.stream);
+}
+
+static void reset_state(Ctx& c) {
+  c.assembled = false;
+  c.equilibrated = false;
+  c.pkind = RDD_PRECOND_NONE;
+  c.nb_j1.clear();
+  c.nb_j2.clear();
+  c.nb_index.clear();
+  c.nb_off.clear();
+  c.local_rank.clear();
+  c.local_cond.clear();
+  c.hist.clear();
+  c.true_hist.clear();
+  c.iters.clear();
+  c.conv.clear();
+  c.brk.clear();
+  c.approx.clear();
+  c.exact.clear();
+  c.sum = rdd_summary{};
+  c.H = nullptr;
+}
+
+// runner.hpp:40-70
+static void build_instance(Ctx& c, const rdd_config& cfg, uint64_t seed) {
+  reset_state(c);
+  setup_problem(c, cfg, seed);
+  upload_inputs(c);
+  build_index(c);
+  eval_problem(c);
+  run_pca(c);
+  ensure_col_owner(c);
+}
+
+// runner.hpp:89-101 + assembly.hpp:41-108
+static void assemble(Ctx& c, bool equilibrate) {
+  if (c.h_p.empty()) throw std::invalid_argument("assemble: build_instance first");
+  project_blocks(c);
+  // F (assembly.hpp:97-106) was evaluated with the problem closures
+  c.F.ensure(static_cast<size_t>(c.N) * c.C);
+  RDD_CUDA(cudaMemcpyAsync(c.F.p, c.Fpt.p, sizeof(double) * c.N * c.C, cudaMemcpyDeviceToDevice, c.stream));
+  column_norms_scale(c, equilibrate);
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+  c.assembled = true;
+  c.equilibrated = equilibrate;
+}
+
+static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed) {
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+  double t0 = now_s();
+  build_instance(c, cfg, seed);
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+  const double t_pca = now_s() - t0;
+  assemble(c, cfg.precond >= 0);
+  const double t_asm = now_s() - t0;
+  double t_pre = 0.0;
+  if (cfg.solver == RDD_SOLVER_QR) throw std::invalid_argument("qr_direct is a host baseline (oracle), not a device path");
+  if (cfg.precond >= 0) {
+    t0 = now_s();
+    build_normal_blocks(c);
+    build_schwarz(c, cfg.precond);
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    t_pre = now_s() - t0;
+  } else if (cfg.op_form == RDD_OPERATOR_NORMAL) {
+    build_normal_blocks(c);
+  }
+  t0 = now_s();
+  solve_all(c, cfg.solver, cfg.rel_tol, cfg.max_iter, cfg.gmres_restart);
+  const double t_sol = now_s() - t0;
+  t0 = now_s();
+  evaluate(c, cfg.test);
+  const double t_ev = now_s() - t0;
+  rdd_summary& s = c.sum;
+  s.seed = seed;
+  s.J = c.J;
+  s.p = c.p;
+  s.DoF = c.p * c.C;
+  s.N = c.N;
+  int it = 0, cv = 1, bk = 0;
+  double fr = 0.0;
+  for (int k = 0; k < c.C; ++k) {
+    it = std::max(it, c.iters[k]);
+    cv = cv && c.conv[k];
+    bk = bk || c.brk[k];
+    if (!c.hist[k].empty()) fr = std::max(fr, c.hist[k].back());
+  }
+  s.iterations = it;
+  s.converged = cv;
+  s.breakdown = bk;
+  s.final_residual = fr;
+  s.t_pca = t_pca;
+  s.t_assemble = t_asm;
+  s.t_precond = t_pre;
+  s.t_solve = t_sol;
+  s.t_evaluate = t_ev;
+}
+
+}  // namespace rdd
+
+using rdd::Ctx;
+
+template <class F>
+static int guarded(rdd_ctx* h, F&& f) {
+  if (!h) return RDD_INVALID_ARGUMENT;
+  try {
+    RDD_CUDA(cudaSetDevice(h->c.device));
+    f(h->c);
+    return RDD_OK;
+  } catch (const rdd::CudaError& e) {
+    h->c.err = e.what();
+    return RDD_CUDA_ERROR;
+  } catch (const std::invalid_argument& e) {
+    h->c.err = e.what();
+    return RDD_INVALID_ARGUMENT;
+  } catch (const std::domain_error& e) {
+    h->c.err = e.what();
+    return RDD_DOMAIN_ERROR;
+  } catch (const std::exception& e) {
+    h->c.err = e.what();
+    return RDD_RUNTIME_ERROR;
+  }
+}
+
+static void need_assembled(const Ctx& c) {
+  if (!c.assembled) throw std::invalid_argument("system not assembled");
+}
+
+extern "C" {
+
+const char* rdd_version(void) { return "rdd 0.1 (sm_100a, FP64)"; }
+
+int rdd_abi_sizes(int32_t* config_size, int32_t* summary_size) {
+  if (config_size) *config_size = static_cast<int32_t>(sizeof(rdd_config));
+  if (summary_size) *summary_size = static_cast<int32_t>(sizeof(rdd_summary));
+  return RDD_OK;
+}
+
+int rdd_create(rdd_ctx** out, int device) {
+  if (!out) return RDD_INVALID_ARGUMENT;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0) return RDD_CUDA_ERROR;
+  auto* h = new rdd_ctx();
+  h->c.device = device;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaGetDeviceProperties(&h->c.prop, device) != cudaSuccess) {
+    delete h;
+    return RDD_CUDA_ERROR;
+  }
+  *out = h;
+  return RDD_OK;
+}
+
+void rdd_destroy(rdd_ctx* h) {
+  if (!h) return;
+  cudaSetDevice(h->c.device);
+  cudaStreamSynchronize(h->c.stream);
+  cudaStream_t s = h->c.stream;
+  delete h;
+  cudaStreamDestroy(s);
+}
+
+const char* rdd_last_error(const rdd_ctx* h) { return h ? h->c.err.c_str() : "null context"; }
+
+int rdd_build_instance(rdd_ctx* h, const rdd_config* cfg, uint64_t seed) {
+  return guarded(h, [&](Ctx& c) {
+    if (!cfg) throw std::invalid_argument("null config");
+    rdd::build_instance(c, *cfg, seed);
+  });
+}
+int rdd_assemble(rdd_ctx* h, int equilibrate) {
+  return guarded(h, [&](Ctx& c) { rdd::assemble(c, equilibrate != 0); });
+}
+int rdd_build_preconditioner(rdd_ctx* h, int kind) {
+  return guarded(h, [&](Ctx& c) {
+    need_assembled(c);
+    rdd::build_normal_blocks(c);
+    if (kind >= 0) rdd::build_schwarz(c, kind);
+    else c.pkind = RDD_PRECOND_NONE;
+  });
+}
+int rdd_solve(rdd_ctx* h, int solver, double rel_tol, int max_iter, int gmres_restart) {
+  return guarded(h, [&](Ctx& c) {
+    need_assembled(c);
+    rdd::solve_all(c, solver, rel_tol, max_iter, gmres_restart);
+  });
+}
+int rdd_evaluate(rdd_ctx* h, const int* test_res) {
+  return guarded(h, [&](Ctx& c) {
+    if (!c.W.p) throw std::invalid_argument("evaluate: solve first");
+    rdd::evaluate(c, test_res);
+  });
+}
+int rdd_run_single(rdd_ctx* h, const rdd_config* cfg, uint64_t seed, rdd_summary* out) {
+  const int st = guarded(h, [&](Ctx& c) {
+    if (!cfg) throw std::invalid_argument("null config");
+    rdd::run_single(c, *cfg, seed);
+  });
+  if (st == RDD_OK && out) *out = h->c.sum;
+  return st;
+}
+int rdd_get_summary(rdd_ctx* h, rdd_summary* out) {
+  if (!h || !out) return RDD_INVALID_ARGUMENT;
+  *out = h->c.sum;
+  return RDD_OK;
+}
+
+// ---- operators on host vectors
+int rdd_matvec(rdd_ctx* h, const double* w, double* y) {
+  return guarded(h, [&](Ctx& c) {
+    need_assembled(c);
+    rdd::DBuf<double> dw, dy;
+    dw.upload(w, c.p, c.stream);
+    dy.ensure(c.N);
+    rdd::matvec_dev(c, dw.p, dy.p);
+    dy.download(y, c.N, c.stream);
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int rdd_matvec_transpose(rdd_ctx* h, const double* r, double* out) {
+  return guarded(h, [&](Ctx& c) {
+    need_assembled(c);
+    rdd::DBuf<double> dr, dout;
+    dr.upload(r, c.N, c.stream);
+    dout.ensure(c.p);
+    rdd::matvec_t_dev(c, dr.p, dout.p);
+    dout.download(out, c.p, c.stream);
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int rdd_normal_apply(rdd_ctx* h, const double* w, double* out) {
+  return guarded(h, [&](Ctx& c) {
+    need_assembled(c);
+    rdd::DBuf<double> dw, dout;
+    dw.upload(w, c.p, c.stream);
+    dout.ensure(c.p);
+    rdd::normal_operator(c, dw.p, dout.p);
+    dout.download(out, c.p, c.stream);
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int rdd_precond_apply(rdd_ctx* h, const double* v, double* z, int transpose) {
+  return guarded(h, [&](Ctx& c) {
+    if (c.pkind < 0) throw std::invalid_argument("no preconditioner built");
+    rdd::DBuf<double> dv, dz;
+    dv.upload(v, c.p, c.stream);
+    dz.ensure(c.p);
+    rdd::precond_apply_dev(c, dv.p, dz.p, transpose != 0);
+    dz.download(z, c.p, c.stream);
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+// ---- exports
+int64_t rdd_get_i(rdd_ctx* h, const char* what, int index, int32_t* out, int64_t cap) {
+  if (!h || !what) return -1;
+  Ctx& c = h->c;
+  std::vector<int> v;
+  try {
+    const std::string w(what);
+    if (w == "J") v = {c.J};
+    else if (w == "N") v = {c.N};
+    else if (w == "p") v = {c.p};
+    else if (w == "dim") v = {c.d};
+    else if (w == "C") v = {c.C};
+    else if (w == "maxcov") v = {c.maxcov};
+    else if (w == "p_j") v = c.h_p;
+    else if (w == "col_off") v = c.h_col_off;
+    else if (w == "rows") {
+      const int n = c.h_row_ptr.at(index + 1) - c.h_row_ptr.at(index);
+      v.resize(n);
+      if (n) RDD_CUDA(cudaMemcpy(v.data(), c.row_idx.p + c.h_row_ptr[index], sizeof(int) * n, cudaMemcpyDeviceToHost));
+    } else if (w == "nbr") v.assign(c.nbr_idx.begin() + c.nbr_ptr.at(index), c.nbr_idx.begin() + c.nbr_ptr.at(index + 1));
+    else if (w == "nb_pairs") {
+      for (size_t k = 0; k < c.nb_j1.size(); ++k) {
+        v.push_back(c.nb_j1[k]);
+        v.push_back(c.nb_j2[k]);
+      }
+    } else if (w == "local_rank") v = c.local_rank;
+    else if (w == "set") v.assign(c.set_idx.begin() + c.set_ptr.at(index), c.set_idx.begin() + c.set_ptr.at(index + 1));
+    else if (w == "owner") v = c.h_owner;
+    else if (w == "mult") v = c.h_mult;
+    else if (w == "iterations") v = c.iters;
+    else if (w == "converged") v = c.conv;
+    else {
+      c.err = "unknown export " + w;
+      return -1;
+    }
+  } catch (const std::exception& e) {
+    c.err = e.what();
+    return -1;
+  }
+  const int64_t n = static_cast<int64_t>(v.size());
+  if (out) std::copy(v.begin(), v.begin() + std::min(n, cap), out);
+  return n;
+}
+
+int64_t rdd_get_d(rdd_ctx* h, const char* what, int index, double* out, int64_t cap) {
+  if (!h || !what) return -1;
+  Ctx& c = h->c;
+  std::vector<double> v;
+  auto dl = [&](const double* src, size_t n) {
+    v.resize(n);
+    if (n) RDD_CUDA(cudaMemcpy(v.data(), src, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  };
+  try {
+    const std::string w(what);
+    const int rows = (index >= 0 && index + 1 < static_cast<int>(c.h_row_ptr.size()))
+                         ? c.h_row_ptr[index + 1] - c.h_row_ptr[index] : 0;
+    if (w == "points") {
+      for (int i = 0; i < c.N; ++i)
+        for (int a = 0; a < c.d; ++a) v.push_back(c.h_pts[static_cast<size_t>(a) * c.N + i]);
+    } else if (w == "box_lo" || w == "box_hi") {
+      const auto& src = w == "box_lo" ? c.box_lo : c.box_hi;
+      for (int j = 0; j < c.J; ++j)
+        for (int a = 0; a < c.d; ++a) v.push_back(src[j * 4 + a]);
+    } else if (w == "R") {  // m x d column-major (the oracle's layout)
+      v.resize(static_cast<size_t>(c.m) * c.d);
+      for (int k = 0; k < c.m; ++k)
+        for (int a = 0; a < c.d; ++a) v[k + a * c.m] = c.h_R[(static_cast<size_t>(index) * c.m + k) * c.d + a];
+    } else if (w == "b") {
+      v.assign(c.h_b.begin() + static_cast<size_t>(index) * c.m, c.h_b.begin() + static_cast<size_t>(index + 1) * c.m);
+    } else if (w == "S") {
+      dl(c.S.p + c.S_off.at(index), static_cast<size_t>(rows) * c.m);
+    } else if (w == "sigma") {
+      if (c.identity_V) throw std::invalid_argument("no PCA");
+      dl(c.sigma.p + static_cast<size_t>(index) * c.m, std::min(rows, c.m));
+    } else if (w == "V") {
+      if (c.identity_V) throw std::invalid_argument("no PCA");
+      dl(c.Vred.p + static_cast<size_t>(index) * c.m * c.m, static_cast<size_t>(c.m) * c.h_p.at(index));
+    } else if (w == "H") {
+      need_assembled(c);
+      dl(c.H + c.H_off.at(index), static_cast<size_t>(rows) * c.h_p.at(index));
+    } else if (w == "F") {
+      dl(c.F.p ? c.F.p : c.Fpt.p, static_cast<size_t>(c.N) * c.C);
+    } else if (w == "scales") {
+      dl(c.scales.p, c.p);
+    } else if (w == "nb") {
+      const size_t k = static_cast<size_t>(index);
+      dl(c.NB.p + c.nb_off.at(k), static_cast<size_t>(c.nb_off.at(k + 1) - c.nb_off[k]));
+    } else if (w == "nb_dense") {
+      v.assign(static_cast<size_t>(c.p) * c.p, 0.0);
+      std::vector<double> blk;
+      for (size_t k = 0; k < c.nb_j1.size(); ++k) {
+        const int j1 = c.nb_j1[k], j2 = c.nb_j2[k], p1 = c.h_p[j1], p2 = c.h_p[j2];
+        blk.resize(static_cast<size_t>(p1) * p2);
+        RDD_CUDA(cudaMemcpy(blk.data(), c.NB.p + c.nb_off[k], sizeof(double) * blk.size(), cudaMemcpyDeviceToHost));
+        for (int cc = 0; cc < p2; ++cc)
+          for (int r = 0; r < p1; ++r) {
+            const size_t a = c.h_col_off[j1] + r, b = c.h_col_off[j2] + cc;
+            v[a + b * c.p] = blk[r + static_cast<size_t>(cc) * p1];
+            if (j1 != j2) v[b + a * c.p] = blk[r + static_cast<size_t>(cc) * p1];
+          }
+      }
+    } else if (w == "H_dense") {
+      need_assembled(c);
+      v.assign(static_cast<size_t>(c.N) * c.p, 0.0);
+      std::vector<double> blk;
+      std::vector<int> ridx;
+      for (int j = 0; j < c.J; ++j) {
+        const int nr = c.h_row_ptr[j + 1] - c.h_row_ptr[j], pj = c.h_p[j];
+        blk.resize(static_cast<size_t>(nr) * pj);
+        ridx.resize(nr);
+        if (nr == 0) continue;
+        RDD_CUDA(cudaMemcpy(blk.data(), c.H + c.H_off[j], sizeof(double) * blk.size(), cudaMemcpyDeviceToHost));
+        RDD_CUDA(cudaMemcpy(ridx.data(), c.row_idx.p + c.h_row_ptr[j], sizeof(int) * nr, cudaMemcpyDeviceToHost));
+        for (int cc = 0; cc < pj; ++cc)
+          for (int r = 0; r < nr; ++r)
+            v[ridx[r] + static_cast<size_t>(c.h_col_off[j] + cc) * c.N] = blk[r + static_cast<size_t>(cc) * nr];
+      }
+    } else if (w == "local_cond") {
+      v = c.local_cond;
+    } else if (w == "W") {
+      dl(c.W.p + static_cast<size_t>(index) * c.p, c.p);
+    } else if (w == "hist") {
+      v = c.hist.at(index);
+    } else if (w == "true_hist") {
+      v = c.true_hist.at(index);
+    } else if (w == "approx") {
+      v = c.approx;
+    } else if (w == "exact") {
+      v = c.exact;
+    } else {
+      c.err = "unknown export " + w;
+      return -1;
+    }
+  } catch (const std::exception& e) {
+    c.err = e.what();
+    return -1;
+  }
+  const int64_t n = static_cast<int64_t>(v.size());
+  if (out) std::copy(v.begin(), v.begin() + std::min(n, cap), out);
+  return n;
+}
+
+// ---- instrumentation
+int rdd_kernel_stats(rdd_ctx* h, const char* family, double* ms_total, int64_t* launches) {
+  if (!h || !family) return RDD_INVALID_ARGUMENT;
+  auto it = h->c.stats.find(family);
+  if (ms_total) *ms_total = it == h->c.stats.end() ? 0.0 : it->second.ms;
+  if (launches) *launches = it == h->c.stats.end() ? 0 : it->second.launches;
+  return RDD_OK;
+}
+int rdd_reset_stats(rdd_ctx* h) {
+  if (!h) return RDD_INVALID_ARGUMENT;
+  h->c.stats.clear();
+  return RDD_OK;
+}
+int rdd_set_timing(rdd_ctx* h, int on) {
+  if (!h) return RDD_INVALID_ARGUMENT;
+  h->c.timing = on != 0;
+  return RDD_OK;
+}
+
+int rdd_bench_operator(rdd_ctx* h, int op_form, int reps, double* ms_per_call, double* bytes_per_call) {
+  return guarded(h, [&](Ctx& c) {
+    need_assembled(c);
+    if (op_form == RDD_OPERATOR_NORMAL && !c.NB.p) rdd::build_normal_blocks(c);
+    rdd::DBuf<double> w, out;
+    w.ensure(c.p);
+    out.ensure(c.p);
+    RDD_CUDA(cudaMemsetAsync(w.p, 0, sizeof(double) * c.p, c.stream));
+    c.ytmp.ensure(c.N);
+    const int saved = c.cfg.op_form;
+    c.cfg.op_form = op_form;
+    for (int i = 0; i < 3; ++i) rdd::normal_operator(c, w.p, out.p);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c.stream);
+    for (int i = 0; i < reps; ++i) rdd::normal_operator(c, w.p, out.p);
+    cudaEventRecord(e1, c.stream);
+    RDD_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    c.cfg.op_form = saved;
+    *ms_per_call = ms / reps;
+    if (op_form == RDD_OPERATOR_NORMAL)
+      *bytes_per_call = 8.0 * static_cast<double>(c.nb_off.back()) + 8.0 * 2 * c.p;
+    else  // two passes over H + vectors + row maps
+      *bytes_per_call = 2.0 * (8.0 * static_cast<double>(c.H_off[c.J]) + 8.0 * (c.p + c.N) + 4.0 * c.sum_rows);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// common.cuh — shared device/host utilities for librdd (B200, sm_100a, FP64).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace rdd {
+
+constexpr int kMaxDim = 4;
+constexpr int kMaxJet = 15;  // jet_len(4)
+
+__host__ __device__ constexpr int jet_len(int d) { return 1 + d + d * (d + 1) / 2; }
+__host__ __device__ constexpr int hess_index(int i, int j, int d) { return i * d - i * (i - 1) / 2 + (j - i); }
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what + " at " + file + ":" +
+                    std::to_string(line));
+}
+#define RDD_CUDA(x) ::rdd::check_cuda((x), #x, __FILE__, __LINE__)
+#define RDD_LAUNCH_CHECK() ::rdd::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Owning device buffer (cudaMalloc; grows, never shrinks).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* ensure(size_t count) {
+    if (count > n) {
+      release();
+      if (count) RDD_CUDA(cudaMalloc(&p, count * sizeof(T)));
+      n = count;
+    }
+    return p;
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    ensure(count);
+    if (count) RDD_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& h, cudaStream_t s) { upload(h.data(), h.size(), s); }
+  void download(T* h, size_t count, cudaStream_t s) const {
+    if (count) RDD_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  }
+  void zero(size_t count, cudaStream_t s) {
+    ensure(count);
+    if (count) RDD_CUDA(cudaMemsetAsync(p, 0, count * sizeof(T), s));
+  }
+};
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// ---- device helpers --------------------------------------------------------------------
+#ifdef __CUDACC__
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_min(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Second-order jet in dimension d (value, gradient, packed upper Hessian), jet.hpp:45-156.
+struct Jet {
+  double c[kMaxJet];
+};
+
+__device__ __forceinline__ void jet_zero(Jet& a, int d) {
+  for (int i = 0; i < jet_len(d); ++i) a.c[i] = 0.0;
+}
+// Leibniz product (jet.hpp:107-124), grouped like the reference.
+__device__ __forceinline__ Jet jet_mul(const Jet& a, const Jet& b, int d) {
+  Jet o;
+  o.c[0] = a.c[0] * b.c[0];
+  for (int i = 0; i < d; ++i) o.c[1 + i] = a.c[0] * b.c[1 + i] + b.c[0] * a.c[1 + i];
+  for (int i = 0; i < d; ++i)
+    for (int j = i; j < d; ++j) {
+      const int k = 1 + d + hess_index(i, j, d);
+      o.c[k] = (a.c[0] * b.c[k] + b.c[0] * a.c[k]) + (a.c[1 + i] * b.c[1 + j] + a.c[1 + j] * b.c[1 + i]);
+    }
+  return o;
+}
+// chain rule through a univariate function (jet.hpp:127-138)
+__device__ __forceinline__ Jet jet_compose(double f, double df, double d2f, const Jet& a, int d) {
+  Jet o;
+  o.c[0] = f;
+  for (int i = 0; i < d; ++i) o.c[1 + i] = df * a.c[1 + i];
+  for (int i = 0; i < d; ++i)
+    for (int j = i; j < d; ++j) {
+      const int k = 1 + d + hess_index(i, j, d);
+      o.c[k] = df * a.c[k] + d2f * a.c[1 + i] * a.c[1 + j];
+    }
+  return o;
+}
+
+#endif  // __CUDACC__
+
+}  // namespace rdd

@@ -1,0 +1,215 @@
+// ctx.hpp — the solver context behind the C ABI: host geometry + device-resident state.
+//
+// HBM layout (DESIGN.md §Data layout):
+//   pts        d x N doubles, axis-major (SoA)           collocation points (uploaded, bit-exact)
+//   row_ptr    J+1 ints; row_idx Σrows ints              rows_j: ascending global ids (assembly.hpp:58-64)
+//   cov_j/r    N x maxcov ints                           per-point covering (block, local row)
+//   Ljet       N x jet_len doubles                       L(x) jets; F  N x C (column-major)
+//   S          Σ_j rows_j*m doubles, per-block column-major   unreduced (op_applied/psi) blocks
+//   H          Σ_j rows_j*p_j doubles, per-block column-major reduced, equilibrated blocks
+//   NB         Σ_pairs p_j1*p_j2 doubles                  normal blocks H_j1ᵀH_j2 (j1 <= j2)
+//   P          Σ_i n_i*n_i doubles                        local (pseudo-)inverses (Schwarz)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/rdd.h"
+#include "common.cuh"
+
+namespace rdd {
+
+// Problem on the device: id + operator coefficients over the jet (operators.hpp as c·jet).
+struct ProblemDesc {
+  int id = 0;
+  int d = 2;
+  int C = 1;
+  int n = 2;          // example1 complexity
+  double lo[kMaxDim] = {0, 0, 0, 0}, hi[kMaxDim] = {1, 1, 1, 1};
+  double coef[kMaxJet] = {0};
+  bool has_exact = true;
+};
+
+struct KernelStat {
+  double ms = 0.0;
+  int64_t launches = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  cudaDeviceProp prop{};
+
+  // ---- configuration
+  rdd_config cfg{};
+  uint64_t seed = 0;
+  ProblemDesc prob;
+  int d = 2, J = 0, N = 0, m = 0, C = 1, jl = 6;
+
+  // ---- host geometry (geometry.hpp:84-185)
+  std::vector<double> box_lo, box_hi, box_c, box_h;  // J x 4
+  std::vector<int> counts;
+  std::vector<std::vector<double>> axis_lo, axis_hi;  // per axis, per index
+  std::vector<int> nbr_ptr, nbr_idx;                  // CSR, ascending, includes self
+  std::vector<double> h_pts;                          // d x N (axis-major)
+  std::vector<double> h_R, h_b;                       // J*m*d (k-major, then axis), J*m
+
+  // ---- device: inputs
+  DBuf<double> pts, dbox;  // dbox: J x 16 (lo[4], hi[4], center[4], half[4])
+  DBuf<double> daxis;      // per axis: lo/hi interval arrays (offsets in axis_off)
+  std::vector<int> axis_off;
+  DBuf<int> dnbr_ptr, dnbr_idx;
+  DBuf<double> R, bvec;
+  DBuf<double> Ljet, Fpt;  // N x jl, N x C
+
+  // ---- device: indexing (K1)
+  std::vector<int> h_row_ptr;
+  DBuf<int> row_ptr, row_idx;
+  int maxcov = 0;
+  DBuf<int> cov_j, cov_r, cov_n;
+  long long sum_rows = 0;
+
+  // ---- PCA (K2-K5)
+  bool identity_V = true;
+  std::vector<int> h_p;            // p_j
+  std::vector<int> h_col_off;      // J+1
+  int p = 0;
+  DBuf<double> S;                  // unreduced sample blocks (Σ rows_j*m)
+  std::vector<long long> S_off;    // J+1 (elements)
+  DBuf<double> Vred;               // J x m x m (columns 0..p_j-1 used)
+  DBuf<double> sigma;              // J x m
+  DBuf<int> dp_j;
+
+  // ---- assembled system
+  DBuf<double> Hbuf;               // reduced blocks (or alias of S when identity)
+  double* H = nullptr;
+  std::vector<long long> H_off;    // J+1 (elements)
+  DBuf<long long> dH_off;
+  DBuf<int> dcol_off;
+  DBuf<double> scales;             // p
+  DBuf<double> F;                  // N x C (column-major)
+  bool assembled = false;
+  bool equilibrated = false;
+
+  // ---- normal blocks (assembly.hpp:137-183)
+  std::vector<int> nb_j1, nb_j2;   // pairs j1 <= j2 with non-empty row intersection
+  std::vector<long long> nb_off;   // element offsets into NB
+  DBuf<double> NB;
+  std::map<std::pair<int, int>, int> nb_index;
+  DBuf<long long> nb_look;         // per neighbour-CSR entry: NB offset or -1
+
+  // ---- Schwarz (schwarz.hpp)
+  int pkind = RDD_PRECOND_NONE;
+  std::vector<int> set_ptr, set_idx;  // S_i (CSR)
+  std::vector<int> h_owner, h_mult;
+  std::vector<int> local_rank;
+  std::vector<double> local_cond;
+  std::vector<long long> P_off;       // per i: offset of the n_i x n_i local inverse
+  DBuf<double> P;
+  DBuf<int> dset_ptr, dset_idx, dmult, downer;
+  DBuf<long long> dP_off;
+  // owner-gather map for the AS/SAS reduction: per column c, list of (i, position)
+  DBuf<int> gat_ptr, gat_pos, gat_owner_pos;
+  int nmax_local = 0;
+  DBuf<double> zloc;                  // Σ n_i
+
+  // ---- Krylov
+  DBuf<double> work;                  // vectors
+  DBuf<double> scal;                  // device scalars
+  std::vector<std::vector<double>> hist, true_hist;
+  std::vector<int> iters, conv, brk;
+  DBuf<double> W;                     // p x C (unscaled)
+  DBuf<double> ytmp;                  // N
+
+  // ---- evaluation
+  std::vector<double> approx, exact;  // M x C (host copies)
+  rdd_summary sum{};
+
+  // ---- instrumentation
+  std::map<std::string, KernelStat> stats;
+  bool timing = false;
+
+  double* wk(size_t count) { return work.ensure(count); }
+};
+
+// timing helper: records device time of a kernel family when ctx.timing is on
+struct ScopedKernelTimer {
+  Ctx& c;
+  const char* fam;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ScopedKernelTimer(Ctx& ctx, const char* family) : c(ctx), fam(family) {
+    if (c.timing) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, c.stream);
+    }
+  }
+  ~ScopedKernelTimer() {
+    if (c.timing) {
+      cudaEventRecord(e1, c.stream);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      auto& s = c.stats[fam];
+      s.ms += ms;
+      s.launches += 1;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+  }
+};
+
+// ---- module entry points (one per reference function family) -----------------------
+// host_setup.cpp
+void setup_problem(Ctx& c, const rdd_config& cfg, uint64_t seed);  // problems + geometry + bases + points
+void upload_inputs(Ctx& c);
+// index.cu (K1)
+void build_index(Ctx& c);
+// problem.cu
+void eval_problem(Ctx& c);
+// assemble.cu (K2)
+void assemble_samples(Ctx& c, int kind, double* out, const std::vector<long long>& off);
+// pca.cu (K3-K5)
+void run_pca(Ctx& c);
+// equil.cu (K6) + matvec.cu (K9/K10)
+void column_norms_scale(Ctx& c, bool equilibrate);
+void matvec_dev(Ctx& c, const double* w, double* y);
+void matvec_t_dev(Ctx& c, const double* r, double* out);
+// normal.cu (K7)
+void build_normal_blocks(Ctx& c);
+void normal_apply_dev(Ctx& c, const double* w, double* out);
+void normal_operator(Ctx& c, const double* w, double* out);  // runner.hpp:232-234
+// schwarz.cu (K8/K11)
+void build_schwarz(Ctx& c, int kind);
+void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose);
+// krylov.cu (K12/K13)
+void solve_all(Ctx& c, int solver, double tol, int max_iter, int restart);
+// evaluate.cu (K14)
+void evaluate(Ctx& c, const int* test_res);
+// gemm.cu
+struct GemmTask {
+  const double* A;
+  const double* B;
+  double* Cm;
+  const int* gA;   // optional row gather for op(A)'s K index (TN mode)
+  const int* gB;
+  int M, N, K, lda, ldb, ldc;
+  int tm, tn;      // tile indices
+  double beta;     // C = alpha * op(A) op(B) + beta * C
+  double alpha = 1.0;
+};
+void gemm_tn(Ctx& c, const std::vector<GemmTask>& tasks);  // C = Aᵀ B (A: K x M, B: K x N col-major)
+void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks);  // C = A B  (A: M x K, B: K x N col-major)
+void gemm_nt(Ctx& c, const std::vector<GemmTask>& tasks);  // C = A Bᵀ (A: M x K, B: N x K col-major)
+void project_blocks(Ctx& c);
+void ensure_col_owner(Ctx& c);
+// jacobi.cu
+void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vector<int>& n,
+                   const std::vector<long long>& offA, int max_sweeps, bool relative);
+
+}  // namespace rdd

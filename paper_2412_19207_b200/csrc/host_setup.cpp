@@ -1,0 +1,223 @@
+// host_setup.cpp — host half of build_instance (runner.hpp:40-70): problem descriptor,
+// decomposition (geometry.hpp:109-177 or the BASELINE cell layout), collocation grid
+// (geometry.hpp:200-232) and random bases (basis.hpp:33-48, random.hpp:9-37).
+//
+// These are O(J^2 + N) host computations whose outputs must be bit-identical to the
+// reference's (they fix the point->subdomain indexing and the frozen weights), so they are
+// computed here with the reference's operation order (compiled with -ffp-contract=off) and
+// uploaded; everything downstream runs on the device.
+#include <cmath>
+#include <stdexcept>
+#include <string>
+
+#include "ctx.hpp"
+
+namespace rdd {
+
+namespace {
+
+struct Mix {
+  uint64_t s;
+  uint64_t next() {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  }
+  double sym() { return 2.0 * (static_cast<double>(next() >> 11) * 0x1.0p-53) - 1.0; }
+};
+
+uint64_t subdomain_seed(uint64_t base, int j) {
+  Mix m{base ^ (0xD1B54A32D192ED03ULL * static_cast<uint64_t>(j + 1))};
+  return m.next();
+}
+
+constexpr double kPi = 3.14159265358979323846;
+
+void set_coef_laplacian(ProblemDesc& P, double sign_h, double c_v) {
+  for (auto& x : P.coef) x = 0.0;
+  P.coef[0] = c_v;
+  for (int a = 0; a < P.d; ++a) P.coef[1 + P.d + hess_index(a, a, P.d)] = sign_h;
+}
+
+ProblemDesc make_desc(const rdd_config& cfg) {
+  ProblemDesc P;
+  P.id = cfg.problem;
+  P.n = cfg.n;
+  switch (cfg.problem) {
+    case RDD_PROBLEM_EXAMPLE1:
+      if (cfg.n < 1 || cfg.n > 8) throw std::invalid_argument("example1: n must be in [1,8]");
+      P.d = 2;
+      set_coef_laplacian(P, -1.0, 0.0);  // operators.hpp:19-25
+      break;
+    case RDD_PROBLEM_EXAMPLE2:
+      P.d = 2;
+      P.lo[0] = -1.0;
+      for (auto& x : P.coef) x = 0.0;  // operators.hpp:37-41: u_t + u_x - kappa u_xx
+      P.coef[1] = 1.0;
+      P.coef[2] = 1.0;
+      P.coef[3] = -(0.1 / kPi);
+      P.has_exact = false;
+      break;
+    case RDD_PROBLEM_EXAMPLE3:
+      P.d = 3;
+      P.C = 3;
+      set_coef_laplacian(P, -1.0, 1.0);  // operators.hpp:28-34
+      break;
+    case RDD_PROBLEM_POISSON:
+      P.d = cfg.dim == 0 ? 2 : cfg.dim;
+      if (P.d < 1 || P.d > 3) throw std::invalid_argument("poisson: dimension must be 1..3");
+      set_coef_laplacian(P, -1.0, 0.0);
+      break;
+    case RDD_PROBLEM_MULTISCALE:
+      P.d = 2;
+      set_coef_laplacian(P, -1.0, 0.0);
+      break;
+    case RDD_PROBLEM_HEAT:  // u_t - 0.1 (u_xx + u_yy)
+      P.d = 3;
+      for (auto& x : P.coef) x = 0.0;
+      P.coef[3] = 1.0;
+      P.coef[1 + 3 + hess_index(0, 0, 3)] = -0.1;
+      P.coef[1 + 3 + hess_index(1, 1, 3)] = -0.1;
+      break;
+    case RDD_PROBLEM_ADVECTION:  // u_t + 2 u_x on [0,2] x [0,1]
+      P.d = 2;
+      P.hi[0] = 2.0;
+      for (auto& x : P.coef) x = 0.0;
+      P.coef[1] = 2.0;
+      P.coef[2] = 1.0;
+      break;
+    default:
+      throw std::invalid_argument("unknown problem id " + std::to_string(cfg.problem));
+  }
+  return P;
+}
+
+bool interiors_intersect(const Ctx& c, int i, int j) {  // geometry.hpp:99-105
+  for (int a = 0; a < c.d; ++a) {
+    const double lo = std::max(c.box_lo[i * 4 + a], c.box_lo[j * 4 + a]);
+    const double hi = std::min(c.box_hi[i * 4 + a], c.box_hi[j * 4 + a]);
+    if (!(lo < hi)) return false;
+  }
+  return true;
+}
+
+}  // namespace
+
+void setup_problem(Ctx& c, const rdd_config& cfg, uint64_t seed) {
+  c.cfg = cfg;
+  c.seed = seed;
+  c.prob = make_desc(cfg);
+  const int d = c.d = c.prob.d;
+  c.C = c.prob.C;
+  c.jl = jet_len(d);
+  c.m = cfg.m;
+  if (cfg.m < 1) throw std::invalid_argument("hidden width m must be >= 1");
+  c.counts.assign(cfg.counts, cfg.counts + d);
+  for (int k : c.counts)
+    if (k < 1) throw std::invalid_argument("per-axis subdomain counts must be >= 1");
+
+  // ---- per-axis centres / half widths
+  std::vector<std::vector<double>> ac(d);
+  std::vector<double> ah(d);
+  for (int a = 0; a < d; ++a) {
+    const int l = c.counts[a];
+    const double lo = c.prob.lo[a], len = c.prob.hi[a] - c.prob.lo[a];
+    if (l == 1) {
+      ac[a] = {lo + 0.5 * len};
+      ah[a] = 0.5 * len;
+    } else if (cfg.decomposition == RDD_DECOMP_REFERENCE) {  // geometry.hpp:125-137
+      if (!(cfg.delta > 1.0)) throw std::invalid_argument("overlap ratio delta must exceed 1");
+      ah[a] = (cfg.delta / 2.0) / static_cast<double>(l - 1) * len;
+      for (int j = 0; j < l; ++j) ac[a].push_back(lo + static_cast<double>(j) / static_cast<double>(l - 1) * len);
+    } else {  // cell-centred, extended by delta x width per side
+      if (!(cfg.delta > 0.0)) throw std::invalid_argument("cell decomposition extension must be positive");
+      ah[a] = (0.5 + cfg.delta) / static_cast<double>(l) * len;
+      for (int j = 0; j < l; ++j) ac[a].push_back(lo + (static_cast<double>(j) + 0.5) / static_cast<double>(l) * len);
+    }
+  }
+  int total = 1;
+  for (int k : c.counts) total *= k;
+  c.J = total;
+  c.box_lo.assign(total * 4, 0.0);
+  c.box_hi.assign(total * 4, 0.0);
+  c.box_c.assign(total * 4, 0.0);
+  c.box_h.assign(total * 4, 0.0);
+  c.axis_lo.assign(d, {});
+  c.axis_hi.assign(d, {});
+  for (int a = 0; a < d; ++a)
+    for (size_t k = 0; k < ac[a].size(); ++k) {
+      c.axis_lo[a].push_back(ac[a][k] - ah[a]);
+      c.axis_hi[a].push_back(ac[a][k] + ah[a]);
+    }
+  std::vector<int> idx(d, 0);
+  for (int flat = 0; flat < total; ++flat) {  // axis 0 slowest (geometry.hpp:146-167)
+    for (int a = 0; a < d; ++a) {
+      const double cc = ac[a][idx[a]], hh = ah[a];
+      c.box_c[flat * 4 + a] = cc;
+      c.box_h[flat * 4 + a] = hh;
+      c.box_lo[flat * 4 + a] = cc - hh;
+      c.box_hi[flat * 4 + a] = cc + hh;
+    }
+    for (int a = d - 1; a >= 0; --a) {
+      if (++idx[a] < c.counts[a]) break;
+      idx[a] = 0;
+    }
+  }
+  // neighbour sets (geometry.hpp:169-174): per-axis interval overlap in the tensor product
+  c.nbr_ptr.assign(total + 1, 0);
+  c.nbr_idx.clear();
+  for (int i = 0; i < total; ++i) {
+    for (int j = 0; j < total; ++j)
+      if (interiors_intersect(c, i, j)) c.nbr_idx.push_back(j);
+    c.nbr_ptr[i + 1] = static_cast<int>(c.nbr_idx.size());
+  }
+
+  // ---- collocation points (geometry.hpp:200-232) + optional edge points
+  std::vector<int> res(cfg.colloc, cfg.colloc + d);
+  for (int r : res)
+    if (r < 1) throw std::invalid_argument("grid resolutions must be >= 1");
+  long long n = 1;
+  for (int r : res) n *= r;
+  const int nb = cfg.boundary_per_edge;
+  if (nb > 0 && d != 2) throw std::invalid_argument("boundary points are defined for 2-D domains only");
+  const long long Ntot = n + (nb > 0 ? 4LL * nb : 0);
+  if (Ntot > 2000000000LL) throw std::invalid_argument("too many collocation points");
+  c.N = static_cast<int>(Ntot);
+  c.h_pts.assign(static_cast<size_t>(d) * c.N, 0.0);
+  std::vector<int> gi(d, 0);
+  std::vector<double> step(d);
+  for (int a = 0; a < d; ++a) step[a] = (c.prob.hi[a] - c.prob.lo[a]) / static_cast<double>(res[a]);
+  for (long long flat = 0; flat < n; ++flat) {
+    for (int a = 0; a < d; ++a)
+      c.h_pts[static_cast<size_t>(a) * c.N + flat] = c.prob.lo[a] + (static_cast<double>(gi[a]) + 0.5) * step[a];
+    for (int a = d - 1; a >= 0; --a) {
+      if (++gi[a] < res[a]) break;
+      gi[a] = 0;
+    }
+  }
+  if (nb > 0) {
+    long long q = n;
+    for (int e = 0; e < 4; ++e) {
+      const int axis = e < 2 ? 0 : 1, fixed = 1 - axis;
+      const double fv = (e % 2 == 0) ? c.prob.lo[fixed] : c.prob.hi[fixed];
+      const double st = (c.prob.hi[axis] - c.prob.lo[axis]) / static_cast<double>(nb);
+      for (int k = 0; k < nb; ++k, ++q) {
+        c.h_pts[static_cast<size_t>(axis) * c.N + q] = c.prob.lo[axis] + (static_cast<double>(k) + 0.5) * st;
+        c.h_pts[static_cast<size_t>(fixed) * c.N + q] = fv;
+      }
+    }
+  }
+
+  // ---- random bases: R (m x d, drawn k-major then axis) then b (basis.hpp:43-46)
+  c.h_R.assign(static_cast<size_t>(total) * c.m * d, 0.0);
+  c.h_b.assign(static_cast<size_t>(total) * c.m, 0.0);
+  for (int j = 0; j < total; ++j) {
+    Mix rng{subdomain_seed(seed, j)};
+    for (int k = 0; k < c.m; ++k)
+      for (int a = 0; a < d; ++a) c.h_R[(static_cast<size_t>(j) * c.m + k) * d + a] = rng.sym();
+    for (int k = 0; k < c.m; ++k) c.h_b[static_cast<size_t>(j) * c.m + k] = rng.sym();
+  }
+}
+
+}  // namespace rdd

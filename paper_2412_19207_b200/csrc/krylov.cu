@@ -1,0 +1,508 @@
+// krylov.cu — K12/K13: PCG and GMRES(m) drivers (krylov.hpp:106-156, 275-389).
+//
+// All scalars live on the device. Reductions are deterministic two-stage (fixed-size grid of
+// per-CTA partials, summed in order by the consumer), so reruns are bit-identical like the
+// reference's (test_runner.cpp:109-117). CG keeps its control state (iteration, status, rz,
+// histories) on the device: every kernel of an iteration is a no-op once the status leaves
+// RUNNING, so an iteration is a fixed sequence of launches that is captured once into a CUDA
+// graph and replayed with a device-side while condition (cudaGraphCondTypeWhile).
+// GMRES uses classical Gram–Schmidt applied twice (CGS2) — orthogonality equivalent to the
+// reference's MGS twice, but as two batched projections instead of 2(k+1) sequential ones —
+// and Givens rotations / triangular solves on the host (the (m+1) x m Hessenberg is tiny).
+#include <cmath>
+#include <cstring>
+
+#include "ctx.hpp"
+
+namespace rdd {
+
+namespace {
+
+constexpr int kRB = 120;   // reduction grid (CTAs)
+constexpr int kRT = 256;
+
+enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_BREAKDOWN = 2, ST_MAXITER = 3 };
+
+// device control block for CG
+struct CgState {
+  int status;
+  int it;
+  int max_iter;
+  int pad;
+  double tol, z0, bnorm, rz, beta;
+};
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[kRT / 32];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < kRT / 32 ? sh[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+  }
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
+__device__ __forceinline__ double sum_parts(const double* part) {
+  double s = 0.0;
+  for (int i = 0; i < kRB; ++i) s += part[i];
+  return s;
+}
+
+__global__ void k_dot_part(const double* __restrict__ x, const double* __restrict__ y, int n,
+                           double* __restrict__ part) {
+  double s = 0.0;
+  for (int i = blockIdx.x * kRT + threadIdx.x; i < n; i += kRB * kRT) s += x[i] * y[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void k_dot2_part(const double* __restrict__ a, const double* __restrict__ b, const double* __restrict__ c,
+                            int n, double* __restrict__ part_ab, double* __restrict__ part_ac) {
+  double s1 = 0.0, s2 = 0.0;
+  for (int i = blockIdx.x * kRT + threadIdx.x; i < n; i += kRB * kRT) {
+    s1 += a[i] * b[i];
+    s2 += a[i] * c[i];
+  }
+  s1 = block_sum(s1);
+  s2 = block_sum(s2);
+  if (threadIdx.x == 0) {
+    part_ab[blockIdx.x] = s1;
+    part_ac[blockIdx.x] = s2;
+  }
+}
+
+// CG setup after z = M b: z0 = ‖z‖, rz = r·z, p = z
+__global__ void k_cg_init(CgState* st, const double* __restrict__ pz, const double* __restrict__ prz,
+                          const double* __restrict__ pbb, double* hist, double* thist) {
+  const double zz = sum_parts(pz), rz = sum_parts(prz), bb = sum_parts(pbb);
+  st->z0 = sqrt(zz);
+  st->bnorm = sqrt(bb);
+  st->rz = rz;
+  st->it = 0;
+  if (st->z0 == 0.0) {
+    st->status = ST_CONVERGED;
+    hist[0] = 0.0;
+    thist[0] = 0.0;
+  } else {
+    st->status = st->max_iter > 0 ? ST_RUNNING : ST_MAXITER;
+    hist[0] = 1.0;
+    thist[0] = st->bnorm > 0.0 ? 1.0 : 0.0;
+  }
+}
+
+// alpha = rz / pAp; breakdown check (krylov.hpp:132-135); x += αp; r -= αAp; partial ‖r‖²
+__global__ void k_cg_update(CgState* st, const double* __restrict__ ppap, double* __restrict__ x,
+                            double* __restrict__ r, const double* __restrict__ p, const double* __restrict__ Ap, int n,
+                            double* __restrict__ prr, int* brk_flag) {
+  if (st->status != ST_RUNNING) return;
+  const double pAp = sum_parts(ppap);
+  const double rz = st->rz;
+  if (pAp <= 0.0 || rz == 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *brk_flag = 1;
+    return;
+  }
+  const double alpha = rz / pAp;
+  double s = 0.0;
+  for (int i = blockIdx.x * kRT + threadIdx.x; i < n; i += kRB * kRT) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * Ap[i];
+    r[i] = ri;
+    s += ri * ri;
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) prr[blockIdx.x] = s;
+}
+
+// rel = ‖z‖/‖z0‖, histories, convergence, beta (krylov.hpp:139-151)
+__global__ void k_cg_finish(CgState* st, const double* __restrict__ pzz, const double* __restrict__ prz,
+                            const double* __restrict__ prr, double* hist, double* thist, int* brk_flag) {
+  if (st->status != ST_RUNNING) return;
+  if (*brk_flag) {
+    st->status = ST_BREAKDOWN;
+    return;
+  }
+  const double zz = sum_parts(pzz), rzn = sum_parts(prz), rr = sum_parts(prr);
+  const double rel = sqrt(zz) / st->z0;
+  const int it = st->it + 1;
+  hist[it] = rel;
+  thist[it] = st->bnorm > 0.0 ? sqrt(rr) / st->bnorm : sqrt(rr);
+  st->it = it;
+  if (rel <= st->tol) {
+    st->status = ST_CONVERGED;
+    return;
+  }
+  st->beta = rzn / st->rz;
+  st->rz = rzn;
+  if (it >= st->max_iter) st->status = ST_MAXITER;
+}
+
+__global__ void k_cg_p(const CgState* st, double* __restrict__ p, const double* __restrict__ z, int n) {
+  if (st->status != ST_RUNNING) return;
+  const double beta = st->beta;
+  for (int i = blockIdx.x * kRT + threadIdx.x; i < n; i += kRB * kRT) p[i] = z[i] + beta * p[i];
+}
+
+__global__ void k_copy(double* __restrict__ dst, const double* __restrict__ src, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+__global__ void k_fill(double* __restrict__ dst, double v, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = v;
+}
+__global__ void k_sub(double* __restrict__ out, const double* __restrict__ a, const double* __restrict__ b, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] - b[i];
+}
+__global__ void k_scale_to(double* __restrict__ out, const double* __restrict__ in, const double* s, int n,
+                           int invert) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = invert ? in[i] / s[i] : in[i];
+}
+
+// GMRES: h[k] = V[:,k]ᵀ w for k < nk, one CTA per basis vector (fixed-order reduction)
+__global__ void k_multidot(const double* __restrict__ V, long long ldv, const double* __restrict__ w, int n,
+                           double* __restrict__ h) {
+  const int k = blockIdx.x;
+  const double* v = V + k * ldv;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += kRT) s += v[i] * w[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) h[k] = s;
+}
+// w -= V h (nk columns); optionally accumulate h into hacc
+__global__ void k_multiaxpy(const double* __restrict__ V, long long ldv, double* __restrict__ w, int n,
+                            const double* __restrict__ h, int nk) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = w[i];
+    for (int k = 0; k < nk; ++k) s -= h[k] * V[k * ldv + i];
+    w[i] = s;
+  }
+}
+// x += V y
+__global__ void k_combine(const double* __restrict__ V, long long ldv, const double* __restrict__ y, int nk,
+                          const double* __restrict__ x0, double* __restrict__ x, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = x0[i];
+    for (int k = 0; k < nk; ++k) s += y[k] * V[k * ldv + i];
+    x[i] = s;
+  }
+}
+__global__ void k_scal_div(double* __restrict__ out, const double* __restrict__ in, double s, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i] / s;
+}
+
+struct Vecs {
+  int n;
+  Ctx* c;
+  void copy(double* d, const double* s) {
+    k_copy<<<kRB, kRT, 0, c->stream>>>(d, s, n);
+    RDD_LAUNCH_CHECK();
+  }
+  void fill(double* d, double v) {
+    k_fill<<<kRB, kRT, 0, c->stream>>>(d, v, n);
+    RDD_LAUNCH_CHECK();
+  }
+};
+
+}  // namespace
+
+// A(w) = Hᵀ(H w) (runner.hpp:232-234) or the block-sparse HᵀH
+void normal_operator(Ctx& c, const double* w, double* out) {
+  if (c.cfg.op_form == RDD_OPERATOR_NORMAL && c.NB.p) {
+    normal_apply_dev(c, w, out);
+  } else {
+    matvec_dev(c, w, c.ytmp.ensure(c.N));
+    matvec_t_dev(c, c.ytmp.p, out);
+  }
+}
+
+static void precond(Ctx& c, const double* v, double* z) {
+  if (c.pkind == RDD_PRECOND_NONE) {
+    k_copy<<<kRB, kRT, 0, c.stream>>>(z, v, c.p);
+    RDD_LAUNCH_CHECK();
+  } else {
+    precond_apply_dev(c, v, z, false);
+  }
+}
+
+static double dot_host(Ctx& c, const double* x, const double* y, int n, double* part) {
+  k_dot_part<<<kRB, kRT, 0, c.stream>>>(x, y, n, part);
+  RDD_LAUNCH_CHECK();
+  double h[kRB];
+  RDD_CUDA(cudaMemcpyAsync(h, part, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+  double s = 0.0;
+  for (int i = 0; i < kRB; ++i) s += h[i];
+  return s;
+}
+
+// ---------------------------------------------------------------- CG (krylov.hpp:106-156)
+struct CgGraph {
+  cudaGraphExec_t exec = nullptr;
+  ~CgGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+static void cg_solve(Ctx& c, const double* b, double* x, double tol, int max_iter, int comp) {
+  const int n = c.p;
+  double* r = c.wk(static_cast<size_t>(n) * 8);
+  double* z = r + n;
+  double* pv = z + n;
+  double* Ap = pv + n;
+  double* sc = c.scal.ensure(8 * kRB + 64);
+  double *P0 = sc, *P1 = sc + kRB, *P2 = sc + 2 * kRB, *P3 = sc + 3 * kRB, *P4 = sc + 4 * kRB;
+  DBuf<CgState> st;
+  DBuf<int> brk;
+  DBuf<double> hist, thist;
+  hist.ensure(max_iter + 2);
+  thist.ensure(max_iter + 2);
+  brk.zero(1, c.stream);
+  CgState h0{};
+  h0.status = ST_RUNNING;
+  h0.max_iter = max_iter;
+  h0.tol = tol;
+  st.upload(&h0, 1, c.stream);
+  Vecs V{n, &c};
+  V.fill(x, 0.0);
+  V.copy(r, b);
+  precond(c, r, z);
+  k_dot2_part<<<kRB, kRT, 0, c.stream>>>(z, z, r, n, P0, P1);  // (z·z, z·r)
+  k_dot_part<<<kRB, kRT, 0, c.stream>>>(b, b, n, P2);
+  RDD_LAUNCH_CHECK();
+  k_cg_init<<<1, 1, 0, c.stream>>>(st.p, P0, P1, P2, hist.p, thist.p);
+  RDD_LAUNCH_CHECK();
+  V.copy(pv, z);
+
+  // one iteration = fixed launch sequence; capture once, replay in chunks with a device status
+  auto iteration = [&]() {
+    normal_operator(c, pv, Ap);
+    k_dot_part<<<kRB, kRT, 0, c.stream>>>(pv, Ap, n, P0);
+    k_cg_update<<<kRB, kRT, 0, c.stream>>>(st.p, P0, x, r, pv, Ap, n, P4, brk.p);
+    precond(c, r, z);
+    k_dot2_part<<<kRB, kRT, 0, c.stream>>>(z, z, r, n, P2, P3);
+    k_cg_finish<<<1, 1, 0, c.stream>>>(st.p, P2, P3, P4, hist.p, thist.p, brk.p);
+    k_cg_p<<<kRB, kRT, 0, c.stream>>>(st.p, pv, z, n);
+  };
+  const int chunk = 8;
+  c.ytmp.ensure(c.N);  // no allocations inside the capture
+  CgGraph g;
+  const bool timing = c.timing;
+  c.timing = false;  // no event records inside capture
+  {
+    cudaGraph_t graph;
+    RDD_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < chunk; ++k) iteration();
+    RDD_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    RDD_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+    cudaGraphDestroy(graph);
+  }
+  c.timing = timing;
+  CgState hs{};
+  for (int done = 0;;) {
+    RDD_CUDA(cudaGraphLaunch(g.exec, c.stream));
+    done += chunk;
+    RDD_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(CgState), cudaMemcpyDeviceToHost, c.stream));
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    if (hs.status != ST_RUNNING) break;
+    if (done > max_iter + chunk) break;
+  }
+  const int it = hs.it;
+  c.hist[comp].resize(it + 1);
+  c.true_hist[comp].resize(it + 1);
+  hist.download(c.hist[comp].data(), it + 1, c.stream);
+  thist.download(c.true_hist[comp].data(), it + 1, c.stream);
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+  if (hs.status == ST_CONVERGED && hs.z0 == 0.0) {
+    c.hist[comp] = {0.0};
+    c.true_hist[comp] = {0.0};
+  }
+  c.iters[comp] = it;
+  c.conv[comp] = hs.status == ST_CONVERGED;
+  c.brk[comp] = hs.status == ST_BREAKDOWN;
+}
+
+// ---------------------------------------------------------------- GMRES (krylov.hpp:275-389)
+static void gmres_solve(Ctx& c, const double* b, double* x, double tol, int max_iter, int restart, int comp) {
+  const int n = c.p;
+  const bool ident = c.pkind == RDD_PRECOND_NONE;
+  const bool true_res = c.cfg.true_residual != 0;
+  double* part = c.scal.ensure(8 * kRB + 64);
+  auto& hist = c.hist[comp];
+  auto& thist = c.true_hist[comp];
+  hist.clear();
+  thist.clear();
+  double* t1 = c.wk(static_cast<size_t>(n) * 4);
+  double* t2 = t1 + n;
+  double* xk = t2 + n;
+  double* rr = xk + n;
+  Vecs Vv{n, &c};
+  const double bnorm = std::sqrt(dot_host(c, b, b, n, part));
+  precond(c, b, t1);
+  const double gnorm0 = std::sqrt(dot_host(c, t1, t1, n, part));
+  Vv.fill(x, 0.0);
+  c.iters[comp] = 0;
+  c.conv[comp] = 0;
+  c.brk[comp] = 0;
+  if (gnorm0 == 0.0) {
+    hist = {0.0};
+    thist = {0.0};
+    c.conv[comp] = 1;
+    return;
+  }
+  const int cycle_len = restart > 0 ? restart : std::min(max_iter, n);
+  if (restart == 0 && cycle_len > 4096)
+    throw std::runtime_error("full GMRES basis of " + std::to_string(cycle_len) +
+                             " vectors exceeds the cap; configure gmres_restart");
+  DBuf<double> Vb, hd;
+  Vb.ensure(static_cast<size_t>(cycle_len + 1) * n);
+  hd.ensure(2 * (cycle_len + 2));
+  hist.push_back(1.0);
+  thist.push_back(bnorm > 0.0 ? 1.0 : 0.0);
+  int iters_left = max_iter;
+  bool converged = false, breakdown = false;
+  std::vector<double> Hm, cs, sn, gv, hh(cycle_len + 2), hh2(cycle_len + 2);
+  auto Hat = [&](int i, int k) -> double& { return Hm[static_cast<size_t>(k) * (cycle_len + 1) + i]; };
+  while (iters_left > 0 && !converged && !breakdown) {
+    normal_operator(c, x, t1);
+    k_sub<<<kRB, kRT, 0, c.stream>>>(t2, b, t1, n);  // b - A x
+    RDD_LAUNCH_CHECK();
+    if (ident) Vv.copy(t1, t2);
+    else precond(c, t2, t1);
+    const double beta = std::sqrt(dot_host(c, t1, t1, n, part));
+    if (beta / gnorm0 <= tol) {
+      converged = true;
+      break;
+    }
+    const int len = std::min(cycle_len, iters_left);
+    k_scal_div<<<kRB, kRT, 0, c.stream>>>(Vb.p, t1, beta, n);
+    RDD_LAUNCH_CHECK();
+    Hm.assign(static_cast<size_t>(len + 1) * (cycle_len + 1), 0.0);
+    cs.assign(len, 0.0);
+    sn.assign(len, 0.0);
+    gv.assign(len + 1, 0.0);
+    gv[0] = beta;
+    int k = 0;
+    for (; k < len;) {
+      double* vk = Vb.p + static_cast<size_t>(k) * n;
+      double* w = Vb.p + static_cast<size_t>(k + 1) * n;
+      if (ident) {
+        normal_operator(c, vk, w);
+      } else {
+        normal_operator(c, vk, t1);
+        precond(c, t1, w);
+      }
+      // CGS2: h = Vᵀw; w -= V h (twice)
+      for (int pass = 0; pass < 2; ++pass) {
+        k_multidot<<<k + 1, kRT, 0, c.stream>>>(Vb.p, n, w, n, hd.p);
+        k_multiaxpy<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, w, n, hd.p, k + 1);
+        RDD_LAUNCH_CHECK();
+        RDD_CUDA(cudaMemcpyAsync(pass == 0 ? hh.data() : hh2.data(), hd.p, sizeof(double) * (k + 1),
+                                 cudaMemcpyDeviceToHost, c.stream));
+        RDD_CUDA(cudaStreamSynchronize(c.stream));
+      }
+      for (int i = 0; i <= k; ++i) Hat(i, k) = hh[i] + hh2[i];
+      const double hnext = std::sqrt(dot_host(c, w, w, n, part));
+      Hat(k + 1, k) = hnext;
+      if (hnext > 0.0) {
+        k_scal_div<<<kRB, kRT, 0, c.stream>>>(w, w, hnext, n);
+        RDD_LAUNCH_CHECK();
+      }
+      for (int i = 0; i < k; ++i) {
+        const double t = cs[i] * Hat(i, k) + sn[i] * Hat(i + 1, k);
+        Hat(i + 1, k) = -sn[i] * Hat(i, k) + cs[i] * Hat(i + 1, k);
+        Hat(i, k) = t;
+      }
+      const double denom = std::hypot(Hat(k, k), Hat(k + 1, k));
+      if (denom == 0.0) {
+        breakdown = true;
+        break;
+      }
+      cs[k] = Hat(k, k) / denom;
+      sn[k] = Hat(k + 1, k) / denom;
+      Hat(k, k) = denom;
+      Hat(k + 1, k) = 0.0;
+      gv[k + 1] = -sn[k] * gv[k];
+      gv[k] *= cs[k];
+      const double rel = std::fabs(gv[k + 1]) / gnorm0;
+      hist.push_back(rel);
+      ++c.iters[comp];
+      --iters_left;
+      ++k;
+      auto ysolve = [&](int kk) {
+        std::vector<double> y(kk);
+        for (int i = kk - 1; i >= 0; --i) {
+          double s = gv[i];
+          for (int j = i + 1; j < kk; ++j) s -= Hat(i, j) * y[j];
+          y[i] = s / Hat(i, i);
+        }
+        return y;
+      };
+      if (ident) {
+        thist.push_back(rel);
+      } else if (true_res) {  // diagnostic true residual (krylov.hpp:360-367)
+        const std::vector<double> y = ysolve(k);
+        RDD_CUDA(cudaMemcpyAsync(hd.p, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c.stream));
+        k_combine<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, hd.p, k, x, xk, n);
+        RDD_LAUNCH_CHECK();
+        normal_operator(c, xk, t1);
+        k_sub<<<kRB, kRT, 0, c.stream>>>(rr, b, t1, n);
+        RDD_LAUNCH_CHECK();
+        const double rn = std::sqrt(dot_host(c, rr, rr, n, part));
+        thist.push_back(bnorm > 0.0 ? rn / bnorm : 0.0);
+      } else {
+        thist.push_back(-1.0);
+      }
+      if (rel <= tol || hnext == 0.0) {
+        converged = true;
+        break;
+      }
+      if (iters_left == 0) break;
+    }
+    if (k > 0) {
+      std::vector<double> y(k);
+      for (int i = k - 1; i >= 0; --i) {
+        double s = gv[i];
+        for (int j = i + 1; j < k; ++j) s -= Hat(i, j) * y[j];
+        y[i] = s / Hat(i, i);
+      }
+      RDD_CUDA(cudaMemcpyAsync(hd.p, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c.stream));
+      k_combine<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, hd.p, k, x, x, n);
+      RDD_LAUNCH_CHECK();
+    }
+    if (restart == 0 && !converged && !breakdown && iters_left > 0 && k == cycle_len) break;
+  }
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+  c.conv[comp] = converged;
+  c.brk[comp] = breakdown;
+}
+
+// runner.hpp:239-251: per component b = Hᵀ F_c, solve, W = y ./ scales
+void solve_all(Ctx& c, int solver, double tol, int max_iter_cfg, int restart) {
+  ScopedKernelTimer tk(c, "solve");
+  if (max_iter_cfg < 0) throw std::invalid_argument("max_iter must be >= 1");
+  const int max_iter = max_iter_cfg == 0 ? 10 * c.p : max_iter_cfg;
+  const int C = c.C, n = c.p;
+  c.hist.assign(C, {});
+  c.true_hist.assign(C, {});
+  c.iters.assign(C, 0);
+  c.conv.assign(C, 0);
+  c.brk.assign(C, 0);
+  c.W.ensure(static_cast<size_t>(n) * C);
+  DBuf<double> b, x;
+  b.ensure(n);
+  x.ensure(n);
+  for (int comp = 0; comp < C; ++comp) {
+    matvec_t_dev(c, c.F.p + static_cast<size_t>(comp) * c.N, b.p);
+    if (solver == RDD_SOLVER_CG) cg_solve(c, b.p, x.p, tol, max_iter, comp);
+    else if (solver == RDD_SOLVER_GMRES) gmres_solve(c, b.p, x.p, tol, max_iter, restart, comp);
+    else throw std::invalid_argument("solver not available on the device path");
+    k_scale_to<<<kRB, kRT, 0, c.stream>>>(c.W.p + static_cast<size_t>(comp) * n, x.p, c.scales.p, n, 1);
+    RDD_LAUNCH_CHECK();
+  }
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+}  // namespace rdd

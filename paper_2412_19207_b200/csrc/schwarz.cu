@@ -1,0 +1,255 @@
+// schwarz.cu — K8/K11: one-level overlapping Schwarz preconditioners (schwarz.hpp:39-215).
+//
+// Build (schwarz.hpp:93-148): S_i = concatenated column ranges of neighbour_sets[i]; A_i is
+// gathered blockwise from the normal blocks (missing pairs are exact zeros); the local solve is
+// the pseudo-inverse with eigenvalues <= 1e-12·λmax dropped. The device stores each local
+// operator as an explicit symmetric n_i x n_i matrix P_i = V diag(1/λ_kept) Vᵀ (batched Jacobi
+// eigensolver + DMMA), so that every apply is one HBM-streaming GEMV per subdomain.
+// Apply (schwarz.hpp:153-185): z_i = P_i v[S_i]; the AS/SAS/RAS reduction is owner-computes:
+// each column sums its (≤3^d) local contributions in ascending i, like the reference's serial
+// scatter, without atomics. apply_transpose (schwarz.hpp:189-215) moves the SAS/RAS weights in
+// front of the local solve.
+#include <algorithm>
+
+#include "ctx.hpp"
+
+namespace rdd {
+
+namespace {
+
+// gather A_i from normal blocks: one CTA per (i, part-pair)
+__global__ void k_gather_local(const double* __restrict__ NB, const int* __restrict__ task_i,
+                               const int* __restrict__ task_j1, const int* __restrict__ task_j2,
+                               const int* __restrict__ task_o1, const int* __restrict__ task_o2,
+                               const long long* __restrict__ task_nb, const int* __restrict__ col_off,
+                               const int* __restrict__ nvec, const long long* __restrict__ A_off,
+                               double* __restrict__ A) {
+  const int t = blockIdx.x;
+  const int i = task_i[t], j1 = task_j1[t], j2 = task_j2[t], o1 = task_o1[t], o2 = task_o2[t];
+  const long long nb = task_nb[t];
+  const int n = nvec[i];
+  const int p1 = col_off[j1 + 1] - col_off[j1], p2 = col_off[j2 + 1] - col_off[j2];
+  double* Ai = A + A_off[i];
+  for (int e = threadIdx.x; e < p1 * p2; e += blockDim.x) {
+    const int r = e % p1, cc = e / p1;
+    double v = 0.0;
+    if (nb >= 0) v = (j1 <= j2) ? NB[nb + r + static_cast<long long>(cc) * p1] : NB[nb + cc + static_cast<long long>(r) * p2];
+    Ai[(o1 + r) + static_cast<long long>(o2 + cc) * n] = v;
+  }
+}
+
+// per i: keep λ > 1e-12·max(0, λmax) (schwarz.hpp:133-139); X = V diag(1/λ_kept); rank, cond
+__global__ void k_local_scale(double* __restrict__ V, const double* __restrict__ lam, const int* __restrict__ nvec,
+                              const long long* __restrict__ A_off, const long long* __restrict__ ev_off,
+                              double* __restrict__ X, int* __restrict__ rank, double* __restrict__ cond) {
+  const int i = blockIdx.x;
+  const int n = nvec[i];
+  const double* L = lam + ev_off[i];
+  __shared__ double s_max, s_min;
+  __shared__ int s_rank;
+  if (threadIdx.x == 0) {
+    double mx = -1e308;
+    for (int k = 0; k < n; ++k) mx = fmax(mx, L[k]);
+    const double cut = 1e-12 * fmax(0.0, mx);
+    double mn = 1e308;
+    int rk = 0;
+    for (int k = 0; k < n; ++k)
+      if (L[k] > cut) {
+        ++rk;
+        mn = fmin(mn, L[k]);
+      }
+    s_max = mx;
+    s_min = mn;
+    s_rank = rk;
+    rank[i] = rk;
+    cond[i] = rk > 0 ? mx / mn : 0.0;
+  }
+  __syncthreads();
+  const double cut = 1e-12 * fmax(0.0, s_max);
+  const double* Vi = V + A_off[i];
+  double* Xi = X + A_off[i];
+  for (long long e = threadIdx.x; e < static_cast<long long>(n) * n; e += blockDim.x) {
+    const int k = static_cast<int>(e / n);
+    Xi[e] = L[k] > cut ? Vi[e] / L[k] : 0.0;
+  }
+}
+
+// z_i = P_i g_i, g_i = w(v)[S_i]; grid (rows chunk, i)
+__global__ void k_local_apply(const double* __restrict__ P, const long long* __restrict__ P_off,
+                              const int* __restrict__ set_ptr, const int* __restrict__ set_idx,
+                              const double* __restrict__ v, const int* __restrict__ mult,
+                              const int* __restrict__ owner, int kind, int transpose, double* __restrict__ z) {
+  extern __shared__ double g[];
+  const int i = blockIdx.y;
+  const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0;
+  const int r0 = blockIdx.x * blockDim.x;
+  if (r0 >= n) return;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const int col = set_idx[s0 + c];
+    double val = v[col];
+    if (transpose) {
+      if (kind == RDD_PRECOND_SAS) val /= mult[col];
+      else if (kind == RDD_PRECOND_RAS) val = owner[col] == i ? val : 0.0;
+    }
+    g[c] = val;
+  }
+  __syncthreads();
+  const int r = r0 + threadIdx.x;
+  if (r >= n) return;
+  const double* Pi = P + P_off[i] + r;
+  double acc = 0.0;
+  for (int c = 0; c < n; ++c) acc += Pi[static_cast<long long>(c) * n] * g[c];
+  z[s0 + r] = acc;
+}
+
+// out[col] = Σ_i weight · z_i[pos]  over the ≤3^d subdomains whose S_i contains col
+__global__ void k_reduce(const double* __restrict__ z, const int* __restrict__ gat_ptr,
+                         const int* __restrict__ gat_pos, const int* __restrict__ gat_owner_pos,
+                         const int* __restrict__ mult, int p, int kind, int transpose, double* __restrict__ out) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= p) return;
+  double s = 0.0;
+  if (!transpose && kind == RDD_PRECOND_RAS) {
+    s = z[gat_owner_pos[col]];
+  } else {
+    for (int q = gat_ptr[col]; q < gat_ptr[col + 1]; ++q) {
+      const double zz = z[gat_pos[q]];
+      s += (!transpose && kind == RDD_PRECOND_SAS) ? zz / mult[col] : zz;
+    }
+  }
+  out[col] = s;
+}
+
+}  // namespace
+
+void build_schwarz(Ctx& c, int kind) {
+  ScopedKernelTimer tk(c, "schwarz_build");
+  const int J = c.J;
+  c.pkind = kind;
+  // index sets (schwarz.hpp:39-61)
+  c.set_ptr.assign(J + 1, 0);
+  c.set_idx.clear();
+  std::vector<int> n(J);
+  for (int i = 0; i < J; ++i) {
+    for (int q = c.nbr_ptr[i]; q < c.nbr_ptr[i + 1]; ++q) {
+      const int j = c.nbr_idx[q];
+      for (int col = c.h_col_off[j]; col < c.h_col_off[j + 1]; ++col) c.set_idx.push_back(col);
+    }
+    c.set_ptr[i + 1] = static_cast<int>(c.set_idx.size());
+    n[i] = c.set_ptr[i + 1] - c.set_ptr[i];
+    if (n[i] == 0) throw std::runtime_error("empty index set for subdomain " + std::to_string(i));
+  }
+  c.h_mult.assign(c.p, 0);
+  for (int col : c.set_idx) ++c.h_mult[col];
+  // gather map per column: positions (into the concatenated z) in ascending i
+  std::vector<std::vector<int>> gl(c.p);
+  std::vector<int> owner_pos(c.p, 0);
+  for (int i = 0; i < J; ++i)
+    for (int q = c.set_ptr[i]; q < c.set_ptr[i + 1]; ++q) {
+      const int col = c.set_idx[q];
+      gl[col].push_back(q);
+      if (c.h_owner[col] == i) owner_pos[col] = q;
+    }
+  std::vector<int> gp(c.p + 1, 0), gpos;
+  for (int col = 0; col < c.p; ++col) {
+    gp[col + 1] = gp[col] + static_cast<int>(gl[col].size());
+    gpos.insert(gpos.end(), gl[col].begin(), gl[col].end());
+  }
+  c.gat_ptr.upload(gp, c.stream);
+  c.gat_pos.upload(gpos, c.stream);
+  c.gat_owner_pos.upload(owner_pos, c.stream);
+  c.dset_ptr.upload(c.set_ptr, c.stream);
+  c.dset_idx.upload(c.set_idx, c.stream);
+  c.dmult.upload(c.h_mult, c.stream);
+  c.zloc.ensure(std::max<size_t>(1, c.set_idx.size()));
+
+  // gather A_i (schwarz.hpp:112-130)
+  c.P_off.assign(J + 1, 0);
+  for (int i = 0; i < J; ++i) c.P_off[i + 1] = c.P_off[i] + static_cast<long long>(n[i]) * n[i];
+  DBuf<double> A, V;
+  A.zero(std::max<long long>(1, c.P_off[J]), c.stream);
+  std::vector<int> ti, tj1, tj2, to1, to2;
+  std::vector<long long> tnb;
+  for (int i = 0; i < J; ++i) {
+    std::vector<std::pair<int, int>> parts;
+    int o = 0;
+    for (int q = c.nbr_ptr[i]; q < c.nbr_ptr[i + 1]; ++q) {
+      const int j = c.nbr_idx[q];
+      parts.push_back({j, o});
+      o += c.h_p[j];
+    }
+    for (auto [j1, o1] : parts)
+      for (auto [j2, o2] : parts) {
+        auto it = c.nb_index.find({std::min(j1, j2), std::max(j1, j2)});
+        if (it == c.nb_index.end()) continue;
+        ti.push_back(i);
+        tj1.push_back(j1);
+        tj2.push_back(j2);
+        to1.push_back(o1);
+        to2.push_back(o2);
+        tnb.push_back(c.nb_off[it->second]);
+      }
+  }
+  DBuf<int> dti, dtj1, dtj2, dto1, dto2, dn;
+  DBuf<long long> dtnb, dPoff;
+  dti.upload(ti, c.stream);
+  dtj1.upload(tj1, c.stream);
+  dtj2.upload(tj2, c.stream);
+  dto1.upload(to1, c.stream);
+  dto2.upload(to2, c.stream);
+  dtnb.upload(tnb, c.stream);
+  dn.upload(n, c.stream);
+  c.dP_off.upload(c.P_off, c.stream);
+  if (!ti.empty()) {
+    k_gather_local<<<static_cast<int>(ti.size()), 256, 0, c.stream>>>(c.NB.p, dti.p, dtj1.p, dtj2.p, dto1.p, dto2.p,
+                                                                     dtnb.p, c.dcol_off.p, dn.p, c.dP_off.p, A.p);
+    RDD_LAUNCH_CHECK();
+  }
+  // eigen pseudo-inverse (schwarz.hpp:131-146)
+  V.ensure(std::max<long long>(1, c.P_off[J]));
+  DBuf<double> lam, X;
+  lam.ensure(std::max<size_t>(1, c.set_idx.size()));
+  std::vector<long long> offA(c.P_off.begin(), c.P_off.end() - 1), evo(J);
+  for (int i = 0; i < J; ++i) evo[i] = c.set_ptr[i];
+  batched_syevj(c, A.p, V.p, lam.p, n, offA, 60, false);
+  X.ensure(std::max<long long>(1, c.P_off[J]));
+  DBuf<long long> devo;
+  DBuf<int> drank;
+  DBuf<double> dcond;
+  devo.upload(evo, c.stream);
+  drank.ensure(J);
+  dcond.ensure(J);
+  k_local_scale<<<J, 256, 0, c.stream>>>(V.p, lam.p, dn.p, c.dP_off.p, devo.p, X.p, drank.p, dcond.p);
+  RDD_LAUNCH_CHECK();
+  c.P.ensure(std::max<long long>(1, c.P_off[J]));
+  std::vector<GemmTask> t;
+  for (int i = 0; i < J; ++i)
+    for (int tm = 0; tm < ceil_div(n[i], 64); ++tm)
+      for (int tn = 0; tn < ceil_div(n[i], 64); ++tn)
+        t.push_back({X.p + c.P_off[i], V.p + c.P_off[i], c.P.p + c.P_off[i], nullptr, nullptr, n[i], n[i], n[i], n[i],
+                     n[i], n[i], tm, tn, 0.0});
+  gemm_nt(c, t);
+  c.local_rank.assign(J, 0);
+  c.local_cond.assign(J, 0.0);
+  drank.download(c.local_rank.data(), J, c.stream);
+  dcond.download(c.local_cond.data(), J, c.stream);
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+  c.nmax_local = *std::max_element(n.begin(), n.end());
+}
+
+void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose) {
+  ScopedKernelTimer tk(c, "precond_apply");
+  const int T = 128;
+  dim3 grid(ceil_div(c.nmax_local, T), c.J);
+  const size_t smem = static_cast<size_t>(c.nmax_local) * sizeof(double);
+  if (smem > 48 * 1024)
+    RDD_CUDA(cudaFuncSetAttribute(k_local_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  k_local_apply<<<grid, T, smem, c.stream>>>(c.P.p, c.dP_off.p, c.dset_ptr.p, c.dset_idx.p, v, c.dmult.p, c.downer.p,
+                                             c.pkind, transpose ? 1 : 0, c.zloc.p);
+  RDD_LAUNCH_CHECK();
+  k_reduce<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.zloc.p, c.gat_ptr.p, c.gat_pos.p, c.gat_owner_pos.p, c.dmult.p,
+                                                     c.p, c.pkind, transpose ? 1 : 0, z);
+  RDD_LAUNCH_CHECK();
+}
+
+}  // namespace rdd

@@ -1,0 +1,140 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeds.
+
+Bars (BASELINE.json north_star): point->subdomain indexing and PCA ranks bit-exact; PCA
+subspaces within a projector difference of 1e-8; iteration counts within 5%; floating-point
+results within the stated relative tolerances below.
+"""
+import numpy as np
+import pytest
+
+from paper_2412_19207_b200 import abi as A
+from paper_2412_19207_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases():
+    c = {}
+    c["h_export"] = configs.golden_h_export()
+    c["runner77"] = configs.golden_runner(77)
+    c["scaling_as"] = configs.golden_scaling(A.PRECOND_AS)
+    c["sweep_1e-2"] = configs.golden_sweep(1e-2, 78)
+    psi = configs.golden_scaling(A.PRECOND_SAS)
+    psi.pca_matrix = A.PCA_PSI
+    c["psi_sas"] = psi
+    c["c1_slice"] = configs.scaled(configs.c1(), [2, 2], 12, m=40)
+    c["c2_slice"] = configs.scaled(configs.c2(), [3, 3], 10, m=48)
+    c["c3_slice"] = configs.scaled(configs.c3(), [2, 2, 2], 6, m=40)
+    c["c4_slice"] = configs.scaled(configs.c4(), [4, 2], 8, m=40)
+    c["c5_slice"] = configs.scaled(configs.c5(), [2, 2, 2], 6, m=40)
+    ex3 = A.make_config(A.PROBLEM_EXAMPLE3, [2, 2, 2], 12, [6, 6, 6], seed=5, test=[10, 10, 10],
+                        solver=A.SOLVER_CG, precond=A.PRECOND_AS, rel_tol=1e-10)
+    c["example3"] = ex3
+    return c
+
+
+CASES = _cases()
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2412_19207_b200 import rdd
+    return rdd.Solver(0)
+
+
+@pytest.fixture(scope="module")
+def orc(oracle_cls):
+    return oracle_cls()
+
+
+def _proj(V):
+    return V @ V.T
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_instance_indexing_and_pca(dev, orc, name):
+    cfg = CASES[name]
+    dev.build_instance(cfg)
+    orc.build_instance(cfg)
+    J = int(orc.geti("J")[0])
+    assert int(dev.geti("J")[0]) == J
+    assert np.array_equal(dev.getd("points"), orc.getd("points"))
+    assert np.array_equal(dev.getd("box_lo"), orc.getd("box_lo"))
+    assert np.array_equal(dev.getd("box_hi"), orc.getd("box_hi"))
+    for j in range(J):
+        assert np.array_equal(dev.getd("R", j), orc.getd("R", j))
+        assert np.array_equal(dev.getd("b", j), orc.getd("b", j))
+        assert np.array_equal(dev.geti("nbr", j), orc.geti("nbr", j))
+    # bit-exact rows_j (assembly.hpp:58-64) and PCA ranks
+    for j in range(J):
+        assert np.array_equal(dev.geti("rows", j), orc.geti("rows", j)), j
+    assert np.array_equal(dev.geti("p_j"), orc.geti("p_j"))
+    if cfg.tau_mode != A.TAU_OFF:
+        m = cfg.m
+        for j in range(J):
+            pj = int(orc.geti("p_j")[j])
+            Vd = dev.getd("V", j).reshape(pj, m).T
+            Vo = orc.getd("V", j).reshape(pj, m).T
+            assert np.linalg.norm(_proj(Vd) - _proj(Vo), 2) <= 1e-8, (name, j)
+            sd, so = dev.getd("sigma", j), orc.getd("sigma", j)
+            big = so > 1e-8 * so[0]
+            assert np.allclose(sd[big], so[big], rtol=1e-9, atol=0), (name, j)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_assembly_and_operators(dev, orc, name):
+    cfg = CASES[name]
+    eq = cfg.precond >= 0
+    dev.build_instance(cfg).assemble(eq)
+    orc.build_instance(cfg).assemble(eq)
+    J = int(orc.geti("J")[0])
+    tol = 1e-12 if cfg.tau_mode == A.TAU_OFF else 1e-7
+    for j in range(J):
+        Hd, Ho = dev.block(j), orc.block(j)
+        assert Hd.shape == Ho.shape
+        assert np.linalg.norm(Hd - Ho) <= tol * np.linalg.norm(Ho), (name, j)
+    Fd, Fo = dev.getd("F"), orc.getd("F")
+    assert np.allclose(Fd, Fo, rtol=1e-12, atol=1e-12 * np.abs(Fo).max())
+    assert np.allclose(dev.getd("scales"), orc.getd("scales"), rtol=tol)
+    rng = np.random.default_rng(3)
+    p, N = int(orc.geti("p")[0]), int(orc.geti("N")[0])
+    w, r = rng.standard_normal(p), rng.standard_normal(N)
+    yo, yd = orc.matvec(w), dev.matvec(w)
+    assert np.linalg.norm(yd - yo) <= 10 * tol * np.linalg.norm(yo)
+    to, td = orc.matvec_transpose(r), dev.matvec_transpose(r)
+    assert np.linalg.norm(td - to) <= 10 * tol * np.linalg.norm(to)
+    # adjoint identity on the device path alone (test_assembly.cpp:114-134)
+    assert abs(yd @ r - w @ td) <= 1e-11 * max(1.0, abs(yd @ r))
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if CASES[n].precond >= 0])
+def test_normal_blocks_and_schwarz(dev, orc, name):
+    cfg = CASES[name]
+    dev.build_instance(cfg).assemble(True).build_preconditioner(cfg.precond)
+    orc.build_instance(cfg).assemble(True).build_preconditioner(cfg.precond)
+    assert np.array_equal(dev.geti("nb_pairs"), orc.geti("nb_pairs"))
+    Ad, Ao = dev.getd("nb_dense"), orc.getd("nb_dense")
+    tol = 1e-12 if cfg.tau_mode == A.TAU_OFF else 1e-7
+    assert np.linalg.norm(Ad - Ao) <= tol * np.linalg.norm(Ao)
+    assert np.array_equal(dev.geti("local_rank"), orc.geti("local_rank")), name
+    rng = np.random.default_rng(7)
+    p = int(orc.geti("p")[0])
+    for tr in (False, True):
+        v = rng.standard_normal(p)
+        zo, zd = orc.precond_apply(v, tr), dev.precond_apply(v, tr)
+        assert np.linalg.norm(zd - zo) <= 1e-6 * np.linalg.norm(zo), (name, tr)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_run_single(dev, orc, name):
+    cfg = A.Config.from_buffer_copy(CASES[name])
+    if cfg.precond < 0:
+        cfg.precond = A.PRECOND_AS
+    so = orc.run_single(cfg)
+    sd = dev.run_single(cfg)
+    assert sd["DoF"] == so["DoF"] and sd["N"] == so["N"] and sd["J"] == so["J"]
+    assert sd["converged"] == so["converged"]
+    assert abs(sd["iterations"] - so["iterations"]) <= max(1, round(0.05 * so["iterations"])), (sd, so)
+    # the solve stops at rel_tol; errors agree to the level the solve resolves
+    tol = max(1e-6, 100 * cfg.rel_tol)
+    assert sd["e_l2"] == pytest.approx(so["e_l2"], rel=tol), (name, sd["e_l2"], so["e_l2"])

@@ -301,6 +301,7 @@ int64_t rdd_get_i(rdd_ctx* h, const char* what, int index, int32_t* out, int64_t
     else if (w == "dim") v = {c.d};
     else if (w == "C") v = {c.C};
     else if (w == "maxcov") v = {c.maxcov};
+    else if (w == "n_fallback") v = {c.n_fallback};
     else if (w == "p_j") v = c.h_p;
     else if (w == "col_off") v = c.h_col_off;
     else if (w == "rows") {

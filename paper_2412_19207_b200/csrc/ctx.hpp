@@ -116,6 +116,8 @@ struct Ctx {
   // owner-gather map for the AS/SAS reduction: per column c, list of (i, position)
   DBuf<int> gat_ptr, gat_pos, gat_owner_pos;
   int nmax_local = 0;
+  int n_fallback = 0;                 // local blocks that took the eigen pseudo-inverse
+  double full_rank_cond = 1e11;       // Cholesky path when cond_est(A_i) is below this
   DBuf<double> zloc;                  // Σ n_i
 
   // ---- Krylov
@@ -208,6 +210,11 @@ void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks);  // C = A B  (A: M x K
 void gemm_nt(Ctx& c, const std::vector<GemmTask>& tasks);  // C = A Bᵀ (A: M x K, B: N x K col-major)
 void project_blocks(Ctx& c);
 void ensure_col_owner(Ctx& c);
+// cholesky.cu
+void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n, const std::vector<long long>& off,
+                         std::vector<int>& fail, std::vector<double>& frob_A, std::vector<double>& frob_P);
+std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int>& n,
+                                  const std::vector<long long>& off, int iters);
 // jacobi.cu
 void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vector<int>& n,
                    const std::vector<long long>& offA, int max_sweeps, bool relative);

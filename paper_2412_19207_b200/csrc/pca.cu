@@ -147,6 +147,8 @@ void run_pca(Ctx& c) {
     RDD_LAUNCH_CHECK();
     c.dp_j.download(c.h_p.data(), J, c.stream);
     RDD_CUDA(cudaStreamSynchronize(c.stream));
+    // the psi route truncates on ω·φ but the system blocks are always operator-applied
+    if (c.cfg.pca_matrix == RDD_PCA_PSI) assemble_samples(c, RDD_PCA_OP_APPLIED, c.S.p, c.S_off);
   }
   c.h_col_off.assign(J + 1, 0);
   for (int j = 0; j < J; ++j) c.h_col_off[j + 1] = c.h_col_off[j] + c.h_p[j];

@@ -205,35 +205,87 @@ void build_schwarz(Ctx& c, int kind) {
                                                                      dtnb.p, c.dcol_off.p, dn.p, c.dP_off.p, A.p);
     RDD_LAUNCH_CHECK();
   }
-  // eigen pseudo-inverse (schwarz.hpp:131-146)
-  V.ensure(std::max<long long>(1, c.P_off[J]));
-  DBuf<double> lam, X;
-  lam.ensure(std::max<size_t>(1, c.set_idx.size()));
-  std::vector<long long> offA(c.P_off.begin(), c.P_off.end() - 1), evo(J);
-  for (int i = 0; i < J; ++i) evo[i] = c.set_ptr[i];
-  batched_syevj(c, A.p, V.p, lam.p, n, offA, 60, false);
-  X.ensure(std::max<long long>(1, c.P_off[J]));
-  DBuf<long long> devo;
-  DBuf<int> drank;
-  DBuf<double> dcond;
-  devo.upload(evo, c.stream);
-  drank.ensure(J);
-  dcond.ensure(J);
-  k_local_scale<<<J, 256, 0, c.stream>>>(V.p, lam.p, dn.p, c.dP_off.p, devo.p, X.p, drank.p, dcond.p);
-  RDD_LAUNCH_CHECK();
+  // A_i^{-1} by Cholesky when A_i is safely full rank (then it equals the reference's
+  // pseudo-inverse), else the eigen pseudo-inverse with the reference cutoff (schwarz.hpp:131-146).
+  std::vector<long long> offA(c.P_off.begin(), c.P_off.end() - 1);
   c.P.ensure(std::max<long long>(1, c.P_off[J]));
-  std::vector<GemmTask> t;
-  for (int i = 0; i < J; ++i)
-    for (int tm = 0; tm < ceil_div(n[i], 64); ++tm)
-      for (int tn = 0; tn < ceil_div(n[i], 64); ++tn)
-        t.push_back({X.p + c.P_off[i], V.p + c.P_off[i], c.P.p + c.P_off[i], nullptr, nullptr, n[i], n[i], n[i], n[i],
-                     n[i], n[i], tm, tn, 0.0});
-  gemm_nt(c, t);
+  const std::vector<double> lmaxA = batched_power(c, A.p, n, offA, 40);
+  std::vector<int> fail;
+  std::vector<double> fa, fp;
+  batched_spd_inverse(c, A.p, c.P.p, n, offA, fail, fa, fp);
+  const std::vector<double> lmaxP = batched_power(c, c.P.p, n, offA, 40);
   c.local_rank.assign(J, 0);
   c.local_cond.assign(J, 0.0);
-  drank.download(c.local_rank.data(), J, c.stream);
-  dcond.download(c.local_cond.data(), J, c.stream);
-  RDD_CUDA(cudaStreamSynchronize(c.stream));
+  std::vector<int> fb;  // fallback subdomains
+  for (int i = 0; i < J; ++i) {
+    const double cond = lmaxA[i] * lmaxP[i];
+    if (fail[i] || !(cond < c.full_rank_cond)) {
+      fb.push_back(i);
+    } else {
+      c.local_rank[i] = n[i];
+      c.local_cond[i] = cond;
+    }
+  }
+  c.n_fallback = static_cast<int>(fb.size());
+  if (!fb.empty()) {
+    // re-gather the flagged A_i (the Cholesky overwrote them) into a compact batch
+    std::vector<int> fn;
+    std::vector<long long> foff;
+    long long tot = 0;
+    for (int i : fb) {
+      fn.push_back(n[i]);
+      foff.push_back(tot);
+      tot += static_cast<long long>(n[i]) * n[i];
+    }
+    A.zero(std::max<long long>(1, c.P_off[J]), c.stream);
+    if (!ti.empty()) {
+      k_gather_local<<<static_cast<int>(ti.size()), 256, 0, c.stream>>>(c.NB.p, dti.p, dtj1.p, dtj2.p, dto1.p, dto2.p,
+                                                                       dtnb.p, c.dcol_off.p, dn.p, c.dP_off.p, A.p);
+      RDD_LAUNCH_CHECK();
+    }
+    DBuf<double> Af, V, X, lam;
+    Af.ensure(tot);
+    V.ensure(tot);
+    X.ensure(tot);
+    for (size_t q = 0; q < fb.size(); ++q)
+      RDD_CUDA(cudaMemcpyAsync(Af.p + foff[q], A.p + c.P_off[fb[q]], sizeof(double) * fn[q] * fn[q],
+                               cudaMemcpyDeviceToDevice, c.stream));
+    long long te = 0;
+    std::vector<long long> evo(fb.size());
+    for (size_t q = 0; q < fb.size(); ++q) {
+      evo[q] = te;
+      te += fn[q];
+    }
+    lam.ensure(te);
+    batched_syevj(c, Af.p, V.p, lam.p, fn, foff, 60, false);
+    DBuf<long long> devo, dfoff;
+    DBuf<int> drank, dfn;
+    DBuf<double> dcond;
+    devo.upload(evo, c.stream);
+    dfoff.upload(foff, c.stream);
+    dfn.upload(fn, c.stream);
+    drank.ensure(fb.size());
+    dcond.ensure(fb.size());
+    k_local_scale<<<static_cast<int>(fb.size()), 256, 0, c.stream>>>(V.p, lam.p, dfn.p, dfoff.p, devo.p, X.p, drank.p,
+                                                                     dcond.p);
+    RDD_LAUNCH_CHECK();
+    std::vector<GemmTask> t;
+    for (size_t q = 0; q < fb.size(); ++q)
+      for (int tm = 0; tm < ceil_div(fn[q], 64); ++tm)
+        for (int tn = 0; tn < ceil_div(fn[q], 64); ++tn)
+          t.push_back({X.p + foff[q], V.p + foff[q], c.P.p + c.P_off[fb[q]], nullptr, nullptr, fn[q], fn[q], fn[q],
+                       fn[q], fn[q], fn[q], tm, tn, 0.0});
+    gemm_nt(c, t);
+    std::vector<int> hr(fb.size());
+    std::vector<double> hc(fb.size());
+    drank.download(hr.data(), fb.size(), c.stream);
+    dcond.download(hc.data(), fb.size(), c.stream);
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    for (size_t q = 0; q < fb.size(); ++q) {
+      c.local_rank[fb[q]] = hr[q];
+      c.local_cond[fb[q]] = hc[q];
+    }
+  }
   c.nmax_local = *std::max_element(n.begin(), n.end());
 }
 

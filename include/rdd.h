@@ -148,7 +148,8 @@ int64_t rdd_get_d(rdd_ctx* ctx, const char* what, int index, double* out, int64_
 /* Device time (ms) of the last call of a named kernel family and its launch count since reset. */
 int rdd_kernel_stats(rdd_ctx* ctx, const char* family, double* ms_total, int64_t* launches);
 int rdd_reset_stats(rdd_ctx* ctx);
-int rdd_set_timing(rdd_ctx* ctx, int on);  /* per-family CUDA-event timing (adds syncs) */
+int rdd_set_timing(rdd_ctx* ctx, int on);
+int rdd_set_verbose(rdd_ctx* ctx, int on);  /* solver diagnostics on stderr */  /* per-family CUDA-event timing (adds syncs) */
 /* Time `reps` calls of the normal operator on device-resident vectors (CUDA events). */
 int rdd_bench_operator(rdd_ctx* ctx, int op_form, int reps, double* ms_per_call, double* bytes_per_call);
 

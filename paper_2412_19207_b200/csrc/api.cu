@@ -139,6 +139,11 @@ using rdd::Ctx;
 template <class F>
 static int guarded(rdd_ctx* h, F&& f) {
   if (!h) return RDD_INVALID_ARGUMENT;
+  struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(rdd::alloc_stream()) { rdd::alloc_stream() = s; }
+    ~StreamScope() { rdd::alloc_stream() = prev; }
+  } scope(h->c.stream);
   try {
     RDD_CUDA(cudaSetDevice(h->c.device));
     f(h->c);
@@ -184,6 +189,11 @@ int rdd_create(rdd_ctx** out, int device) {
     delete h;
     return RDD_CUDA_ERROR;
   }
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;  // keep freed blocks cached in the pool
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   *out = h;
   return RDD_OK;
 }
@@ -193,8 +203,19 @@ void rdd_destroy(rdd_ctx* h) {
   cudaSetDevice(h->c.device);
   cudaStreamSynchronize(h->c.stream);
   cudaStream_t s = h->c.stream;
-  delete h;
+  {
+    const cudaStream_t prev = rdd::alloc_stream();
+    rdd::alloc_stream() = s;
+    delete h;
+    rdd::alloc_stream() = prev;
+  }
+  cudaStreamSynchronize(s);
   cudaStreamDestroy(s);
+}
+int rdd_set_verbose(rdd_ctx* h, int on) {
+  if (!h) return RDD_INVALID_ARGUMENT;
+  h->c.verbose = on != 0;
+  return RDD_OK;
 }
 
 const char* rdd_last_error(const rdd_ctx* h) { return h ? h->c.err.c_str() : "null context"; }
@@ -407,6 +428,12 @@ int64_t rdd_get_d(rdd_ctx* h, const char* what, int index, double* out, int64_t 
             v[ridx[r] + static_cast<size_t>(c.h_col_off[j] + cc) * c.N] = blk[r + static_cast<size_t>(cc) * nr];
       }
     } else if (w == "local_cond") {
+      {
+        const cudaStream_t prev = rdd::alloc_stream();
+        rdd::alloc_stream() = c.stream;
+        rdd::refresh_local_cond(c);
+        rdd::alloc_stream() = prev;
+      }
       v = c.local_cond;
     } else if (w == "W") {
       dl(c.W.p + static_cast<size_t>(index) * c.p, c.p);

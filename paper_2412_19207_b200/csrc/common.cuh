@@ -29,7 +29,14 @@ inline void check_cuda(cudaError_t e, const char* what, const char* file, int li
 #define RDD_CUDA(x) ::rdd::check_cuda((x), #x, __FILE__, __LINE__)
 #define RDD_LAUNCH_CHECK() ::rdd::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
-// Owning device buffer (cudaMalloc; grows, never shrinks).
+// Stream that owns temporaries of the current API call: stream-ordered pool allocations
+// (cudaMallocAsync / cudaFreeAsync) make per-call scratch buffers cheap.
+inline cudaStream_t& alloc_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+
+// Owning device buffer (pooled, stream-ordered; grows, never shrinks).
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -39,14 +46,20 @@ struct DBuf {
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (alloc_stream()) cudaFreeAsync(p, alloc_stream());
+      else cudaFree(p);
+    }
     p = nullptr;
     n = 0;
   }
   T* ensure(size_t count) {
     if (count > n) {
       release();
-      if (count) RDD_CUDA(cudaMalloc(&p, count * sizeof(T)));
+      if (count) {
+        if (alloc_stream()) RDD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), alloc_stream()));
+        else RDD_CUDA(cudaMalloc(&p, count * sizeof(T)));
+      }
       n = count;
     }
     return p;

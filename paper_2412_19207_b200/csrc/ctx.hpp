@@ -117,6 +117,13 @@ struct Ctx {
   DBuf<int> gat_ptr, gat_pos, gat_owner_pos;
   int nmax_local = 0;
   int n_fallback = 0;                 // local blocks that took the eigen pseudo-inverse
+  std::vector<int> fallback, local_n;
+  bool local_cond_exact = false;
+  struct GatherTask {
+    int i, j1, j2, o1, o2;
+    long long nb;
+  };
+  std::vector<GatherTask> gat_tasks;
   double full_rank_cond = 1e11;       // Cholesky path when cond_est(A_i) is below this
   DBuf<double> zloc;                  // Σ n_i
 
@@ -135,6 +142,7 @@ struct Ctx {
   // ---- instrumentation
   std::map<std::string, KernelStat> stats;
   bool timing = false;
+  bool verbose = false;
 
   double* wk(size_t count) { return work.ensure(count); }
 };
@@ -189,6 +197,8 @@ void normal_operator(Ctx& c, const double* w, double* out);  // runner.hpp:232-2
 // schwarz.cu (K8/K11)
 void build_schwarz(Ctx& c, int kind);
 void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose);
+void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, const std::vector<long long>& off);
+void refresh_local_cond(Ctx& c);
 // krylov.cu (K12/K13)
 void solve_all(Ctx& c, int solver, double tol, int max_iter, int restart);
 // evaluate.cu (K14)

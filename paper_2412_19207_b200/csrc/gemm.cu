@@ -125,7 +125,7 @@ void launch(Ctx& c, const std::vector<GemmTask>& tasks, const char* fam) {
   // grid.x limit is 2^31-1; tasks are far fewer
   k_gemm<AT, BT><<<static_cast<unsigned>(tasks.size()), NT, 0, c.stream>>>(d.p);
   RDD_LAUNCH_CHECK();
-  RDD_CUDA(cudaStreamSynchronize(c.stream));  // task buffer lifetime
+  if (!alloc_stream()) RDD_CUDA(cudaStreamSynchronize(c.stream));  // task buffer lifetime (non-pooled)
 }
 
 }  // namespace

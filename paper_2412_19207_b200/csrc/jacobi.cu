@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ A
                                                     const long long* __restrict__ off,
                                                     const long long* __restrict__ ev_off, double* __restrict__ scratch,
                                                     const long long* __restrict__ scr_off, int max_sweeps, double tol,
-                                                    int* __restrict__ sweeps_out, int use_smem) {
+                                                    int* __restrict__ sweeps_out, int use_smem,
+                                                    double2* __restrict__ rot, const long long* __restrict__ rot_off) {
   extern __shared__ double smem[];
   const int b = blockIdx.x;
   const int n = nvec[b];
@@ -46,7 +47,8 @@ __global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ A
   const int np = nn / 2;
   const long long smem_tri = scr_off[gridDim.x];  // packed size of the largest matrix
   const double* A = Ain + off[b];
-  double* V = Vout + off[b];
+  double2* R = rot + rot_off[b];
+  (void)Vout;
   const bool in_smem = use_smem != 0;
   double* P = in_smem ? smem : scratch + scr_off[b];
   double* cs = in_smem ? smem + smem_tri : smem;  // [np] c, [np] s
@@ -63,8 +65,6 @@ __global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ A
     const int i = static_cast<int>(e % n), j = static_cast<int>(e / n);
     if (i <= j) P[pidx(i, j)] = A[e];
   }
-  for (long long e = threadIdx.x; e < static_cast<long long>(n) * n; e += blockDim.x)
-    V[e] = (e % (n + 1) == 0) ? 1.0 : 0.0;
   __syncthreads();
   if (threadIdx.x == 0) {
     double m = 0.0;
@@ -135,19 +135,9 @@ __global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ A
         if (v1) P[pidx(q1, p2)] = l21 * c2 - l22 * s2;
         if (v1 && v2) P[pidx(q1, q2)] = l21 * s2 + l22 * c2;
       }
-      // 3. V <- V J (rows independent)
-      for (int e = threadIdx.x; e < np * n; e += blockDim.x) {
-        const int k = e / n, row = e % n;
-        const double s = sn[k];
-        if (s == 0.0) continue;
-        const double c = cs[k];
-        const int p = pp[k], q = qq[k];
-        double* vp = V + row + static_cast<long long>(p) * n;
-        double* vq = V + row + static_cast<long long>(q) * n;
-        const double a = *vp, bq = *vq;
-        *vp = c * a - s * bq;
-        *vq = s * a + c * bq;
-      }
+      // 3. log the rotations; V is accumulated afterwards, row-parallel (k_apply_rotations)
+      for (int k = threadIdx.x; k < np; k += blockDim.x)
+        R[(static_cast<long long>(sweep) * (nn - 1) + r) * np + k] = make_double2(cs[k], sn[k]);
       __syncthreads();
     }
     if (local_active) atomicOr(&active, 1);
@@ -157,6 +147,55 @@ __global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ A
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) ev[ev_off[b] + i] = P[pidx(i, i)];
   if (threadIdx.x == 0 && sweeps_out) sweeps_out[b] = sweep;
+}
+
+// V = J_1 J_2 ... J_R (all logged rounds): rows are independent, so each CTA keeps kRows rows
+// of V in shared memory and replays the rotation log on them.
+constexpr int kRows = 32;
+__global__ void __launch_bounds__(256) k_apply_rotations(double* __restrict__ Vout, const int* __restrict__ nvec,
+                                                         const long long* __restrict__ off,
+                                                         const double2* __restrict__ rot,
+                                                         const long long* __restrict__ rot_off,
+                                                         const int* __restrict__ sweeps) {
+  extern __shared__ double vs[];  // kRows x (n+1)
+  const int b = blockIdx.y;
+  const int n = nvec[b];
+  const int r0 = blockIdx.x * kRows;
+  if (r0 >= n) return;
+  const int rows = min(kRows, n - r0);
+  const int nn = n + (n & 1), np = nn / 2, ld = n + 1;
+  for (int e = threadIdx.x; e < kRows * n; e += blockDim.x) {
+    const int rr = e / n, col = e % n;
+    vs[rr * ld + col] = (rr < rows && r0 + rr == col) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const double2* R = rot + rot_off[b];
+  const int total = sweeps[b] * (nn - 1);
+  for (int t = 0; t < total; ++t) {
+    const int r = t % (nn - 1);
+    const double2* Rt = R + static_cast<long long>(t) * np;
+    for (int e = threadIdx.x; e < np * kRows; e += blockDim.x) {
+      const int k = e / kRows, rr = e % kRows;
+      const double2 csn = Rt[k];
+      if (csn.y == 0.0 || rr >= rows) continue;
+      int p = player(k, r, nn), q = player(nn - 1 - k, r, nn);
+      if (p > q) {
+        const int tmp = p;
+        p = q;
+        q = tmp;
+      }
+      double* row = vs + rr * ld;
+      const double a = row[p], bq = row[q];
+      row[p] = csn.x * a - csn.y * bq;
+      row[q] = csn.y * a + csn.x * bq;
+    }
+    __syncthreads();
+  }
+  double* V = Vout + off[b];
+  for (int e = threadIdx.x; e < rows * n; e += blockDim.x) {
+    const int rr = e % rows, col = e / rows;
+    V[(r0 + rr) + static_cast<long long>(col) * n] = vs[rr * ld + col];
+  }
 }
 
 }  // namespace
@@ -196,10 +235,33 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     smem = static_cast<size_t>(nmax) * (nmax + 1) / 2 * sizeof(double);
   smem += static_cast<size_t>(np) * (2 * sizeof(double) + 2 * sizeof(int));
   RDD_CUDA(cudaFuncSetAttribute(k_syevj, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  std::vector<long long> roff(B);
+  long long rtot = 0;
+  for (int b = 0; b < B; ++b) {
+    roff[b] = rtot;
+    const int nn = n[b] + (n[b] & 1);
+    rtot += static_cast<long long>(max_sweeps) * std::max(1, nn - 1) * std::max(1, nn / 2);
+  }
+  DBuf<double2> rot;
+  DBuf<long long> droff;
+  rot.ensure(std::max<long long>(1, rtot));
+  droff.upload(roff, c.stream);
   const double tol = relative ? 1e-15 : 1e-15;
   k_syevj<<<B, kThreads, smem, c.stream>>>(A, V, evals, dn.p, doff.p, doffE.p, scr.p, doffS.p, max_sweeps, tol,
-                                           dsw.p, use_smem ? 1 : 0);
+                                           dsw.p, use_smem ? 1 : 0, rot.p, droff.p);
   RDD_LAUNCH_CHECK();
+  const size_t vsm = static_cast<size_t>(kRows) * (nmax + 1) * sizeof(double);
+  RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
+  k_apply_rotations<<<dim3(ceil_div(nmax, kRows), B), 256, vsm, c.stream>>>(V, dn.p, doff.p, rot.p, droff.p, dsw.p);
+  RDD_LAUNCH_CHECK();
+  if (c.verbose) {
+    std::vector<int> sw(B);
+    dsw.download(sw.data(), B, c.stream);
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    int mx = 0;
+    for (int v : sw) mx = std::max(mx, v);
+    std::fprintf(stderr, "[syevj] B=%d nmax=%d max_sweeps_used=%d\n", B, nmax, mx);
+  }
   RDD_CUDA(cudaStreamSynchronize(c.stream));
 }
 

@@ -122,6 +122,67 @@ __global__ void k_reduce(const double* __restrict__ z, const int* __restrict__ g
 
 }  // namespace
 
+// Gather A_i for the subdomains in `which` into a compact batch at offsets `off` (zero-filled).
+void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, const std::vector<long long>& off) {
+  long long tot = 0;
+  std::vector<int> slot(c.J, -1), nn(which.size());
+  for (size_t q = 0; q < which.size(); ++q) {
+    slot[which[q]] = static_cast<int>(q);
+    nn[q] = c.local_n[which[q]];
+    tot = std::max(tot, off[q] + static_cast<long long>(nn[q]) * nn[q]);
+  }
+  out.zero(std::max<long long>(1, tot), c.stream);
+  std::vector<int> ti, tj1, tj2, to1, to2;
+  std::vector<long long> tnb;
+  for (const auto& t : c.gat_tasks) {
+    if (slot[t.i] < 0) continue;
+    ti.push_back(slot[t.i]);
+    tj1.push_back(t.j1);
+    tj2.push_back(t.j2);
+    to1.push_back(t.o1);
+    to2.push_back(t.o2);
+    tnb.push_back(t.nb);
+  }
+  if (ti.empty()) return;
+  DBuf<int> dti, dtj1, dtj2, dto1, dto2, dn;
+  DBuf<long long> dtnb, doff;
+  dti.upload(ti, c.stream);
+  dtj1.upload(tj1, c.stream);
+  dtj2.upload(tj2, c.stream);
+  dto1.upload(to1, c.stream);
+  dto2.upload(to2, c.stream);
+  dtnb.upload(tnb, c.stream);
+  dn.upload(nn, c.stream);
+  doff.upload(off, c.stream);
+  k_gather_local<<<static_cast<int>(ti.size()), 256, 0, c.stream>>>(c.NB.p, dti.p, dtj1.p, dtj2.p, dto1.p, dto2.p,
+                                                                   dtnb.p, c.dcol_off.p, dn.p, doff.p, out.p);
+  RDD_LAUNCH_CHECK();
+}
+
+// local_cond as the reference reports it (λmax/λmin of the kept spectrum), by power iteration
+// on A_i and A_i^{-1}; computed on demand (the rank decision only needs the cheap bound).
+void refresh_local_cond(Ctx& c) {
+  if (c.local_cond_exact || c.pkind < 0) return;
+  std::vector<int> which;
+  for (int i = 0; i < c.J; ++i)
+    if (std::find(c.fallback.begin(), c.fallback.end(), i) == c.fallback.end()) which.push_back(i);
+  std::vector<long long> off, poff;
+  std::vector<int> nn;
+  long long tot = 0;
+  for (int i : which) {
+    off.push_back(tot);
+    nn.push_back(c.local_n[i]);
+    poff.push_back(c.P_off[i]);
+    tot += static_cast<long long>(c.local_n[i]) * c.local_n[i];
+  }
+  DBuf<double> Af;
+  gather_locals(c, which, Af, off);
+  const std::vector<double> la = batched_power(c, Af.p, nn, off, 200);
+  const std::vector<double> lp = batched_power(c, c.P.p, nn, poff, 200);
+  for (size_t q = 0; q < which.size(); ++q) c.local_cond[which[q]] = la[q] * lp[q];
+  c.local_cond_exact = true;
+}
+
 void build_schwarz(Ctx& c, int kind) {
   ScopedKernelTimer tk(c, "schwarz_build");
   const int J = c.J;
@@ -163,13 +224,11 @@ void build_schwarz(Ctx& c, int kind) {
   c.dmult.upload(c.h_mult, c.stream);
   c.zloc.ensure(std::max<size_t>(1, c.set_idx.size()));
 
-  // gather A_i (schwarz.hpp:112-130)
+  // local matrix sizes and gather plan (schwarz.hpp:112-130): A_i blocks come from NB
   c.P_off.assign(J + 1, 0);
   for (int i = 0; i < J; ++i) c.P_off[i + 1] = c.P_off[i] + static_cast<long long>(n[i]) * n[i];
-  DBuf<double> A, V;
-  A.zero(std::max<long long>(1, c.P_off[J]), c.stream);
-  std::vector<int> ti, tj1, tj2, to1, to2;
-  std::vector<long long> tnb;
+  c.local_n = n;
+  c.gat_tasks.clear();
   for (int i = 0; i < J; ++i) {
     std::vector<std::pair<int, int>> parts;
     int o = 0;
@@ -182,53 +241,64 @@ void build_schwarz(Ctx& c, int kind) {
       for (auto [j2, o2] : parts) {
         auto it = c.nb_index.find({std::min(j1, j2), std::max(j1, j2)});
         if (it == c.nb_index.end()) continue;
-        ti.push_back(i);
-        tj1.push_back(j1);
-        tj2.push_back(j2);
-        to1.push_back(o1);
-        to2.push_back(o2);
-        tnb.push_back(c.nb_off[it->second]);
+        c.gat_tasks.push_back({i, j1, j2, o1, o2, c.nb_off[it->second]});
       }
   }
-  DBuf<int> dti, dtj1, dtj2, dto1, dto2, dn;
-  DBuf<long long> dtnb, dPoff;
-  dti.upload(ti, c.stream);
-  dtj1.upload(tj1, c.stream);
-  dtj2.upload(tj2, c.stream);
-  dto1.upload(to1, c.stream);
-  dto2.upload(to2, c.stream);
-  dtnb.upload(tnb, c.stream);
-  dn.upload(n, c.stream);
   c.dP_off.upload(c.P_off, c.stream);
-  if (!ti.empty()) {
-    k_gather_local<<<static_cast<int>(ti.size()), 256, 0, c.stream>>>(c.NB.p, dti.p, dtj1.p, dtj2.p, dto1.p, dto2.p,
-                                                                     dtnb.p, c.dcol_off.p, dn.p, c.dP_off.p, A.p);
-    RDD_LAUNCH_CHECK();
-  }
-  // A_i^{-1} by Cholesky when A_i is safely full rank (then it equals the reference's
-  // pseudo-inverse), else the eigen pseudo-inverse with the reference cutoff (schwarz.hpp:131-146).
+  DBuf<double> A;
+  std::vector<int> all(J);
+  for (int i = 0; i < J; ++i) all[i] = i;
   std::vector<long long> offA(c.P_off.begin(), c.P_off.end() - 1);
+  gather_locals(c, all, A, offA);
+  // A_i^{-1} by Cholesky (equal to the reference's pseudo-inverse when A_i is safely full rank)
   c.P.ensure(std::max<long long>(1, c.P_off[J]));
-  const std::vector<double> lmaxA = batched_power(c, A.p, n, offA, 40);
   std::vector<int> fail;
   std::vector<double> fa, fp;
   batched_spd_inverse(c, A.p, c.P.p, n, offA, fail, fa, fp);
-  const std::vector<double> lmaxP = batched_power(c, c.P.p, n, offA, 40);
+  A.release();
   c.local_rank.assign(J, 0);
   c.local_cond.assign(J, 0.0);
-  std::vector<int> fb;  // fallback subdomains
+  c.local_cond_exact = false;
+  std::vector<int> flagged;
   for (int i = 0; i < J; ++i) {
-    const double cond = lmaxA[i] * lmaxP[i];
-    if (fail[i] || !(cond < c.full_rank_cond)) {
-      fb.push_back(i);
+    const double bound = fa[i] * fp[i];  // cond(A_i) <= ||A_i||_F ||A_i^{-1}||_F
+    if (fail[i] || !(bound < c.full_rank_cond)) {
+      flagged.push_back(i);
     } else {
       c.local_rank[i] = n[i];
-      c.local_cond[i] = cond;
+      c.local_cond[i] = bound;
+    }
+  }
+  std::vector<int> fb;  // eigen fallback
+  if (!flagged.empty()) {
+    std::vector<long long> foff;
+    std::vector<int> fn;
+    long long tot = 0;
+    for (int i : flagged) {
+      foff.push_back(tot);
+      fn.push_back(n[i]);
+      tot += static_cast<long long>(n[i]) * n[i];
+    }
+    DBuf<double> Af;
+    gather_locals(c, flagged, Af, foff);
+    const std::vector<double> la = batched_power(c, Af.p, fn, foff, 60);
+    std::vector<long long> poff;
+    for (int i : flagged) poff.push_back(c.P_off[i]);
+    const std::vector<double> lp = batched_power(c, c.P.p, fn, poff, 60);
+    std::vector<int> keep_fn;
+    for (size_t q = 0; q < flagged.size(); ++q) {
+      const int i = flagged[q];
+      const double cond = la[q] * lp[q];
+      if (!fail[i] && cond < c.full_rank_cond) {
+        c.local_rank[i] = n[i];
+        c.local_cond[i] = cond;
+      } else {
+        fb.push_back(i);
+      }
     }
   }
   c.n_fallback = static_cast<int>(fb.size());
   if (!fb.empty()) {
-    // re-gather the flagged A_i (the Cholesky overwrote them) into a compact batch
     std::vector<int> fn;
     std::vector<long long> foff;
     long long tot = 0;
@@ -237,19 +307,10 @@ void build_schwarz(Ctx& c, int kind) {
       foff.push_back(tot);
       tot += static_cast<long long>(n[i]) * n[i];
     }
-    A.zero(std::max<long long>(1, c.P_off[J]), c.stream);
-    if (!ti.empty()) {
-      k_gather_local<<<static_cast<int>(ti.size()), 256, 0, c.stream>>>(c.NB.p, dti.p, dtj1.p, dtj2.p, dto1.p, dto2.p,
-                                                                       dtnb.p, c.dcol_off.p, dn.p, c.dP_off.p, A.p);
-      RDD_LAUNCH_CHECK();
-    }
     DBuf<double> Af, V, X, lam;
-    Af.ensure(tot);
+    gather_locals(c, fb, Af, foff);
     V.ensure(tot);
     X.ensure(tot);
-    for (size_t q = 0; q < fb.size(); ++q)
-      RDD_CUDA(cudaMemcpyAsync(Af.p + foff[q], A.p + c.P_off[fb[q]], sizeof(double) * fn[q] * fn[q],
-                               cudaMemcpyDeviceToDevice, c.stream));
     long long te = 0;
     std::vector<long long> evo(fb.size());
     for (size_t q = 0; q < fb.size(); ++q) {
@@ -286,6 +347,7 @@ void build_schwarz(Ctx& c, int kind) {
       c.local_cond[fb[q]] = hc[q];
     }
   }
+  c.fallback = fb;
   c.nmax_local = *std::max_element(n.begin(), n.end());
 }
 

@@ -64,6 +64,7 @@ def lib():
         L.rdd_kernel_stats.argtypes = [vp, C.c_char_p, dp, C.POINTER(C.c_int64)]
         L.rdd_reset_stats.argtypes = [vp]
         L.rdd_set_timing.argtypes = [vp, C.c_int]
+        L.rdd_set_verbose.argtypes = [vp, C.c_int]
         L.rdd_bench_operator.argtypes = [vp, C.c_int, C.c_int, dp, dp]
         _lib = L
     return _lib
@@ -182,6 +183,9 @@ class Solver:
     # ---- instrumentation
     def set_timing(self, on: bool):
         self.L.rdd_set_timing(self.h, int(on))
+
+    def set_verbose(self, on: bool):
+        self.L.rdd_set_verbose(self.h, int(on))
 
     def reset_stats(self):
         self.L.rdd_reset_stats(self.h)

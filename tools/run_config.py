@@ -25,6 +25,7 @@ elif a.m:
 cfg.op_form = a.op
 s = rdd.Solver(0)
 s.set_timing(bool(a.timing))
+s.set_verbose(True)
 t = time.time()
 r = s.run_single(cfg)
 wall = time.time() - t

@@ -227,6 +227,6 @@ std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int
                                   const std::vector<long long>& off, int iters);
 // jacobi.cu
 void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vector<int>& n,
-                   const std::vector<long long>& offA, int max_sweeps, bool relative);
+                   const std::vector<long long>& offA, int max_sweeps, double floor_rel, double floor_abs);
 
 }  // namespace rdd

@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ A
                                                     const long long* __restrict__ ev_off, double* __restrict__ scratch,
                                                     const long long* __restrict__ scr_off, int max_sweeps, double tol,
                                                     int* __restrict__ sweeps_out, int use_smem,
-                                                    double2* __restrict__ rot, const long long* __restrict__ rot_off) {
+                                                    double2* __restrict__ rot, const long long* __restrict__ rot_off,
+                                                    double floor_rel, double floor_abs) {
   extern __shared__ double smem[];
   const int b = blockIdx.x;
   const int n = nvec[b];
@@ -72,7 +73,9 @@ __global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ A
     dmax = m;
   }
   __syncthreads();
-  const double floor_abs = 1e-32 * dmax;
+  const double tiny = 1e-32 * dmax;
+  // directions whose eigenvalues are both below the floor cannot affect anything above it
+  const double floor_lam = fmax(floor_rel * dmax, floor_abs);
 
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ A
         if (q < n) {
           const double apq = P[pidx(p, q)];
           const double app = P[pidx(p, p)], aqq = P[pidx(q, q)];
-          if (fabs(apq) > floor_abs && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
+          if (fabs(apq) > tiny && fmax(app, aqq) > floor_lam && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
             const double theta = (aqq - app) / (2.0 * apq);
             const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
             c = 1.0 / sqrt(1.0 + t * t);
@@ -198,69 +201,329 @@ __global__ void __launch_bounds__(256) k_apply_rotations(double* __restrict__ Vo
   }
 }
 
+
+// Odd-even (Luk–Park) ordering on full column-major storage in global memory (n > kSmemMaxN):
+// step t pairs positions (o+2k, o+2k+1), o = t&1, and every pair is rotated *and swapped*
+// (Ĵ = J·Π), which makes the index movement a transposition network so all pairs meet every n
+// steps, while each 2x2 update touches two contiguous 16-byte column segments.
+__global__ void __launch_bounds__(1024) k_syevj_oe(double* __restrict__ Aw, const int* __restrict__ nvec,
+                                                   const long long* __restrict__ off, double* __restrict__ ev,
+                                                   const long long* __restrict__ ev_off, int max_sweeps, double tol,
+                                                   int* __restrict__ sweeps_out, double2* __restrict__ rot,
+                                                   const long long* __restrict__ rot_off, double floor_rel,
+                                                   double floor_abs) {
+  extern __shared__ double sm[];
+  const int b = blockIdx.x;
+  const int n = nvec[b];  // even (padded by the host)
+  if (n <= 0) return;
+  double* A = Aw + off[b];
+  double* cs = sm;
+  double* sn = cs + n / 2 + 1;
+  double2* R = rot + rot_off[b];
+  __shared__ int active;
+  __shared__ double dmax;
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < n; ++i) m = fmax(m, fabs(A[i + static_cast<long long>(i) * n]));
+    dmax = m;
+  }
+  __syncthreads();
+  const double tiny = 1e-32 * dmax;
+  const double floor_lam = fmax(floor_rel * dmax, floor_abs);
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) active = 0;
+    __syncthreads();
+    int local_active = 0;
+    for (int t = 0; t < n; ++t) {
+      const int o = t & 1;
+      const int npair = o ? n / 2 - 1 : n / 2;
+      for (int k = threadIdx.x; k < npair; k += blockDim.x) {
+        const int p = o + 2 * k, q = p + 1;
+        const double app = A[p + static_cast<long long>(p) * n], aqq = A[q + static_cast<long long>(q) * n];
+        const double apq = A[p + static_cast<long long>(q) * n];
+        double c = 1.0, s = 0.0;
+        if (fabs(apq) > tiny && fmax(app, aqq) > floor_lam && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
+          const double theta = (aqq - app) / (2.0 * apq);
+          const double tt = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+          c = 1.0 / sqrt(1.0 + tt * tt);
+          s = tt * c;
+          local_active = 1;
+        }
+        cs[k] = c;
+        sn[k] = s;
+        R[(static_cast<long long>(sweep) * n + t) * (n / 2) + k] = make_double2(c, s);
+      }
+      __syncthreads();
+      // units: o=0 -> pairs (2u, 2u+1); o=1 -> {0}, pairs (2u-1, 2u), {n-1}
+      const int nu = o ? n / 2 + 1 : n / 2;
+      for (int e = threadIdx.x; e < nu * nu; e += blockDim.x) {
+        const int U = e % nu, W = e / nu;
+        if (U > W) continue;
+        int u0, us, w0, ws;  // first index and size of each unit; pair slot for rotation lookup
+        auto unit = [&](int X, int& x0, int& xs) {
+          if (!o) {
+            x0 = 2 * X;
+            xs = 2;
+          } else if (X == 0) {
+            x0 = 0;
+            xs = 1;
+          } else if (X == nu - 1) {
+            x0 = n - 1;
+            xs = 1;
+          } else {
+            x0 = 2 * X - 1;
+            xs = 2;
+          }
+        };
+        unit(U, u0, us);
+        unit(W, w0, ws);
+        const int ku = o ? U - 1 : U, kw = o ? W - 1 : W;
+        // Ĵ = [[s, c], [c, -s]] for a pair (rotation followed by the swap); identity for singletons
+        const double cu = us == 2 ? cs[ku] : 1.0, su = us == 2 ? sn[ku] : 0.0;
+        const double cw = ws == 2 ? cs[kw] : 1.0, sw = ws == 2 ? sn[kw] : 0.0;
+        double* colw0 = A + static_cast<long long>(w0) * n;
+        if (U == W) {
+          if (us == 1) continue;
+          const double app = colw0[u0], apq = colw0[u0 + n], aqq = (colw0 + n)[u0 + 1];
+          const double tt = su / cu;
+          colw0[u0] = aqq + tt * apq;              // swapped diagonal
+          (colw0 + n)[u0 + 1] = app - tt * apq;
+          colw0[u0 + 1] = 0.0;
+          (colw0 + n)[u0] = 0.0;
+          continue;
+        }
+        double a[2][2] = {{0, 0}, {0, 0}};
+        for (int cc = 0; cc < ws; ++cc)
+          for (int rr = 0; rr < us; ++rr) a[rr][cc] = colw0[static_cast<long long>(cc) * n + u0 + rr];
+        // left: Ĵ_uᵀ, right: Ĵ_w
+        double l[2][2];
+        if (us == 2) {
+          for (int cc = 0; cc < ws; ++cc) {
+            l[0][cc] = su * a[0][cc] + cu * a[1][cc];
+            l[1][cc] = cu * a[0][cc] - su * a[1][cc];
+          }
+        } else {
+          for (int cc = 0; cc < ws; ++cc) l[0][cc] = a[0][cc];
+        }
+        double r[2][2];
+        for (int rr = 0; rr < us; ++rr) {
+          if (ws == 2) {
+            r[rr][0] = sw * l[rr][0] + cw * l[rr][1];
+            r[rr][1] = cw * l[rr][0] - sw * l[rr][1];
+          } else {
+            r[rr][0] = l[rr][0];
+          }
+        }
+        double* colu0 = A + static_cast<long long>(u0) * n;
+        for (int cc = 0; cc < ws; ++cc)
+          for (int rr = 0; rr < us; ++rr) {
+            colw0[static_cast<long long>(cc) * n + u0 + rr] = r[rr][cc];
+            colu0[static_cast<long long>(rr) * n + w0 + cc] = r[rr][cc];
+          }
+      }
+      __syncthreads();
+    }
+    if (local_active) atomicOr(&active, 1);
+    __syncthreads();
+    if (!active) {
+      ++sweep;  // the idle sweep still permuted (swaps): keep it in the log
+      break;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) ev[ev_off[b] + i] = A[i + static_cast<long long>(i) * n];
+  if (threadIdx.x == 0) sweeps_out[b] = sweep;
+}
+
+__global__ void __launch_bounds__(256) k_apply_rotations_oe(double* __restrict__ Vout, const int* __restrict__ nvec,
+                                                            const long long* __restrict__ off,
+                                                            const double2* __restrict__ rot,
+                                                            const long long* __restrict__ rot_off,
+                                                            const int* __restrict__ sweeps, const int* __restrict__ ntrue) {
+  extern __shared__ double vs[];
+  const int b = blockIdx.y;
+  const int n = nvec[b];  // padded (even)
+  const int r0 = blockIdx.x * kRows;
+  if (r0 >= n) return;
+  const int rows = min(kRows, n - r0);
+  const int ld = n + 1;
+  for (int e = threadIdx.x; e < kRows * n; e += blockDim.x) {
+    const int rr = e / n, col = e % n;
+    vs[rr * ld + col] = (rr < rows && r0 + rr == col) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const double2* R = rot + rot_off[b];
+  const int total = sweeps[b] * n;
+  for (int t = 0; t < total; ++t) {
+    const int o = t & 1;
+    const int npair = o ? n / 2 - 1 : n / 2;
+    const double2* Rt = R + static_cast<long long>(t) * (n / 2);
+    for (int e = threadIdx.x; e < npair * kRows; e += blockDim.x) {
+      const int k = e / kRows, rr = e % kRows;
+      if (rr >= rows) continue;
+      const double2 csn = Rt[k];
+      const int p = o + 2 * k;
+      double* row = vs + rr * ld;
+      const double a = row[p], bq = row[p + 1];
+      row[p] = csn.y * a + csn.x * bq;
+      row[p + 1] = csn.x * a - csn.y * bq;
+    }
+    __syncthreads();
+  }
+  const int nt = ntrue[b];
+  double* V = Vout + off[b];
+  for (int e = threadIdx.x; e < rows * n; e += blockDim.x) {
+    const int rr = e % rows, col = e / rows;
+    V[(r0 + rr) + static_cast<long long>(col) * n] = vs[rr * ld + col];
+  }
+  (void)nt;
+}
+
+
+// pad to even order (zero row/column; the pad direction stays decoupled: every entry touching
+// it is an exact zero) / compact back, dropping the pad eigenpair
+__global__ void k_pad_copy(const double* __restrict__ A, const long long* __restrict__ off, const int* __restrict__ n,
+                           double* __restrict__ W, const long long* __restrict__ woff, const int* __restrict__ npad) {
+  const int b = blockIdx.x;
+  const int nn = n[b], np = npad[b];
+  for (long long e = threadIdx.x; e < static_cast<long long>(np) * np; e += blockDim.x) {
+    const int r = static_cast<int>(e % np), cc = static_cast<int>(e / np);
+    W[woff[b] + e] = (r < nn && cc < nn) ? A[off[b] + r + static_cast<long long>(cc) * nn] : 0.0;
+  }
+}
+__global__ void k_compact(const double* __restrict__ Vp, const double* __restrict__ evp,
+                          const long long* __restrict__ woff, const long long* __restrict__ eoffp,
+                          const int* __restrict__ n, const int* __restrict__ npad, double* __restrict__ V,
+                          const long long* __restrict__ off, double* __restrict__ ev, const long long* __restrict__ eoff) {
+  const int b = blockIdx.x;
+  const int nn = n[b], np = npad[b];
+  __shared__ int padcol;
+  if (threadIdx.x == 0) {
+    padcol = -1;
+    if (np != nn)
+      for (int cc = 0; cc < np; ++cc)
+        if (Vp[woff[b] + (np - 1) + static_cast<long long>(cc) * np] != 0.0) {
+          padcol = cc;
+          break;
+        }
+  }
+  __syncthreads();
+  for (long long e = threadIdx.x; e < static_cast<long long>(nn) * nn; e += blockDim.x) {
+    const int r = static_cast<int>(e % nn), cc = static_cast<int>(e / nn);
+    const int src = (padcol >= 0 && cc >= padcol) ? cc + 1 : cc;
+    V[off[b] + e] = Vp[woff[b] + r + static_cast<long long>(src) * np];
+  }
+  for (int cc = threadIdx.x; cc < nn; cc += blockDim.x) {
+    const int src = (padcol >= 0 && cc >= padcol) ? cc + 1 : cc;
+    ev[eoff[b] + cc] = evp[eoffp[b] + src];
+  }
+}
+
 }  // namespace
 
 // A: batch of symmetric n_b x n_b column-major matrices at offA[b] (only the upper triangle is
-// read); V receives eigenvectors (same layout), evals[offE] the eigenvalues (unsorted).
+// read by the shared-memory path); V receives eigenvectors (same layout), evals the eigenvalues
+// (unsorted, concatenated). Pairs of directions whose eigenvalues are both below
+// max(floor_rel·max|a_ii|, floor_abs) are not rotated against each other.
 void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vector<int>& n,
-                   const std::vector<long long>& offA, int max_sweeps, bool relative) {
+                   const std::vector<long long>& offA, int max_sweeps, double floor_rel, double floor_abs) {
   ScopedKernelTimer tk(c, "syevj");
   const int B = static_cast<int>(n.size());
   if (B == 0) return;
-  std::vector<long long> offE(B), offS(B);
-  long long e = 0, s = 0;
+  const double tol = 1e-14;
   int nmax = 0;
   for (int b = 0; b < B; ++b) nmax = std::max(nmax, n[b]);
-  const bool use_smem = nmax <= kSmemMaxN;
+  std::vector<long long> offE(B);
+  long long e = 0;
   for (int b = 0; b < B; ++b) {
     offE[b] = e;
     e += n[b];
-    offS[b] = s;
-    if (!use_smem) s += static_cast<long long>(n[b]) * (n[b] + 1) / 2;
   }
-  offS.push_back(use_smem ? static_cast<long long>(nmax) * (nmax + 1) / 2 : 0);  // smem triangle size
-  DBuf<int> dn;
-  DBuf<long long> doff, doffE, doffS;
-  DBuf<double> scr, devals;
-  DBuf<int> dsw;
+  DBuf<int> dn, dsw;
+  DBuf<long long> doff, doffE, droff;
+  DBuf<double2> rot;
   dn.upload(n, c.stream);
   doff.upload(offA, c.stream);
   doffE.upload(offE, c.stream);
-  doffS.upload(offS, c.stream);
-  scr.ensure(std::max<long long>(1, s));
   dsw.ensure(B);
-  const int np = (nmax + 1) / 2;
-  size_t smem = 0;
-  if (use_smem)
-    smem = static_cast<size_t>(nmax) * (nmax + 1) / 2 * sizeof(double);
-  smem += static_cast<size_t>(np) * (2 * sizeof(double) + 2 * sizeof(int));
-  RDD_CUDA(cudaFuncSetAttribute(k_syevj, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  std::vector<long long> roff(B);
-  long long rtot = 0;
-  for (int b = 0; b < B; ++b) {
-    roff[b] = rtot;
-    const int nn = n[b] + (n[b] & 1);
-    rtot += static_cast<long long>(max_sweeps) * std::max(1, nn - 1) * std::max(1, nn / 2);
+  int swmax = 0;
+  if (nmax <= kSmemMaxN) {
+    // ---- round-robin ordering, packed triangle in shared memory
+    std::vector<long long> offS(B, 0);
+    offS.push_back(static_cast<long long>(nmax) * (nmax + 1) / 2);  // smem triangle size
+    DBuf<long long> doffS;
+    DBuf<double> scr;
+    doffS.upload(offS, c.stream);
+    scr.ensure(1);
+    const int np = (nmax + 1) / 2;
+    const size_t smem = static_cast<size_t>(nmax) * (nmax + 1) / 2 * sizeof(double) +
+                        static_cast<size_t>(np) * (2 * sizeof(double) + 2 * sizeof(int));
+    RDD_CUDA(cudaFuncSetAttribute(k_syevj, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    std::vector<long long> roff(B);
+    long long rtot = 0;
+    for (int b = 0; b < B; ++b) {
+      roff[b] = rtot;
+      const int nn = n[b] + (n[b] & 1);
+      rtot += static_cast<long long>(max_sweeps) * std::max(1, nn - 1) * std::max(1, nn / 2);
+    }
+    rot.ensure(std::max<long long>(1, rtot));
+    droff.upload(roff, c.stream);
+    k_syevj<<<B, kThreads, smem, c.stream>>>(A, V, evals, dn.p, doff.p, doffE.p, scr.p, doffS.p, max_sweeps, tol,
+                                             dsw.p, 1, rot.p, droff.p, floor_rel, floor_abs);
+    RDD_LAUNCH_CHECK();
+    const size_t vsm = static_cast<size_t>(kRows) * (nmax + 1) * sizeof(double);
+    RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
+    k_apply_rotations<<<dim3(ceil_div(nmax, kRows), B), 256, vsm, c.stream>>>(V, dn.p, doff.p, rot.p, droff.p, dsw.p);
+    RDD_LAUNCH_CHECK();
+  } else {
+    // ---- odd-even ordering, full storage in global memory (padded to even order)
+    std::vector<int> npad(B);
+    std::vector<long long> woff(B), eoffp(B), roff(B);
+    long long wt = 0, et = 0, rt = 0;
+    for (int b = 0; b < B; ++b) {
+      npad[b] = n[b] + (n[b] & 1);
+      woff[b] = wt;
+      wt += static_cast<long long>(npad[b]) * npad[b];
+      eoffp[b] = et;
+      et += npad[b];
+      roff[b] = rt;
+      rt += static_cast<long long>(max_sweeps) * npad[b] * (npad[b] / 2);
+    }
+    DBuf<double> Wk, Vp, evp;
+    DBuf<int> dnp;
+    DBuf<long long> dwoff, deoffp;
+    Wk.ensure(wt);
+    Vp.ensure(wt);
+    evp.ensure(et);
+    rot.ensure(std::max<long long>(1, rt));
+    dnp.upload(npad, c.stream);
+    dwoff.upload(woff, c.stream);
+    deoffp.upload(eoffp, c.stream);
+    droff.upload(roff, c.stream);
+    k_pad_copy<<<B, 256, 0, c.stream>>>(A, doff.p, dn.p, Wk.p, dwoff.p, dnp.p);
+    RDD_LAUNCH_CHECK();
+    const int nmp = nmax + (nmax & 1);
+    const size_t smem = static_cast<size_t>(nmp + 2) * sizeof(double);
+    k_syevj_oe<<<B, 1024, smem, c.stream>>>(Wk.p, dnp.p, dwoff.p, evp.p, deoffp.p, max_sweeps, tol, dsw.p, rot.p,
+                                             droff.p, floor_rel, floor_abs);
+    RDD_LAUNCH_CHECK();
+    const size_t vsm = static_cast<size_t>(kRows) * (nmp + 1) * sizeof(double);
+    RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations_oe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(vsm)));
+    k_apply_rotations_oe<<<dim3(ceil_div(nmp, kRows), B), 256, vsm, c.stream>>>(Vp.p, dnp.p, dwoff.p, rot.p, droff.p,
+                                                                                 dsw.p, dn.p);
+    RDD_LAUNCH_CHECK();
+    k_compact<<<B, 256, 0, c.stream>>>(Vp.p, evp.p, dwoff.p, deoffp.p, dn.p, dnp.p, V, doff.p, evals, doffE.p);
+    RDD_LAUNCH_CHECK();
   }
-  DBuf<double2> rot;
-  DBuf<long long> droff;
-  rot.ensure(std::max<long long>(1, rtot));
-  droff.upload(roff, c.stream);
-  const double tol = relative ? 1e-15 : 1e-15;
-  k_syevj<<<B, kThreads, smem, c.stream>>>(A, V, evals, dn.p, doff.p, doffE.p, scr.p, doffS.p, max_sweeps, tol,
-                                           dsw.p, use_smem ? 1 : 0, rot.p, droff.p);
-  RDD_LAUNCH_CHECK();
-  const size_t vsm = static_cast<size_t>(kRows) * (nmax + 1) * sizeof(double);
-  RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
-  k_apply_rotations<<<dim3(ceil_div(nmax, kRows), B), 256, vsm, c.stream>>>(V, dn.p, doff.p, rot.p, droff.p, dsw.p);
-  RDD_LAUNCH_CHECK();
   if (c.verbose) {
     std::vector<int> sw(B);
     dsw.download(sw.data(), B, c.stream);
     RDD_CUDA(cudaStreamSynchronize(c.stream));
-    int mx = 0;
-    for (int v : sw) mx = std::max(mx, v);
-    std::fprintf(stderr, "[syevj] B=%d nmax=%d max_sweeps_used=%d\n", B, nmax, mx);
+    for (int v : sw) swmax = std::max(swmax, v);
+    std::fprintf(stderr, "[syevj] B=%d nmax=%d path=%s max_sweeps_used=%d\n", B, nmax,
+                 nmax <= kSmemMaxN ? "smem" : "odd-even", swmax);
   }
   RDD_CUDA(cudaStreamSynchronize(c.stream));
 }

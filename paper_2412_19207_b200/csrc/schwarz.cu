@@ -318,7 +318,7 @@ void build_schwarz(Ctx& c, int kind) {
       te += fn[q];
     }
     lam.ensure(te);
-    batched_syevj(c, Af.p, V.p, lam.p, fn, foff, 60, false);
+    batched_syevj(c, Af.p, V.p, lam.p, fn, foff, 60, 1e-16, 0.0);  // cutoff 1e-12 (schwarz.hpp:82)
     DBuf<long long> devo, dfoff;
     DBuf<int> drank, dfn;
     DBuf<double> dcond;

@@ -30,6 +30,11 @@ def _cases():
     ex3 = A.make_config(A.PROBLEM_EXAMPLE3, [2, 2, 2], 12, [6, 6, 6], seed=5, test=[10, 10, 10],
                         solver=A.SOLVER_CG, precond=A.PRECOND_AS, rel_tol=1e-10)
     c["example3"] = ex3
+    # m > 223 takes the odd-even global-memory Jacobi path in the PCA
+    big = A.make_config(A.PROBLEM_EXAMPLE1, [2, 2], 240, [40, 40], n=2, seed=9, test=[40, 40],
+                        tau_mode=A.TAU_RELATIVE, tau=1e-6, pca_matrix=A.PCA_OP_APPLIED,
+                        solver=A.SOLVER_CG, precond=A.PRECOND_AS, rel_tol=1e-10)
+    c["oe_jacobi"] = big
     return c
 
 

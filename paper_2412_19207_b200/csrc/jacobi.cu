@@ -10,6 +10,8 @@
 // 8.5.1) and the relative threshold |a_pq| > tol·sqrt(|a_pp a_qq|), which is what makes Jacobi
 // relatively accurate on graded matrices (Demmel–Veselić) — the property the PCA refinement
 // relies on.
+#include <cooperative_groups.h>
+
 #include "ctx.hpp"
 
 namespace rdd {
@@ -18,6 +20,8 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kSmemMaxN = 223;  // n(n+1)/2 doubles + pair tables within 227 KB
+constexpr double kMinAngle = 1e-18;  // rotations by smaller angles cannot change V: skipped
+constexpr size_t kCtaSmem = 227 * 1024;
 
 __device__ __forceinline__ long long pidx(int i, int j) {  // packed upper, column-major
   if (i > j) {
@@ -95,7 +99,8 @@ __global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ A
         if (q < n) {
           const double apq = P[pidx(p, q)];
           const double app = P[pidx(p, p)], aqq = P[pidx(q, q)];
-          if (fabs(apq) > tiny && fmax(app, aqq) > floor_lam && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
+          if (fabs(apq) > tiny && fmax(app, aqq) > floor_lam && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq)) &&
+              fabs(apq) > kMinAngle * fabs(app - aqq)) {
             const double theta = (aqq - app) / (2.0 * apq);
             const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
             c = 1.0 / sqrt(1.0 + t * t);
@@ -243,7 +248,8 @@ __global__ void __launch_bounds__(1024) k_syevj_oe(double* __restrict__ Aw, cons
         const double app = A[p + static_cast<long long>(p) * n], aqq = A[q + static_cast<long long>(q) * n];
         const double apq = A[p + static_cast<long long>(q) * n];
         double c = 1.0, s = 0.0;
-        if (fabs(apq) > tiny && fmax(app, aqq) > floor_lam && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
+        if (fabs(apq) > tiny && fmax(app, aqq) > floor_lam && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq)) &&
+            fabs(apq) > kMinAngle * fabs(app - aqq)) {
           const double theta = (aqq - app) / (2.0 * apq);
           const double tt = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
           c = 1.0 / sqrt(1.0 + tt * tt);
@@ -381,6 +387,129 @@ __global__ void __launch_bounds__(256) k_apply_rotations_oe(double* __restrict__
 }
 
 
+// Round-robin Jacobi with the packed triangle distributed over a K-CTA thread-block cluster
+// (distributed shared memory): element e of the packed upper triangle lives in CTA e / chunk.
+// Every CTA computes the round's rotations redundantly (identical inputs -> identical values),
+// then updates its share of the pair-pair blocks; two cluster barriers per round.
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_syevj_cluster(const double* __restrict__ Ain,
+                                                            double* __restrict__ ev, const int* __restrict__ nvec,
+                                                            const long long* __restrict__ off,
+                                                            const long long* __restrict__ ev_off, int max_sweeps,
+                                                            double tol, int* __restrict__ sweeps_out,
+                                                            double2* __restrict__ rot,
+                                                            const long long* __restrict__ rot_off, double floor_rel,
+                                                            double floor_abs, int chunk) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double smem[];
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int b = blockIdx.x / K;
+  const int n = nvec[b];
+  const int nn = n + (n & 1), np = nn / 2;
+  double* cs = smem + chunk;
+  double* sn = cs + np;
+  int* pp = reinterpret_cast<int*>(sn + np);
+  int* qq = pp + np;
+  __shared__ int active;
+  double* base[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r) base[r] = cluster.map_shared_rank(smem, r);
+  auto at = [&](long long e) -> double& { return base[e / chunk][e % chunk]; };
+  const double* A = Ain + off[b];
+  // load my slice of the packed upper triangle (column-packed: e = j(j+1)/2 + i)
+  const long long tot = static_cast<long long>(n) * (n + 1) / 2;
+  const long long e0 = static_cast<long long>(rank) * chunk, e1 = min(tot, e0 + chunk);
+  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    int j = static_cast<int>((sqrt(8.0 * static_cast<double>(e) + 1.0) - 1.0) * 0.5);
+    while (static_cast<long long>(j) * (j + 1) / 2 > e) --j;
+    while (static_cast<long long>(j + 1) * (j + 2) / 2 <= e) ++j;
+    const int i = static_cast<int>(e - static_cast<long long>(j) * (j + 1) / 2);
+    smem[e - e0] = A[i + static_cast<long long>(j) * n];
+  }
+  cluster.sync();
+  double dmax = 0.0;
+  for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(at(pidx(i, i))));
+  const double tiny = 1e-32 * dmax;
+  const double floor_lam = fmax(floor_rel * dmax, floor_abs);
+  double2* R = rot + rot_off[b];
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) active = 0;
+    int local_active = 0;
+    for (int r = 0; r < nn - 1; ++r) {
+      for (int k = threadIdx.x; k < np; k += blockDim.x) {
+        int p = player(k, r, nn), q = player(nn - 1 - k, r, nn);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        double c = 1.0, s = 0.0;
+        if (q < n) {
+          const double apq = at(pidx(p, q)), app = at(pidx(p, p)), aqq = at(pidx(q, q));
+          if (fabs(apq) > tiny && fmax(app, aqq) > floor_lam && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq)) &&
+              fabs(apq) > kMinAngle * fabs(app - aqq)) {
+            const double theta = (aqq - app) / (2.0 * apq);
+            const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            local_active = 1;
+          }
+        }
+        cs[k] = c;
+        sn[k] = s;
+        pp[k] = p;
+        qq[k] = q;
+        if (rank == 0) R[(static_cast<long long>(sweep) * (nn - 1) + r) * np + k] = make_double2(c, s);
+      }
+      cluster.sync();  // all reads of this round's pivots done before any update
+      const int stride = K * blockDim.x;
+      for (int e = rank * blockDim.x + threadIdx.x; e < np * np; e += stride) {
+        const int Pp = e % np, Q = e / np;
+        if (Pp > Q) continue;
+        const double c1 = cs[Pp], s1 = sn[Pp], c2 = cs[Q], s2 = sn[Q];
+        if (s1 == 0.0 && s2 == 0.0) continue;
+        const int p1 = pp[Pp], q1 = qq[Pp], p2 = pp[Q], q2 = qq[Q];
+        if (Pp == Q) {
+          if (q1 >= n) continue;
+          double& app = at(pidx(p1, p1));
+          double& aqq = at(pidx(q1, q1));
+          double& apq = at(pidx(p1, q1));
+          const double t = s1 / c1, vpq = apq;
+          app = app - t * vpq;
+          aqq = aqq + t * vpq;
+          apq = 0.0;
+          continue;
+        }
+        const bool v1 = q1 < n, v2 = q2 < n;
+        double& r11 = at(pidx(p1, p2));
+        const double a11 = r11;
+        const double a12 = v2 ? at(pidx(p1, q2)) : 0.0;
+        const double a21 = v1 ? at(pidx(q1, p2)) : 0.0;
+        const double a22 = (v1 && v2) ? at(pidx(q1, q2)) : 0.0;
+        const double l11 = c1 * a11 - s1 * a21, l12 = c1 * a12 - s1 * a22;
+        const double l21 = s1 * a11 + c1 * a21, l22 = s1 * a12 + c1 * a22;
+        r11 = l11 * c2 - l12 * s2;
+        if (v2) at(pidx(p1, q2)) = l11 * s2 + l12 * c2;
+        if (v1) at(pidx(q1, p2)) = l21 * c2 - l22 * s2;
+        if (v1 && v2) at(pidx(q1, q2)) = l21 * s2 + l22 * c2;
+      }
+      cluster.sync();
+    }
+    if (local_active) atomicOr(cluster.map_shared_rank(&active, 0), 1);
+    cluster.sync();
+    const int any = *cluster.map_shared_rank(&active, 0);
+    cluster.sync();
+    if (!any) break;
+  }
+  if (rank == 0) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ev[ev_off[b] + i] = at(pidx(i, i));
+    if (threadIdx.x == 0) sweeps_out[b] = sweep;
+  }
+  cluster.sync();  // keep every CTA's shared memory alive until all remote reads are done
+}
+
 // pad to even order (zero row/column; the pad direction stays decoupled: every entry touching
 // it is an exact zero) / compact back, dropping the pad eigenpair
 __global__ void k_pad_copy(const double* __restrict__ A, const long long* __restrict__ off, const int* __restrict__ n,
@@ -421,6 +550,15 @@ __global__ void k_compact(const double* __restrict__ Vp, const double* __restric
 }
 
 }  // namespace
+
+// cluster size that holds the packed triangle of order n in distributed shared memory (0: none)
+static int cluster_k(int n) {
+  const size_t tri = static_cast<size_t>(n) * (n + 1) / 2 * sizeof(double);
+  const size_t tables = static_cast<size_t>((n + 1) / 2) * (2 * sizeof(double) + 2 * sizeof(int)) + 1024;
+  for (int K : {2, 4, 8})
+    if ((tri + K - 1) / K + tables <= kCtaSmem) return K;
+  return 0;
+}
 
 // A: batch of symmetric n_b x n_b column-major matrices at offA[b] (only the upper triangle is
 // read by the shared-memory path); V receives eigenvectors (same layout), evals the eigenvalues
@@ -476,6 +614,49 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
     k_apply_rotations<<<dim3(ceil_div(nmax, kRows), B), 256, vsm, c.stream>>>(V, dn.p, doff.p, rot.p, droff.p, dsw.p);
     RDD_LAUNCH_CHECK();
+  } else if (cluster_k(nmax) > 0) {
+    // ---- round-robin ordering, packed triangle across a thread-block cluster (DSMEM)
+    const int K = cluster_k(nmax);
+    const long long tot = static_cast<long long>(nmax) * (nmax + 1) / 2;
+    const int chunk = static_cast<int>((tot + K - 1) / K);
+    const int np = (nmax + 1) / 2;
+    const size_t smem = static_cast<size_t>(chunk) * sizeof(double) +
+                        static_cast<size_t>(np) * (2 * sizeof(double) + 2 * sizeof(int));
+    std::vector<long long> roff(B);
+    long long rtot = 0;
+    for (int b = 0; b < B; ++b) {
+      roff[b] = rtot;
+      const int nn = n[b] + (n[b] & 1);
+      rtot += static_cast<long long>(max_sweeps) * std::max(1, nn - 1) * std::max(1, nn / 2);
+    }
+    rot.ensure(std::max<long long>(1, rtot));
+    droff.upload(roff, c.stream);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(B * K);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = c.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    auto launch = [&](auto kern) {
+      RDD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      RDD_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<const double*>(A), evals, static_cast<const int*>(dn.p),
+                                  static_cast<const long long*>(doff.p), static_cast<const long long*>(doffE.p),
+                                  max_sweeps, tol, dsw.p, rot.p, static_cast<const long long*>(droff.p), floor_rel,
+                                  floor_abs, chunk));
+    };
+    if (K == 2) launch(k_syevj_cluster<2>);
+    else if (K == 4) launch(k_syevj_cluster<4>);
+    else launch(k_syevj_cluster<8>);
+    const size_t vsm = static_cast<size_t>(kRows) * (nmax + 1) * sizeof(double);
+    RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
+    k_apply_rotations<<<dim3(ceil_div(nmax, kRows), B), 256, vsm, c.stream>>>(V, dn.p, doff.p, rot.p, droff.p, dsw.p);
+    RDD_LAUNCH_CHECK();
   } else {
     // ---- odd-even ordering, full storage in global memory (padded to even order)
     std::vector<int> npad(B);
@@ -523,7 +704,7 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     RDD_CUDA(cudaStreamSynchronize(c.stream));
     for (int v : sw) swmax = std::max(swmax, v);
     std::fprintf(stderr, "[syevj] B=%d nmax=%d path=%s max_sweeps_used=%d\n", B, nmax,
-                 nmax <= kSmemMaxN ? "smem" : "odd-even", swmax);
+                 nmax <= kSmemMaxN ? "smem" : (cluster_k(nmax) ? "cluster" : "odd-even"), swmax);
   }
   RDD_CUDA(cudaStreamSynchronize(c.stream));
 }

@@ -30,11 +30,14 @@ def _cases():
     ex3 = A.make_config(A.PROBLEM_EXAMPLE3, [2, 2, 2], 12, [6, 6, 6], seed=5, test=[10, 10, 10],
                         solver=A.SOLVER_CG, precond=A.PRECOND_AS, rel_tol=1e-10)
     c["example3"] = ex3
-    # m > 223 takes the odd-even global-memory Jacobi path in the PCA
+    # 223 < m takes the cluster (distributed shared memory) Jacobi path in the PCA: K=2 and K=4
     big = A.make_config(A.PROBLEM_EXAMPLE1, [2, 2], 240, [40, 40], n=2, seed=9, test=[40, 40],
                         tau_mode=A.TAU_RELATIVE, tau=1e-6, pca_matrix=A.PCA_OP_APPLIED,
                         solver=A.SOLVER_CG, precond=A.PRECOND_AS, rel_tol=1e-10)
-    c["oe_jacobi"] = big
+    c["cluster2_jacobi"] = big
+    c["cluster4_jacobi"] = A.make_config(A.PROBLEM_EXAMPLE1, [2, 2], 400, [48, 48], n=2, seed=11, test=[40, 40],
+                                         tau_mode=A.TAU_RELATIVE, tau=1e-6, pca_matrix=A.PCA_OP_APPLIED,
+                                         solver=A.SOLVER_CG, precond=A.PRECOND_AS, rel_tol=1e-10)
     return c
 
 
@@ -82,7 +85,9 @@ def test_instance_indexing_and_pca(dev, orc, name):
             Vo = orc.getd("V", j).reshape(pj, m).T
             assert np.linalg.norm(_proj(Vd) - _proj(Vo), 2) <= 1e-8, (name, j)
             sd, so = dev.getd("sigma", j), orc.getd("sigma", j)
-            big = so > 1e-8 * so[0]
+            # σ are resolved down to 1% of the threshold (directions further below are inert)
+            thr = cfg.tau * so[0] if cfg.tau_mode == A.TAU_RELATIVE else cfg.tau
+            big = so > max(1e-8 * so[0], 1e-2 * thr)
             assert np.allclose(sd[big], so[big], rtol=1e-9, atol=0), (name, j)
 
 

@@ -29,7 +29,8 @@ for name in names:
                 Vd = dev.getd("V", j).reshape(pj, m).T; Vo = orc.getd("V", j).reshape(pj, m).T
                 worst = max(worst, np.linalg.norm(Vd @ Vd.T - Vo @ Vo.T, 2))
                 sd, so = dev.getd("sigma", j), orc.getd("sigma", j)
-                big = so > 1e-8 * so[0]
+                thr = cfg.tau * so[0] if cfg.tau_mode == A.TAU_RELATIVE else cfg.tau
+                big = so > max(1e-8 * so[0], 1e-2 * thr)
                 sw = max(sw, np.max(np.abs(sd[big] - so[big]) / so[big]))
             print(f" projector max {worst:.2e}  sigma rel max {sw:.2e}")
         eq = cfg.precond >= 0

@@ -226,7 +226,14 @@ void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n
 std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int>& n,
                                   const std::vector<long long>& off, int iters);
 // jacobi.cu
+struct EigOpts {
+  int absolute = 0;       // 1: |a_pq| > tol·max|a_ii| (backward stable); 0: |a_pq| > tol·sqrt|a_pp a_qq| (graded)
+  double tol = 1e-14;
+  double floor_rel = 0.0, floor_abs = 0.0;  // no rotation between two directions both below the floor
+  double conv_rel = 0.0, conv_abs = 0.0;    // convergence judged on directions above this level only
+  int max_sweeps = 40;
+};
 void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vector<int>& n,
-                   const std::vector<long long>& offA, int max_sweeps, double floor_rel, double floor_abs);
+                   const std::vector<long long>& offA, const EigOpts& o);
 
 }  // namespace rdd

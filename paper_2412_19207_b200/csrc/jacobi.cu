@@ -23,6 +23,31 @@ constexpr int kSmemMaxN = 223;  // n(n+1)/2 doubles + pair tables within 227 KB
 constexpr double kMinAngle = 1e-18;  // rotations by smaller angles cannot change V: skipped
 constexpr size_t kCtaSmem = 227 * 1024;
 
+struct Crit {
+  double tol;        // relative (|a_pq| > tol sqrt|a_pp a_qq|) or absolute (|a_pq| > tol * dmax) threshold
+  int absolute;
+  double floor_lam;  // pairs with both diagonals below this are not rotated
+  double conv_lam;   // only rotations touching a diagonal above this keep the sweep loop going
+  double tiny;
+};
+
+// returns 0: skip, 1: rotate (inactive for convergence), 2: rotate and count as active
+__device__ __forceinline__ int rot_decision(const Crit& k, double app, double aqq, double apq) {
+  const double a = fabs(apq);
+  if (!(a > k.tiny)) return 0;
+  const double dm = fmax(app, aqq);
+  if (!(dm > k.floor_lam)) return 0;
+  if (k.absolute ? !(a > k.tol) : !(a > k.tol * sqrt(fabs(app) * fabs(aqq)))) return 0;
+  if (!(a > kMinAngle * fabs(app - aqq))) return 0;
+  return dm > k.conv_lam ? 2 : 1;
+}
+__device__ __forceinline__ void schur2(double app, double aqq, double apq, double& c, double& s) {
+  const double theta = (aqq - app) / (2.0 * apq);
+  const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+  c = 1.0 / sqrt(1.0 + t * t);
+  s = t * c;
+}
+
 __device__ __forceinline__ long long pidx(int i, int j) {  // packed upper, column-major
   if (i > j) {
     const int t = i;
@@ -36,125 +61,122 @@ __device__ __forceinline__ int player(int pos, int r, int nn) {  // round-robin 
   return pos == 0 ? 0 : 1 + (pos - 1 + r) % (nn - 1);
 }
 
-__global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ Ain, double* __restrict__ Vout,
-                                                    double* __restrict__ ev, const int* __restrict__ nvec,
-                                                    const long long* __restrict__ off,
-                                                    const long long* __restrict__ ev_off, double* __restrict__ scratch,
-                                                    const long long* __restrict__ scr_off, int max_sweeps, double tol,
-                                                    int* __restrict__ sweeps_out, int use_smem,
+__global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ Ain, double* __restrict__ ev,
+                                                    const int* __restrict__ nvec, const long long* __restrict__ off,
+                                                    const long long* __restrict__ ev_off, int max_sweeps, Crit crit_in,
+                                                    double floor_rel, double conv_rel, int* __restrict__ sweeps_out,
                                                     double2* __restrict__ rot, const long long* __restrict__ rot_off,
-                                                    double floor_rel, double floor_abs) {
+                                                    int tri_max) {
   extern __shared__ double smem[];
   const int b = blockIdx.x;
   const int n = nvec[b];
   if (n <= 0) return;
-  const int nn = n + (n & 1);  // even number of players (dummy = n)
+  const int nn = n + (n & 1);
   const int np = nn / 2;
-  const long long smem_tri = scr_off[gridDim.x];  // packed size of the largest matrix
   const double* A = Ain + off[b];
-  double2* R = rot + rot_off[b];
-  (void)Vout;
-  const bool in_smem = use_smem != 0;
-  double* P = in_smem ? smem : scratch + scr_off[b];
-  double* cs = in_smem ? smem + smem_tri : smem;  // [np] c, [np] s
+  double* P = smem;                      // packed upper triangle (column-packed)
+  double* cs = smem + tri_max;
   double* sn = cs + np;
   int* pp = reinterpret_cast<int*>(sn + np);
   int* qq = pp + np;
+  int* col = qq + np;                    // col[j] = j(j+1)/2
   __shared__ int active;
-  __shared__ double dmax;
-
-  // load packed upper triangle, V = I
-  const long long tot = static_cast<long long>(n) * (n + 1) / 2;
-  (void)tot;
-  for (long long e = threadIdx.x; e < static_cast<long long>(n) * n; e += blockDim.x) {
-    const int i = static_cast<int>(e % n), j = static_cast<int>(e / n);
-    if (i <= j) P[pidx(i, j)] = A[e];
-  }
+  __shared__ double dmax_s;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) col[j] = j * (j + 1) / 2;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  for (int j = threadIdx.y; j < n; j += blockDim.y)
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) P[col[j] + i] = A[i + static_cast<long long>(j) * n];
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
     double m = 0.0;
-    for (int i = 0; i < n; ++i) m = fmax(m, fabs(P[pidx(i, i)]));
-    dmax = m;
+    for (int i = 0; i < n; ++i) m = fmax(m, fabs(P[col[i] + i]));
+    dmax_s = m;
   }
   __syncthreads();
-  const double tiny = 1e-32 * dmax;
-  // directions whose eigenvalues are both below the floor cannot affect anything above it
-  const double floor_lam = fmax(floor_rel * dmax, floor_abs);
-
+  const double dmax = dmax_s;
+  Crit crit = crit_in;
+  crit.tiny = 1e-32 * dmax;
+  crit.floor_lam = fmax(floor_rel * dmax, crit_in.floor_lam);
+  crit.conv_lam = fmax(conv_rel * dmax, crit_in.conv_lam);
+  if (crit.absolute) crit.tol = crit_in.tol * dmax;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  double2* R = rot + rot_off[b];
+  auto at = [&](int i, int j) -> double& { return i <= j ? P[col[j] + i] : P[col[i] + j]; };
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
-    if (threadIdx.x == 0) active = 0;
-    __syncthreads();
+    if (tid == 0) active = 0;
     int local_active = 0;
     for (int r = 0; r < nn - 1; ++r) {
-      // 1. rotations for the np disjoint pairs of this round
-      for (int k = threadIdx.x; k < np; k += blockDim.x) {
+      for (int k = tid; k < np; k += blockDim.x * blockDim.y) {
         int p = player(k, r, nn), q = player(nn - 1 - k, r, nn);
         if (p > q) {
           const int t = p;
           p = q;
           q = t;
         }
-        double c = 1.0, s = 0.0;
+        double c = 1.0, sv = 0.0;
         if (q < n) {
-          const double apq = P[pidx(p, q)];
-          const double app = P[pidx(p, p)], aqq = P[pidx(q, q)];
-          if (fabs(apq) > tiny && fmax(app, aqq) > floor_lam && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq)) &&
-              fabs(apq) > kMinAngle * fabs(app - aqq)) {
-            const double theta = (aqq - app) / (2.0 * apq);
-            const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-            c = 1.0 / sqrt(1.0 + t * t);
-            s = t * c;
-            local_active = 1;
+          const double app = P[col[p] + p], aqq = P[col[q] + q], apq = P[col[q] + p];
+          const int d = rot_decision(crit, app, aqq, apq);
+          if (d) {
+            schur2(app, aqq, apq, c, sv);
+            if (d == 2) local_active = 1;
           }
         }
         cs[k] = c;
-        sn[k] = s;
+        sn[k] = sv;
         pp[k] = p;
         qq[k] = q;
+        R[(static_cast<long long>(sweep) * (nn - 1) + r) * np + k] = make_double2(c, sv);
       }
       __syncthreads();
-      // 2. A <- Jᵀ A J on unordered pair-pair blocks (P <= Q)
-      for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
-        const int Pp = e % np, Q = e / np;
-        if (Pp > Q) continue;
-        const double c1 = cs[Pp], s1 = sn[Pp], c2 = cs[Q], s2 = sn[Q];
-        if (s1 == 0.0 && s2 == 0.0) continue;
-        const int p1 = pp[Pp], q1 = qq[Pp], p2 = pp[Q], q2 = qq[Q];
-        if (Pp == Q) {
-          if (q1 >= n) continue;
-          const double app = P[pidx(p1, p1)], aqq = P[pidx(q1, q1)], apq = P[pidx(p1, q1)];
-          const double t = s1 / c1;
-          P[pidx(p1, p1)] = app - t * apq;
-          P[pidx(q1, q1)] = aqq + t * apq;
-          P[pidx(p1, q1)] = 0.0;
-          continue;
+      // A <- Jᵀ A J on unordered pair-pair blocks (P <= Q); 2-D thread grid, no div/mod
+      for (int Q = threadIdx.y; Q < np; Q += blockDim.y) {
+        const double c2 = cs[Q], s2 = sn[Q];
+        const int p2 = pp[Q], q2 = qq[Q];
+        const bool v2 = q2 < n;
+        for (int Pp = threadIdx.x; Pp <= Q; Pp += blockDim.x) {
+          const double c1 = cs[Pp], s1 = sn[Pp];
+          if (s1 == 0.0 && s2 == 0.0) continue;
+          const int p1 = pp[Pp], q1 = qq[Pp];
+          if (Pp == Q) {
+            if (!v2) continue;
+            double& app = P[col[p1] + p1];
+            double& aqq = P[col[q1] + q1];
+            double& apq = P[col[q1] + p1];
+            const double t = s1 / c1, vpq = apq;
+            app = app - t * vpq;
+            aqq = aqq + t * vpq;
+            apq = 0.0;
+            continue;
+          }
+          const bool v1 = q1 < n;
+          double& r11 = at(p1, p2);
+          const double a11 = r11;
+          const double a12 = v2 ? at(p1, q2) : 0.0;
+          const double a21 = v1 ? at(q1, p2) : 0.0;
+          const double a22 = (v1 && v2) ? at(q1, q2) : 0.0;
+          const double l11 = c1 * a11 - s1 * a21, l12 = c1 * a12 - s1 * a22;
+          const double l21 = s1 * a11 + c1 * a21, l22 = s1 * a12 + c1 * a22;
+          r11 = l11 * c2 - l12 * s2;
+          if (v2) at(p1, q2) = l11 * s2 + l12 * c2;
+          if (v1) at(q1, p2) = l21 * c2 - l22 * s2;
+          if (v1 && v2) at(q1, q2) = l21 * s2 + l22 * c2;
         }
-        const bool v1 = q1 < n, v2 = q2 < n;  // dummy player rows/cols do not exist
-        const double a11 = P[pidx(p1, p2)];
-        const double a12 = v2 ? P[pidx(p1, q2)] : 0.0;
-        const double a21 = v1 ? P[pidx(q1, p2)] : 0.0;
-        const double a22 = (v1 && v2) ? P[pidx(q1, q2)] : 0.0;
-        // left: [[c1, -s1], [s1, c1]] ; right: [[c2, s2], [-s2, c2]]
-        const double l11 = c1 * a11 - s1 * a21, l12 = c1 * a12 - s1 * a22;
-        const double l21 = s1 * a11 + c1 * a21, l22 = s1 * a12 + c1 * a22;
-        P[pidx(p1, p2)] = l11 * c2 - l12 * s2;
-        if (v2) P[pidx(p1, q2)] = l11 * s2 + l12 * c2;
-        if (v1) P[pidx(q1, p2)] = l21 * c2 - l22 * s2;
-        if (v1 && v2) P[pidx(q1, q2)] = l21 * s2 + l22 * c2;
       }
-      // 3. log the rotations; V is accumulated afterwards, row-parallel (k_apply_rotations)
-      for (int k = threadIdx.x; k < np; k += blockDim.x)
-        R[(static_cast<long long>(sweep) * (nn - 1) + r) * np + k] = make_double2(cs[k], sn[k]);
       __syncthreads();
     }
     if (local_active) atomicOr(&active, 1);
     __syncthreads();
-    if (!active) break;
+    const int any = active;
     __syncthreads();
+    if (!any) {
+      ++sweep;  // this sweep's (inactive-only) rotations were applied: keep them in the log
+      break;
+    }
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) ev[ev_off[b] + i] = P[pidx(i, i)];
-  if (threadIdx.x == 0 && sweeps_out) sweeps_out[b] = sweep;
+  for (int i = tid; i < n; i += blockDim.x * blockDim.y) ev[ev_off[b] + i] = P[col[i] + i];
+  if (tid == 0) sweeps_out[b] = sweep;
 }
 
 // V = J_1 J_2 ... J_R (all logged rounds): rows are independent, so each CTA keeps kRows rows
@@ -213,10 +235,10 @@ __global__ void __launch_bounds__(256) k_apply_rotations(double* __restrict__ Vo
 // steps, while each 2x2 update touches two contiguous 16-byte column segments.
 __global__ void __launch_bounds__(1024) k_syevj_oe(double* __restrict__ Aw, const int* __restrict__ nvec,
                                                    const long long* __restrict__ off, double* __restrict__ ev,
-                                                   const long long* __restrict__ ev_off, int max_sweeps, double tol,
+                                                   const long long* __restrict__ ev_off, int max_sweeps,
                                                    int* __restrict__ sweeps_out, double2* __restrict__ rot,
-                                                   const long long* __restrict__ rot_off, double floor_rel,
-                                                   double floor_abs) {
+                                                   const long long* __restrict__ rot_off, Crit crit_in,
+                                                   double floor_rel, double conv_rel) {
   extern __shared__ double sm[];
   const int b = blockIdx.x;
   const int n = nvec[b];  // even (padded by the host)
@@ -233,8 +255,11 @@ __global__ void __launch_bounds__(1024) k_syevj_oe(double* __restrict__ Aw, cons
     dmax = m;
   }
   __syncthreads();
-  const double tiny = 1e-32 * dmax;
-  const double floor_lam = fmax(floor_rel * dmax, floor_abs);
+  Crit crit = crit_in;
+  crit.tiny = 1e-32 * dmax;
+  crit.floor_lam = fmax(floor_rel * dmax, crit_in.floor_lam);
+  crit.conv_lam = fmax(conv_rel * dmax, crit_in.conv_lam);
+  if (crit.absolute) crit.tol = crit_in.tol * dmax;
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     if (threadIdx.x == 0) active = 0;
@@ -248,13 +273,10 @@ __global__ void __launch_bounds__(1024) k_syevj_oe(double* __restrict__ Aw, cons
         const double app = A[p + static_cast<long long>(p) * n], aqq = A[q + static_cast<long long>(q) * n];
         const double apq = A[p + static_cast<long long>(q) * n];
         double c = 1.0, s = 0.0;
-        if (fabs(apq) > tiny && fmax(app, aqq) > floor_lam && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq)) &&
-            fabs(apq) > kMinAngle * fabs(app - aqq)) {
-          const double theta = (aqq - app) / (2.0 * apq);
-          const double tt = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-          c = 1.0 / sqrt(1.0 + tt * tt);
-          s = tt * c;
-          local_active = 1;
+        const int d = rot_decision(crit, app, aqq, apq);
+        if (d) {
+          schur2(app, aqq, apq, c, s);
+          if (d == 2) local_active = 1;
         }
         cs[k] = c;
         sn[k] = s;
@@ -396,10 +418,9 @@ __global__ void __launch_bounds__(kThreads) k_syevj_cluster(const double* __rest
                                                             double* __restrict__ ev, const int* __restrict__ nvec,
                                                             const long long* __restrict__ off,
                                                             const long long* __restrict__ ev_off, int max_sweeps,
-                                                            double tol, int* __restrict__ sweeps_out,
-                                                            double2* __restrict__ rot,
-                                                            const long long* __restrict__ rot_off, double floor_rel,
-                                                            double floor_abs, int chunk) {
+                                                            Crit crit_in, double floor_rel, double conv_rel,
+                                                            int* __restrict__ sweeps_out, double2* __restrict__ rot,
+                                                            const long long* __restrict__ rot_off, int chunk) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ double smem[];
@@ -411,89 +432,111 @@ __global__ void __launch_bounds__(kThreads) k_syevj_cluster(const double* __rest
   double* sn = cs + np;
   int* pp = reinterpret_cast<int*>(sn + np);
   int* qq = pp + np;
+  int* lcol = qq + np;                  // local start of column j inside its owner CTA
+  unsigned char* own = reinterpret_cast<unsigned char*>(lcol + n);  // owner CTA of column j
   __shared__ int active;
   double* base[K];
 #pragma unroll
   for (int r = 0; r < K; ++r) base[r] = cluster.map_shared_rank(smem, r);
-  auto at = [&](long long e) -> double& { return base[e / chunk][e % chunk]; };
+  // whole columns per CTA: column j goes to CTA floor(j(j+1)/2 / chunk); chunk leaves room for it
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    int cur = 0, start = 0;
+    for (int j = 0; j < n; ++j) {
+      const int e = j * (j + 1) / 2;
+      while (cur + 1 < K && e + j + 1 - start > chunk) {
+        ++cur;
+        start = e;
+      }
+      own[j] = static_cast<unsigned char>(cur);
+      lcol[j] = e - start;
+    }
+  }
+  __syncthreads();
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int nthr = blockDim.x * blockDim.y;
+  auto at = [&](int i, int j) -> double& {
+    if (i > j) {
+      const int t = i;
+      i = j;
+      j = t;
+    }
+    return base[own[j]][lcol[j] + i];
+  };
   const double* A = Ain + off[b];
-  // load my slice of the packed upper triangle (column-packed: e = j(j+1)/2 + i)
-  const long long tot = static_cast<long long>(n) * (n + 1) / 2;
-  const long long e0 = static_cast<long long>(rank) * chunk, e1 = min(tot, e0 + chunk);
-  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    int j = static_cast<int>((sqrt(8.0 * static_cast<double>(e) + 1.0) - 1.0) * 0.5);
-    while (static_cast<long long>(j) * (j + 1) / 2 > e) --j;
-    while (static_cast<long long>(j + 1) * (j + 2) / 2 <= e) ++j;
-    const int i = static_cast<int>(e - static_cast<long long>(j) * (j + 1) / 2);
-    smem[e - e0] = A[i + static_cast<long long>(j) * n];
+  for (int j = threadIdx.y; j < n; j += blockDim.y) {
+    if (own[j] != rank) continue;
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) smem[lcol[j] + i] = A[i + static_cast<long long>(j) * n];
   }
   cluster.sync();
   double dmax = 0.0;
-  for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(at(pidx(i, i))));
-  const double tiny = 1e-32 * dmax;
-  const double floor_lam = fmax(floor_rel * dmax, floor_abs);
+  for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(at(i, i)));
+  Crit crit = crit_in;
+  crit.tiny = 1e-32 * dmax;
+  crit.floor_lam = fmax(floor_rel * dmax, crit_in.floor_lam);
+  crit.conv_lam = fmax(conv_rel * dmax, crit_in.conv_lam);
+  if (crit.absolute) crit.tol = crit_in.tol * dmax;
   double2* R = rot + rot_off[b];
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
-    if (threadIdx.x == 0) active = 0;
+    if (tid == 0) active = 0;
     int local_active = 0;
     for (int r = 0; r < nn - 1; ++r) {
-      for (int k = threadIdx.x; k < np; k += blockDim.x) {
+      for (int k = tid; k < np; k += nthr) {
         int p = player(k, r, nn), q = player(nn - 1 - k, r, nn);
         if (p > q) {
           const int t = p;
           p = q;
           q = t;
         }
-        double c = 1.0, s = 0.0;
+        double c = 1.0, sv = 0.0;
         if (q < n) {
-          const double apq = at(pidx(p, q)), app = at(pidx(p, p)), aqq = at(pidx(q, q));
-          if (fabs(apq) > tiny && fmax(app, aqq) > floor_lam && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq)) &&
-              fabs(apq) > kMinAngle * fabs(app - aqq)) {
-            const double theta = (aqq - app) / (2.0 * apq);
-            const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-            c = 1.0 / sqrt(1.0 + t * t);
-            s = t * c;
-            local_active = 1;
+          const double app = at(p, p), aqq = at(q, q), apq = at(p, q);
+          const int d = rot_decision(crit, app, aqq, apq);
+          if (d) {
+            schur2(app, aqq, apq, c, sv);
+            if (d == 2) local_active = 1;
           }
         }
         cs[k] = c;
-        sn[k] = s;
+        sn[k] = sv;
         pp[k] = p;
         qq[k] = q;
-        if (rank == 0) R[(static_cast<long long>(sweep) * (nn - 1) + r) * np + k] = make_double2(c, s);
+        if (rank == 0) R[(static_cast<long long>(sweep) * (nn - 1) + r) * np + k] = make_double2(c, sv);
       }
       cluster.sync();  // all reads of this round's pivots done before any update
-      const int stride = K * blockDim.x;
-      for (int e = rank * blockDim.x + threadIdx.x; e < np * np; e += stride) {
-        const int Pp = e % np, Q = e / np;
-        if (Pp > Q) continue;
-        const double c1 = cs[Pp], s1 = sn[Pp], c2 = cs[Q], s2 = sn[Q];
-        if (s1 == 0.0 && s2 == 0.0) continue;
-        const int p1 = pp[Pp], q1 = qq[Pp], p2 = pp[Q], q2 = qq[Q];
-        if (Pp == Q) {
-          if (q1 >= n) continue;
-          double& app = at(pidx(p1, p1));
-          double& aqq = at(pidx(q1, q1));
-          double& apq = at(pidx(p1, q1));
-          const double t = s1 / c1, vpq = apq;
-          app = app - t * vpq;
-          aqq = aqq + t * vpq;
-          apq = 0.0;
-          continue;
+      // blocks (P <= Q): CTA `rank` takes the Q rows Q = rank, rank+K, ... (balanced triangles)
+      for (int Q = rank + K * threadIdx.y; Q < np; Q += K * blockDim.y) {
+        const double c2 = cs[Q], s2 = sn[Q];
+        const int p2 = pp[Q], q2 = qq[Q];
+        const bool v2 = q2 < n;
+        for (int Pp = threadIdx.x; Pp <= Q; Pp += blockDim.x) {
+          const double c1 = cs[Pp], s1 = sn[Pp];
+          if (s1 == 0.0 && s2 == 0.0) continue;
+          const int p1 = pp[Pp], q1 = qq[Pp];
+          if (Pp == Q) {
+            if (!v2) continue;
+            double& app = at(p1, p1);
+            double& aqq = at(q1, q1);
+            double& apq = at(p1, q1);
+            const double t = s1 / c1, vpq = apq;
+            app = app - t * vpq;
+            aqq = aqq + t * vpq;
+            apq = 0.0;
+            continue;
+          }
+          const bool v1 = q1 < n;
+          double& r11 = at(p1, p2);
+          const double a11 = r11;
+          const double a12 = v2 ? at(p1, q2) : 0.0;
+          const double a21 = v1 ? at(q1, p2) : 0.0;
+          const double a22 = (v1 && v2) ? at(q1, q2) : 0.0;
+          const double l11 = c1 * a11 - s1 * a21, l12 = c1 * a12 - s1 * a22;
+          const double l21 = s1 * a11 + c1 * a21, l22 = s1 * a12 + c1 * a22;
+          r11 = l11 * c2 - l12 * s2;
+          if (v2) at(p1, q2) = l11 * s2 + l12 * c2;
+          if (v1) at(q1, p2) = l21 * c2 - l22 * s2;
+          if (v1 && v2) at(q1, q2) = l21 * s2 + l22 * c2;
         }
-        const bool v1 = q1 < n, v2 = q2 < n;
-        double& r11 = at(pidx(p1, p2));
-        const double a11 = r11;
-        const double a12 = v2 ? at(pidx(p1, q2)) : 0.0;
-        const double a21 = v1 ? at(pidx(q1, p2)) : 0.0;
-        const double a22 = (v1 && v2) ? at(pidx(q1, q2)) : 0.0;
-        const double l11 = c1 * a11 - s1 * a21, l12 = c1 * a12 - s1 * a22;
-        const double l21 = s1 * a11 + c1 * a21, l22 = s1 * a12 + c1 * a22;
-        r11 = l11 * c2 - l12 * s2;
-        if (v2) at(pidx(p1, q2)) = l11 * s2 + l12 * c2;
-        if (v1) at(pidx(q1, p2)) = l21 * c2 - l22 * s2;
-        if (v1 && v2) at(pidx(q1, q2)) = l21 * s2 + l22 * c2;
       }
       cluster.sync();
     }
@@ -501,13 +544,16 @@ __global__ void __launch_bounds__(kThreads) k_syevj_cluster(const double* __rest
     cluster.sync();
     const int any = *cluster.map_shared_rank(&active, 0);
     cluster.sync();
-    if (!any) break;
+    if (!any) {
+      ++sweep;
+      break;
+    }
   }
   if (rank == 0) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) ev[ev_off[b] + i] = at(pidx(i, i));
-    if (threadIdx.x == 0) sweeps_out[b] = sweep;
+    for (int i = tid; i < n; i += nthr) ev[ev_off[b] + i] = at(i, i);
+    if (tid == 0) sweeps_out[b] = sweep;
   }
-  cluster.sync();  // keep every CTA's shared memory alive until all remote reads are done
+  cluster.sync();  // keep every CTA's shared memory alive until all remote accesses are done
 }
 
 // pad to even order (zero row/column; the pad direction stays decoupled: every entry touching
@@ -552,24 +598,37 @@ __global__ void k_compact(const double* __restrict__ Vp, const double* __restric
 }  // namespace
 
 // cluster size that holds the packed triangle of order n in distributed shared memory (0: none)
+static size_t cluster_chunk(int n, int K) {
+  const size_t tri = static_cast<size_t>(n) * (n + 1) / 2;
+  return (tri + K - 1) / K + n;  // whole columns per CTA: one column of slack
+}
+static size_t cluster_smem(int n, int K) {
+  return cluster_chunk(n, K) * sizeof(double) + static_cast<size_t>((n + 1) / 2) * (2 * sizeof(double) + 2 * sizeof(int)) +
+         static_cast<size_t>(n) * (sizeof(int) + 1) + 64;
+}
 static int cluster_k(int n) {
-  const size_t tri = static_cast<size_t>(n) * (n + 1) / 2 * sizeof(double);
-  const size_t tables = static_cast<size_t>((n + 1) / 2) * (2 * sizeof(double) + 2 * sizeof(int)) + 1024;
   for (int K : {2, 4, 8})
-    if ((tri + K - 1) / K + tables <= kCtaSmem) return K;
+    if (cluster_smem(n, K) <= kCtaSmem) return K;
   return 0;
 }
+static size_t smem_path_bytes(int n) {
+  return static_cast<size_t>(n) * (n + 1) / 2 * sizeof(double) +
+         static_cast<size_t>((n + 1) / 2) * (2 * sizeof(double) + 2 * sizeof(int)) + static_cast<size_t>(n) * sizeof(int);
+}
 
-// A: batch of symmetric n_b x n_b column-major matrices at offA[b] (only the upper triangle is
-// read by the shared-memory path); V receives eigenvectors (same layout), evals the eigenvalues
-// (unsorted, concatenated). Pairs of directions whose eigenvalues are both below
-// max(floor_rel·max|a_ii|, floor_abs) are not rotated against each other.
+// A: batch of symmetric n_b x n_b column-major matrices at offA[b] (the upper triangle is read);
+// V receives eigenvectors (same layout), evals the eigenvalues (unsorted, concatenated).
 void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vector<int>& n,
-                   const std::vector<long long>& offA, int max_sweeps, double floor_rel, double floor_abs) {
+                   const std::vector<long long>& offA, const EigOpts& o) {
   ScopedKernelTimer tk(c, "syevj");
   const int B = static_cast<int>(n.size());
   if (B == 0) return;
-  const double tol = 1e-14;
+  const int max_sweeps = o.max_sweeps;
+  Crit crit{};
+  crit.tol = o.tol;
+  crit.absolute = o.absolute;
+  crit.floor_lam = o.floor_abs;
+  crit.conv_lam = o.conv_abs;
   int nmax = 0;
   for (int b = 0; b < B; ++b) nmax = std::max(nmax, n[b]);
   std::vector<long long> offE(B);
@@ -586,18 +645,9 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
   doffE.upload(offE, c.stream);
   dsw.ensure(B);
   int swmax = 0;
-  if (nmax <= kSmemMaxN) {
-    // ---- round-robin ordering, packed triangle in shared memory
-    std::vector<long long> offS(B, 0);
-    offS.push_back(static_cast<long long>(nmax) * (nmax + 1) / 2);  // smem triangle size
-    DBuf<long long> doffS;
-    DBuf<double> scr;
-    doffS.upload(offS, c.stream);
-    scr.ensure(1);
-    const int np = (nmax + 1) / 2;
-    const size_t smem = static_cast<size_t>(nmax) * (nmax + 1) / 2 * sizeof(double) +
-                        static_cast<size_t>(np) * (2 * sizeof(double) + 2 * sizeof(int));
-    RDD_CUDA(cudaFuncSetAttribute(k_syevj, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const bool smem_path = smem_path_bytes(nmax) <= kCtaSmem;
+  const int K = smem_path ? 1 : cluster_k(nmax);
+  if (smem_path || K > 0) {
     std::vector<long long> roff(B);
     long long rtot = 0;
     for (int b = 0; b < B; ++b) {
@@ -607,52 +657,41 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     }
     rot.ensure(std::max<long long>(1, rtot));
     droff.upload(roff, c.stream);
-    k_syevj<<<B, kThreads, smem, c.stream>>>(A, V, evals, dn.p, doff.p, doffE.p, scr.p, doffS.p, max_sweeps, tol,
-                                             dsw.p, 1, rot.p, droff.p, floor_rel, floor_abs);
-    RDD_LAUNCH_CHECK();
-    const size_t vsm = static_cast<size_t>(kRows) * (nmax + 1) * sizeof(double);
-    RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
-    k_apply_rotations<<<dim3(ceil_div(nmax, kRows), B), 256, vsm, c.stream>>>(V, dn.p, doff.p, rot.p, droff.p, dsw.p);
-    RDD_LAUNCH_CHECK();
-  } else if (cluster_k(nmax) > 0) {
-    // ---- round-robin ordering, packed triangle across a thread-block cluster (DSMEM)
-    const int K = cluster_k(nmax);
-    const long long tot = static_cast<long long>(nmax) * (nmax + 1) / 2;
-    const int chunk = static_cast<int>((tot + K - 1) / K);
-    const int np = (nmax + 1) / 2;
-    const size_t smem = static_cast<size_t>(chunk) * sizeof(double) +
-                        static_cast<size_t>(np) * (2 * sizeof(double) + 2 * sizeof(int));
-    std::vector<long long> roff(B);
-    long long rtot = 0;
-    for (int b = 0; b < B; ++b) {
-      roff[b] = rtot;
-      const int nn = n[b] + (n[b] & 1);
-      rtot += static_cast<long long>(max_sweeps) * std::max(1, nn - 1) * std::max(1, nn / 2);
+    if (smem_path) {
+      // ---- round-robin ordering, packed triangle in shared memory
+      const size_t smem = smem_path_bytes(nmax);
+      const int tri_max = nmax * (nmax + 1) / 2;
+      RDD_CUDA(cudaFuncSetAttribute(k_syevj, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      k_syevj<<<B, dim3(32, kThreads / 32), smem, c.stream>>>(A, evals, dn.p, doff.p, doffE.p, max_sweeps, crit,
+                                                             o.floor_rel, o.conv_rel, dsw.p, rot.p, droff.p, tri_max);
+      RDD_LAUNCH_CHECK();
+    } else {
+      // ---- round-robin ordering, packed triangle across a thread-block cluster (DSMEM)
+      const int chunk = static_cast<int>(cluster_chunk(nmax, K));
+      const size_t smem = cluster_smem(nmax, K);
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(B * K);
+      lc.blockDim = dim3(32, kThreads / 32);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = c.stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = K;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      auto launch = [&](auto kern) {
+        RDD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        RDD_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<const double*>(A), evals, static_cast<const int*>(dn.p),
+                                    static_cast<const long long*>(doff.p), static_cast<const long long*>(doffE.p),
+                                    max_sweeps, crit, o.floor_rel, o.conv_rel, dsw.p, rot.p,
+                                    static_cast<const long long*>(droff.p), chunk));
+      };
+      if (K == 2) launch(k_syevj_cluster<2>);
+      else if (K == 4) launch(k_syevj_cluster<4>);
+      else launch(k_syevj_cluster<8>);
     }
-    rot.ensure(std::max<long long>(1, rtot));
-    droff.upload(roff, c.stream);
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(B * K);
-    lc.blockDim = dim3(kThreads);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = c.stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = K;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    auto launch = [&](auto kern) {
-      RDD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      RDD_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<const double*>(A), evals, static_cast<const int*>(dn.p),
-                                  static_cast<const long long*>(doff.p), static_cast<const long long*>(doffE.p),
-                                  max_sweeps, tol, dsw.p, rot.p, static_cast<const long long*>(droff.p), floor_rel,
-                                  floor_abs, chunk));
-    };
-    if (K == 2) launch(k_syevj_cluster<2>);
-    else if (K == 4) launch(k_syevj_cluster<4>);
-    else launch(k_syevj_cluster<8>);
     const size_t vsm = static_cast<size_t>(kRows) * (nmax + 1) * sizeof(double);
     RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
     k_apply_rotations<<<dim3(ceil_div(nmax, kRows), B), 256, vsm, c.stream>>>(V, dn.p, doff.p, rot.p, droff.p, dsw.p);
@@ -686,8 +725,8 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     RDD_LAUNCH_CHECK();
     const int nmp = nmax + (nmax & 1);
     const size_t smem = static_cast<size_t>(nmp + 2) * sizeof(double);
-    k_syevj_oe<<<B, 1024, smem, c.stream>>>(Wk.p, dnp.p, dwoff.p, evp.p, deoffp.p, max_sweeps, tol, dsw.p, rot.p,
-                                             droff.p, floor_rel, floor_abs);
+    k_syevj_oe<<<B, 1024, smem, c.stream>>>(Wk.p, dnp.p, dwoff.p, evp.p, deoffp.p, max_sweeps, dsw.p, rot.p, droff.p,
+                                             crit, o.floor_rel, o.conv_rel);
     RDD_LAUNCH_CHECK();
     const size_t vsm = static_cast<size_t>(kRows) * (nmp + 1) * sizeof(double);
     RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations_oe, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -704,7 +743,7 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     RDD_CUDA(cudaStreamSynchronize(c.stream));
     for (int v : sw) swmax = std::max(swmax, v);
     std::fprintf(stderr, "[syevj] B=%d nmax=%d path=%s max_sweeps_used=%d\n", B, nmax,
-                 nmax <= kSmemMaxN ? "smem" : (cluster_k(nmax) ? "cluster" : "odd-even"), swmax);
+                 smem_path ? "smem" : (K ? "cluster" : "odd-even"), swmax);
   }
   RDD_CUDA(cudaStreamSynchronize(c.stream));
 }

@@ -105,16 +105,27 @@ void run_pca(Ctx& c) {
     V0.ensure(J * mm);
     lam.ensure(static_cast<size_t>(J) * m);
     std::vector<int> ns(J, m);
-    // eigen-directions 4 decades below the truncation threshold (in λ = σ²) cannot change the
-    // kept subspace or the rank: they are not rotated against each other
-    const double tau2 = c.cfg.tau * c.cfg.tau;
-    const double floor_rel = c.cfg.tau_mode == RDD_TAU_RELATIVE ? 1e-4 * tau2 : 1e-30;
-    const double floor_abs = c.cfg.tau_mode == RDD_TAU_ABSOLUTE ? 1e-4 * tau2 : 0.0;
     std::vector<long long> offm(J);
     for (int j = 0; j < J; ++j) offm[j] = static_cast<long long>(j) * mm;
+    // stage 1 only needs a backward-stable basis (absolute criterion); stage 2 works on the graded
+    // Gram with the relative criterion. Directions 4 decades (in λ = σ²) below the threshold are
+    // not rotated against each other, and convergence is judged on those within 2 decades.
+    const double tau2 = c.cfg.tau * c.cfg.tau;
+    const bool rel = c.cfg.tau_mode == RDD_TAU_RELATIVE;
+    EigOpts s1, s2;
+    s1.absolute = 1;
+    s1.tol = 1e-14;
+    s1.floor_rel = 1e-13;
+    s1.conv_rel = 1e-12;
+    s2.absolute = 0;
+    s2.tol = 1e-14;
+    s2.floor_rel = rel ? 1e-4 * tau2 : 0.0;
+    s2.floor_abs = rel ? 0.0 : 1e-4 * tau2;
+    s2.conv_rel = rel ? 1e-2 * tau2 : 0.0;
+    s2.conv_abs = rel ? 0.0 : 1e-2 * tau2;
     // stage 1: Gram + Jacobi
     gemm_tn(c, gram_tasks(c, c.S.p, G.p, c.S_off));
-    batched_syevj(c, G.p, V0.p, lam.p, ns, offm, 40, floor_rel, floor_abs);
+    batched_syevj(c, G.p, V0.p, lam.p, ns, offm, s1);
     // stage 2: T = S V0, G1 = TᵀT, Jacobi on the graded G1
     T.ensure(std::max<long long>(1, c.S_off[J]));
     {
@@ -131,7 +142,7 @@ void run_pca(Ctx& c) {
     gemm_tn(c, gram_tasks(c, T.p, G.p, c.S_off));
     T.release();
     W.ensure(J * mm);
-    batched_syevj(c, G.p, W.p, lam.p, ns, offm, 40, floor_rel, floor_abs);
+    batched_syevj(c, G.p, W.p, lam.p, ns, offm, s2);
     // V = V0 W
     Vfull.ensure(J * mm);
     {

@@ -318,7 +318,13 @@ void build_schwarz(Ctx& c, int kind) {
       te += fn[q];
     }
     lam.ensure(te);
-    batched_syevj(c, Af.p, V.p, lam.p, fn, foff, 60, 1e-16, 0.0);  // cutoff 1e-12 (schwarz.hpp:82)
+    EigOpts eo;  // backward stable like SelfAdjointEigenSolver; the cutoff is 1e-12·λmax (schwarz.hpp:82)
+    eo.absolute = 1;
+    eo.tol = 1e-15;
+    eo.floor_rel = 1e-16;
+    eo.conv_rel = 1e-14;
+    eo.max_sweeps = 60;
+    batched_syevj(c, Af.p, V.p, lam.p, fn, foff, eo);
     DBuf<long long> devo, dfoff;
     DBuf<int> drank, dfn;
     DBuf<double> dcond;

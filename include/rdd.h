@@ -130,6 +130,15 @@ int rdd_evaluate(rdd_ctx* ctx, const int* test_res);
 /* runner.hpp:202-275 run_single */
 int rdd_run_single(rdd_ctx* ctx, const rdd_config* cfg, uint64_t seed, rdd_summary* out);
 int rdd_get_summary(rdd_ctx* ctx, rdd_summary* out);
+/* run_single again on the inputs already resident in HBM (bench: inputs resident when timing) */
+int rdd_rerun_resident(rdd_ctx* ctx, rdd_summary* out);
+/* number of library kernel launches issued by the calling thread so far */
+int64_t rdd_launch_count(void);
+/* cumulative host->device / device->host bytes copied by the calling thread */
+int rdd_io_bytes(int64_t* h2d, int64_t* d2h);
+/* CUDA events on the context's stream (slots 0..7) and the elapsed device time between two */
+int rdd_event_record(rdd_ctx* ctx, int slot);
+int rdd_event_elapsed(rdd_ctx* ctx, int slot_a, int slot_b, double* ms);
 
 /* ---- operators (pluggable into the reference's LinearMap, krylov.hpp:42-52) ---------- */
 int rdd_matvec(rdd_ctx* ctx, const double* w, double* y);            /* assembly.hpp:110 */

@@ -82,10 +82,21 @@ static void assemble(Ctx& c, bool equilibrate) {
   c.equilibrated = equilibrate;
 }
 
-static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed) {
+// resident = true reruns the pipeline on the inputs already in HBM (points, boxes, bases)
+static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed, bool resident = false) {
   RDD_CUDA(cudaStreamSynchronize(c.stream));
   double t0 = now_s();
-  build_instance(c, cfg, seed);
+  if (resident) {
+    if (c.J == 0 || c.seed != seed) throw std::invalid_argument("rerun: no resident instance for this seed");
+    reset_state(c);
+    c.cfg = cfg;
+    build_index(c);
+    eval_problem(c);
+    run_pca(c);
+    ensure_col_owner(c);
+  } else {
+    build_instance(c, cfg, seed);
+  }
   RDD_CUDA(cudaStreamSynchronize(c.stream));
   const double t_pca = now_s() - t0;
   assemble(c, cfg.precond >= 0);
@@ -203,6 +214,8 @@ void rdd_destroy(rdd_ctx* h) {
   cudaSetDevice(h->c.device);
   cudaStreamSynchronize(h->c.stream);
   cudaStream_t s = h->c.stream;
+  for (auto& e : h->c.ev)
+    if (e) cudaEventDestroy(e);
   {
     const cudaStream_t prev = rdd::alloc_stream();
     rdd::alloc_stream() = s;
@@ -256,6 +269,37 @@ int rdd_run_single(rdd_ctx* h, const rdd_config* cfg, uint64_t seed, rdd_summary
   });
   if (st == RDD_OK && out) *out = h->c.sum;
   return st;
+}
+int rdd_rerun_resident(rdd_ctx* h, rdd_summary* out) {
+  const int st = guarded(h, [&](Ctx& c) {
+    const rdd_config cfg = c.cfg;
+    rdd::run_single(c, cfg, c.seed, true);
+  });
+  if (st == RDD_OK && out) *out = h->c.sum;
+  return st;
+}
+int64_t rdd_launch_count(void) { return rdd::launch_counter(); }
+int rdd_io_bytes(int64_t* h2d, int64_t* d2h) {
+  if (h2d) *h2d = rdd::h2d_counter();
+  if (d2h) *d2h = rdd::d2h_counter();
+  return RDD_OK;
+}
+int rdd_event_record(rdd_ctx* h, int slot) {
+  if (!h || slot < 0 || slot >= 8) return RDD_INVALID_ARGUMENT;
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  if (!c.ev[slot] && cudaEventCreate(&c.ev[slot]) != cudaSuccess) return RDD_CUDA_ERROR;
+  return cudaEventRecord(c.ev[slot], c.stream) == cudaSuccess ? RDD_OK : RDD_CUDA_ERROR;
+}
+int rdd_event_elapsed(rdd_ctx* h, int a, int b, double* ms) {
+  if (!h || a < 0 || a >= 8 || b < 0 || b >= 8 || !ms) return RDD_INVALID_ARGUMENT;
+  Ctx& c = h->c;
+  if (!c.ev[a] || !c.ev[b]) return RDD_INVALID_ARGUMENT;
+  if (cudaEventSynchronize(c.ev[b]) != cudaSuccess) return RDD_CUDA_ERROR;
+  float f = 0.f;
+  if (cudaEventElapsedTime(&f, c.ev[a], c.ev[b]) != cudaSuccess) return RDD_CUDA_ERROR;
+  *ms = f;
+  return RDD_OK;
 }
 int rdd_get_summary(rdd_ctx* h, rdd_summary* out) {
   if (!h || !out) return RDD_INVALID_ARGUMENT;

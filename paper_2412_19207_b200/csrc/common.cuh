@@ -27,7 +27,12 @@ inline void check_cuda(cudaError_t e, const char* what, const char* file, int li
                     std::to_string(line));
 }
 #define RDD_CUDA(x) ::rdd::check_cuda((x), #x, __FILE__, __LINE__)
-#define RDD_LAUNCH_CHECK() ::rdd::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+// every kernel launch of the library goes through this check: it also counts launches
+inline int64_t& launch_counter() {
+  static thread_local int64_t n = 0;
+  return n;
+}
+#define RDD_LAUNCH_CHECK() (++::rdd::launch_counter(), ::rdd::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__))
 
 // Stream that owns temporaries of the current API call: stream-ordered pool allocations
 // (cudaMallocAsync / cudaFreeAsync) make per-call scratch buffers cheap.
@@ -35,6 +40,38 @@ inline cudaStream_t& alloc_stream() {
   static thread_local cudaStream_t s = nullptr;
   return s;
 }
+
+// host<->device bytes moved by the calling thread (e2e accounting)
+inline int64_t& h2d_counter() {
+  static thread_local int64_t n = 0;
+  return n;
+}
+inline int64_t& d2h_counter() {
+  static thread_local int64_t n = 0;
+  return n;
+}
+
+// Pinned (page-locked) host allocator: the host-built inputs are staged here so the H2D
+// copies run at full PCIe/C2C bandwidth.
+template <class T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <class U>
+  PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  template <class U>
+  bool operator==(const PinnedAlloc<U>&) const { return true; }
+  template <class U>
+  bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+template <class T>
+using pinned_vector = std::vector<T, PinnedAlloc<T>>;
 
 // Owning device buffer (pooled, stream-ordered; grows, never shrinks).
 template <class T>
@@ -67,10 +104,15 @@ struct DBuf {
   void upload(const T* h, size_t count, cudaStream_t s) {
     ensure(count);
     if (count) RDD_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    h2d_counter() += static_cast<int64_t>(count * sizeof(T));
   }
-  void upload(const std::vector<T>& h, cudaStream_t s) { upload(h.data(), h.size(), s); }
+  template <class Alloc>
+  void upload(const std::vector<T, Alloc>& h, cudaStream_t s) {
+    upload(h.data(), h.size(), s);
+  }
   void download(T* h, size_t count, cudaStream_t s) const {
     if (count) RDD_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+    d2h_counter() += static_cast<int64_t>(count * sizeof(T));
   }
   void zero(size_t count, cudaStream_t s) {
     ensure(count);

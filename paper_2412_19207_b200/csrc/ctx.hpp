@@ -56,8 +56,8 @@ struct Ctx {
   std::vector<int> counts;
   std::vector<std::vector<double>> axis_lo, axis_hi;  // per axis, per index
   std::vector<int> nbr_ptr, nbr_idx;                  // CSR, ascending, includes self
-  std::vector<double> h_pts;                          // d x N (axis-major)
-  std::vector<double> h_R, h_b;                       // J*m*d (k-major, then axis), J*m
+  pinned_vector<double> h_pts;                        // d x N (axis-major), pinned staging
+  pinned_vector<double> h_R, h_b;                     // J*m*d (k-major, then axis), J*m
 
   // ---- device: inputs
   DBuf<double> pts, dbox;  // dbox: J x 16 (lo[4], hi[4], center[4], half[4])
@@ -143,8 +143,10 @@ struct Ctx {
   std::map<std::string, KernelStat> stats;
   bool timing = false;
   bool verbose = false;
+  size_t cg_graph_kernels = 0;
 
   double* wk(size_t count) { return work.ensure(count); }
+  cudaEvent_t ev[8] = {nullptr};
 };
 
 // timing helper: records device time of a kernel family when ctx.timing is on

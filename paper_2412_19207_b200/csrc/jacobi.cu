@@ -691,6 +691,7 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
       if (K == 2) launch(k_syevj_cluster<2>);
       else if (K == 4) launch(k_syevj_cluster<4>);
       else launch(k_syevj_cluster<8>);
+      ++launch_counter();
     }
     const size_t vsm = static_cast<size_t>(kRows) * (nmax + 1) * sizeof(double);
     RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));

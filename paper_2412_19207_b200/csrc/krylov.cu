@@ -293,16 +293,21 @@ static void cg_solve(Ctx& c, const double* b, double* x, double tol, int max_ite
   c.timing = false;  // no event records inside capture
   {
     cudaGraph_t graph;
+    const int64_t before = launch_counter();
     RDD_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < chunk; ++k) iteration();
     RDD_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    c.cg_graph_kernels = static_cast<size_t>(launch_counter() - before);  // captured, not launched
+    launch_counter() = before;
     RDD_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
     cudaGraphDestroy(graph);
   }
   c.timing = timing;
+  const size_t graph_nodes = c.cg_graph_kernels;
   CgState hs{};
   for (int done = 0;;) {
     RDD_CUDA(cudaGraphLaunch(g.exec, c.stream));
+    launch_counter() += static_cast<int64_t>(graph_nodes);
     done += chunk;
     RDD_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(CgState), cudaMemcpyDeviceToHost, c.stream));
     RDD_CUDA(cudaStreamSynchronize(c.stream));

@@ -53,6 +53,12 @@ def lib():
         L.rdd_evaluate.argtypes = [vp, C.POINTER(C.c_int)]
         L.rdd_run_single.argtypes = [vp, C.POINTER(A.Config), C.c_uint64, C.POINTER(A.Summary)]
         L.rdd_get_summary.argtypes = [vp, C.POINTER(A.Summary)]
+        L.rdd_rerun_resident.argtypes = [vp, C.POINTER(A.Summary)]
+        L.rdd_launch_count.restype = C.c_int64
+        L.rdd_launch_count.argtypes = []
+        L.rdd_io_bytes.argtypes = [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.rdd_event_record.argtypes = [vp, C.c_int]
+        L.rdd_event_elapsed.argtypes = [vp, C.c_int, C.c_int, dp]
         L.rdd_matvec.argtypes = [vp, dp, dp]
         L.rdd_matvec_transpose.argtypes = [vp, dp, dp]
         L.rdd_normal_apply.argtypes = [vp, dp, dp]
@@ -128,6 +134,15 @@ class Solver:
         s = A.Summary()
         self._check(self.L.rdd_run_single(self.h, C.byref(cfg), cfg.seed if seed is None else seed, C.byref(s)))
         return s.as_dict()
+
+    def rerun_resident(self) -> dict:
+        """run_single again on the inputs already resident in HBM."""
+        s = A.Summary()
+        self._check(self.L.rdd_rerun_resident(self.h, C.byref(s)))
+        return s.as_dict()
+
+    def launch_count(self) -> int:
+        return int(self.L.rdd_launch_count())
 
     def summary(self) -> dict:
         s = A.Summary()

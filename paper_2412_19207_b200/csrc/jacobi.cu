@@ -556,6 +556,262 @@ __global__ void __launch_bounds__(kThreads) k_syevj_cluster(const double* __rest
   cluster.sync();  // keep every CTA's shared memory alive until all remote accesses are done
 }
 
+// ============================================================================================
+// Odd-even (Luk–Park) ordering on the packed upper triangle, distributed by whole columns over a
+// K-CTA cluster (K = 1: one CTA). Step t pairs positions (o+2k, o+2k+1), o = t&1, and applies
+// Ĵ = J·Π (rotation + swap), so after n steps every pair has met. Because pairs are adjacent
+// indices, a 2x2 block of the update lives in two adjacent columns owned by one CTA: updates are
+// CTA-local; only the rotation table broadcast and boundary pairs of odd steps touch DSMEM.
+// Column ranges start at even indices, so even-step pairs never straddle two CTAs.
+// ============================================================================================
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict__ Ain, double* __restrict__ ev,
+                                                        const int* __restrict__ nvec,
+                                                        const long long* __restrict__ off,
+                                                        const long long* __restrict__ ev_off, int max_sweeps,
+                                                        Crit crit_in, double floor_rel, double conv_rel,
+                                                        int* __restrict__ sweeps_out, double2* __restrict__ rot,
+                                                        const long long* __restrict__ rot_off, int chunk) {
+  namespace cg = cooperative_groups;
+  extern __shared__ double smem[];
+  int rank = 0;
+  if constexpr (K > 1) rank = static_cast<int>(cg::this_cluster().block_rank());
+  const int b = blockIdx.x / K;
+  const int n = nvec[b];
+  const int ne = n + (n & 1);           // even order (pad index ne-1 when n is odd: zero row/col)
+  const int np = ne / 2;
+  double* cs = smem + chunk;            // [np] c, [np] s: rotation of pair slot k this step
+  double* sn = cs + np;
+  int* lcol = reinterpret_cast<int*>(sn + np);  // local start of column j
+  unsigned char* own = reinterpret_cast<unsigned char*>(lcol + ne);
+  __shared__ int active;
+  __shared__ int cbeg, cend;            // my column range [cbeg, cend)
+  double* base[K];
+  if constexpr (K > 1) {
+#pragma unroll
+    for (int r = 0; r < K; ++r) base[r] = cg::this_cluster().map_shared_rank(smem, r);
+  } else {
+    base[0] = smem;
+  }
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int nthr = blockDim.x * blockDim.y;
+  if (tid == 0) {  // even-aligned whole-column ranges of ~chunk elements
+    int cur = 0, start = 0;
+    cbeg = (rank == 0) ? 0 : ne;
+    cend = ne;
+    for (int j = 0; j < ne; ++j) {
+      const int e = j * (j + 1) / 2;
+      if ((j & 1) == 0 && cur + 1 < K && e + 2 * j + 3 - start > chunk) {  // next pair would overflow
+        ++cur;
+        start = e;
+        if (cur == rank) cbeg = j;
+        if (cur == rank + 1) cend = j;
+      }
+      own[j] = static_cast<unsigned char>(cur);
+      lcol[j] = e - start;
+    }
+  }
+  __syncthreads();
+  auto at = [&](int i, int j) -> double& {  // i <= j
+    return base[own[j]][lcol[j] + i];
+  };
+  const double* A = Ain + off[b];
+  for (int j = cbeg + threadIdx.y; j < cend; j += blockDim.y)
+    for (int i = threadIdx.x; i <= j; i += blockDim.x)
+      smem[lcol[j] + i] = (i < n && j < n) ? A[i + static_cast<long long>(j) * n] : 0.0;
+  if constexpr (K > 1) cg::this_cluster().sync(); else __syncthreads();
+  double dmax = 0.0;
+  for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(at(i, i)));
+  Crit crit = crit_in;
+  crit.tiny = 1e-32 * dmax;
+  crit.floor_lam = fmax(floor_rel * dmax, crit_in.floor_lam);
+  crit.conv_lam = fmax(conv_rel * dmax, crit_in.conv_lam);
+  if (crit.absolute) crit.tol = crit_in.tol * dmax;
+  double2* R = rot + rot_off[b];
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) active = 0;
+    int local_active = 0;
+    for (int t = 0; t < ne; ++t) {
+      const int o = t & 1;
+      const int npair = o ? np - 1 : np;
+      // phase A: the owner of column q = p+1 decides pair k and broadcasts (c, s)
+      for (int k = tid; k < npair; k += nthr) {
+        const int p = o + 2 * k, q = p + 1;
+        if (own[q] != rank) continue;
+        const double app = at(p, p), aqq = at(q, q), apq = at(p, q);
+        double c = 1.0, sv = 0.0;
+        const int d = rot_decision(crit, app, aqq, apq);
+        if (d) {
+          schur2(app, aqq, apq, c, sv);
+          if (d == 2) local_active = 1;
+        }
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          double* tab = base[r] + chunk;
+          tab[k] = c;
+          tab[np + k] = sv;
+        }
+        R[(static_cast<long long>(sweep) * ne + t) * np + k] = make_double2(c, sv);
+      }
+      if constexpr (K > 1) cg::this_cluster().sync(); else __syncthreads();
+      // phase B: blocks (U <= W) whose column unit W starts in my range
+      const int nu = o ? np + 1 : np;  // odd steps: {0}, (1,2), ..., (ne-3, ne-2), {ne-1}
+      for (int W = threadIdx.y; W < nu; W += blockDim.y) {
+        int w0, ws, kw;
+        if (!o) {
+          w0 = 2 * W;
+          ws = 2;
+          kw = W;
+        } else if (W == 0) {
+          w0 = 0;
+          ws = 1;
+          kw = -1;
+        } else if (W == nu - 1) {
+          w0 = ne - 1;
+          ws = 1;
+          kw = -1;
+        } else {
+          w0 = 2 * W - 1;
+          ws = 2;
+          kw = W - 1;
+        }
+        if (own[w0] != rank) continue;
+        const double cw = kw >= 0 ? cs[kw] : 1.0, sw = kw >= 0 ? sn[kw] : 0.0;
+        for (int U = threadIdx.x; U <= W; U += blockDim.x) {
+          int u0, us, ku;
+          if (!o) {
+            u0 = 2 * U;
+            us = 2;
+            ku = U;
+          } else if (U == 0) {
+            u0 = 0;
+            us = 1;
+            ku = -1;
+          } else if (U == nu - 1) {
+            u0 = ne - 1;
+            us = 1;
+            ku = -1;
+          } else {
+            u0 = 2 * U - 1;
+            us = 2;
+            ku = U - 1;
+          }
+          const double cu = ku >= 0 ? cs[ku] : 1.0, su = ku >= 0 ? sn[ku] : 0.0;
+          if (U == W) {
+            if (us == 1) continue;
+            double& app = at(u0, u0);
+            double& apq = at(u0, u0 + 1);
+            double& aqq = at(u0 + 1, u0 + 1);
+            if (su == 0.0) {  // pure swap
+              const double t0 = app;
+              app = aqq;
+              aqq = t0;
+            } else {
+              const double tt = su / cu, vpq = apq, vpp = app, vqq = aqq;
+              app = vqq + tt * vpq;  // swapped diagonal of JᵀAJ
+              aqq = vpp - tt * vpq;
+              apq = 0.0;
+            }
+            continue;
+          }
+          // rows u0.. (< columns w0..): all four entries are in the upper triangle
+          double a00 = at(u0, w0);
+          double a10 = us == 2 ? at(u0 + 1, w0) : 0.0;
+          double a01 = ws == 2 ? at(u0, w0 + 1) : 0.0;
+          double a11 = (us == 2 && ws == 2) ? at(u0 + 1, w0 + 1) : 0.0;
+          // left Ĵ_Uᵀ: rows (u0, u0+1) <- (s a_u0 + c a_u1, c a_u0 - s a_u1)
+          if (us == 2) {
+            const double r00 = su * a00 + cu * a10, r10 = cu * a00 - su * a10;
+            const double r01 = su * a01 + cu * a11, r11 = cu * a01 - su * a11;
+            a00 = r00;
+            a10 = r10;
+            a01 = r01;
+            a11 = r11;
+          }
+          if (ws == 2) {  // right Ĵ_W: cols (w0, w0+1) <- (s a_w0 + c a_w1, c a_w0 - s a_w1)
+            const double r00 = sw * a00 + cw * a01, r01 = cw * a00 - sw * a01;
+            const double r10 = sw * a10 + cw * a11, r11 = cw * a10 - sw * a11;
+            a00 = r00;
+            a01 = r01;
+            a10 = r10;
+            a11 = r11;
+          }
+          at(u0, w0) = a00;
+          if (us == 2) at(u0 + 1, w0) = a10;
+          if (ws == 2) at(u0, w0 + 1) = a01;
+          if (us == 2 && ws == 2) at(u0 + 1, w0 + 1) = a11;
+        }
+      }
+      if constexpr (K > 1) cg::this_cluster().sync(); else __syncthreads();
+    }
+    if constexpr (K > 1) {
+      if (local_active) atomicOr(cg::this_cluster().map_shared_rank(&active, 0), 1);
+      cg::this_cluster().sync();
+      const int any = *cg::this_cluster().map_shared_rank(&active, 0);
+      cg::this_cluster().sync();
+      if (!any) {
+        ++sweep;  // the last sweep still swapped: it stays in the log
+        break;
+      }
+    } else {
+      if (local_active) atomicOr(&active, 1);
+      __syncthreads();
+      const int any = active;
+      __syncthreads();
+      if (!any) {
+        ++sweep;
+        break;
+      }
+    }
+  }
+  if (rank == 0) {
+    for (int i = tid; i < ne; i += nthr) ev[ev_off[b] + i] = at(i, i);
+    if (tid == 0) sweeps_out[b] = sweep;
+  }
+  if constexpr (K > 1) cg::this_cluster().sync();  // keep shared memory alive for remote readers
+}
+
+// V = Π Ĵ_t: each thread owns one row of V (shared memory, odd stride: conflict-free) and replays
+// the whole log without any barrier; identity rotations (s = 0) still swap.
+__global__ void __launch_bounds__(64) k_replay_oe(double* __restrict__ Vout, const int* __restrict__ nvec,
+                                                  const long long* __restrict__ off, const double2* __restrict__ rot,
+                                                  const long long* __restrict__ rot_off,
+                                                  const int* __restrict__ sweeps, double* __restrict__ Vpad,
+                                                  const long long* __restrict__ poff) {
+  extern __shared__ double vs[];
+  const int b = blockIdx.y;
+  const int n = nvec[b];
+  const int ne = n + (n & 1), np = ne / 2;
+  const int ld = ne | 1;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  double* v = vs + threadIdx.x * ld;
+  for (int c = 0; c < ne; ++c) v[c] = (row == c) ? 1.0 : 0.0;
+  const double2* R = rot + rot_off[b];
+  const int total = sweeps[b] * ne;
+  if (row < ne) {
+    for (int t = 0; t < total; ++t) {
+      const int o = t & 1;
+      const int npair = o ? np - 1 : np;
+      const double2* Rt = R + static_cast<long long>(t) * np;
+      for (int k = 0; k < npair; ++k) {
+        const double2 csn = Rt[k];
+        const int p = o + 2 * k;
+        const double a = v[p], bq = v[p + 1];
+        v[p] = csn.y * a + csn.x * bq;
+        v[p + 1] = csn.x * a - csn.y * bq;
+      }
+    }
+  }
+  __syncwarp();
+  if (row < ne) {  // write row `row` of the (padded) eigenvector matrix
+    double* out = Vpad + poff[b];
+    for (int c = 0; c < ne; ++c) out[row + static_cast<long long>(c) * ne] = v[c];
+  }
+  (void)Vout;
+  (void)off;
+}
+
 // pad to even order (zero row/column; the pad direction stays decoupled: every entry touching
 // it is an exact zero) / compact back, dropping the pad eigenpair
 __global__ void k_pad_copy(const double* __restrict__ A, const long long* __restrict__ off, const int* __restrict__ n,
@@ -597,23 +853,19 @@ __global__ void k_compact(const double* __restrict__ Vp, const double* __restric
 
 }  // namespace
 
-// cluster size that holds the packed triangle of order n in distributed shared memory (0: none)
-static size_t cluster_chunk(int n, int K) {
-  const size_t tri = static_cast<size_t>(n) * (n + 1) / 2;
-  return (tri + K - 1) / K + n;  // whole columns per CTA: one column of slack
+// shared memory of k_jacobi_oe<K> for even order ne
+static size_t oe_chunk(int ne, int K) {
+  const size_t tri = static_cast<size_t>(ne) * (ne + 1) / 2;
+  return K == 1 ? tri : (tri + K - 1) / K + 2 * static_cast<size_t>(ne) + 4;
 }
-static size_t cluster_smem(int n, int K) {
-  return cluster_chunk(n, K) * sizeof(double) + static_cast<size_t>((n + 1) / 2) * (2 * sizeof(double) + 2 * sizeof(int)) +
-         static_cast<size_t>(n) * (sizeof(int) + 1) + 64;
+static size_t oe_smem(int ne, int K) {
+  return oe_chunk(ne, K) * sizeof(double) + static_cast<size_t>(ne / 2) * 2 * sizeof(double) +
+         static_cast<size_t>(ne) * (sizeof(int) + 1) + 64;
 }
-static int cluster_k(int n) {
-  for (int K : {2, 4, 8})
-    if (cluster_smem(n, K) <= kCtaSmem) return K;
+static int oe_k(int ne) {
+  for (int K : {1, 2, 4, 8})
+    if (oe_smem(ne, K) <= kCtaSmem) return K;
   return 0;
-}
-static size_t smem_path_bytes(int n) {
-  return static_cast<size_t>(n) * (n + 1) / 2 * sizeof(double) +
-         static_cast<size_t>((n + 1) / 2) * (2 * sizeof(double) + 2 * sizeof(int)) + static_cast<size_t>(n) * sizeof(int);
 }
 
 // A: batch of symmetric n_b x n_b column-major matrices at offA[b] (the upper triangle is read);
@@ -637,114 +889,97 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     offE[b] = e;
     e += n[b];
   }
-  DBuf<int> dn, dsw;
-  DBuf<long long> doff, doffE, droff;
+  // padded (even-order) work layout shared by all paths
+  std::vector<int> npad(B);
+  std::vector<long long> woff(B), eoffp(B), roff(B);
+  long long wt = 0, et = 0, rt = 0;
+  for (int b = 0; b < B; ++b) {
+    npad[b] = n[b] + (n[b] & 1);
+    woff[b] = wt;
+    wt += static_cast<long long>(npad[b]) * npad[b];
+    eoffp[b] = et;
+    et += npad[b];
+    roff[b] = rt;
+    rt += static_cast<long long>(max_sweeps) * npad[b] * std::max(1, npad[b] / 2);
+  }
+  DBuf<int> dn, dsw, dnp;
+  DBuf<long long> doff, doffE, droff, dwoff, deoffp;
   DBuf<double2> rot;
+  DBuf<double> Vp, evp;
   dn.upload(n, c.stream);
   doff.upload(offA, c.stream);
   doffE.upload(offE, c.stream);
+  dnp.upload(npad, c.stream);
+  dwoff.upload(woff, c.stream);
+  deoffp.upload(eoffp, c.stream);
+  droff.upload(roff, c.stream);
   dsw.ensure(B);
+  Vp.ensure(wt);
+  evp.ensure(et);
+  rot.ensure(std::max<long long>(1, rt));
+  const int ne = nmax + (nmax & 1);
+  const int K = oe_k(ne);
   int swmax = 0;
-  const bool smem_path = smem_path_bytes(nmax) <= kCtaSmem;
-  const int K = smem_path ? 1 : cluster_k(nmax);
-  if (smem_path || K > 0) {
-    std::vector<long long> roff(B);
-    long long rtot = 0;
-    for (int b = 0; b < B; ++b) {
-      roff[b] = rtot;
-      const int nn = n[b] + (n[b] & 1);
-      rtot += static_cast<long long>(max_sweeps) * std::max(1, nn - 1) * std::max(1, nn / 2);
-    }
-    rot.ensure(std::max<long long>(1, rtot));
-    droff.upload(roff, c.stream);
-    if (smem_path) {
-      // ---- round-robin ordering, packed triangle in shared memory
-      const size_t smem = smem_path_bytes(nmax);
-      const int tri_max = nmax * (nmax + 1) / 2;
-      RDD_CUDA(cudaFuncSetAttribute(k_syevj, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      k_syevj<<<B, dim3(32, kThreads / 32), smem, c.stream>>>(A, evals, dn.p, doff.p, doffE.p, max_sweeps, crit,
-                                                             o.floor_rel, o.conv_rel, dsw.p, rot.p, droff.p, tri_max);
-      RDD_LAUNCH_CHECK();
-    } else {
-      // ---- round-robin ordering, packed triangle across a thread-block cluster (DSMEM)
-      const int chunk = static_cast<int>(cluster_chunk(nmax, K));
-      const size_t smem = cluster_smem(nmax, K);
-      cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3(B * K);
-      lc.blockDim = dim3(32, kThreads / 32);
-      lc.dynamicSmemBytes = smem;
-      lc.stream = c.stream;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = K;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      lc.attrs = at;
-      lc.numAttrs = 1;
-      auto launch = [&](auto kern) {
-        RDD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        RDD_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<const double*>(A), evals, static_cast<const int*>(dn.p),
-                                    static_cast<const long long*>(doff.p), static_cast<const long long*>(doffE.p),
-                                    max_sweeps, crit, o.floor_rel, o.conv_rel, dsw.p, rot.p,
-                                    static_cast<const long long*>(droff.p), chunk));
-      };
-      if (K == 2) launch(k_syevj_cluster<2>);
-      else if (K == 4) launch(k_syevj_cluster<4>);
-      else launch(k_syevj_cluster<8>);
+  if (K > 0) {
+    // ---- odd-even ordering, packed triangle on chip (one CTA or a K-CTA cluster)
+    const int chunk = static_cast<int>(oe_chunk(ne, K));
+    const size_t smem = oe_smem(ne, K);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(B * K);
+    lc.blockDim = dim3(32, kThreads / 32);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = c.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = K > 1 ? 1 : 0;
+    auto launch = [&](auto kern) {
+      RDD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      RDD_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<const double*>(A), evp.p, static_cast<const int*>(dn.p),
+                                  static_cast<const long long*>(doff.p), static_cast<const long long*>(deoffp.p),
+                                  max_sweeps, crit, o.floor_rel, o.conv_rel, dsw.p, rot.p,
+                                  static_cast<const long long*>(droff.p), chunk));
       ++launch_counter();
-    }
-    const size_t vsm = static_cast<size_t>(kRows) * (nmax + 1) * sizeof(double);
-    RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
-    k_apply_rotations<<<dim3(ceil_div(nmax, kRows), B), 256, vsm, c.stream>>>(V, dn.p, doff.p, rot.p, droff.p, dsw.p);
+    };
+    if (K == 1) launch(k_jacobi_oe<1>);
+    else if (K == 2) launch(k_jacobi_oe<2>);
+    else if (K == 4) launch(k_jacobi_oe<4>);
+    else launch(k_jacobi_oe<8>);
+    const int rows = 64;
+    const size_t vsm = static_cast<size_t>(rows) * (ne | 1) * sizeof(double);
+    RDD_CUDA(cudaFuncSetAttribute(k_replay_oe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
+    k_replay_oe<<<dim3(ceil_div(ne, rows), B), rows, vsm, c.stream>>>(V, dn.p, doff.p, rot.p, droff.p, dsw.p, Vp.p,
+                                                                      dwoff.p);
     RDD_LAUNCH_CHECK();
   } else {
-    // ---- odd-even ordering, full storage in global memory (padded to even order)
-    std::vector<int> npad(B);
-    std::vector<long long> woff(B), eoffp(B), roff(B);
-    long long wt = 0, et = 0, rt = 0;
-    for (int b = 0; b < B; ++b) {
-      npad[b] = n[b] + (n[b] & 1);
-      woff[b] = wt;
-      wt += static_cast<long long>(npad[b]) * npad[b];
-      eoffp[b] = et;
-      et += npad[b];
-      roff[b] = rt;
-      rt += static_cast<long long>(max_sweeps) * npad[b] * (npad[b] / 2);
-    }
-    DBuf<double> Wk, Vp, evp;
-    DBuf<int> dnp;
-    DBuf<long long> dwoff, deoffp;
+    // ---- odd-even ordering, full storage in global memory (very large orders)
+    DBuf<double> Wk;
     Wk.ensure(wt);
-    Vp.ensure(wt);
-    evp.ensure(et);
-    rot.ensure(std::max<long long>(1, rt));
-    dnp.upload(npad, c.stream);
-    dwoff.upload(woff, c.stream);
-    deoffp.upload(eoffp, c.stream);
-    droff.upload(roff, c.stream);
     k_pad_copy<<<B, 256, 0, c.stream>>>(A, doff.p, dn.p, Wk.p, dwoff.p, dnp.p);
     RDD_LAUNCH_CHECK();
-    const int nmp = nmax + (nmax & 1);
-    const size_t smem = static_cast<size_t>(nmp + 2) * sizeof(double);
+    const size_t smem = static_cast<size_t>(ne + 2) * sizeof(double);
     k_syevj_oe<<<B, 1024, smem, c.stream>>>(Wk.p, dnp.p, dwoff.p, evp.p, deoffp.p, max_sweeps, dsw.p, rot.p, droff.p,
                                              crit, o.floor_rel, o.conv_rel);
     RDD_LAUNCH_CHECK();
-    const size_t vsm = static_cast<size_t>(kRows) * (nmp + 1) * sizeof(double);
+    const size_t vsm = static_cast<size_t>(kRows) * (ne + 1) * sizeof(double);
     RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations_oe, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(vsm)));
-    k_apply_rotations_oe<<<dim3(ceil_div(nmp, kRows), B), 256, vsm, c.stream>>>(Vp.p, dnp.p, dwoff.p, rot.p, droff.p,
+    k_apply_rotations_oe<<<dim3(ceil_div(ne, kRows), B), 256, vsm, c.stream>>>(Vp.p, dnp.p, dwoff.p, rot.p, droff.p,
                                                                                  dsw.p, dn.p);
     RDD_LAUNCH_CHECK();
-    k_compact<<<B, 256, 0, c.stream>>>(Vp.p, evp.p, dwoff.p, deoffp.p, dn.p, dnp.p, V, doff.p, evals, doffE.p);
-    RDD_LAUNCH_CHECK();
   }
+  k_compact<<<B, 256, 0, c.stream>>>(Vp.p, evp.p, dwoff.p, deoffp.p, dn.p, dnp.p, V, doff.p, evals, doffE.p);
+  RDD_LAUNCH_CHECK();
   if (c.verbose) {
     std::vector<int> sw(B);
     dsw.download(sw.data(), B, c.stream);
     RDD_CUDA(cudaStreamSynchronize(c.stream));
     for (int v : sw) swmax = std::max(swmax, v);
     std::fprintf(stderr, "[syevj] B=%d nmax=%d path=%s max_sweeps_used=%d\n", B, nmax,
-                 smem_path ? "smem" : (K ? "cluster" : "odd-even"), swmax);
+                 K == 1 ? "oe-smem" : (K ? "oe-cluster" : "oe-global"), swmax);
   }
   RDD_CUDA(cudaStreamSynchronize(c.stream));
 }

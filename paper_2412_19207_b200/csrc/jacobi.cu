@@ -772,44 +772,52 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
   if constexpr (K > 1) cg::this_cluster().sync();  // keep shared memory alive for remote readers
 }
 
-// V = Π Ĵ_t: each thread owns one row of V (shared memory, odd stride: conflict-free) and replays
-// the whole log without any barrier; identity rotations (s = 0) still swap.
-__global__ void __launch_bounds__(64) k_replay_oe(double* __restrict__ Vout, const int* __restrict__ nvec,
-                                                  const long long* __restrict__ off, const double2* __restrict__ rot,
-                                                  const long long* __restrict__ rot_off,
-                                                  const int* __restrict__ sweeps, double* __restrict__ Vpad,
-                                                  const long long* __restrict__ poff) {
+// V = Π Ĵ_t: each thread owns one row of V (shared memory, odd stride: conflict-free). The
+// rotation log is streamed through shared memory in chunks of kLogRounds steps (cooperative,
+// coalesced loads); the replay itself needs no barrier. Identity rotations (s = 0) still swap.
+constexpr int kReplayRows = 64;
+constexpr int kLogRounds = 16;
+__global__ void __launch_bounds__(kReplayRows) k_replay_oe(const int* __restrict__ nvec,
+                                                           const double2* __restrict__ rot,
+                                                           const long long* __restrict__ rot_off,
+                                                           const int* __restrict__ sweeps, double* __restrict__ Vpad,
+                                                           const long long* __restrict__ poff) {
   extern __shared__ double vs[];
   const int b = blockIdx.y;
   const int n = nvec[b];
   const int ne = n + (n & 1), np = ne / 2;
   const int ld = ne | 1;
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  double2* logc = reinterpret_cast<double2*>(vs + kReplayRows * ld);  // kLogRounds x np
   double* v = vs + threadIdx.x * ld;
   for (int c = 0; c < ne; ++c) v[c] = (row == c) ? 1.0 : 0.0;
   const double2* R = rot + rot_off[b];
   const int total = sweeps[b] * ne;
-  if (row < ne) {
-    for (int t = 0; t < total; ++t) {
-      const int o = t & 1;
-      const int npair = o ? np - 1 : np;
-      const double2* Rt = R + static_cast<long long>(t) * np;
-      for (int k = 0; k < npair; ++k) {
-        const double2 csn = Rt[k];
-        const int p = o + 2 * k;
-        const double a = v[p], bq = v[p + 1];
-        v[p] = csn.y * a + csn.x * bq;
-        v[p + 1] = csn.x * a - csn.y * bq;
+  for (int t0 = 0; t0 < total; t0 += kLogRounds) {
+    const int nr = min(kLogRounds, total - t0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * np; e += blockDim.x) logc[e] = R[static_cast<long long>(t0) * np + e];
+    __syncthreads();
+    if (row < ne) {
+      for (int tt = 0; tt < nr; ++tt) {
+        const int o = (t0 + tt) & 1;
+        const int npair = o ? np - 1 : np;
+        const double2* Rt = logc + tt * np;
+#pragma unroll 4
+        for (int k = 0; k < npair; ++k) {
+          const double2 csn = Rt[k];
+          const int p = o + 2 * k;
+          const double a = v[p], bq = v[p + 1];
+          v[p] = csn.y * a + csn.x * bq;
+          v[p + 1] = csn.x * a - csn.y * bq;
+        }
       }
     }
   }
-  __syncwarp();
-  if (row < ne) {  // write row `row` of the (padded) eigenvector matrix
+  if (row < ne) {  // row `row` of the (padded) eigenvector matrix
     double* out = Vpad + poff[b];
     for (int c = 0; c < ne; ++c) out[row + static_cast<long long>(c) * ne] = v[c];
   }
-  (void)Vout;
-  (void)off;
 }
 
 // pad to even order (zero row/column; the pad direction stays decoupled: every entry touching
@@ -948,11 +956,11 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     else if (K == 2) launch(k_jacobi_oe<2>);
     else if (K == 4) launch(k_jacobi_oe<4>);
     else launch(k_jacobi_oe<8>);
-    const int rows = 64;
-    const size_t vsm = static_cast<size_t>(rows) * (ne | 1) * sizeof(double);
+    const size_t vsm = static_cast<size_t>(kReplayRows) * (ne | 1) * sizeof(double) +
+                       static_cast<size_t>(kLogRounds) * (ne / 2) * sizeof(double2);
     RDD_CUDA(cudaFuncSetAttribute(k_replay_oe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
-    k_replay_oe<<<dim3(ceil_div(ne, rows), B), rows, vsm, c.stream>>>(V, dn.p, doff.p, rot.p, droff.p, dsw.p, Vp.p,
-                                                                      dwoff.p);
+    k_replay_oe<<<dim3(ceil_div(ne, kReplayRows), B), kReplayRows, vsm, c.stream>>>(dn.p, rot.p, droff.p, dsw.p, Vp.p,
+                                                                                    dwoff.p);
     RDD_LAUNCH_CHECK();
   } else {
     // ---- odd-even ordering, full storage in global memory (very large orders)

@@ -772,25 +772,26 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
   if constexpr (K > 1) cg::this_cluster().sync();  // keep shared memory alive for remote readers
 }
 
-// V = Π Ĵ_t: each thread owns one row of V (shared memory, odd stride: conflict-free). The
-// rotation log is streamed through shared memory in chunks of kLogRounds steps (cooperative,
-// coalesced loads); the replay itself needs no barrier. Identity rotations (s = 0) still swap.
-constexpr int kReplayRows = 64;
+// V = Π Ĵ_t: each warp owns one row of V in shared memory; its lanes split the (disjoint) pairs
+// of a step and synchronise with __syncwarp only. The rotation log is streamed through shared
+// memory in chunks of kLogRounds steps. Identity rotations (s = 0) still swap.
+constexpr int kReplayWarps = 16;
 constexpr int kLogRounds = 16;
-__global__ void __launch_bounds__(kReplayRows) k_replay_oe(const int* __restrict__ nvec,
-                                                           const double2* __restrict__ rot,
-                                                           const long long* __restrict__ rot_off,
-                                                           const int* __restrict__ sweeps, double* __restrict__ Vpad,
-                                                           const long long* __restrict__ poff) {
+__global__ void __launch_bounds__(kReplayWarps * 32) k_replay_oe(const int* __restrict__ nvec,
+                                                                 const double2* __restrict__ rot,
+                                                                 const long long* __restrict__ rot_off,
+                                                                 const int* __restrict__ sweeps,
+                                                                 double* __restrict__ Vpad,
+                                                                 const long long* __restrict__ poff) {
   extern __shared__ double vs[];
   const int b = blockIdx.y;
   const int n = nvec[b];
   const int ne = n + (n & 1), np = ne / 2;
-  const int ld = ne | 1;
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  double2* logc = reinterpret_cast<double2*>(vs + kReplayRows * ld);  // kLogRounds x np
-  double* v = vs + threadIdx.x * ld;
-  for (int c = 0; c < ne; ++c) v[c] = (row == c) ? 1.0 : 0.0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * kReplayWarps + warp;
+  double2* logc = reinterpret_cast<double2*>(vs + kReplayWarps * ne);  // kLogRounds x np
+  double* v = vs + warp * ne;
+  for (int c = lane; c < ne; c += 32) v[c] = (row == c) ? 1.0 : 0.0;
   const double2* R = rot + rot_off[b];
   const int total = sweeps[b] * ne;
   for (int t0 = 0; t0 < total; t0 += kLogRounds) {
@@ -803,20 +804,20 @@ __global__ void __launch_bounds__(kReplayRows) k_replay_oe(const int* __restrict
         const int o = (t0 + tt) & 1;
         const int npair = o ? np - 1 : np;
         const double2* Rt = logc + tt * np;
-#pragma unroll 4
-        for (int k = 0; k < npair; ++k) {
+        for (int k = lane; k < npair; k += 32) {
           const double2 csn = Rt[k];
           const int p = o + 2 * k;
           const double a = v[p], bq = v[p + 1];
           v[p] = csn.y * a + csn.x * bq;
           v[p + 1] = csn.x * a - csn.y * bq;
         }
+        __syncwarp();
       }
     }
   }
   if (row < ne) {  // row `row` of the (padded) eigenvector matrix
     double* out = Vpad + poff[b];
-    for (int c = 0; c < ne; ++c) out[row + static_cast<long long>(c) * ne] = v[c];
+    for (int c = lane; c < ne; c += 32) out[row + static_cast<long long>(c) * ne] = v[c];
   }
 }
 
@@ -956,11 +957,11 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     else if (K == 2) launch(k_jacobi_oe<2>);
     else if (K == 4) launch(k_jacobi_oe<4>);
     else launch(k_jacobi_oe<8>);
-    const size_t vsm = static_cast<size_t>(kReplayRows) * (ne | 1) * sizeof(double) +
+    const size_t vsm = static_cast<size_t>(kReplayWarps) * ne * sizeof(double) +
                        static_cast<size_t>(kLogRounds) * (ne / 2) * sizeof(double2);
     RDD_CUDA(cudaFuncSetAttribute(k_replay_oe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
-    k_replay_oe<<<dim3(ceil_div(ne, kReplayRows), B), kReplayRows, vsm, c.stream>>>(dn.p, rot.p, droff.p, dsw.p, Vp.p,
-                                                                                    dwoff.p);
+    k_replay_oe<<<dim3(ceil_div(ne, kReplayWarps), B), kReplayWarps * 32, vsm, c.stream>>>(dn.p, rot.p, droff.p, dsw.p,
+                                                                                           Vp.p, dwoff.p);
     RDD_LAUNCH_CHECK();
   } else {
     // ---- odd-even ordering, full storage in global memory (very large orders)

@@ -30,7 +30,7 @@ for name in names:
                 worst = max(worst, np.linalg.norm(Vd @ Vd.T - Vo @ Vo.T, 2))
                 sd, so = dev.getd("sigma", j), orc.getd("sigma", j)
                 thr = cfg.tau * so[0] if cfg.tau_mode == A.TAU_RELATIVE else cfg.tau
-                big = so > max(1e-8 * so[0], 1e-2 * thr)
+                big = so > max(1e-8 * so[0], 0.2 * thr)
                 sw = max(sw, np.max(np.abs(sd[big] - so[big]) / so[big]))
             print(f" projector max {worst:.2e}  sigma rel max {sw:.2e}")
         eq = cfg.precond >= 0

@@ -130,10 +130,13 @@ def test_normal_blocks_and_schwarz(dev, orc, name):
     assert np.array_equal(dev.geti("local_rank"), orc.geti("local_rank")), name
     rng = np.random.default_rng(7)
     p = int(orc.geti("p")[0])
+    # Cholesky inverse (device) vs eigen pseudo-inverse (oracle, as the reference): both are
+    # accurate to ~eps·cond(A_i), the reported local condition (schwarz.hpp:144)
+    tol = max(1e-8, 1e-14 * float(orc.getd("local_cond").max()))
     for tr in (False, True):
         v = rng.standard_normal(p)
         zo, zd = orc.precond_apply(v, tr), dev.precond_apply(v, tr)
-        assert np.linalg.norm(zd - zo) <= 1e-6 * np.linalg.norm(zo), (name, tr)
+        assert np.linalg.norm(zd - zo) <= tol * np.linalg.norm(zo), (name, tr, tol)
 
 
 @pytest.mark.parametrize("name", list(CASES))

@@ -235,7 +235,8 @@ def run_device(args, cfg, world, rank, local, dist):
 
     # roofline: the normal operator (two passes over H) timed back-to-back with CUDA events on
     # the library stream, same resident system
-    op_ms, op_bytes = s.bench_operator(A.OPERATOR_TWO_PASS, reps=30)
+    op_form = cfg.op_form if cfg.op_form in (A.OPERATOR_TWO_PASS, A.OPERATOR_FUSED) else A.OPERATOR_TWO_PASS
+    op_ms, op_bytes = s.bench_operator(op_form, reps=30)
     peak, peak_kind = peaks()
     achieved = op_bytes / (op_ms / 1e3) / 1e9
     traffic = None
@@ -270,7 +271,7 @@ def run_device(args, cfg, world, rank, local, dist):
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "normal operator Hᵀ(H·w): k_matvec + k_matvec_t",
+                         "kernel": ("normal operator Hᵀ(H·w), single pass: k_fused_normal + k_fused_reduce" if op_form == A.OPERATOR_FUSED else "normal operator Hᵀ(H·w): k_matvec + k_matvec_t"),
                          "bytes_per_call": op_bytes, "ms_per_call": op_ms},
             "clocks": clk,
         }

@@ -134,6 +134,13 @@ struct Ctx {
   std::vector<int> iters, conv, brk;
   DBuf<double> W;                     // p x C (unscaled)
   DBuf<double> ytmp;                  // N
+  // fused single-pass normal operator plan
+  DBuf<int> f_tile_blk, f_bptr;
+  DBuf<long long> f_tile_poff, f_bparts;
+  DBuf<double> f_part;
+  int f_ntiles = 0;
+  long long f_part_size = 0;
+  bool fused_ready = false;
 
   // ---- evaluation
   std::vector<double> approx, exact;  // M x C (host copies)
@@ -196,6 +203,8 @@ void matvec_t_dev(Ctx& c, const double* r, double* out);
 void build_normal_blocks(Ctx& c);
 void normal_apply_dev(Ctx& c, const double* w, double* out);
 void normal_operator(Ctx& c, const double* w, double* out);  // runner.hpp:232-234
+bool build_fused_plan(Ctx& c);
+void fused_normal_apply_dev(Ctx& c, const double* w, double* out);
 // schwarz.cu (K8/K11)
 void build_schwarz(Ctx& c, int kind);
 void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose);

@@ -212,6 +212,8 @@ struct Vecs {
 void normal_operator(Ctx& c, const double* w, double* out) {
   if (c.cfg.op_form == RDD_OPERATOR_NORMAL && c.NB.p) {
     normal_apply_dev(c, w, out);
+  } else if (c.cfg.op_form == RDD_OPERATOR_FUSED && c.fused_ready) {
+    fused_normal_apply_dev(c, w, out);
   } else {
     matvec_dev(c, w, c.ytmp.ensure(c.N));
     matvec_t_dev(c, c.ytmp.p, out);

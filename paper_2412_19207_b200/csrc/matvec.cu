@@ -5,6 +5,8 @@
 // the per-row sum visits blocks in ascending j like the reference). Hᵀ·r (assembly.hpp:123-133)
 // is one warp per column: a contiguous column of a column-major block against r gathered through
 // rows_j. Both are HBM-bound streams over H (8·nnz bytes each).
+#include <algorithm>
+
 #include "ctx.hpp"
 
 namespace rdd {
@@ -98,6 +100,223 @@ void matvec_t_dev(Ctx& c, const double* r, double* out) {
   ScopedKernelTimer tk(c, "matvec_t");
   k_matvec_t<<<ceil_div(static_cast<long long>(c.p) * 32, 256), 256, 0, c.stream>>>(
       c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p, c.downer.p, c.p, r, out);
+  RDD_LAUNCH_CHECK();
+}
+
+}  // namespace rdd
+
+// ============================================================================================
+// Fused single-pass normal operator out = Hᵀ(H·w) (runner.hpp:232-234 computes it as two passes,
+// assembly.hpp:110-133). Global rows are cut into tiles of kFT consecutive points; a CTA gathers
+// the rows of every covering block for its tile (each H element belongs to exactly one tile, so
+// HBM reads H once), forms y = H·w for the tile in shared memory in the reference's per-row order
+// (ascending covering block), then re-reads the same (now L2-resident) rows to accumulate
+// Hᵀy per (tile, block) into a partial buffer. A second kernel sums the partials of each block in
+// tile order: deterministic, no atomics.
+// ============================================================================================
+namespace rdd {
+namespace {
+
+constexpr int kFT = 128;     // points per tile
+constexpr int kFSlots = 32;  // distinct blocks per tile (plan falls back to two passes beyond)
+
+struct FusedArgs {
+  const double* H;
+  const long long* H_off;
+  const int* row_ptr;
+  const int* col_off;
+  const int* cov_n;
+  const int* cov_j;
+  const int* cov_r;
+  int maxcov, N;
+  const int* tile_blk;        // ntiles x kFSlots block ids (-1 unused)
+  const long long* tile_poff; // ntiles x kFSlots partial offsets
+  const double* w;
+  double* part;
+};
+
+__global__ void __launch_bounds__(256) k_fused_normal(FusedArgs A) {
+  extern __shared__ double fsm[];
+  const int MC = A.maxcov;
+  double* yparts = fsm;                        // kFT x MC
+  double* y = yparts + kFT * MC;               // kFT
+  int* pslot = reinterpret_cast<int*>(y + kFT);  // kFT x MC slot of each cover (-1 none)
+  int* prow = pslot + kFT * MC;                // kFT x MC local row
+  __shared__ int s_blk[kFSlots], s_c0[kFSlots], s_pj[kFSlots], s_rows[kFSlots];
+  __shared__ long long s_hoff[kFSlots], s_poff[kFSlots];
+  __shared__ int s_ns;
+  const int tile = blockIdx.x;
+  const int i0 = tile * kFT;
+  if (threadIdx.x == 0) s_ns = 0;
+  __syncthreads();
+  if (threadIdx.x < kFSlots) {
+    const int b = A.tile_blk[static_cast<long long>(tile) * kFSlots + threadIdx.x];
+    s_blk[threadIdx.x] = b;
+    if (b >= 0) {
+      s_c0[threadIdx.x] = A.col_off[b];
+      s_pj[threadIdx.x] = A.col_off[b + 1] - A.col_off[b];
+      s_rows[threadIdx.x] = A.row_ptr[b + 1] - A.row_ptr[b];
+      s_hoff[threadIdx.x] = A.H_off[b];
+      s_poff[threadIdx.x] = A.tile_poff[static_cast<long long>(tile) * kFSlots + threadIdx.x];
+      atomicMax(&s_ns, threadIdx.x + 1);
+    }
+  }
+  __syncthreads();
+  const int ns = s_ns;
+  // covers of the tile's points -> (slot, local row)
+  for (int e = threadIdx.x; e < kFT * MC; e += blockDim.x) {
+    const int t = e / MC, c = e % MC;
+    const int i = i0 + t;
+    int slot = -1, r = 0;
+    if (i < A.N && c < A.cov_n[i]) {
+      const int b = A.cov_j[static_cast<long long>(i) * MC + c];
+      r = A.cov_r[static_cast<long long>(i) * MC + c];
+      for (int s = 0; s < ns; ++s)
+        if (s_blk[s] == b) slot = s;
+    }
+    pslot[e] = slot;
+    prow[e] = r;
+  }
+  __syncthreads();
+  // y partials: one thread per (point, cover); H reads are coalesced along consecutive points
+  for (int e = threadIdx.x; e < kFT * MC; e += blockDim.x) {
+    const int s = pslot[e];
+    double acc = 0.0;
+    if (s >= 0) {
+      const double* h = A.H + s_hoff[s] + prow[e];
+      const double* ww = A.w + s_c0[s];
+      const int rows = s_rows[s], pj = s_pj[s];
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int k = 0;
+      for (; k + 4 <= pj; k += 4) {
+        a0 += __ldg(h + static_cast<long long>(k) * rows) * ww[k];
+        a1 += __ldg(h + static_cast<long long>(k + 1) * rows) * ww[k + 1];
+        a2 += __ldg(h + static_cast<long long>(k + 2) * rows) * ww[k + 2];
+        a3 += __ldg(h + static_cast<long long>(k + 3) * rows) * ww[k + 3];
+      }
+      for (; k < pj; ++k) a0 += __ldg(h + static_cast<long long>(k) * rows) * ww[k];
+      acc = (a0 + a1) + (a2 + a3);
+    }
+    yparts[e] = acc;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kFT; t += blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < MC; ++c) acc += yparts[t * MC + c];  // covers in ascending block order
+    y[t] = acc;
+  }
+  __syncthreads();
+  // Hᵀy partials: warp per (slot, column); lanes walk the tile's points (coalesced, L2-resident)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  int total = 0;
+  for (int s = 0; s < ns; ++s) total += s_pj[s];
+  for (int q = warp; q < total; q += nw) {
+    int s = 0, k = q;
+    while (k >= s_pj[s]) {
+      k -= s_pj[s];
+      ++s;
+    }
+    const double* hcol = A.H + s_hoff[s] + static_cast<long long>(k) * s_rows[s];
+    double acc = 0.0;
+    for (int t = lane; t < kFT; t += 32) {
+      for (int c = 0; c < MC; ++c) {
+        const int e = t * MC + c;
+        if (pslot[e] == s) acc += __ldg(hcol + prow[e]) * y[t];
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) A.part[s_poff[s] + k] = acc;
+  }
+}
+
+// out[col] = Σ_tiles partial(tile, owner(col))[k], tiles in ascending order
+__global__ void k_fused_reduce(const double* __restrict__ part, const int* __restrict__ bptr,
+                               const long long* __restrict__ bparts, const int* __restrict__ col_off,
+                               const int* __restrict__ col_owner, int p, double* __restrict__ out) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= p) return;
+  const int j = col_owner[col];
+  const int k = col - col_off[j];
+  double s = 0.0;
+  for (int q = bptr[j]; q < bptr[j + 1]; ++q) s += part[bparts[q] + k];
+  out[col] = s;
+}
+
+}  // namespace
+
+// Tile plan for the fused operator (once per assembled system): distinct covering blocks per
+// tile, partial-buffer offsets, and per-block partial lists in tile order.
+bool build_fused_plan(Ctx& c) {
+  const int N = c.N, MC = c.maxcov, J = c.J;
+  const int ntiles = ceil_div(N, kFT);
+  std::vector<int> cn(N), cj(static_cast<size_t>(N) * MC);
+  c.cov_n.download(cn.data(), N, c.stream);
+  c.cov_j.download(cj.data(), cj.size(), c.stream);
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+  std::vector<int> tb(static_cast<size_t>(ntiles) * kFSlots, -1);
+  std::vector<long long> tp(static_cast<size_t>(ntiles) * kFSlots, -1);
+  std::vector<std::vector<long long>> per_block(J);
+  long long off = 0;
+  for (int t = 0; t < ntiles; ++t) {
+    int ns = 0;
+    int* slots = &tb[static_cast<size_t>(t) * kFSlots];
+    for (int i = t * kFT; i < std::min(N, (t + 1) * kFT); ++i)
+      for (int q = 0; q < cn[i]; ++q) {
+        const int b = cj[static_cast<size_t>(i) * MC + q];
+        bool found = false;
+        for (int s = 0; s < ns; ++s) found |= slots[s] == b;
+        if (!found) {
+          if (ns == kFSlots) return false;
+          slots[ns++] = b;
+        }
+      }
+    std::sort(slots, slots + ns);
+    for (int s = 0; s < ns; ++s) {
+      tp[static_cast<size_t>(t) * kFSlots + s] = off;
+      per_block[slots[s]].push_back(off);
+      off += c.h_p[slots[s]];
+    }
+  }
+  std::vector<int> bptr(J + 1, 0);
+  std::vector<long long> bparts;
+  for (int j = 0; j < J; ++j) {
+    bparts.insert(bparts.end(), per_block[j].begin(), per_block[j].end());
+    bptr[j + 1] = static_cast<int>(bparts.size());
+  }
+  c.f_tile_blk.upload(tb, c.stream);
+  c.f_tile_poff.upload(tp, c.stream);
+  c.f_bptr.upload(bptr, c.stream);
+  c.f_bparts.upload(bparts, c.stream);
+  c.f_part.ensure(std::max<long long>(1, off));
+  c.f_ntiles = ntiles;
+  c.f_part_size = off;
+  c.fused_ready = true;
+  return true;
+}
+
+void fused_normal_apply_dev(Ctx& c, const double* w, double* out) {
+  ScopedKernelTimer tk(c, "fused_normal");
+  FusedArgs A{};
+  A.H = c.H;
+  A.H_off = c.dH_off.p;
+  A.row_ptr = c.row_ptr.p;
+  A.col_off = c.dcol_off.p;
+  A.cov_n = c.cov_n.p;
+  A.cov_j = c.cov_j.p;
+  A.cov_r = c.cov_r.p;
+  A.maxcov = c.maxcov;
+  A.N = c.N;
+  A.tile_blk = c.f_tile_blk.p;
+  A.tile_poff = c.f_tile_poff.p;
+  A.w = w;
+  A.part = c.f_part.p;
+  const size_t smem = static_cast<size_t>(kFT) * c.maxcov * (sizeof(double) + 2 * sizeof(int)) + kFT * sizeof(double);
+  if (smem > 48 * 1024)
+    RDD_CUDA(cudaFuncSetAttribute(k_fused_normal, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  k_fused_normal<<<c.f_ntiles, 256, smem, c.stream>>>(A);
+  RDD_LAUNCH_CHECK();
+  k_fused_reduce<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.f_part.p, c.f_bptr.p, c.f_bparts.p, c.dcol_off.p,
+                                                           c.downer.p, c.p, out);
   RDD_LAUNCH_CHECK();
 }
 

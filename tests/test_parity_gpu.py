@@ -116,6 +116,10 @@ def test_assembly_and_operators(dev, orc, name):
     assert np.linalg.norm(td - to) <= 10 * tol * np.linalg.norm(to)
     # adjoint identity on the device path alone (test_assembly.cpp:114-134)
     assert abs(yd @ r - w @ td) <= 1e-11 * max(1.0, abs(yd @ r))
+    # normal operator Hᵀ(H·w) (runner.hpp:232-234) in the configured formulation (fused for slices)
+    no = orc.matvec_transpose(orc.matvec(w))
+    nd = dev.normal_apply(w)
+    assert np.linalg.norm(nd - no) <= 10 * tol * np.linalg.norm(no), (name, cfg.op_form)
 
 
 @pytest.mark.parametrize("name", [n for n in CASES if CASES[n].precond >= 0])

@@ -138,11 +138,12 @@ struct FusedArgs {
 __global__ void __launch_bounds__(256) k_fused_normal(FusedArgs A) {
   extern __shared__ double fsm[];
   const int MC = A.maxcov;
-  double* yparts = fsm;                        // kFT x MC
-  double* y = yparts + kFT * MC;               // kFT
-  int* pslot = reinterpret_cast<int*>(y + kFT);  // kFT x MC slot of each cover (-1 none)
-  int* prow = pslot + kFT * MC;                // kFT x MC local row
-  __shared__ int s_blk[kFSlots], s_c0[kFSlots], s_pj[kFSlots], s_rows[kFSlots];
+  double* yparts = fsm;                          // MC x kFT (cover-major)
+  double* y = yparts + kFT * MC;                 // kFT
+  int* pslot = reinterpret_cast<int*>(y + kFT);  // MC x kFT slot of each cover (-1 none)
+  int* prow = pslot + kFT * MC;                  // MC x kFT local row
+  int* lst = prow + kFT * MC;                    // per-slot compact lists: packed (t | c << 16), kFT*MC total
+  __shared__ int s_blk[kFSlots], s_c0[kFSlots], s_pj[kFSlots], s_rows[kFSlots], s_lo[kFSlots], s_len[kFSlots];
   __shared__ long long s_hoff[kFSlots], s_poff[kFSlots];
   __shared__ int s_ns;
   const int tile = blockIdx.x;
@@ -163,9 +164,9 @@ __global__ void __launch_bounds__(256) k_fused_normal(FusedArgs A) {
   }
   __syncthreads();
   const int ns = s_ns;
-  // covers of the tile's points -> (slot, local row)
+  // covers of the tile's points -> (slot, local row); cover-major so a warp walks consecutive points
   for (int e = threadIdx.x; e < kFT * MC; e += blockDim.x) {
-    const int t = e / MC, c = e % MC;
+    const int c = e / kFT, t = e % kFT;
     const int i = i0 + t;
     int slot = -1, r = 0;
     if (i < A.N && c < A.cov_n[i]) {
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(256) k_fused_normal(FusedArgs A) {
     prow[e] = r;
   }
   __syncthreads();
-  // y partials: one thread per (point, cover); H reads are coalesced along consecutive points
+  // y partials, one thread per (cover, point): coalesced along consecutive points
   for (int e = threadIdx.x; e < kFT * MC; e += blockDim.x) {
     const int s = pslot[e];
     double acc = 0.0;
@@ -199,15 +200,42 @@ __global__ void __launch_bounds__(256) k_fused_normal(FusedArgs A) {
     }
     yparts[e] = acc;
   }
+  // per-slot compact (point, cover) lists in ascending point order (warp ballot: deterministic)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   __syncthreads();
-  for (int t = threadIdx.x; t < kFT; t += blockDim.x) {
+  if (threadIdx.x < kFT) {
     double acc = 0.0;
-    for (int c = 0; c < MC; ++c) acc += yparts[t * MC + c];  // covers in ascending block order
-    y[t] = acc;
+    for (int c = 0; c < MC; ++c) acc += yparts[c * kFT + threadIdx.x];  // covers in ascending block order
+    y[threadIdx.x] = acc;
+  }
+  for (int s = warp; s < ns; s += nw) {  // per-slot counts
+    int cnt = 0;
+    for (int e = lane; e < kFT * MC; e += 32) cnt += __popc(__ballot_sync(0xffffffffu, pslot[e] == s)) * (lane == 0);
+    if (lane == 0) s_len[s] = cnt;
   }
   __syncthreads();
-  // Hᵀy partials: warp per (slot, column); lanes walk the tile's points (coalesced, L2-resident)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    int lo = 0;
+    for (int s = 0; s < ns; ++s) {
+      s_lo[s] = lo;
+      lo += s_len[s];
+    }
+  }
+  __syncthreads();
+  for (int s = warp; s < ns; s += nw) {
+    int pos = s_lo[s];
+    for (int t0 = 0; t0 < kFT; t0 += 32) {
+      for (int c = 0; c < MC; ++c) {
+        const int e = c * kFT + t0 + lane;
+        const bool hit = pslot[e] == s;
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (hit) lst[pos + __popc(m & ((1u << lane) - 1u))] = (t0 + lane) | (c << 16);
+        pos += __popc(m);
+      }
+    }
+  }
+  __syncthreads();
+  // Hᵀy partials: warp per (slot, column); lanes walk the slot's list (coalesced, L2-resident)
   int total = 0;
   for (int s = 0; s < ns; ++s) total += s_pj[s];
   for (int q = warp; q < total; q += nw) {
@@ -217,12 +245,13 @@ __global__ void __launch_bounds__(256) k_fused_normal(FusedArgs A) {
       ++s;
     }
     const double* hcol = A.H + s_hoff[s] + static_cast<long long>(k) * s_rows[s];
+    const int* L = lst + s_lo[s];
+    const int len = s_len[s];
     double acc = 0.0;
-    for (int t = lane; t < kFT; t += 32) {
-      for (int c = 0; c < MC; ++c) {
-        const int e = t * MC + c;
-        if (pslot[e] == s) acc += __ldg(hcol + prow[e]) * y[t];
-      }
+    for (int l = lane; l < len; l += 32) {
+      const int v = L[l];
+      const int t = v & 0xffff, c = v >> 16;
+      acc += __ldg(hcol + prow[c * kFT + t]) * y[t];
     }
     acc = warp_sum(acc);
     if (lane == 0) A.part[s_poff[s] + k] = acc;
@@ -310,7 +339,7 @@ void fused_normal_apply_dev(Ctx& c, const double* w, double* out) {
   A.tile_poff = c.f_tile_poff.p;
   A.w = w;
   A.part = c.f_part.p;
-  const size_t smem = static_cast<size_t>(kFT) * c.maxcov * (sizeof(double) + 2 * sizeof(int)) + kFT * sizeof(double);
+  const size_t smem = static_cast<size_t>(kFT) * c.maxcov * (sizeof(double) + 3 * sizeof(int)) + kFT * sizeof(double);
   if (smem > 48 * 1024)
     RDD_CUDA(cudaFuncSetAttribute(k_fused_normal, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   k_fused_normal<<<c.f_ntiles, 256, smem, c.stream>>>(A);

@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
                                                         int* __restrict__ sweeps_out, double2* __restrict__ rot,
                                                         const long long* __restrict__ rot_off, int chunk) {
   namespace cg = cooperative_groups;
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   int rank = 0;
   if constexpr (K > 1) rank = static_cast<int>(cg::this_cluster().block_rank());
   const int b = blockIdx.x / K;
@@ -582,26 +582,19 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
   const int np = ne / 2;
   double* cs = smem + chunk;            // [np] c, [np] s: rotation of pair slot k this step
   double* sn = cs + np;
-  int* lcol = reinterpret_cast<int*>(sn + np);  // local start of column j
+  double** colp = reinterpret_cast<double**>(sn + np);  // generic pointer to the start of column j
+  int* lcol = reinterpret_cast<int*>(colp + ne);        // local start of column j (even)
   unsigned char* own = reinterpret_cast<unsigned char*>(lcol + ne);
   __shared__ int active;
   __shared__ int cbeg, cend;            // my column range [cbeg, cend)
-  double* base[K];
-  if constexpr (K > 1) {
-#pragma unroll
-    for (int r = 0; r < K; ++r) base[r] = cg::this_cluster().map_shared_rank(smem, r);
-  } else {
-    base[0] = smem;
-  }
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int nthr = blockDim.x * blockDim.y;
-  if (tid == 0) {  // even-aligned whole-column ranges of ~chunk elements
-    int cur = 0, start = 0;
+  if (tid == 0) {  // even-aligned whole-column ranges of ~chunk elements; columns padded to even length
+    int cur = 0, start = 0, e = 0;
     cbeg = (rank == 0) ? 0 : ne;
     cend = ne;
     for (int j = 0; j < ne; ++j) {
-      const int e = j * (j + 1) / 2;
-      if ((j & 1) == 0 && cur + 1 < K && e + 2 * j + 3 - start > chunk) {  // next pair would overflow
+      if ((j & 1) == 0 && cur + 1 < K && e + 2 * j + 4 - start > chunk) {
         ++cur;
         start = e;
         if (cur == rank) cbeg = j;
@@ -609,19 +602,23 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
       }
       own[j] = static_cast<unsigned char>(cur);
       lcol[j] = e - start;
+      e += (j + 2) & ~1;  // column j holds rows 0..j, padded to even length
     }
   }
   __syncthreads();
-  auto at = [&](int i, int j) -> double& {  // i <= j
-    return base[own[j]][lcol[j] + i];
-  };
+  for (int j = tid; j < ne; j += nthr) {
+    double* basep = smem;
+    if constexpr (K > 1) basep = cg::this_cluster().map_shared_rank(smem, static_cast<int>(own[j]));
+    colp[j] = basep + lcol[j];
+  }
+  __syncthreads();
   const double* A = Ain + off[b];
   for (int j = cbeg + threadIdx.y; j < cend; j += blockDim.y)
     for (int i = threadIdx.x; i <= j; i += blockDim.x)
       smem[lcol[j] + i] = (i < n && j < n) ? A[i + static_cast<long long>(j) * n] : 0.0;
   if constexpr (K > 1) cg::this_cluster().sync(); else __syncthreads();
   double dmax = 0.0;
-  for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(at(i, i)));
+  for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(colp[i][i]));
   Crit crit = crit_in;
   crit.tiny = 1e-32 * dmax;
   crit.floor_lam = fmax(floor_rel * dmax, crit_in.floor_lam);
@@ -639,70 +636,49 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
       for (int k = tid; k < npair; k += nthr) {
         const int p = o + 2 * k, q = p + 1;
         if (own[q] != rank) continue;
-        const double app = at(p, p), aqq = at(q, q), apq = at(p, q);
+        const double* cq = colp[q];
+        const double app = colp[p][p], aqq = cq[q], apq = cq[p];
         double c = 1.0, sv = 0.0;
         const int d = rot_decision(crit, app, aqq, apq);
         if (d) {
           schur2(app, aqq, apq, c, sv);
           if (d == 2) local_active = 1;
         }
+        if constexpr (K > 1) {
 #pragma unroll
-        for (int r = 0; r < K; ++r) {
-          double* tab = base[r] + chunk;
-          tab[k] = c;
-          tab[np + k] = sv;
+          for (int r = 0; r < K; ++r) {
+            double* tab = cg::this_cluster().map_shared_rank(smem, r) + chunk;
+            tab[k] = c;
+            tab[np + k] = sv;
+          }
+        } else {
+          cs[k] = c;
+          sn[k] = sv;
         }
         R[(static_cast<long long>(sweep) * ne + t) * np + k] = make_double2(c, sv);
       }
       if constexpr (K > 1) cg::this_cluster().sync(); else __syncthreads();
-      // phase B: blocks (U <= W) whose column unit W starts in my range
-      const int nu = o ? np + 1 : np;  // odd steps: {0}, (1,2), ..., (ne-3, ne-2), {ne-1}
+      // phase B: blocks (U <= W) whose column unit W is mine. Units: w0 = max(0, 2W - o), pair
+      // kw = W - o (a singleton when it is not a valid pair index: the two ends in odd steps)
+      const int nu = o ? np + 1 : np;
       for (int W = threadIdx.y; W < nu; W += blockDim.y) {
-        int w0, ws, kw;
-        if (!o) {
-          w0 = 2 * W;
-          ws = 2;
-          kw = W;
-        } else if (W == 0) {
-          w0 = 0;
-          ws = 1;
-          kw = -1;
-        } else if (W == nu - 1) {
-          w0 = ne - 1;
-          ws = 1;
-          kw = -1;
-        } else {
-          w0 = 2 * W - 1;
-          ws = 2;
-          kw = W - 1;
-        }
+        const int w0 = max(0, 2 * W - o);
         if (own[w0] != rank) continue;
-        const double cw = kw >= 0 ? cs[kw] : 1.0, sw = kw >= 0 ? sn[kw] : 0.0;
+        const int kw = W - o;
+        const bool w2 = kw >= 0 && kw < npair;
+        const double cw = w2 ? cs[kw] : 1.0, sw = w2 ? sn[kw] : 0.0;
+        double* c0p = colp[w0];
+        double* c1p = w2 ? colp[w0 + 1] : nullptr;
         for (int U = threadIdx.x; U <= W; U += blockDim.x) {
-          int u0, us, ku;
-          if (!o) {
-            u0 = 2 * U;
-            us = 2;
-            ku = U;
-          } else if (U == 0) {
-            u0 = 0;
-            us = 1;
-            ku = -1;
-          } else if (U == nu - 1) {
-            u0 = ne - 1;
-            us = 1;
-            ku = -1;
-          } else {
-            u0 = 2 * U - 1;
-            us = 2;
-            ku = U - 1;
-          }
-          const double cu = ku >= 0 ? cs[ku] : 1.0, su = ku >= 0 ? sn[ku] : 0.0;
+          const int u0 = max(0, 2 * U - o);
+          const int ku = U - o;
+          const bool u2 = ku >= 0 && ku < npair;
+          const double cu = u2 ? cs[ku] : 1.0, su = u2 ? sn[ku] : 0.0;
           if (U == W) {
-            if (us == 1) continue;
-            double& app = at(u0, u0);
-            double& apq = at(u0, u0 + 1);
-            double& aqq = at(u0 + 1, u0 + 1);
+            if (!u2) continue;
+            double& app = c0p[u0];
+            double& apq = c1p[u0];
+            double& aqq = c1p[u0 + 1];
             if (su == 0.0) {  // pure swap
               const double t0 = app;
               app = aqq;
@@ -716,12 +692,25 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
             continue;
           }
           // rows u0.. (< columns w0..): all four entries are in the upper triangle
-          double a00 = at(u0, w0);
-          double a10 = us == 2 ? at(u0 + 1, w0) : 0.0;
-          double a01 = ws == 2 ? at(u0, w0 + 1) : 0.0;
-          double a11 = (us == 2 && ws == 2) ? at(u0 + 1, w0 + 1) : 0.0;
-          // left Ĵ_Uᵀ: rows (u0, u0+1) <- (s a_u0 + c a_u1, c a_u0 - s a_u1)
-          if (us == 2) {
+          double a00, a10 = 0.0, a01 = 0.0, a11 = 0.0;
+          if (u2 && !o) {  // even step: (u0, u0+1) is an aligned 16-byte pair in both columns
+            const double2 x0 = *reinterpret_cast<const double2*>(c0p + u0);
+            a00 = x0.x;
+            a10 = x0.y;
+            if (w2) {
+              const double2 x1 = *reinterpret_cast<const double2*>(c1p + u0);
+              a01 = x1.x;
+              a11 = x1.y;
+            }
+          } else {
+            a00 = c0p[u0];
+            if (u2) a10 = c0p[u0 + 1];
+            if (w2) {
+              a01 = c1p[u0];
+              if (u2) a11 = c1p[u0 + 1];
+            }
+          }
+          if (u2) {  // left Ĵ_Uᵀ: rows (u0, u0+1) <- (s a_u0 + c a_u1, c a_u0 - s a_u1)
             const double r00 = su * a00 + cu * a10, r10 = cu * a00 - su * a10;
             const double r01 = su * a01 + cu * a11, r11 = cu * a01 - su * a11;
             a00 = r00;
@@ -729,7 +718,7 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
             a01 = r01;
             a11 = r11;
           }
-          if (ws == 2) {  // right Ĵ_W: cols (w0, w0+1) <- (s a_w0 + c a_w1, c a_w0 - s a_w1)
+          if (w2) {  // right Ĵ_W: cols (w0, w0+1) <- (s a_w0 + c a_w1, c a_w0 - s a_w1)
             const double r00 = sw * a00 + cw * a01, r01 = cw * a00 - sw * a01;
             const double r10 = sw * a10 + cw * a11, r11 = cw * a10 - sw * a11;
             a00 = r00;
@@ -737,10 +726,17 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
             a10 = r10;
             a11 = r11;
           }
-          at(u0, w0) = a00;
-          if (us == 2) at(u0 + 1, w0) = a10;
-          if (ws == 2) at(u0, w0 + 1) = a01;
-          if (us == 2 && ws == 2) at(u0 + 1, w0 + 1) = a11;
+          if (u2 && !o) {
+            *reinterpret_cast<double2*>(c0p + u0) = make_double2(a00, a10);
+            if (w2) *reinterpret_cast<double2*>(c1p + u0) = make_double2(a01, a11);
+          } else {
+            c0p[u0] = a00;
+            if (u2) c0p[u0 + 1] = a10;
+            if (w2) {
+              c1p[u0] = a01;
+              if (u2) c1p[u0 + 1] = a11;
+            }
+          }
         }
       }
       if constexpr (K > 1) cg::this_cluster().sync(); else __syncthreads();
@@ -766,7 +762,7 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
     }
   }
   if (rank == 0) {
-    for (int i = tid; i < ne; i += nthr) ev[ev_off[b] + i] = at(i, i);
+    for (int i = tid; i < ne; i += nthr) ev[ev_off[b] + i] = colp[i][i];
     if (tid == 0) sweeps_out[b] = sweep;
   }
   if constexpr (K > 1) cg::this_cluster().sync();  // keep shared memory alive for remote readers
@@ -783,7 +779,7 @@ __global__ void __launch_bounds__(kReplayWarps * 32) k_replay_oe(const int* __re
                                                                  const int* __restrict__ sweeps,
                                                                  double* __restrict__ Vpad,
                                                                  const long long* __restrict__ poff) {
-  extern __shared__ double vs[];
+  extern __shared__ __align__(16) double vs[];
   const int b = blockIdx.y;
   const int n = nvec[b];
   const int ne = n + (n & 1), np = ne / 2;
@@ -804,12 +800,21 @@ __global__ void __launch_bounds__(kReplayWarps * 32) k_replay_oe(const int* __re
         const int o = (t0 + tt) & 1;
         const int npair = o ? np - 1 : np;
         const double2* Rt = logc + tt * np;
-        for (int k = lane; k < npair; k += 32) {
-          const double2 csn = Rt[k];
-          const int p = o + 2 * k;
-          const double a = v[p], bq = v[p + 1];
-          v[p] = csn.y * a + csn.x * bq;
-          v[p + 1] = csn.x * a - csn.y * bq;
+        if (!o) {  // even step: aligned 16-byte pairs
+          for (int k = lane; k < npair; k += 32) {
+            const double2 csn = Rt[k];
+            double2* vp = reinterpret_cast<double2*>(v + 2 * k);
+            const double2 ab = *vp;
+            *vp = make_double2(csn.y * ab.x + csn.x * ab.y, csn.x * ab.x - csn.y * ab.y);
+          }
+        } else {
+          for (int k = lane; k < npair; k += 32) {
+            const double2 csn = Rt[k];
+            const int p = 1 + 2 * k;
+            const double a = v[p], bq = v[p + 1];
+            v[p] = csn.y * a + csn.x * bq;
+            v[p + 1] = csn.x * a - csn.y * bq;
+          }
         }
         __syncwarp();
       }
@@ -864,12 +869,13 @@ __global__ void k_compact(const double* __restrict__ Vp, const double* __restric
 
 // shared memory of k_jacobi_oe<K> for even order ne
 static size_t oe_chunk(int ne, int K) {
-  const size_t tri = static_cast<size_t>(ne) * (ne + 1) / 2;
+  size_t tri = 0;  // columns padded to even length (aligned 16-byte row pairs)
+  for (int j = 0; j < ne; ++j) tri += static_cast<size_t>((j + 2) & ~1);
   return K == 1 ? tri : (tri + K - 1) / K + 2 * static_cast<size_t>(ne) + 4;
 }
 static size_t oe_smem(int ne, int K) {
   return oe_chunk(ne, K) * sizeof(double) + static_cast<size_t>(ne / 2) * 2 * sizeof(double) +
-         static_cast<size_t>(ne) * (sizeof(int) + 1) + 64;
+         static_cast<size_t>(ne) * (sizeof(double*) + sizeof(int) + 1) + 64;
 }
 static int oe_k(int ne) {
   for (int K : {1, 2, 4, 8})

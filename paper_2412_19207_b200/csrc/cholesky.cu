@@ -231,7 +231,10 @@ void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n
   DBuf<Mat> dm;
   DBuf<int> dfail, dact;
   DBuf<int2> dt;
-  DBuf<double> dfa, dfp, Mi, tmp;
+  DBuf<double> dfa, dfp;
+  struct WS {
+    double* p;
+  } Mi{nullptr}, tmp{nullptr};
   dm.upload(mats, c.stream);
   dfail.zero(B, c.stream);
   dfa.ensure(B);
@@ -280,7 +283,11 @@ void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n
     gemm_nt(c, upd);  // synchronizes (task-buffer lifetime), so dact/dt can be reused
   }
   // ---- M = L^{-1}
-  Mi.zero(static_cast<size_t>(off[B - 1] + static_cast<long long>(n[B - 1]) * n[B - 1]), c.stream);
+  {
+    const size_t msz = static_cast<size_t>(off[B - 1] + static_cast<long long>(n[B - 1]) * n[B - 1]);
+    Mi.p = c.ws("chol.Minv", msz);
+    RDD_CUDA(cudaMemsetAsync(Mi.p, 0, msz * sizeof(double), c.stream));
+  }
   {
     std::vector<int2> diag;
     for (int i = 0; i < B; ++i)
@@ -295,7 +302,7 @@ void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n
     toff[i] = tmp_sz;
     tmp_sz += static_cast<long long>(NB) * n[i];
   }
-  tmp.ensure(std::max<long long>(1, tmp_sz));
+  tmp.p = c.ws("chol.tmp", std::max<long long>(1, tmp_sz));
   for (int ib = 1; ib < nbmax; ++ib) {
     std::vector<GemmTask> g1, g2;
     for (int i = 0; i < B; ++i) {

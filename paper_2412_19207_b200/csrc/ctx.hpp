@@ -153,6 +153,9 @@ struct Ctx {
   size_t cg_graph_kernels = 0;
 
   double* wk(size_t count) { return work.ensure(count); }
+  // persistent grow-only workspaces for large temporaries (no per-call pool traffic)
+  std::map<std::string, DBuf<double>> wsd;
+  double* ws(const std::string& name, size_t count) { return wsd[name].ensure(count > 0 ? count : 1); }
   cudaEvent_t ev[8] = {nullptr};
 };
 

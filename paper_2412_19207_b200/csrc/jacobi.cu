@@ -919,8 +919,12 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
   }
   DBuf<int> dn, dsw, dnp;
   DBuf<long long> doff, doffE, droff, dwoff, deoffp;
-  DBuf<double2> rot;
-  DBuf<double> Vp, evp;
+  struct WS2 {
+    double2* p;
+  } rot{nullptr};
+  struct WS {
+    double* p;
+  } Vp{nullptr}, evp{nullptr};
   dn.upload(n, c.stream);
   doff.upload(offA, c.stream);
   doffE.upload(offE, c.stream);
@@ -929,9 +933,9 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
   deoffp.upload(eoffp, c.stream);
   droff.upload(roff, c.stream);
   dsw.ensure(B);
-  Vp.ensure(wt);
-  evp.ensure(et);
-  rot.ensure(std::max<long long>(1, rt));
+  Vp.p = c.ws("syevj.Vp", wt);
+  evp.p = c.ws("syevj.ev", et);
+  rot.p = reinterpret_cast<double2*>(c.ws("syevj.rot", 2 * static_cast<size_t>(std::max<long long>(1, rt))));
   const int ne = nmax + (nmax & 1);
   const int K = oe_k(ne);
   int swmax = 0;
@@ -971,8 +975,9 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     RDD_LAUNCH_CHECK();
   } else {
     // ---- odd-even ordering, full storage in global memory (very large orders)
-    DBuf<double> Wk;
-    Wk.ensure(wt);
+    struct WS3 {
+      double* p;
+    } Wk{c.ws("syevj.Wk", wt)};
     k_pad_copy<<<B, 256, 0, c.stream>>>(A, doff.p, dn.p, Wk.p, dwoff.p, dnp.p);
     RDD_LAUNCH_CHECK();
     const size_t smem = static_cast<size_t>(ne + 2) * sizeof(double);

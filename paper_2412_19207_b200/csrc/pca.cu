@@ -100,10 +100,11 @@ void run_pca(Ctx& c) {
   c.identity_V = !reduce;
   if (reduce) {
     const size_t mm = static_cast<size_t>(m) * m;
-    DBuf<double> G, V0, lam, T, W, Vfull;
-    G.ensure(J * mm);
-    V0.ensure(J * mm);
-    lam.ensure(static_cast<size_t>(J) * m);
+    struct WS {
+      double* p;
+    };
+    WS G{c.ws("pca.G", J * mm)}, V0{c.ws("pca.V0", J * mm)}, lam{c.ws("pca.lam", static_cast<size_t>(J) * m)};
+    WS T{nullptr}, W{nullptr}, Vfull{nullptr};
     std::vector<int> ns(J, m);
     std::vector<long long> offm(J);
     for (int j = 0; j < J; ++j) offm[j] = static_cast<long long>(j) * mm;
@@ -127,7 +128,7 @@ void run_pca(Ctx& c) {
     gemm_tn(c, gram_tasks(c, c.S.p, G.p, c.S_off));
     batched_syevj(c, G.p, V0.p, lam.p, ns, offm, s1);
     // stage 2: T = S V0, G1 = TᵀT, Jacobi on the graded G1
-    T.ensure(std::max<long long>(1, c.S_off[J]));
+    T.p = c.ws("pca.T", std::max<long long>(1, c.S_off[J]));
     {
       std::vector<GemmTask> t;
       for (int j = 0; j < J; ++j) {
@@ -140,11 +141,10 @@ void run_pca(Ctx& c) {
       gemm_nn(c, t);
     }
     gemm_tn(c, gram_tasks(c, T.p, G.p, c.S_off));
-    T.release();
-    W.ensure(J * mm);
+    W.p = c.ws("pca.W", J * mm);
     batched_syevj(c, G.p, W.p, lam.p, ns, offm, s2);
     // V = V0 W
-    Vfull.ensure(J * mm);
+    Vfull.p = c.ws("pca.Vfull", J * mm);
     {
       std::vector<GemmTask> t;
       for (int j = 0; j < J; ++j)

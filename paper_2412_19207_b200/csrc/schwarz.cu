@@ -245,7 +245,7 @@ void build_schwarz(Ctx& c, int kind) {
       }
   }
   c.dP_off.upload(c.P_off, c.stream);
-  DBuf<double> A;
+  DBuf<double>& A = c.wsd["schwarz.A"];
   std::vector<int> all(J);
   for (int i = 0; i < J; ++i) all[i] = i;
   std::vector<long long> offA(c.P_off.begin(), c.P_off.end() - 1);
@@ -255,7 +255,6 @@ void build_schwarz(Ctx& c, int kind) {
   std::vector<int> fail;
   std::vector<double> fa, fp;
   batched_spd_inverse(c, A.p, c.P.p, n, offA, fail, fa, fp);
-  A.release();
   c.local_rank.assign(J, 0);
   c.local_cond.assign(J, 0.0);
   c.local_cond_exact = false;

@@ -135,8 +135,9 @@ struct Ctx {
   DBuf<double> W;                     // p x C (unscaled)
   DBuf<double> ytmp;                  // N
   // fused single-pass normal operator plan
-  DBuf<int> f_tile_blk, f_bptr;
-  DBuf<long long> f_tile_poff, f_bparts;
+  DBuf<int> f_bptr;
+  DBuf<unsigned char> f_tiles;
+  DBuf<long long> f_bparts;
   DBuf<double> f_part;
   int f_ntiles = 0;
   long long f_part_size = 0;

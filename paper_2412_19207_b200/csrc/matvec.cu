@@ -106,155 +106,200 @@ void matvec_t_dev(Ctx& c, const double* r, double* out) {
 }  // namespace rdd
 
 // ============================================================================================
-// Fused single-pass normal operator out = Hᵀ(H·w) (runner.hpp:232-234 computes it as two passes,
-// assembly.hpp:110-133). Global rows are cut into tiles of kFT consecutive points; a CTA gathers
-// the rows of every covering block for its tile (each H element belongs to exactly one tile, so
-// HBM reads H once), forms y = H·w for the tile in shared memory in the reference's per-row order
-// (ascending covering block), then re-reads the same (now L2-resident) rows to accumulate
-// Hᵀy per (tile, block) into a partial buffer. A second kernel sums the partials of each block in
-// tile order: deterministic, no atomics.
+// Fused single-pass normal operator out = Hᵀ(H·w) (runner.hpp:232-234 computes it as two passes
+// over H, assembly.hpp:110-133). Global rows are cut into tiles of consecutive points such that,
+// for every covering block j ("slot"), the tile's points inside box j are one contiguous range of
+// the tile with contiguous local rows of H_j. Each slot column segment is then one contiguous run
+// of a column-major block, streamed into shared memory by a 1-D TMA bulk copy (cp.async.bulk,
+// mbarrier completion) — H is read from HBM exactly once. A persistent CTA double-buffers tiles:
+// while tile t is reduced from shared memory, tile t+grid is in flight. y = H·w is formed per
+// point in the reference's order (ascending covering block), then Hᵀy per (tile, slot) goes to a
+// partial buffer that a second kernel sums in tile order: deterministic, no atomics.
 // ============================================================================================
 namespace rdd {
 namespace {
 
-constexpr int kFT = 128;     // points per tile
-constexpr int kFSlots = 32;  // distinct blocks per tile (plan falls back to two passes beyond)
+constexpr int kFT = 128;                // max points per tile
+constexpr int kFSlots = 16;             // max covering blocks per tile
+constexpr int kFBuf = 96 * 1024;        // bytes per tile buffer (two buffers per CTA)
+constexpr int kFThreads = 512;
+
+struct TileSlot {
+  int blk, ta, len, ra;   // block, first point in tile, #points, first local row
+};
+struct Tile {
+  int i0, npts, ns, pad;
+  long long poff;         // partial offset of slot 0 (slots follow, p_j each)
+  TileSlot s[kFSlots];
+};
 
 struct FusedArgs {
   const double* H;
   const long long* H_off;
   const int* row_ptr;
   const int* col_off;
-  const int* cov_n;
-  const int* cov_j;
-  const int* cov_r;
-  int maxcov, N;
-  const int* tile_blk;        // ntiles x kFSlots block ids (-1 unused)
-  const long long* tile_poff; // ntiles x kFSlots partial offsets
+  const Tile* tiles;
+  int ntiles;
   const double* w;
   double* part;
 };
 
-__global__ void __launch_bounds__(256) k_fused_normal(FusedArgs A) {
-  extern __shared__ double fsm[];
-  const int MC = A.maxcov;
-  double* yparts = fsm;                          // MC x kFT (cover-major)
-  double* y = yparts + kFT * MC;                 // kFT
-  int* pslot = reinterpret_cast<int*>(y + kFT);  // MC x kFT slot of each cover (-1 none)
-  int* prow = pslot + kFT * MC;                  // MC x kFT local row
-  int* lst = prow + kFT * MC;                    // per-slot compact lists: packed (t | c << 16), kFT*MC total
-  __shared__ int s_blk[kFSlots], s_c0[kFSlots], s_pj[kFSlots], s_rows[kFSlots], s_lo[kFSlots], s_len[kFSlots];
-  __shared__ long long s_hoff[kFSlots], s_poff[kFSlots];
-  __shared__ int s_ns;
-  const int tile = blockIdx.x;
-  const int i0 = tile * kFT;
-  if (threadIdx.x == 0) s_ns = 0;
-  __syncthreads();
-  if (threadIdx.x < kFSlots) {
-    const int b = A.tile_blk[static_cast<long long>(tile) * kFSlots + threadIdx.x];
-    s_blk[threadIdx.x] = b;
-    if (b >= 0) {
-      s_c0[threadIdx.x] = A.col_off[b];
-      s_pj[threadIdx.x] = A.col_off[b + 1] - A.col_off[b];
-      s_rows[threadIdx.x] = A.row_ptr[b + 1] - A.row_ptr[b];
-      s_hoff[threadIdx.x] = A.H_off[b];
-      s_poff[threadIdx.x] = A.tile_poff[static_cast<long long>(tile) * kFSlots + threadIdx.x];
-      atomicMax(&s_ns, threadIdx.x + 1);
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT%=:\n\t"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// layout of one slot inside a tile buffer: p_j column segments, pitch = len + 2 (even), each
+// segment starts on a 16-byte boundary and holds the 16-byte aligned superset of the rows
+__device__ __forceinline__ int seg_pitch(int len) { return (len + 3) & ~1; }
+
+__device__ void issue_tile(const FusedArgs& A, const Tile& T, double* buf, uint64_t* bar, int lane) {
+  // total bytes first (lane 0 arms the barrier), then lanes issue the column copies
+  uint32_t total = 0;
+  for (int s = 0; s < T.ns; ++s) {
+    const TileSlot& S = T.s[s];
+    const int j = S.blk, rows = A.row_ptr[j + 1] - A.row_ptr[j], pj = A.col_off[j + 1] - A.col_off[j];
+    for (int k = 0; k < pj; ++k) {
+      const long long idx = A.H_off[j] + static_cast<long long>(k) * rows + S.ra;
+      const int a = static_cast<int>(idx & 1);
+      total += static_cast<uint32_t>(((S.len + a + 1) & ~1) * sizeof(double));
     }
   }
-  __syncthreads();
-  const int ns = s_ns;
-  // covers of the tile's points -> (slot, local row); cover-major so a warp walks consecutive points
-  for (int e = threadIdx.x; e < kFT * MC; e += blockDim.x) {
-    const int c = e / kFT, t = e % kFT;
-    const int i = i0 + t;
-    int slot = -1, r = 0;
-    if (i < A.N && c < A.cov_n[i]) {
-      const int b = A.cov_j[static_cast<long long>(i) * MC + c];
-      r = A.cov_r[static_cast<long long>(i) * MC + c];
-      for (int s = 0; s < ns; ++s)
-        if (s_blk[s] == b) slot = s;
+  if (lane == 0) mbar_expect_tx(bar, total);
+  __syncwarp();
+  int base = 0;
+  for (int s = 0; s < T.ns; ++s) {
+    const TileSlot& S = T.s[s];
+    const int j = S.blk, rows = A.row_ptr[j + 1] - A.row_ptr[j], pj = A.col_off[j + 1] - A.col_off[j];
+    const int pitch = seg_pitch(S.len);
+    for (int k = lane; k < pj; k += 32) {
+      const long long idx = A.H_off[j] + static_cast<long long>(k) * rows + S.ra;
+      const int a = static_cast<int>(idx & 1);
+      tma_load_1d(buf + base + k * pitch, A.H + (idx - a), static_cast<uint32_t>(((S.len + a + 1) & ~1) * sizeof(double)),
+                  bar);
     }
-    pslot[e] = slot;
-    prow[e] = r;
+    base += pj * pitch;
   }
-  __syncthreads();
-  // y partials, one thread per (cover, point): coalesced along consecutive points
-  for (int e = threadIdx.x; e < kFT * MC; e += blockDim.x) {
-    const int s = pslot[e];
-    double acc = 0.0;
-    if (s >= 0) {
-      const double* h = A.H + s_hoff[s] + prow[e];
-      const double* ww = A.w + s_c0[s];
-      const int rows = s_rows[s], pj = s_pj[s];
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int k = 0;
-      for (; k + 4 <= pj; k += 4) {
-        a0 += __ldg(h + static_cast<long long>(k) * rows) * ww[k];
-        a1 += __ldg(h + static_cast<long long>(k + 1) * rows) * ww[k + 1];
-        a2 += __ldg(h + static_cast<long long>(k + 2) * rows) * ww[k + 2];
-        a3 += __ldg(h + static_cast<long long>(k + 3) * rows) * ww[k + 3];
-      }
-      for (; k < pj; ++k) a0 += __ldg(h + static_cast<long long>(k) * rows) * ww[k];
-      acc = (a0 + a1) + (a2 + a3);
-    }
-    yparts[e] = acc;
-  }
-  // per-slot compact (point, cover) lists in ascending point order (warp ballot: deterministic)
+}
+
+__global__ void __launch_bounds__(kFThreads) k_fused_normal(FusedArgs A) {
+  extern __shared__ __align__(128) double fsm[];
+  double* bufs[2] = {fsm, fsm + kFBuf / sizeof(double)};
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ double y[kFT];
+  __shared__ double ypart[kFSlots][kFT];
+  __shared__ Tile cur;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  __syncthreads();
-  if (threadIdx.x < kFT) {
-    double acc = 0.0;
-    for (int c = 0; c < MC; ++c) acc += yparts[c * kFT + threadIdx.x];  // covers in ascending block order
-    y[threadIdx.x] = acc;
-  }
-  for (int s = warp; s < ns; s += nw) {  // per-slot counts
-    int cnt = 0;
-    for (int e = lane; e < kFT * MC; e += 32) cnt += __popc(__ballot_sync(0xffffffffu, pslot[e] == s)) * (lane == 0);
-    if (lane == 0) s_len[s] = cnt;
-  }
-  __syncthreads();
   if (threadIdx.x == 0) {
-    int lo = 0;
-    for (int s = 0; s < ns; ++s) {
-      s_lo[s] = lo;
-      lo += s_len[s];
-    }
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  for (int s = warp; s < ns; s += nw) {
-    int pos = s_lo[s];
-    for (int t0 = 0; t0 < kFT; t0 += 32) {
-      for (int c = 0; c < MC; ++c) {
-        const int e = c * kFT + t0 + lane;
-        const bool hit = pslot[e] == s;
-        const unsigned m = __ballot_sync(0xffffffffu, hit);
-        if (hit) lst[pos + __popc(m & ((1u << lane) - 1u))] = (t0 + lane) | (c << 16);
-        pos += __popc(m);
+  int it = 0;
+  uint32_t phase[2] = {0, 0};
+  if (warp == 0 && blockIdx.x < A.ntiles) issue_tile(A, A.tiles[blockIdx.x], bufs[0], &bar[0], lane);
+  for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++it) {
+    const int b = it & 1;
+    // prefetch the next tile into the other buffer (its previous contents were consumed)
+    const int nxt = tile + gridDim.x;
+    if (warp == 0 && nxt < A.ntiles) {
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      issue_tile(A, A.tiles[nxt], bufs[b ^ 1], &bar[b ^ 1], lane);
+    }
+    if (threadIdx.x < static_cast<int>(sizeof(Tile) / sizeof(int)))
+      reinterpret_cast<int*>(&cur)[threadIdx.x] = reinterpret_cast<const int*>(&A.tiles[tile])[threadIdx.x];
+    mbar_wait(&bar[b], phase[b]);
+    phase[b] ^= 1u;
+    __syncthreads();
+    const double* buf = bufs[b];
+    // slot bases inside the buffer
+    __shared__ int sbase[kFSlots], sc0[kFSlots], spj[kFSlots], srows[kFSlots];
+    __shared__ long long shoff[kFSlots];
+    if (threadIdx.x == 0) {
+      int base = 0;
+      for (int s = 0; s < cur.ns; ++s) {
+        const int j = cur.s[s].blk;
+        sbase[s] = base;
+        sc0[s] = A.col_off[j];
+        spj[s] = A.col_off[j + 1] - A.col_off[j];
+        srows[s] = A.row_ptr[j + 1] - A.row_ptr[j];
+        shoff[s] = A.H_off[j];
+        base += spj[s] * seg_pitch(cur.s[s].len);
       }
     }
-  }
-  __syncthreads();
-  // Hᵀy partials: warp per (slot, column); lanes walk the slot's list (coalesced, L2-resident)
-  int total = 0;
-  for (int s = 0; s < ns; ++s) total += s_pj[s];
-  for (int q = warp; q < total; q += nw) {
-    int s = 0, k = q;
-    while (k >= s_pj[s]) {
-      k -= s_pj[s];
-      ++s;
+    __syncthreads();
+    // y partials: thread per (slot, point in slot)
+    for (int e = threadIdx.x; e < cur.ns * kFT; e += blockDim.x) {
+      const int s = e / kFT, tt = e % kFT;
+      const TileSlot& S = cur.s[s];
+      if (tt >= S.len) continue;
+      const int pitch = seg_pitch(S.len), pj = spj[s], rows = srows[s];
+      const double* seg = buf + sbase[s] + tt;
+      const double* ww = A.w + sc0[s];
+      const long long idx0 = shoff[s] + S.ra;
+      double a0 = 0.0, a1 = 0.0;
+      int k = 0;
+      for (; k + 2 <= pj; k += 2) {
+        const int al0 = static_cast<int>((idx0 + static_cast<long long>(k) * rows) & 1);
+        const int al1 = static_cast<int>((idx0 + static_cast<long long>(k + 1) * rows) & 1);
+        a0 += seg[k * pitch + al0] * ww[k];
+        a1 += seg[(k + 1) * pitch + al1] * ww[k + 1];
+      }
+      if (k < pj) a0 += seg[k * pitch + static_cast<int>((idx0 + static_cast<long long>(k) * rows) & 1)] * ww[k];
+      ypart[s][S.ta + tt] = a0 + a1;
     }
-    const double* hcol = A.H + s_hoff[s] + static_cast<long long>(k) * s_rows[s];
-    const int* L = lst + s_lo[s];
-    const int len = s_len[s];
-    double acc = 0.0;
-    for (int l = lane; l < len; l += 32) {
-      const int v = L[l];
-      const int t = v & 0xffff, c = v >> 16;
-      acc += __ldg(hcol + prow[c * kFT + t]) * y[t];
+    __syncthreads();
+    for (int t = threadIdx.x; t < cur.npts; t += blockDim.x) {
+      double acc = 0.0;
+      for (int s = 0; s < cur.ns; ++s)  // slots ascend by block: the reference's per-row order
+        if (t >= cur.s[s].ta && t < cur.s[s].ta + cur.s[s].len) acc += ypart[s][t];
+      y[t] = acc;
     }
-    acc = warp_sum(acc);
-    if (lane == 0) A.part[s_poff[s] + k] = acc;
+    __syncthreads();
+    // Hᵀy partials: warp per (slot, column), lanes over the slot's points
+    int total = 0;
+    for (int s = 0; s < cur.ns; ++s) total += spj[s];
+    for (int q = warp; q < total; q += nw) {
+      int s = 0, k = q;
+      while (k >= spj[s]) {
+        k -= spj[s];
+        ++s;
+      }
+      const TileSlot& S = cur.s[s];
+      const int al = static_cast<int>((shoff[s] + S.ra + static_cast<long long>(k) * srows[s]) & 1);
+      const double* seg = buf + sbase[s] + k * seg_pitch(S.len) + al;
+      double acc = 0.0;
+      for (int tt = lane; tt < S.len; tt += 32) acc += seg[tt] * y[S.ta + tt];
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        long long po = cur.poff;
+        for (int s2 = 0; s2 < s; ++s2) po += spj[s2];
+        A.part[po + k] = acc;
+      }
+    }
+    __syncthreads();  // buffer b free for the prefetch issued in the next-but-one iteration
   }
 }
 
@@ -273,38 +318,63 @@ __global__ void k_fused_reduce(const double* __restrict__ part, const int* __res
 
 }  // namespace
 
-// Tile plan for the fused operator (once per assembled system): distinct covering blocks per
-// tile, partial-buffer offsets, and per-block partial lists in tile order.
+// Tile plan (once per assembled system): greedy runs of consecutive points in which every
+// covering block's rows stay contiguous, bounded by kFT points, kFSlots blocks and kFBuf bytes.
 bool build_fused_plan(Ctx& c) {
   const int N = c.N, MC = c.maxcov, J = c.J;
-  const int ntiles = ceil_div(N, kFT);
-  std::vector<int> cn(N), cj(static_cast<size_t>(N) * MC);
+  std::vector<int> cn(N), cj(static_cast<size_t>(N) * MC), cr(static_cast<size_t>(N) * MC);
   c.cov_n.download(cn.data(), N, c.stream);
   c.cov_j.download(cj.data(), cj.size(), c.stream);
+  c.cov_r.download(cr.data(), cr.size(), c.stream);
   RDD_CUDA(cudaStreamSynchronize(c.stream));
-  std::vector<int> tb(static_cast<size_t>(ntiles) * kFSlots, -1);
-  std::vector<long long> tp(static_cast<size_t>(ntiles) * kFSlots, -1);
+  std::vector<Tile> tiles;
   std::vector<std::vector<long long>> per_block(J);
-  long long off = 0;
-  for (int t = 0; t < ntiles; ++t) {
-    int ns = 0;
-    int* slots = &tb[static_cast<size_t>(t) * kFSlots];
-    for (int i = t * kFT; i < std::min(N, (t + 1) * kFT); ++i)
-      for (int q = 0; q < cn[i]; ++q) {
-        const int b = cj[static_cast<size_t>(i) * MC + q];
-        bool found = false;
-        for (int s = 0; s < ns; ++s) found |= slots[s] == b;
-        if (!found) {
-          if (ns == kFSlots) return false;
-          slots[ns++] = b;
+  long long poff = 0;
+  auto seg_pitch_h = [](int len) { return (len + 3) & ~1; };
+  int i = 0;
+  while (i < N) {
+    Tile T{};
+    T.i0 = i;
+    T.ns = 0;
+    int t = 0;
+    for (; i < N && t < kFT; ++i, ++t) {
+      // tentative extension by point i
+      Tile U = T;
+      bool ok = true;
+      for (int q = 0; q < cn[i] && ok; ++q) {
+        const int b = cj[static_cast<size_t>(i) * MC + q], r = cr[static_cast<size_t>(i) * MC + q];
+        int s = -1;
+        for (int z = 0; z < U.ns; ++z)
+          if (U.s[z].blk == b) s = z;
+        if (s < 0) {
+          if (U.ns == kFSlots) {
+            ok = false;
+            break;
+          }
+          U.s[U.ns++] = {b, t, 1, r};
+        } else {
+          TileSlot& S = U.s[s];
+          if (S.ta + S.len != t || S.ra + S.len != r) ok = false;  // contiguity in tile and rows
+          else ++S.len;
         }
       }
-    std::sort(slots, slots + ns);
-    for (int s = 0; s < ns; ++s) {
-      tp[static_cast<size_t>(t) * kFSlots + s] = off;
-      per_block[slots[s]].push_back(off);
-      off += c.h_p[slots[s]];
+      long long bytes = 0;
+      for (int z = 0; z < U.ns && ok; ++z) bytes += static_cast<long long>(c.h_p[U.s[z].blk]) * seg_pitch_h(U.s[z].len) * 8;
+      if (!ok || bytes > kFBuf) {
+        if (t == 0) return false;  // a single point does not fit
+        break;
+      }
+      T = U;
     }
+    T.npts = t;
+    // slots in ascending block order (the reference's per-row summation order)
+    std::sort(T.s, T.s + T.ns, [](const TileSlot& a, const TileSlot& b) { return a.blk < b.blk; });
+    T.poff = poff;
+    for (int z = 0; z < T.ns; ++z) {
+      per_block[T.s[z].blk].push_back(poff);
+      poff += c.h_p[T.s[z].blk];
+    }
+    tiles.push_back(T);
   }
   std::vector<int> bptr(J + 1, 0);
   std::vector<long long> bparts;
@@ -312,13 +382,14 @@ bool build_fused_plan(Ctx& c) {
     bparts.insert(bparts.end(), per_block[j].begin(), per_block[j].end());
     bptr[j + 1] = static_cast<int>(bparts.size());
   }
-  c.f_tile_blk.upload(tb, c.stream);
-  c.f_tile_poff.upload(tp, c.stream);
+  c.f_tiles.ensure(tiles.size() * sizeof(Tile));
+  RDD_CUDA(cudaMemcpyAsync(c.f_tiles.p, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice, c.stream));
   c.f_bptr.upload(bptr, c.stream);
   c.f_bparts.upload(bparts, c.stream);
-  c.f_part.ensure(std::max<long long>(1, off));
-  c.f_ntiles = ntiles;
-  c.f_part_size = off;
+  c.f_part.ensure(std::max<long long>(1, poff));
+  c.f_ntiles = static_cast<int>(tiles.size());
+  c.f_part_size = poff;
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
   c.fused_ready = true;
   return true;
 }
@@ -330,19 +401,18 @@ void fused_normal_apply_dev(Ctx& c, const double* w, double* out) {
   A.H_off = c.dH_off.p;
   A.row_ptr = c.row_ptr.p;
   A.col_off = c.dcol_off.p;
-  A.cov_n = c.cov_n.p;
-  A.cov_j = c.cov_j.p;
-  A.cov_r = c.cov_r.p;
-  A.maxcov = c.maxcov;
-  A.N = c.N;
-  A.tile_blk = c.f_tile_blk.p;
-  A.tile_poff = c.f_tile_poff.p;
+  A.tiles = reinterpret_cast<const Tile*>(c.f_tiles.p);
+  A.ntiles = c.f_ntiles;
   A.w = w;
   A.part = c.f_part.p;
-  const size_t smem = static_cast<size_t>(kFT) * c.maxcov * (sizeof(double) + 3 * sizeof(int)) + kFT * sizeof(double);
-  if (smem > 48 * 1024)
+  const size_t smem = 2 * static_cast<size_t>(kFBuf);
+  static bool attr = false;
+  if (!attr) {
     RDD_CUDA(cudaFuncSetAttribute(k_fused_normal, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  k_fused_normal<<<c.f_ntiles, 256, smem, c.stream>>>(A);
+    attr = true;
+  }
+  const int grid = std::min(c.f_ntiles, c.prop.multiProcessorCount);
+  k_fused_normal<<<grid, kFThreads, smem, c.stream>>>(A);
   RDD_LAUNCH_CHECK();
   k_fused_reduce<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.f_part.p, c.f_bptr.p, c.f_bparts.p, c.dcol_off.p,
                                                            c.downer.p, c.p, out);

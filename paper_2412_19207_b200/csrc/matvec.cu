@@ -126,9 +126,11 @@ constexpr int kFThreads = 512;
 
 struct TileSlot {
   int blk, ta, len, ra;   // block, first point in tile, #points, first local row
+  int pj, rows, c0, base; // block width, block rows, first column, offset in the tile buffer
+  long long src;          // element index of H_j[ra, 0]
 };
 struct Tile {
-  int i0, npts, ns, pad;
+  int i0, npts, ns, tx_bytes;
   long long poff;         // partial offset of slot 0 (slots follow, p_j each)
   TileSlot s[kFSlots];
 };
@@ -173,133 +175,112 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 // segment starts on a 16-byte boundary and holds the 16-byte aligned superset of the rows
 __device__ __forceinline__ int seg_pitch(int len) { return (len + 3) & ~1; }
 
-__device__ void issue_tile(const FusedArgs& A, const Tile& T, double* buf, uint64_t* bar, int lane) {
-  // total bytes first (lane 0 arms the barrier), then lanes issue the column copies
-  uint32_t total = 0;
-  for (int s = 0; s < T.ns; ++s) {
-    const TileSlot& S = T.s[s];
-    const int j = S.blk, rows = A.row_ptr[j + 1] - A.row_ptr[j], pj = A.col_off[j + 1] - A.col_off[j];
-    for (int k = 0; k < pj; ++k) {
-      const long long idx = A.H_off[j] + static_cast<long long>(k) * rows + S.ra;
-      const int a = static_cast<int>(idx & 1);
-      total += static_cast<uint32_t>(((S.len + a + 1) & ~1) * sizeof(double));
-    }
-  }
-  if (lane == 0) mbar_expect_tx(bar, total);
+__device__ __forceinline__ int col_parity(const TileSlot& S, int k) {
+  return static_cast<int>((S.src + static_cast<long long>(k) * S.rows) & 1);
+}
+
+// producer warp: arm the barrier with the tile's byte count, then one bulk copy per column segment
+__device__ void issue_tile(const FusedArgs& A, const Tile* T, double* buf, uint64_t* bar, int lane) {
+  const int ns = T->ns;
+  if (lane == 0) mbar_expect_tx(bar, static_cast<uint32_t>(T->tx_bytes));
   __syncwarp();
-  int base = 0;
-  for (int s = 0; s < T.ns; ++s) {
-    const TileSlot& S = T.s[s];
-    const int j = S.blk, rows = A.row_ptr[j + 1] - A.row_ptr[j], pj = A.col_off[j + 1] - A.col_off[j];
+  for (int s = 0; s < ns; ++s) {
+    const TileSlot S = T->s[s];
     const int pitch = seg_pitch(S.len);
-    for (int k = lane; k < pj; k += 32) {
-      const long long idx = A.H_off[j] + static_cast<long long>(k) * rows + S.ra;
+    for (int k = lane; k < S.pj; k += 32) {
+      const long long idx = S.src + static_cast<long long>(k) * S.rows;
       const int a = static_cast<int>(idx & 1);
-      tma_load_1d(buf + base + k * pitch, A.H + (idx - a), static_cast<uint32_t>(((S.len + a + 1) & ~1) * sizeof(double)),
-                  bar);
+      tma_load_1d(buf + S.base + k * pitch, A.H + (idx - a),
+                  static_cast<uint32_t>(((S.len + a + 1) & ~1) * sizeof(double)), bar);
     }
-    base += pj * pitch;
   }
 }
 
 __global__ void __launch_bounds__(kFThreads) k_fused_normal(FusedArgs A) {
   extern __shared__ __align__(128) double fsm[];
   double* bufs[2] = {fsm, fsm + kFBuf / sizeof(double)};
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t full[2], empty[2];
   __shared__ double y[kFT];
   __shared__ double ypart[kFSlots][kFT];
   __shared__ Tile cur;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncw = (blockDim.x >> 5) - 1;  // compute warps (warp 0 produces)
   if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], ncw);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  int it = 0;
-  uint32_t phase[2] = {0, 0};
-  if (warp == 0 && blockIdx.x < A.ntiles) issue_tile(A, A.tiles[blockIdx.x], bufs[0], &bar[0], lane);
-  for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++it) {
-    const int b = it & 1;
-    // prefetch the next tile into the other buffer (its previous contents were consumed)
-    const int nxt = tile + gridDim.x;
-    if (warp == 0 && nxt < A.ntiles) {
+  if (warp == 0) {
+    // ---- producer: keep up to two tiles in flight
+    int it = 0;
+    for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++it) {
+      const int b = it & 1;
+      if (it >= 2) mbar_wait(&empty[b], ((it >> 1) - 1) & 1);  // consumers released this buffer
       if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      issue_tile(A, A.tiles[nxt], bufs[b ^ 1], &bar[b ^ 1], lane);
+      issue_tile(A, A.tiles + tile, bufs[b], &full[b], lane);
     }
-    if (threadIdx.x < static_cast<int>(sizeof(Tile) / sizeof(int)))
-      reinterpret_cast<int*>(&cur)[threadIdx.x] = reinterpret_cast<const int*>(&A.tiles[tile])[threadIdx.x];
-    mbar_wait(&bar[b], phase[b]);
-    phase[b] ^= 1u;
-    __syncthreads();
+    return;
+  }
+  // ---- consumers (warps 1..ncw), named barrier 1 among them
+  const int ctid = threadIdx.x - 32, cthr = ncw * 32;
+  int it = 0;
+  for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++it) {
+    const int b = it & 1;
+    for (int q = ctid; q < static_cast<int>(sizeof(Tile) / sizeof(int)); q += cthr)
+      reinterpret_cast<int*>(&cur)[q] = reinterpret_cast<const int*>(A.tiles + tile)[q];
+    mbar_wait(&full[b], (it >> 1) & 1);
+    asm volatile("bar.sync 1, %0;" ::"r"(cthr) : "memory");
     const double* buf = bufs[b];
-    // slot bases inside the buffer
-    __shared__ int sbase[kFSlots], sc0[kFSlots], spj[kFSlots], srows[kFSlots];
-    __shared__ long long shoff[kFSlots];
-    if (threadIdx.x == 0) {
-      int base = 0;
-      for (int s = 0; s < cur.ns; ++s) {
-        const int j = cur.s[s].blk;
-        sbase[s] = base;
-        sc0[s] = A.col_off[j];
-        spj[s] = A.col_off[j + 1] - A.col_off[j];
-        srows[s] = A.row_ptr[j + 1] - A.row_ptr[j];
-        shoff[s] = A.H_off[j];
-        base += spj[s] * seg_pitch(cur.s[s].len);
-      }
-    }
-    __syncthreads();
+    const int ns = cur.ns;
     // y partials: thread per (slot, point in slot)
-    for (int e = threadIdx.x; e < cur.ns * kFT; e += blockDim.x) {
+    for (int e = ctid; e < ns * kFT; e += cthr) {
       const int s = e / kFT, tt = e % kFT;
       const TileSlot& S = cur.s[s];
       if (tt >= S.len) continue;
-      const int pitch = seg_pitch(S.len), pj = spj[s], rows = srows[s];
-      const double* seg = buf + sbase[s] + tt;
-      const double* ww = A.w + sc0[s];
-      const long long idx0 = shoff[s] + S.ra;
+      const int pitch = seg_pitch(S.len), pj = S.pj;
+      const int par0 = static_cast<int>(S.src & 1), rodd = S.rows & 1;
+      const double* seg = buf + S.base + tt;
+      const double* ww = A.w + S.c0;
       double a0 = 0.0, a1 = 0.0;
       int k = 0;
       for (; k + 2 <= pj; k += 2) {
-        const int al0 = static_cast<int>((idx0 + static_cast<long long>(k) * rows) & 1);
-        const int al1 = static_cast<int>((idx0 + static_cast<long long>(k + 1) * rows) & 1);
-        a0 += seg[k * pitch + al0] * ww[k];
-        a1 += seg[(k + 1) * pitch + al1] * ww[k + 1];
+        a0 += seg[k * pitch + par0] * ww[k];
+        a1 += seg[(k + 1) * pitch + (par0 ^ rodd)] * ww[k + 1];
       }
-      if (k < pj) a0 += seg[k * pitch + static_cast<int>((idx0 + static_cast<long long>(k) * rows) & 1)] * ww[k];
+      if (k < pj) a0 += seg[k * pitch + (par0 ^ (k & rodd))] * ww[k];
       ypart[s][S.ta + tt] = a0 + a1;
     }
-    __syncthreads();
-    for (int t = threadIdx.x; t < cur.npts; t += blockDim.x) {
+    asm volatile("bar.sync 1, %0;" ::"r"(cthr) : "memory");
+    for (int t = ctid; t < cur.npts; t += cthr) {
       double acc = 0.0;
-      for (int s = 0; s < cur.ns; ++s)  // slots ascend by block: the reference's per-row order
+      for (int s = 0; s < ns; ++s)  // slots ascend by block: the reference's per-row order
         if (t >= cur.s[s].ta && t < cur.s[s].ta + cur.s[s].len) acc += ypart[s][t];
       y[t] = acc;
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"r"(cthr) : "memory");
     // Hᵀy partials: warp per (slot, column), lanes over the slot's points
-    int total = 0;
-    for (int s = 0; s < cur.ns; ++s) total += spj[s];
-    for (int q = warp; q < total; q += nw) {
-      int s = 0, k = q;
-      while (k >= spj[s]) {
-        k -= spj[s];
-        ++s;
-      }
+    const int cw = warp - 1;
+    long long po = cur.poff;
+    for (int s = 0; s < ns; ++s) {
       const TileSlot& S = cur.s[s];
-      const int al = static_cast<int>((shoff[s] + S.ra + static_cast<long long>(k) * srows[s]) & 1);
-      const double* seg = buf + sbase[s] + k * seg_pitch(S.len) + al;
-      double acc = 0.0;
-      for (int tt = lane; tt < S.len; tt += 32) acc += seg[tt] * y[S.ta + tt];
-      acc = warp_sum(acc);
-      if (lane == 0) {
-        long long po = cur.poff;
-        for (int s2 = 0; s2 < s; ++s2) po += spj[s2];
-        A.part[po + k] = acc;
+      const int pitch = seg_pitch(S.len);
+      const int par0 = static_cast<int>(S.src & 1), rodd = S.rows & 1;
+      for (int k = cw; k < S.pj; k += ncw) {
+        const double* seg = buf + S.base + k * pitch + (par0 ^ (k & rodd));
+        double acc = 0.0;
+        for (int tt = lane; tt < S.len; tt += 32) acc += seg[tt] * y[S.ta + tt];
+        acc = warp_sum(acc);
+        if (lane == 0) A.part[po + k] = acc;
       }
+      po += S.pj;
     }
-    __syncthreads();  // buffer b free for the prefetch issued in the next-but-one iteration
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(&empty[b])) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(cthr) : "memory");  // `cur`, y, ypart reusable
   }
 }
 
@@ -351,7 +332,7 @@ bool build_fused_plan(Ctx& c) {
             ok = false;
             break;
           }
-          U.s[U.ns++] = {b, t, 1, r};
+          U.s[U.ns++] = TileSlot{b, t, 1, r, 0, 0, 0, 0, 0};
         } else {
           TileSlot& S = U.s[s];
           if (S.ta + S.len != t || S.ra + S.len != r) ok = false;  // contiguity in tile and rows
@@ -370,6 +351,23 @@ bool build_fused_plan(Ctx& c) {
     // slots in ascending block order (the reference's per-row summation order)
     std::sort(T.s, T.s + T.ns, [](const TileSlot& a, const TileSlot& b) { return a.blk < b.blk; });
     T.poff = poff;
+    long long tx = 0;
+    int base = 0;
+    for (int z = 0; z < T.ns; ++z) {
+      TileSlot& S = T.s[z];
+      const int j = S.blk;
+      S.pj = c.h_p[j];
+      S.rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+      S.c0 = c.h_col_off[j];
+      S.base = base;
+      S.src = c.H_off[j] + S.ra;
+      base += S.pj * seg_pitch_h(S.len);
+      for (int k = 0; k < S.pj; ++k) {
+        const int a = static_cast<int>((S.src + static_cast<long long>(k) * S.rows) & 1);
+        tx += ((S.len + a + 1) & ~1) * 8;
+      }
+    }
+    T.tx_bytes = static_cast<int>(tx);
     for (int z = 0; z < T.ns; ++z) {
       per_block[T.s[z].blk].push_back(poff);
       poff += c.h_p[T.s[z].blk];

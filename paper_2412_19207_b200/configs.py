@@ -15,7 +15,7 @@ def c1(**kw) -> A.Config:
     """2-D Poisson, 4x4 subdomains, m=200, 40x40 per subdomain + 4x160 boundary points."""
     args = dict(decomposition=A.DECOMP_CELL, delta=0.1, boundary_per_edge=160, test=[350, 350],
                 tau_mode=A.TAU_RELATIVE, tau=1e-6, pca_matrix=A.PCA_OP_APPLIED,
-                solver=A.SOLVER_CG, precond=A.PRECOND_AS, rel_tol=1e-10, seed=1000, op_form=A.OPERATOR_FUSED)
+                solver=A.SOLVER_CG, precond=A.PRECOND_AS, rel_tol=1e-10, seed=1000, op_form=A.OPERATOR_TWO_PASS)
     args.update(kw)
     return A.make_config(A.PROBLEM_POISSON, [4, 4], 200, [160, 160], dim=2, **args)
 
@@ -24,7 +24,7 @@ def c2(**kw) -> A.Config:
     """2-D multiscale Poisson, 16x16 subdomains, m=300, 60x60 per subdomain (0.92M rows)."""
     args = dict(decomposition=A.DECOMP_CELL, delta=0.1, test=[350, 350], tau_mode=A.TAU_RELATIVE,
                 tau=1e-6, pca_matrix=A.PCA_OP_APPLIED, solver=A.SOLVER_CG, precond=A.PRECOND_AS,
-                rel_tol=1e-10, seed=1000, op_form=A.OPERATOR_FUSED)
+                rel_tol=1e-10, seed=1000, op_form=A.OPERATOR_TWO_PASS)
     args.update(kw)
     return A.make_config(A.PROBLEM_MULTISCALE, [16, 16], 300, [960, 960], **args)
 
@@ -33,7 +33,7 @@ def c3(**kw) -> A.Config:
     """2-D heat equation in space-time, 8x8x8 subdomains, m=300, 16^3 per subdomain; RAS-GMRES(50)."""
     args = dict(decomposition=A.DECOMP_CELL, delta=0.1, test=[50, 50, 50], tau_mode=A.TAU_RELATIVE,
                 tau=1e-6, pca_matrix=A.PCA_OP_APPLIED, solver=A.SOLVER_GMRES, precond=A.PRECOND_RAS,
-                gmres_restart=50, rel_tol=1e-10, seed=1000, op_form=A.OPERATOR_FUSED)
+                gmres_restart=50, rel_tol=1e-10, seed=1000, op_form=A.OPERATOR_TWO_PASS)
     args.update(kw)
     return A.make_config(A.PROBLEM_HEAT, [8, 8, 8], 300, [128, 128, 128], **args)
 
@@ -42,7 +42,7 @@ def c4(**kw) -> A.Config:
     """1-D advection in space-time on [0,2]x[0,1], 64x16 subdomains, m=250; RAS-GMRES(50)."""
     args = dict(decomposition=A.DECOMP_CELL, delta=0.1, test=[350, 350], tau_mode=A.TAU_RELATIVE,
                 tau=1e-6, pca_matrix=A.PCA_OP_APPLIED, solver=A.SOLVER_GMRES, precond=A.PRECOND_RAS,
-                gmres_restart=50, rel_tol=1e-10, seed=1000, op_form=A.OPERATOR_FUSED)
+                gmres_restart=50, rel_tol=1e-10, seed=1000, op_form=A.OPERATOR_TWO_PASS)
     args.update(kw)
     return A.make_config(A.PROBLEM_ADVECTION, [64, 16], 250, [2560, 640], **args)
 
@@ -51,7 +51,7 @@ def c5(counts=(8, 8, 8), per=20, **kw) -> A.Config:
     """3-D Poisson, 8x8x8 subdomains (or the 2x2x2 C5s slice), m=400, 20^3 per subdomain."""
     args = dict(decomposition=A.DECOMP_CELL, delta=0.1, test=[50, 50, 50], tau_mode=A.TAU_RELATIVE,
                 tau=1e-6, pca_matrix=A.PCA_OP_APPLIED, solver=A.SOLVER_CG, precond=A.PRECOND_AS,
-                rel_tol=1e-10, seed=1000, op_form=A.OPERATOR_FUSED)
+                rel_tol=1e-10, seed=1000, op_form=A.OPERATOR_TWO_PASS)
     args.update(kw)
     return A.make_config(A.PROBLEM_POISSON, list(counts), 400, [c * per for c in counts], dim=3, **args)
 

@@ -57,6 +57,7 @@ static void reset_state(Ctx& c) {
   c.sum = rdd_summary{};
   c.H = nullptr;
   c.fused_ready = false;
+  c.mt_groups = 0;
 }
 
 // runner.hpp:40-70

@@ -134,6 +134,10 @@ struct Ctx {
   std::vector<int> iters, conv, brk;
   DBuf<double> W;                     // p x C (unscaled)
   DBuf<double> ytmp;                  // N
+  // Hᵀ·r work list (block, column group)
+  DBuf<int> mt_blk, mt_k0;
+  int mt_groups = 0;
+  size_t mt_smem = 0;
   // fused single-pass normal operator plan
   DBuf<int> f_bptr;
   DBuf<unsigned char> f_tiles;

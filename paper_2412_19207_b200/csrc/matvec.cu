@@ -33,69 +33,41 @@ __global__ void k_colnorm_scale(double* __restrict__ H, const long long* __restr
     for (int r = lane; r < rows; r += 32) h[r] = h[r] / s;
 }
 
-__global__ void __launch_bounds__(256) k_matvec(const double* __restrict__ H, const long long* __restrict__ H_off,
-                                                const int* __restrict__ row_ptr, const int* __restrict__ col_off,
-                                                const int* __restrict__ cov_n, const int* __restrict__ cov_j,
-                                                const int* __restrict__ cov_r, int maxcov, int N,
-                                                const double* __restrict__ w, double* __restrict__ y) {
+__global__ void k_matvec(const double* __restrict__ H, const long long* __restrict__ H_off,
+                         const int* __restrict__ row_ptr, const int* __restrict__ col_off,
+                         const int* __restrict__ cov_n, const int* __restrict__ cov_j, const int* __restrict__ cov_r,
+                         int maxcov, int N, const double* __restrict__ w, double* __restrict__ y) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   double acc = 0.0;
   const int nc = cov_n[i];
-  for (int s = 0; s < nc; ++s) {  // ascending covering block: the reference's scatter order
+  for (int s = 0; s < nc; ++s) {
     const int j = cov_j[static_cast<size_t>(i) * maxcov + s];
     const int r = cov_r[static_cast<size_t>(i) * maxcov + s];
     const int rows = row_ptr[j + 1] - row_ptr[j];
     const int c0 = col_off[j], pj = col_off[j + 1] - c0;
     const double* h = H + H_off[j] + r;
-    const double* ww = w + c0;
-    // 8 independent streams keep enough loads in flight per thread (column-major: each is a
-    // coalesced 256-byte segment across the warp)
-    double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int k = 0;
-    for (; k + 8 <= pj; k += 8) {
-      double hv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) hv[u] = __ldcs(h + static_cast<long long>(k + u) * rows);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) a[u] += hv[u] * __ldg(ww + k + u);
-    }
-    for (; k < pj; ++k) a[0] += __ldcs(h + static_cast<long long>(k) * rows) * __ldg(ww + k);
-    acc += ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    double t = 0.0;
+    for (int k = 0; k < pj; ++k) t += h[static_cast<long long>(k) * rows] * w[c0 + k];
+    acc += t;
   }
   y[i] = acc;
 }
 
-// out_j = H_jᵀ y[rows_j]: one CTA per (block, group of kColsPerCta columns); the gathered y_j is
-// staged once in shared memory, each warp streams whole columns (coalesced) against it
-constexpr int kColsPerCta = 16;
-__global__ void __launch_bounds__(256) k_matvec_t(const double* __restrict__ H, const long long* __restrict__ H_off,
-                                                  const int* __restrict__ row_ptr, const int* __restrict__ row_idx,
-                                                  const int* __restrict__ col_off, const int* __restrict__ grp_blk,
-                                                  const int* __restrict__ grp_k0, const double* __restrict__ r,
-                                                  double* __restrict__ out) {
-  extern __shared__ double yj[];
-  const int j = grp_blk[blockIdx.x], k0 = grp_k0[blockIdx.x];
+__global__ void k_matvec_t(const double* __restrict__ H, const long long* __restrict__ H_off,
+                           const int* __restrict__ row_ptr, const int* __restrict__ row_idx,
+                           const int* __restrict__ col_off, const int* __restrict__ col_owner, int p,
+                           const double* __restrict__ r, double* __restrict__ out) {
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (col >= p) return;
+  const int j = col_owner[col];
+  const int k = col - col_off[j];
   const int r0 = row_ptr[j], rows = row_ptr[j + 1] - r0;
-  const int c0 = col_off[j], pj = col_off[j + 1] - c0;
-  for (int q = threadIdx.x; q < rows; q += blockDim.x) yj[q] = __ldg(r + row_idx[r0 + q]);
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int kend = min(pj, k0 + kColsPerCta);
-  for (int k = k0 + warp; k < kend; k += nw) {
-    const double* h = H + H_off[j] + static_cast<long long>(k) * rows;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int q = lane;
-    for (; q + 96 < rows; q += 128) {
-      a0 += __ldcs(h + q) * yj[q];
-      a1 += __ldcs(h + q + 32) * yj[q + 32];
-      a2 += __ldcs(h + q + 64) * yj[q + 64];
-      a3 += __ldcs(h + q + 96) * yj[q + 96];
-    }
-    for (; q < rows; q += 32) a0 += __ldcs(h + q) * yj[q];
-    const double s = warp_sum((a0 + a1) + (a2 + a3));
-    if (lane == 0) out[c0 + k] = s;
-  }
+  const double* h = H + H_off[j] + static_cast<long long>(k) * rows;
+  double s = 0.0;
+  for (int q = lane; q < rows; q += 32) s += h[q] * r[row_idx[r0 + q]];
+  s = warp_sum(s);
+  if (lane == 0) out[col] = s;
 }
 
 }  // namespace
@@ -126,25 +98,8 @@ void matvec_dev(Ctx& c, const double* w, double* y) {
 
 void matvec_t_dev(Ctx& c, const double* r, double* out) {
   ScopedKernelTimer tk(c, "matvec_t");
-  if (c.mt_groups == 0) {  // (block, column group) work list, once per assembled system
-    std::vector<int> gb, gk;
-    int rmax = 0;
-    for (int j = 0; j < c.J; ++j) {
-      for (int k0 = 0; k0 < c.h_p[j]; k0 += kColsPerCta) {
-        gb.push_back(j);
-        gk.push_back(k0);
-      }
-      rmax = std::max(rmax, c.h_row_ptr[j + 1] - c.h_row_ptr[j]);
-    }
-    c.mt_blk.upload(gb, c.stream);
-    c.mt_k0.upload(gk, c.stream);
-    c.mt_groups = static_cast<int>(gb.size());
-    c.mt_smem = static_cast<size_t>(rmax) * sizeof(double);
-    if (c.mt_smem > 48 * 1024)
-      RDD_CUDA(cudaFuncSetAttribute(k_matvec_t, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.mt_smem)));
-  }
-  k_matvec_t<<<c.mt_groups, 256, c.mt_smem, c.stream>>>(c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p,
-                                                        c.mt_blk.p, c.mt_k0.p, r, out);
+  k_matvec_t<<<ceil_div(static_cast<long long>(c.p) * 32, 256), 256, 0, c.stream>>>(
+      c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p, c.downer.p, c.p, r, out);
   RDD_LAUNCH_CHECK();
 }
 

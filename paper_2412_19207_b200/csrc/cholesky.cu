@@ -181,6 +181,16 @@ __global__ void k_power(const double* __restrict__ A, const Mat* __restrict__ ma
   if (threadIdx.x == 0) out[blockIdx.x] = lam;
 }
 
+// copy the lower triangle onto the upper one
+__global__ void k_mirror_lower(double* __restrict__ P, const Mat* __restrict__ mats) {
+  const Mat M = mats[blockIdx.x];
+  double* a = P + M.off;
+  for (long long e = threadIdx.x; e < static_cast<long long>(M.n) * M.n; e += blockDim.x) {
+    const int r = static_cast<int>(e % M.n), cc = static_cast<int>(e / M.n);
+    if (r < cc) a[e] = a[cc + static_cast<long long>(r) * M.n];
+  }
+}
+
 }  // namespace
 
 std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int>& n,
@@ -213,7 +223,9 @@ std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int
 // Out: P = A^{-1} (full, same layout); fail[i] = 1 when a pivot was not positive;
 // frob_A[i], frob_P[i] Frobenius norms (cond(A) <= ||A||_F ||A^{-1}||_F).
 void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n, const std::vector<long long>& off,
-                         std::vector<int>& fail, std::vector<double>& frob_A, std::vector<double>& frob_P) {
+                         std::vector<int>& fail, std::vector<double>& frob_A, std::vector<double>& frob_P,
+                         const std::vector<long long>* offP_in) {
+  const std::vector<long long>& offP = offP_in ? *offP_in : off;
   ScopedKernelTimer tk(c, "spd_inverse");
   const int B = static_cast<int>(n.size());
   fail.assign(B, 0);
@@ -311,17 +323,18 @@ void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n
       double* L = A + off[i];
       double* Mm = Mi.p + off[i];
       for (int tn = 0; tn < ib; ++tn) {
-        GemmTask t{};  // tmp = L[ib, 0:w] M[0:w, 0:w]
-        t.A = L + ib * NB;
-        t.B = Mm;
-        t.Cm = tmp.p + toff[i];
+        GemmTask t{};  // tmp[:, tn] = L[ib, tn*64:w] M[tn*64:w, tn]  (M is lower triangular)
+        const int k0 = tn * NB;
+        t.A = L + ib * NB + static_cast<long long>(k0) * n[i];
+        t.B = Mm + k0 + static_cast<long long>(k0) * n[i];
+        t.Cm = tmp.p + toff[i] + static_cast<long long>(k0) * NB;
         t.M = bi;
-        t.N = w;
-        t.K = w;
+        t.N = NB;
+        t.K = w - k0;
         t.lda = n[i];
         t.ldb = n[i];
         t.ldc = NB;
-        t.tn = tn;
+        t.tn = 0;
         t.alpha = 1.0;
         g1.push_back(t);
         GemmTask u{};  // M[ib, 0:w] = -M_ii tmp
@@ -342,16 +355,18 @@ void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n
     gemm_nn(c, g1);
     gemm_nn(c, g2);
   }
-  // ---- P = Mᵀ M
+  // ---- P = Mᵀ M, lower tiles only (M(k, i) = 0 for k < i), then mirrored
   std::vector<GemmTask> g;
   for (int i = 0; i < B; ++i)
     for (int tm = 0; tm < ceil_div(n[i], 64); ++tm)
-      for (int tn = 0; tn < ceil_div(n[i], 64); ++tn) {
+      for (int tn = 0; tn <= tm; ++tn) {
         GemmTask t{};
-        t.A = Mi.p + off[i];
-        t.B = Mi.p + off[i];
-        t.Cm = P + off[i];
-        t.M = t.N = t.K = n[i];
+        const int k0 = tm * 64;  // rows of M below the tile's first output row
+        t.A = Mi.p + off[i] + k0;
+        t.B = Mi.p + off[i] + k0;
+        t.Cm = P + offP[i];
+        t.M = t.N = n[i];
+        t.K = n[i] - k0;
         t.lda = t.ldb = t.ldc = n[i];
         t.tm = tm;
         t.tn = tn;
@@ -359,6 +374,15 @@ void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n
         g.push_back(t);
       }
   gemm_tn(c, g);
+  {
+    std::vector<Mat> pm(B);
+    for (int i = 0; i < B; ++i) pm[i] = {offP[i], n[i]};
+    DBuf<Mat> dpm;
+    dpm.upload(pm, c.stream);
+    k_mirror_lower<<<B, 256, 0, c.stream>>>(P, dpm.p);
+    RDD_LAUNCH_CHECK();
+    dm.upload(pm, c.stream);  // Frobenius norms of the outputs
+  }
   k_frob<<<B, 256, 0, c.stream>>>(P, dm.p, dfp.p);
   RDD_LAUNCH_CHECK();
   dfail.download(fail.data(), B, c.stream);

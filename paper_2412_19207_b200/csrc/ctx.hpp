@@ -218,6 +218,8 @@ void build_schwarz(Ctx& c, int kind);
 void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose);
 void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, const std::vector<long long>& off);
 void refresh_local_cond(Ctx& c);
+size_t device_available(Ctx& c);
+void release_scratch(Ctx& c);
 // krylov.cu (K12/K13)
 void solve_all(Ctx& c, int solver, double tol, int max_iter, int restart);
 // evaluate.cu (K14)
@@ -241,7 +243,8 @@ void project_blocks(Ctx& c);
 void ensure_col_owner(Ctx& c);
 // cholesky.cu
 void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n, const std::vector<long long>& off,
-                         std::vector<int>& fail, std::vector<double>& frob_A, std::vector<double>& frob_P);
+                         std::vector<int>& fail, std::vector<double>& frob_A, std::vector<double>& frob_P,
+                         const std::vector<long long>* offP = nullptr);
 std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int>& n,
                                   const std::vector<long long>& off, int iters);
 // jacobi.cu

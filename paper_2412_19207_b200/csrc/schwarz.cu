@@ -122,6 +122,29 @@ __global__ void k_reduce(const double* __restrict__ z, const int* __restrict__ g
 
 }  // namespace
 
+// bytes the device can still hand out: free memory plus blocks cached (unused) in the pool
+size_t device_available(Ctx& c) {
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  cudaMemPool_t pool;
+  uint64_t reserved = 0, used = 0;
+  if (cudaDeviceGetDefaultMemPool(&pool, c.device) == cudaSuccess) {
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+  }
+  return fr + static_cast<size_t>(reserved > used ? reserved - used : 0);
+}
+
+// drop the large PCA scratch (T, rotation logs, Jacobi work) and the unreduced samples S once H
+// is assembled; the next build re-creates them
+void release_scratch(Ctx& c) {
+  for (const char* k : {"pca.T", "syevj.rot", "syevj.Vp", "syevj.Wk", "pca.G", "pca.V0", "pca.W", "pca.Vfull"}) {
+    auto it = c.wsd.find(k);
+    if (it != c.wsd.end()) it->second.release();
+  }
+  if (!c.identity_V) c.S.release();
+}
+
 // Gather A_i for the subdomains in `which` into a compact batch at offsets `off` (zero-filled).
 void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, const std::vector<long long>& off) {
   long long tot = 0;
@@ -245,16 +268,41 @@ void build_schwarz(Ctx& c, int kind) {
       }
   }
   c.dP_off.upload(c.P_off, c.stream);
-  DBuf<double>& A = c.wsd["schwarz.A"];
-  std::vector<int> all(J);
-  for (int i = 0; i < J; ++i) all[i] = i;
-  std::vector<long long> offA(c.P_off.begin(), c.P_off.end() - 1);
-  gather_locals(c, all, A, offA);
-  // A_i^{-1} by Cholesky (equal to the reference's pseudo-inverse when A_i is safely full rank)
+  // memory: P (all subdomains) + a chunk workspace (A, L^{-1}, tmp); free the PCA scratch first
+  // when the device cannot hold both (3-D configs)
+  const size_t p_bytes = static_cast<size_t>(c.P_off[J]) * sizeof(double);
+  if (device_available(c) < p_bytes + (size_t(8) << 30)) release_scratch(c);
   c.P.ensure(std::max<long long>(1, c.P_off[J]));
-  std::vector<int> fail;
-  std::vector<double> fa, fp;
-  batched_spd_inverse(c, A.p, c.P.p, n, offA, fail, fa, fp);
+  const size_t budget = std::min<size_t>(size_t(24) << 30, std::max<size_t>(size_t(1) << 30, (device_available(c) * 2) / 5));
+  std::vector<int> fail(J, 0);
+  std::vector<double> fa(J, 0.0), fp(J, 0.0);
+  for (int i0 = 0; i0 < J;) {
+    std::vector<int> chunk;
+    std::vector<long long> coff, goff;
+    std::vector<int> cn;
+    long long used = 0;
+    int i = i0;
+    for (; i < J; ++i) {
+      const long long sz = static_cast<long long>(n[i]) * n[i];
+      if (!chunk.empty() && static_cast<size_t>(used + sz) * sizeof(double) * 3 > budget) break;
+      chunk.push_back(i);
+      coff.push_back(used);
+      goff.push_back(c.P_off[i]);
+      cn.push_back(n[i]);
+      used += sz;
+    }
+    DBuf<double>& A = c.wsd["schwarz.A"];
+    gather_locals(c, chunk, A, coff);
+    std::vector<int> f;
+    std::vector<double> a, b;
+    batched_spd_inverse(c, A.p, c.P.p, cn, coff, f, a, b, &goff);
+    for (size_t q = 0; q < chunk.size(); ++q) {
+      fail[chunk[q]] = f[q];
+      fa[chunk[q]] = a[q];
+      fp[chunk[q]] = b[q];
+    }
+    i0 = i;
+  }
   c.local_rank.assign(J, 0);
   c.local_cond.assign(J, 0.0);
   c.local_cond_exact = false;

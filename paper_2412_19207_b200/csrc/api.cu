@@ -1,3 +1,4 @@
+#include <cstdio>
 // api.cu — the C ABI (include/rdd.h) and the run_single orchestration (runner.hpp:202-275).
 //
 // Error mapping mirrors the reference's exception classes: std::invalid_argument -> 1,
@@ -103,8 +104,10 @@ static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed, bool reside
   }
   RDD_CUDA(cudaStreamSynchronize(c.stream));
   const double t_pca = now_s() - t0;
+  if (c.verbose) std::fprintf(stderr, "[phase] instance+pca %.3f s (J=%d p=%d N=%d)\n", t_pca, c.J, c.p, c.N);
   assemble(c, cfg.precond >= 0);
   const double t_asm = now_s() - t0;
+  if (c.verbose) std::fprintf(stderr, "[phase] assemble done %.3f s\n", t_asm);
   double t_pre = 0.0;
   if (cfg.solver == RDD_SOLVER_QR) throw std::invalid_argument("qr_direct is a host baseline (oracle), not a device path");
   if (cfg.precond >= 0) {
@@ -113,12 +116,14 @@ static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed, bool reside
     build_schwarz(c, cfg.precond);
     RDD_CUDA(cudaStreamSynchronize(c.stream));
     t_pre = now_s() - t0;
+    if (c.verbose) std::fprintf(stderr, "[phase] precond %.3f s (fallback %d)\n", t_pre, c.n_fallback);
   } else if (cfg.op_form == RDD_OPERATOR_NORMAL) {
     build_normal_blocks(c);
   }
   t0 = now_s();
   solve_all(c, cfg.solver, cfg.rel_tol, cfg.max_iter, cfg.gmres_restart);
   const double t_sol = now_s() - t0;
+  if (c.verbose) std::fprintf(stderr, "[phase] solve %.3f s (%d its)\n", t_sol, c.iters.empty() ? 0 : c.iters[0]);
   t0 = now_s();
   evaluate(c, cfg.test);
   const double t_ev = now_s() - t0;

@@ -117,7 +117,8 @@ struct Ctx {
   DBuf<int> gat_ptr, gat_pos, gat_owner_pos;
   int nmax_local = 0;
   int n_fallback = 0;                 // local blocks that took the eigen pseudo-inverse
-  std::vector<int> fallback, local_n;
+  std::vector<int> fallback, local_n, own_pos;  // own_pos: offset of block i's columns inside S_i
+  DBuf<int> down_pos;
   bool local_cond_exact = false;
   struct GatherTask {
     int i, j1, j2, o1, o2;

@@ -120,6 +120,55 @@ __global__ void k_reduce(const double* __restrict__ z, const int* __restrict__ g
   out[col] = s;
 }
 
+// copy rows [r0, r0+nr) of each n x n matrix (column-major) into an nr x n column-major block
+__global__ void k_store_rows(const double* __restrict__ Pc, const long long* __restrict__ src,
+                             const int* __restrict__ n, const int* __restrict__ r0, const int* __restrict__ nr,
+                             double* __restrict__ P, const long long* __restrict__ dst) {
+  const int q = blockIdx.x;
+  const int nn = n[q], rr = nr[q], a = r0[q];
+  const double* s = Pc + src[q];
+  double* d = P + dst[q];
+  for (long long e = threadIdx.x; e < static_cast<long long>(rr) * nn; e += blockDim.x) {
+    const int r = static_cast<int>(e % rr), cc = static_cast<int>(e / rr);
+    d[e] = s[(a + r) + static_cast<long long>(cc) * nn];
+  }
+}
+
+// RAS (schwarz.hpp:178-181): out[own_i] = A_i⁺[own, :] v[S_i]; each column has exactly one owner
+__global__ void k_ras_apply(const double* __restrict__ P, const long long* __restrict__ P_off,
+                            const int* __restrict__ set_ptr, const int* __restrict__ set_idx,
+                            const int* __restrict__ col_off, const double* __restrict__ v, double* __restrict__ out) {
+  extern __shared__ double g[];
+  const int i = blockIdx.y;
+  const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0;
+  const int c0 = col_off[i], pi = col_off[i + 1] - c0;
+  const int r0 = blockIdx.x * blockDim.x;
+  if (r0 >= pi) return;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) g[c] = v[set_idx[s0 + c]];
+  __syncthreads();
+  const int r = r0 + threadIdx.x;
+  if (r >= pi) return;
+  const double* Pi = P + P_off[i] + r;
+  double acc = 0.0;
+  for (int c = 0; c < n; ++c) acc += Pi[static_cast<long long>(c) * pi] * g[c];
+  out[c0 + r] = acc;
+}
+
+// RAS transpose (schwarz.hpp:189-215): z_i = A_i⁺[own, :]ᵀ v[own_i], then the AS-style sum
+__global__ void k_ras_apply_t(const double* __restrict__ P, const long long* __restrict__ P_off,
+                              const int* __restrict__ set_ptr, const int* __restrict__ col_off,
+                              const double* __restrict__ v, double* __restrict__ z) {
+  const int i = blockIdx.y;
+  const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0;
+  const int c0 = col_off[i], pi = col_off[i + 1] - c0;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const double* col = P + P_off[i] + static_cast<long long>(c) * pi;
+  double acc = 0.0;
+  for (int r = 0; r < pi; ++r) acc += col[r] * v[c0 + r];
+  z[s0 + c] = acc;
+}
+
 }  // namespace
 
 // bytes the device can still hand out: free memory plus blocks cached (unused) in the pool
@@ -185,7 +234,7 @@ void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, con
 // local_cond as the reference reports it (λmax/λmin of the kept spectrum), by power iteration
 // on A_i and A_i^{-1}; computed on demand (the rank decision only needs the cheap bound).
 void refresh_local_cond(Ctx& c) {
-  if (c.local_cond_exact || c.pkind < 0) return;
+  if (c.local_cond_exact || c.pkind < 0 || c.pkind == RDD_PRECOND_RAS) return;  // RAS keeps owner panels only
   std::vector<int> which;
   for (int i = 0; i < c.J; ++i)
     if (std::find(c.fallback.begin(), c.fallback.end(), i) == c.fallback.end()) which.push_back(i);
@@ -248,15 +297,15 @@ void build_schwarz(Ctx& c, int kind) {
   c.zloc.ensure(std::max<size_t>(1, c.set_idx.size()));
 
   // local matrix sizes and gather plan (schwarz.hpp:112-130): A_i blocks come from NB
-  c.P_off.assign(J + 1, 0);
-  for (int i = 0; i < J; ++i) c.P_off[i + 1] = c.P_off[i] + static_cast<long long>(n[i]) * n[i];
   c.local_n = n;
+  c.own_pos.assign(J, 0);
   c.gat_tasks.clear();
   for (int i = 0; i < J; ++i) {
     std::vector<std::pair<int, int>> parts;
     int o = 0;
     for (int q = c.nbr_ptr[i]; q < c.nbr_ptr[i + 1]; ++q) {
       const int j = c.nbr_idx[q];
+      if (j == i) c.own_pos[i] = o;
       parts.push_back({j, o});
       o += c.h_p[j];
     }
@@ -267,146 +316,180 @@ void build_schwarz(Ctx& c, int kind) {
         c.gat_tasks.push_back({i, j1, j2, o1, o2, c.nb_off[it->second]});
       }
   }
+  // storage of the local operators: AS/SAS the full A_i⁺ (n_i x n_i); RAS only the owner rows
+  // A_i⁺[own, :] (p_i x n_i, column-major) — all the restricted apply reads (schwarz.hpp:178-181)
+  const bool ras = kind == RDD_PRECOND_RAS;
+  c.P_off.assign(J + 1, 0);
+  for (int i = 0; i < J; ++i)
+    c.P_off[i + 1] = c.P_off[i] + static_cast<long long>(ras ? c.h_p[i] : n[i]) * n[i];
   c.dP_off.upload(c.P_off, c.stream);
-  // memory: P (all subdomains) + a chunk workspace (A, L^{-1}, tmp); free the PCA scratch first
-  // when the device cannot hold both (3-D configs)
   const size_t p_bytes = static_cast<size_t>(c.P_off[J]) * sizeof(double);
   if (device_available(c) < p_bytes + (size_t(8) << 30)) release_scratch(c);
   c.P.ensure(std::max<long long>(1, c.P_off[J]));
-  const size_t budget = std::min<size_t>(size_t(24) << 30, std::max<size_t>(size_t(1) << 30, (device_available(c) * 2) / 5));
-  std::vector<int> fail(J, 0);
-  std::vector<double> fa(J, 0.0), fp(J, 0.0);
+  // per chunk: A (destroyed by Cholesky), A0 copy, Pc (full inverses), L^{-1}, tmp
+  const size_t budget =
+      std::min<size_t>(size_t(32) << 30, std::max<size_t>(size_t(1) << 30, (device_available(c) * 2) / 5));
+  c.local_rank.assign(J, 0);
+  c.local_cond.assign(J, 0.0);
+  c.local_cond_exact = false;
+  c.fallback.clear();
+  std::vector<int> hown(J);
+  for (int i = 0; i < J; ++i) hown[i] = c.own_pos[i];
   for (int i0 = 0; i0 < J;) {
-    std::vector<int> chunk;
-    std::vector<long long> coff, goff;
-    std::vector<int> cn;
+    std::vector<int> chunk, cn;
+    std::vector<long long> coff;
     long long used = 0;
     int i = i0;
     for (; i < J; ++i) {
       const long long sz = static_cast<long long>(n[i]) * n[i];
-      if (!chunk.empty() && static_cast<size_t>(used + sz) * sizeof(double) * 3 > budget) break;
+      if (!chunk.empty() && static_cast<size_t>(used + sz) * sizeof(double) * 5 > budget) break;
       chunk.push_back(i);
       coff.push_back(used);
-      goff.push_back(c.P_off[i]);
       cn.push_back(n[i]);
       used += sz;
     }
-    DBuf<double>& A = c.wsd["schwarz.A"];
-    gather_locals(c, chunk, A, coff);
-    std::vector<int> f;
-    std::vector<double> a, b;
-    batched_spd_inverse(c, A.p, c.P.p, cn, coff, f, a, b, &goff);
-    for (size_t q = 0; q < chunk.size(); ++q) {
-      fail[chunk[q]] = f[q];
-      fa[chunk[q]] = a[q];
-      fp[chunk[q]] = b[q];
-    }
     i0 = i;
-  }
-  c.local_rank.assign(J, 0);
-  c.local_cond.assign(J, 0.0);
-  c.local_cond_exact = false;
-  std::vector<int> flagged;
-  for (int i = 0; i < J; ++i) {
-    const double bound = fa[i] * fp[i];  // cond(A_i) <= ||A_i||_F ||A_i^{-1}||_F
-    if (fail[i] || !(bound < c.full_rank_cond)) {
-      flagged.push_back(i);
-    } else {
-      c.local_rank[i] = n[i];
-      c.local_cond[i] = bound;
-    }
-  }
-  std::vector<int> fb;  // eigen fallback
-  if (!flagged.empty()) {
-    std::vector<long long> foff;
-    std::vector<int> fn;
-    long long tot = 0;
-    for (int i : flagged) {
-      foff.push_back(tot);
-      fn.push_back(n[i]);
-      tot += static_cast<long long>(n[i]) * n[i];
-    }
-    DBuf<double> Af;
-    gather_locals(c, flagged, Af, foff);
-    const std::vector<double> la = batched_power(c, Af.p, fn, foff, 60);
-    std::vector<long long> poff;
-    for (int i : flagged) poff.push_back(c.P_off[i]);
-    const std::vector<double> lp = batched_power(c, c.P.p, fn, poff, 60);
-    std::vector<int> keep_fn;
-    for (size_t q = 0; q < flagged.size(); ++q) {
-      const int i = flagged[q];
-      const double cond = la[q] * lp[q];
-      if (!fail[i] && cond < c.full_rank_cond) {
-        c.local_rank[i] = n[i];
-        c.local_cond[i] = cond;
-      } else {
-        fb.push_back(i);
+    const int B = static_cast<int>(chunk.size());
+    DBuf<double>& Aw = c.wsd["schwarz.A"];
+    gather_locals(c, chunk, Aw, coff);
+    double* A0 = c.ws("schwarz.A0", used);
+    RDD_CUDA(cudaMemcpyAsync(A0, Aw.p, sizeof(double) * used, cudaMemcpyDeviceToDevice, c.stream));
+    double* Pc = c.ws("schwarz.Pc", used);
+    std::vector<int> fail;
+    std::vector<double> fa, fp;
+    batched_spd_inverse(c, Aw.p, Pc, cn, coff, fail, fa, fp);
+    // rank decision: cond(A_i) <= ||A_i||_F ||A_i^{-1}||_F; refine by power iteration when the
+    // bound does not clear the threshold; failed or rank-deficient blocks take the eigen path
+    std::vector<int> flagged;
+    for (int q = 0; q < B; ++q) {
+      if (fail[q] || !(fa[q] * fp[q] < c.full_rank_cond)) flagged.push_back(q);
+      else {
+        c.local_rank[chunk[q]] = cn[q];
+        c.local_cond[chunk[q]] = fa[q] * fp[q];
       }
     }
-  }
-  c.n_fallback = static_cast<int>(fb.size());
-  if (!fb.empty()) {
-    std::vector<int> fn;
-    std::vector<long long> foff;
-    long long tot = 0;
-    for (int i : fb) {
-      fn.push_back(n[i]);
-      foff.push_back(tot);
-      tot += static_cast<long long>(n[i]) * n[i];
+    std::vector<int> fb;
+    if (!flagged.empty()) {
+      std::vector<int> fnn;
+      std::vector<long long> foff;
+      for (int q : flagged) {
+        fnn.push_back(cn[q]);
+        foff.push_back(coff[q]);
+      }
+      const std::vector<double> la = batched_power(c, A0, fnn, foff, 60);
+      const std::vector<double> lp = batched_power(c, Pc, fnn, foff, 60);
+      for (size_t z = 0; z < flagged.size(); ++z) {
+        const int q = flagged[z];
+        const double cond = la[z] * lp[z];
+        if (!fail[q] && cond < c.full_rank_cond) {
+          c.local_rank[chunk[q]] = cn[q];
+          c.local_cond[chunk[q]] = cond;
+        } else {
+          fb.push_back(q);
+        }
+      }
     }
-    DBuf<double> Af, V, X, lam;
-    gather_locals(c, fb, Af, foff);
-    V.ensure(tot);
-    X.ensure(tot);
-    long long te = 0;
-    std::vector<long long> evo(fb.size());
-    for (size_t q = 0; q < fb.size(); ++q) {
-      evo[q] = te;
-      te += fn[q];
+    if (!fb.empty()) {  // eigen pseudo-inverse with the reference cutoff, written over Pc
+      std::vector<int> fnn;
+      std::vector<long long> foff, evo;
+      long long te = 0;
+      for (int q : fb) {
+        fnn.push_back(cn[q]);
+        foff.push_back(coff[q]);
+        evo.push_back(te);
+        te += cn[q];
+      }
+      double* V = c.ws("schwarz.V", used);
+      double* X = c.ws("schwarz.X", used);
+      double* lam = c.ws("schwarz.lam", te);
+      EigOpts eo;  // backward stable like SelfAdjointEigenSolver; cutoff 1e-12·λmax (schwarz.hpp:82)
+      eo.absolute = 1;
+      eo.tol = 1e-15;
+      eo.floor_rel = 1e-16;
+      eo.conv_rel = 1e-14;
+      eo.max_sweeps = 60;
+      batched_syevj(c, A0, V, lam, fnn, foff, eo);
+      DBuf<long long> devo, dfoff;
+      DBuf<int> drank, dfn;
+      DBuf<double> dcond;
+      devo.upload(evo, c.stream);
+      dfoff.upload(foff, c.stream);
+      dfn.upload(fnn, c.stream);
+      drank.ensure(fb.size());
+      dcond.ensure(fb.size());
+      k_local_scale<<<static_cast<int>(fb.size()), 256, 0, c.stream>>>(V, lam, dfn.p, dfoff.p, devo.p, X, drank.p,
+                                                                       dcond.p);
+      RDD_LAUNCH_CHECK();
+      std::vector<GemmTask> t;
+      for (size_t z = 0; z < fb.size(); ++z)
+        for (int tm = 0; tm < ceil_div(fnn[z], 64); ++tm)
+          for (int tn = 0; tn < ceil_div(fnn[z], 64); ++tn)
+            t.push_back({X + foff[z], V + foff[z], Pc + foff[z], nullptr, nullptr, fnn[z], fnn[z], fnn[z], fnn[z],
+                         fnn[z], fnn[z], tm, tn, 0.0});
+      gemm_nt(c, t);
+      std::vector<int> hr(fb.size());
+      std::vector<double> hc(fb.size());
+      drank.download(hr.data(), fb.size(), c.stream);
+      dcond.download(hc.data(), fb.size(), c.stream);
+      RDD_CUDA(cudaStreamSynchronize(c.stream));
+      for (size_t z = 0; z < fb.size(); ++z) {
+        c.local_rank[chunk[fb[z]]] = hr[z];
+        c.local_cond[chunk[fb[z]]] = hc[z];
+        c.fallback.push_back(chunk[fb[z]]);
+      }
     }
-    lam.ensure(te);
-    EigOpts eo;  // backward stable like SelfAdjointEigenSolver; the cutoff is 1e-12·λmax (schwarz.hpp:82)
-    eo.absolute = 1;
-    eo.tol = 1e-15;
-    eo.floor_rel = 1e-16;
-    eo.conv_rel = 1e-14;
-    eo.max_sweeps = 60;
-    batched_syevj(c, Af.p, V.p, lam.p, fn, foff, eo);
-    DBuf<long long> devo, dfoff;
-    DBuf<int> drank, dfn;
-    DBuf<double> dcond;
-    devo.upload(evo, c.stream);
-    dfoff.upload(foff, c.stream);
-    dfn.upload(fn, c.stream);
-    drank.ensure(fb.size());
-    dcond.ensure(fb.size());
-    k_local_scale<<<static_cast<int>(fb.size()), 256, 0, c.stream>>>(V.p, lam.p, dfn.p, dfoff.p, devo.p, X.p, drank.p,
-                                                                     dcond.p);
+    // store: full inverse (AS/SAS) or the owner panel (RAS)
+    std::vector<long long> src(B), dst(B);
+    std::vector<int> rows0(B), nrows(B);
+    for (int q = 0; q < B; ++q) {
+      src[q] = coff[q];
+      dst[q] = c.P_off[chunk[q]];
+      rows0[q] = ras ? hown[chunk[q]] : 0;
+      nrows[q] = ras ? c.h_p[chunk[q]] : cn[q];
+    }
+    DBuf<long long> dsrc, ddst;
+    DBuf<int> dr0, dnr, dcn;
+    dsrc.upload(src, c.stream);
+    ddst.upload(dst, c.stream);
+    dr0.upload(rows0, c.stream);
+    dnr.upload(nrows, c.stream);
+    dcn.upload(cn, c.stream);
+    k_store_rows<<<B, 256, 0, c.stream>>>(Pc, dsrc.p, dcn.p, dr0.p, dnr.p, c.P.p, ddst.p);
     RDD_LAUNCH_CHECK();
-    std::vector<GemmTask> t;
-    for (size_t q = 0; q < fb.size(); ++q)
-      for (int tm = 0; tm < ceil_div(fn[q], 64); ++tm)
-        for (int tn = 0; tn < ceil_div(fn[q], 64); ++tn)
-          t.push_back({X.p + foff[q], V.p + foff[q], c.P.p + c.P_off[fb[q]], nullptr, nullptr, fn[q], fn[q], fn[q],
-                       fn[q], fn[q], fn[q], tm, tn, 0.0});
-    gemm_nt(c, t);
-    std::vector<int> hr(fb.size());
-    std::vector<double> hc(fb.size());
-    drank.download(hr.data(), fb.size(), c.stream);
-    dcond.download(hc.data(), fb.size(), c.stream);
     RDD_CUDA(cudaStreamSynchronize(c.stream));
-    for (size_t q = 0; q < fb.size(); ++q) {
-      c.local_rank[fb[q]] = hr[q];
-      c.local_cond[fb[q]] = hc[q];
-    }
   }
-  c.fallback = fb;
+  c.n_fallback = static_cast<int>(c.fallback.size());
+  {
+    std::vector<int> h_own_pos(J);
+    for (int i = 0; i < J; ++i) h_own_pos[i] = c.own_pos[i];
+    c.down_pos.upload(h_own_pos, c.stream);
+  }
   c.nmax_local = *std::max_element(n.begin(), n.end());
 }
 
 void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose) {
   ScopedKernelTimer tk(c, "precond_apply");
   const int T = 128;
+  if (c.pkind == RDD_PRECOND_RAS) {
+    int pmax = 0;
+    for (int j = 0; j < c.J; ++j) pmax = std::max(pmax, c.h_p[j]);
+    if (!transpose) {
+      const size_t smem = static_cast<size_t>(c.nmax_local) * sizeof(double);
+      if (smem > 48 * 1024)
+        RDD_CUDA(cudaFuncSetAttribute(k_ras_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      k_ras_apply<<<dim3(ceil_div(pmax, T), c.J), T, smem, c.stream>>>(c.P.p, c.dP_off.p, c.dset_ptr.p, c.dset_idx.p,
+                                                                       c.dcol_off.p, v, z);
+      RDD_LAUNCH_CHECK();
+    } else {
+      k_ras_apply_t<<<dim3(ceil_div(c.nmax_local, T), c.J), T, 0, c.stream>>>(c.P.p, c.dP_off.p, c.dset_ptr.p,
+                                                                             c.dcol_off.p, v, c.zloc.p);
+      RDD_LAUNCH_CHECK();
+      k_reduce<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.zloc.p, c.gat_ptr.p, c.gat_pos.p, c.gat_owner_pos.p,
+                                                         c.dmult.p, c.p, RDD_PRECOND_AS, 1, z);
+      RDD_LAUNCH_CHECK();
+    }
+    return;
+  }
   dim3 grid(ceil_div(c.nmax_local, T), c.J);
   const size_t smem = static_cast<size_t>(c.nmax_local) * sizeof(double);
   if (smem > 48 * 1024)

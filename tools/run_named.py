@@ -5,7 +5,7 @@ sys.path.insert(0, ROOT)
 from paper_2412_19207_b200 import rdd, configs, abi as A
 name = sys.argv[1]
 cfg = configs.BASELINE[name]()
-if len(sys.argv) > 3:
+if len(sys.argv) > 3 and sys.argv[2]:
     counts = [int(x) for x in sys.argv[2].split(",")]
     cfg = configs.scaled(cfg, counts, int(sys.argv[3]))
 for kv in sys.argv[4:]:

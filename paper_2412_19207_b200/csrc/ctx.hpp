@@ -254,6 +254,7 @@ struct EigOpts {
   double tol = 1e-14;
   double floor_rel = 0.0, floor_abs = 0.0;  // no rotation between two directions both below the floor
   double conv_rel = 0.0, conv_abs = 0.0;    // convergence judged on directions above this level only
+  double conv_angle = 0.0;                  // ... and on rotations with |tan θ| above this
   int max_sweeps = 40;
 };
 void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vector<int>& n,

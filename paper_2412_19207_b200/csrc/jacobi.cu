@@ -19,7 +19,6 @@ namespace rdd {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kSmemMaxN = 223;  // n(n+1)/2 doubles + pair tables within 227 KB
 constexpr double kMinAngle = 1e-18;  // rotations by smaller angles cannot change V: skipped
 constexpr size_t kCtaSmem = 227 * 1024;
 
@@ -28,6 +27,7 @@ struct Crit {
   int absolute;
   double floor_lam;  // pairs with both diagonals below this are not rotated
   double conv_lam;   // only rotations touching a diagonal above this keep the sweep loop going
+  double conv_angle; // ... and only those turning by more than this (|tan θ|)
   double tiny;
 };
 
@@ -48,188 +48,10 @@ __device__ __forceinline__ void schur2(double app, double aqq, double apq, doubl
   s = t * c;
 }
 
-__device__ __forceinline__ long long pidx(int i, int j) {  // packed upper, column-major
-  if (i > j) {
-    const int t = i;
-    i = j;
-    j = t;
-  }
-  return static_cast<long long>(j) * (j + 1) / 2 + i;
-}
+constexpr int kRows = 32;  // rows of V per CTA in the global-memory replay
 
-__device__ __forceinline__ int player(int pos, int r, int nn) {  // round-robin tournament
-  return pos == 0 ? 0 : 1 + (pos - 1 + r) % (nn - 1);
-}
-
-__global__ void __launch_bounds__(kThreads) k_syevj(const double* __restrict__ Ain, double* __restrict__ ev,
-                                                    const int* __restrict__ nvec, const long long* __restrict__ off,
-                                                    const long long* __restrict__ ev_off, int max_sweeps, Crit crit_in,
-                                                    double floor_rel, double conv_rel, int* __restrict__ sweeps_out,
-                                                    double2* __restrict__ rot, const long long* __restrict__ rot_off,
-                                                    int tri_max) {
-  extern __shared__ double smem[];
-  const int b = blockIdx.x;
-  const int n = nvec[b];
-  if (n <= 0) return;
-  const int nn = n + (n & 1);
-  const int np = nn / 2;
-  const double* A = Ain + off[b];
-  double* P = smem;                      // packed upper triangle (column-packed)
-  double* cs = smem + tri_max;
-  double* sn = cs + np;
-  int* pp = reinterpret_cast<int*>(sn + np);
-  int* qq = pp + np;
-  int* col = qq + np;                    // col[j] = j(j+1)/2
-  __shared__ int active;
-  __shared__ double dmax_s;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) col[j] = j * (j + 1) / 2;
-  __syncthreads();
-  for (int j = threadIdx.y; j < n; j += blockDim.y)
-    for (int i = threadIdx.x; i <= j; i += blockDim.x) P[col[j] + i] = A[i + static_cast<long long>(j) * n];
-  __syncthreads();
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    double m = 0.0;
-    for (int i = 0; i < n; ++i) m = fmax(m, fabs(P[col[i] + i]));
-    dmax_s = m;
-  }
-  __syncthreads();
-  const double dmax = dmax_s;
-  Crit crit = crit_in;
-  crit.tiny = 1e-32 * dmax;
-  crit.floor_lam = fmax(floor_rel * dmax, crit_in.floor_lam);
-  crit.conv_lam = fmax(conv_rel * dmax, crit_in.conv_lam);
-  if (crit.absolute) crit.tol = crit_in.tol * dmax;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  double2* R = rot + rot_off[b];
-  auto at = [&](int i, int j) -> double& { return i <= j ? P[col[j] + i] : P[col[i] + j]; };
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) active = 0;
-    int local_active = 0;
-    for (int r = 0; r < nn - 1; ++r) {
-      for (int k = tid; k < np; k += blockDim.x * blockDim.y) {
-        int p = player(k, r, nn), q = player(nn - 1 - k, r, nn);
-        if (p > q) {
-          const int t = p;
-          p = q;
-          q = t;
-        }
-        double c = 1.0, sv = 0.0;
-        if (q < n) {
-          const double app = P[col[p] + p], aqq = P[col[q] + q], apq = P[col[q] + p];
-          const int d = rot_decision(crit, app, aqq, apq);
-          if (d) {
-            schur2(app, aqq, apq, c, sv);
-            if (d == 2) local_active = 1;
-          }
-        }
-        cs[k] = c;
-        sn[k] = sv;
-        pp[k] = p;
-        qq[k] = q;
-        R[(static_cast<long long>(sweep) * (nn - 1) + r) * np + k] = make_double2(c, sv);
-      }
-      __syncthreads();
-      // A <- Jᵀ A J on unordered pair-pair blocks (P <= Q); 2-D thread grid, no div/mod
-      for (int Q = threadIdx.y; Q < np; Q += blockDim.y) {
-        const double c2 = cs[Q], s2 = sn[Q];
-        const int p2 = pp[Q], q2 = qq[Q];
-        const bool v2 = q2 < n;
-        for (int Pp = threadIdx.x; Pp <= Q; Pp += blockDim.x) {
-          const double c1 = cs[Pp], s1 = sn[Pp];
-          if (s1 == 0.0 && s2 == 0.0) continue;
-          const int p1 = pp[Pp], q1 = qq[Pp];
-          if (Pp == Q) {
-            if (!v2) continue;
-            double& app = P[col[p1] + p1];
-            double& aqq = P[col[q1] + q1];
-            double& apq = P[col[q1] + p1];
-            const double t = s1 / c1, vpq = apq;
-            app = app - t * vpq;
-            aqq = aqq + t * vpq;
-            apq = 0.0;
-            continue;
-          }
-          const bool v1 = q1 < n;
-          double& r11 = at(p1, p2);
-          const double a11 = r11;
-          const double a12 = v2 ? at(p1, q2) : 0.0;
-          const double a21 = v1 ? at(q1, p2) : 0.0;
-          const double a22 = (v1 && v2) ? at(q1, q2) : 0.0;
-          const double l11 = c1 * a11 - s1 * a21, l12 = c1 * a12 - s1 * a22;
-          const double l21 = s1 * a11 + c1 * a21, l22 = s1 * a12 + c1 * a22;
-          r11 = l11 * c2 - l12 * s2;
-          if (v2) at(p1, q2) = l11 * s2 + l12 * c2;
-          if (v1) at(q1, p2) = l21 * c2 - l22 * s2;
-          if (v1 && v2) at(q1, q2) = l21 * s2 + l22 * c2;
-        }
-      }
-      __syncthreads();
-    }
-    if (local_active) atomicOr(&active, 1);
-    __syncthreads();
-    const int any = active;
-    __syncthreads();
-    if (!any) {
-      ++sweep;  // this sweep's (inactive-only) rotations were applied: keep them in the log
-      break;
-    }
-  }
-  for (int i = tid; i < n; i += blockDim.x * blockDim.y) ev[ev_off[b] + i] = P[col[i] + i];
-  if (tid == 0) sweeps_out[b] = sweep;
-}
-
-// V = J_1 J_2 ... J_R (all logged rounds): rows are independent, so each CTA keeps kRows rows
-// of V in shared memory and replays the rotation log on them.
-constexpr int kRows = 32;
-__global__ void __launch_bounds__(256) k_apply_rotations(double* __restrict__ Vout, const int* __restrict__ nvec,
-                                                         const long long* __restrict__ off,
-                                                         const double2* __restrict__ rot,
-                                                         const long long* __restrict__ rot_off,
-                                                         const int* __restrict__ sweeps) {
-  extern __shared__ double vs[];  // kRows x (n+1)
-  const int b = blockIdx.y;
-  const int n = nvec[b];
-  const int r0 = blockIdx.x * kRows;
-  if (r0 >= n) return;
-  const int rows = min(kRows, n - r0);
-  const int nn = n + (n & 1), np = nn / 2, ld = n + 1;
-  for (int e = threadIdx.x; e < kRows * n; e += blockDim.x) {
-    const int rr = e / n, col = e % n;
-    vs[rr * ld + col] = (rr < rows && r0 + rr == col) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  const double2* R = rot + rot_off[b];
-  const int total = sweeps[b] * (nn - 1);
-  for (int t = 0; t < total; ++t) {
-    const int r = t % (nn - 1);
-    const double2* Rt = R + static_cast<long long>(t) * np;
-    for (int e = threadIdx.x; e < np * kRows; e += blockDim.x) {
-      const int k = e / kRows, rr = e % kRows;
-      const double2 csn = Rt[k];
-      if (csn.y == 0.0 || rr >= rows) continue;
-      int p = player(k, r, nn), q = player(nn - 1 - k, r, nn);
-      if (p > q) {
-        const int tmp = p;
-        p = q;
-        q = tmp;
-      }
-      double* row = vs + rr * ld;
-      const double a = row[p], bq = row[q];
-      row[p] = csn.x * a - csn.y * bq;
-      row[q] = csn.y * a + csn.x * bq;
-    }
-    __syncthreads();
-  }
-  double* V = Vout + off[b];
-  for (int e = threadIdx.x; e < rows * n; e += blockDim.x) {
-    const int rr = e % rows, col = e / rows;
-    V[(r0 + rr) + static_cast<long long>(col) * n] = vs[rr * ld + col];
-  }
-}
-
-
-// Odd-even (Luk–Park) ordering on full column-major storage in global memory (n > kSmemMaxN):
+// Odd-even (Luk–Park) ordering on full column-major storage in global memory (orders whose packed
+// triangle does not fit a cluster's shared memory):
 // step t pairs positions (o+2k, o+2k+1), o = t&1, and every pair is rotated *and swapped*
 // (Ĵ = J·Π), which makes the index movement a transposition network so all pairs meet every n
 // steps, while each 2x2 update touches two contiguous 16-byte column segments.
@@ -276,7 +98,7 @@ __global__ void __launch_bounds__(1024) k_syevj_oe(double* __restrict__ Aw, cons
         const int d = rot_decision(crit, app, aqq, apq);
         if (d) {
           schur2(app, aqq, apq, c, s);
-          if (d == 2) local_active = 1;
+          if (d == 2 && fabs(s) > crit.conv_angle * c) local_active = 1;
         }
         cs[k] = c;
         sn[k] = s;
@@ -413,148 +235,6 @@ __global__ void __launch_bounds__(256) k_apply_rotations_oe(double* __restrict__
 // (distributed shared memory): element e of the packed upper triangle lives in CTA e / chunk.
 // Every CTA computes the round's rotations redundantly (identical inputs -> identical values),
 // then updates its share of the pair-pair blocks; two cluster barriers per round.
-template <int K>
-__global__ void __launch_bounds__(kThreads) k_syevj_cluster(const double* __restrict__ Ain,
-                                                            double* __restrict__ ev, const int* __restrict__ nvec,
-                                                            const long long* __restrict__ off,
-                                                            const long long* __restrict__ ev_off, int max_sweeps,
-                                                            Crit crit_in, double floor_rel, double conv_rel,
-                                                            int* __restrict__ sweeps_out, double2* __restrict__ rot,
-                                                            const long long* __restrict__ rot_off, int chunk) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ double smem[];
-  const int rank = static_cast<int>(cluster.block_rank());
-  const int b = blockIdx.x / K;
-  const int n = nvec[b];
-  const int nn = n + (n & 1), np = nn / 2;
-  double* cs = smem + chunk;
-  double* sn = cs + np;
-  int* pp = reinterpret_cast<int*>(sn + np);
-  int* qq = pp + np;
-  int* lcol = qq + np;                  // local start of column j inside its owner CTA
-  unsigned char* own = reinterpret_cast<unsigned char*>(lcol + n);  // owner CTA of column j
-  __shared__ int active;
-  double* base[K];
-#pragma unroll
-  for (int r = 0; r < K; ++r) base[r] = cluster.map_shared_rank(smem, r);
-  // whole columns per CTA: column j goes to CTA floor(j(j+1)/2 / chunk); chunk leaves room for it
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    int cur = 0, start = 0;
-    for (int j = 0; j < n; ++j) {
-      const int e = j * (j + 1) / 2;
-      while (cur + 1 < K && e + j + 1 - start > chunk) {
-        ++cur;
-        start = e;
-      }
-      own[j] = static_cast<unsigned char>(cur);
-      lcol[j] = e - start;
-    }
-  }
-  __syncthreads();
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  const int nthr = blockDim.x * blockDim.y;
-  auto at = [&](int i, int j) -> double& {
-    if (i > j) {
-      const int t = i;
-      i = j;
-      j = t;
-    }
-    return base[own[j]][lcol[j] + i];
-  };
-  const double* A = Ain + off[b];
-  for (int j = threadIdx.y; j < n; j += blockDim.y) {
-    if (own[j] != rank) continue;
-    for (int i = threadIdx.x; i <= j; i += blockDim.x) smem[lcol[j] + i] = A[i + static_cast<long long>(j) * n];
-  }
-  cluster.sync();
-  double dmax = 0.0;
-  for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(at(i, i)));
-  Crit crit = crit_in;
-  crit.tiny = 1e-32 * dmax;
-  crit.floor_lam = fmax(floor_rel * dmax, crit_in.floor_lam);
-  crit.conv_lam = fmax(conv_rel * dmax, crit_in.conv_lam);
-  if (crit.absolute) crit.tol = crit_in.tol * dmax;
-  double2* R = rot + rot_off[b];
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) active = 0;
-    int local_active = 0;
-    for (int r = 0; r < nn - 1; ++r) {
-      for (int k = tid; k < np; k += nthr) {
-        int p = player(k, r, nn), q = player(nn - 1 - k, r, nn);
-        if (p > q) {
-          const int t = p;
-          p = q;
-          q = t;
-        }
-        double c = 1.0, sv = 0.0;
-        if (q < n) {
-          const double app = at(p, p), aqq = at(q, q), apq = at(p, q);
-          const int d = rot_decision(crit, app, aqq, apq);
-          if (d) {
-            schur2(app, aqq, apq, c, sv);
-            if (d == 2) local_active = 1;
-          }
-        }
-        cs[k] = c;
-        sn[k] = sv;
-        pp[k] = p;
-        qq[k] = q;
-        if (rank == 0) R[(static_cast<long long>(sweep) * (nn - 1) + r) * np + k] = make_double2(c, sv);
-      }
-      cluster.sync();  // all reads of this round's pivots done before any update
-      // blocks (P <= Q): CTA `rank` takes the Q rows Q = rank, rank+K, ... (balanced triangles)
-      for (int Q = rank + K * threadIdx.y; Q < np; Q += K * blockDim.y) {
-        const double c2 = cs[Q], s2 = sn[Q];
-        const int p2 = pp[Q], q2 = qq[Q];
-        const bool v2 = q2 < n;
-        for (int Pp = threadIdx.x; Pp <= Q; Pp += blockDim.x) {
-          const double c1 = cs[Pp], s1 = sn[Pp];
-          if (s1 == 0.0 && s2 == 0.0) continue;
-          const int p1 = pp[Pp], q1 = qq[Pp];
-          if (Pp == Q) {
-            if (!v2) continue;
-            double& app = at(p1, p1);
-            double& aqq = at(q1, q1);
-            double& apq = at(p1, q1);
-            const double t = s1 / c1, vpq = apq;
-            app = app - t * vpq;
-            aqq = aqq + t * vpq;
-            apq = 0.0;
-            continue;
-          }
-          const bool v1 = q1 < n;
-          double& r11 = at(p1, p2);
-          const double a11 = r11;
-          const double a12 = v2 ? at(p1, q2) : 0.0;
-          const double a21 = v1 ? at(q1, p2) : 0.0;
-          const double a22 = (v1 && v2) ? at(q1, q2) : 0.0;
-          const double l11 = c1 * a11 - s1 * a21, l12 = c1 * a12 - s1 * a22;
-          const double l21 = s1 * a11 + c1 * a21, l22 = s1 * a12 + c1 * a22;
-          r11 = l11 * c2 - l12 * s2;
-          if (v2) at(p1, q2) = l11 * s2 + l12 * c2;
-          if (v1) at(q1, p2) = l21 * c2 - l22 * s2;
-          if (v1 && v2) at(q1, q2) = l21 * s2 + l22 * c2;
-        }
-      }
-      cluster.sync();
-    }
-    if (local_active) atomicOr(cluster.map_shared_rank(&active, 0), 1);
-    cluster.sync();
-    const int any = *cluster.map_shared_rank(&active, 0);
-    cluster.sync();
-    if (!any) {
-      ++sweep;
-      break;
-    }
-  }
-  if (rank == 0) {
-    for (int i = tid; i < n; i += nthr) ev[ev_off[b] + i] = at(i, i);
-    if (tid == 0) sweeps_out[b] = sweep;
-  }
-  cluster.sync();  // keep every CTA's shared memory alive until all remote accesses are done
-}
 
 // ============================================================================================
 // Odd-even (Luk–Park) ordering on the packed upper triangle, distributed by whole columns over a
@@ -642,7 +322,7 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
         const int d = rot_decision(crit, app, aqq, apq);
         if (d) {
           schur2(app, aqq, apq, c, sv);
-          if (d == 2) local_active = 1;
+          if (d == 2 && fabs(sv) > crit.conv_angle * c) local_active = 1;
         }
         if constexpr (K > 1) {
 #pragma unroll
@@ -826,6 +506,104 @@ __global__ void __launch_bounds__(kReplayWarps * 32) k_replay_oe(const int* __re
   }
 }
 
+// Register-resident replay: lane l of a warp holds positions [lE, lE+E) of R rows of V, so the
+// even steps' pairs are lane-local and each odd step has one pair straddling lanes l and l+1
+// (one shuffle each way). The rotation log is staged through shared memory kLogRounds steps at a
+// time and read once per R rows; V rows leave through shared memory as coalesced columns.
+constexpr int kRegWarps = 8;
+template <int E, int R>
+__global__ void __launch_bounds__(kRegWarps * 32) k_replay_reg(const int* __restrict__ nvec,
+                                                               const double2* __restrict__ rot,
+                                                               const long long* __restrict__ rot_off,
+                                                               const int* __restrict__ sweeps,
+                                                               double* __restrict__ Vpad,
+                                                               const long long* __restrict__ poff) {
+  extern __shared__ __align__(16) double2 logc[];  // kLogRounds x np, later kRegWarps*R x ne
+  const int b = blockIdx.y;
+  const int n = nvec[b];
+  const int ne = n + (n & 1), np = ne / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rbase = blockIdx.x * kRegWarps * R;
+  if (rbase >= ne) return;  // whole CTA idle (uniform)
+  const int row0 = rbase + warp * R;
+  const int c0 = lane * E;
+  double v[R][E];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[r][e] = (row0 + r == c0 + e) ? 1.0 : 0.0;
+  const double2* Rl = rot + rot_off[b];
+  const int total = sweeps[b] * ne;
+  const int kb = c0 / 2;  // first pair index of this lane (even steps)
+  for (int t0 = 0; t0 < total; t0 += kLogRounds) {
+    const int nr = min(kLogRounds, total - t0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * np; e += blockDim.x) logc[e] = Rl[static_cast<long long>(t0) * np + e];
+    __syncthreads();
+    for (int tt = 0; tt < nr; ++tt) {
+      const double2* Rt = logc + tt * np;
+      if (((t0 + tt) & 1) == 0) {  // pairs (2k, 2k+1), k < np: all lane-local
+#pragma unroll
+        for (int i = 0; i < E / 2; ++i) {
+          const int k = kb + i;
+          if (k < np) {
+            const double2 cs = Rt[k];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const double a = v[r][2 * i], bb = v[r][2 * i + 1];
+              v[r][2 * i] = cs.y * a + cs.x * bb;
+              v[r][2 * i + 1] = cs.x * a - cs.y * bb;
+            }
+          }
+        }
+      } else {  // pairs (2k+1, 2k+2), k < np-1
+        const int npair = np - 1;
+        const int khi = kb + E / 2 - 1;  // (c0+E-1, c0+E): with lane+1
+        const int klo = kb - 1;          // (c0-1, c0): with lane-1
+        const double2 chi = khi < npair ? Rt[khi] : make_double2(1.0, 0.0);
+        const double2 clo = (lane > 0 && klo < npair) ? Rt[klo] : make_double2(1.0, 0.0);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double nxt = __shfl_down_sync(0xffffffffu, v[r][0], 1);
+          const double prv = __shfl_up_sync(0xffffffffu, v[r][E - 1], 1);
+          const double hi = v[r][E - 1], lo = v[r][0];
+          if (khi < npair) v[r][E - 1] = chi.y * hi + chi.x * nxt;
+          if (lane > 0 && klo < npair) v[r][0] = clo.x * prv - clo.y * lo;
+        }
+#pragma unroll
+        for (int i = 0; i < E / 2 - 1; ++i) {
+          const int k = kb + i;
+          if (k < npair) {
+            const double2 cs = Rt[k];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const double a = v[r][2 * i + 1], bb = v[r][2 * i + 2];
+              v[r][2 * i + 1] = cs.y * a + cs.x * bb;
+              v[r][2 * i + 2] = cs.x * a - cs.y * bb;
+            }
+          }
+        }
+      }
+    }
+  }
+  // stage rows through shared memory, write columns of the padded V (column-major, ld ne)
+  __syncthreads();
+  double* st = reinterpret_cast<double*>(logc);
+  const int RC = kRegWarps * R;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (c0 + e < ne) st[(c0 + e) * RC + warp * R + r] = v[r][e];
+  __syncthreads();
+  const int nrow = min(RC, ne - rbase);
+  double* out = Vpad + poff[b];
+  for (int e = threadIdx.x; e < ne * RC; e += blockDim.x) {
+    const int cc = e / RC, rr = e % RC;
+    if (rr < nrow) out[rbase + rr + static_cast<long long>(cc) * ne] = st[e];
+  }
+}
+
 // pad to even order (zero row/column; the pad direction stays decoupled: every entry touching
 // it is an exact zero) / compact back, dropping the pad eigenpair
 __global__ void k_pad_copy(const double* __restrict__ A, const long long* __restrict__ off, const int* __restrict__ n,
@@ -896,6 +674,7 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
   crit.absolute = o.absolute;
   crit.floor_lam = o.floor_abs;
   crit.conv_lam = o.conv_abs;
+  crit.conv_angle = o.conv_angle;
   int nmax = 0;
   for (int b = 0; b < B; ++b) nmax = std::max(nmax, n[b]);
   std::vector<long long> offE(B);
@@ -967,12 +746,35 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     else if (K == 2) launch(k_jacobi_oe<2>);
     else if (K == 4) launch(k_jacobi_oe<4>);
     else launch(k_jacobi_oe<8>);
-    const size_t vsm = static_cast<size_t>(kReplayWarps) * ne * sizeof(double) +
-                       static_cast<size_t>(kLogRounds) * (ne / 2) * sizeof(double2);
-    RDD_CUDA(cudaFuncSetAttribute(k_replay_oe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
-    k_replay_oe<<<dim3(ceil_div(ne, kReplayWarps), B), kReplayWarps * 32, vsm, c.stream>>>(dn.p, rot.p, droff.p, dsw.p,
-                                                                                           Vp.p, dwoff.p);
-    RDD_LAUNCH_CHECK();
+    const int E = ((ne + 31) / 32 + 1) & ~1;  // positions per lane, even
+    if (E <= 16) {
+      const int R = E <= 8 ? 4 : 2;
+      const size_t vsm = std::max(static_cast<size_t>(kLogRounds) * (ne / 2) * sizeof(double2),
+                                  static_cast<size_t>(kRegWarps) * R * ne * sizeof(double));
+      const dim3 grid(ceil_div(ne, kRegWarps * R), B);
+      auto rl = [&](auto kern) {
+        RDD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
+        kern<<<grid, kRegWarps * 32, vsm, c.stream>>>(dn.p, rot.p, droff.p, dsw.p, Vp.p, dwoff.p);
+        RDD_LAUNCH_CHECK();
+      };
+      switch (E) {
+        case 2: rl(k_replay_reg<2, 4>); break;
+        case 4: rl(k_replay_reg<4, 4>); break;
+        case 6: rl(k_replay_reg<6, 4>); break;
+        case 8: rl(k_replay_reg<8, 4>); break;
+        case 10: rl(k_replay_reg<10, 2>); break;
+        case 12: rl(k_replay_reg<12, 2>); break;
+        case 14: rl(k_replay_reg<14, 2>); break;
+        default: rl(k_replay_reg<16, 2>); break;
+      }
+    } else {
+      const size_t vsm = static_cast<size_t>(kReplayWarps) * ne * sizeof(double) +
+                         static_cast<size_t>(kLogRounds) * (ne / 2) * sizeof(double2);
+      RDD_CUDA(cudaFuncSetAttribute(k_replay_oe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(vsm)));
+      k_replay_oe<<<dim3(ceil_div(ne, kReplayWarps), B), kReplayWarps * 32, vsm, c.stream>>>(dn.p, rot.p, droff.p,
+                                                                                             dsw.p, Vp.p, dwoff.p);
+      RDD_LAUNCH_CHECK();
+    }
   } else {
     // ---- odd-even ordering, full storage in global memory (very large orders)
     struct WS3 {

@@ -118,12 +118,17 @@ void run_pca(Ctx& c) {
     s1.tol = 1e-14;
     s1.floor_rel = 1e-13;
     s1.conv_rel = 1e-12;
+    s1.conv_angle = 1e-8;  // stage 2 refines: stage 1 only has to make the columns of S·V0 graded
     s2.absolute = 0;
     s2.tol = 1e-14;
     s2.floor_rel = rel ? 1e-4 * tau2 : 0.0;
     s2.floor_abs = rel ? 0.0 : 1e-4 * tau2;
     s2.conv_rel = rel ? 1e-2 * tau2 : 0.0;
     s2.conv_abs = rel ? 0.0 : 1e-2 * tau2;
+    // rotations by angles below 1e-12 move the kept subspace and σ by less than the parity
+    // tolerance; without this the sweep loop keeps chasing re-coupling through the unrotated
+    // sub-floor directions (measured: 16 sweeps → 7 at identical projectors and σ)
+    s2.conv_angle = 1e-12;
     // stage 1: Gram + Jacobi
     gemm_tn(c, gram_tasks(c, c.S.p, G.p, c.S_off));
     batched_syevj(c, G.p, V0.p, lam.p, ns, offm, s1);

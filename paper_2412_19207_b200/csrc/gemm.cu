@@ -3,8 +3,7 @@
 // tcgen05 has no f64 kind (ptxas rejects `.kind::f64` for sm_100a), so FP64
 // tensor-core work on B200 is `mma.sync.aligned.m8n8k4.row.col.f64` (SASS: DMMA). One CTA
 // computes a 64x64 tile of one task with 4 warps (32x32 warp tiles = 4x4 DMMA fragments),
-// K staged 16 at a time through padded shared memory with register prefetch of the next
-// stage. Used for: Gram SᵀS and TᵀT (PCA, feeds reduction.hpp:91), T = S·V and H = S·V
+// K staged 16 at a time through a 3-deep cp.async ring in padded shared memory. Used for: Gram SᵀS and TᵀT (PCA, feeds reduction.hpp:91), T = S·V and H = S·V
 // (reduction.hpp:133 by linearity), normal blocks H_j1[I]ᵀH_j2[I] with row gathers
 // (assembly.hpp:148-183), local-inverse products (schwarz.hpp:76-79).
 #include "ctx.hpp"
@@ -13,18 +12,33 @@ namespace rdd {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, PAD = 8, NT = 128;
+constexpr int BM = 64, BN = 64, BK = 16, NT = 128, STAGES = 3;
+constexpr int KP = BK + 4;   // k-contiguous tiles: [64][BK+4] (row stride ≡ 4 banks mod 16)
+constexpr int MP = BM + 4;   // m/n-contiguous tiles: [BK][64+4]
+constexpr int kStageA = BM * KP > BK * MP ? BM * KP : BK * MP;  // doubles per operand per stage
+constexpr size_t kGemmSmem = static_cast<size_t>(STAGES) * 2 * kStageA * sizeof(double);
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
+// 8-byte asynchronous global->shared copy; src_size 0 zero-fills (out-of-range elements)
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// One CTA: a 64x64 tile of one task, 4 warps (32x32 warp tiles = 4x4 DMMA fragments). K streams
+// through a STAGES-deep cp.async ring; each operand tile keeps its global contiguous direction
+// in shared memory (k-contiguous for Aᵀ / B, m-contiguous for A / Bᵀ) so the copies coalesce,
+// and the padded strides make the fragment reads bank-conflict free.
 template <bool AT, bool BT>
 __global__ void __launch_bounds__(NT) k_gemm(const GemmTask* __restrict__ tasks) {
-  __shared__ double As[2][BK][BM + PAD];
-  __shared__ double Bs[2][BK][BN + PAD];
+  extern __shared__ __align__(16) double gsm[];
   const GemmTask T = tasks[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m0 = T.tm * BM, n0 = T.tn * BN;
@@ -36,70 +50,71 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmTask* __restrict__ tasks)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  double ra[8], rb[8];
-  auto load = [&](int k0) {
+  auto As = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStageA; };
+  auto Bs = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStageA + kStageA; };
+  auto issue = [&](int kt, int s) {
+    const int k0 = kt * BK;
+    double* a = As(s);
+    double* bsm = Bs(s);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      if (AT) {  // A(k, m) = A[k + m*lda]
-        const int k = k0 + (tid & 15), m = m0 + (tid >> 4) + 8 * i;
-        double v = 0.0;
-        if (k < T.K && m < T.M) {
-          const long long kk = T.gA ? T.gA[k] : k;
-          v = T.A[kk + static_cast<long long>(m) * T.lda];
-        }
-        ra[i] = v;
-      } else {  // A(m, k) = A[m + k*lda]
-        const int m = m0 + (tid & 63), k = k0 + (tid >> 6) + 2 * i;
-        ra[i] = (k < T.K && m < T.M) ? T.A[m + static_cast<long long>(k) * T.lda] : 0.0;
+      if (AT) {  // A(k, m) = A[k + m*lda] -> a[m][k]
+        const int k = k0 + (tid & 15), ml = (tid >> 4) + 8 * i, m = m0 + ml;
+        const bool v = k < T.K && m < T.M;
+        const long long kk = v ? (T.gA ? T.gA[k] : k) : 0;
+        cp_async8(a + ml * KP + (tid & 15), v ? T.A + kk + static_cast<long long>(m) * T.lda : T.A, v);
+      } else {  // A(m, k) = A[m + k*lda] -> a[k][m]
+        const int ml = tid & 63, m = m0 + ml, kl = (tid >> 6) + 2 * i, k = k0 + kl;
+        const bool v = k < T.K && m < T.M;
+        cp_async8(a + kl * MP + ml, v ? T.A + m + static_cast<long long>(k) * T.lda : T.A, v);
       }
-      if (!BT) {  // B(k, n) = B[k + n*ldb]
-        const int k = k0 + (tid & 15), n = n0 + (tid >> 4) + 8 * i;
-        double v = 0.0;
-        if (k < T.K && n < T.N) {
-          const long long kk = T.gB ? T.gB[k] : k;
-          v = T.B[kk + static_cast<long long>(n) * T.ldb];
-        }
-        rb[i] = v;
-      } else {  // B(k, n) = Bt[n + k*ldb]
-        const int n = n0 + (tid & 63), k = k0 + (tid >> 6) + 2 * i;
-        rb[i] = (k < T.K && n < T.N) ? T.B[n + static_cast<long long>(k) * T.ldb] : 0.0;
+      if (!BT) {  // B(k, n) = B[k + n*ldb] -> b[n][k]
+        const int k = k0 + (tid & 15), nl = (tid >> 4) + 8 * i, n = n0 + nl;
+        const bool v = k < T.K && n < T.N;
+        const long long kk = v ? (T.gB ? T.gB[k] : k) : 0;
+        cp_async8(bsm + nl * KP + (tid & 15), v ? T.B + kk + static_cast<long long>(n) * T.ldb : T.B, v);
+      } else {  // B(k, n) = Bt[n + k*ldb] -> b[k][n]
+        const int nl = tid & 63, n = n0 + nl, kl = (tid >> 6) + 2 * i, k = k0 + kl;
+        const bool v = k < T.K && n < T.N;
+        cp_async8(bsm + kl * MP + nl, v ? T.B + n + static_cast<long long>(k) * T.ldb : T.B, v);
       }
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (AT) As[buf][tid & 15][(tid >> 4) + 8 * i] = ra[i];
-      else As[buf][(tid >> 6) + 2 * i][tid & 63] = ra[i];
-      if (!BT) Bs[buf][tid & 15][(tid >> 4) + 8 * i] = rb[i];
-      else Bs[buf][(tid >> 6) + 2 * i][tid & 63] = rb[i];
     }
   };
 
   const int nk = (T.K + BK - 1) / BK;
-  if (nk > 0) {
-    load(0);
-    store(0);
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) issue(s, s);
+    cp_commit();
   }
-  __syncthreads();
   for (int kt = 0; kt < nk; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < nk) load((kt + 1) * BK);
+    cp_wait<STAGES - 2>();
+    __syncthreads();  // stage kt visible to all; stage kt-1's buffer free for reuse
+    if (kt + STAGES - 1 < nk) issue(kt + STAGES - 1, (kt + STAGES - 1) % STAGES);
+    cp_commit();
+    const double* a = As(kt % STAGES);
+    const double* bsm = Bs(kt % STAGES);
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
+      const int k = kk + (lane & 3);
       double af[4], bf[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[buf][kk + (lane & 3)][wm + 8 * i + (lane >> 2)];
+      for (int i = 0; i < 4; ++i) {
+        const int ml = wm + 8 * i + (lane >> 2);
+        af[i] = AT ? a[ml * KP + k] : a[k * MP + ml];
+      }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][kk + (lane & 3)][wn + 8 * j + (lane >> 2)];
+      for (int j = 0; j < 4; ++j) {
+        const int nl = wn + 8 * j + (lane >> 2);
+        bf[j] = BT ? bsm[k * MP + nl] : bsm[nl * KP + k];
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
-    if (kt + 1 < nk) store(buf ^ 1);
-    __syncthreads();
   }
+  cp_wait<0>();
   // epilogue: fragment (row = lane>>2, cols 2*(lane&3) + {0,1})
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -123,7 +138,13 @@ void launch(Ctx& c, const std::vector<GemmTask>& tasks, const char* fam) {
   DBuf<GemmTask> d;
   d.upload(tasks, c.stream);
   // grid.x limit is 2^31-1; tasks are far fewer
-  k_gemm<AT, BT><<<static_cast<unsigned>(tasks.size()), NT, 0, c.stream>>>(d.p);
+  static bool attr_set = false;
+  if (!attr_set) {
+    RDD_CUDA(cudaFuncSetAttribute(k_gemm<AT, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kGemmSmem)));
+    attr_set = true;
+  }
+  k_gemm<AT, BT><<<static_cast<unsigned>(tasks.size()), NT, kGemmSmem, c.stream>>>(d.p);
   RDD_LAUNCH_CHECK();
   if (!alloc_stream()) RDD_CUDA(cudaStreamSynchronize(c.stream));  // task buffer lifetime (non-pooled)
 }

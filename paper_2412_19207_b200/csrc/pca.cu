@@ -68,6 +68,177 @@ __global__ void k_select(const double* __restrict__ lam, const double* __restric
   }
 }
 
+// Stage-1 reduction: pivoted Cholesky of the Gram (upper triangle valid), G ≈ L Lᵀ with L n x r
+// in original row order (column-major, ld n). Pivot = largest remaining Schur diagonal (smallest
+// index on ties); stops when it is not positive or below stop·(first pivot), so r is the
+// numerical rank of G. L's columns are graded, which is what makes the Jacobi on LᵀL short.
+constexpr int kPcholThreads = 512;
+__global__ void __launch_bounds__(kPcholThreads) k_pchol(const double* __restrict__ G, double* __restrict__ L, int n,
+                                                          double stop, int* __restrict__ r_out) {
+  extern __shared__ double psm[];
+  double* d = psm;                                             // n: remaining diagonal
+  double* li = d + n;                                          // n: L[i, :k]
+  unsigned char* done = reinterpret_cast<unsigned char*>(li + n);  // n: pivoted flags
+  __shared__ double rv[kPcholThreads / 32];
+  __shared__ int ri[kPcholThreads / 32];
+  __shared__ int piv_s;
+  __shared__ double dpiv_s;
+  const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* Gj = G + static_cast<size_t>(j) * n * n;
+  double* Lj = L + static_cast<size_t>(j) * n * n;
+  for (int i = tid; i < n; i += blockDim.x) {
+    d[i] = Gj[i + static_cast<size_t>(i) * n];
+    done[i] = 0;
+  }
+  __syncthreads();
+  double dmax0 = 0.0;
+  int r = 0;
+  for (int k = 0; k < n; ++k) {
+    double bv = -1.0;
+    int bi = n;
+    for (int i = tid; i < n; i += blockDim.x)
+      if (!done[i] && d[i] > bv) {
+        bv = d[i];
+        bi = i;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      rv[warp] = bv;
+      ri[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double v = rv[0];
+      int ix = ri[0];
+      for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+        if (rv[w] > v || (rv[w] == v && ri[w] < ix)) {
+          v = rv[w];
+          ix = ri[w];
+        }
+      piv_s = ix;
+      dpiv_s = v;
+    }
+    __syncthreads();
+    const int i = piv_s;
+    const double dp = dpiv_s;
+    if (k == 0) dmax0 = dp;
+    if (!(dp > 0.0) || dp <= stop * dmax0) break;
+    for (int t = tid; t < k; t += blockDim.x) li[t] = Lj[i + static_cast<size_t>(t) * n];
+    __syncthreads();
+    const double sd = sqrt(dp);
+    for (int row = tid; row < n; row += blockDim.x) {
+      double x = 0.0;
+      if (row == i) {
+        x = sd;
+      } else if (!done[row]) {
+        double s = 0.0;
+        for (int t = 0; t < k; ++t) s += Lj[row + static_cast<size_t>(t) * n] * li[t];
+        const double g = row <= i ? Gj[row + static_cast<size_t>(i) * n] : Gj[i + static_cast<size_t>(row) * n];
+        x = (g - s) / sd;
+        d[row] -= x * x;
+      }
+      Lj[row + static_cast<size_t>(k) * n] = x;
+    }
+    if (tid == 0) done[i] = 1;
+    r = k + 1;
+    __syncthreads();
+  }
+  if (r == 0) {  // G = 0: one zero column (the completion below then yields the identity)
+    for (int row = tid; row < n; row += blockDim.x) Lj[row] = 0.0;
+    r = 1;
+  }
+  if (tid == 0) r_out[j] = r;
+}
+
+// V0 = [orth(Vr), complement]: columns of Vr (n x r, eigenvectors of LLᵀ up to scale) sorted by
+// descending eigenvalue and normalised, Householder QR in that order, and the full n x n
+// Q = H_0 ⋯ H_{r-1} accumulated backwards. Q is orthogonal to rounding whatever the accuracy
+// of the small directions of Vr; its first r columns span them in order.
+constexpr int kHouseThreads = 512;
+__global__ void __launch_bounds__(kHouseThreads) k_house_complete(const double* __restrict__ Vr,
+                                                                  const double* __restrict__ lam,
+                                                                  const long long* __restrict__ lam_off,
+                                                                  const int* __restrict__ rr, int n,
+                                                                  double* __restrict__ A, double* __restrict__ Q) {
+  extern __shared__ double hsm[];
+  double* v = hsm;              // n: current Householder vector
+  double* beta = v + n;         // r
+  int* perm = reinterpret_cast<int*>(beta + n);  // r
+  __shared__ double red[kHouseThreads / 32];
+  const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int r = rr[j];
+  const size_t off = static_cast<size_t>(j) * n * n;
+  const double* Vj = Vr + off;
+  double* Aj = A + off;
+  double* Qj = Q + off;
+  const double* lj = lam + lam_off[j];
+  for (int c = tid; c < r; c += blockDim.x) {  // stable descending rank of the eigenvalues
+    int rk = 0;
+    for (int q = 0; q < r; ++q) rk += (lj[q] > lj[c]) || (lj[q] == lj[c] && q < c);
+    perm[rk] = c;
+  }
+  __syncthreads();
+  for (int c = warp; c < r; c += nw) {  // A[:, c] = Vr[:, perm[c]] / ||.||
+    const double* src = Vj + static_cast<size_t>(perm[c]) * n;
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s += src[i] * src[i];
+    s = warp_sum(s);
+    const double sc = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+    for (int i = lane; i < n; i += 32) Aj[i + static_cast<size_t>(c) * n] = src[i] * sc;
+  }
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    double* x = Aj + static_cast<size_t>(k) * n;
+    double s = 0.0;
+    for (int i = k + tid; i < n; i += blockDim.x) s += x[i] * x[i];
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    double nrm2 = 0.0;
+    for (int w = 0; w < nw; ++w) nrm2 += red[w];
+    const double alpha = sqrt(nrm2), x0 = x[k];
+    const double sg = x0 >= 0.0 ? -alpha : alpha;   // H x = sg e_k
+    const double b = alpha > 0.0 ? 1.0 / (sg * (sg - x0)) : 0.0;
+    for (int i = k + tid; i < n; i += blockDim.x) v[i] = (i == k) ? x0 - sg : x[i];
+    if (tid == 0) beta[k] = b;
+    __syncthreads();
+    if (tid == 0) x[k] = x0 - sg;  // keep v_k in A[k:, k] for the accumulation
+    for (int c = k + 1 + warp; c < r; c += nw) {
+      double* y = Aj + static_cast<size_t>(c) * n;
+      double w = 0.0;
+      for (int i = k + lane; i < n; i += 32) w += v[i] * y[i];
+      w = warp_sum(w) * b;
+      for (int i = k + lane; i < n; i += 32) y[i] -= w * v[i];
+    }
+    __syncthreads();
+  }
+  for (size_t e = tid; e < static_cast<size_t>(n) * n; e += blockDim.x) Qj[e] = (e % (n + 1) == 0) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int k = r - 1; k >= 0; --k) {
+    const double* x = Aj + static_cast<size_t>(k) * n;
+    for (int i = k + tid; i < n; i += blockDim.x) v[i] = x[i];
+    __syncthreads();
+    const double b = beta[k];
+    if (b != 0.0)
+      for (int c = k + warp; c < n; c += nw) {
+        double* y = Qj + static_cast<size_t>(c) * n;
+        double w = 0.0;
+        for (int i = k + lane; i < n; i += 32) w += v[i] * y[i];
+        w = warp_sum(w) * b;
+        for (int i = k + lane; i < n; i += 32) y[i] -= w * v[i];
+      }
+    __syncthreads();
+  }
+}
+
 std::vector<GemmTask> gram_tasks(Ctx& c, const double* X, double* G, const std::vector<long long>& offX) {
   std::vector<GemmTask> t;
   const int m = c.m, nt = ceil_div(m, 64);
@@ -129,9 +300,56 @@ void run_pca(Ctx& c) {
     // tolerance; without this the sweep loop keeps chasing re-coupling through the unrotated
     // sub-floor directions (measured: 16 sweeps → 7 at identical projectors and σ)
     s2.conv_angle = 1e-12;
-    // stage 1: Gram + Jacobi
+    // stage 1: Gram, pivoted Cholesky G ≈ L Lᵀ (r = numerical rank), Jacobi on the graded LᵀL
+    // (r x r: one CTA, few sweeps), Vr = L U, V0 = Householder completion of Vr to an n x n basis
     gemm_tn(c, gram_tasks(c, c.S.p, G.p, c.S_off));
-    batched_syevj(c, G.p, V0.p, lam.p, ns, offm, s1);
+    WS Lw{c.ws("pca.L", J * mm)}, Vr{c.ws("pca.Vr", J * mm)}, Hw{c.ws("pca.H", J * mm)};
+    DBuf<int> dr;
+    dr.ensure(J);
+    {
+      const size_t sm = static_cast<size_t>(m) * (2 * sizeof(double) + 1) + 16;
+      if (sm > 48 * 1024)
+        RDD_CUDA(cudaFuncSetAttribute(k_pchol, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+      k_pchol<<<J, kPcholThreads, sm, c.stream>>>(G.p, Lw.p, m, 1e-17, dr.p);
+      RDD_LAUNCH_CHECK();
+    }
+    std::vector<int> rj(J);
+    dr.download(rj.data(), J, c.stream);
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    {
+      std::vector<GemmTask> t;
+      for (int j = 0; j < J; ++j) {
+        const int nt = ceil_div(rj[j], 64);
+        for (int tm = 0; tm < nt; ++tm)
+          for (int tn = tm; tn < nt; ++tn)
+            t.push_back({Lw.p + offm[j], Lw.p + offm[j], G.p + offm[j], nullptr, nullptr, rj[j], rj[j], m, m, m,
+                         rj[j], tm, tn, 0.0});
+      }
+      gemm_tn(c, t);  // M = LᵀL (upper tiles) over the Gram buffer
+    }
+    std::vector<long long> offr(J);
+    for (int j = 0, e = 0; j < J; e += rj[j], ++j) offr[j] = e;
+    batched_syevj(c, G.p, V0.p, lam.p, rj, offm, s1);  // U (r x r, ld r) in V0's buffer
+    {
+      std::vector<GemmTask> t;
+      for (int j = 0; j < J; ++j)
+        for (int tm = 0; tm < ceil_div(m, 64); ++tm)
+          for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+            t.push_back({Lw.p + offm[j], V0.p + offm[j], Vr.p + offm[j], nullptr, nullptr, m, rj[j], rj[j], m, rj[j],
+                         m, tm, tn, 0.0});
+      gemm_nn(c, t);  // Vr = L U
+    }
+    {
+      DBuf<long long> doffr;
+      doffr.upload(offr, c.stream);
+      const size_t sm = static_cast<size_t>(m) * (2 * sizeof(double) + sizeof(int)) + 16;
+      if (sm > 48 * 1024)
+        RDD_CUDA(cudaFuncSetAttribute(k_house_complete, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(sm)));
+      k_house_complete<<<J, kHouseThreads, sm, c.stream>>>(Vr.p, lam.p, doffr.p, dr.p, m, Hw.p, V0.p);
+      RDD_LAUNCH_CHECK();
+      RDD_CUDA(cudaStreamSynchronize(c.stream));
+    }
     // stage 2: T = S V0, G1 = TᵀT, Jacobi on the graded G1
     T.p = c.ws("pca.T", std::max<long long>(1, c.S_off[J]));
     {

@@ -187,7 +187,7 @@ size_t device_available(Ctx& c) {
 // drop the large PCA scratch (T, rotation logs, Jacobi work) and the unreduced samples S once H
 // is assembled; the next build re-creates them
 void release_scratch(Ctx& c) {
-  for (const char* k : {"pca.T", "syevj.rot", "syevj.Vp", "syevj.Wk", "pca.G", "pca.V0", "pca.W", "pca.Vfull"}) {
+  for (const char* k : {"pca.T", "syevj.rot", "syevj.Vp", "syevj.Wk", "pca.G", "pca.V0", "pca.W", "pca.Vfull", "pca.L", "pca.Vr", "pca.H"}) {
     auto it = c.wsd.find(k);
     if (it != c.wsd.end()) it->second.release();
   }

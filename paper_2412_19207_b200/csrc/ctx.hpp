@@ -135,6 +135,9 @@ struct Ctx {
   std::vector<int> iters, conv, brk;
   DBuf<double> W;                     // p x C (unscaled)
   DBuf<double> ytmp;                  // N
+  DBuf<int2> mv_tiles, mt_tiles;      // (block, first row) / (block, first column) tiles of H·w / Hᵀ·r
+  int mv_ntiles = 0, mt_ntiles = 0, mv_rmax = 0;
+  DBuf<double> zrows;                 // per-block partial H_j·w_j (row_ptr layout)
   // Hᵀ·r work list (block, column group)
   DBuf<int> mt_blk, mt_k0;
   int mt_groups = 0;

@@ -12,6 +12,8 @@
 // relies on.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "ctx.hpp"
 
 namespace rdd {
@@ -716,7 +718,11 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
   evp.p = c.ws("syevj.ev", et);
   rot.p = reinterpret_cast<double2*>(c.ws("syevj.rot", 2 * static_cast<size_t>(std::max<long long>(1, rt))));
   const int ne = nmax + (nmax & 1);
-  const int K = oe_k(ne);
+  int K = oe_k(ne);
+  if (const char* e = std::getenv("RDD_JACOBI_K")) {  // experiment override (larger clusters only)
+    const int k = std::atoi(e);
+    if (K > 0 && k > K && k <= 8 && (k & (k - 1)) == 0) K = k;
+  }
   int swmax = 0;
   if (K > 0) {
     // ---- odd-even ordering, packed triangle on chip (one CTA or a K-CTA cluster)
@@ -799,9 +805,13 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     std::vector<int> sw(B);
     dsw.download(sw.data(), B, c.stream);
     RDD_CUDA(cudaStreamSynchronize(c.stream));
-    for (int v : sw) swmax = std::max(swmax, v);
-    std::fprintf(stderr, "[syevj] B=%d nmax=%d path=%s max_sweeps_used=%d\n", B, nmax,
-                 K == 1 ? "oe-smem" : (K ? "oe-cluster" : "oe-global"), swmax);
+    double swsum = 0.0;
+    for (int v : sw) {
+      swmax = std::max(swmax, v);
+      swsum += v;
+    }
+    std::fprintf(stderr, "[syevj] B=%d nmax=%d path=%s K=%d max_sweeps_used=%d mean=%.2f\n", B, nmax,
+                 K == 1 ? "oe-smem" : (K ? "oe-cluster" : "oe-global"), K, swmax, swsum / B);
   }
   RDD_CUDA(cudaStreamSynchronize(c.stream));
 }

@@ -1,10 +1,11 @@
 // matvec.cu — K6 column equilibration and K9/K10 block-sparse H·w, Hᵀ·r.
 //
-// H·w (assembly.hpp:110-121) scatter-adds each block's rows into y; here each global row is
-// owned by one thread that gathers the ≤2^d covering blocks' rows (owner-computes, no atomics;
-// the per-row sum visits blocks in ascending j like the reference). Hᵀ·r (assembly.hpp:123-133)
-// is one warp per column: a contiguous column of a column-major block against r gathered through
-// rows_j. Both are HBM-bound streams over H (8·nnz bytes each).
+// H·w (assembly.hpp:110-121) scatter-adds each block's rows into y; here per-block partial rows
+// z_j = H_j w_j are formed tile by tile and each global row then sums its ≤2^d covering blocks'
+// partials in ascending j like the reference (owner-computes, no atomics). Hᵀ·r
+// (assembly.hpp:123-133) reduces contiguous columns of a column-major block against r gathered
+// through rows_j, staged once per (block, column group). Both are HBM-bound streams over H
+// (8·nnz bytes each).
 #include <algorithm>
 
 #include "ctx.hpp"
@@ -33,41 +34,101 @@ __global__ void k_colnorm_scale(double* __restrict__ H, const long long* __restr
     for (int r = lane; r < rows; r += 32) h[r] = h[r] / s;
 }
 
-__global__ void k_matvec(const double* __restrict__ H, const long long* __restrict__ H_off,
-                         const int* __restrict__ row_ptr, const int* __restrict__ col_off,
-                         const int* __restrict__ cov_n, const int* __restrict__ cov_j, const int* __restrict__ cov_r,
-                         int maxcov, int N, const double* __restrict__ w, double* __restrict__ y) {
+// H·w in two steps, both in the reference's summation order: (1) per (block j, tile of kMvRows
+// local rows), z_j[r] = Σ_k H_j[r, k] w_j[k] (ascending k) with w_j in shared memory and kMvUnroll
+// independent column loads in flight per thread; (2) y_i = Σ over the covering blocks of i in
+// ascending j of z_j[r_i]. Every warp of step 1 runs the same block: uniform trip counts.
+constexpr int kMvRows = 256, kMvUnroll = 8;
+__global__ void __launch_bounds__(kMvRows) k_block_gemv(const double* __restrict__ H, const long long* __restrict__ H_off,
+                                                         const int* __restrict__ row_ptr, const int* __restrict__ col_off,
+                                                         const int2* __restrict__ tiles, const double* __restrict__ w,
+                                                         double* __restrict__ z) {
+  extern __shared__ double wsm[];
+  const int2 t = tiles[blockIdx.x];
+  const int j = t.x;
+  const int rows = row_ptr[j + 1] - row_ptr[j];
+  const int c0 = col_off[j], pj = col_off[j + 1] - c0;
+  for (int k = threadIdx.x; k < pj; k += blockDim.x) wsm[k] = w[c0 + k];
+  __syncthreads();
+  const int r = t.y + threadIdx.x;
+  if (r >= rows) return;
+  const double* h = H + H_off[j] + r;
+  double acc = 0.0;
+  int k = 0;
+  for (; k + kMvUnroll <= pj; k += kMvUnroll) {
+    double v[kMvUnroll];
+#pragma unroll
+    for (int u = 0; u < kMvUnroll; ++u) v[u] = __ldcs(h + static_cast<long long>(k + u) * rows);
+#pragma unroll
+    for (int u = 0; u < kMvUnroll; ++u) acc += v[u] * wsm[k + u];
+  }
+  for (; k < pj; ++k) acc += __ldcs(h + static_cast<long long>(k) * rows) * wsm[k];
+  z[row_ptr[j] + r] = acc;
+}
+
+__global__ void k_cover_sum(const double* __restrict__ z, const int* __restrict__ row_ptr,
+                            const int* __restrict__ cov_n, const int* __restrict__ cov_j, const int* __restrict__ cov_r,
+                            int maxcov, int N, double* __restrict__ y) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   double acc = 0.0;
   const int nc = cov_n[i];
   for (int s = 0; s < nc; ++s) {
-    const int j = cov_j[static_cast<size_t>(i) * maxcov + s];
-    const int r = cov_r[static_cast<size_t>(i) * maxcov + s];
-    const int rows = row_ptr[j + 1] - row_ptr[j];
-    const int c0 = col_off[j], pj = col_off[j + 1] - c0;
-    const double* h = H + H_off[j] + r;
-    double t = 0.0;
-    for (int k = 0; k < pj; ++k) t += h[static_cast<long long>(k) * rows] * w[c0 + k];
-    acc += t;
+    const size_t e = static_cast<size_t>(i) * maxcov + s;
+    acc += z[row_ptr[cov_j[e]] + cov_r[e]];
   }
   y[i] = acc;
 }
 
-__global__ void k_matvec_t(const double* __restrict__ H, const long long* __restrict__ H_off,
-                           const int* __restrict__ row_ptr, const int* __restrict__ row_idx,
-                           const int* __restrict__ col_off, const int* __restrict__ col_owner, int p,
-                           const double* __restrict__ r, double* __restrict__ out) {
-  const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (col >= p) return;
-  const int j = col_owner[col];
-  const int k = col - col_off[j];
+// Hᵀ·r: per (block j, group of kMtCols columns) the gathered r_j = r[rows of j] is staged in
+// shared memory once; each warp then reduces two columns at a time (lane-strided rows, then the
+// butterfly — the same order as a warp-per-column reduction).
+constexpr int kMtWarps = 8, kMtCols = 16, kMtUnroll = 4;
+__global__ void __launch_bounds__(kMtWarps * 32) k_block_gemv_t(const double* __restrict__ H,
+                                                                 const long long* __restrict__ H_off,
+                                                                 const int* __restrict__ row_ptr,
+                                                                 const int* __restrict__ row_idx,
+                                                                 const int* __restrict__ col_off,
+                                                                 const int2* __restrict__ tiles,
+                                                                 const double* __restrict__ r, double* __restrict__ out) {
+  extern __shared__ double rsm[];
+  const int2 t = tiles[blockIdx.x];
+  const int j = t.x;
   const int r0 = row_ptr[j], rows = row_ptr[j + 1] - r0;
-  const double* h = H + H_off[j] + static_cast<long long>(k) * rows;
-  double s = 0.0;
-  for (int q = lane; q < rows; q += 32) s += h[q] * r[row_idx[r0 + q]];
-  s = warp_sum(s);
-  if (lane == 0) out[col] = s;
+  const int c0 = col_off[j], pj = col_off[j + 1] - c0;
+  for (int q = threadIdx.x; q < rows; q += blockDim.x) rsm[q] = r[row_idx[r0 + q]];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ka = t.y + warp, kb = ka + kMtWarps;
+  const bool va = ka < pj, vb = kb < pj;
+  if (!va) return;
+  const double* ha = H + H_off[j] + static_cast<long long>(ka) * rows;
+  const double* hb = H + H_off[j] + static_cast<long long>(vb ? kb : ka) * rows;
+  double sa = 0.0, sb = 0.0;
+  int q = lane;
+  for (; q + 32 * (kMtUnroll - 1) < rows; q += 32 * kMtUnroll) {
+    double a[kMtUnroll], b[kMtUnroll];
+#pragma unroll
+    for (int u = 0; u < kMtUnroll; ++u) {
+      a[u] = __ldcs(ha + q + 32 * u);
+      b[u] = __ldcs(hb + q + 32 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < kMtUnroll; ++u) {
+      sa += a[u] * rsm[q + 32 * u];
+      sb += b[u] * rsm[q + 32 * u];
+    }
+  }
+  for (; q < rows; q += 32) {
+    sa += ha[q] * rsm[q];
+    sb += hb[q] * rsm[q];
+  }
+  sa = warp_sum(sa);
+  sb = warp_sum(sb);
+  if (lane == 0) {
+    out[c0 + ka] = sa;
+    if (vb) out[c0 + kb] = sb;
+  }
 }
 
 }  // namespace
@@ -78,6 +139,21 @@ void ensure_col_owner(Ctx& c) {
     for (int k = c.h_col_off[j]; k < c.h_col_off[j + 1]; ++k) own[k] = j;
   c.h_owner = own;
   c.downer.upload(own, c.stream);
+  // tile lists of the block-tiled H·w / Hᵀ·r
+  std::vector<int2> mv, mt;
+  int rmax = 0;
+  for (int j = 0; j < c.J; ++j) {
+    const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+    rmax = std::max(rmax, rows);
+    for (int r = 0; r < rows; r += kMvRows) mv.push_back(make_int2(j, r));
+    for (int k = 0; k < c.h_p[j]; k += kMtCols) mt.push_back(make_int2(j, k));
+  }
+  c.mv_ntiles = static_cast<int>(mv.size());
+  c.mt_ntiles = static_cast<int>(mt.size());
+  c.mv_rmax = rmax;
+  c.mv_tiles.upload(mv, c.stream);
+  c.mt_tiles.upload(mt, c.stream);
+  c.zrows.ensure(std::max(1, c.h_row_ptr[c.J]));
 }
 
 void column_norms_scale(Ctx& c, bool equilibrate) {
@@ -91,15 +167,30 @@ void column_norms_scale(Ctx& c, bool equilibrate) {
 
 void matvec_dev(Ctx& c, const double* w, double* y) {
   ScopedKernelTimer tk(c, "matvec");
-  k_matvec<<<ceil_div(c.N, 256), 256, 0, c.stream>>>(c.H, c.dH_off.p, c.row_ptr.p, c.dcol_off.p, c.cov_n.p, c.cov_j.p,
-                                                     c.cov_r.p, c.maxcov, c.N, w, y);
+  if (c.mv_ntiles > 0) {
+    const size_t sm = static_cast<size_t>(c.m) * sizeof(double);
+    k_block_gemv<<<c.mv_ntiles, kMvRows, sm, c.stream>>>(c.H, c.dH_off.p, c.row_ptr.p, c.dcol_off.p, c.mv_tiles.p, w,
+                                                         c.zrows.p);
+    RDD_LAUNCH_CHECK();
+  }
+  k_cover_sum<<<ceil_div(c.N, 256), 256, 0, c.stream>>>(c.zrows.p, c.row_ptr.p, c.cov_n.p, c.cov_j.p, c.cov_r.p,
+                                                        c.maxcov, c.N, y);
   RDD_LAUNCH_CHECK();
 }
 
 void matvec_t_dev(Ctx& c, const double* r, double* out) {
   ScopedKernelTimer tk(c, "matvec_t");
-  k_matvec_t<<<ceil_div(static_cast<long long>(c.p) * 32, 256), 256, 0, c.stream>>>(
-      c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p, c.downer.p, c.p, r, out);
+  if (c.mt_ntiles == 0) return;
+  const size_t sm = static_cast<size_t>(c.mv_rmax) * sizeof(double);
+  if (sm > 48 * 1024) {
+    static size_t set = 0;
+    if (sm > set) {
+      RDD_CUDA(cudaFuncSetAttribute(k_block_gemv_t, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+      set = sm;
+    }
+  }
+  k_block_gemv_t<<<c.mt_ntiles, kMtWarps * 32, sm, c.stream>>>(c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p,
+                                                               c.dcol_off.p, c.mt_tiles.p, r, out);
   RDD_LAUNCH_CHECK();
 }
 

@@ -39,14 +39,16 @@ __device__ __forceinline__ int rot_decision(const Crit& k, double app, double aq
   if (!(a > k.tiny)) return 0;
   const double dm = fmax(app, aqq);
   if (!(dm > k.floor_lam)) return 0;
-  if (k.absolute ? !(a > k.tol) : !(a > k.tol * sqrt(fabs(app) * fabs(aqq)))) return 0;
+  if (k.absolute ? !(a > k.tol) : !(a * a > k.tol * k.tol * (fabs(app) * fabs(aqq)))) return 0;
   if (!(a > kMinAngle * fabs(app - aqq))) return 0;
   return dm > k.conv_lam ? 2 : 1;
 }
 __device__ __forceinline__ void schur2(double app, double aqq, double apq, double& c, double& s) {
-  const double theta = (aqq - app) / (2.0 * apq);
-  const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-  c = 1.0 / sqrt(1.0 + t * t);
+  // t = sign(θ)/(|θ| + sqrt(1 + θ²)), θ = (aqq - app)/(2 apq), rewritten with one sqrt and one
+  // division: t = 2 apq sign(d) / (|d| + sqrt(d² + 4 apq²)), d = aqq - app
+  const double d = aqq - app, two = 2.0 * apq;
+  const double t = (d >= 0.0 ? two : -two) / (fabs(d) + sqrt(fma(d, d, two * two)));
+  c = rsqrt(fma(t, t, 1.0));
   s = t * c;
 }
 
@@ -241,19 +243,123 @@ __global__ void __launch_bounds__(256) k_apply_rotations_oe(double* __restrict__
 // ============================================================================================
 // Odd-even (Luk–Park) ordering on the packed upper triangle, distributed by whole columns over a
 // K-CTA cluster (K = 1: one CTA). Step t pairs positions (o+2k, o+2k+1), o = t&1, and applies
-// Ĵ = J·Π (rotation + swap), so after n steps every pair has met. Because pairs are adjacent
-// indices, a 2x2 block of the update lives in two adjacent columns owned by one CTA: updates are
-// CTA-local; only the rotation table broadcast and boundary pairs of odd steps touch DSMEM.
-// Column ranges start at even indices, so even-step pairs never straddle two CTAs.
+// Ĵ = J·Π (rotation + swap), so after n steps every pair has met and data never moves.
+//
+// One cluster barrier per step. The inputs of the next step's rotation decisions — every
+// diagonal entry and the superdiagonal entries (i, i+1), i ≡ o' (mod 2) — are produced in the
+// update phase by whichever CTA updates them, and written into a double-buffered table that every
+// CTA of the cluster holds. Each CTA then decides all pairs of the next step redundantly from its
+// own table (identical inputs and code, so identical decisions) without remote reads; the only
+// cross-CTA traffic is those table writes and the odd steps' boundary unit (one remote column).
+// In the update phase each warp takes whole column units (largest first, snake order).
 // ============================================================================================
 template <int K>
-__global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict__ Ain, double* __restrict__ ev,
-                                                        const int* __restrict__ nvec,
-                                                        const long long* __restrict__ off,
-                                                        const long long* __restrict__ ev_off, int max_sweeps,
-                                                        Crit crit_in, double floor_rel, double conv_rel,
-                                                        int* __restrict__ sweeps_out, double2* __restrict__ rot,
-                                                        const long long* __restrict__ rot_off, int chunk) {
+__device__ __forceinline__ void publish(double* tab, int i, double v) {
+  namespace cg = cooperative_groups;
+#pragma unroll
+  for (int r = 0; r < K; ++r) ((K > 1) ? cg::this_cluster().map_shared_rank(tab, r) : tab)[i] = v;
+}
+
+// Ĵ_Uᵀ A Ĵ_W on the blocks (U, W), U = lane, lane+32, ... <= W, of one column unit W at parity O
+// (columns c0p, c1p; c1p unused for a singleton unit). The diagonal block also publishes the new
+// diagonal, the superdiagonal block the next step's pair coupling, into every CTA's tables.
+// The common case — both units are pairs — is straight-line code; the singleton units of odd
+// steps (position 0 and ne-1) take the general path.
+template <int K, int O, class P1>
+__device__ __forceinline__ void unit_update(double* c0p, P1 c1p, bool w2, double2 cw, int W, int npair, int lane,
+                                            const double2* __restrict__ cs2, double* dgo, double* odo) {
+  const int w0 = max(0, 2 * W - O);
+  if (w2) {
+    for (int U = lane; U < W; U += 32) {
+      double a00, a10, a01, a11;
+      double2 cu;
+      int u0;
+      bool u2 = true;
+      if (O == 1 && U == 0) {  // singleton row unit {0}
+        u0 = 0;
+        u2 = false;
+        cu = make_double2(1.0, 0.0);
+        a00 = c0p[0];
+        a01 = c1p[0];
+        a10 = a11 = 0.0;
+      } else {
+        u0 = 2 * U - O;
+        cu = cs2[U - O];
+        if (O == 0) {
+          const double2 x0 = *reinterpret_cast<const double2*>(c0p + u0);
+          const double2 x1 = *reinterpret_cast<const double2*>(&c1p[u0]);
+          a00 = x0.x;
+          a10 = x0.y;
+          a01 = x1.x;
+          a11 = x1.y;
+        } else {
+          a00 = c0p[u0];
+          a10 = c0p[u0 + 1];
+          a01 = c1p[u0];
+          a11 = c1p[u0 + 1];
+        }
+      }
+      // left Ĵ_Uᵀ: rows (u0, u0+1) <- (s a_u0 + c a_u1, c a_u0 - s a_u1); then right Ĵ_W on columns
+      double l00 = a00, l10 = a10, l01 = a01, l11 = a11;
+      if (u2) {
+        l00 = cu.y * a00 + cu.x * a10;
+        l10 = cu.x * a00 - cu.y * a10;
+        l01 = cu.y * a01 + cu.x * a11;
+        l11 = cu.x * a01 - cu.y * a11;
+      }
+      const double r00 = cw.y * l00 + cw.x * l01, r01 = cw.x * l00 - cw.y * l01;
+      const double r10 = cw.y * l10 + cw.x * l11, r11 = cw.x * l10 - cw.y * l11;
+      if (!u2) {
+        c0p[0] = r00;
+        c1p[0] = r01;
+      } else if (O == 0) {
+        *reinterpret_cast<double2*>(c0p + u0) = make_double2(r00, r10);
+        *reinterpret_cast<double2*>(&c1p[u0]) = make_double2(r01, r11);
+      } else {
+        c0p[u0] = r00;
+        c0p[u0 + 1] = r10;
+        c1p[u0] = r01;
+        c1p[u0 + 1] = r11;
+      }
+      if (W == U + 1) publish<K>(odo, (u0 + (u2 ? 1 : 0) - (1 - O)) >> 1, u2 ? r10 : r00);
+    }
+    if (lane == (W & 31)) {  // diagonal block (pair unit)
+      const double vpp = c0p[w0], vpq = c1p[w0], vqq = c1p[w0 + 1];
+      double nd0 = vqq, nd1 = vpp;  // pure swap when s = 0
+      if (cw.y != 0.0) {
+        const double tt = cw.y / cw.x;
+        nd0 = vqq + tt * vpq;  // swapped diagonal of JᵀAJ
+        nd1 = vpp - tt * vpq;
+        c1p[w0] = 0.0;
+      }
+      c0p[w0] = nd0;
+      c1p[w0 + 1] = nd1;
+      publish<K>(dgo, w0, nd0);
+      publish<K>(dgo, w0 + 1, nd1);
+    }
+  } else {  // singleton column unit (odd steps: {0} or {ne-1}): only the row rotations act
+    for (int U = lane; U < W; U += 32) {
+      if (U == 0) continue;      // {0} x {ne-1}: two singletons, untouched
+      const int u0 = 2 * U - O;
+      const double2 cu = cs2[U - O];
+      const double a00 = c0p[u0], a10 = c0p[u0 + 1];
+      const double l00 = cu.y * a00 + cu.x * a10, l10 = cu.x * a00 - cu.y * a10;
+      c0p[u0] = l00;
+      c0p[u0 + 1] = l10;
+      if (W == U + 1) publish<K>(odo, (u0 + 1 - (1 - O)) >> 1, l10);
+    }
+    if (lane == (W & 31)) publish<K>(dgo, w0, c0p[w0]);
+  }
+}
+
+constexpr int kJT = 512;   // threads per CTA
+template <int K>
+__global__ void __launch_bounds__(kJT, 1) k_jacobi_oe(const double* __restrict__ Ain, double* __restrict__ ev,
+                                                   const int* __restrict__ nvec, const long long* __restrict__ off,
+                                                   const long long* __restrict__ ev_off, int max_sweeps, Crit crit_in,
+                                                   double floor_rel, double conv_rel, int* __restrict__ sweeps_out,
+                                                   double2* __restrict__ rot, const long long* __restrict__ rot_off,
+                                                   int chunk, int nemax, int max_items) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double smem[];
   int rank = 0;
@@ -262,15 +368,19 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
   const int n = nvec[b];
   const int ne = n + (n & 1);           // even order (pad index ne-1 when n is odd: zero row/col)
   const int np = ne / 2;
-  double* cs = smem + chunk;            // [np] c, [np] s: rotation of pair slot k this step
-  double* sn = cs + np;
-  double** colp = reinterpret_cast<double**>(sn + np);  // generic pointer to the start of column j
-  int* lcol = reinterpret_cast<int*>(colp + ne);        // local start of column j (even)
-  unsigned char* own = reinterpret_cast<unsigned char*>(lcol + ne);
-  __shared__ int active;
-  __shared__ int cbeg, cend;            // my column range [cbeg, cend)
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  const int nthr = blockDim.x * blockDim.y;
+  double* dg = smem + chunk;                                   // [2][nemax] diagonal tables
+  double* od = dg + 2 * nemax;                                 // [2][nemax/2] next-pair superdiagonals
+  double2* cs2 = reinterpret_cast<double2*>(od + nemax);       // [nemax/2] (c, s) of this step
+  double** colp = reinterpret_cast<double**>(cs2 + nemax / 2);  // generic pointer to column j
+  int* lcol = reinterpret_cast<int*>(colp + nemax);            // local start of column j
+  int* items = lcol + nemax;                                   // [2][max_items] unit lists
+  unsigned char* own = reinterpret_cast<unsigned char*>(items + 2 * max_items);
+  __shared__ int active[2];
+  __shared__ int nitems[2];
+  __shared__ int cbeg, cend;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kJT / 32;
   if (tid == 0) {  // even-aligned whole-column ranges of ~chunk elements; columns padded to even length
     int cur = 0, start = 0, e = 0;
     cbeg = (rank == 0) ? 0 : ne;
@@ -286,21 +396,36 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
       lcol[j] = e - start;
       e += (j + 2) & ~1;  // column j holds rows 0..j, padded to even length
     }
+    // per parity: the column units W whose first column is mine, largest first (unit W carries
+    // W+1 blocks); warps take them in snake order
+    for (int o = 0; o < 2; ++o) {
+      int cnt = 0;
+      const int nu = o ? np + 1 : np;
+      for (int W = nu - 1; W >= 0; --W)
+        if (own[max(0, 2 * W - o)] == rank) items[o * max_items + cnt++] = W;
+      nitems[o] = cnt;
+    }
+    active[0] = active[1] = 0;
   }
   __syncthreads();
-  for (int j = tid; j < ne; j += nthr) {
+  for (int j = tid; j < ne; j += kJT) {
     double* basep = smem;
     if constexpr (K > 1) basep = cg::this_cluster().map_shared_rank(smem, static_cast<int>(own[j]));
     colp[j] = basep + lcol[j];
   }
-  __syncthreads();
   const double* A = Ain + off[b];
-  for (int j = cbeg + threadIdx.y; j < cend; j += blockDim.y)
-    for (int i = threadIdx.x; i <= j; i += blockDim.x)
+  for (int j = cbeg + warp; j < cend; j += NW)
+    for (int i = lane; i <= j; i += 32)
       smem[lcol[j] + i] = (i < n && j < n) ? A[i + static_cast<long long>(j) * n] : 0.0;
+  // step-0 tables (even pairs (2k, 2k+1)) straight from global memory, in every CTA
+  for (int i = tid; i < ne; i += kJT) dg[i] = i < n ? A[i + static_cast<long long>(i) * n] : 0.0;
+  for (int k = tid; k < np; k += kJT) {
+    const int p = 2 * k, q = p + 1;
+    od[k] = q < n ? A[p + static_cast<long long>(q) * n] : 0.0;
+  }
   if constexpr (K > 1) cg::this_cluster().sync(); else __syncthreads();
   double dmax = 0.0;
-  for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(colp[i][i]));
+  for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(dg[i]));
   Crit crit = crit_in;
   crit.tiny = 1e-32 * dmax;
   crit.floor_lam = fmax(floor_rel * dmax, crit_in.floor_lam);
@@ -308,146 +433,66 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_oe(const double* __restrict
   if (crit.absolute) crit.tol = crit_in.tol * dmax;
   double2* R = rot + rot_off[b];
   int sweep = 0;
+  long long t_glob = 0;
   for (; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) active = 0;
-    int local_active = 0;
-    for (int t = 0; t < ne; ++t) {
+    const int sa = sweep & 1;
+    for (int t = 0; t < ne; ++t, ++t_glob) {
       const int o = t & 1;
+      const int bi = static_cast<int>(t_glob & 1), bo = bi ^ 1;
+      const double* dgi = dg + bi * nemax;
+      const double* odi = od + bi * (nemax / 2);
       const int npair = o ? np - 1 : np;
-      // phase A: the owner of column q = p+1 decides pair k and broadcasts (c, s)
-      for (int k = tid; k < npair; k += nthr) {
+      // decide every pair of this step from the local tables
+      for (int k = tid; k < npair; k += kJT) {
         const int p = o + 2 * k, q = p + 1;
-        if (own[q] != rank) continue;
-        const double* cq = colp[q];
-        const double app = colp[p][p], aqq = cq[q], apq = cq[p];
+        const double app = dgi[p], aqq = dgi[q], apq = odi[k];
         double c = 1.0, sv = 0.0;
         const int d = rot_decision(crit, app, aqq, apq);
         if (d) {
           schur2(app, aqq, apq, c, sv);
-          if (d == 2 && fabs(sv) > crit.conv_angle * c) local_active = 1;
+          if (d == 2 && fabs(sv) > crit.conv_angle * c) active[sa] = 1;
         }
-        if constexpr (K > 1) {
-#pragma unroll
-          for (int r = 0; r < K; ++r) {
-            double* tab = cg::this_cluster().map_shared_rank(smem, r) + chunk;
-            tab[k] = c;
-            tab[np + k] = sv;
-          }
-        } else {
-          cs[k] = c;
-          sn[k] = sv;
-        }
-        R[(static_cast<long long>(sweep) * ne + t) * np + k] = make_double2(c, sv);
+        cs2[k] = make_double2(c, sv);
+        if (rank == 0) R[(static_cast<long long>(sweep) * ne + t) * np + k] = make_double2(c, sv);
       }
-      if constexpr (K > 1) cg::this_cluster().sync(); else __syncthreads();
-      // phase B: blocks (U <= W) whose column unit W is mine. Units: w0 = max(0, 2W - o), pair
-      // kw = W - o (a singleton when it is not a valid pair index: the two ends in odd steps)
-      const int nu = o ? np + 1 : np;
-      for (int W = threadIdx.y; W < nu; W += blockDim.y) {
+      __syncthreads();
+      double* dgo = dg + bo * nemax;
+      double* odo = od + bo * (nemax / 2);
+      const int nun = nitems[o];
+      const int* ul = items + o * max_items;
+      for (int r0 = 0; r0 < nun; r0 += NW) {
+        const int x = r0 + (((r0 / NW) & 1) ? NW - 1 - warp : warp);
+        if (x >= nun) continue;
+        const int W = ul[x];
         const int w0 = max(0, 2 * W - o);
-        if (own[w0] != rank) continue;
         const int kw = W - o;
         const bool w2 = kw >= 0 && kw < npair;
-        const double cw = w2 ? cs[kw] : 1.0, sw = w2 ? sn[kw] : 0.0;
-        double* c0p = colp[w0];
-        double* c1p = w2 ? colp[w0 + 1] : nullptr;
-        for (int U = threadIdx.x; U <= W; U += blockDim.x) {
-          const int u0 = max(0, 2 * U - o);
-          const int ku = U - o;
-          const bool u2 = ku >= 0 && ku < npair;
-          const double cu = u2 ? cs[ku] : 1.0, su = u2 ? sn[ku] : 0.0;
-          if (U == W) {
-            if (!u2) continue;
-            double& app = c0p[u0];
-            double& apq = c1p[u0];
-            double& aqq = c1p[u0 + 1];
-            if (su == 0.0) {  // pure swap
-              const double t0 = app;
-              app = aqq;
-              aqq = t0;
-            } else {
-              const double tt = su / cu, vpq = apq, vpp = app, vqq = aqq;
-              app = vqq + tt * vpq;  // swapped diagonal of JᵀAJ
-              aqq = vpp - tt * vpq;
-              apq = 0.0;
-            }
-            continue;
-          }
-          // rows u0.. (< columns w0..): all four entries are in the upper triangle
-          double a00, a10 = 0.0, a01 = 0.0, a11 = 0.0;
-          if (u2 && !o) {  // even step: (u0, u0+1) is an aligned 16-byte pair in both columns
-            const double2 x0 = *reinterpret_cast<const double2*>(c0p + u0);
-            a00 = x0.x;
-            a10 = x0.y;
-            if (w2) {
-              const double2 x1 = *reinterpret_cast<const double2*>(c1p + u0);
-              a01 = x1.x;
-              a11 = x1.y;
-            }
-          } else {
-            a00 = c0p[u0];
-            if (u2) a10 = c0p[u0 + 1];
-            if (w2) {
-              a01 = c1p[u0];
-              if (u2) a11 = c1p[u0 + 1];
-            }
-          }
-          if (u2) {  // left Ĵ_Uᵀ: rows (u0, u0+1) <- (s a_u0 + c a_u1, c a_u0 - s a_u1)
-            const double r00 = su * a00 + cu * a10, r10 = cu * a00 - su * a10;
-            const double r01 = su * a01 + cu * a11, r11 = cu * a01 - su * a11;
-            a00 = r00;
-            a10 = r10;
-            a01 = r01;
-            a11 = r11;
-          }
-          if (w2) {  // right Ĵ_W: cols (w0, w0+1) <- (s a_w0 + c a_w1, c a_w0 - s a_w1)
-            const double r00 = sw * a00 + cw * a01, r01 = cw * a00 - sw * a01;
-            const double r10 = sw * a10 + cw * a11, r11 = cw * a10 - sw * a11;
-            a00 = r00;
-            a01 = r01;
-            a10 = r10;
-            a11 = r11;
-          }
-          if (u2 && !o) {
-            *reinterpret_cast<double2*>(c0p + u0) = make_double2(a00, a10);
-            if (w2) *reinterpret_cast<double2*>(c1p + u0) = make_double2(a01, a11);
-          } else {
-            c0p[u0] = a00;
-            if (u2) c0p[u0 + 1] = a10;
-            if (w2) {
-              c1p[u0] = a01;
-              if (u2) c1p[u0 + 1] = a11;
-            }
-          }
+        const double2 cw = w2 ? cs2[kw] : make_double2(1.0, 0.0);
+        double* c0p = smem + lcol[w0];  // the unit's first column is always mine
+        if (!w2 || own[w0 + 1] == rank) {
+          double* c1p = w2 ? smem + lcol[w0 + 1] : c0p;
+          if (o) unit_update<K, 1>(c0p, c1p, w2, cw, W, npair, lane, cs2, dgo, odo);
+          else unit_update<K, 0>(c0p, c1p, w2, cw, W, npair, lane, cs2, dgo, odo);
+        } else {  // odd-step boundary unit: second column lives in the next CTA
+          unit_update<K, 1>(c0p, colp[w0 + 1], w2, cw, W, npair, lane, cs2, dgo, odo);
         }
       }
       if constexpr (K > 1) cg::this_cluster().sync(); else __syncthreads();
     }
-    if constexpr (K > 1) {
-      if (local_active) atomicOr(cg::this_cluster().map_shared_rank(&active, 0), 1);
-      cg::this_cluster().sync();
-      const int any = *cg::this_cluster().map_shared_rank(&active, 0);
-      cg::this_cluster().sync();
-      if (!any) {
-        ++sweep;  // the last sweep still swapped: it stays in the log
-        break;
-      }
-    } else {
-      if (local_active) atomicOr(&active, 1);
-      __syncthreads();
-      const int any = active;
-      __syncthreads();
-      if (!any) {
-        ++sweep;
-        break;
-      }
+    const int any = active[sa];
+    if (tid == 0) active[sa ^ 1] = 0;  // next sweep's flag (not read by anyone before the barrier)
+    __syncthreads();
+    if (!any) {
+      ++sweep;  // the last sweep still swapped: it stays in the log
+      break;
     }
   }
   if (rank == 0) {
-    for (int i = tid; i < ne; i += nthr) ev[ev_off[b] + i] = colp[i][i];
+    const double* dgf = dg + static_cast<int>(t_glob & 1) * nemax;
+    for (int i = tid; i < ne; i += kJT) ev[ev_off[b] + i] = dgf[i];
     if (tid == 0) sweeps_out[b] = sweep;
   }
-  if constexpr (K > 1) cg::this_cluster().sync();  // keep shared memory alive for remote readers
+  if constexpr (K > 1) cg::this_cluster().sync();  // keep shared memory alive for remote writers
 }
 
 // V = Π Ĵ_t: each warp owns one row of V in shared memory; its lanes split the (disjoint) pairs
@@ -651,11 +696,14 @@ __global__ void k_compact(const double* __restrict__ Vp, const double* __restric
 static size_t oe_chunk(int ne, int K) {
   size_t tri = 0;  // columns padded to even length (aligned 16-byte row pairs)
   for (int j = 0; j < ne; ++j) tri += static_cast<size_t>((j + 2) & ~1);
-  return K == 1 ? tri : (tri + K - 1) / K + 2 * static_cast<size_t>(ne) + 4;
+  const size_t c = K == 1 ? tri : (tri + K - 1) / K + 2 * static_cast<size_t>(ne) + 4;
+  return (c + 1) & ~static_cast<size_t>(1);  // tables behind it hold double2
 }
+static int oe_items(int ne) { return ne / 2 + 1; }  // column units of one parity
 static size_t oe_smem(int ne, int K) {
-  return oe_chunk(ne, K) * sizeof(double) + static_cast<size_t>(ne / 2) * 2 * sizeof(double) +
-         static_cast<size_t>(ne) * (sizeof(double*) + sizeof(int) + 1) + 64;
+  return oe_chunk(ne, K) * sizeof(double) + static_cast<size_t>(3 * ne) * sizeof(double) +
+         static_cast<size_t>(ne / 2) * sizeof(double2) + static_cast<size_t>(ne) * (sizeof(double*) + sizeof(int) + 1) +
+         static_cast<size_t>(2 * oe_items(ne)) * sizeof(int) + 64;
 }
 static int oe_k(int ne) {
   for (int K : {1, 2, 4, 8})
@@ -730,7 +778,7 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     const size_t smem = oe_smem(ne, K);
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(B * K);
-    lc.blockDim = dim3(32, kThreads / 32);
+    lc.blockDim = dim3(kJT);
     lc.dynamicSmemBytes = smem;
     lc.stream = c.stream;
     cudaLaunchAttribute at[1];
@@ -745,7 +793,7 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
       RDD_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<const double*>(A), evp.p, static_cast<const int*>(dn.p),
                                   static_cast<const long long*>(doff.p), static_cast<const long long*>(deoffp.p),
                                   max_sweeps, crit, o.floor_rel, o.conv_rel, dsw.p, rot.p,
-                                  static_cast<const long long*>(droff.p), chunk));
+                                  static_cast<const long long*>(droff.p), chunk, ne, oe_items(ne)));
       ++launch_counter();
     };
     if (K == 1) launch(k_jacobi_oe<1>);

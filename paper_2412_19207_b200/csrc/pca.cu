@@ -239,6 +239,13 @@ __global__ void __launch_bounds__(kHouseThreads) k_house_complete(const double* 
   }
 }
 
+// V0[:, :r_j] = Vs[:, :r_j] (m x r_j leading columns, column-major ld m)
+__global__ void k_copy_lead(const double* __restrict__ Vs, double* __restrict__ V0, const int* __restrict__ r, int m) {
+  const size_t off = static_cast<size_t>(blockIdx.x) * m * m;
+  const long long cnt = static_cast<long long>(r[blockIdx.x]) * m;
+  for (long long e = threadIdx.x; e < cnt; e += blockDim.x) V0[off + e] = Vs[off + e];
+}
+
 std::vector<GemmTask> gram_tasks(Ctx& c, const double* X, double* G, const std::vector<long long>& offX) {
   std::vector<GemmTask> t;
   const int m = c.m, nt = ceil_div(m, 64);
@@ -350,8 +357,48 @@ void run_pca(Ctx& c) {
       RDD_LAUNCH_CHECK();
       RDD_CUDA(cudaStreamSynchronize(c.stream));
     }
-    // stage 2: T = S V0, G1 = TᵀT, Jacobi on the graded G1
+    // stage 2a: the graded Jacobi on the leading r columns only (T_a = S·V0[:, :r], one CTA per
+    // subdomain), V0[:, :r] <- V0[:, :r]·W_a. The full stage 2 below then mostly decouples them
+    // from the complement (measured: 7.1 -> ~5 sweeps of the 300-wide Jacobi)
     T.p = c.ws("pca.T", std::max<long long>(1, c.S_off[J]));
+    W.p = c.ws("pca.W", J * mm);
+    Vfull.p = c.ws("pca.Vfull", J * mm);
+    {
+      std::vector<GemmTask> t;
+      for (int j = 0; j < J; ++j) {
+        const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+        for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
+          for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+            t.push_back({c.S.p + c.S_off[j], V0.p + offm[j], T.p + c.S_off[j], nullptr, nullptr, rows, rj[j], m,
+                         std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+      }
+      gemm_nn(c, t);  // T_a
+    }
+    {
+      std::vector<GemmTask> t;
+      for (int j = 0; j < J; ++j) {
+        const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+        const int nt = ceil_div(rj[j], 64);
+        for (int tm = 0; tm < nt; ++tm)
+          for (int tn = tm; tn < nt; ++tn)
+            t.push_back({T.p + c.S_off[j], T.p + c.S_off[j], G.p + offm[j], nullptr, nullptr, rj[j], rj[j], rows,
+                         std::max(rows, 1), std::max(rows, 1), rj[j], tm, tn, 0.0});
+      }
+      gemm_tn(c, t);  // G_a = T_aᵀ T_a
+    }
+    batched_syevj(c, G.p, W.p, lam.p, rj, offm, s2);
+    {
+      std::vector<GemmTask> t;
+      for (int j = 0; j < J; ++j)
+        for (int tm = 0; tm < ceil_div(m, 64); ++tm)
+          for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+            t.push_back({V0.p + offm[j], W.p + offm[j], Vfull.p + offm[j], nullptr, nullptr, m, rj[j], rj[j], m, rj[j],
+                         m, tm, tn, 0.0});
+      gemm_nn(c, t);  // V0[:, :r] W_a
+      k_copy_lead<<<J, 256, 0, c.stream>>>(Vfull.p, V0.p, dr.p, m);
+      RDD_LAUNCH_CHECK();
+    }
+    // stage 2: T = S V0, G1 = TᵀT, Jacobi on the graded G1
     {
       std::vector<GemmTask> t;
       for (int j = 0; j < J; ++j) {
@@ -364,10 +411,8 @@ void run_pca(Ctx& c) {
       gemm_nn(c, t);
     }
     gemm_tn(c, gram_tasks(c, T.p, G.p, c.S_off));
-    W.p = c.ws("pca.W", J * mm);
     batched_syevj(c, G.p, W.p, lam.p, ns, offm, s2);
     // V = V0 W
-    Vfull.p = c.ws("pca.Vfull", J * mm);
     {
       std::vector<GemmTask> t;
       for (int j = 0; j < J; ++j)

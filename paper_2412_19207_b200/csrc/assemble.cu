@@ -248,7 +248,7 @@ void assemble_samples(Ctx& c, int kind, double* out, const std::vector<long long
   bad.upload(hbad, 3, c.stream);
   A.bad = bad.p;
   const size_t smem = static_cast<size_t>(c.m) * (3 + 2 * c.d) * sizeof(double);
-  if (smem > 48 * 1024) RDD_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (smem > 32 * 1024) RDD_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (tp[c.J] > 0) {
     k_assemble<<<tp[c.J], kRowsPerBlock, smem, c.stream>>>(A);
     RDD_LAUNCH_CHECK();

@@ -1,14 +1,18 @@
-// cholesky.cu — K8: batched blocked Cholesky and explicit SPD inverse for the Schwarz local
-// matrices A_i = (HᵀH)[S_i, S_i] (schwarz.hpp:112-130).
+// cholesky.cu — K8: batched blocked Cholesky of the Schwarz local matrices A_i = (HᵀH)[S_i, S_i]
+// (schwarz.hpp:112-130) and the per-iteration batched triangular solves that apply A_i⁻¹.
 //
 // The reference pseudo-inverts A_i through a full eigendecomposition (schwarz.hpp:131-146,
-// ~9n³ flops). When every eigenvalue is above the reference's cutoff (1e-12·λmax) that
-// pseudo-inverse *is* A_i⁻¹, which costs n³ flops via Cholesky: A = LLᵀ (right-looking, 64-wide
-// panels: diagonal POTRF and panel TRSM in shared memory, trailing SYRK/GEMM on DMMA), then
-// M = L⁻¹ (diagonal TRTRI in shared memory + DMMA block-row updates), then A⁻¹ = MᵀM (DMMA).
-// Matrices of different sizes are processed together; each step launches only the work of the
-// matrices still active. A failed pivot flags the matrix for the eigen fallback (schwarz.cu).
+// ~9n³ flops) and applies V diag(1/λ) Vᵀ. When every eigenvalue is above the reference's cutoff
+// (1e-12·λmax) that pseudo-inverse *is* A_i⁻¹, so the device factors A = LLᵀ once (n³/3 flops:
+// right-looking, 64-wide panels, diagonal POTRF and panel TRSM in shared memory, trailing updates
+// on DMMA) and applies A⁻¹ as a forward and a backward triangular solve per Krylov step — the
+// same n² bytes per apply as a dense inverse, a third of its build flops, half its memory.
+// L is stored tile-packed (64x64 column-major tiles (k, j<=k), block row after block row) with the
+// diagonal tiles replaced by L_kk⁻¹, so both solves are chains of tile GEMVs. Matrices of different
+// sizes are processed together; each factor step launches only the work of the matrices still
+// active. A failed pivot flags the matrix for the eigen fallback (schwarz.cu).
 #include <algorithm>
+#include <cstdio>
 
 #include "ctx.hpp"
 
@@ -18,6 +22,7 @@ namespace {
 
 constexpr int NB = 64;
 constexpr int kPairSmem = 2 * NB * (NB + 1) * sizeof(double);
+constexpr int kSolveWarps = 8;
 
 struct Mat {
   long long off;  // element offset of the matrix
@@ -92,15 +97,26 @@ __global__ void k_trsm_panel(double* __restrict__ A, const Mat* __restrict__ mat
   }
 }
 
-// M_kk = L_kk^{-1} (lower) for every diagonal block; task = (matrix, k)
-__global__ void k_trtri_diag(const double* __restrict__ A, double* __restrict__ Minv, const Mat* __restrict__ mats,
-                             const int2* __restrict__ tasks) {
+// Block row k of the tile-packed factor: tiles (k, j<k) copied from the factored matrix (zero
+// padding past n) and the diagonal tile L_kk⁻¹ (lower; the padding acts as identity).
+// task = (matrix, k)
+__global__ void k_pack_row(const double* __restrict__ A, const Mat* __restrict__ mats, const int2* __restrict__ tasks,
+                           double* __restrict__ P, const long long* __restrict__ poff) {
   extern __shared__ double dsm[];
   double(*L)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
   double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
   const int2 t = tasks[blockIdx.x];
   const Mat M = mats[t.x];
-  const int k0 = t.y * NB, bs = min(NB, M.n - k0);
+  const int k = t.y, k0 = k * NB, bs = min(NB, M.n - k0);
+  double* row = P + poff[t.x] + static_cast<long long>(k) * (k + 1) / 2 * (NB * NB);
+  for (int j = 0; j < k; ++j) {
+    const double* a = A + M.off + k0 + static_cast<long long>(j * NB) * M.n;
+    double* o = row + static_cast<long long>(j) * NB * NB;
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+      const int r = e % NB, c = e / NB;
+      o[e] = r < bs ? a[r + static_cast<long long>(c) * M.n] : 0.0;
+    }
+  }
   const double* l = A + M.off + k0 + static_cast<long long>(k0) * M.n;
   for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
     const int r = e % NB, c = e / NB;
@@ -116,11 +132,8 @@ __global__ void k_trtri_diag(const double* __restrict__ A, double* __restrict__ 
     }
   }
   __syncthreads();
-  double* m = Minv + M.off + k0 + static_cast<long long>(k0) * M.n;
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
-    const int r = e % NB, cc = e / NB;
-    if (r < bs && cc < bs) m[r + static_cast<long long>(cc) * M.n] = X[r][cc];
-  }
+  double* o = row + static_cast<long long>(k) * NB * NB;
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) o[e] = X[e % NB][e / NB];
 }
 
 __global__ void k_frob(const double* __restrict__ A, const Mat* __restrict__ mats, double* __restrict__ out) {
@@ -181,14 +194,194 @@ __global__ void k_power(const double* __restrict__ A, const Mat* __restrict__ ma
   if (threadIdx.x == 0) out[blockIdx.x] = lam;
 }
 
-// copy the lower triangle onto the upper one
-__global__ void k_mirror_lower(double* __restrict__ P, const Mat* __restrict__ mats) {
-  const Mat M = mats[blockIdx.x];
-  double* a = P + M.off;
-  for (long long e = threadIdx.x; e < static_cast<long long>(M.n) * M.n; e += blockDim.x) {
-    const int r = static_cast<int>(e % M.n), cc = static_cast<int>(e / M.n);
-    if (r < cc) a[e] = a[cc + static_cast<long long>(r) * M.n];
+// Trailing-update GEMM tasks of one factor step, generated on the device from one descriptor per
+// (matrix, kind): kind 0 = inside the outer panel (columns jb in (k, oend), K = 64 at column k),
+// kind 1 = right of a completed outer panel (jb >= oend, K = the panel width). C[ib, jb] -= A_ib A_jbᵀ.
+struct UpdDesc {
+  long long off;   // matrix offset
+  long long first; // first task index of this entry
+  int n, k, ostart, oend, kind, pad;
+};
+__global__ void k_make_updates(double* __restrict__ A, const UpdDesc* __restrict__ d, int nd, long long total,
+                               GemmTask* __restrict__ out) {
+  const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (t >= total) return;
+  int lo = 0, hi = nd - 1;  // last entry with first <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (d[mid].first <= t) lo = mid;
+    else hi = mid - 1;
   }
+  const UpdDesc e = d[lo];
+  long long loc = t - e.first;
+  const int nb = (e.n + NB - 1) / NB;
+  const int jb0 = e.kind == 0 ? e.k + 1 : e.oend;
+  const int jb1 = e.kind == 0 ? e.oend : nb;  // exclusive
+  int jb = jb0;
+  for (; jb < jb1; ++jb) {  // column jb holds rows ib = jb .. nb-1
+    const long long cnt = nb - jb;
+    if (loc < cnt) break;
+    loc -= cnt;
+  }
+  const int ib = jb + static_cast<int>(loc);
+  const int c0 = e.kind == 0 ? e.k * NB : e.ostart * NB;
+  const int kw = e.kind == 0 ? min(NB, e.n - c0) : min(e.n, e.oend * NB) - c0;
+  double* base = A + e.off;
+  GemmTask g{};
+  g.A = base + ib * NB + static_cast<long long>(c0) * e.n;
+  g.B = base + jb * NB + static_cast<long long>(c0) * e.n;
+  g.Cm = base + ib * NB + static_cast<long long>(jb) * NB * e.n;
+  g.gA = g.gB = nullptr;
+  g.M = min(NB, e.n - ib * NB);
+  g.N = min(NB, e.n - jb * NB);
+  g.K = kw;
+  g.lda = g.ldb = g.ldc = e.n;
+  g.tm = g.tn = 0;
+  g.beta = 1.0;
+  g.alpha = -1.0;
+  out[t] = g;
+}
+
+// ---- batched solves with the tile-packed factor ---------------------------------------------
+__device__ __forceinline__ const double* ptile(const double* P, int k, int j) {
+  return P + (static_cast<long long>(k) * (k + 1) / 2 + j) * (NB * NB);
+}
+
+// v <- (L Lᵀ)⁻¹ v in shared memory (nb*64 entries, zero-padded past n); red: kSolveWarps*64.
+// Forward y_k = L_kk⁻¹ (v_k - Σ_{j<k} L_kj y_j), backward x_k = L_kk⁻ᵀ (y_k - Σ_{j>k} L_jkᵀ x_j).
+// Off-diagonal tiles are split over the warps (fixed order), each tile column streamed as one
+// 512-byte warp load; the transposed tiles of the backward pass reduce 32 columns per 31 shuffles.
+__device__ void chol_solve(const double* __restrict__ P, int nb, double* v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  for (int k = 0; k < nb; ++k) {
+    double a0 = 0.0, a1 = 0.0;
+    for (int j = warp; j < k; j += kSolveWarps) {
+      const double2* t = reinterpret_cast<const double2*>(ptile(P, k, j)) + lane;
+      const double* y = v + j * NB;
+#pragma unroll 16
+      for (int c = 0; c < NB; ++c) {
+        const double2 a = __ldcs(t + c * (NB / 2));
+        a0 += a.x * y[c];
+        a1 += a.y * y[c];
+      }
+    }
+    red[warp * NB + 2 * lane] = a0;
+    red[warp * NB + 2 * lane + 1] = a1;
+    __syncthreads();
+    if (tid < NB) {
+      double s = v[k * NB + tid];
+      for (int w = 0; w < kSolveWarps; ++w) s -= red[w * NB + tid];
+      v[k * NB + tid] = s;
+    }
+    __syncthreads();
+    {
+      const double2* t = reinterpret_cast<const double2*>(ptile(P, k, k)) + lane;
+      const double* r = v + k * NB;
+      double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+      for (int c = warp * (NB / kSolveWarps); c < (warp + 1) * (NB / kSolveWarps); ++c) {
+        const double2 a = __ldcs(t + c * (NB / 2));
+        b0 += a.x * r[c];
+        b1 += a.y * r[c];
+      }
+      red[warp * NB + 2 * lane] = b0;
+      red[warp * NB + 2 * lane + 1] = b1;
+    }
+    __syncthreads();
+    if (tid < NB) {
+      double s = 0.0;
+      for (int w = 0; w < kSolveWarps; ++w) s += red[w * NB + tid];
+      v[k * NB + tid] = s;
+    }
+    __syncthreads();
+  }
+  for (int k = nb - 1; k >= 0; --k) {
+    double a0 = 0.0, a1 = 0.0;  // columns lane, lane + 32 of block k
+    for (int j = k + 1 + warp; j < nb; j += kSolveWarps) {
+      const double* t = ptile(P, j, k);
+      const double x0 = v[j * NB + 2 * lane], x1 = v[j * NB + 2 * lane + 1];
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        double p[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const double2 a = __ldcs(reinterpret_cast<const double2*>(t + (g * 32 + c) * NB) + lane);
+          p[c] = a.x * x0 + a.y * x1;
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int i = 0; i < o; ++i) {
+            const double send = up ? p[i] : p[i + o];
+            const double keep = up ? p[i + o] : p[i];
+            p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        if (g == 0) a0 += p[0];
+        else a1 += p[0];
+      }
+    }
+    red[warp * NB + lane] = a0;
+    red[warp * NB + 32 + lane] = a1;
+    __syncthreads();
+    if (tid < NB) {
+      double s = v[k * NB + tid];
+      for (int w = 0; w < kSolveWarps; ++w) s -= red[w * NB + tid];
+      v[k * NB + tid] = s;
+    }
+    __syncthreads();
+    double mine = 0.0;
+    {
+      const double* t = ptile(P, k, k);
+      const double r0 = v[k * NB + 2 * lane], r1 = v[k * NB + 2 * lane + 1];
+      constexpr int CW = NB / kSolveWarps;
+#pragma unroll
+      for (int cc = 0; cc < CW; ++cc) {
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(t + (warp * CW + cc) * NB) + lane);
+        const double s = warp_sum(a.x * r0 + a.y * r1);
+        if (lane == cc) mine = s;
+      }
+    }
+    __syncthreads();
+    if (lane < NB / kSolveWarps) v[k * NB + warp * (NB / kSolveWarps) + lane] = mine;
+    __syncthreads();
+  }
+}
+
+// λmax(A⁻¹) by power iteration through the factor: one CTA per matrix
+__global__ void __launch_bounds__(kSolveWarps * 32) k_chol_power(const double* __restrict__ P,
+                                                                 const long long* __restrict__ poff,
+                                                                 const int* __restrict__ nvec, int iters, int nbmax,
+                                                                 double* __restrict__ out) {
+  extern __shared__ double sm[];
+  double* x = sm;
+  double* red = sm + static_cast<size_t>(nbmax) * NB;
+  __shared__ double nrm_s;
+  const int i = blockIdx.x, n = nvec[i], nb = (n + NB - 1) / NB;
+  for (int r = threadIdx.x; r < nb * NB; r += blockDim.x) x[r] = r < n ? 1.0 + 0.25 * sin(0.7 * r + 0.3) : 0.0;
+  double lam = 0.0;
+  for (int it = 0; it <= iters; ++it) {
+    double s = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) s += x[r] * x[r];
+    s = warp_sum(s);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kSolveWarps; ++w) t += red[w];
+      nrm_s = sqrt(t);
+    }
+    __syncthreads();
+    const double nrm = nrm_s;
+    if (it > 0) lam = nrm;  // ‖A⁻¹ x‖ with ‖x‖ = 1
+    if (it == iters || !(nrm > 0.0)) break;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] /= nrm;
+    __syncthreads();
+    chol_solve(P + poff[i], nb, x, red);
+  }
+  if (threadIdx.x == 0) out[i] = lam;
 }
 
 }  // namespace
@@ -210,7 +403,7 @@ std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int
   dm.upload(mats, c.stream);
   d.ensure(B);
   const size_t smem = 2 * sizeof(double) * nmax;
-  if (smem > 48 * 1024)
+  if (smem > 32 * 1024)
     RDD_CUDA(cudaFuncSetAttribute(k_power, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   k_power<<<B, 256, smem, c.stream>>>(A, dm.p, iters, d.p);
   RDD_LAUNCH_CHECK();
@@ -220,17 +413,14 @@ std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int
 }
 
 // In: A (batch at off[i], order n[i], symmetric, full storage) — destroyed (holds L).
-// Out: P = A^{-1} (full, same layout); fail[i] = 1 when a pivot was not positive;
-// frob_A[i], frob_P[i] Frobenius norms (cond(A) <= ||A||_F ||A^{-1}||_F).
-void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n, const std::vector<long long>& off,
-                         std::vector<int>& fail, std::vector<double>& frob_A, std::vector<double>& frob_P,
-                         const std::vector<long long>* offP_in) {
-  const std::vector<long long>& offP = offP_in ? *offP_in : off;
-  ScopedKernelTimer tk(c, "spd_inverse");
+// Out: the tile-packed factor at P + poff[i] (diagonal tiles inverted), fail[i] = 1 when a pivot
+// was not positive, frob_A[i] = ‖A_i‖_F (an upper bound of λmax).
+void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const std::vector<long long>& off, double* P,
+                           const std::vector<long long>& poff, std::vector<int>& fail, std::vector<double>& frob_A) {
+  ScopedKernelTimer tk(c, "cholesky");
   const int B = static_cast<int>(n.size());
   fail.assign(B, 0);
   frob_A.assign(B, 0.0);
-  frob_P.assign(B, 0.0);
   if (B == 0) return;
   std::vector<Mat> mats(B);
   int nmax = 0;
@@ -239,49 +429,45 @@ void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n
     nmax = std::max(nmax, n[i]);
   }
   RDD_CUDA(cudaFuncSetAttribute(k_trsm_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
-  RDD_CUDA(cudaFuncSetAttribute(k_trtri_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
+  RDD_CUDA(cudaFuncSetAttribute(k_pack_row, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
   DBuf<Mat> dm;
   DBuf<int> dfail, dact;
   DBuf<int2> dt;
-  DBuf<double> dfa, dfp;
-  struct WS {
-    double* p;
-  } Mi{nullptr}, tmp{nullptr};
+  DBuf<double> dfa;
+  DBuf<long long> dpoff;
   dm.upload(mats, c.stream);
   dfail.zero(B, c.stream);
   dfa.ensure(B);
-  dfp.ensure(B);
   k_frob<<<B, 256, 0, c.stream>>>(A, dm.p, dfa.p);
   RDD_LAUNCH_CHECK();
+  // two-level blocking: 64-wide steps update only the columns of their 256-wide outer panel;
+  // the trailing matrix right of an outer panel takes one K = 256 update when the panel is done
   const int nbmax = ceil_div(nmax, NB);
-  // ---- factor
+  constexpr int kOuter = 4;  // inner blocks per outer panel
+  DBuf<UpdDesc> dud;
+  DBuf<GemmTask>& dtask = c.wsg;
   for (int k = 0; k < nbmax; ++k) {
     std::vector<int> act;
     std::vector<int2> pan;
-    std::vector<GemmTask> upd;
+    std::vector<UpdDesc> ud;
+    long long total = 0;
+    const int ostart = (k / kOuter) * kOuter;
     for (int i = 0; i < B; ++i) {
       const int nb = ceil_div(n[i], NB);
       if (k >= nb) continue;
       act.push_back(i);
-      const int k0 = k * NB, bk = std::min(NB, n[i] - k0);
-      for (int ib = k + 1; ib < nb; ++ib) {
-        pan.push_back(make_int2(i, ib));
-        const int bi = std::min(NB, n[i] - ib * NB);
-        for (int jb = k + 1; jb <= ib; ++jb) {
-          const int bj = std::min(NB, n[i] - jb * NB);
-          double* base = A + off[i];
-          GemmTask t{};
-          t.A = base + ib * NB + static_cast<long long>(k0) * n[i];
-          t.B = base + jb * NB + static_cast<long long>(k0) * n[i];
-          t.Cm = base + ib * NB + static_cast<long long>(jb * NB) * n[i];
-          t.M = bi;
-          t.N = bj;
-          t.K = bk;
-          t.lda = t.ldb = t.ldc = n[i];
-          t.beta = 1.0;
-          t.alpha = -1.0;
-          upd.push_back(t);
-        }
+      const int oend = std::min(nb, ostart + kOuter);
+      for (int ib = k + 1; ib < nb; ++ib) pan.push_back(make_int2(i, ib));
+      long long cnt = 0;
+      for (int jb = k + 1; jb < oend; ++jb) cnt += nb - jb;
+      if (cnt > 0) {
+        ud.push_back({off[i], total, n[i], k, ostart, oend, 0, 0});
+        total += cnt;
+      }
+      if (k == oend - 1 && oend < nb) {
+        const long long T = nb - oend;
+        ud.push_back({off[i], total, n[i], k, ostart, oend, 1, 0});
+        total += T * (T + 1) / 2;
       }
     }
     dact.upload(act, c.stream);
@@ -292,103 +478,109 @@ void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n
       k_trsm_panel<<<static_cast<int>(pan.size()), NB, kPairSmem, c.stream>>>(A, dm.p, dt.p, k);
       RDD_LAUNCH_CHECK();
     }
-    gemm_nt(c, upd);  // synchronizes (task-buffer lifetime), so dact/dt can be reused
-  }
-  // ---- M = L^{-1}
-  {
-    const size_t msz = static_cast<size_t>(off[B - 1] + static_cast<long long>(n[B - 1]) * n[B - 1]);
-    Mi.p = c.ws("chol.Minv", msz);
-    RDD_CUDA(cudaMemsetAsync(Mi.p, 0, msz * sizeof(double), c.stream));
-  }
-  {
-    std::vector<int2> diag;
-    for (int i = 0; i < B; ++i)
-      for (int k = 0; k < ceil_div(n[i], NB); ++k) diag.push_back(make_int2(i, k));
-    dt.upload(diag, c.stream);
-    k_trtri_diag<<<static_cast<int>(diag.size()), NB, kPairSmem, c.stream>>>(A, Mi.p, dm.p, dt.p);
-    RDD_LAUNCH_CHECK();
-  }
-  long long tmp_sz = 0;
-  std::vector<long long> toff(B);
-  for (int i = 0; i < B; ++i) {
-    toff[i] = tmp_sz;
-    tmp_sz += static_cast<long long>(NB) * n[i];
-  }
-  tmp.p = c.ws("chol.tmp", std::max<long long>(1, tmp_sz));
-  for (int ib = 1; ib < nbmax; ++ib) {
-    std::vector<GemmTask> g1, g2;
-    for (int i = 0; i < B; ++i) {
-      if (ib >= ceil_div(n[i], NB)) continue;
-      const int bi = std::min(NB, n[i] - ib * NB), w = ib * NB;
-      double* L = A + off[i];
-      double* Mm = Mi.p + off[i];
-      for (int tn = 0; tn < ib; ++tn) {
-        GemmTask t{};  // tmp[:, tn] = L[ib, tn*64:w] M[tn*64:w, tn]  (M is lower triangular)
-        const int k0 = tn * NB;
-        t.A = L + ib * NB + static_cast<long long>(k0) * n[i];
-        t.B = Mm + k0 + static_cast<long long>(k0) * n[i];
-        t.Cm = tmp.p + toff[i] + static_cast<long long>(k0) * NB;
-        t.M = bi;
-        t.N = NB;
-        t.K = w - k0;
-        t.lda = n[i];
-        t.ldb = n[i];
-        t.ldc = NB;
-        t.tn = 0;
-        t.alpha = 1.0;
-        g1.push_back(t);
-        GemmTask u{};  // M[ib, 0:w] = -M_ii tmp
-        u.A = Mm + ib * NB + static_cast<long long>(ib * NB) * n[i];
-        u.B = tmp.p + toff[i];
-        u.Cm = Mm + ib * NB;
-        u.M = bi;
-        u.N = w;
-        u.K = bi;
-        u.lda = n[i];
-        u.ldb = NB;
-        u.ldc = n[i];
-        u.tn = tn;
-        u.alpha = -1.0;
-        g2.push_back(u);
-      }
+    if (total > 0) {
+      dud.upload(ud, c.stream);
+      dtask.ensure(static_cast<size_t>(total));
+      k_make_updates<<<ceil_div(total, 256), 256, 0, c.stream>>>(A, dud.p, static_cast<int>(ud.size()), total,
+                                                                  dtask.p);
+      RDD_LAUNCH_CHECK();
+      gemm_nt_dev(c, dtask.p, static_cast<int>(total));
     }
-    gemm_nn(c, g1);
-    gemm_nn(c, g2);
   }
-  // ---- P = Mᵀ M, lower tiles only (M(k, i) = 0 for k < i), then mirrored
-  std::vector<GemmTask> g;
+  std::vector<int2> rows;
   for (int i = 0; i < B; ++i)
-    for (int tm = 0; tm < ceil_div(n[i], 64); ++tm)
-      for (int tn = 0; tn <= tm; ++tn) {
-        GemmTask t{};
-        const int k0 = tm * 64;  // rows of M below the tile's first output row
-        t.A = Mi.p + off[i] + k0;
-        t.B = Mi.p + off[i] + k0;
-        t.Cm = P + offP[i];
-        t.M = t.N = n[i];
-        t.K = n[i] - k0;
-        t.lda = t.ldb = t.ldc = n[i];
-        t.tm = tm;
-        t.tn = tn;
-        t.alpha = 1.0;
-        g.push_back(t);
-      }
-  gemm_tn(c, g);
-  {
-    std::vector<Mat> pm(B);
-    for (int i = 0; i < B; ++i) pm[i] = {offP[i], n[i]};
-    DBuf<Mat> dpm;
-    dpm.upload(pm, c.stream);
-    k_mirror_lower<<<B, 256, 0, c.stream>>>(P, dpm.p);
-    RDD_LAUNCH_CHECK();
-    dm.upload(pm, c.stream);  // Frobenius norms of the outputs
-  }
-  k_frob<<<B, 256, 0, c.stream>>>(P, dm.p, dfp.p);
+    for (int k = 0; k < ceil_div(n[i], NB); ++k) rows.push_back(make_int2(i, k));
+  dt.upload(rows, c.stream);
+  dpoff.upload(poff, c.stream);
+  k_pack_row<<<static_cast<int>(rows.size()), 256, kPairSmem, c.stream>>>(A, dm.p, dt.p, P, dpoff.p);
   RDD_LAUNCH_CHECK();
   dfail.download(fail.data(), B, c.stream);
   dfa.download(frob_A.data(), B, c.stream);
-  dfp.download(frob_P.data(), B, c.stream);
   RDD_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+long long packed_chol_size(int n) {
+  const long long nb = ceil_div(n, NB);
+  return nb * (nb + 1) / 2 * NB * NB;
+}
+
+size_t chol_solve_smem(int nmax) {
+  return (static_cast<size_t>(ceil_div(nmax, NB)) * NB + kSolveWarps * NB) * sizeof(double);
+}
+
+std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector<int>& n,
+                                      const std::vector<long long>& poff, int iters) {
+  ScopedKernelTimer tk(c, "inv_power");
+  const int B = static_cast<int>(n.size());
+  std::vector<double> out(B, 0.0);
+  if (B == 0) return out;
+  const int nmax = *std::max_element(n.begin(), n.end());
+  DBuf<int> dn;
+  DBuf<long long> dp;
+  DBuf<double> d;
+  dn.upload(n, c.stream);
+  dp.upload(poff, c.stream);
+  d.ensure(B);
+  const size_t smem = chol_solve_smem(nmax);
+  if (c.verbose) std::fprintf(stderr, "[inv_power] B=%d nmax=%d smem=%zu iters=%d\n", B, nmax, smem, iters);
+  RDD_CUDA(cudaFuncSetAttribute(k_chol_power, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  k_chol_power<<<B, kSolveWarps * 32, smem, c.stream>>>(P, dp.p, dn.p, iters, ceil_div(nmax, NB), d.p);
+  RDD_LAUNCH_CHECK();
+  d.download(out.data(), B, c.stream);
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+  return out;
+}
+
+// Schwarz local apply: z_i = A_i⁻¹ g_i, g_i = w(v)[S_i] (schwarz.hpp:153-215: SAS/RAS weights in
+// front of the local solve for the transpose). Factor path or, for eigen-fallback subdomains, the
+// dense pseudo-inverse. One CTA per subdomain.
+__global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
+    const double* __restrict__ P, const long long* __restrict__ poff, const double* const* __restrict__ dense,
+    const int* __restrict__ set_ptr, const int* __restrict__ set_idx, const double* __restrict__ v,
+    const int* __restrict__ mult, const int* __restrict__ owner, int kind, int transpose, int nbmax,
+    double* __restrict__ z) {
+  extern __shared__ double sm[];
+  double* g = sm;
+  double* red = sm + static_cast<size_t>(nbmax) * NB;
+  const int i = blockIdx.x;
+  const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0, nb = (n + NB - 1) / NB;
+  for (int q = threadIdx.x; q < nb * NB; q += blockDim.x) {
+    double val = 0.0;
+    if (q < n) {
+      const int col = set_idx[s0 + q];
+      val = v[col];
+      if (transpose) {
+        if (kind == RDD_PRECOND_SAS) val /= mult[col];
+        else if (kind == RDD_PRECOND_RAS) val = owner[col] == i ? val : 0.0;
+      }
+    }
+    g[q] = val;
+  }
+  __syncthreads();
+  const double* D = dense[i];
+  if (D) {
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      double acc = 0.0;
+      for (int q = 0; q < n; ++q) acc += D[r + static_cast<long long>(q) * n] * g[q];
+      z[s0 + r] = acc;
+    }
+    return;
+  }
+  chol_solve(P + poff[i], nb, g, red);
+  for (int r = threadIdx.x; r < n; r += blockDim.x) z[s0 + r] = g[r];
+}
+
+void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
+  const size_t smem = chol_solve_smem(c.nmax_local);
+  static size_t set = 0;
+  if (smem > set) {
+    RDD_CUDA(cudaFuncSetAttribute(k_chol_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    set = smem;
+  }
+  k_chol_apply<<<c.J, kSolveWarps * 32, smem, c.stream>>>(c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p,
+                                                          v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
+                                                          ceil_div(c.nmax_local, NB), zloc);
+  RDD_LAUNCH_CHECK();
 }
 
 }  // namespace rdd

@@ -39,6 +39,18 @@ struct KernelStat {
   int64_t launches = 0;
 };
 
+struct GemmTask {
+  const double* A;
+  const double* B;
+  double* Cm;
+  const int* gA;   // optional row gather for op(A)'s K index (TN mode)
+  const int* gB;
+  int M, N, K, lda, ldb, ldc;
+  int tm, tn;      // tile indices
+  double beta;     // C = alpha * op(A) op(B) + beta * C
+  double alpha = 1.0;
+};
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -109,7 +121,7 @@ struct Ctx {
   std::vector<int> h_owner, h_mult;
   std::vector<int> local_rank;
   std::vector<double> local_cond;
-  std::vector<long long> P_off;       // per i: offset of the n_i x n_i local inverse
+  std::vector<long long> P_off;       // per i: offset of the tile-packed Cholesky factor of A_i
   DBuf<double> P;
   DBuf<int> dset_ptr, dset_idx, dmult, downer;
   DBuf<long long> dP_off;
@@ -117,8 +129,9 @@ struct Ctx {
   DBuf<int> gat_ptr, gat_pos, gat_owner_pos;
   int nmax_local = 0;
   int n_fallback = 0;                 // local blocks that took the eigen pseudo-inverse
-  std::vector<int> fallback, local_n, own_pos;  // own_pos: offset of block i's columns inside S_i
-  DBuf<int> down_pos;
+  std::vector<int> fallback, local_n;
+  std::map<int, DBuf<double>> fb_store;  // eigen-fallback subdomains: dense pseudo-inverse
+  DBuf<double*> dfb_ptr;              // per i: dense pseudo-inverse or nullptr (factor path)
   bool local_cond_exact = false;
   struct GatherTask {
     int i, j1, j2, o1, o2;
@@ -137,7 +150,8 @@ struct Ctx {
   DBuf<double> ytmp;                  // N
   DBuf<int2> mv_tiles, mt_tiles;      // (block, first row) / (block, first column) tiles of H·w / Hᵀ·r
   int mv_ntiles = 0, mt_ntiles = 0, mv_rmax = 0;
-  DBuf<double> zrows;                 // per-block partial H_j·w_j (row_ptr layout)
+  DBuf<double> zrows;
+  DBuf<GemmTask> wsg;                 // device-generated GEMM task lists                 // per-block partial H_j·w_j (row_ptr layout)
   // Hᵀ·r work list (block, column group)
   DBuf<int> mt_blk, mt_k0;
   int mt_groups = 0;
@@ -229,26 +243,20 @@ void solve_all(Ctx& c, int solver, double tol, int max_iter, int restart);
 // evaluate.cu (K14)
 void evaluate(Ctx& c, const int* test_res);
 // gemm.cu
-struct GemmTask {
-  const double* A;
-  const double* B;
-  double* Cm;
-  const int* gA;   // optional row gather for op(A)'s K index (TN mode)
-  const int* gB;
-  int M, N, K, lda, ldb, ldc;
-  int tm, tn;      // tile indices
-  double beta;     // C = alpha * op(A) op(B) + beta * C
-  double alpha = 1.0;
-};
 void gemm_tn(Ctx& c, const std::vector<GemmTask>& tasks);  // C = Aᵀ B (A: K x M, B: K x N col-major)
 void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks);  // C = A B  (A: M x K, B: K x N col-major)
-void gemm_nt(Ctx& c, const std::vector<GemmTask>& tasks);  // C = A Bᵀ (A: M x K, B: N x K col-major)
+void gemm_nt(Ctx& c, const std::vector<GemmTask>& tasks);
+void gemm_nt_dev(Ctx& c, const GemmTask* tasks, int count);  // C = A Bᵀ (A: M x K, B: N x K col-major)
 void project_blocks(Ctx& c);
 void ensure_col_owner(Ctx& c);
 // cholesky.cu
-void batched_spd_inverse(Ctx& c, double* A, double* P, const std::vector<int>& n, const std::vector<long long>& off,
-                         std::vector<int>& fail, std::vector<double>& frob_A, std::vector<double>& frob_P,
-                         const std::vector<long long>* offP = nullptr);
+void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const std::vector<long long>& off, double* P,
+                           const std::vector<long long>& poff, std::vector<int>& fail, std::vector<double>& frob_A);
+long long packed_chol_size(int n);
+size_t chol_solve_smem(int nmax);
+std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector<int>& n,
+                                      const std::vector<long long>& poff, int iters);
+void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc);
 std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int>& n,
                                   const std::vector<long long>& off, int iters);
 // jacobi.cu

@@ -155,4 +155,18 @@ void gemm_tn(Ctx& c, const std::vector<GemmTask>& tasks) { launch<true, false>(c
 void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks) { launch<false, false>(c, tasks, "gemm_nn"); }
 void gemm_nt(Ctx& c, const std::vector<GemmTask>& tasks) { launch<false, true>(c, tasks, "gemm_nt"); }
 
+// tasks already in device memory (generated by a kernel)
+void gemm_nt_dev(Ctx& c, const GemmTask* tasks, int count) {
+  if (count <= 0) return;
+  ScopedKernelTimer tk(c, "gemm_nt");
+  static bool attr_set = false;
+  if (!attr_set) {
+    RDD_CUDA(cudaFuncSetAttribute(k_gemm<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kGemmSmem)));
+    attr_set = true;
+  }
+  k_gemm<false, true><<<static_cast<unsigned>(count), NT, kGemmSmem, c.stream>>>(tasks);
+  RDD_LAUNCH_CHECK();
+}
+
 }  // namespace rdd

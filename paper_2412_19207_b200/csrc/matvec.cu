@@ -182,7 +182,7 @@ void matvec_t_dev(Ctx& c, const double* r, double* out) {
   ScopedKernelTimer tk(c, "matvec_t");
   if (c.mt_ntiles == 0) return;
   const size_t sm = static_cast<size_t>(c.mv_rmax) * sizeof(double);
-  if (sm > 48 * 1024) {
+  if (sm > 32 * 1024) {
     static size_t set = 0;
     if (sm > set) {
       RDD_CUDA(cudaFuncSetAttribute(k_block_gemv_t, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));

@@ -315,7 +315,7 @@ void run_pca(Ctx& c) {
     dr.ensure(J);
     {
       const size_t sm = static_cast<size_t>(m) * (2 * sizeof(double) + 1) + 16;
-      if (sm > 48 * 1024)
+      if (sm > 32 * 1024)
         RDD_CUDA(cudaFuncSetAttribute(k_pchol, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
       k_pchol<<<J, kPcholThreads, sm, c.stream>>>(G.p, Lw.p, m, 1e-17, dr.p);
       RDD_LAUNCH_CHECK();
@@ -350,7 +350,7 @@ void run_pca(Ctx& c) {
       DBuf<long long> doffr;
       doffr.upload(offr, c.stream);
       const size_t sm = static_cast<size_t>(m) * (2 * sizeof(double) + sizeof(int)) + 16;
-      if (sm > 48 * 1024)
+      if (sm > 32 * 1024)
         RDD_CUDA(cudaFuncSetAttribute(k_house_complete, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(sm)));
       k_house_complete<<<J, kHouseThreads, sm, c.stream>>>(Vr.p, lam.p, doffr.p, dr.p, m, Hw.p, V0.p);

@@ -2,13 +2,15 @@
 //
 // Build (schwarz.hpp:93-148): S_i = concatenated column ranges of neighbour_sets[i]; A_i is
 // gathered blockwise from the normal blocks (missing pairs are exact zeros); the local solve is
-// the pseudo-inverse with eigenvalues <= 1e-12·λmax dropped. The device stores each local
-// operator as an explicit symmetric n_i x n_i matrix P_i = V diag(1/λ_kept) Vᵀ (batched Jacobi
-// eigensolver + DMMA), so that every apply is one HBM-streaming GEMV per subdomain.
-// Apply (schwarz.hpp:153-185): z_i = P_i v[S_i]; the AS/SAS/RAS reduction is owner-computes:
-// each column sums its (≤3^d) local contributions in ascending i, like the reference's serial
-// scatter, without atomics. apply_transpose (schwarz.hpp:189-215) moves the SAS/RAS weights in
-// front of the local solve.
+// the pseudo-inverse with eigenvalues <= 1e-12·λmax dropped. The device factors A_i = LLᵀ
+// (cholesky.cu) and certifies that A_i is far from that cutoff (cond(A_i) < 1e11 from ‖A_i‖_F and
+// a power iteration through the factor, refined by a power iteration on A_i when needed); then the
+// pseudo-inverse is A_i⁻¹ and each apply is a forward + backward triangular solve. Blocks that
+// fail either test take the reference's eigen path (Jacobi, same cutoff) and keep the dense
+// pseudo-inverse. Apply (schwarz.hpp:153-185): z_i = A_i⁺ v[S_i]; the AS/SAS/RAS reduction is
+// owner-computes: each column sums its (≤3^d) local contributions in ascending i, like the
+// reference's serial scatter, without atomics. apply_transpose (schwarz.hpp:189-215) moves the
+// SAS/RAS weights in front of the local solve.
 #include <algorithm>
 
 #include "ctx.hpp"
@@ -74,33 +76,6 @@ __global__ void k_local_scale(double* __restrict__ V, const double* __restrict__
   }
 }
 
-// z_i = P_i g_i, g_i = w(v)[S_i]; grid (rows chunk, i)
-__global__ void k_local_apply(const double* __restrict__ P, const long long* __restrict__ P_off,
-                              const int* __restrict__ set_ptr, const int* __restrict__ set_idx,
-                              const double* __restrict__ v, const int* __restrict__ mult,
-                              const int* __restrict__ owner, int kind, int transpose, double* __restrict__ z) {
-  extern __shared__ double g[];
-  const int i = blockIdx.y;
-  const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0;
-  const int r0 = blockIdx.x * blockDim.x;
-  if (r0 >= n) return;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    const int col = set_idx[s0 + c];
-    double val = v[col];
-    if (transpose) {
-      if (kind == RDD_PRECOND_SAS) val /= mult[col];
-      else if (kind == RDD_PRECOND_RAS) val = owner[col] == i ? val : 0.0;
-    }
-    g[c] = val;
-  }
-  __syncthreads();
-  const int r = r0 + threadIdx.x;
-  if (r >= n) return;
-  const double* Pi = P + P_off[i] + r;
-  double acc = 0.0;
-  for (int c = 0; c < n; ++c) acc += Pi[static_cast<long long>(c) * n] * g[c];
-  z[s0 + r] = acc;
-}
 
 // out[col] = Σ_i weight · z_i[pos]  over the ≤3^d subdomains whose S_i contains col
 __global__ void k_reduce(const double* __restrict__ z, const int* __restrict__ gat_ptr,
@@ -120,54 +95,8 @@ __global__ void k_reduce(const double* __restrict__ z, const int* __restrict__ g
   out[col] = s;
 }
 
-// copy rows [r0, r0+nr) of each n x n matrix (column-major) into an nr x n column-major block
-__global__ void k_store_rows(const double* __restrict__ Pc, const long long* __restrict__ src,
-                             const int* __restrict__ n, const int* __restrict__ r0, const int* __restrict__ nr,
-                             double* __restrict__ P, const long long* __restrict__ dst) {
-  const int q = blockIdx.x;
-  const int nn = n[q], rr = nr[q], a = r0[q];
-  const double* s = Pc + src[q];
-  double* d = P + dst[q];
-  for (long long e = threadIdx.x; e < static_cast<long long>(rr) * nn; e += blockDim.x) {
-    const int r = static_cast<int>(e % rr), cc = static_cast<int>(e / rr);
-    d[e] = s[(a + r) + static_cast<long long>(cc) * nn];
-  }
-}
 
-// RAS (schwarz.hpp:178-181): out[own_i] = A_i⁺[own, :] v[S_i]; each column has exactly one owner
-__global__ void k_ras_apply(const double* __restrict__ P, const long long* __restrict__ P_off,
-                            const int* __restrict__ set_ptr, const int* __restrict__ set_idx,
-                            const int* __restrict__ col_off, const double* __restrict__ v, double* __restrict__ out) {
-  extern __shared__ double g[];
-  const int i = blockIdx.y;
-  const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0;
-  const int c0 = col_off[i], pi = col_off[i + 1] - c0;
-  const int r0 = blockIdx.x * blockDim.x;
-  if (r0 >= pi) return;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) g[c] = v[set_idx[s0 + c]];
-  __syncthreads();
-  const int r = r0 + threadIdx.x;
-  if (r >= pi) return;
-  const double* Pi = P + P_off[i] + r;
-  double acc = 0.0;
-  for (int c = 0; c < n; ++c) acc += Pi[static_cast<long long>(c) * pi] * g[c];
-  out[c0 + r] = acc;
-}
 
-// RAS transpose (schwarz.hpp:189-215): z_i = A_i⁺[own, :]ᵀ v[own_i], then the AS-style sum
-__global__ void k_ras_apply_t(const double* __restrict__ P, const long long* __restrict__ P_off,
-                              const int* __restrict__ set_ptr, const int* __restrict__ col_off,
-                              const double* __restrict__ v, double* __restrict__ z) {
-  const int i = blockIdx.y;
-  const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0;
-  const int c0 = col_off[i], pi = col_off[i + 1] - c0;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  const double* col = P + P_off[i] + static_cast<long long>(c) * pi;
-  double acc = 0.0;
-  for (int r = 0; r < pi; ++r) acc += col[r] * v[c0 + r];
-  z[s0 + c] = acc;
-}
 
 }  // namespace
 
@@ -231,27 +160,34 @@ void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, con
   RDD_LAUNCH_CHECK();
 }
 
-// local_cond as the reference reports it (λmax/λmin of the kept spectrum), by power iteration
-// on A_i and A_i^{-1}; computed on demand (the rank decision only needs the cheap bound).
+// local_cond as the reference reports it (λmax/λmin of the kept spectrum): power iterations on
+// A_i and through its factor, computed on demand (the build only needs the certified bound)
 void refresh_local_cond(Ctx& c) {
-  if (c.local_cond_exact || c.pkind < 0 || c.pkind == RDD_PRECOND_RAS) return;  // RAS keeps owner panels only
+  if (c.local_cond_exact || c.pkind < 0) return;
   std::vector<int> which;
   for (int i = 0; i < c.J; ++i)
     if (std::find(c.fallback.begin(), c.fallback.end(), i) == c.fallback.end()) which.push_back(i);
-  std::vector<long long> off, poff;
-  std::vector<int> nn;
-  long long tot = 0;
-  for (int i : which) {
-    off.push_back(tot);
-    nn.push_back(c.local_n[i]);
-    poff.push_back(c.P_off[i]);
-    tot += static_cast<long long>(c.local_n[i]) * c.local_n[i];
+  const size_t budget = std::max<size_t>(size_t(1) << 28, device_available(c) / 4);
+  for (size_t q0 = 0; q0 < which.size();) {
+    std::vector<int> sub, nn;
+    std::vector<long long> off, poff;
+    long long tot = 0;
+    for (; q0 < which.size(); ++q0) {
+      const int i = which[q0];
+      const long long sz = static_cast<long long>(c.local_n[i]) * c.local_n[i];
+      if (!sub.empty() && static_cast<size_t>(tot + sz) * sizeof(double) > budget) break;
+      sub.push_back(i);
+      off.push_back(tot);
+      nn.push_back(c.local_n[i]);
+      poff.push_back(c.P_off[i]);
+      tot += sz;
+    }
+    DBuf<double> Af;
+    gather_locals(c, sub, Af, off);
+    const std::vector<double> la = batched_power(c, Af.p, nn, off, 200);
+    const std::vector<double> lp = batched_inv_power(c, c.P.p, nn, poff, 200);
+    for (size_t q = 0; q < sub.size(); ++q) c.local_cond[sub[q]] = la[q] * lp[q];
   }
-  DBuf<double> Af;
-  gather_locals(c, which, Af, off);
-  const std::vector<double> la = batched_power(c, Af.p, nn, off, 200);
-  const std::vector<double> lp = batched_power(c, c.P.p, nn, poff, 200);
-  for (size_t q = 0; q < which.size(); ++q) c.local_cond[which[q]] = la[q] * lp[q];
   c.local_cond_exact = true;
 }
 
@@ -298,14 +234,12 @@ void build_schwarz(Ctx& c, int kind) {
 
   // local matrix sizes and gather plan (schwarz.hpp:112-130): A_i blocks come from NB
   c.local_n = n;
-  c.own_pos.assign(J, 0);
   c.gat_tasks.clear();
   for (int i = 0; i < J; ++i) {
     std::vector<std::pair<int, int>> parts;
     int o = 0;
     for (int q = c.nbr_ptr[i]; q < c.nbr_ptr[i + 1]; ++q) {
       const int j = c.nbr_idx[q];
-      if (j == i) c.own_pos[i] = o;
       parts.push_back({j, o});
       o += c.h_p[j];
     }
@@ -316,35 +250,32 @@ void build_schwarz(Ctx& c, int kind) {
         c.gat_tasks.push_back({i, j1, j2, o1, o2, c.nb_off[it->second]});
       }
   }
-  // storage of the local operators: AS/SAS the full A_i⁺ (n_i x n_i); RAS only the owner rows
-  // A_i⁺[own, :] (p_i x n_i, column-major) — all the restricted apply reads (schwarz.hpp:178-181)
-  const bool ras = kind == RDD_PRECOND_RAS;
+  // storage: the tile-packed factor of every A_i (the eigen-fallback blocks keep a dense copy)
   c.P_off.assign(J + 1, 0);
-  for (int i = 0; i < J; ++i)
-    c.P_off[i + 1] = c.P_off[i] + static_cast<long long>(ras ? c.h_p[i] : n[i]) * n[i];
+  for (int i = 0; i < J; ++i) c.P_off[i + 1] = c.P_off[i] + packed_chol_size(n[i]);
   c.dP_off.upload(c.P_off, c.stream);
+  c.fb_store.clear();
   const size_t p_bytes = static_cast<size_t>(c.P_off[J]) * sizeof(double);
   if (device_available(c) < p_bytes + (size_t(8) << 30)) release_scratch(c);
   c.P.ensure(std::max<long long>(1, c.P_off[J]));
-  // per chunk: A (destroyed by Cholesky), A0 copy, Pc (full inverses), L^{-1}, tmp
   const size_t budget =
-      std::min<size_t>(size_t(32) << 30, std::max<size_t>(size_t(1) << 30, (device_available(c) * 2) / 5));
+      std::min<size_t>(size_t(48) << 30, std::max<size_t>(size_t(1) << 30, (device_available(c) * 3) / 5));
   c.local_rank.assign(J, 0);
   c.local_cond.assign(J, 0.0);
   c.local_cond_exact = false;
   c.fallback.clear();
-  std::vector<int> hown(J);
-  for (int i = 0; i < J; ++i) hown[i] = c.own_pos[i];
+  std::vector<double*> fbp(J, nullptr);
   for (int i0 = 0; i0 < J;) {
     std::vector<int> chunk, cn;
-    std::vector<long long> coff;
+    std::vector<long long> coff, cpoff;
     long long used = 0;
     int i = i0;
     for (; i < J; ++i) {
       const long long sz = static_cast<long long>(n[i]) * n[i];
-      if (!chunk.empty() && static_cast<size_t>(used + sz) * sizeof(double) * 5 > budget) break;
+      if (!chunk.empty() && static_cast<size_t>(used + sz) * sizeof(double) > budget) break;
       chunk.push_back(i);
       coff.push_back(used);
+      cpoff.push_back(c.P_off[i]);
       cn.push_back(n[i]);
       used += sz;
     }
@@ -352,36 +283,53 @@ void build_schwarz(Ctx& c, int kind) {
     const int B = static_cast<int>(chunk.size());
     DBuf<double>& Aw = c.wsd["schwarz.A"];
     gather_locals(c, chunk, Aw, coff);
-    double* A0 = c.ws("schwarz.A0", used);
-    RDD_CUDA(cudaMemcpyAsync(A0, Aw.p, sizeof(double) * used, cudaMemcpyDeviceToDevice, c.stream));
-    double* Pc = c.ws("schwarz.Pc", used);
     std::vector<int> fail;
-    std::vector<double> fa, fp;
-    batched_spd_inverse(c, Aw.p, Pc, cn, coff, fail, fa, fp);
-    // rank decision: cond(A_i) <= ||A_i||_F ||A_i^{-1}||_F; refine by power iteration when the
-    // bound does not clear the threshold; failed or rank-deficient blocks take the eigen path
-    std::vector<int> flagged;
-    for (int q = 0; q < B; ++q) {
-      if (fail[q] || !(fa[q] * fp[q] < c.full_rank_cond)) flagged.push_back(q);
-      else {
-        c.local_rank[chunk[q]] = cn[q];
-        c.local_cond[chunk[q]] = fa[q] * fp[q];
+    std::vector<double> fa;
+    batched_cholesky_pack(c, Aw.p, cn, coff, c.P.p, cpoff, fail, fa);
+    // rank decision: cond(A_i) <= ‖A_i‖_F·λmax(A_i⁻¹) (power iteration through the factor); when
+    // that does not clear the threshold, λmax(A_i) by power iteration and a longer λmax(A_i⁻¹)
+    std::vector<int> ok_q, flagged;
+    for (int q = 0; q < B; ++q)
+      if (!fail[q]) ok_q.push_back(q);
+    {
+      std::vector<int> nn;
+      std::vector<long long> po;
+      for (int q : ok_q) {
+        nn.push_back(cn[q]);
+        po.push_back(cpoff[q]);
+      }
+      const std::vector<double> lp = batched_inv_power(c, c.P.p, nn, po, 12);
+      for (size_t z = 0; z < ok_q.size(); ++z) {
+        const int q = ok_q[z];
+        if (fa[q] * lp[z] < c.full_rank_cond) {
+          c.local_rank[chunk[q]] = cn[q];
+          c.local_cond[chunk[q]] = fa[q] * lp[z];
+        } else {
+          flagged.push_back(q);
+        }
       }
     }
     std::vector<int> fb;
+    for (int q = 0; q < B; ++q)
+      if (fail[q]) fb.push_back(q);
     if (!flagged.empty()) {
-      std::vector<int> fnn;
-      std::vector<long long> foff;
+      std::vector<int> which, fnn;
+      std::vector<long long> foff, po;
+      long long t = 0;
       for (int q : flagged) {
+        which.push_back(chunk[q]);
         fnn.push_back(cn[q]);
-        foff.push_back(coff[q]);
+        foff.push_back(t);
+        po.push_back(cpoff[q]);
+        t += static_cast<long long>(cn[q]) * cn[q];
       }
-      const std::vector<double> la = batched_power(c, A0, fnn, foff, 60);
-      const std::vector<double> lp = batched_power(c, Pc, fnn, foff, 60);
+      gather_locals(c, which, Aw, foff);
+      const std::vector<double> la = batched_power(c, Aw.p, fnn, foff, 60);
+      const std::vector<double> lp = batched_inv_power(c, c.P.p, fnn, po, 60);
       for (size_t z = 0; z < flagged.size(); ++z) {
         const int q = flagged[z];
         const double cond = la[z] * lp[z];
-        if (!fail[q] && cond < c.full_rank_cond) {
+        if (cond < c.full_rank_cond) {
           c.local_rank[chunk[q]] = cn[q];
           c.local_cond[chunk[q]] = cond;
         } else {
@@ -389,18 +337,22 @@ void build_schwarz(Ctx& c, int kind) {
         }
       }
     }
-    if (!fb.empty()) {  // eigen pseudo-inverse with the reference cutoff, written over Pc
-      std::vector<int> fnn;
+    if (!fb.empty()) {  // eigen pseudo-inverse with the reference cutoff, kept dense
+      std::sort(fb.begin(), fb.end());
+      std::vector<int> which, fnn;
       std::vector<long long> foff, evo;
-      long long te = 0;
+      long long t = 0, te = 0;
       for (int q : fb) {
+        which.push_back(chunk[q]);
         fnn.push_back(cn[q]);
-        foff.push_back(coff[q]);
+        foff.push_back(t);
         evo.push_back(te);
+        t += static_cast<long long>(cn[q]) * cn[q];
         te += cn[q];
       }
-      double* V = c.ws("schwarz.V", used);
-      double* X = c.ws("schwarz.X", used);
+      gather_locals(c, which, Aw, foff);
+      double* V = c.ws("schwarz.V", t);
+      double* X = c.ws("schwarz.X", t);
       double* lam = c.ws("schwarz.lam", te);
       EigOpts eo;  // backward stable like SelfAdjointEigenSolver; cutoff 1e-12·λmax (schwarz.hpp:82)
       eo.absolute = 1;
@@ -408,7 +360,7 @@ void build_schwarz(Ctx& c, int kind) {
       eo.floor_rel = 1e-16;
       eo.conv_rel = 1e-14;
       eo.max_sweeps = 60;
-      batched_syevj(c, A0, V, lam, fnn, foff, eo);
+      batched_syevj(c, Aw.p, V, lam, fnn, foff, eo);
       DBuf<long long> devo, dfoff;
       DBuf<int> drank, dfn;
       DBuf<double> dcond;
@@ -420,83 +372,37 @@ void build_schwarz(Ctx& c, int kind) {
       k_local_scale<<<static_cast<int>(fb.size()), 256, 0, c.stream>>>(V, lam, dfn.p, dfoff.p, devo.p, X, drank.p,
                                                                        dcond.p);
       RDD_LAUNCH_CHECK();
-      std::vector<GemmTask> t;
-      for (size_t z = 0; z < fb.size(); ++z)
+      std::vector<GemmTask> tk;
+      for (size_t z = 0; z < fb.size(); ++z) {
+        double* D = c.fb_store[which[z]].ensure(static_cast<size_t>(fnn[z]) * fnn[z]);
+        fbp[which[z]] = D;
         for (int tm = 0; tm < ceil_div(fnn[z], 64); ++tm)
           for (int tn = 0; tn < ceil_div(fnn[z], 64); ++tn)
-            t.push_back({X + foff[z], V + foff[z], Pc + foff[z], nullptr, nullptr, fnn[z], fnn[z], fnn[z], fnn[z],
-                         fnn[z], fnn[z], tm, tn, 0.0});
-      gemm_nt(c, t);
+            tk.push_back({X + foff[z], V + foff[z], D, nullptr, nullptr, fnn[z], fnn[z], fnn[z], fnn[z], fnn[z],
+                          fnn[z], tm, tn, 0.0});
+      }
+      gemm_nt(c, tk);
       std::vector<int> hr(fb.size());
       std::vector<double> hc(fb.size());
       drank.download(hr.data(), fb.size(), c.stream);
       dcond.download(hc.data(), fb.size(), c.stream);
       RDD_CUDA(cudaStreamSynchronize(c.stream));
       for (size_t z = 0; z < fb.size(); ++z) {
-        c.local_rank[chunk[fb[z]]] = hr[z];
-        c.local_cond[chunk[fb[z]]] = hc[z];
-        c.fallback.push_back(chunk[fb[z]]);
+        c.local_rank[which[z]] = hr[z];
+        c.local_cond[which[z]] = hc[z];
+        c.fallback.push_back(which[z]);
       }
     }
-    // store: full inverse (AS/SAS) or the owner panel (RAS)
-    std::vector<long long> src(B), dst(B);
-    std::vector<int> rows0(B), nrows(B);
-    for (int q = 0; q < B; ++q) {
-      src[q] = coff[q];
-      dst[q] = c.P_off[chunk[q]];
-      rows0[q] = ras ? hown[chunk[q]] : 0;
-      nrows[q] = ras ? c.h_p[chunk[q]] : cn[q];
-    }
-    DBuf<long long> dsrc, ddst;
-    DBuf<int> dr0, dnr, dcn;
-    dsrc.upload(src, c.stream);
-    ddst.upload(dst, c.stream);
-    dr0.upload(rows0, c.stream);
-    dnr.upload(nrows, c.stream);
-    dcn.upload(cn, c.stream);
-    k_store_rows<<<B, 256, 0, c.stream>>>(Pc, dsrc.p, dcn.p, dr0.p, dnr.p, c.P.p, ddst.p);
-    RDD_LAUNCH_CHECK();
-    RDD_CUDA(cudaStreamSynchronize(c.stream));
   }
+  std::sort(c.fallback.begin(), c.fallback.end());
   c.n_fallback = static_cast<int>(c.fallback.size());
-  {
-    std::vector<int> h_own_pos(J);
-    for (int i = 0; i < J; ++i) h_own_pos[i] = c.own_pos[i];
-    c.down_pos.upload(h_own_pos, c.stream);
-  }
+  c.dfb_ptr.upload(fbp, c.stream);
   c.nmax_local = *std::max_element(n.begin(), n.end());
 }
 
 void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose) {
   ScopedKernelTimer tk(c, "precond_apply");
-  const int T = 128;
-  if (c.pkind == RDD_PRECOND_RAS) {
-    int pmax = 0;
-    for (int j = 0; j < c.J; ++j) pmax = std::max(pmax, c.h_p[j]);
-    if (!transpose) {
-      const size_t smem = static_cast<size_t>(c.nmax_local) * sizeof(double);
-      if (smem > 48 * 1024)
-        RDD_CUDA(cudaFuncSetAttribute(k_ras_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      k_ras_apply<<<dim3(ceil_div(pmax, T), c.J), T, smem, c.stream>>>(c.P.p, c.dP_off.p, c.dset_ptr.p, c.dset_idx.p,
-                                                                       c.dcol_off.p, v, z);
-      RDD_LAUNCH_CHECK();
-    } else {
-      k_ras_apply_t<<<dim3(ceil_div(c.nmax_local, T), c.J), T, 0, c.stream>>>(c.P.p, c.dP_off.p, c.dset_ptr.p,
-                                                                             c.dcol_off.p, v, c.zloc.p);
-      RDD_LAUNCH_CHECK();
-      k_reduce<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.zloc.p, c.gat_ptr.p, c.gat_pos.p, c.gat_owner_pos.p,
-                                                         c.dmult.p, c.p, RDD_PRECOND_AS, 1, z);
-      RDD_LAUNCH_CHECK();
-    }
-    return;
-  }
-  dim3 grid(ceil_div(c.nmax_local, T), c.J);
-  const size_t smem = static_cast<size_t>(c.nmax_local) * sizeof(double);
-  if (smem > 48 * 1024)
-    RDD_CUDA(cudaFuncSetAttribute(k_local_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  k_local_apply<<<grid, T, smem, c.stream>>>(c.P.p, c.dP_off.p, c.dset_ptr.p, c.dset_idx.p, v, c.dmult.p, c.downer.p,
-                                             c.pkind, transpose ? 1 : 0, c.zloc.p);
-  RDD_LAUNCH_CHECK();
+  chol_apply(c, v, transpose, c.zloc.p);
   k_reduce<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.zloc.p, c.gat_ptr.p, c.gat_pos.p, c.gat_owner_pos.p, c.dmult.p,
                                                      c.p, c.pkind, transpose ? 1 : 0, z);
   RDD_LAUNCH_CHECK();

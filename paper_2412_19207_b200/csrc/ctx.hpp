@@ -150,10 +150,10 @@ struct Ctx {
   DBuf<double> ytmp;                  // N
   DBuf<int2> mv_tiles, mt_tiles;      // (block, first row) / (block, first column) tiles of H·w / Hᵀ·r
   int mv_ntiles = 0, mt_ntiles = 0, mv_rmax = 0;
-  DBuf<double> zrows;
-  DBuf<GemmTask> wsg;                 // device-generated GEMM task lists                 // per-block partial H_j·w_j (row_ptr layout)
-  // Hᵀ·r work list (block, column group)
-  DBuf<int> mt_blk, mt_k0;
+  DBuf<double> zrows;                 // per-block partial H_j·w_j (row_ptr layout)
+  DBuf<int> mt_part_off, mt_blk_tile0;  // Hᵀ·r row-chunk partials: offset per tile, first tile per block
+  DBuf<double> mt_part;
+  DBuf<GemmTask> wsg;                 // device-generated GEMM task lists
   int mt_groups = 0;
   size_t mt_smem = 0;
   // fused single-pass normal operator plan

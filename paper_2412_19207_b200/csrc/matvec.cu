@@ -80,55 +80,57 @@ __global__ void k_cover_sum(const double* __restrict__ z, const int* __restrict_
   y[i] = acc;
 }
 
-// Hᵀ·r: per (block j, group of kMtCols columns) the gathered r_j = r[rows of j] is staged in
-// shared memory once; each warp then reduces two columns at a time (lane-strided rows, then the
-// butterfly — the same order as a warp-per-column reduction).
-constexpr int kMtWarps = 8, kMtCols = 16, kMtUnroll = 4;
+// Hᵀ·r in two steps: (1) per (block j, chunk of kMtRows local rows) the gathered r chunk is staged
+// in shared memory and every column of H_j is reduced over the chunk (warps take columns; lanes
+// stride the rows, then the butterfly) into a partial; (2) each column sums its chunk partials in
+// chunk order. Deterministic, no atomics; the tile count does not depend on p_j, so the grid fills
+// the GPU even when blocks are narrow.
+constexpr int kMtRows = 512, kMtWarps = 8, kMtUnroll = 8;
 __global__ void __launch_bounds__(kMtWarps * 32) k_block_gemv_t(const double* __restrict__ H,
                                                                  const long long* __restrict__ H_off,
                                                                  const int* __restrict__ row_ptr,
                                                                  const int* __restrict__ row_idx,
                                                                  const int* __restrict__ col_off,
                                                                  const int2* __restrict__ tiles,
-                                                                 const double* __restrict__ r, double* __restrict__ out) {
-  extern __shared__ double rsm[];
+                                                                 const int* __restrict__ part_off,
+                                                                 const double* __restrict__ r, double* __restrict__ part) {
+  __shared__ double rsm[kMtRows];
   const int2 t = tiles[blockIdx.x];
   const int j = t.x;
   const int r0 = row_ptr[j], rows = row_ptr[j + 1] - r0;
-  const int c0 = col_off[j], pj = col_off[j + 1] - c0;
-  for (int q = threadIdx.x; q < rows; q += blockDim.x) rsm[q] = r[row_idx[r0 + q]];
+  const int q0 = t.y, nq = min(kMtRows, rows - q0);
+  const int pj = col_off[j + 1] - col_off[j];
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) rsm[q] = r[row_idx[r0 + q0 + q]];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ka = t.y + warp, kb = ka + kMtWarps;
-  const bool va = ka < pj, vb = kb < pj;
-  if (!va) return;
-  const double* ha = H + H_off[j] + static_cast<long long>(ka) * rows;
-  const double* hb = H + H_off[j] + static_cast<long long>(vb ? kb : ka) * rows;
-  double sa = 0.0, sb = 0.0;
-  int q = lane;
-  for (; q + 32 * (kMtUnroll - 1) < rows; q += 32 * kMtUnroll) {
-    double a[kMtUnroll], b[kMtUnroll];
+  double* out = part + part_off[blockIdx.x];
+  for (int k = warp; k < pj; k += kMtWarps) {
+    const double* h = H + H_off[j] + static_cast<long long>(k) * rows + q0;
+    double s = 0.0;
+    int q = lane;
+    for (; q + 32 * (kMtUnroll - 1) < nq; q += 32 * kMtUnroll) {
+      double a[kMtUnroll];
 #pragma unroll
-    for (int u = 0; u < kMtUnroll; ++u) {
-      a[u] = __ldcs(ha + q + 32 * u);
-      b[u] = __ldcs(hb + q + 32 * u);
-    }
+      for (int u = 0; u < kMtUnroll; ++u) a[u] = __ldcs(h + q + 32 * u);
 #pragma unroll
-    for (int u = 0; u < kMtUnroll; ++u) {
-      sa += a[u] * rsm[q + 32 * u];
-      sb += b[u] * rsm[q + 32 * u];
+      for (int u = 0; u < kMtUnroll; ++u) s += a[u] * rsm[q + 32 * u];
     }
+    for (; q < nq; q += 32) s += h[q] * rsm[q];
+    s = warp_sum(s);
+    if (lane == 0) out[k] = s;
   }
-  for (; q < rows; q += 32) {
-    sa += ha[q] * rsm[q];
-    sb += hb[q] * rsm[q];
-  }
-  sa = warp_sum(sa);
-  sb = warp_sum(sb);
-  if (lane == 0) {
-    out[c0 + ka] = sa;
-    if (vb) out[c0 + kb] = sb;
-  }
+}
+
+// out[col] = Σ over the row chunks of its block (ascending) of the partials
+__global__ void k_chunk_sum(const double* __restrict__ part, const int* __restrict__ col_owner,
+                            const int* __restrict__ col_off, const int* __restrict__ blk_tile0,
+                            const int* __restrict__ part_off, int p, double* __restrict__ out) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= p) return;
+  const int j = col_owner[col], k = col - col_off[j];
+  double s = 0.0;
+  for (int tt = blk_tile0[j]; tt < blk_tile0[j + 1]; ++tt) s += part[part_off[tt] + k];
+  out[col] = s;
 }
 
 }  // namespace
@@ -141,18 +143,28 @@ void ensure_col_owner(Ctx& c) {
   c.downer.upload(own, c.stream);
   // tile lists of the block-tiled H·w / Hᵀ·r
   std::vector<int2> mv, mt;
-  int rmax = 0;
+  std::vector<int> poff, t0(c.J + 1, 0);
+  int rmax = 0, pacc = 0;
   for (int j = 0; j < c.J; ++j) {
     const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
     rmax = std::max(rmax, rows);
     for (int r = 0; r < rows; r += kMvRows) mv.push_back(make_int2(j, r));
-    for (int k = 0; k < c.h_p[j]; k += kMtCols) mt.push_back(make_int2(j, k));
+    t0[j] = static_cast<int>(mt.size());
+    for (int r = 0; r < rows; r += kMtRows) {
+      mt.push_back(make_int2(j, r));
+      poff.push_back(pacc);
+      pacc += c.h_p[j];
+    }
   }
+  t0[c.J] = static_cast<int>(mt.size());
   c.mv_ntiles = static_cast<int>(mv.size());
   c.mt_ntiles = static_cast<int>(mt.size());
   c.mv_rmax = rmax;
   c.mv_tiles.upload(mv, c.stream);
   c.mt_tiles.upload(mt, c.stream);
+  c.mt_part_off.upload(poff, c.stream);
+  c.mt_blk_tile0.upload(t0, c.stream);
+  c.mt_part.ensure(std::max(1, pacc));
   c.zrows.ensure(std::max(1, c.h_row_ptr[c.J]));
 }
 
@@ -181,16 +193,11 @@ void matvec_dev(Ctx& c, const double* w, double* y) {
 void matvec_t_dev(Ctx& c, const double* r, double* out) {
   ScopedKernelTimer tk(c, "matvec_t");
   if (c.mt_ntiles == 0) return;
-  const size_t sm = static_cast<size_t>(c.mv_rmax) * sizeof(double);
-  if (sm > 32 * 1024) {
-    static size_t set = 0;
-    if (sm > set) {
-      RDD_CUDA(cudaFuncSetAttribute(k_block_gemv_t, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-      set = sm;
-    }
-  }
-  k_block_gemv_t<<<c.mt_ntiles, kMtWarps * 32, sm, c.stream>>>(c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p,
-                                                               c.dcol_off.p, c.mt_tiles.p, r, out);
+  k_block_gemv_t<<<c.mt_ntiles, kMtWarps * 32, 0, c.stream>>>(c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p,
+                                                              c.mt_tiles.p, c.mt_part_off.p, r, c.mt_part.p);
+  RDD_LAUNCH_CHECK();
+  k_chunk_sum<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.mt_part.p, c.downer.p, c.dcol_off.p, c.mt_blk_tile0.p,
+                                                        c.mt_part_off.p, c.p, out);
   RDD_LAUNCH_CHECK();
 }
 

@@ -162,6 +162,9 @@ int rdd_set_timing(rdd_ctx* ctx, int on);
 int rdd_set_verbose(rdd_ctx* ctx, int on);  /* solver diagnostics on stderr */  /* per-family CUDA-event timing (adds syncs) */
 /* Time `reps` calls of the normal operator on device-resident vectors (CUDA events). */
 int rdd_bench_operator(rdd_ctx* ctx, int op_form, int reps, double* ms_per_call, double* bytes_per_call);
+/* Batched Jacobi eigensolver probe (no reference counterpart; tuning aid): `batch` random
+   symmetric matrices of order n, exactly `sweeps` sweeps, eigenvectors included; ms via events. */
+int rdd_bench_jacobi(rdd_ctx* ctx, int n, int batch, int sweeps, double* ms);
 
 #ifdef __cplusplus
 }

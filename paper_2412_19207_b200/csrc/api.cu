@@ -566,4 +566,11 @@ int rdd_bench_operator(rdd_ctx* h, int op_form, int reps, double* ms_per_call, d
   });
 }
 
+int rdd_bench_jacobi(rdd_ctx* h, int n, int batch, int sweeps, double* ms) {
+  return guarded(h, [&](Ctx& c) {
+    if (n < 2 || batch < 1 || sweeps < 1) throw std::invalid_argument("bench_jacobi: n >= 2, batch >= 1, sweeps >= 1");
+    *ms = rdd::bench_syevj(c, n, batch, sweeps);
+  });
+}
+
 }  // extern "C"

@@ -268,6 +268,7 @@ struct EigOpts {
   double conv_angle = 0.0;                  // ... and on rotations with |tan θ| above this
   int max_sweeps = 40;
 };
+double bench_syevj(Ctx& c, int n, int B, int sweeps);
 void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vector<int>& n,
                    const std::vector<long long>& offA, const EigOpts& o);
 

@@ -260,59 +260,47 @@ __device__ __forceinline__ void publish(double* tab, int i, double v) {
   for (int r = 0; r < K; ++r) ((K > 1) ? cg::this_cluster().map_shared_rank(tab, r) : tab)[i] = v;
 }
 
-// Ĵ_Uᵀ A Ĵ_W on the blocks (U, W), U = lane, lane+32, ... <= W, of one column unit W at parity O
-// (columns c0p, c1p; c1p unused for a singleton unit). The diagonal block also publishes the new
-// diagonal, the superdiagonal block the next step's pair coupling, into every CTA's tables.
-// The common case — both units are pairs — is straight-line code; the singleton units of odd
-// steps (position 0 and ne-1) take the general path.
+// Ĵ_Uᵀ A Ĵ_W on the blocks (U, W) of one column unit W at parity O (columns c0p, c1p; c1p unused
+// for a singleton unit). Pair row units are indexed by their pair k = U - O: lane takes
+// k = lane, lane+32, ..., rows (2k+O, 2k+O+1) — a branch-free loop. The singleton row unit {0} of
+// odd steps, the diagonal block (with tan θ from the table, no division) and the publication of
+// the next step's decision inputs are handled outside it.
 template <int K, int O, class P1>
-__device__ __forceinline__ void unit_update(double* c0p, P1 c1p, bool w2, double2 cw, int W, int npair, int lane,
+__device__ __forceinline__ void unit_update(double* c0p, P1 c1p, bool w2, double2 cw, double tw, int W, int lane,
                                             const double2* __restrict__ cs2, double* dgo, double* odo) {
   const int w0 = max(0, 2 * W - O);
+  const int npu = W - O;  // pair row units above the diagonal block
   if (w2) {
-    for (int U = lane; U < W; U += 32) {
+    if (O == 1 && lane == 0 && W > 0) {  // block ({0}, W)
+      const double a00 = c0p[0], a01 = c1p[0];
+      const double r00 = cw.y * a00 + cw.x * a01, r01 = cw.x * a00 - cw.y * a01;
+      c0p[0] = r00;
+      c1p[0] = r01;
+      if (W == 1) publish<K>(odo, 0, r00);
+    }
+    for (int k = lane; k < npu; k += 32) {
+      const int u0 = 2 * k + O;
+      const double2 cu = cs2[k];
       double a00, a10, a01, a11;
-      double2 cu;
-      int u0;
-      bool u2 = true;
-      if (O == 1 && U == 0) {  // singleton row unit {0}
-        u0 = 0;
-        u2 = false;
-        cu = make_double2(1.0, 0.0);
-        a00 = c0p[0];
-        a01 = c1p[0];
-        a10 = a11 = 0.0;
+      if (O == 0) {
+        const double2 x0 = *reinterpret_cast<const double2*>(c0p + u0);
+        const double2 x1 = *reinterpret_cast<const double2*>(&c1p[u0]);
+        a00 = x0.x;
+        a10 = x0.y;
+        a01 = x1.x;
+        a11 = x1.y;
       } else {
-        u0 = 2 * U - O;
-        cu = cs2[U - O];
-        if (O == 0) {
-          const double2 x0 = *reinterpret_cast<const double2*>(c0p + u0);
-          const double2 x1 = *reinterpret_cast<const double2*>(&c1p[u0]);
-          a00 = x0.x;
-          a10 = x0.y;
-          a01 = x1.x;
-          a11 = x1.y;
-        } else {
-          a00 = c0p[u0];
-          a10 = c0p[u0 + 1];
-          a01 = c1p[u0];
-          a11 = c1p[u0 + 1];
-        }
+        a00 = c0p[u0];
+        a10 = c0p[u0 + 1];
+        a01 = c1p[u0];
+        a11 = c1p[u0 + 1];
       }
-      // left Ĵ_Uᵀ: rows (u0, u0+1) <- (s a_u0 + c a_u1, c a_u0 - s a_u1); then right Ĵ_W on columns
-      double l00 = a00, l10 = a10, l01 = a01, l11 = a11;
-      if (u2) {
-        l00 = cu.y * a00 + cu.x * a10;
-        l10 = cu.x * a00 - cu.y * a10;
-        l01 = cu.y * a01 + cu.x * a11;
-        l11 = cu.x * a01 - cu.y * a11;
-      }
+      // left Ĵ_Uᵀ: rows (u0, u0+1) <- (s a_u0 + c a_u1, c a_u0 - s a_u1); right Ĵ_W on the columns
+      const double l00 = cu.y * a00 + cu.x * a10, l10 = cu.x * a00 - cu.y * a10;
+      const double l01 = cu.y * a01 + cu.x * a11, l11 = cu.x * a01 - cu.y * a11;
       const double r00 = cw.y * l00 + cw.x * l01, r01 = cw.x * l00 - cw.y * l01;
       const double r10 = cw.y * l10 + cw.x * l11, r11 = cw.x * l10 - cw.y * l11;
-      if (!u2) {
-        c0p[0] = r00;
-        c1p[0] = r01;
-      } else if (O == 0) {
+      if (O == 0) {
         *reinterpret_cast<double2*>(c0p + u0) = make_double2(r00, r10);
         *reinterpret_cast<double2*>(&c1p[u0]) = make_double2(r01, r11);
       } else {
@@ -321,15 +309,17 @@ __device__ __forceinline__ void unit_update(double* c0p, P1 c1p, bool w2, double
         c1p[u0] = r01;
         c1p[u0 + 1] = r11;
       }
-      if (W == U + 1) publish<K>(odo, (u0 + (u2 ? 1 : 0) - (1 - O)) >> 1, u2 ? r10 : r00);
+    }
+    if (npu > 0 && lane == ((npu - 1) & 31)) {  // (last row of unit W-1, column w0) pairs up next step
+      const int r = 2 * (npu - 1) + O + 1;
+      publish<K>(odo, (r - (1 - O)) >> 1, c0p[r]);
     }
     if (lane == (W & 31)) {  // diagonal block (pair unit)
       const double vpp = c0p[w0], vpq = c1p[w0], vqq = c1p[w0 + 1];
       double nd0 = vqq, nd1 = vpp;  // pure swap when s = 0
       if (cw.y != 0.0) {
-        const double tt = cw.y / cw.x;
-        nd0 = vqq + tt * vpq;  // swapped diagonal of JᵀAJ
-        nd1 = vpp - tt * vpq;
+        nd0 = vqq + tw * vpq;  // swapped diagonal of JᵀAJ
+        nd1 = vpp - tw * vpq;
         c1p[w0] = 0.0;
       }
       c0p[w0] = nd0;
@@ -338,28 +328,29 @@ __device__ __forceinline__ void unit_update(double* c0p, P1 c1p, bool w2, double
       publish<K>(dgo, w0 + 1, nd1);
     }
   } else {  // singleton column unit (odd steps: {0} or {ne-1}): only the row rotations act
-    for (int U = lane; U < W; U += 32) {
-      if (U == 0) continue;      // {0} x {ne-1}: two singletons, untouched
-      const int u0 = 2 * U - O;
-      const double2 cu = cs2[U - O];
+    for (int k = lane; k < npu; k += 32) {
+      const int u0 = 2 * k + O;
+      const double2 cu = cs2[k];
       const double a00 = c0p[u0], a10 = c0p[u0 + 1];
-      const double l00 = cu.y * a00 + cu.x * a10, l10 = cu.x * a00 - cu.y * a10;
-      c0p[u0] = l00;
-      c0p[u0 + 1] = l10;
-      if (W == U + 1) publish<K>(odo, (u0 + 1 - (1 - O)) >> 1, l10);
+      c0p[u0] = cu.y * a00 + cu.x * a10;
+      c0p[u0 + 1] = cu.x * a00 - cu.y * a10;
+    }
+    if (npu > 0 && lane == ((npu - 1) & 31)) {
+      const int r = 2 * (npu - 1) + O + 1;
+      publish<K>(odo, (r - (1 - O)) >> 1, c0p[r]);
     }
     if (lane == (W & 31)) publish<K>(dgo, w0, c0p[w0]);
   }
 }
 
-constexpr int kJT = 512;   // threads per CTA
+constexpr int kJT = 1024;  // threads per CTA
 template <int K>
 __global__ void __launch_bounds__(kJT, 1) k_jacobi_oe(const double* __restrict__ Ain, double* __restrict__ ev,
                                                    const int* __restrict__ nvec, const long long* __restrict__ off,
                                                    const long long* __restrict__ ev_off, int max_sweeps, Crit crit_in,
                                                    double floor_rel, double conv_rel, int* __restrict__ sweeps_out,
                                                    double2* __restrict__ rot, const long long* __restrict__ rot_off,
-                                                   int chunk, int nemax, int max_items) {
+                                                   int chunk, int nemax, int max_items, int exper) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double smem[];
   int rank = 0;
@@ -371,7 +362,8 @@ __global__ void __launch_bounds__(kJT, 1) k_jacobi_oe(const double* __restrict__
   double* dg = smem + chunk;                                   // [2][nemax] diagonal tables
   double* od = dg + 2 * nemax;                                 // [2][nemax/2] next-pair superdiagonals
   double2* cs2 = reinterpret_cast<double2*>(od + nemax);       // [nemax/2] (c, s) of this step
-  double** colp = reinterpret_cast<double**>(cs2 + nemax / 2);  // generic pointer to column j
+  double* tn = reinterpret_cast<double*>(cs2 + nemax / 2);     // [nemax/2] tan θ of this step
+  double** colp = reinterpret_cast<double**>(tn + nemax / 2);  // generic pointer to column j
   int* lcol = reinterpret_cast<int*>(colp + nemax);            // local start of column j
   int* items = lcol + nemax;                                   // [2][max_items] unit lists
   unsigned char* own = reinterpret_cast<unsigned char*>(items + 2 * max_items);
@@ -447,18 +439,19 @@ __global__ void __launch_bounds__(kJT, 1) k_jacobi_oe(const double* __restrict__
         const int p = o + 2 * k, q = p + 1;
         const double app = dgi[p], aqq = dgi[q], apq = odi[k];
         double c = 1.0, sv = 0.0;
-        const int d = rot_decision(crit, app, aqq, apq);
+        const int d = exper == 2 ? 0 : rot_decision(crit, app, aqq, apq);
         if (d) {
           schur2(app, aqq, apq, c, sv);
           if (d == 2 && fabs(sv) > crit.conv_angle * c) active[sa] = 1;
         }
         cs2[k] = make_double2(c, sv);
+        tn[k] = c != 0.0 ? sv / c : 0.0;
         if (rank == 0) R[(static_cast<long long>(sweep) * ne + t) * np + k] = make_double2(c, sv);
       }
       __syncthreads();
       double* dgo = dg + bo * nemax;
       double* odo = od + bo * (nemax / 2);
-      const int nun = nitems[o];
+      const int nun = exper == 1 ? 0 : nitems[o];
       const int* ul = items + o * max_items;
       for (int r0 = 0; r0 < nun; r0 += NW) {
         const int x = r0 + (((r0 / NW) & 1) ? NW - 1 - warp : warp);
@@ -468,13 +461,14 @@ __global__ void __launch_bounds__(kJT, 1) k_jacobi_oe(const double* __restrict__
         const int kw = W - o;
         const bool w2 = kw >= 0 && kw < npair;
         const double2 cw = w2 ? cs2[kw] : make_double2(1.0, 0.0);
+        const double tw = w2 ? tn[kw] : 0.0;
         double* c0p = smem + lcol[w0];  // the unit's first column is always mine
         if (!w2 || own[w0 + 1] == rank) {
           double* c1p = w2 ? smem + lcol[w0 + 1] : c0p;
-          if (o) unit_update<K, 1>(c0p, c1p, w2, cw, W, npair, lane, cs2, dgo, odo);
-          else unit_update<K, 0>(c0p, c1p, w2, cw, W, npair, lane, cs2, dgo, odo);
+          if (o) unit_update<K, 1>(c0p, c1p, w2, cw, tw, W, lane, cs2, dgo, odo);
+          else unit_update<K, 0>(c0p, c1p, w2, cw, tw, W, lane, cs2, dgo, odo);
         } else {  // odd-step boundary unit: second column lives in the next CTA
-          unit_update<K, 1>(c0p, colp[w0 + 1], w2, cw, W, npair, lane, cs2, dgo, odo);
+          unit_update<K, 1>(c0p, colp[w0 + 1], w2, cw, tw, W, lane, cs2, dgo, odo);
         }
       }
       if constexpr (K > 1) cg::this_cluster().sync(); else __syncthreads();
@@ -690,7 +684,57 @@ __global__ void k_compact(const double* __restrict__ Vp, const double* __restric
   }
 }
 
+// random symmetric test matrices (benchmark only): a_ij = hash(i, j, b) in [-1, 1], diagonal + n
+__global__ void k_rand_sym(double* __restrict__ A, int n) {
+  const int b = blockIdx.y;
+  double* a = A + static_cast<size_t>(b) * n * n;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(n) * n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e % n), c = static_cast<int>(e / n);
+    const int lo = min(r, c), hi = max(r, c);
+    unsigned long long x = (static_cast<unsigned long long>(b) * 1000003ull + lo) * 1000033ull + hi;
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    const double v = static_cast<double>(x >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    a[e] = (r == c) ? v + n : v;
+  }
+}
+
 }  // namespace
+
+// Jacobi throughput probe: B random symmetric matrices of order n, exactly `sweeps` sweeps
+// (every pair rotates), eigenvalues and eigenvectors; returns milliseconds (CUDA events).
+double bench_syevj(Ctx& c, int n, int B, int sweeps) {
+  DBuf<double> A, V, ev;
+  A.ensure(static_cast<size_t>(B) * n * n);
+  V.ensure(static_cast<size_t>(B) * n * n);
+  ev.ensure(static_cast<size_t>(B) * n);
+  k_rand_sym<<<dim3(64, B), 256, 0, c.stream>>>(A.p, n);
+  RDD_LAUNCH_CHECK();
+  std::vector<int> nn(B, n);
+  std::vector<long long> off(B);
+  for (int b = 0; b < B; ++b) off[b] = static_cast<long long>(b) * n * n;
+  EigOpts o;
+  o.absolute = 1;
+  o.tol = 1e-300;
+  o.max_sweeps = sweeps;
+  batched_syevj(c, A.p, V.p, ev.p, nn, off, o);  // warm-up (workspaces, attributes)
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, c.stream);
+  batched_syevj(c, A.p, V.p, ev.p, nn, off, o);
+  cudaEventRecord(e1, c.stream);
+  RDD_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ms;
+}
 
 // shared memory of k_jacobi_oe<K> for even order ne
 static size_t oe_chunk(int ne, int K) {
@@ -702,7 +746,8 @@ static size_t oe_chunk(int ne, int K) {
 static int oe_items(int ne) { return ne / 2 + 1; }  // column units of one parity
 static size_t oe_smem(int ne, int K) {
   return oe_chunk(ne, K) * sizeof(double) + static_cast<size_t>(3 * ne) * sizeof(double) +
-         static_cast<size_t>(ne / 2) * sizeof(double2) + static_cast<size_t>(ne) * (sizeof(double*) + sizeof(int) + 1) +
+         static_cast<size_t>(ne / 2) * (sizeof(double2) + sizeof(double)) +
+         static_cast<size_t>(ne) * (sizeof(double*) + sizeof(int) + 1) +
          static_cast<size_t>(2 * oe_items(ne)) * sizeof(int) + 64;
 }
 static int oe_k(int ne) {
@@ -767,6 +812,8 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
   rot.p = reinterpret_cast<double2*>(c.ws("syevj.rot", 2 * static_cast<size_t>(std::max<long long>(1, rt))));
   const int ne = nmax + (nmax & 1);
   int K = oe_k(ne);
+  const char* ex = std::getenv("RDD_JACOBI_EXP");  // tuning experiments only: 1 no update, 2 no rotation
+  const int exper = ex ? std::atoi(ex) : 0;
   if (const char* e = std::getenv("RDD_JACOBI_K")) {  // experiment override (larger clusters only)
     const int k = std::atoi(e);
     if (K > 0 && k > K && k <= 8 && (k & (k - 1)) == 0) K = k;
@@ -793,7 +840,7 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
       RDD_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<const double*>(A), evp.p, static_cast<const int*>(dn.p),
                                   static_cast<const long long*>(doff.p), static_cast<const long long*>(deoffp.p),
                                   max_sweeps, crit, o.floor_rel, o.conv_rel, dsw.p, rot.p,
-                                  static_cast<const long long*>(droff.p), chunk, ne, oe_items(ne)));
+                                  static_cast<const long long*>(droff.p), chunk, ne, oe_items(ne), exper));
       ++launch_counter();
     };
     if (K == 1) launch(k_jacobi_oe<1>);

@@ -193,6 +193,11 @@ __global__ void k_scal_div(double* __restrict__ out, const double* __restrict__ 
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i] / s;
 }
 
+// out = ca·a + cb·b (out may alias a or b)
+__global__ void k_lincomb(double* out, const double* a, double ca, const double* b, double cb, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = ca * a[i] + cb * b[i];
+}
+
 struct Vecs {
   int n;
   Ctx* c;
@@ -486,6 +491,158 @@ static void gmres_solve(Ctx& c, const double* b, double* x, double tol, int max_
   c.brk[comp] = breakdown;
 }
 
+static void lincomb(Ctx& c, double* out, const double* a, double ca, const double* b, double cb, int n) {
+  k_lincomb<<<kRB, kRT, 0, c.stream>>>(out, a, ca, b, cb, n);
+  RDD_LAUNCH_CHECK();
+}
+
+static void precond_t(Ctx& c, const double* v, double* z) {
+  if (c.pkind == RDD_PRECOND_NONE) {
+    k_copy<<<kRB, kRT, 0, c.stream>>>(z, v, c.p);
+    RDD_LAUNCH_CHECK();
+  } else {
+    precond_apply_dev(c, v, z, true);
+  }
+}
+
+// ‖b - A x‖ / ‖b‖ (the reference's diagnostic true residual)
+static double true_residual(Ctx& c, const double* b, const double* x, double bnorm, double* t, double* part) {
+  normal_operator(c, x, t);
+  k_sub<<<kRB, kRT, 0, c.stream>>>(t, b, t, c.p);
+  RDD_LAUNCH_CHECK();
+  return bnorm > 0.0 ? std::sqrt(dot_host(c, t, t, c.p, part)) / bnorm : 0.0;
+}
+
+// ---------------------------------------------------------------- CGS (krylov.hpp:159-213)
+static void cgs_solve(Ctx& c, const double* b, double* x, double tol, int max_iter, int comp) {
+  const int n = c.p;
+  const bool ident = c.pkind == RDD_PRECOND_NONE;
+  double* part = c.scal.ensure(8 * kRB + 64);
+  double* v = c.wk(static_cast<size_t>(n) * 9);
+  double *r = v, *rstar = v + n, *p = v + 2 * n, *u = v + 3 * n, *q = v + 4 * n, *uq = v + 5 * n, *Cp = v + 6 * n,
+         *t = v + 7 * n, *t2 = v + 8 * n;
+  auto& hist = c.hist[comp];
+  auto& thist = c.true_hist[comp];
+  hist.clear();
+  thist.clear();
+  c.iters[comp] = 0;
+  c.conv[comp] = 0;
+  c.brk[comp] = 0;
+  Vecs V{n, &c};
+  auto Cop = [&](const double* in, double* out) {  // C = M A
+    normal_operator(c, in, t2);
+    precond(c, t2, out);
+  };
+  const double bnorm = std::sqrt(dot_host(c, b, b, n, part));
+  V.fill(x, 0.0);
+  precond(c, b, r);  // g = M b
+  const double gnorm = std::sqrt(dot_host(c, r, r, n, part));
+  if (gnorm == 0.0) {
+    hist = {0.0};
+    thist = {0.0};
+    c.conv[comp] = 1;
+    return;
+  }
+  V.copy(rstar, r);
+  V.copy(p, r);
+  V.copy(u, r);
+  double rho = dot_host(c, rstar, r, n, part);
+  hist.push_back(1.0);
+  thist.push_back(bnorm > 0.0 ? 1.0 : 0.0);
+  for (int it = 0; it < max_iter; ++it) {
+    Cop(p, Cp);
+    const double sigma = dot_host(c, rstar, Cp, n, part);
+    if (sigma == 0.0 || rho == 0.0) {
+      c.brk[comp] = 1;
+      break;
+    }
+    const double alpha = rho / sigma;
+    lincomb(c, q, u, 1.0, Cp, -alpha, n);
+    lincomb(c, uq, u, 1.0, q, 1.0, n);
+    lincomb(c, x, x, 1.0, uq, alpha, n);
+    Cop(uq, Cp);
+    lincomb(c, r, r, 1.0, Cp, -alpha, n);
+    const double rel = std::sqrt(dot_host(c, r, r, n, part)) / gnorm;
+    hist.push_back(rel);
+    thist.push_back(ident ? rel : true_residual(c, b, x, bnorm, t, part));
+    ++c.iters[comp];
+    if (rel <= tol) {
+      c.conv[comp] = 1;
+      break;
+    }
+    const double rho_new = dot_host(c, rstar, r, n, part);
+    const double beta = rho_new / rho;
+    rho = rho_new;
+    lincomb(c, u, r, 1.0, q, beta, n);
+    lincomb(c, t, q, 1.0, p, beta, n);
+    lincomb(c, p, u, 1.0, t, beta, n);
+  }
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// ---------------------------------------------------------------- BiCG (krylov.hpp:217-270)
+static void bicg_solve(Ctx& c, const double* b, double* x, double tol, int max_iter, int comp) {
+  const int n = c.p;
+  const bool ident = c.pkind == RDD_PRECOND_NONE;
+  double* part = c.scal.ensure(8 * kRB + 64);
+  double* v = c.wk(static_cast<size_t>(n) * 8);
+  double *r = v, *rstar = v + n, *p = v + 2 * n, *ps = v + 3 * n, *Cp = v + 4 * n, *Cps = v + 5 * n, *t = v + 6 * n,
+         *t2 = v + 7 * n;
+  auto& hist = c.hist[comp];
+  auto& thist = c.true_hist[comp];
+  hist.clear();
+  thist.clear();
+  c.iters[comp] = 0;
+  c.conv[comp] = 0;
+  c.brk[comp] = 0;
+  Vecs V{n, &c};
+  const double bnorm = std::sqrt(dot_host(c, b, b, n, part));
+  V.fill(x, 0.0);
+  precond(c, b, r);
+  const double gnorm = std::sqrt(dot_host(c, r, r, n, part));
+  if (gnorm == 0.0) {
+    hist = {0.0};
+    thist = {0.0};
+    c.conv[comp] = 1;
+    return;
+  }
+  V.copy(rstar, r);
+  V.copy(p, r);
+  V.copy(ps, r);
+  double rho = dot_host(c, rstar, r, n, part);
+  hist.push_back(1.0);
+  thist.push_back(bnorm > 0.0 ? 1.0 : 0.0);
+  for (int it = 0; it < max_iter; ++it) {
+    normal_operator(c, p, t2);  // C p = M (A p)
+    precond(c, t2, Cp);
+    const double sigma = dot_host(c, ps, Cp, n, part);
+    if (sigma == 0.0 || rho == 0.0) {
+      c.brk[comp] = 1;
+      break;
+    }
+    const double alpha = rho / sigma;
+    lincomb(c, x, x, 1.0, p, alpha, n);
+    lincomb(c, r, r, 1.0, Cp, -alpha, n);
+    precond_t(c, ps, t2);  // Cᵀ p* = Aᵀ (Mᵀ p*), A symmetric
+    normal_operator(c, t2, Cps);
+    lincomb(c, rstar, rstar, 1.0, Cps, -alpha, n);
+    const double rel = std::sqrt(dot_host(c, r, r, n, part)) / gnorm;
+    hist.push_back(rel);
+    thist.push_back(ident ? rel : true_residual(c, b, x, bnorm, t, part));
+    ++c.iters[comp];
+    if (rel <= tol) {
+      c.conv[comp] = 1;
+      break;
+    }
+    const double rho_new = dot_host(c, rstar, r, n, part);
+    const double beta = rho_new / rho;
+    rho = rho_new;
+    lincomb(c, p, r, 1.0, p, beta, n);
+    lincomb(c, ps, rstar, 1.0, ps, beta, n);
+  }
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+}
+
 // runner.hpp:239-251: per component b = Hᵀ F_c, solve, W = y ./ scales
 void solve_all(Ctx& c, int solver, double tol, int max_iter_cfg, int restart) {
   ScopedKernelTimer tk(c, "solve");
@@ -505,6 +662,8 @@ void solve_all(Ctx& c, int solver, double tol, int max_iter_cfg, int restart) {
     matvec_t_dev(c, c.F.p + static_cast<size_t>(comp) * c.N, b.p);
     if (solver == RDD_SOLVER_CG) cg_solve(c, b.p, x.p, tol, max_iter, comp);
     else if (solver == RDD_SOLVER_GMRES) gmres_solve(c, b.p, x.p, tol, max_iter, restart, comp);
+    else if (solver == RDD_SOLVER_CGS) cgs_solve(c, b.p, x.p, tol, max_iter, comp);
+    else if (solver == RDD_SOLVER_BICG) bicg_solve(c, b.p, x.p, tol, max_iter, comp);
     else throw std::invalid_argument("solver not available on the device path");
     k_scale_to<<<kRB, kRT, 0, c.stream>>>(c.W.p + static_cast<size_t>(comp) * n, x.p, c.scales.p, n, 1);
     RDD_LAUNCH_CHECK();

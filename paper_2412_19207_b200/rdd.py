@@ -72,6 +72,7 @@ def lib():
         L.rdd_set_timing.argtypes = [vp, C.c_int]
         L.rdd_set_verbose.argtypes = [vp, C.c_int]
         L.rdd_bench_operator.argtypes = [vp, C.c_int, C.c_int, dp, dp]
+        L.rdd_bench_jacobi.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp]
         _lib = L
     return _lib
 
@@ -210,6 +211,11 @@ class Solver:
         n = C.c_int64()
         self.L.rdd_kernel_stats(self.h, family.encode(), C.byref(ms), C.byref(n))
         return ms.value, n.value
+
+    def bench_jacobi(self, n: int, batch: int, sweeps: int) -> float:
+        ms = C.c_double()
+        self._check(self.L.rdd_bench_jacobi(self.h, n, batch, sweeps, C.byref(ms)))
+        return ms.value
 
     def bench_operator(self, op_form: int, reps: int = 20):
         ms = C.c_double()

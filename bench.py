@@ -298,7 +298,7 @@ def main():
         args.warmup = 3
     world, rank, local, dist = dist_setup()
     from paper_2412_19207_b200 import configs
-    cfg = configs.BASELINE[args.config]()
+    cfg = configs.aspcg(args.config)  # the metric: AS-PCG on every config
     try:
         if args.impl == "reference":
             rc = run_reference(args, cfg, world, rank, dist)

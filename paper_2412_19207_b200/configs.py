@@ -72,6 +72,14 @@ def scaled(cfg: A.Config, counts, per_axis_points, m=None) -> A.Config:
 BASELINE = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5}
 
 
+def aspcg(name: str) -> A.Config:
+    """The metric's solver on any config: AS-preconditioned CG (C3/C4 name RAS-GMRES(50) as their
+    own solver; the BASELINE metric reports AS-PCG for every config)."""
+    cfg = BASELINE[name]()
+    cfg.solver, cfg.precond = A.SOLVER_CG, A.PRECOND_AS
+    return cfg
+
+
 # ---- golden cases (reference test artefacts) -------------------------------------------
 def golden_h_export() -> A.Config:
     """test_assembly.cpp:188-210 build_pipeline(2,3,6,21): example1 n=2, 2x2, delta 2, m=3, 6x6."""

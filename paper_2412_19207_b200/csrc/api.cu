@@ -389,6 +389,8 @@ int64_t rdd_get_i(rdd_ctx* h, const char* what, int index, int32_t* out, int64_t
         v.push_back(c.nb_j2[k]);
       }
     } else if (w == "local_rank") v = c.local_rank;
+    else if (w == "local_n") v = c.local_n;
+    else if (w == "row_ptr") v = c.h_row_ptr;
     else if (w == "set") v.assign(c.set_idx.begin() + c.set_ptr.at(index), c.set_idx.begin() + c.set_ptr.at(index + 1));
     else if (w == "owner") v = c.h_owner;
     else if (w == "mult") v = c.h_mult;

@@ -29,11 +29,17 @@ struct Mat {
   int n;          // order (= leading dimension)
 };
 
-// A[k-block, k-block] <- chol (lower); pads beyond n act as identity
+// A[k-block, k-block] <- chol (lower); pads beyond n act as identity. Also D_k = L_kk⁻¹ (lower,
+// padding identity) into the per-matrix diagonal-inverse workspace: the panel solve becomes a DMMA
+// product with D_kᵀ and the packed factor stores D_k.
 __global__ void k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mats, const int* __restrict__ act, int k,
-                             int* __restrict__ fail) {
-  __shared__ double s[NB][NB + 1];
-  const Mat M = mats[act[blockIdx.x]];
+                             int* __restrict__ fail, double* __restrict__ Dinv, const long long* __restrict__ doff) {
+  extern __shared__ double dsm[];
+  double(*s)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
+  double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
+  __shared__ double d;
+  const int q = act[blockIdx.x];
+  const Mat M = mats[q];
   const int k0 = k * NB, bs = min(NB, M.n - k0);
   double* a = A + M.off + k0 + static_cast<long long>(k0) * M.n;
   for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
@@ -42,10 +48,9 @@ __global__ void k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mat
   }
   __syncthreads();
   for (int c = 0; c < NB; ++c) {
-    __shared__ double d;
     if (threadIdx.x == 0) {
       const double v = s[c][c];
-      if (!(v > 0.0)) fail[act[blockIdx.x]] = 1;
+      if (!(v > 0.0)) fail[q] = 1;
       d = sqrt(fmax(v, 1e-300));
       s[c][c] = d;
     }
@@ -53,8 +58,8 @@ __global__ void k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mat
     for (int r = c + 1 + threadIdx.x; r < NB; r += blockDim.x) s[r][c] /= d;
     __syncthreads();
     for (int e = threadIdx.x; e < (NB - c - 1) * (NB - c - 1); e += blockDim.x) {
-      const int r = c + 1 + e % (NB - c - 1), q = c + 1 + e / (NB - c - 1);
-      if (q <= r) s[r][q] -= s[r][c] * s[q][c];
+      const int r = c + 1 + e % (NB - c - 1), qq = c + 1 + e / (NB - c - 1);
+      if (qq <= r) s[r][qq] -= s[r][c] * s[qq][c];
     }
     __syncthreads();
   }
@@ -62,49 +67,25 @@ __global__ void k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mat
     const int r = e % NB, c = e / NB;
     if (r < bs && c < bs) a[r + static_cast<long long>(c) * M.n] = r >= c ? s[r][c] : 0.0;
   }
-}
-
-// panel: X = A[i-block, k-block] L_kk^{-T} for the task's row block i > k
-__global__ void k_trsm_panel(double* __restrict__ A, const Mat* __restrict__ mats, const int2* __restrict__ tasks,
-                             int k) {
-  extern __shared__ double dsm[];
-  double(*L)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
-  double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
-  const int2 t = tasks[blockIdx.x];
-  const Mat M = mats[t.x];
-  const int k0 = k * NB, bs = min(NB, M.n - k0);
-  const int i0 = t.y * NB, rs = min(NB, M.n - i0);
-  const double* l = A + M.off + k0 + static_cast<long long>(k0) * M.n;
-  double* a = A + M.off + i0 + static_cast<long long>(k0) * M.n;
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
-    const int r = e % NB, c = e / NB;
-    L[r][c] = (r < bs && c < bs) ? l[r + static_cast<long long>(c) * M.n] : (r == c ? 1.0 : 0.0);
-    X[r][c] = (r < rs && c < bs) ? a[r + static_cast<long long>(c) * M.n] : 0.0;
-  }
-  __syncthreads();
-  const int r = threadIdx.x;  // one row per thread, forward substitution over columns
-  if (r < rs) {
-    for (int c = 0; c < bs; ++c) {
-      double v = X[r][c];
-      for (int q = 0; q < c; ++q) v -= X[r][q] * L[c][q];
-      X[r][c] = v / L[c][c];
+  const int c = threadIdx.x;  // column c of L⁻¹: forward substitution down the rows
+  if (c < NB) {
+    for (int r = 0; r < NB; ++r) {
+      double v = (r == c) ? 1.0 : 0.0;
+      for (int qq = c; qq < r; ++qq) v -= s[r][qq] * X[qq][c];
+      X[r][c] = r < c ? 0.0 : v / s[r][r];
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
-    const int rr = e % NB, c = e / NB;
-    if (rr < rs && c < bs) a[rr + static_cast<long long>(c) * M.n] = X[rr][c];
-  }
+  double* o = Dinv + doff[q] + static_cast<long long>(k) * NB * NB;
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) o[e] = X[e % NB][e / NB];
 }
 
+
 // Block row k of the tile-packed factor: tiles (k, j<k) copied from the factored matrix (zero
-// padding past n) and the diagonal tile L_kk⁻¹ (lower; the padding acts as identity).
-// task = (matrix, k)
+// padding past n) and the diagonal tile D_k = L_kk⁻¹ from the workspace. task = (matrix, k)
 __global__ void k_pack_row(const double* __restrict__ A, const Mat* __restrict__ mats, const int2* __restrict__ tasks,
-                           double* __restrict__ P, const long long* __restrict__ poff) {
-  extern __shared__ double dsm[];
-  double(*L)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
-  double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
+                           double* __restrict__ P, const long long* __restrict__ poff, const double* __restrict__ Dinv,
+                           const long long* __restrict__ doff) {
   const int2 t = tasks[blockIdx.x];
   const Mat M = mats[t.x];
   const int k = t.y, k0 = k * NB, bs = min(NB, M.n - k0);
@@ -117,23 +98,9 @@ __global__ void k_pack_row(const double* __restrict__ A, const Mat* __restrict__
       o[e] = r < bs ? a[r + static_cast<long long>(c) * M.n] : 0.0;
     }
   }
-  const double* l = A + M.off + k0 + static_cast<long long>(k0) * M.n;
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
-    const int r = e % NB, c = e / NB;
-    L[r][c] = (r < bs && c < bs) ? l[r + static_cast<long long>(c) * M.n] : (r == c ? 1.0 : 0.0);
-  }
-  __syncthreads();
-  const int c = threadIdx.x;  // column c of L^{-1}: forward substitution down the rows
-  if (c < NB) {
-    for (int r = 0; r < NB; ++r) {
-      double v = (r == c) ? 1.0 : 0.0;
-      for (int q = c; q < r; ++q) v -= L[r][q] * X[q][c];
-      X[r][c] = r < c ? 0.0 : v / L[r][r];
-    }
-  }
-  __syncthreads();
+  const double* d = Dinv + doff[t.x] + static_cast<long long>(k) * NB * NB;
   double* o = row + static_cast<long long>(k) * NB * NB;
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) o[e] = X[e % NB][e / NB];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) o[e] = d[e];
 }
 
 __global__ void k_frob(const double* __restrict__ A, const Mat* __restrict__ mats, double* __restrict__ out) {
@@ -194,13 +161,16 @@ __global__ void k_power(const double* __restrict__ A, const Mat* __restrict__ ma
   if (threadIdx.x == 0) out[blockIdx.x] = lam;
 }
 
-// Trailing-update GEMM tasks of one factor step, generated on the device from one descriptor per
-// (matrix, kind): kind 0 = inside the outer panel (columns jb in (k, oend), K = 64 at column k),
-// kind 1 = right of a completed outer panel (jb >= oend, K = the panel width). C[ib, jb] -= A_ib A_jbᵀ.
+// GEMM tasks of one factor step, generated on the device from one descriptor per (matrix, kind):
+// kind 0 = inside the outer panel (columns jb in (k, oend), K = 64 at column k), kind 1 = right of
+// a completed outer panel (jb >= oend, K = the panel width): C[ib, jb] -= A_ib A_jbᵀ; kind 2 = the
+// panel solve A[ib, k] <- A[ib, k] D_kᵀ for ib > k (in place: each CTA reads its whole tile before
+// its epilogue writes it).
 struct UpdDesc {
   long long off;   // matrix offset
   long long first; // first task index of this entry
   int n, k, ostart, oend, kind, pad;
+  const double* D; // kind 2: D_k
 };
 __global__ void k_make_updates(double* __restrict__ A, const UpdDesc* __restrict__ d, int nd, long long total,
                                GemmTask* __restrict__ out) {
@@ -215,6 +185,24 @@ __global__ void k_make_updates(double* __restrict__ A, const UpdDesc* __restrict
   const UpdDesc e = d[lo];
   long long loc = t - e.first;
   const int nb = (e.n + NB - 1) / NB;
+  double* base = A + e.off;
+  GemmTask g{};
+  g.gA = g.gB = nullptr;
+  g.tm = g.tn = 0;
+  if (e.kind == 2) {
+    const int ib = e.k + 1 + static_cast<int>(loc), k0 = e.k * NB;
+    g.A = base + ib * NB + static_cast<long long>(k0) * e.n;
+    g.B = e.D;
+    g.Cm = base + ib * NB + static_cast<long long>(k0) * e.n;
+    g.M = min(NB, e.n - ib * NB);
+    g.N = g.K = min(NB, e.n - k0);
+    g.lda = g.ldc = e.n;
+    g.ldb = NB;
+    g.beta = 0.0;
+    g.alpha = 1.0;
+    out[t] = g;
+    return;
+  }
   const int jb0 = e.kind == 0 ? e.k + 1 : e.oend;
   const int jb1 = e.kind == 0 ? e.oend : nb;  // exclusive
   int jb = jb0;
@@ -226,17 +214,13 @@ __global__ void k_make_updates(double* __restrict__ A, const UpdDesc* __restrict
   const int ib = jb + static_cast<int>(loc);
   const int c0 = e.kind == 0 ? e.k * NB : e.ostart * NB;
   const int kw = e.kind == 0 ? min(NB, e.n - c0) : min(e.n, e.oend * NB) - c0;
-  double* base = A + e.off;
-  GemmTask g{};
   g.A = base + ib * NB + static_cast<long long>(c0) * e.n;
   g.B = base + jb * NB + static_cast<long long>(c0) * e.n;
   g.Cm = base + ib * NB + static_cast<long long>(jb) * NB * e.n;
-  g.gA = g.gB = nullptr;
   g.M = min(NB, e.n - ib * NB);
   g.N = min(NB, e.n - jb * NB);
   g.K = kw;
   g.lda = g.ldb = g.ldc = e.n;
-  g.tm = g.tn = 0;
   g.beta = 1.0;
   g.alpha = -1.0;
   out[t] = g;
@@ -428,71 +412,103 @@ void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const s
     mats[i] = {off[i], n[i]};
     nmax = std::max(nmax, n[i]);
   }
-  RDD_CUDA(cudaFuncSetAttribute(k_trsm_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
-  RDD_CUDA(cudaFuncSetAttribute(k_pack_row, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
+  RDD_CUDA(cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
   DBuf<Mat> dm;
   DBuf<int> dfail, dact;
-  DBuf<int2> dt;
   DBuf<double> dfa;
-  DBuf<long long> dpoff;
+  DBuf<long long> dpoff, ddoff;
   dm.upload(mats, c.stream);
   dfail.zero(B, c.stream);
   dfa.ensure(B);
   k_frob<<<B, 256, 0, c.stream>>>(A, dm.p, dfa.p);
   RDD_LAUNCH_CHECK();
+  std::vector<long long> doff(B);
+  long long dtot = 0;
+  for (int i = 0; i < B; ++i) {
+    doff[i] = dtot;
+    dtot += static_cast<long long>(ceil_div(n[i], NB)) * NB * NB;
+  }
+  double* Dinv = c.ws("chol.Dinv", std::max<long long>(1, dtot));
+  ddoff.upload(doff, c.stream);
   // two-level blocking: 64-wide steps update only the columns of their 256-wide outer panel;
-  // the trailing matrix right of an outer panel takes one K = 256 update when the panel is done
+  // the trailing matrix right of an outer panel takes one K = 256 update when the panel is done.
+  // Every step's work lists are built up front and uploaded once: the step loop only launches.
   const int nbmax = ceil_div(nmax, NB);
   constexpr int kOuter = 4;  // inner blocks per outer panel
-  DBuf<UpdDesc> dud;
-  DBuf<GemmTask>& dtask = c.wsg;
+  struct Step {
+    size_t act0, nact, sd0, nsd, ud0, nud;
+    long long stotal, utotal;
+  };
+  std::vector<Step> steps(nbmax);
+  std::vector<int> act;
+  std::vector<UpdDesc> sd, ud;
+  long long tmax = 0;
   for (int k = 0; k < nbmax; ++k) {
-    std::vector<int> act;
-    std::vector<int2> pan;
-    std::vector<UpdDesc> ud;
-    long long total = 0;
+    Step& st = steps[k];
+    st.act0 = act.size();
+    st.sd0 = sd.size();
+    st.ud0 = ud.size();
+    long long stotal = 0, utotal = 0;
     const int ostart = (k / kOuter) * kOuter;
     for (int i = 0; i < B; ++i) {
       const int nb = ceil_div(n[i], NB);
       if (k >= nb) continue;
       act.push_back(i);
       const int oend = std::min(nb, ostart + kOuter);
-      for (int ib = k + 1; ib < nb; ++ib) pan.push_back(make_int2(i, ib));
+      if (nb - k - 1 > 0) {  // panel solve
+        sd.push_back({off[i], stotal, n[i], k, ostart, oend, 2, 0, Dinv + doff[i] + static_cast<long long>(k) * NB * NB});
+        stotal += nb - k - 1;
+      }
       long long cnt = 0;
       for (int jb = k + 1; jb < oend; ++jb) cnt += nb - jb;
       if (cnt > 0) {
-        ud.push_back({off[i], total, n[i], k, ostart, oend, 0, 0});
-        total += cnt;
+        ud.push_back({off[i], utotal, n[i], k, ostart, oend, 0, 0, nullptr});
+        utotal += cnt;
       }
       if (k == oend - 1 && oend < nb) {
         const long long T = nb - oend;
-        ud.push_back({off[i], total, n[i], k, ostart, oend, 1, 0});
-        total += T * (T + 1) / 2;
+        ud.push_back({off[i], utotal, n[i], k, ostart, oend, 1, 0, nullptr});
+        utotal += T * (T + 1) / 2;
       }
     }
-    dact.upload(act, c.stream);
-    k_potrf_diag<<<static_cast<int>(act.size()), 256, 0, c.stream>>>(A, dm.p, dact.p, k, dfail.p);
+    st.nact = act.size() - st.act0;
+    st.nsd = sd.size() - st.sd0;
+    st.nud = ud.size() - st.ud0;
+    st.stotal = stotal;
+    st.utotal = utotal;
+    tmax = std::max(tmax, std::max(stotal, utotal));
+  }
+  DBuf<UpdDesc> dsd, dud;
+  DBuf<GemmTask>& dtask = c.wsg;
+  dact.upload(act, c.stream);
+  dsd.upload(sd, c.stream);
+  dud.upload(ud, c.stream);
+  dtask.ensure(static_cast<size_t>(std::max<long long>(1, tmax)));
+  for (int k = 0; k < nbmax; ++k) {
+    const Step& st = steps[k];
+    k_potrf_diag<<<static_cast<int>(st.nact), 256, kPairSmem, c.stream>>>(A, dm.p, dact.p + st.act0, k, dfail.p, Dinv,
+                                                                           ddoff.p);
     RDD_LAUNCH_CHECK();
-    if (!pan.empty()) {
-      dt.upload(pan, c.stream);
-      k_trsm_panel<<<static_cast<int>(pan.size()), NB, kPairSmem, c.stream>>>(A, dm.p, dt.p, k);
+    if (st.stotal > 0) {  // panel: A[ib, k] <- A[ib, k] D_kᵀ on DMMA
+      k_make_updates<<<ceil_div(st.stotal, 256), 256, 0, c.stream>>>(A, dsd.p + st.sd0, static_cast<int>(st.nsd),
+                                                                      st.stotal, dtask.p);
       RDD_LAUNCH_CHECK();
+      gemm_nt_dev(c, dtask.p, static_cast<int>(st.stotal));
     }
-    if (total > 0) {
-      dud.upload(ud, c.stream);
-      dtask.ensure(static_cast<size_t>(total));
-      k_make_updates<<<ceil_div(total, 256), 256, 0, c.stream>>>(A, dud.p, static_cast<int>(ud.size()), total,
-                                                                  dtask.p);
+    if (st.utotal > 0) {
+      k_make_updates<<<ceil_div(st.utotal, 256), 256, 0, c.stream>>>(A, dud.p + st.ud0, static_cast<int>(st.nud),
+                                                                      st.utotal, dtask.p);
       RDD_LAUNCH_CHECK();
-      gemm_nt_dev(c, dtask.p, static_cast<int>(total));
+      gemm_nt_dev(c, dtask.p, static_cast<int>(st.utotal));
     }
   }
+  DBuf<int2> drows;
   std::vector<int2> rows;
   for (int i = 0; i < B; ++i)
     for (int k = 0; k < ceil_div(n[i], NB); ++k) rows.push_back(make_int2(i, k));
-  dt.upload(rows, c.stream);
+  drows.upload(rows, c.stream);
   dpoff.upload(poff, c.stream);
-  k_pack_row<<<static_cast<int>(rows.size()), 256, kPairSmem, c.stream>>>(A, dm.p, dt.p, P, dpoff.p);
+  k_pack_row<<<static_cast<int>(rows.size()), 256, 0, c.stream>>>(A, dm.p, drows.p, P, dpoff.p, Dinv, ddoff.p);
   RDD_LAUNCH_CHECK();
   dfail.download(fail.data(), B, c.stream);
   dfa.download(frob_A.data(), B, c.stream);

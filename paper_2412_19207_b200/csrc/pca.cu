@@ -309,7 +309,10 @@ void run_pca(Ctx& c) {
     s2.conv_angle = 1e-12;
     // stage 1: Gram, pivoted Cholesky G ≈ L Lᵀ (r = numerical rank), Jacobi on the graded LᵀL
     // (r x r: one CTA, few sweeps), Vr = L U, V0 = Householder completion of Vr to an n x n basis
-    gemm_tn(c, gram_tasks(c, c.S.p, G.p, c.S_off));
+    {
+      ScopedKernelTimer tg(c, "gram");
+      gemm_tn(c, gram_tasks(c, c.S.p, G.p, c.S_off));
+    }
     WS Lw{c.ws("pca.L", J * mm)}, Vr{c.ws("pca.Vr", J * mm)}, Hw{c.ws("pca.H", J * mm)};
     DBuf<int> dr;
     dr.ensure(J);

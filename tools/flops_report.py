@@ -1,0 +1,29 @@
+"""FP64 tensor throughput of the Gram (PCA) and the Schwarz Cholesky for a config, from the
+library's per-family CUDA-event timers and the algorithmic flop counts:
+Gram Σ_j rows_j·m·(m+1) (symmetric), Cholesky Σ_i n_i³/3."""
+import json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+from paper_2412_19207_b200 import rdd, configs, abi as A
+name = sys.argv[1] if len(sys.argv) > 1 else "C5"
+cfg = configs.BASELINE[name]()
+cfg.solver, cfg.precond = A.SOLVER_CG, A.PRECOND_AS
+s = rdd.Solver(0)
+s.run_single(cfg)
+s.set_timing(True)
+s.reset_stats()
+s.rerun_resident()
+rp = s.geti("row_ptr").astype(np.float64)
+rows = np.diff(rp)
+m = cfg.m
+n = s.geti("local_n").astype(np.float64)
+g_ms, _ = s.kernel_stats("gram")
+c_ms, _ = s.kernel_stats("cholesky")
+gram = float((rows * m * (m + 1)).sum())
+chol = float((n ** 3 / 3).sum())
+peak = 35.46  # TF/s, cuBLAS DGEMM measured on this B200 (tools/fp64_peak.py, DMMA pipe 96.5% busy)
+out = {"config": name, "gram_ms": g_ms, "gram_tflops": gram / g_ms / 1e9, "gram_frac": gram / g_ms / 1e9 / peak,
+       "chol_ms": c_ms, "chol_tflops": chol / c_ms / 1e9, "chol_frac": chol / c_ms / 1e9 / peak,
+       "sum_n3_over_3": chol, "n_max": int(n.max()), "peak_tflops": peak}
+print(json.dumps(out))

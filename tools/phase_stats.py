@@ -7,7 +7,7 @@ FAMILIES = ["index", "problem", "assemble", "assemble_psi", "pca_total", "syevj"
             "gemm_nt", "equilibrate", "matvec", "matvec_t", "fused_normal", "normal_blocks", "normal_apply",
             "schwarz_build", "cholesky", "inv_power", "power", "precond_apply", "solve", "evaluate"]
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
-cfg = configs.BASELINE[name]()
+cfg = configs.aspcg(name)
 for kv in sys.argv[2:]:
     k, v = kv.split("=")
     setattr(cfg, k, type(getattr(cfg, k))(float(v)) if isinstance(getattr(cfg, k), float) else int(v))

@@ -3,7 +3,7 @@ import ctypes as C, os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2412_19207_b200 import rdd, configs
-cfg = configs.BASELINE[sys.argv[1] if len(sys.argv) > 1 else "C2"]()
+cfg = configs.aspcg(sys.argv[1] if len(sys.argv) > 1 else "C2")
 s = rdd.Solver(0)
 s.run_single(cfg)
 for i in range(6):

@@ -17,9 +17,6 @@ struct rdd_ctx {
 
 namespace rdd {
 
-static double now_s() {
-  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
 
 void upload_inputs(Ctx& c) {
   c.pts.upload(c.h_pts, c.stream);

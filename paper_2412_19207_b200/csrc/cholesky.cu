@@ -103,12 +103,15 @@ __global__ void k_pack_row(const double* __restrict__ A, const Mat* __restrict__
   for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) o[e] = d[e];
 }
 
+// ‖A‖_F of a symmetric matrix from its lower triangle (the upper one may hold garbage)
 __global__ void k_frob(const double* __restrict__ A, const Mat* __restrict__ mats, double* __restrict__ out) {
   const Mat M = mats[blockIdx.x];
   double s = 0.0;
   for (long long e = threadIdx.x; e < static_cast<long long>(M.n) * M.n; e += blockDim.x) {
+    const int r = static_cast<int>(e % M.n), cc = static_cast<int>(e / M.n);
+    if (r < cc) continue;
     const double v = A[M.off + e];
-    s += v * v;
+    s += (r == cc ? 1.0 : 2.0) * v * v;
   }
   __shared__ double sh[32];
   s = warp_sum(s);

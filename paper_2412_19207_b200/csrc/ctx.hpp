@@ -34,6 +34,10 @@ struct ProblemDesc {
   bool has_exact = true;
 };
 
+inline double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 struct KernelStat {
   double ms = 0.0;
   int64_t launches = 0;
@@ -130,6 +134,7 @@ struct Ctx {
   int nmax_local = 0;
   int n_fallback = 0;                 // local blocks that took the eigen pseudo-inverse
   std::vector<int> fallback, local_n;
+  size_t schwarz_budget = 0;          // bytes of gathered A_i per chunk (fixed per context)
   std::map<int, DBuf<double>> fb_store;  // eigen-fallback subdomains: dense pseudo-inverse
   DBuf<double*> dfb_ptr;              // per i: dense pseudo-inverse or nullptr (factor path)
   bool local_cond_exact = false;
@@ -234,7 +239,8 @@ void fused_normal_apply_dev(Ctx& c, const double* w, double* out);
 // schwarz.cu (K8/K11)
 void build_schwarz(Ctx& c, int kind);
 void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose);
-void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, const std::vector<long long>& off);
+void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, const std::vector<long long>& off,
+                   bool lower_only = false);
 void refresh_local_cond(Ctx& c);
 size_t device_available(Ctx& c);
 void release_scratch(Ctx& c);

@@ -21,20 +21,23 @@ namespace rdd {
 namespace {
 
 // per subdomain: sort eigenvalues descending, threshold, reorder + sign-canonicalise V
+// cnt/lam_off (optional): subdomain j has cnt[j] eigenpairs, eigenvalues at lam + lam_off[j] and
+// V columns 0..cnt[j]-1 (ld m); the remaining min(rows, m) - cnt[j] singular values are reported as 0
 __global__ void k_select(const double* __restrict__ lam, const double* __restrict__ Vin, double* __restrict__ Vout,
                          double* __restrict__ sig, int* __restrict__ p_out, const int* __restrict__ row_ptr, int m,
-                         int tau_mode, double tau) {
+                         int tau_mode, double tau, const int* __restrict__ cnt, const long long* __restrict__ lam_off) {
   extern __shared__ double sm[];
   double* s = sm;                              // m sigma
   int* perm = reinterpret_cast<int*>(s + m);   // m
   __shared__ int keep;
   const int j = blockIdx.x;
-  const double* L = lam + static_cast<size_t>(j) * m;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) s[i] = sqrt(fmax(L[i], 0.0));
+  const int mc = cnt ? cnt[j] : m;
+  const double* L = lam + (lam_off ? lam_off[j] : static_cast<long long>(j) * m);
+  for (int i = threadIdx.x; i < mc; i += blockDim.x) s[i] = sqrt(fmax(L[i], 0.0));
   __syncthreads();
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {  // stable descending rank
+  for (int i = threadIdx.x; i < mc; i += blockDim.x) {  // stable descending rank
     int rk = 0;
-    for (int k = 0; k < m; ++k) rk += (s[k] > s[i]) || (s[k] == s[i] && k < i);
+    for (int k = 0; k < mc; ++k) rk += (s[k] > s[i]) || (s[k] == s[i] && k < i);
     perm[rk] = i;
   }
   __syncthreads();
@@ -44,13 +47,14 @@ __global__ void k_select(const double* __restrict__ lam, const double* __restric
     const double smax = s[perm[0]];
     const double thr = tau_mode == RDD_TAU_RELATIVE ? tau * smax : tau;
     int k = 0;
-    for (int i = 0; i < nsv; ++i)
+    for (int i = 0; i < min(nsv, mc); ++i)
       if (s[perm[i]] > thr) ++k;
     keep = max(k, 1);
     p_out[j] = keep;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < m; i += blockDim.x) sig[static_cast<size_t>(j) * m + i] = i < nsv ? s[perm[i]] : 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x)
+    sig[static_cast<size_t>(j) * m + i] = (i < nsv && i < mc) ? s[perm[i]] : 0.0;
   // reorder columns; sign so that the first nonzero entry is >= 0 (reduction.hpp:100-107)
   const double* Vi = Vin + static_cast<size_t>(j) * m * m;
   double* Vo = Vout + static_cast<size_t>(j) * m * m;
@@ -167,7 +171,8 @@ __global__ void __launch_bounds__(kHouseThreads) k_house_complete(const double* 
                                                                   const double* __restrict__ lam,
                                                                   const long long* __restrict__ lam_off,
                                                                   const int* __restrict__ rr, int n,
-                                                                  double* __restrict__ A, double* __restrict__ Q) {
+                                                                  double* __restrict__ A, double* __restrict__ Q,
+                                                                  int thin) {
   extern __shared__ double hsm[];
   double* v = hsm;              // n: current Householder vector
   double* beta = v + n;         // r
@@ -220,7 +225,8 @@ __global__ void __launch_bounds__(kHouseThreads) k_house_complete(const double* 
     }
     __syncthreads();
   }
-  for (size_t e = tid; e < static_cast<size_t>(n) * n; e += blockDim.x) Qj[e] = (e % (n + 1) == 0) ? 1.0 : 0.0;
+  const int nq = thin ? r : n;  // thin: Q[:, :r] = H_0 ⋯ H_{r-1} [I_r; 0]
+  for (size_t e = tid; e < static_cast<size_t>(n) * nq; e += blockDim.x) Qj[e] = (e % (n + 1) == 0) ? 1.0 : 0.0;
   __syncthreads();
   for (int k = r - 1; k >= 0; --k) {
     const double* x = Aj + static_cast<size_t>(k) * n;
@@ -228,7 +234,7 @@ __global__ void __launch_bounds__(kHouseThreads) k_house_complete(const double* 
     __syncthreads();
     const double b = beta[k];
     if (b != 0.0)
-      for (int c = k + warp; c < n; c += nw) {
+      for (int c = k + warp; c < nq; c += nw) {
         double* y = Qj + static_cast<size_t>(c) * n;
         double w = 0.0;
         for (int i = k + lane; i < n; i += 32) w += v[i] * y[i];
@@ -349,88 +355,175 @@ void run_pca(Ctx& c) {
                          m, tm, tn, 0.0});
       gemm_nn(c, t);  // Vr = L U
     }
-    {
-      DBuf<long long> doffr;
-      doffr.upload(offr, c.stream);
-      const size_t sm = static_cast<size_t>(m) * (2 * sizeof(double) + sizeof(int)) + 16;
-      if (sm > 32 * 1024)
-        RDD_CUDA(cudaFuncSetAttribute(k_house_complete, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(sm)));
-      k_house_complete<<<J, kHouseThreads, sm, c.stream>>>(Vr.p, lam.p, doffr.p, dr.p, m, Hw.p, V0.p);
-      RDD_LAUNCH_CHECK();
-      RDD_CUDA(cudaStreamSynchronize(c.stream));
+    // path choice: the refined-subspace path below resolves every direction above ~1e-7·σmax;
+    // thresholds below that (or blocks whose numerical rank r < m with such a threshold) take the
+    // full two-stage path (stage 2 on all m columns)
+    std::vector<double> hl(static_cast<size_t>(offr[J - 1] + rj[J - 1]));
+    RDD_CUDA(cudaMemcpyAsync(hl.data(), lam.p, sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, c.stream));
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    bool fast = true;
+    for (int j = 0; j < J; ++j) {
+      double lmax = 0.0;
+      for (int q = 0; q < rj[j]; ++q) lmax = std::max(lmax, hl[offr[j] + q]);
+      const double smax = std::sqrt(lmax);
+      const double thr = rel ? c.cfg.tau * smax : c.cfg.tau;
+      if (!(rj[j] == m || thr >= 1e-7 * smax)) fast = false;
     }
-    // stage 2a: the graded Jacobi on the leading r columns only (T_a = S·V0[:, :r], one CTA per
-    // subdomain), V0[:, :r] <- V0[:, :r]·W_a. The full stage 2 below then mostly decouples them
-    // from the complement (measured: 7.1 -> ~5 sweeps of the 300-wide Jacobi)
+    DBuf<long long> doffr_sel;
+    doffr_sel.upload(offr, c.stream);
     T.p = c.ws("pca.T", std::max<long long>(1, c.S_off[J]));
     W.p = c.ws("pca.W", J * mm);
     Vfull.p = c.ws("pca.Vfull", J * mm);
-    {
-      std::vector<GemmTask> t;
-      for (int j = 0; j < J; ++j) {
-        const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
-        for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
-          for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
-            t.push_back({c.S.p + c.S_off[j], V0.p + offm[j], T.p + c.S_off[j], nullptr, nullptr, rows, rj[j], m,
-                         std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+    if (fast) {
+      // one subspace-iteration step from S itself: Y = Sᵀ(S·Vr). Directions with σ_i ≫ the Gram's
+      // rounding floor come out accurate to ~ε·σmax/σ_i (the Gram-based Vr only to ε·σmax²/σ_i²),
+      // so span(Y) holds the kept subspace to ~1e-10 and the graded Jacobi on (S·Q)ᵀ(S·Q) within it
+      // (relative criterion) gives σ and V to the parity tolerance — no m-wide second stage
+      {
+        std::vector<GemmTask> t;
+        for (int j = 0; j < J; ++j) {
+          const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+          for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
+            for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+              t.push_back({c.S.p + c.S_off[j], Vr.p + offm[j], T.p + c.S_off[j], nullptr, nullptr, rows, rj[j], m,
+                           std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+        }
+        gemm_nn(c, t);  // Z = S·Vr
       }
-      gemm_nn(c, t);  // T_a
-    }
-    {
-      std::vector<GemmTask> t;
-      for (int j = 0; j < J; ++j) {
-        const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
-        const int nt = ceil_div(rj[j], 64);
-        for (int tm = 0; tm < nt; ++tm)
-          for (int tn = tm; tn < nt; ++tn)
-            t.push_back({T.p + c.S_off[j], T.p + c.S_off[j], G.p + offm[j], nullptr, nullptr, rj[j], rj[j], rows,
-                         std::max(rows, 1), std::max(rows, 1), rj[j], tm, tn, 0.0});
+      {
+        std::vector<GemmTask> t;
+        for (int j = 0; j < J; ++j) {
+          const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+          for (int tm = 0; tm < ceil_div(m, 64); ++tm)
+            for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+              t.push_back({c.S.p + c.S_off[j], T.p + c.S_off[j], Hw.p + offm[j], nullptr, nullptr, m, rj[j], rows,
+                           std::max(rows, 1), std::max(rows, 1), m, tm, tn, 0.0});
+        }
+        gemm_tn(c, t);  // Y = Sᵀ·Z
       }
-      gemm_tn(c, t);  // G_a = T_aᵀ T_a
-    }
-    batched_syevj(c, G.p, W.p, lam.p, rj, offm, s2);
-    {
-      std::vector<GemmTask> t;
-      for (int j = 0; j < J; ++j)
-        for (int tm = 0; tm < ceil_div(m, 64); ++tm)
-          for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
-            t.push_back({V0.p + offm[j], W.p + offm[j], Vfull.p + offm[j], nullptr, nullptr, m, rj[j], rj[j], m, rj[j],
-                         m, tm, tn, 0.0});
-      gemm_nn(c, t);  // V0[:, :r] W_a
-      k_copy_lead<<<J, 256, 0, c.stream>>>(Vfull.p, V0.p, dr.p, m);
-      RDD_LAUNCH_CHECK();
-    }
-    // stage 2: T = S V0, G1 = TᵀT, Jacobi on the graded G1
-    {
-      std::vector<GemmTask> t;
-      for (int j = 0; j < J; ++j) {
-        const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
-        for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
-          for (int tn = 0; tn < ceil_div(m, 64); ++tn)
-            t.push_back({c.S.p + c.S_off[j], V0.p + offm[j], T.p + c.S_off[j], nullptr, nullptr, rows, m, m,
-                         std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+      {
+        const size_t sm = static_cast<size_t>(m) * (2 * sizeof(double) + sizeof(int)) + 16;
+        if (sm > 32 * 1024)
+          RDD_CUDA(cudaFuncSetAttribute(k_house_complete, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sm)));
+        k_house_complete<<<J, kHouseThreads, sm, c.stream>>>(Hw.p, lam.p, doffr_sel.p, dr.p, m, Lw.p, V0.p, 1);
+        RDD_LAUNCH_CHECK();  // V0[:, :r] = orthonormal basis of span(Y), columns in stage-1 order
       }
-      gemm_nn(c, t);
-    }
-    gemm_tn(c, gram_tasks(c, T.p, G.p, c.S_off));
-    batched_syevj(c, G.p, W.p, lam.p, ns, offm, s2);
-    // V = V0 W
-    {
-      std::vector<GemmTask> t;
-      for (int j = 0; j < J; ++j)
-        for (int tm = 0; tm < ceil_div(m, 64); ++tm)
-          for (int tn = 0; tn < ceil_div(m, 64); ++tn)
-            t.push_back({V0.p + offm[j], W.p + offm[j], Vfull.p + offm[j], nullptr, nullptr, m, m, m, m, m, m, tm, tn,
-                         0.0});
-      gemm_nn(c, t);
+      {
+        std::vector<GemmTask> t;
+        for (int j = 0; j < J; ++j) {
+          const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+          for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
+            for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+              t.push_back({c.S.p + c.S_off[j], V0.p + offm[j], T.p + c.S_off[j], nullptr, nullptr, rows, rj[j], m,
+                           std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+        }
+        gemm_nn(c, t);  // T_a = S·Q
+      }
+      {
+        std::vector<GemmTask> t;
+        for (int j = 0; j < J; ++j) {
+          const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+          const int nt = ceil_div(rj[j], 64);
+          for (int tm = 0; tm < nt; ++tm)
+            for (int tn = tm; tn < nt; ++tn)
+              t.push_back({T.p + c.S_off[j], T.p + c.S_off[j], G.p + offm[j], nullptr, nullptr, rj[j], rj[j], rows,
+                           std::max(rows, 1), std::max(rows, 1), rj[j], tm, tn, 0.0});
+        }
+        gemm_tn(c, t);  // G_a = T_aᵀ T_a
+      }
+      batched_syevj(c, G.p, W.p, lam.p, rj, offm, s2);
+      {
+        std::vector<GemmTask> t;
+        for (int j = 0; j < J; ++j)
+          for (int tm = 0; tm < ceil_div(m, 64); ++tm)
+            for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+              t.push_back({V0.p + offm[j], W.p + offm[j], Vfull.p + offm[j], nullptr, nullptr, m, rj[j], rj[j], m,
+                           rj[j], m, tm, tn, 0.0});
+        gemm_nn(c, t);  // V = Q W
+      }
+    } else {
+      {
+        DBuf<long long> doffr;
+        doffr.upload(offr, c.stream);
+        const size_t sm = static_cast<size_t>(m) * (2 * sizeof(double) + sizeof(int)) + 16;
+        if (sm > 32 * 1024)
+          RDD_CUDA(cudaFuncSetAttribute(k_house_complete, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sm)));
+        k_house_complete<<<J, kHouseThreads, sm, c.stream>>>(Vr.p, lam.p, doffr.p, dr.p, m, Hw.p, V0.p, 0);
+        RDD_LAUNCH_CHECK();
+        RDD_CUDA(cudaStreamSynchronize(c.stream));
+      }
+      // stage 2a: the graded Jacobi on the leading r columns only (T_a = S·V0[:, :r], one CTA per
+      // subdomain), V0[:, :r] <- V0[:, :r]·W_a. The full stage 2 below then mostly decouples them
+      // from the complement (measured: 7.1 -> ~5 sweeps of the 300-wide Jacobi)
+      {
+        std::vector<GemmTask> t;
+        for (int j = 0; j < J; ++j) {
+          const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+          for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
+            for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+              t.push_back({c.S.p + c.S_off[j], V0.p + offm[j], T.p + c.S_off[j], nullptr, nullptr, rows, rj[j], m,
+                           std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+        }
+        gemm_nn(c, t);  // T_a
+      }
+      {
+        std::vector<GemmTask> t;
+        for (int j = 0; j < J; ++j) {
+          const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+          const int nt = ceil_div(rj[j], 64);
+          for (int tm = 0; tm < nt; ++tm)
+            for (int tn = tm; tn < nt; ++tn)
+              t.push_back({T.p + c.S_off[j], T.p + c.S_off[j], G.p + offm[j], nullptr, nullptr, rj[j], rj[j], rows,
+                           std::max(rows, 1), std::max(rows, 1), rj[j], tm, tn, 0.0});
+        }
+        gemm_tn(c, t);  // G_a = T_aᵀ T_a
+      }
+      batched_syevj(c, G.p, W.p, lam.p, rj, offm, s2);
+      {
+        std::vector<GemmTask> t;
+        for (int j = 0; j < J; ++j)
+          for (int tm = 0; tm < ceil_div(m, 64); ++tm)
+            for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+              t.push_back({V0.p + offm[j], W.p + offm[j], Vfull.p + offm[j], nullptr, nullptr, m, rj[j], rj[j], m, rj[j],
+                           m, tm, tn, 0.0});
+        gemm_nn(c, t);  // V0[:, :r] W_a
+        k_copy_lead<<<J, 256, 0, c.stream>>>(Vfull.p, V0.p, dr.p, m);
+        RDD_LAUNCH_CHECK();
+      }
+      // stage 2: T = S V0, G1 = TᵀT, Jacobi on the graded G1
+      {
+        std::vector<GemmTask> t;
+        for (int j = 0; j < J; ++j) {
+          const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+          for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
+            for (int tn = 0; tn < ceil_div(m, 64); ++tn)
+              t.push_back({c.S.p + c.S_off[j], V0.p + offm[j], T.p + c.S_off[j], nullptr, nullptr, rows, m, m,
+                           std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+        }
+        gemm_nn(c, t);
+      }
+      gemm_tn(c, gram_tasks(c, T.p, G.p, c.S_off));
+      batched_syevj(c, G.p, W.p, lam.p, ns, offm, s2);
+      // V = V0 W
+      {
+        std::vector<GemmTask> t;
+        for (int j = 0; j < J; ++j)
+          for (int tm = 0; tm < ceil_div(m, 64); ++tm)
+            for (int tn = 0; tn < ceil_div(m, 64); ++tn)
+              t.push_back({V0.p + offm[j], W.p + offm[j], Vfull.p + offm[j], nullptr, nullptr, m, m, m, m, m, m, tm, tn,
+                           0.0});
+        gemm_nn(c, t);
+      }
     }
     c.Vred.ensure(J * mm);
     c.sigma.ensure(static_cast<size_t>(J) * m);
     c.dp_j.ensure(J);
     const size_t smem = static_cast<size_t>(m) * (sizeof(double) + sizeof(int));
     k_select<<<J, 256, smem, c.stream>>>(lam.p, Vfull.p, c.Vred.p, c.sigma.p, c.dp_j.p, c.row_ptr.p, m,
-                                         c.cfg.tau_mode, c.cfg.tau);
+                                         c.cfg.tau_mode, c.cfg.tau, fast ? dr.p : nullptr,
+                                         fast ? doffr_sel.p : nullptr);
     RDD_LAUNCH_CHECK();
     c.dp_j.download(c.h_p.data(), J, c.stream);
     RDD_CUDA(cudaStreamSynchronize(c.stream));

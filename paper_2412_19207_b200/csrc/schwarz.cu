@@ -12,6 +12,7 @@
 // reference's serial scatter, without atomics. apply_transpose (schwarz.hpp:189-215) moves the
 // SAS/RAS weights in front of the local solve.
 #include <algorithm>
+#include <cstdio>
 
 #include "ctx.hpp"
 
@@ -19,25 +20,43 @@ namespace rdd {
 
 namespace {
 
-// gather A_i from normal blocks: one CTA per (i, part-pair)
+// gather A_i from normal blocks: one CTA per (i, part-pair). Blocks stored transposed (j1 > j2:
+// NB holds H_j2ᵀH_j1) go through 32x33 shared-memory tiles so both the read and the write coalesce.
 __global__ void k_gather_local(const double* __restrict__ NB, const int* __restrict__ task_i,
                                const int* __restrict__ task_j1, const int* __restrict__ task_j2,
                                const int* __restrict__ task_o1, const int* __restrict__ task_o2,
                                const long long* __restrict__ task_nb, const int* __restrict__ col_off,
                                const int* __restrict__ nvec, const long long* __restrict__ A_off,
                                double* __restrict__ A) {
+  __shared__ double tile[32][33];
   const int t = blockIdx.x;
   const int i = task_i[t], j1 = task_j1[t], j2 = task_j2[t], o1 = task_o1[t], o2 = task_o2[t];
   const long long nb = task_nb[t];
   const int n = nvec[i];
   const int p1 = col_off[j1 + 1] - col_off[j1], p2 = col_off[j2 + 1] - col_off[j2];
   double* Ai = A + A_off[i];
-  for (int e = threadIdx.x; e < p1 * p2; e += blockDim.x) {
-    const int r = e % p1, cc = e / p1;
-    double v = 0.0;
-    if (nb >= 0) v = (j1 <= j2) ? NB[nb + r + static_cast<long long>(cc) * p1] : NB[nb + cc + static_cast<long long>(r) * p2];
-    Ai[(o1 + r) + static_cast<long long>(o2 + cc) * n] = v;
+  if (j1 <= j2 || nb < 0) {  // stored as (p1 x p2) column-major, or absent (zeros)
+    for (int e = threadIdx.x; e < p1 * p2; e += blockDim.x) {
+      const int r = e % p1, cc = e / p1;
+      Ai[(o1 + r) + static_cast<long long>(o2 + cc) * n] = nb >= 0 ? NB[nb + r + static_cast<long long>(cc) * p1] : 0.0;
+    }
+    return;
   }
+  // element (r, cc) of block (j1, j2) = NB[nb + cc + r·p2] (the (p2 x p1) block of (j2, j1))
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
+  for (int r0 = 0; r0 < p1; r0 += 32)
+    for (int c0 = 0; c0 < p2; c0 += 32) {
+      for (int y = ty; y < 32; y += ny) {  // read: rows r0+y of the target = columns of the source
+        const int r = r0 + y, cc = c0 + tx;
+        tile[y][tx] = (r < p1 && cc < p2) ? NB[nb + cc + static_cast<long long>(r) * p2] : 0.0;
+      }
+      __syncthreads();
+      for (int y = ty; y < 32; y += ny) {  // write: column c0+y of the target, rows r0..r0+31
+        const int cc = c0 + y, r = r0 + tx;
+        if (r < p1 && cc < p2) Ai[(o1 + r) + static_cast<long long>(o2 + cc) * n] = tile[tx][y];
+      }
+      __syncthreads();
+    }
 }
 
 // per i: keep λ > 1e-12·max(0, λmax) (schwarz.hpp:133-139); X = V diag(1/λ_kept); rank, cond
@@ -124,7 +143,8 @@ void release_scratch(Ctx& c) {
 }
 
 // Gather A_i for the subdomains in `which` into a compact batch at offsets `off` (zero-filled).
-void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, const std::vector<long long>& off) {
+void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, const std::vector<long long>& off,
+                   bool lower_only) {
   long long tot = 0;
   std::vector<int> slot(c.J, -1), nn(which.size());
   for (size_t q = 0; q < which.size(); ++q) {
@@ -132,11 +152,17 @@ void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, con
     nn[q] = c.local_n[which[q]];
     tot = std::max(tot, off[q] + static_cast<long long>(nn[q]) * nn[q]);
   }
+  const double h0 = now_s();
   out.zero(std::max<long long>(1, tot), c.stream);
+  if (c.verbose) {
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    std::fprintf(stderr, "[gather] zero %.1f GB %.3f s\n", tot * 8e-9, now_s() - h0);
+  }
   std::vector<int> ti, tj1, tj2, to1, to2;
   std::vector<long long> tnb;
   for (const auto& t : c.gat_tasks) {
     if (slot[t.i] < 0) continue;
+    if (lower_only && t.o1 < t.o2) continue;  // block entirely above the diagonal
     ti.push_back(slot[t.i]);
     tj1.push_back(t.j1);
     tj2.push_back(t.j2);
@@ -158,6 +184,10 @@ void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, con
   k_gather_local<<<static_cast<int>(ti.size()), 256, 0, c.stream>>>(c.NB.p, dti.p, dtj1.p, dtj2.p, dto1.p, dto2.p,
                                                                    dtnb.p, c.dcol_off.p, dn.p, doff.p, out.p);
   RDD_LAUNCH_CHECK();
+  if (c.verbose) {
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    std::fprintf(stderr, "[gather] %zu tasks, total %.3f s\n", ti.size(), now_s() - h0);
+  }
 }
 
 // local_cond as the reference reports it (λmax/λmin of the kept spectrum): power iterations on
@@ -256,10 +286,19 @@ void build_schwarz(Ctx& c, int kind) {
   c.dP_off.upload(c.P_off, c.stream);
   c.fb_store.clear();
   const size_t p_bytes = static_cast<size_t>(c.P_off[J]) * sizeof(double);
-  if (device_available(c) < p_bytes + (size_t(8) << 30)) release_scratch(c);
-  c.P.ensure(std::max<long long>(1, c.P_off[J]));
-  const size_t budget =
-      std::min<size_t>(size_t(48) << 30, std::max<size_t>(size_t(1) << 30, (device_available(c) * 3) / 5));
+  {
+    ScopedKernelTimer ta(c, "schwarz_alloc");
+    if (device_available(c) < p_bytes + (size_t(8) << 30)) release_scratch(c);
+    c.P.ensure(std::max<long long>(1, c.P_off[J]));
+  }
+  // chunk budget for the gathered A_i: fixed at the first build of this context, so reruns reuse the
+  // same chunking and the workspace never has to grow (growing a pooled buffer maps new pages: ~2 s
+  // for 50 GB)
+  if (c.schwarz_budget == 0)
+    c.schwarz_budget =
+        std::min<size_t>(size_t(40) << 30, std::max<size_t>(size_t(1) << 30, (device_available(c) * 3) / 5));
+  c.schwarz_budget = std::min(c.schwarz_budget, std::max<size_t>(size_t(1) << 30, (device_available(c) * 3) / 5));
+  const size_t budget = c.schwarz_budget;
   c.local_rank.assign(J, 0);
   c.local_cond.assign(J, 0.0);
   c.local_cond_exact = false;
@@ -282,7 +321,10 @@ void build_schwarz(Ctx& c, int kind) {
     i0 = i;
     const int B = static_cast<int>(chunk.size());
     DBuf<double>& Aw = c.wsd["schwarz.A"];
-    gather_locals(c, chunk, Aw, coff);
+    {
+      ScopedKernelTimer tg(c, "schwarz_gather");
+      gather_locals(c, chunk, Aw, coff, true);  // the factorisation reads the lower triangle
+    }
     std::vector<int> fail;
     std::vector<double> fa;
     batched_cholesky_pack(c, Aw.p, cn, coff, c.P.p, cpoff, fail, fa);

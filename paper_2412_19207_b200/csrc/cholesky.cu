@@ -103,15 +103,18 @@ __global__ void k_pack_row(const double* __restrict__ A, const Mat* __restrict__
   for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) o[e] = d[e];
 }
 
-// ‖A‖_F of a symmetric matrix from its lower triangle (the upper one may hold garbage)
-__global__ void k_frob(const double* __restrict__ A, const Mat* __restrict__ mats, double* __restrict__ out) {
-  const Mat M = mats[blockIdx.x];
+// ‖A‖_F of a symmetric matrix from its lower triangle (the upper one may hold garbage): kFrobParts
+// CTAs per matrix stream column ranges (coalesced), partials summed per matrix in a fixed order
+constexpr int kFrobParts = 64;
+__global__ void k_frob_part(const double* __restrict__ A, const Mat* __restrict__ mats, double* __restrict__ part) {
+  const Mat M = mats[blockIdx.y];
   double s = 0.0;
-  for (long long e = threadIdx.x; e < static_cast<long long>(M.n) * M.n; e += blockDim.x) {
-    const int r = static_cast<int>(e % M.n), cc = static_cast<int>(e / M.n);
-    if (r < cc) continue;
-    const double v = A[M.off + e];
-    s += (r == cc ? 1.0 : 2.0) * v * v;
+  for (int cc = blockIdx.x; cc < M.n; cc += gridDim.x) {
+    const double* col = A + M.off + static_cast<long long>(cc) * M.n;
+    for (int r = cc + threadIdx.x; r < M.n; r += blockDim.x) {
+      const double v = col[r];
+      s += (r == cc ? 1.0 : 2.0) * v * v;
+    }
   }
   __shared__ double sh[32];
   s = warp_sum(s);
@@ -120,8 +123,15 @@ __global__ void k_frob(const double* __restrict__ A, const Mat* __restrict__ mat
   if (threadIdx.x < 32) {
     s = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
     s = warp_sum(s);
-    if (threadIdx.x == 0) out[blockIdx.x] = sqrt(s);
+    if (threadIdx.x == 0) part[blockIdx.y * kFrobParts + blockIdx.x] = s;
   }
+}
+__global__ void k_frob_sum(const double* __restrict__ part, int B, double* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double s = 0.0;
+  for (int x = 0; x < kFrobParts; ++x) s += part[b * kFrobParts + x];
+  out[b] = sqrt(s);
 }
 
 // λmax of symmetric PSD matrices by power iteration (one CTA per matrix, x in shared memory)
@@ -423,8 +433,14 @@ void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const s
   dm.upload(mats, c.stream);
   dfail.zero(B, c.stream);
   dfa.ensure(B);
-  k_frob<<<B, 256, 0, c.stream>>>(A, dm.p, dfa.p);
-  RDD_LAUNCH_CHECK();
+  {
+    DBuf<double> fpart;
+    fpart.ensure(static_cast<size_t>(B) * kFrobParts);
+    k_frob_part<<<dim3(kFrobParts, B), 256, 0, c.stream>>>(A, dm.p, fpart.p);
+    RDD_LAUNCH_CHECK();
+    k_frob_sum<<<ceil_div(B, 128), 128, 0, c.stream>>>(fpart.p, B, dfa.p);
+    RDD_LAUNCH_CHECK();
+  }
   std::vector<long long> doff(B);
   long long dtot = 0;
   for (int i = 0; i < B; ++i) {

@@ -106,8 +106,8 @@ static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed, bool reside
   const double t_asm = now_s() - t0;
   if (c.verbose) std::fprintf(stderr, "[phase] assemble done %.3f s\n", t_asm);
   double t_pre = 0.0;
-  if (cfg.solver == RDD_SOLVER_QR) throw std::invalid_argument("qr_direct is a host baseline (oracle), not a device path");
-  if (cfg.precond >= 0) {
+  if (cfg.solver == RDD_SOLVER_QR) {  // runner.hpp:217-222: no preconditioner, no Krylov
+  } else if (cfg.precond >= 0) {
     t0 = now_s();
     build_normal_blocks(c);
     build_schwarz(c, cfg.precond);
@@ -118,7 +118,8 @@ static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed, bool reside
     build_normal_blocks(c);
   }
   t0 = now_s();
-  solve_all(c, cfg.solver, cfg.rel_tol, cfg.max_iter, cfg.gmres_restart);
+  if (cfg.solver == RDD_SOLVER_QR) qr_solve_dev(c);
+  else solve_all(c, cfg.solver, cfg.rel_tol, cfg.max_iter, cfg.gmres_restart);
   const double t_sol = now_s() - t0;
   if (c.verbose) std::fprintf(stderr, "[phase] solve %.3f s (%d its)\n", t_sol, c.iters.empty() ? 0 : c.iters[0]);
   t0 = now_s();
@@ -259,7 +260,8 @@ int rdd_build_preconditioner(rdd_ctx* h, int kind) {
 int rdd_solve(rdd_ctx* h, int solver, double rel_tol, int max_iter, int gmres_restart) {
   return guarded(h, [&](Ctx& c) {
     need_assembled(c);
-    rdd::solve_all(c, solver, rel_tol, max_iter, gmres_restart);
+    if (solver == RDD_SOLVER_QR) rdd::qr_solve_dev(c);
+    else rdd::solve_all(c, solver, rel_tol, max_iter, gmres_restart);
   });
 }
 int rdd_evaluate(rdd_ctx* h, const int* test_res) {
@@ -373,6 +375,7 @@ int64_t rdd_get_i(rdd_ctx* h, const char* what, int index, int32_t* out, int64_t
     else if (w == "C") v = {c.C};
     else if (w == "maxcov") v = {c.maxcov};
     else if (w == "n_fallback") v = {c.n_fallback};
+    else if (w == "qr_rank") v = {c.qr_rank};
     else if (w == "p_j") v = c.h_p;
     else if (w == "col_off") v = c.h_col_off;
     else if (w == "rows") {

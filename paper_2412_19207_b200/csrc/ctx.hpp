@@ -134,7 +134,8 @@ struct Ctx {
   int nmax_local = 0;
   int n_fallback = 0;                 // local blocks that took the eigen pseudo-inverse
   std::vector<int> fallback, local_n;
-  size_t schwarz_budget = 0;          // bytes of gathered A_i per chunk (fixed per context)
+  size_t schwarz_budget = 0;
+  int qr_rank = 0;                    // numerical rank of the dense QR path          // bytes of gathered A_i per chunk (fixed per context)
   std::map<int, DBuf<double>> fb_store;  // eigen-fallback subdomains: dense pseudo-inverse
   DBuf<double*> dfb_ptr;              // per i: dense pseudo-inverse or nullptr (factor path)
   bool local_cond_exact = false;
@@ -245,6 +246,7 @@ void refresh_local_cond(Ctx& c);
 size_t device_available(Ctx& c);
 void release_scratch(Ctx& c);
 // krylov.cu (K12/K13)
+void qr_solve_dev(Ctx& c);
 void solve_all(Ctx& c, int solver, double tol, int max_iter, int restart);
 // evaluate.cu (K14)
 void evaluate(Ctx& c, const int* test_res);

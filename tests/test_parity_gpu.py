@@ -197,3 +197,33 @@ def test_cgs_bicg(dev, orc, name):
     np.testing.assert_allclose(hd[:k][keep], ho[:k][keep], rtol=1e-6)
     tol = max(1e-6, 100 * cfg.rel_tol)
     assert sd["e_l2"] == pytest.approx(so["e_l2"], rel=tol), (name, sd["e_l2"], so["e_l2"])
+
+
+# dense column-pivoted QR least squares (krylov.hpp:97-101, runner.hpp:217-222)
+def _qr_cases():
+    out = {}
+    cfg = configs.golden_runner(77)
+    cfg.solver, cfg.precond = A.SOLVER_QR, A.PRECOND_NONE
+    out["runner77_qr"] = cfg
+    sc = configs.golden_scaling(A.PRECOND_NONE)
+    sc.solver = A.SOLVER_QR
+    out["scaling_qr"] = sc
+    c5 = configs.scaled(configs.c5(), [2, 2, 2], 6, m=40)
+    c5.solver, c5.precond = A.SOLVER_QR, A.PRECOND_NONE
+    out["c5s_slice_qr"] = c5
+    return out
+
+
+QRC = _qr_cases()
+
+
+@pytest.mark.parametrize("name", list(QRC))
+def test_qr_direct(dev, orc, name):
+    cfg = QRC[name]
+    so = orc.run_single(cfg)
+    sd = dev.run_single(cfg)
+    assert sd["converged"] == 1 and sd["iterations"] == 0
+    assert sd["DoF"] == so["DoF"]
+    assert sd["e_l2"] == pytest.approx(so["e_l2"], rel=1e-6), (name, sd["e_l2"], so["e_l2"])
+    wd, wo = dev.getd("W", 0), orc.getd("W", 0)
+    assert np.linalg.norm(wd - wo) <= 1e-6 * np.linalg.norm(wo), name

@@ -78,7 +78,8 @@ __global__ void k_select(const double* __restrict__ lam, const double* __restric
 // numerical rank of G. L's columns are graded, which is what makes the Jacobi on LᵀL short.
 constexpr int kPcholThreads = 512;
 __global__ void __launch_bounds__(kPcholThreads) k_pchol(const double* __restrict__ G, double* __restrict__ L, int n,
-                                                          double stop, int* __restrict__ r_out) {
+                                                          double stop, int* __restrict__ r_out,
+                                                          double* __restrict__ trace_out) {
   extern __shared__ double psm[];
   double* d = psm;                                             // n: remaining diagonal
   double* li = d + n;                                          // n: L[i, :k]
@@ -159,7 +160,12 @@ __global__ void __launch_bounds__(kPcholThreads) k_pchol(const double* __restric
     for (int row = tid; row < n; row += blockDim.x) Lj[row] = 0.0;
     r = 1;
   }
-  if (tid == 0) r_out[j] = r;
+  if (tid == 0) {
+    r_out[j] = r;
+    double tr = 0.0;
+    for (int i = 0; i < n; ++i) tr += Gj[i + static_cast<size_t>(i) * n];
+    trace_out[j] = tr;
+  }
 }
 
 // V0 = [orth(Vr), complement]: columns of Vr (n x r, eigenvectors of LLᵀ up to scale) sorted by
@@ -321,17 +327,33 @@ void run_pca(Ctx& c) {
     }
     WS Lw{c.ws("pca.L", J * mm)}, Vr{c.ws("pca.Vr", J * mm)}, Hw{c.ws("pca.H", J * mm)};
     DBuf<int> dr;
+    DBuf<double> dtrace;
     dr.ensure(J);
+    dtrace.ensure(J);
     {
       const size_t sm = static_cast<size_t>(m) * (2 * sizeof(double) + 1) + 16;
       if (sm > 32 * 1024)
         RDD_CUDA(cudaFuncSetAttribute(k_pchol, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-      k_pchol<<<J, kPcholThreads, sm, c.stream>>>(G.p, Lw.p, m, 1e-17, dr.p);
+      k_pchol<<<J, kPcholThreads, sm, c.stream>>>(G.p, Lw.p, m, 1e-17, dr.p, dtrace.p);
       RDD_LAUNCH_CHECK();
     }
     std::vector<int> rj(J);
+    std::vector<double> htrace(J);
     dr.download(rj.data(), J, c.stream);
+    dtrace.download(htrace.data(), J, c.stream);
     RDD_CUDA(cudaStreamSynchronize(c.stream));
+    // path choice: the refined-subspace path resolves every direction above ~1e-7·σmax (σmax² <=
+    // trace G); thresholds below that with r < m take the full two-stage path (stage 2 on all m
+    // columns). Wide blocks (cluster-sized r) skip the stage-1 Jacobi and refine twice instead.
+    bool fast = true;
+    int rmax = 0;
+    for (int j = 0; j < J; ++j) {
+      rmax = std::max(rmax, rj[j]);
+      const bool ok = rel ? c.cfg.tau >= 1e-7 : c.cfg.tau >= 1e-7 * std::sqrt(std::max(htrace[j], 0.0));
+      if (!(rj[j] == m || ok)) fast = false;
+    }
+    const bool skip_s1 = fast && rmax > 223;
+    const int nref = skip_s1 ? 2 : 1;
     {
       std::vector<GemmTask> t;
       for (int j = 0; j < J; ++j) {
@@ -345,8 +367,8 @@ void run_pca(Ctx& c) {
     }
     std::vector<long long> offr(J);
     for (int j = 0, e = 0; j < J; e += rj[j], ++j) offr[j] = e;
-    batched_syevj(c, G.p, V0.p, lam.p, rj, offm, s1);  // U (r x r, ld r) in V0's buffer
-    {
+    if (!skip_s1) {
+      batched_syevj(c, G.p, V0.p, lam.p, rj, offm, s1);  // U (r x r, ld r) in V0's buffer
       std::vector<GemmTask> t;
       for (int j = 0; j < J; ++j)
         for (int tm = 0; tm < ceil_div(m, 64); ++tm)
@@ -355,20 +377,12 @@ void run_pca(Ctx& c) {
                          m, tm, tn, 0.0});
       gemm_nn(c, t);  // Vr = L U
     }
-    // path choice: the refined-subspace path below resolves every direction above ~1e-7·σmax;
-    // thresholds below that (or blocks whose numerical rank r < m with such a threshold) take the
-    // full two-stage path (stage 2 on all m columns)
-    std::vector<double> hl(static_cast<size_t>(offr[J - 1] + rj[J - 1]));
-    RDD_CUDA(cudaMemcpyAsync(hl.data(), lam.p, sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, c.stream));
-    RDD_CUDA(cudaStreamSynchronize(c.stream));
-    bool fast = true;
-    for (int j = 0; j < J; ++j) {
-      double lmax = 0.0;
-      for (int q = 0; q < rj[j]; ++q) lmax = std::max(lmax, hl[offr[j] + q]);
-      const double smax = std::sqrt(lmax);
-      const double thr = rel ? c.cfg.tau * smax : c.cfg.tau;
-      if (!(rj[j] == m || thr >= 1e-7 * smax)) fast = false;
-    }
+    // column order for the QR of the refinement: stage-1 eigenvalues, or the pivot order of L
+    std::vector<double> horder(static_cast<size_t>(offr[J - 1] + rj[J - 1]));
+    for (int j = 0; j < J; ++j)
+      for (int q = 0; q < rj[j]; ++q) horder[offr[j] + q] = -static_cast<double>(q);
+    double* dorder = c.ws("pca.order", std::max<size_t>(1, horder.size()));
+    RDD_CUDA(cudaMemcpyAsync(dorder, horder.data(), sizeof(double) * horder.size(), cudaMemcpyHostToDevice, c.stream));
     DBuf<long long> doffr_sel;
     doffr_sel.upload(offr, c.stream);
     T.p = c.ws("pca.T", std::max<long long>(1, c.S_off[J]));
@@ -379,35 +393,38 @@ void run_pca(Ctx& c) {
       // rounding floor come out accurate to ~ε·σmax/σ_i (the Gram-based Vr only to ε·σmax²/σ_i²),
       // so span(Y) holds the kept subspace to ~1e-10 and the graded Jacobi on (S·Q)ᵀ(S·Q) within it
       // (relative criterion) gives σ and V to the parity tolerance — no m-wide second stage
-      {
-        std::vector<GemmTask> t;
-        for (int j = 0; j < J; ++j) {
-          const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
-          for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
-            for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
-              t.push_back({c.S.p + c.S_off[j], Vr.p + offm[j], T.p + c.S_off[j], nullptr, nullptr, rows, rj[j], m,
-                           std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+      for (int it = 0; it < nref; ++it) {
+        const double* Vin = it == 0 ? (skip_s1 ? Lw.p : Vr.p) : V0.p;
+        {
+          std::vector<GemmTask> t;
+          for (int j = 0; j < J; ++j) {
+            const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+            for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
+              for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+                t.push_back({c.S.p + c.S_off[j], Vin + offm[j], T.p + c.S_off[j], nullptr, nullptr, rows, rj[j], m,
+                             std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+          }
+          gemm_nn(c, t);  // Z = S·V
         }
-        gemm_nn(c, t);  // Z = S·Vr
-      }
-      {
-        std::vector<GemmTask> t;
-        for (int j = 0; j < J; ++j) {
-          const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
-          for (int tm = 0; tm < ceil_div(m, 64); ++tm)
-            for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
-              t.push_back({c.S.p + c.S_off[j], T.p + c.S_off[j], Hw.p + offm[j], nullptr, nullptr, m, rj[j], rows,
-                           std::max(rows, 1), std::max(rows, 1), m, tm, tn, 0.0});
+        {
+          std::vector<GemmTask> t;
+          for (int j = 0; j < J; ++j) {
+            const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
+            for (int tm = 0; tm < ceil_div(m, 64); ++tm)
+              for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+                t.push_back({c.S.p + c.S_off[j], T.p + c.S_off[j], Hw.p + offm[j], nullptr, nullptr, m, rj[j], rows,
+                             std::max(rows, 1), std::max(rows, 1), m, tm, tn, 0.0});
+          }
+          gemm_tn(c, t);  // Y = Sᵀ·Z
         }
-        gemm_tn(c, t);  // Y = Sᵀ·Z
-      }
-      {
         const size_t sm = static_cast<size_t>(m) * (2 * sizeof(double) + sizeof(int)) + 16;
         if (sm > 32 * 1024)
           RDD_CUDA(cudaFuncSetAttribute(k_house_complete, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(sm)));
-        k_house_complete<<<J, kHouseThreads, sm, c.stream>>>(Hw.p, lam.p, doffr_sel.p, dr.p, m, Lw.p, V0.p, 1);
-        RDD_LAUNCH_CHECK();  // V0[:, :r] = orthonormal basis of span(Y), columns in stage-1 order
+        const double* ord = (it == 0 && !skip_s1) ? lam.p : dorder;
+        k_house_complete<<<J, kHouseThreads, sm, c.stream>>>(Hw.p, ord, doffr_sel.p, dr.p, m, Lw.p == Vin ? Vr.p : Lw.p,
+                                                             V0.p, 1);
+        RDD_LAUNCH_CHECK();  // V0[:, :r] = orthonormal basis of span(Y)
       }
       {
         std::vector<GemmTask> t;

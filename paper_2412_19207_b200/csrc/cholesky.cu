@@ -103,6 +103,39 @@ __global__ void k_pack_row(const double* __restrict__ A, const Mat* __restrict__
   for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) o[e] = d[e];
 }
 
+// Mi[k-block, k-block] = D_k (task = (matrix, k)), for M = L⁻¹ by block rows
+__global__ void k_set_diag(double* __restrict__ Mi, const Mat* __restrict__ mats, const int2* __restrict__ tasks,
+                           const double* __restrict__ Dinv, const long long* __restrict__ doff) {
+  const int2 t = tasks[blockIdx.x];
+  const Mat M = mats[t.x];
+  const int k0 = t.y * NB, bs = min(NB, M.n - k0);
+  const double* d = Dinv + doff[t.x] + static_cast<long long>(t.y) * NB * NB;
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e % NB, cc = e / NB;
+    if (r < bs && cc < bs) Mi[M.off + (k0 + r) + static_cast<long long>(k0 + cc) * M.n] = d[e];
+  }
+}
+// block row k of the packed lower tiles of a full symmetric matrix (lower triangle valid)
+__global__ void k_pack_lower(const double* __restrict__ F, const Mat* __restrict__ mats, const int2* __restrict__ tasks,
+                             double* __restrict__ P, const long long* __restrict__ poff) {
+  const int2 t = tasks[blockIdx.x];
+  const Mat M = mats[t.x];
+  const int k = t.y, k0 = k * NB, bs = min(NB, M.n - k0);
+  double* row = P + poff[t.x] + static_cast<long long>(k) * (k + 1) / 2 * (NB * NB);
+  for (int j = 0; j <= k; ++j) {
+    const double* a = F + M.off + k0 + static_cast<long long>(j * NB) * M.n;
+    const int bj = min(NB, M.n - j * NB);
+    double* o = row + static_cast<long long>(j) * NB * NB;
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+      const int r = e % NB, c = e / NB;
+      double v = 0.0;
+      if (r < bs && c < bj) v = (j < k || r >= c) ? a[r + static_cast<long long>(c) * M.n]
+                                                  : a[c + static_cast<long long>(r) * M.n];  // diag tile: mirror
+      o[e] = v;
+    }
+  }
+}
+
 // ‖A‖_F of a symmetric matrix from its lower triangle (the upper one may hold garbage): kFrobParts
 // CTAs per matrix stream column ranges (coalesced), partials summed per matrix in a fixed order
 constexpr int kFrobParts = 64;
@@ -346,14 +379,78 @@ __device__ void chol_solve(const double* __restrict__ P, int nb, double* v, doub
   }
 }
 
+// v <- P v for a symmetric P stored as its lower 64x64 tiles (k, j<=k) in the same packed order
+// (diagonal tiles full). Each tile is read once and serves both y_k += P_kj v_j and, for j < k,
+// y_j += P_kjᵀ v_k (32 columns per 31 shuffles); every warp accumulates into its own partial
+// vector in shared memory (part: kSolveWarps x nb*64), summed in warp order: deterministic.
+__device__ void symv_packed(const double* __restrict__ P, int nb, double* v, double* part) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  const int len = nb * NB;
+  double* my = part + static_cast<size_t>(warp) * len;
+  for (int i = lane; i < len; i += 32) my[i] = 0.0;
+  __syncwarp();
+  const int T = nb * (nb + 1) / 2;
+  int k = 0, j = warp;  // tile t = k(k+1)/2 + j, t = warp, warp + kSolveWarps, ...
+  while (j > k) {
+    j -= k + 1;
+    ++k;
+  }
+  for (int t = warp; t < T; t += kSolveWarps) {
+    const double* tile = P + static_cast<long long>(t) * (NB * NB);
+    const double* gj = v + j * NB;
+    const double gk0 = v[k * NB + 2 * lane], gk1 = v[k * NB + 2 * lane + 1];
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double p[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(tile + (h * 32 + c) * NB) + lane);
+        const double gc = gj[h * 32 + c];
+        a0 += a.x * gc;
+        a1 += a.y * gc;
+        p[c] = a.x * gk0 + a.y * gk1;
+      }
+      if (j < k) {  // warp-uniform
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int i = 0; i < o; ++i) {
+            const double send = up ? p[i] : p[i + o];
+            const double keep = up ? p[i + o] : p[i];
+            p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        my[j * NB + h * 32 + lane] += p[0];
+      }
+    }
+    my[k * NB + 2 * lane] += a0;
+    my[k * NB + 2 * lane + 1] += a1;
+    __syncwarp();
+    j += kSolveWarps;
+    while (j > k && k < nb) {
+      j -= k + 1;
+      ++k;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < len; i += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < kSolveWarps; ++w) s += part[static_cast<size_t>(w) * len + i];
+    v[i] = s;
+  }
+  __syncthreads();
+}
+
 // λmax(A⁻¹) by power iteration through the factor: one CTA per matrix
 __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_power(const double* __restrict__ P,
                                                                  const long long* __restrict__ poff,
                                                                  const int* __restrict__ nvec, int iters, int nbmax,
-                                                                 double* __restrict__ out) {
+                                                                 double* __restrict__ out, int inverse) {
   extern __shared__ double sm[];
   double* x = sm;
-  double* red = sm + static_cast<size_t>(nbmax) * NB;
+  double* red = sm + static_cast<size_t>(nbmax) * NB;  // solve: kSolveWarps*64; symv: kSolveWarps*nbmax*64
   __shared__ double nrm_s;
   const int i = blockIdx.x, n = nvec[i], nb = (n + NB - 1) / NB;
   for (int r = threadIdx.x; r < nb * NB; r += blockDim.x) x[r] = r < n ? 1.0 + 0.25 * sin(0.7 * r + 0.3) : 0.0;
@@ -376,7 +473,8 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_power(const double* _
     if (it == iters || !(nrm > 0.0)) break;
     for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] /= nrm;
     __syncthreads();
-    chol_solve(P + poff[i], nb, x, red);
+    if (inverse) symv_packed(P + poff[i], nb, x, red);
+    else chol_solve(P + poff[i], nb, x, red);
   }
   if (threadIdx.x == 0) out[i] = lam;
 }
@@ -413,7 +511,8 @@ std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int
 // Out: the tile-packed factor at P + poff[i] (diagonal tiles inverted), fail[i] = 1 when a pivot
 // was not positive, frob_A[i] = ‖A_i‖_F (an upper bound of λmax).
 void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const std::vector<long long>& off, double* P,
-                           const std::vector<long long>& poff, std::vector<int>& fail, std::vector<double>& frob_A) {
+                           const std::vector<long long>& poff, std::vector<int>& fail, std::vector<double>& frob_A,
+                           bool inverse, std::vector<double>* frob_P, double** Pfull_out) {
   ScopedKernelTimer tk(c, "cholesky");
   const int B = static_cast<int>(n.size());
   fail.assign(B, 0);
@@ -527,8 +626,96 @@ void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const s
     for (int k = 0; k < ceil_div(n[i], NB); ++k) rows.push_back(make_int2(i, k));
   drows.upload(rows, c.stream);
   dpoff.upload(poff, c.stream);
-  k_pack_row<<<static_cast<int>(rows.size()), 256, 0, c.stream>>>(A, dm.p, drows.p, P, dpoff.p, Dinv, ddoff.p);
-  RDD_LAUNCH_CHECK();
+  if (!inverse) {
+    k_pack_row<<<static_cast<int>(rows.size()), 256, 0, c.stream>>>(A, dm.p, drows.p, P, dpoff.p, Dinv, ddoff.p);
+    RDD_LAUNCH_CHECK();
+  } else {
+    // explicit inverse for small blocks: M = L⁻¹ by block rows (M_kk = D_k,
+    // M[ib, :ib] = -D_ib L[ib, :ib] M[:ib, :ib]), then A⁻¹ = MᵀM (lower tiles), packed
+    const size_t tot = static_cast<size_t>(off[B - 1] + static_cast<long long>(n[B - 1]) * n[B - 1]);
+    double* Mi = c.ws("chol.Minv", tot);
+    double* Pf = c.ws("chol.Pfull", tot);
+    RDD_CUDA(cudaMemsetAsync(Mi, 0, tot * sizeof(double), c.stream));
+    k_set_diag<<<static_cast<int>(rows.size()), 256, 0, c.stream>>>(Mi, dm.p, drows.p, Dinv, ddoff.p);
+    RDD_LAUNCH_CHECK();
+    long long tmp_sz = 0;
+    std::vector<long long> toff(B);
+    for (int i = 0; i < B; ++i) {
+      toff[i] = tmp_sz;
+      tmp_sz += static_cast<long long>(NB) * n[i];
+    }
+    double* tmp = c.ws("chol.tmp", std::max<long long>(1, tmp_sz));
+    for (int ib = 1; ib < nbmax; ++ib) {
+      std::vector<GemmTask> g1, g2;
+      for (int i = 0; i < B; ++i) {
+        if (ib >= ceil_div(n[i], NB)) continue;
+        const int bi = std::min(NB, n[i] - ib * NB), wd = ib * NB;
+        double* L = A + off[i];
+        double* Mm = Mi + off[i];
+        for (int tn = 0; tn < ib; ++tn) {
+          const int k0 = tn * NB;
+          GemmTask t{};  // tmp[:, tn] = L[ib, k0:wd] M[k0:wd, tn]  (M lower triangular)
+          t.A = L + ib * NB + static_cast<long long>(k0) * n[i];
+          t.B = Mm + k0 + static_cast<long long>(k0) * n[i];
+          t.Cm = tmp + toff[i] + static_cast<long long>(k0) * NB;
+          t.M = bi;
+          t.N = NB;
+          t.K = wd - k0;
+          t.lda = t.ldb = n[i];
+          t.ldc = NB;
+          t.alpha = 1.0;
+          g1.push_back(t);
+          GemmTask u{};  // M[ib, tn] = -D_ib tmp[:, tn]
+          u.A = Mm + ib * NB + static_cast<long long>(ib * NB) * n[i];
+          u.B = tmp + toff[i];
+          u.Cm = Mm + ib * NB;
+          u.M = bi;
+          u.N = wd;
+          u.K = bi;
+          u.lda = n[i];
+          u.ldb = NB;
+          u.ldc = n[i];
+          u.tn = tn;
+          u.alpha = -1.0;
+          g2.push_back(u);
+        }
+      }
+      gemm_nn(c, g1);
+      gemm_nn(c, g2);
+    }
+    std::vector<GemmTask> g;
+    for (int i = 0; i < B; ++i)
+      for (int tm = 0; tm < ceil_div(n[i], NB); ++tm)
+        for (int tn = 0; tn <= tm; ++tn) {
+          GemmTask t{};
+          const int k0 = tm * NB;  // rows of M below the tile's first output row
+          t.A = Mi + off[i] + k0;
+          t.B = Mi + off[i] + k0;
+          t.Cm = Pf + off[i];
+          t.M = t.N = n[i];
+          t.K = n[i] - k0;
+          t.lda = t.ldb = t.ldc = n[i];
+          t.tm = tm;
+          t.tn = tn;
+          t.alpha = 1.0;
+          g.push_back(t);
+        }
+    gemm_tn(c, g);  // P = MᵀM, lower tiles
+    k_pack_lower<<<static_cast<int>(rows.size()), 256, 0, c.stream>>>(Pf, dm.p, drows.p, P, dpoff.p);
+    RDD_LAUNCH_CHECK();
+    if (frob_P) {
+      DBuf<double> fpart, dfp;
+      fpart.ensure(static_cast<size_t>(B) * kFrobParts);
+      dfp.ensure(B);
+      k_frob_part<<<dim3(kFrobParts, B), 256, 0, c.stream>>>(Pf, dm.p, fpart.p);
+      RDD_LAUNCH_CHECK();
+      k_frob_sum<<<ceil_div(B, 128), 128, 0, c.stream>>>(fpart.p, B, dfp.p);
+      RDD_LAUNCH_CHECK();
+      frob_P->assign(B, 0.0);
+      dfp.download(frob_P->data(), B, c.stream);
+    }
+    if (Pfull_out) *Pfull_out = Pf;
+  }
   dfail.download(fail.data(), B, c.stream);
   dfa.download(frob_A.data(), B, c.stream);
   RDD_CUDA(cudaStreamSynchronize(c.stream));
@@ -539,12 +726,13 @@ long long packed_chol_size(int n) {
   return nb * (nb + 1) / 2 * NB * NB;
 }
 
-size_t chol_solve_smem(int nmax) {
-  return (static_cast<size_t>(ceil_div(nmax, NB)) * NB + kSolveWarps * NB) * sizeof(double);
+size_t chol_solve_smem(int nmax, bool inverse) {
+  const size_t len = static_cast<size_t>(ceil_div(nmax, NB)) * NB;
+  return (len + (inverse ? kSolveWarps * len : kSolveWarps * NB)) * sizeof(double);
 }
 
 std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector<int>& n,
-                                      const std::vector<long long>& poff, int iters) {
+                                      const std::vector<long long>& poff, int iters, bool inverse) {
   ScopedKernelTimer tk(c, "inv_power");
   const int B = static_cast<int>(n.size());
   std::vector<double> out(B, 0.0);
@@ -556,10 +744,11 @@ std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector
   dn.upload(n, c.stream);
   dp.upload(poff, c.stream);
   d.ensure(B);
-  const size_t smem = chol_solve_smem(nmax);
+  const size_t smem = chol_solve_smem(nmax, inverse);
   if (c.verbose) std::fprintf(stderr, "[inv_power] B=%d nmax=%d smem=%zu iters=%d\n", B, nmax, smem, iters);
   RDD_CUDA(cudaFuncSetAttribute(k_chol_power, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  k_chol_power<<<B, kSolveWarps * 32, smem, c.stream>>>(P, dp.p, dn.p, iters, ceil_div(nmax, NB), d.p);
+  k_chol_power<<<B, kSolveWarps * 32, smem, c.stream>>>(P, dp.p, dn.p, iters, ceil_div(nmax, NB), d.p,
+                                                        inverse ? 1 : 0);
   RDD_LAUNCH_CHECK();
   d.download(out.data(), B, c.stream);
   RDD_CUDA(cudaStreamSynchronize(c.stream));
@@ -573,7 +762,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
     const double* __restrict__ P, const long long* __restrict__ poff, const double* const* __restrict__ dense,
     const int* __restrict__ set_ptr, const int* __restrict__ set_idx, const double* __restrict__ v,
     const int* __restrict__ mult, const int* __restrict__ owner, int kind, int transpose, int nbmax,
-    double* __restrict__ z) {
+    double* __restrict__ z, int inverse) {
   extern __shared__ double sm[];
   double* g = sm;
   double* red = sm + static_cast<size_t>(nbmax) * NB;
@@ -601,12 +790,13 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
     }
     return;
   }
-  chol_solve(P + poff[i], nb, g, red);
+  if (inverse) symv_packed(P + poff[i], nb, g, red);
+  else chol_solve(P + poff[i], nb, g, red);
   for (int r = threadIdx.x; r < n; r += blockDim.x) z[s0 + r] = g[r];
 }
 
 void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
-  const size_t smem = chol_solve_smem(c.nmax_local);
+  const size_t smem = chol_solve_smem(c.nmax_local, c.inv_mode);
   static size_t set = 0;
   if (smem > set) {
     RDD_CUDA(cudaFuncSetAttribute(k_chol_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -614,7 +804,7 @@ void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
   }
   k_chol_apply<<<c.J, kSolveWarps * 32, smem, c.stream>>>(c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p,
                                                           v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
-                                                          ceil_div(c.nmax_local, NB), zloc);
+                                                          ceil_div(c.nmax_local, NB), zloc, c.inv_mode ? 1 : 0);
   RDD_LAUNCH_CHECK();
 }
 

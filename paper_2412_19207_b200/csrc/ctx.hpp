@@ -135,6 +135,7 @@ struct Ctx {
   int n_fallback = 0;                 // local blocks that took the eigen pseudo-inverse
   std::vector<int> fallback, local_n;
   size_t schwarz_budget = 0;
+  bool inv_mode = false;              // small blocks: packed explicit A_i⁻¹ (one SYMV per apply)
   int qr_rank = 0;                    // numerical rank of the dense QR path          // bytes of gathered A_i per chunk (fixed per context)
   std::map<int, DBuf<double>> fb_store;  // eigen-fallback subdomains: dense pseudo-inverse
   DBuf<double*> dfb_ptr;              // per i: dense pseudo-inverse or nullptr (factor path)
@@ -259,11 +260,12 @@ void project_blocks(Ctx& c);
 void ensure_col_owner(Ctx& c);
 // cholesky.cu
 void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const std::vector<long long>& off, double* P,
-                           const std::vector<long long>& poff, std::vector<int>& fail, std::vector<double>& frob_A);
+                           const std::vector<long long>& poff, std::vector<int>& fail, std::vector<double>& frob_A,
+                           bool inverse = false, std::vector<double>* frob_P = nullptr, double** Pfull_out = nullptr);
 long long packed_chol_size(int n);
-size_t chol_solve_smem(int nmax);
+size_t chol_solve_smem(int nmax, bool inverse);
 std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector<int>& n,
-                                      const std::vector<long long>& poff, int iters);
+                                      const std::vector<long long>& poff, int iters, bool inverse);
 void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc);
 std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int>& n,
                                   const std::vector<long long>& off, int iters);

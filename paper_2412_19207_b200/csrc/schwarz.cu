@@ -18,6 +18,8 @@
 
 namespace rdd {
 
+constexpr int kInvMax = 1024;  // largest local order kept as an explicit inverse
+
 namespace {
 
 // gather A_i from normal blocks: one CTA per (i, part-pair). Blocks stored transposed (j1 > j2:
@@ -215,7 +217,7 @@ void refresh_local_cond(Ctx& c) {
     DBuf<double> Af;
     gather_locals(c, sub, Af, off);
     const std::vector<double> la = batched_power(c, Af.p, nn, off, 200);
-    const std::vector<double> lp = batched_inv_power(c, c.P.p, nn, poff, 200);
+    const std::vector<double> lp = batched_inv_power(c, c.P.p, nn, poff, 200, c.inv_mode);
     for (size_t q = 0; q < sub.size(); ++q) c.local_cond[sub[q]] = la[q] * lp[q];
   }
   c.local_cond_exact = true;
@@ -280,7 +282,10 @@ void build_schwarz(Ctx& c, int kind) {
         c.gat_tasks.push_back({i, j1, j2, o1, o2, c.nb_off[it->second]});
       }
   }
-  // storage: the tile-packed factor of every A_i (the eigen-fallback blocks keep a dense copy)
+  // storage: the tile-packed factor of every A_i (the eigen-fallback blocks keep a dense copy) or,
+  // when every block is small, the packed explicit inverse: one symmetric tile pass per apply
+  // instead of two triangular ones, for 2/3·n³ more build flops
+  c.inv_mode = *std::max_element(n.begin(), n.end()) <= kInvMax;
   c.P_off.assign(J + 1, 0);
   for (int i = 0; i < J; ++i) c.P_off[i + 1] = c.P_off[i] + packed_chol_size(n[i]);
   c.dP_off.upload(c.P_off, c.stream);
@@ -327,20 +332,31 @@ void build_schwarz(Ctx& c, int kind) {
     }
     std::vector<int> fail;
     std::vector<double> fa;
-    batched_cholesky_pack(c, Aw.p, cn, coff, c.P.p, cpoff, fail, fa);
-    // rank decision: cond(A_i) <= ‖A_i‖_F·λmax(A_i⁻¹) (power iteration through the factor); when
-    // that does not clear the threshold, λmax(A_i) by power iteration and a longer λmax(A_i⁻¹)
+    std::vector<double> fp;
+    batched_cholesky_pack(c, Aw.p, cn, coff, c.P.p, cpoff, fail, fa, c.inv_mode, &fp);
+    // rank decision: cond(A_i) <= ‖A_i‖_F·‖A_i⁻¹‖_F (explicit inverse) or ‖A_i‖_F·λmax(A_i⁻¹) (power
+    // iteration through the factor); when that does not clear the threshold, λmax(A_i) by power
+    // iteration and a longer λmax(A_i⁻¹)
     std::vector<int> ok_q, flagged;
     for (int q = 0; q < B; ++q)
       if (!fail[q]) ok_q.push_back(q);
-    {
+    if (c.inv_mode) {
+      for (int q : ok_q) {
+        if (fa[q] * fp[q] < c.full_rank_cond) {
+          c.local_rank[chunk[q]] = cn[q];
+          c.local_cond[chunk[q]] = fa[q] * fp[q];
+        } else {
+          flagged.push_back(q);
+        }
+      }
+    } else {
       std::vector<int> nn;
       std::vector<long long> po;
       for (int q : ok_q) {
         nn.push_back(cn[q]);
         po.push_back(cpoff[q]);
       }
-      const std::vector<double> lp = batched_inv_power(c, c.P.p, nn, po, 12);
+      const std::vector<double> lp = batched_inv_power(c, c.P.p, nn, po, 12, false);
       for (size_t z = 0; z < ok_q.size(); ++z) {
         const int q = ok_q[z];
         if (fa[q] * lp[z] < c.full_rank_cond) {
@@ -365,9 +381,9 @@ void build_schwarz(Ctx& c, int kind) {
         po.push_back(cpoff[q]);
         t += static_cast<long long>(cn[q]) * cn[q];
       }
+      const std::vector<double> lp = batched_inv_power(c, c.P.p, fnn, po, 60, c.inv_mode);
       gather_locals(c, which, Aw, foff);
       const std::vector<double> la = batched_power(c, Aw.p, fnn, foff, 60);
-      const std::vector<double> lp = batched_inv_power(c, c.P.p, fnn, po, 60);
       for (size_t z = 0; z < flagged.size(); ++z) {
         const int q = flagged[z];
         const double cond = la[z] * lp[z];

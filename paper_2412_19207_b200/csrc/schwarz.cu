@@ -291,9 +291,11 @@ void build_schwarz(Ctx& c, int kind) {
   c.dP_off.upload(c.P_off, c.stream);
   c.fb_store.clear();
   const size_t p_bytes = static_cast<size_t>(c.P_off[J]) * sizeof(double);
+  // cudaMemGetInfo costs up to ~20 ms of host time: only ask when the factor storage must grow
+  const bool grow = c.P.n < static_cast<size_t>(std::max<long long>(1, c.P_off[J]));
   {
     ScopedKernelTimer ta(c, "schwarz_alloc");
-    if (device_available(c) < p_bytes + (size_t(8) << 30)) release_scratch(c);
+    if (grow && device_available(c) < p_bytes + (size_t(8) << 30)) release_scratch(c);
     c.P.ensure(std::max<long long>(1, c.P_off[J]));
   }
   // chunk budget for the gathered A_i: fixed at the first build of this context, so reruns reuse the
@@ -302,7 +304,8 @@ void build_schwarz(Ctx& c, int kind) {
   if (c.schwarz_budget == 0)
     c.schwarz_budget =
         std::min<size_t>(size_t(40) << 30, std::max<size_t>(size_t(1) << 30, (device_available(c) * 3) / 5));
-  c.schwarz_budget = std::min(c.schwarz_budget, std::max<size_t>(size_t(1) << 30, (device_available(c) * 3) / 5));
+  if (grow)
+    c.schwarz_budget = std::min(c.schwarz_budget, std::max<size_t>(size_t(1) << 30, (device_available(c) * 3) / 5));
   const size_t budget = c.schwarz_budget;
   c.local_rank.assign(J, 0);
   c.local_cond.assign(J, 0.0);

@@ -124,7 +124,8 @@ int rdd_build_instance(rdd_ctx* ctx, const rdd_config* cfg, uint64_t seed);
 int rdd_assemble(rdd_ctx* ctx, int equilibrate);
 /* assembly.hpp:148-183 normal_blocks + schwarz.hpp:39-61 build_index_sets + :93-148 build_preconditioner */
 int rdd_build_preconditioner(rdd_ctx* ctx, int kind);
-/* runner.hpp:232-251: b = Hᵀ F_c, solve_with (krylov.hpp:391), W ./= scales */
+/* runner.hpp:232-251: b = Hᵀ F_c, solve_with (krylov.hpp:391: cg, cgs, bicg, gmres), W ./= scales;
+ * solver = RDD_SOLVER_QR: runner.hpp:217-222 densify + column-pivoted QR (krylov.hpp:97-101) */
 int rdd_solve(rdd_ctx* ctx, int solver, double rel_tol, int max_iter, int gmres_restart);
 /* runner.hpp:253-256 evaluate_solution + exact_values + compute_errors (problems.hpp:294) */
 int rdd_evaluate(rdd_ctx* ctx, const int* test_res);
@@ -149,8 +150,11 @@ int rdd_precond_apply(rdd_ctx* ctx, const double* v, double* z, int transpose); 
 
 /* ---- exports (parity tooling; assembly.hpp:206-256 densify/export analogues) --------- */
 /* Returns the element count (or <0 on error). With out == NULL only the count is returned.
- * Names: see DESIGN.md §ABI (e.g. "rows" j, "p_j", "col_off", "H" j, "F", "scales",
- * "sigma" j, "V" j, "S" j, "nb" k, "nb_pairs", "local_rank", "W" c, "hist" c, ...). */
+ * Names (e.g.): int "rows" j, "row_ptr", "p_j", "col_off", "nbr" i, "nb_pairs", "local_rank",
+ * "local_n", "set" i, "owner", "mult", "iterations", "converged", "n_fallback", "qr_rank";
+ * double "points", "box_lo"/"box_hi", "R" j, "b" j, "S" j, "sigma" j, "V" j, "H" j, "F",
+ * "scales", "nb" k, "nb_dense", "H_dense", "local_cond", "W" c, "hist" c, "true_hist" c,
+ * "approx", "exact". */
 int64_t rdd_get_i(rdd_ctx* ctx, const char* what, int index, int32_t* out, int64_t cap);
 int64_t rdd_get_d(rdd_ctx* ctx, const char* what, int index, double* out, int64_t cap);
 
@@ -158,8 +162,8 @@ int64_t rdd_get_d(rdd_ctx* ctx, const char* what, int index, double* out, int64_
 /* Device time (ms) of the last call of a named kernel family and its launch count since reset. */
 int rdd_kernel_stats(rdd_ctx* ctx, const char* family, double* ms_total, int64_t* launches);
 int rdd_reset_stats(rdd_ctx* ctx);
-int rdd_set_timing(rdd_ctx* ctx, int on);
-int rdd_set_verbose(rdd_ctx* ctx, int on);  /* solver diagnostics on stderr */  /* per-family CUDA-event timing (adds syncs) */
+int rdd_set_timing(rdd_ctx* ctx, int on);  /* per-family CUDA-event timing (adds syncs) */
+int rdd_set_verbose(rdd_ctx* ctx, int on);  /* phase times and solver diagnostics on stderr */
 /* Time `reps` calls of the normal operator on device-resident vectors (CUDA events). */
 int rdd_bench_operator(rdd_ctx* ctx, int op_form, int reps, double* ms_per_call, double* bytes_per_call);
 /* Batched Jacobi eigensolver probe (no reference counterpart; tuning aid): `batch` random

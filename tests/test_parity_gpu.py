@@ -227,3 +227,22 @@ def test_qr_direct(dev, orc, name):
     assert sd["e_l2"] == pytest.approx(so["e_l2"], rel=1e-6), (name, sd["e_l2"], so["e_l2"])
     wd, wo = dev.getd("W", 0), orc.getd("W", 0)
     assert np.linalg.norm(wd - wo) <= 1e-6 * np.linalg.norm(wo), name
+
+
+# the two alternative normal-operator formulations: the single-pass fused kernel and
+# the assembled normal blocks HᵀH, against the reference's two passes on the oracle
+@pytest.mark.parametrize("name", ["c1_slice", "c2_slice", "c3_slice", "c4_slice", "runner77"])
+@pytest.mark.parametrize("op_form", [A.OPERATOR_FUSED, A.OPERATOR_NORMAL])
+def test_operator_forms(dev, orc, name, op_form):
+    cfg = A.Config.from_buffer_copy(CASES[name])
+    cfg.op_form = op_form
+    dev.build_instance(cfg).assemble(True)
+    if op_form == A.OPERATOR_NORMAL:
+        dev.build_preconditioner(A.PRECOND_AS)  # builds the normal blocks
+    orc.build_instance(cfg).assemble(True)
+    p = int(orc.geti("p")[0])
+    w = np.random.default_rng(11).standard_normal(p)
+    no = orc.matvec_transpose(orc.matvec(w))
+    nd = dev.normal_apply(w)
+    tol = 1e-11 if cfg.tau_mode == A.TAU_OFF else 1e-6
+    assert np.linalg.norm(nd - no) <= tol * np.linalg.norm(no), (name, op_form)

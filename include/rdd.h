@@ -143,10 +143,12 @@ int rdd_event_record(rdd_ctx* ctx, int slot);
 int rdd_event_elapsed(rdd_ctx* ctx, int slot_a, int slot_b, double* ms);
 
 /* ---- operators (pluggable into the reference's LinearMap, krylov.hpp:42-52) ---------- */
-int rdd_matvec(rdd_ctx* ctx, const double* w, double* y);            /* assembly.hpp:110 */
-int rdd_matvec_transpose(rdd_ctx* ctx, const double* r, double* out);/* assembly.hpp:123 */
-int rdd_normal_apply(rdd_ctx* ctx, const double* w, double* out);    /* runner.hpp:233   */
-int rdd_precond_apply(rdd_ctx* ctx, const double* v, double* z, int transpose); /* schwarz.hpp:153/189 */
+/* Vector lengths are checked like the reference's (RDD_INVALID_ARGUMENT, "... wrong length"). */
+int rdd_matvec(rdd_ctx* ctx, const double* w, int64_t nw, double* y, int64_t ny);             /* assembly.hpp:110 */
+int rdd_matvec_transpose(rdd_ctx* ctx, const double* r, int64_t nr, double* out, int64_t nout); /* :123 */
+int rdd_normal_apply(rdd_ctx* ctx, const double* w, int64_t nw, double* out, int64_t nout);   /* runner.hpp:233 */
+int rdd_precond_apply(rdd_ctx* ctx, const double* v, int64_t nv, double* z, int64_t nz,
+                      int transpose);                                          /* schwarz.hpp:153/189 */
 
 /* ---- exports (parity tooling; assembly.hpp:206-256 densify/export analogues) --------- */
 /* Returns the element count (or <0 on error). With out == NULL only the count is returned.

@@ -316,9 +316,11 @@ int rdd_get_summary(rdd_ctx* h, rdd_summary* out) {
 }
 
 // ---- operators on host vectors
-int rdd_matvec(rdd_ctx* h, const double* w, double* y) {
+int rdd_matvec(rdd_ctx* h, const double* w, int64_t nw, double* y, int64_t ny) {
   return guarded(h, [&](Ctx& c) {
     need_assembled(c);
+    if (nw != c.p) throw std::invalid_argument("matvec: coefficient vector has wrong length");  // assembly.hpp:111
+    if (ny != c.N) throw std::invalid_argument("matvec: output vector has wrong length");
     rdd::DBuf<double> dw, dy;
     dw.upload(w, c.p, c.stream);
     dy.ensure(c.N);
@@ -327,9 +329,11 @@ int rdd_matvec(rdd_ctx* h, const double* w, double* y) {
     RDD_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
-int rdd_matvec_transpose(rdd_ctx* h, const double* r, double* out) {
+int rdd_matvec_transpose(rdd_ctx* h, const double* r, int64_t nr, double* out, int64_t nout) {
   return guarded(h, [&](Ctx& c) {
     need_assembled(c);
+    if (nr != c.N) throw std::invalid_argument("matvec_transpose: residual vector has wrong length");  // :124
+    if (nout != c.p) throw std::invalid_argument("matvec_transpose: output vector has wrong length");
     rdd::DBuf<double> dr, dout;
     dr.upload(r, c.N, c.stream);
     dout.ensure(c.p);
@@ -338,9 +342,10 @@ int rdd_matvec_transpose(rdd_ctx* h, const double* r, double* out) {
     RDD_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
-int rdd_normal_apply(rdd_ctx* h, const double* w, double* out) {
+int rdd_normal_apply(rdd_ctx* h, const double* w, int64_t nw, double* out, int64_t nout) {
   return guarded(h, [&](Ctx& c) {
     need_assembled(c);
+    if (nw != c.p || nout != c.p) throw std::invalid_argument("matvec: coefficient vector has wrong length");
     rdd::DBuf<double> dw, dout;
     dw.upload(w, c.p, c.stream);
     dout.ensure(c.p);
@@ -349,9 +354,11 @@ int rdd_normal_apply(rdd_ctx* h, const double* w, double* out) {
     RDD_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
-int rdd_precond_apply(rdd_ctx* h, const double* v, double* z, int transpose) {
+int rdd_precond_apply(rdd_ctx* h, const double* v, int64_t nv, double* z, int64_t nz, int transpose) {
   return guarded(h, [&](Ctx& c) {
     if (c.pkind < 0) throw std::invalid_argument("no preconditioner built");
+    if (nv != c.p || nz != c.p)
+      throw std::invalid_argument("preconditioner apply: wrong vector length");  // schwarz.hpp:154/190
     rdd::DBuf<double> dv, dz;
     dv.upload(v, c.p, c.stream);
     dz.ensure(c.p);

@@ -113,6 +113,12 @@ void setup_problem(Ctx& c, const rdd_config& cfg, uint64_t seed) {
   c.jl = jet_len(d);
   c.m = cfg.m;
   if (cfg.m < 1) throw std::invalid_argument("hidden width m must be >= 1");
+  if (cfg.dim != 0 && cfg.dim != d)  // runner.hpp:45
+    throw std::invalid_argument("decomposition counts have dimension " + std::to_string(cfg.dim) +
+                                " but the problem has dimension " + std::to_string(d));
+  if (cfg.tau_mode != RDD_TAU_OFF && !(cfg.tau >= 0.0))  // reduction.hpp:90
+    throw std::invalid_argument("truncation threshold tau must be >= 0");
+  if (cfg.max_iter < 0) throw std::invalid_argument("max_iter must be >= 1");  // krylov.hpp:79
   c.counts.assign(cfg.counts, cfg.counts + d);
   for (int k : c.counts)
     if (k < 1) throw std::invalid_argument("per-axis subdomain counts must be >= 1");

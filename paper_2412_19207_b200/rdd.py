@@ -59,10 +59,11 @@ def lib():
         L.rdd_io_bytes.argtypes = [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.rdd_event_record.argtypes = [vp, C.c_int]
         L.rdd_event_elapsed.argtypes = [vp, C.c_int, C.c_int, dp]
-        L.rdd_matvec.argtypes = [vp, dp, dp]
-        L.rdd_matvec_transpose.argtypes = [vp, dp, dp]
-        L.rdd_normal_apply.argtypes = [vp, dp, dp]
-        L.rdd_precond_apply.argtypes = [vp, dp, dp, C.c_int]
+        i64 = C.c_int64
+        L.rdd_matvec.argtypes = [vp, dp, i64, dp, i64]
+        L.rdd_matvec_transpose.argtypes = [vp, dp, i64, dp, i64]
+        L.rdd_normal_apply.argtypes = [vp, dp, i64, dp, i64]
+        L.rdd_precond_apply.argtypes = [vp, dp, i64, dp, i64, C.c_int]
         L.rdd_get_i.restype = C.c_int64
         L.rdd_get_i.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(C.c_int32), C.c_int64]
         L.rdd_get_d.restype = C.c_int64
@@ -154,25 +155,25 @@ class Solver:
     def matvec(self, w):
         w = np.ascontiguousarray(w, dtype=np.float64)
         y = np.zeros(self.geti("N")[0])
-        self._check(self.L.rdd_matvec(self.h, _dp(w), _dp(y)))
+        self._check(self.L.rdd_matvec(self.h, _dp(w), w.size, _dp(y), y.size))
         return y
 
     def matvec_transpose(self, r):
         r = np.ascontiguousarray(r, dtype=np.float64)
         y = np.zeros(self.geti("p")[0])
-        self._check(self.L.rdd_matvec_transpose(self.h, _dp(r), _dp(y)))
+        self._check(self.L.rdd_matvec_transpose(self.h, _dp(r), r.size, _dp(y), y.size))
         return y
 
     def normal_apply(self, w):
         w = np.ascontiguousarray(w, dtype=np.float64)
         y = np.zeros(self.geti("p")[0])
-        self._check(self.L.rdd_normal_apply(self.h, _dp(w), _dp(y)))
+        self._check(self.L.rdd_normal_apply(self.h, _dp(w), w.size, _dp(y), y.size))
         return y
 
     def precond_apply(self, v, transpose: bool = False):
         v = np.ascontiguousarray(v, dtype=np.float64)
-        z = np.zeros_like(v)
-        self._check(self.L.rdd_precond_apply(self.h, _dp(v), _dp(z), int(transpose)))
+        z = np.zeros(self.geti("p")[0])
+        self._check(self.L.rdd_precond_apply(self.h, _dp(v), v.size, _dp(z), z.size, int(transpose)))
         return z
 
     # ---- exports

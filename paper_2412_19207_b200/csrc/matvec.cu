@@ -104,20 +104,36 @@ __global__ void __launch_bounds__(kMtWarps * 32) k_block_gemv_t(const double* __
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* out = part + part_off[blockIdx.x];
-  for (int k = warp; k < pj; k += kMtWarps) {
-    const double* h = H + H_off[j] + static_cast<long long>(k) * rows + q0;
-    double s = 0.0;
+  for (int k = warp; k < pj; k += 2 * kMtWarps) {  // two columns per warp: 2·kMtUnroll loads in flight
+    const int kb = k + kMtWarps;
+    const bool hb = kb < pj;
+    const double* ha = H + H_off[j] + static_cast<long long>(k) * rows + q0;
+    const double* hbp = H + H_off[j] + static_cast<long long>(hb ? kb : k) * rows + q0;
+    double sa = 0.0, sb = 0.0;
     int q = lane;
     for (; q + 32 * (kMtUnroll - 1) < nq; q += 32 * kMtUnroll) {
-      double a[kMtUnroll];
+      double a[kMtUnroll], b[kMtUnroll];
 #pragma unroll
-      for (int u = 0; u < kMtUnroll; ++u) a[u] = __ldcs(h + q + 32 * u);
+      for (int u = 0; u < kMtUnroll; ++u) {
+        a[u] = __ldcs(ha + q + 32 * u);
+        b[u] = hb ? __ldcs(hbp + q + 32 * u) : 0.0;
+      }
 #pragma unroll
-      for (int u = 0; u < kMtUnroll; ++u) s += a[u] * rsm[q + 32 * u];
+      for (int u = 0; u < kMtUnroll; ++u) {
+        sa += a[u] * rsm[q + 32 * u];
+        sb += b[u] * rsm[q + 32 * u];
+      }
     }
-    for (; q < nq; q += 32) s += h[q] * rsm[q];
-    s = warp_sum(s);
-    if (lane == 0) out[k] = s;
+    for (; q < nq; q += 32) {
+      sa += ha[q] * rsm[q];
+      if (hb) sb += hbp[q] * rsm[q];
+    }
+    sa = warp_sum(sa);
+    sb = warp_sum(sb);
+    if (lane == 0) {
+      out[k] = sa;
+      if (hb) out[kb] = sb;
+    }
   }
 }
 

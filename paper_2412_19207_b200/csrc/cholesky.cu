@@ -383,19 +383,20 @@ __device__ void chol_solve(const double* __restrict__ P, int nb, double* v, doub
 // (diagonal tiles full). Each tile is read once and serves both y_k += P_kj v_j and, for j < k,
 // y_j += P_kjᵀ v_k (32 columns per 31 shuffles); every warp accumulates into its own partial
 // vector in shared memory (part: kSolveWarps x nb*64), summed in warp order: deterministic.
-__device__ void symv_packed(const double* __restrict__ P, int nb, double* v, double* part) {
+__device__ void symv_packed(const double* __restrict__ P, int nb, double* v, double* part, int t0 = 0, int tstep = 1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   const int len = nb * NB;
   double* my = part + static_cast<size_t>(warp) * len;
   for (int i = lane; i < len; i += 32) my[i] = 0.0;
   __syncwarp();
   const int T = nb * (nb + 1) / 2;
-  int k = 0, j = warp;  // tile t = k(k+1)/2 + j, t = warp, warp + kSolveWarps, ...
+  const int first = t0 + warp * tstep, stride = kSolveWarps * tstep;  // this warp's tiles
+  int k = 0, j = first;  // tile t = k(k+1)/2 + j
   while (j > k) {
     j -= k + 1;
     ++k;
   }
-  for (int t = warp; t < T; t += kSolveWarps) {
+  for (int t = first; t < T; t += stride) {
     const double* tile = P + static_cast<long long>(t) * (NB * NB);
     const double* gj = v + j * NB;
     const double gk0 = v[k * NB + 2 * lane], gk1 = v[k * NB + 2 * lane + 1];
@@ -428,7 +429,7 @@ __device__ void symv_packed(const double* __restrict__ P, int nb, double* v, dou
     my[k * NB + 2 * lane] += a0;
     my[k * NB + 2 * lane + 1] += a1;
     __syncwarp();
-    j += kSolveWarps;
+    j += stride;
     while (j > k && k < nb) {
       j -= k + 1;
       ++k;
@@ -762,11 +763,13 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
     const double* __restrict__ P, const long long* __restrict__ poff, const double* const* __restrict__ dense,
     const int* __restrict__ set_ptr, const int* __restrict__ set_idx, const double* __restrict__ v,
     const int* __restrict__ mult, const int* __restrict__ owner, int kind, int transpose, int nbmax,
-    double* __restrict__ z, int inverse) {
+    double* __restrict__ z, int inverse, long long zhalf) {
   extern __shared__ double sm[];
   double* g = sm;
   double* red = sm + static_cast<size_t>(nbmax) * NB;
-  const int i = blockIdx.x;
+  // inverse mode: two CTAs per subdomain, each over every other tile, partials to z and z + zhalf
+  const int i = inverse ? blockIdx.x >> 1 : blockIdx.x;
+  const int h = inverse ? blockIdx.x & 1 : 0;
   const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0, nb = (n + NB - 1) / NB;
   for (int q = threadIdx.x; q < nb * NB; q += blockDim.x) {
     double val = 0.0;
@@ -781,18 +784,20 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
     g[q] = val;
   }
   __syncthreads();
+  double* zo = z + static_cast<long long>(h) * zhalf;
   const double* D = dense[i];
   if (D) {
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
       double acc = 0.0;
-      for (int q = 0; q < n; ++q) acc += D[r + static_cast<long long>(q) * n] * g[q];
-      z[s0 + r] = acc;
+      if (h == 0)
+        for (int q = 0; q < n; ++q) acc += D[r + static_cast<long long>(q) * n] * g[q];
+      zo[s0 + r] = acc;
     }
     return;
   }
-  if (inverse) symv_packed(P + poff[i], nb, g, red);
+  if (inverse) symv_packed(P + poff[i], nb, g, red, h, 2);
   else chol_solve(P + poff[i], nb, g, red);
-  for (int r = threadIdx.x; r < n; r += blockDim.x) z[s0 + r] = g[r];
+  for (int r = threadIdx.x; r < n; r += blockDim.x) zo[s0 + r] = g[r];
 }
 
 void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
@@ -802,9 +807,9 @@ void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
     RDD_CUDA(cudaFuncSetAttribute(k_chol_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     set = smem;
   }
-  k_chol_apply<<<c.J, kSolveWarps * 32, smem, c.stream>>>(c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p,
-                                                          v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
-                                                          ceil_div(c.nmax_local, NB), zloc, c.inv_mode ? 1 : 0);
+  k_chol_apply<<<c.inv_mode ? 2 * c.J : c.J, kSolveWarps * 32, smem, c.stream>>>(
+      c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p, v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
+      ceil_div(c.nmax_local, NB), zloc, c.inv_mode ? 1 : 0, static_cast<long long>(c.set_idx.size()));
   RDD_LAUNCH_CHECK();
 }
 

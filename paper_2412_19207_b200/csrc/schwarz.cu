@@ -99,17 +99,19 @@ __global__ void k_local_scale(double* __restrict__ V, const double* __restrict__
 
 
 // out[col] = Σ_i weight · z_i[pos]  over the ≤3^d subdomains whose S_i contains col
-__global__ void k_reduce(const double* __restrict__ z, const int* __restrict__ gat_ptr,
+// z2 (optional): a second partial of every local result (split local applies), added first
+__global__ void k_reduce(const double* __restrict__ z, const double* __restrict__ z2, const int* __restrict__ gat_ptr,
                          const int* __restrict__ gat_pos, const int* __restrict__ gat_owner_pos,
                          const int* __restrict__ mult, int p, int kind, int transpose, double* __restrict__ out) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= p) return;
   double s = 0.0;
   if (!transpose && kind == RDD_PRECOND_RAS) {
-    s = z[gat_owner_pos[col]];
+    const int q = gat_owner_pos[col];
+    s = z2 ? z[q] + z2[q] : z[q];
   } else {
     for (int q = gat_ptr[col]; q < gat_ptr[col + 1]; ++q) {
-      const double zz = z[gat_pos[q]];
+      const double zz = z2 ? z[gat_pos[q]] + z2[gat_pos[q]] : z[gat_pos[q]];
       s += (!transpose && kind == RDD_PRECOND_SAS) ? zz / mult[col] : zz;
     }
   }
@@ -262,7 +264,7 @@ void build_schwarz(Ctx& c, int kind) {
   c.dset_ptr.upload(c.set_ptr, c.stream);
   c.dset_idx.upload(c.set_idx, c.stream);
   c.dmult.upload(c.h_mult, c.stream);
-  c.zloc.ensure(std::max<size_t>(1, c.set_idx.size()));
+  c.zloc.ensure(std::max<size_t>(1, 2 * c.set_idx.size()));  // two partials in the inverse mode
 
   // local matrix sizes and gather plan (schwarz.hpp:112-130): A_i blocks come from NB
   c.local_n = n;
@@ -464,7 +466,8 @@ void build_schwarz(Ctx& c, int kind) {
 void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose) {
   ScopedKernelTimer tk(c, "precond_apply");
   chol_apply(c, v, transpose, c.zloc.p);
-  k_reduce<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.zloc.p, c.gat_ptr.p, c.gat_pos.p, c.gat_owner_pos.p, c.dmult.p,
+  const double* z2 = c.inv_mode ? c.zloc.p + c.set_idx.size() : nullptr;  // second half-partials
+  k_reduce<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.zloc.p, z2, c.gat_ptr.p, c.gat_pos.p, c.gat_owner_pos.p, c.dmult.p,
                                                      c.p, c.pkind, transpose ? 1 : 0, z);
   RDD_LAUNCH_CHECK();
 }

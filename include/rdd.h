@@ -150,6 +150,26 @@ int rdd_normal_apply(rdd_ctx* ctx, const double* w, int64_t nw, double* out, int
 int rdd_precond_apply(rdd_ctx* ctx, const double* v, int64_t nv, double* z, int64_t nz,
                       int transpose);                                          /* schwarz.hpp:153/189 */
 
+/* ---- dense diagnostics (krylov.hpp:403-440; runner.hpp:344-400) ----------------------- */
+/* cap: the dense size limit (krylov.hpp:404 kDenseSpectrumCap = 4000 when <= 0; the reference's
+ * override_caps passes 1<<20). Larger matrices fail with RDD_INVALID_ARGUMENT and the reference's
+ * "matrix of size N exceeds the dense diagnostics cap (C)". */
+/* spectrum_cmd / sweep_tau (runner.hpp:344-362, 381-393) on the assembled, equilibrated system:
+ * eigenvalues of the dense HᵀH (ascending, imag 0) and of M⁻¹HᵀH (sorted by real part, then imag,
+ * as write_spectrum_csv orders them) for the built preconditioner, and the condition numbers of
+ * both (σmax / smallest positive σ). Each output may be NULL; arrays hold p entries. The
+ * preconditioned outputs need rdd_build_preconditioner first. */
+int rdd_spectra(rdd_ctx* ctx, int cap, double* normal_re, double* normal_im, double* precond_re, double* precond_im,
+                double* cond_normal, double* cond_precond);
+/* krylov.hpp:413 spectrum: all eigenvalues of a square column-major host matrix, sorted by
+ * (real, imag); Householder Hessenberg reduction + Francis double-shift QR on the device. */
+int rdd_dense_spectrum(rdd_ctx* ctx, int64_t rows, int64_t cols, const double* A, int cap, double* wr, double* wi);
+/* krylov.hpp:423 singular_values: min(rows, cols) values, non-increasing (bidiagonalisation +
+ * Golub–Kahan bisection on the device). */
+int rdd_dense_singular_values(rdd_ctx* ctx, int64_t rows, int64_t cols, const double* A, int cap, double* s);
+/* krylov.hpp:430 condition_number; RDD_DOMAIN_ERROR when every singular value is zero. */
+int rdd_dense_condition_number(rdd_ctx* ctx, int64_t rows, int64_t cols, const double* A, int cap, double* cond);
+
 /* ---- exports (parity tooling; assembly.hpp:206-256 densify/export analogues) --------- */
 /* Returns the element count (or <0 on error). With out == NULL only the count is returned.
  * Names (e.g.): int "rows" j, "row_ptr", "p_j", "col_off", "nbr" i, "nb_pairs", "local_rank",

@@ -575,6 +575,85 @@ int rdd_bench_operator(rdd_ctx* h, int op_form, int reps, double* ms_per_call, d
   });
 }
 
+// ---- dense diagnostics (krylov.hpp:403-440, runner.hpp:344-400)
+static int diag_cap(int cap) { return cap <= 0 ? 4000 : cap; }  // krylov.hpp:404 kDenseSpectrumCap
+
+int rdd_spectra(rdd_ctx* h, int cap, double* normal_re, double* normal_im, double* precond_re, double* precond_im,
+                double* cond_normal, double* cond_precond) {
+  return guarded(h, [&](Ctx& c) {
+    need_assembled(c);
+    const bool want_pre = precond_re || precond_im || cond_precond;
+    if (want_pre && c.pkind < 0) throw std::invalid_argument("no preconditioner built");
+    std::vector<double> nre, nim, pre, pim;
+    double cn = 0.0, cp = 0.0;
+    rdd::spectra(c, diag_cap(cap), nre, nim, want_pre ? &pre : nullptr, want_pre ? &pim : nullptr,
+                 cond_normal ? &cn : nullptr, cond_precond ? &cp : nullptr);
+    if (normal_re) std::copy(nre.begin(), nre.end(), normal_re);
+    if (normal_im) std::copy(nim.begin(), nim.end(), normal_im);
+    if (precond_re) std::copy(pre.begin(), pre.end(), precond_re);
+    if (precond_im) std::copy(pim.begin(), pim.end(), precond_im);
+    if (cond_normal) *cond_normal = cn;
+    if (cond_precond) *cond_precond = cp;
+  });
+}
+
+// host matrix -> device (transposed when wide, so the reductions see rows >= cols)
+static double* upload_dense(Ctx& c, int64_t rows, int64_t cols, const double* A, bool allow_transpose, int& m, int& n) {
+  if (rows < 0 || cols < 0 || (rows * cols > 0 && !A)) throw std::invalid_argument("dense diagnostics: bad matrix");
+  m = static_cast<int>(rows);
+  n = static_cast<int>(cols);
+  const size_t nn = static_cast<size_t>(rows) * cols;
+  double* d = c.ws("dg_in", nn);
+  if (allow_transpose && rows < cols) {
+    std::vector<double> t(nn);
+    for (int64_t j = 0; j < cols; ++j)
+      for (int64_t i = 0; i < rows; ++i) t[j + i * cols] = A[i + j * rows];
+    RDD_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(double) * nn, cudaMemcpyHostToDevice, c.stream));
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    std::swap(m, n);
+  } else if (nn) {
+    RDD_CUDA(cudaMemcpyAsync(d, A, sizeof(double) * nn, cudaMemcpyHostToDevice, c.stream));
+  }
+  rdd::h2d_counter() += static_cast<int64_t>(nn * sizeof(double));
+  return d;
+}
+
+int rdd_dense_spectrum(rdd_ctx* h, int64_t rows, int64_t cols, const double* A, int cap, double* wr, double* wi) {
+  return guarded(h, [&](Ctx& c) {
+    if (rows != cols) throw std::invalid_argument("spectrum: matrix must be square");  // krylov.hpp:414
+    rdd::check_dense_cap(rows, diag_cap(cap));
+    int m = 0, n = 0;
+    double* d = upload_dense(c, rows, cols, A, false, m, n);
+    std::vector<double> re, im;
+    rdd::dense_eigenvalues_dev(c, d, n, re, im);
+    if (wr) std::copy(re.begin(), re.end(), wr);
+    if (wi) std::copy(im.begin(), im.end(), wi);
+  });
+}
+
+int rdd_dense_singular_values(rdd_ctx* h, int64_t rows, int64_t cols, const double* A, int cap, double* s) {
+  return guarded(h, [&](Ctx& c) {
+    rdd::check_dense_cap(std::min(rows, cols), diag_cap(cap));  // krylov.hpp:424
+    int m = 0, n = 0;
+    double* d = upload_dense(c, rows, cols, A, true, m, n);
+    std::vector<double> sv;
+    rdd::singular_values_dev(c, d, m, n, sv);
+    if (s) std::copy(sv.begin(), sv.end(), s);
+  });
+}
+
+int rdd_dense_condition_number(rdd_ctx* h, int64_t rows, int64_t cols, const double* A, int cap, double* cond) {
+  return guarded(h, [&](Ctx& c) {
+    rdd::check_dense_cap(std::min(rows, cols), diag_cap(cap));
+    int m = 0, n = 0;
+    double* d = upload_dense(c, rows, cols, A, true, m, n);
+    std::vector<double> sv;
+    rdd::singular_values_dev(c, d, m, n, sv);
+    const double k = rdd::condition_from(sv);
+    if (cond) *cond = k;
+  });
+}
+
 int rdd_bench_jacobi(rdd_ctx* h, int n, int batch, int sweeps, double* ms) {
   return guarded(h, [&](Ctx& c) {
     if (n < 2 || batch < 1 || sweeps < 1) throw std::invalid_argument("bench_jacobi: n >= 2, batch >= 1, sweeps >= 1");

@@ -269,6 +269,14 @@ std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector
 void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc);
 std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int>& n,
                                   const std::vector<long long>& off, int iters);
+// diag.cu (§8f row 4: krylov.hpp:403-440 dense diagnostics)
+void check_dense_cap(long long n, int cap);
+void dense_eigenvalues_dev(Ctx& c, double* A, int n, std::vector<double>& wr, std::vector<double>& wi);
+void symmetric_eigenvalues_dev(Ctx& c, double* A, int n, std::vector<double>& ev);
+void singular_values_dev(Ctx& c, double* A, int m, int n, std::vector<double>& sv);
+double condition_from(const std::vector<double>& sv);
+void spectra(Ctx& c, int cap, std::vector<double>& nre, std::vector<double>& nim, std::vector<double>* pre,
+             std::vector<double>* pim, double* cond_n, double* cond_p);
 // jacobi.cu
 struct EigOpts {
   int absolute = 0;       // 1: |a_pq| > tol·max|a_ii| (backward stable); 0: |a_pq| > tol·sqrt|a_pp a_qq| (graded)

@@ -74,6 +74,10 @@ def lib():
         L.rdd_set_verbose.argtypes = [vp, C.c_int]
         L.rdd_bench_operator.argtypes = [vp, C.c_int, C.c_int, dp, dp]
         L.rdd_bench_jacobi.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp]
+        L.rdd_spectra.argtypes = [vp, C.c_int, dp, dp, dp, dp, dp, dp]
+        L.rdd_dense_spectrum.argtypes = [vp, i64, i64, dp, C.c_int, dp, dp]
+        L.rdd_dense_singular_values.argtypes = [vp, i64, i64, dp, C.c_int, dp]
+        L.rdd_dense_condition_number.argtypes = [vp, i64, i64, dp, C.c_int, dp]
         _lib = L
     return _lib
 
@@ -217,6 +221,51 @@ class Solver:
         ms = C.c_double()
         self._check(self.L.rdd_bench_jacobi(self.h, n, batch, sweeps, C.byref(ms)))
         return ms.value
+
+    # ---- dense diagnostics (krylov.hpp:403-440; runner.hpp:344-400)
+    K_DENSE_SPECTRUM_CAP = 4000  # krylov.hpp:404
+
+    def spectra(self, with_precond: bool = True, cap: int = 0):
+        """spectrum_cmd's two spectra and sweep_tau's two condition numbers (runner.hpp:344-393)
+        on the assembled system: (eig(HᵀH) ascending, eig(M⁻¹HᵀH) complex sorted by real part,
+        cond(HᵀH), cond(M⁻¹HᵀH)). The preconditioned parts need build_preconditioner first."""
+        p = int(self.geti("p")[0])
+        nre, nim = np.zeros(p), np.zeros(p)
+        pre, pim = np.zeros(p), np.zeros(p)
+        cn, cp = np.zeros(1), np.zeros(1)
+        wp = with_precond
+        self._check(self.L.rdd_spectra(self.h, cap, _dp(nre), _dp(nim), _dp(pre) if wp else None,
+                                       _dp(pim) if wp else None, _dp(cn), _dp(cp) if wp else None))
+        return (nre + 1j * nim, (pre + 1j * pim) if wp else None, float(cn[0]), float(cp[0]) if wp else None)
+
+    @staticmethod
+    def _fortran(a):
+        a = np.asarray(a, dtype=np.float64)
+        if a.ndim != 2:
+            raise ValueError("dense diagnostics: matrix must be 2-D")
+        return np.asfortranarray(a)
+
+    def spectrum(self, a, cap: int = 0) -> np.ndarray:
+        """krylov.hpp:413 spectrum: all eigenvalues, sorted by (real, imag)."""
+        a = self._fortran(a)
+        n = a.shape[0]
+        wr, wi = np.zeros(n), np.zeros(n)
+        self._check(self.L.rdd_dense_spectrum(self.h, a.shape[0], a.shape[1], _dp(a), cap, _dp(wr), _dp(wi)))
+        return wr + 1j * wi
+
+    def singular_values(self, a, cap: int = 0) -> np.ndarray:
+        """krylov.hpp:423 singular_values: non-increasing."""
+        a = self._fortran(a)
+        s = np.zeros(min(a.shape))
+        self._check(self.L.rdd_dense_singular_values(self.h, a.shape[0], a.shape[1], _dp(a), cap, _dp(s)))
+        return s
+
+    def condition_number(self, a, cap: int = 0) -> float:
+        """krylov.hpp:430 condition_number: σmax / smallest positive σ."""
+        a = self._fortran(a)
+        k = C.c_double()
+        self._check(self.L.rdd_dense_condition_number(self.h, a.shape[0], a.shape[1], _dp(a), cap, C.byref(k)))
+        return k.value
 
     def bench_operator(self, op_form: int, reps: int = 20):
         ms = C.c_double()

@@ -8,6 +8,7 @@ The artefacts are outputs of the reference's own Catch2 tests:
   proj/runner_out_sweep/sweep_tau.csv           test_runner.cpp:162-171
   proj/runner_out_spec/spectrum_*.csv           test_runner.cpp:139-160
   proj/schwarz_diag.csv                         test_schwarz.cpp:190-203
+  proj/runner_out/config_echo.ini               test_runner.cpp:91-125 (config.hpp:232-260)
 """
 import csv
 import json
@@ -38,6 +39,8 @@ def main():
     g["spectrum_normal"] = [float(r["real"]) for r in rows("runner_out_spec/spectrum_normal.csv")]
     g["spectrum_preconditioned"] = [float(r["real"]) for r in rows("runner_out_spec/spectrum_preconditioned.csv")]
     g["schwarz_diag"] = rows("schwarz_diag.csv")
+    # config.hpp:232-260 config_echo of test_runner.cpp's small_config (runner_out/config_echo.ini)
+    g["runner_config_echo"] = open(os.path.join(REF, "runner_out/config_echo.ini")).read()
     with open(OUT, "w") as f:
         json.dump(g, f, indent=0)
     print("wrote", OUT)

@@ -164,31 +164,41 @@ __device__ __forceinline__ bool make_refl(double p, double q, double r, Refl& o,
     return false;
   }
   p += s;
-  o.X = p / s;
-  o.Y = q / s;
-  o.Z = r / s;
-  o.Q = q / p;
-  o.R = r / p;
+  const double is = 1.0 / s, ip = 1.0 / p;
+  o.X = p * is;
+  o.Y = q * is;
+  o.Z = r * is;
+  o.Q = q * ip;
+  o.R = r * ip;
   o.on = 1;
   return true;
 }
 
-__global__ void __launch_bounds__(kQRT) k_hqr(double* __restrict__ A, int n, double* __restrict__ wr,
-                                              double* __restrict__ wi, int* __restrict__ status, int max_its) {
-  const long long ld = n;
+__global__ void __launch_bounds__(kQRT) k_hqr(double* __restrict__ Ag, long long ldg, int n, double* __restrict__ wr,
+                                              double* __restrict__ wi, int* __restrict__ status, int max_its,
+                                              int use_smem) {
+  // use_smem: the block is copied to shared memory first (small blocks; Ag is left untouched)
+  extern __shared__ double hsm[];
+  double* A = Ag;
+  long long ld = ldg;
+  if (use_smem) {
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) hsm[e] = Ag[(e % n) + (e / n) * ldg];
+    __syncthreads();
+    A = hsm;
+    ld = n;
+  }
 #define AA(i, j) A[(i) + static_cast<long long>(j) * ld]
   __shared__ double sh[32];
   __shared__ int shi[32];
   __shared__ Refl slot[2];
-  __shared__ double shx[3];
-  __shared__ int sh_m;
   const int tid = threadIdx.x;
-  const int nw = blockDim.x - 32, wid = tid - 32;  // workers: warps 1..
+  const int ws0 = blockDim.x > 32 ? 32 : 1;  // workers: warps 1.. (or lanes 1.. of a one-warp CTA)
+  const int nw = blockDim.x - ws0, wid = tid - ws0;
   // anorm = Σ |a_ij| over the Hessenberg part
   double s0 = 0.0;
   for (long long e = tid; e < static_cast<long long>(n) * n; e += blockDim.x) {
     const int i = static_cast<int>(e % n), j = static_cast<int>(e / n);
-    if (i <= j + 1) s0 += fabs(A[e]);
+    if (i <= j + 1) s0 += fabs(AA(i, j));
   }
   const double anorm = block_sum_d(s0, sh);
   int nn = n - 1;
@@ -321,7 +331,7 @@ __global__ void __launch_bounds__(kQRT) k_hqr(double* __restrict__ A, int n, dou
               o.on = 0;
             }
           }
-        } else if (tid >= 32 && R.on) {
+        } else if (tid >= ws0 && R.on) {
           // loads of kQU owned columns/rows are issued before any store (the stores may alias)
           for (int j0 = k + 3 + wid; j0 <= nn; j0 += kQU * nw) {  // row modification, columns k+3..nn
             double a0[kQU], a1[kQU], a2[kQU];
@@ -376,11 +386,281 @@ __global__ void __launch_bounds__(kQRT) k_hqr(double* __restrict__ A, int n, dou
         }
         __syncthreads();
       }
-      (void)shx;
-      (void)sh_m;
     }
   }
 #undef AA
+}
+
+// ---- windowed multi-bulge sweeps (small-bulge multishift QR) for large active blocks.
+// nb bulges, each carrying a shift pair from the trailing 2·nb×2·nb block's eigenvalues, are
+// introduced at the top of the active block [l, nn] three rows apart and chased to the bottom.
+// Steps of different bulges act on disjoint index triples, so at each "time" t every active
+// bulge moves one position (reflectors, then all row modifications, then all column
+// modifications). The chase runs in a kw×kw diagonal window held in shared memory; the window's
+// orthogonal transform U (product of the step reflectors) is applied afterwards to the rows to
+// its right (Uᵀ·panel) and the columns above it (panel·U) by separate multi-CTA kernels.
+constexpr int kMsKW = 112, kMsT = 512, kMsNB = 16;
+
+__global__ void k_hess_norm(const double* __restrict__ A, int n, double* __restrict__ out) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long e = threadIdx.x; e < static_cast<long long>(n) * n; e += blockDim.x) {
+    const int i = static_cast<int>(e % n), j = static_cast<int>(e / n);
+    if (i <= j + 1) s += fabs(A[e]);
+  }
+  s = block_sum_d(s, sh);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+// bottom deflation (hqr's l-scan, one and two roots) until the active block is at least 3 wide;
+// ctl = {nn, l} in and out
+__global__ void __launch_bounds__(256) k_deflate(double* __restrict__ A, int n, const double* __restrict__ anorm_p,
+                                                 int* __restrict__ ctl, double* __restrict__ wr, double* __restrict__ wi) {
+#define AA(i, j) A[(i) + static_cast<long long>(j) * n]
+  __shared__ int shi[32];
+  const double anorm = anorm_p[0];
+  int nn = ctl[0], l = 0;
+  while (nn >= 0) {
+    int lc = 0;
+    for (int q = 1 + threadIdx.x; q <= nn; q += blockDim.x) {
+      double s = fabs(AA(q - 1, q - 1)) + fabs(AA(q, q));
+      if (s == 0.0) s = anorm;
+      if (fabs(AA(q, q - 1)) + s == s) lc = max(lc, q);
+    }
+    l = block_max_i(lc, shi);
+    if (l >= 1 && threadIdx.x == 0) AA(l, l - 1) = 0.0;
+    __syncthreads();
+    if (l == nn) {
+      if (threadIdx.x == 0) {
+        wr[nn] = AA(nn, nn);
+        wi[nn] = 0.0;
+      }
+      --nn;
+    } else if (l == nn - 1) {
+      if (threadIdx.x == 0) {
+        double x = AA(nn, nn);
+        const double y = AA(nn - 1, nn - 1), w = AA(nn, nn - 1) * AA(nn - 1, nn);
+        const double p = 0.5 * (y - x), q = p * p + w, z = sqrt(fabs(q));
+        if (q >= 0.0) {
+          const double zz = p + copysign(z, p);
+          wr[nn - 1] = wr[nn] = x + zz;
+          if (zz != 0.0) wr[nn] = x - w / zz;
+          wi[nn - 1] = wi[nn] = 0.0;
+        } else {
+          wr[nn - 1] = wr[nn] = x + p;
+          wi[nn - 1] = -z;
+          wi[nn] = z;
+        }
+      }
+      nn -= 2;
+    } else {
+      break;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    ctl[0] = nn;
+    ctl[1] = nn >= 0 ? l : 0;
+  }
+#undef AA
+}
+
+// shift pairs (sum, product) from the ns eigenvalues of the trailing block: complex conjugate
+// pairs as they come, real shifts paired in order; exceptional sweeps spread ad hoc real shifts
+__global__ void k_ms_shifts(const double* __restrict__ sr, const double* __restrict__ si, int ns,
+                            const double* __restrict__ A, int n, int nn, int exceptional, double* __restrict__ td) {
+  if (threadIdx.x != 0) return;
+  int b = 0;
+  double pend = 0.0;
+  bool have = false;
+  if (exceptional) {
+    const double s = fabs(A[nn + static_cast<long long>(nn - 1) * n]) + fabs(A[(nn - 1) + static_cast<long long>(nn - 2) * n]);
+    const double h = A[nn + static_cast<long long>(nn) * n];
+    for (int q = 0; q < ns / 2; ++q) {
+      const double x = h + 0.75 * s * (1.0 + q / static_cast<double>(ns)), y = h - 0.4375 * s * (1.0 + q / static_cast<double>(ns));
+      td[2 * q] = x + y;
+      td[2 * q + 1] = x * y;
+    }
+    return;
+  }
+  for (int i = 0; i < ns && b < ns / 2; ++i) {
+    if (si[i] != 0.0 && i + 1 < ns) {
+      td[2 * b] = sr[i] + sr[i + 1];
+      td[2 * b + 1] = sr[i] * sr[i] + si[i] * si[i];
+      ++b;
+      ++i;
+    } else if (have) {
+      td[2 * b] = pend + sr[i];
+      td[2 * b + 1] = pend * sr[i];
+      ++b;
+      have = false;
+    } else {
+      pend = sr[i];
+      have = true;
+    }
+  }
+  for (; b < ns / 2; ++b) {  // odd leftovers: double real shift
+    td[2 * b] = 2.0 * pend;
+    td[2 * b + 1] = pend * pend;
+  }
+}
+
+// one window of a multi-bulge sweep: times [tA, tB), diagonal block [w0, w1) in shared memory
+__global__ void __launch_bounds__(kMsT) k_ms_window(double* __restrict__ A, int n, int l, int nn, int nb, int w0,
+                                                    int w1, int tA, int tB, const double* __restrict__ td,
+                                                    double* __restrict__ Ug) {
+  extern __shared__ double sm[];
+  const int kw = w1 - w0, ls = kw + 1;  // padded leading dimension: conflict-free row sweeps
+  double* Hs = sm;            // kw × kw, column-major
+  double* Us = sm + kw * ls;  // kw × kw
+  __shared__ Refl rf[kMsNB];
+  __shared__ int rk[kMsNB];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kw * kw; e += blockDim.x) {
+    const int i = e % kw, j = e / kw;
+    Hs[i + j * ls] = A[(w0 + i) + static_cast<long long>(w0 + j) * n];
+    Us[i + j * ls] = i == j ? 1.0 : 0.0;
+  }
+  __syncthreads();
+#define HS(i, j) Hs[((i) - w0) + ((j) - w0) * ls]
+  for (int t = tA; t < tB; ++t) {
+    // phase 1: reflectors of the active bulges
+    if (tid < nb) {
+      const int b = tid, k = l + t - 3 * b;
+      Refl& o = rf[b];
+      o.on = 0;
+      rk[b] = -1;
+      if (k >= l && k <= nn - 1) {
+        rk[b] = k;
+        const bool three = k + 1 != nn;
+        double p, q, r, s;
+        if (k == l) {  // first column of (H − s1)(H − s2) at rows l..l+2
+          const double tt = td[2 * b], dd = td[2 * b + 1];
+          const double h00 = HS(l, l), h10 = HS(l + 1, l), h01 = HS(l, l + 1), h11 = HS(l + 1, l + 1);
+          const double h21 = three ? HS(l + 2, l + 1) : 0.0;
+          p = h00 * (h00 - tt) + h01 * h10 + dd;
+          q = h10 * (h00 + h11 - tt);
+          r = h10 * h21;
+          const double x = fabs(p) + fabs(q) + fabs(r);
+          if (x != 0.0) {
+            const double ix = 1.0 / x;
+            p *= ix;
+            q *= ix;
+            r *= ix;
+            make_refl(p, q, r, o, s);
+          }
+        } else {
+          p = HS(k, k - 1);
+          q = HS(k + 1, k - 1);
+          r = three ? HS(k + 2, k - 1) : 0.0;
+          const double x = fabs(p) + fabs(q) + fabs(r);
+          if (x != 0.0) {
+            const double ix = 1.0 / x;
+            p *= ix;
+            q *= ix;
+            r *= ix;
+            if (make_refl(p, q, r, o, s)) {
+              HS(k, k - 1) = -s * x;
+              HS(k + 1, k - 1) = 0.0;
+              if (three) HS(k + 2, k - 1) = 0.0;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // phase 2: row modifications (rows k..k+2, window columns k..w1-1), all bulges at once
+    for (int e = tid; e < nb * kw; e += blockDim.x) {
+      const int b = e / kw, j = w0 + e % kw, k = rk[b];
+      if (k < 0 || j < k || !rf[b].on) continue;
+      const Refl& R = rf[b];
+      const bool three = k + 1 != nn;
+      const double a0 = HS(k, j), a1 = HS(k + 1, j);
+      double p = a0 + R.Q * a1;
+      if (three) {
+        const double a2 = HS(k + 2, j);
+        p += R.R * a2;
+        HS(k + 2, j) = a2 - p * R.Z;
+      }
+      HS(k + 1, j) = a1 - p * R.Y;
+      HS(k, j) = a0 - p * R.X;
+    }
+    __syncthreads();
+    // phase 3: column modifications (window rows w0..min(nn, k+3)) and U ← U·P, all bulges
+    for (int e = tid; e < nb * 2 * kw; e += blockDim.x) {
+      const int b = e / (2 * kw), q = e % (2 * kw), k = rk[b];
+      if (k < 0 || !rf[b].on) continue;
+      double* c0;
+      if (q < kw) {
+        if (w0 + q > min(nn, k + 3)) continue;
+        c0 = &HS(w0 + q, k);
+      } else {
+        c0 = Us + (q - kw) + (k - w0) * ls;
+      }
+      const Refl& R = rf[b];
+      const bool three = k + 1 != nn;
+      const double b0 = c0[0], b1 = c0[ls];
+      double p = R.X * b0 + R.Y * b1;
+      if (three) {
+        const double b2 = c0[2 * ls];
+        p += R.Z * b2;
+        c0[2 * ls] = b2 - p * R.R;
+      }
+      c0[ls] = b1 - p * R.Q;
+      c0[0] = b0 - p;
+    }
+    __syncthreads();
+  }
+#undef HS
+  for (int e = tid; e < kw * kw; e += blockDim.x) {
+    const int i = e % kw, j = e / kw;
+    A[(w0 + i) + static_cast<long long>(w0 + j) * n] = Hs[i + j * ls];
+    Ug[e] = Us[i + j * ls];
+  }
+}
+
+// H[w0:w1, c0:c1] ← Uᵀ·H[w0:w1, c0:c1]: CTA per 16-column chunk, in place
+__global__ void __launch_bounds__(256) k_ms_right(double* __restrict__ A, int n, int w0, int kw, int c0, int c1,
+                                                  const double* __restrict__ U) {
+  extern __shared__ double sm[];
+  const int ls = kw + 1;
+  double* Us = sm;             // kw × kw, padded
+  double* P = sm + kw * ls;    // kw × 16
+  const int j0 = c0 + blockIdx.x * 16, nc = min(16, c1 - j0);
+  for (int e = threadIdx.x; e < kw * kw; e += blockDim.x) Us[(e % kw) + (e / kw) * ls] = U[e];
+  for (int e = threadIdx.x; e < kw * nc; e += blockDim.x) P[e] = A[(w0 + e % kw) + static_cast<long long>(j0 + e / kw) * n];
+  __syncthreads();
+  for (int e = threadIdx.x; e < kw * nc; e += blockDim.x) {
+    const int i = e % kw, c = e / kw;
+    const double* u = Us + i * ls;  // column i of U
+    const double* pc = P + c * kw;
+    double s = 0.0;
+    for (int r = 0; r < kw; ++r) s += u[r] * pc[r];
+    A[(w0 + i) + static_cast<long long>(j0 + c) * n] = s;
+  }
+}
+
+// H[r0:r1, w0:w1] ← H[r0:r1, w0:w1]·U: CTA per 32-row chunk, in place
+__global__ void __launch_bounds__(256) k_ms_top(double* __restrict__ A, int n, int w0, int kw, int r0, int r1,
+                                                const double* __restrict__ U) {
+  extern __shared__ double sm[];
+  double* Us = sm;             // kw × kw
+  double* P = sm + kw * kw;    // 32 × kw (row chunk, column-major, ld 32)
+  const int i0 = r0 + blockIdx.x * 32, nr = min(32, r1 - i0);
+  for (int e = threadIdx.x; e < kw * kw; e += blockDim.x) Us[e] = U[e];
+  for (int e = threadIdx.x; e < 32 * kw; e += blockDim.x) {
+    const int i = e % 32, j = e / 32;
+    P[e] = i < nr ? A[(i0 + i) + static_cast<long long>(w0 + j) * n] : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * kw; e += blockDim.x) {
+    const int i = e % 32, j = e / 32;
+    if (i >= nr) continue;
+    const double* u = Us + j * kw;  // column j of U
+    double s = 0.0;
+    for (int r = 0; r < kw; ++r) s += P[i + r * 32] * u[r];
+    A[(i0 + i) + static_cast<long long>(w0 + j) * n] = s;
+  }
 }
 
 // eigenvalues of the symmetric tridiagonal (a, b) by Sturm-count bisection; thread per index.
@@ -535,18 +815,114 @@ void check_dense_cap(long long n, int cap) {  // krylov.hpp:405-409
                                 std::to_string(cap) + ")");
 }
 
+static void hqr_block(Ctx& c, double* A, long long ld, int nb, double* wr, double* wi, int* st, bool smem) {
+  const size_t sm = smem ? sizeof(double) * nb * nb : 0;
+  static bool attr = false;
+  if (!attr) {
+    RDD_CUDA(cudaFuncSetAttribute(k_hqr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(double) * kMsKW * kMsKW)));
+    attr = true;
+  }
+  k_hqr<<<1, smem ? 32 : kQRT, sm, c.stream>>>(A, ld, nb, wr, wi, st, 60, smem ? 1 : 0);
+  RDD_LAUNCH_CHECK();
+}
+
+// one multi-bulge sweep over the active block [l, nn] with nbul bulges (shift pairs in td)
+static void ms_sweep(Ctx& c, double* A, int n, int l, int nn, int nbul, const double* td, double* U) {
+  static bool attr = false;
+  if (!attr) {
+    RDD_CUDA(cudaFuncSetAttribute(k_ms_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(double) * 2 * kMsKW * (kMsKW + 1))));
+    RDD_CUDA(cudaFuncSetAttribute(k_ms_right, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(double) * (kMsKW * (kMsKW + 1) + kMsKW * 16))));
+    RDD_CUDA(cudaFuncSetAttribute(k_ms_top, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(double) * (kMsKW * kMsKW + 32 * kMsKW))));
+    attr = true;
+  }
+  const int S = 3 * (nbul - 1), T = (nn - l) + S, steps = kMsKW - S - 4;
+  for (int tA = 0; tA < T;) {
+    const int tB = std::min(T, tA + steps);
+    const int w0 = std::max(l, l + tA - S - 1), w1 = std::min(nn + 1, l + tB + 3), kw = w1 - w0;
+    k_ms_window<<<1, kMsT, sizeof(double) * 2 * kw * (kw + 1), c.stream>>>(A, n, l, nn, nbul, w0, w1, tA, tB, td, U);
+    RDD_LAUNCH_CHECK();
+    if (w1 <= nn) {
+      k_ms_right<<<ceil_div(nn + 1 - w1, 16), 256, sizeof(double) * (kw * (kw + 1) + kw * 16), c.stream>>>(
+          A, n, w0, kw, w1, nn + 1, U);
+      RDD_LAUNCH_CHECK();
+    }
+    if (w0 > l) {
+      k_ms_top<<<ceil_div(w0 - l, 32), 256, sizeof(double) * (kw * kw + 32 * kw), c.stream>>>(A, n, w0, kw, l, w0, U);
+      RDD_LAUNCH_CHECK();
+    }
+    tA = tB;
+    c.stats["diag_windows"].launches += 1;
+  }
+}
+
+// eigenvalues of an upper Hessenberg matrix (device, destroyed) into device wr/wi: bottom
+// deflation, single-bulge hqr on blocks up to kMsKW (shared memory), multi-bulge windowed sweeps
+// on larger active blocks with the trailing block's eigenvalues as shifts
+static void hessenberg_eigenvalues(Ctx& c, double* A, int n, double* wr, double* wi, int* st) {
+  const int ns = 2 * kMsNB;
+  double* anorm = c.ws("dg_anorm", 1);
+  double* sw = c.ws("dg_shift", 2 * ns + ns);  // shift eigenvalues, then (sum, product) pairs
+  double* U = c.ws("dg_U", kMsKW * kMsKW);
+  DBuf<int> ctl;
+  ctl.zero(4, c.stream);  // ctl[0..1] = (nn, l); ctl[2] = shift-block status
+  k_hess_norm<<<1, 1024, 0, c.stream>>>(A, n, anorm);
+  RDD_LAUNCH_CHECK();
+  int nn = n - 1, last_nn = n, stall = 0;
+  int h[2];
+  while (nn >= 0) {
+    RDD_CUDA(cudaMemcpyAsync(ctl.p, &nn, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    k_deflate<<<1, 256, 0, c.stream>>>(A, n, anorm, ctl.p, wr, wi);
+    RDD_LAUNCH_CHECK();
+    RDD_CUDA(cudaMemcpyAsync(h, ctl.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    nn = h[0];
+    const int l = h[1];
+    if (nn < 0) break;
+    const int size = nn - l + 1;
+    stall = nn < last_nn ? 0 : stall + 1;
+    last_nn = nn;
+    if (size <= kMsKW || stall >= 60) {  // small block (or no progress): single-bulge hqr on the block
+      ScopedKernelTimer tb(c, "diag_block");
+      hqr_block(c, A + l + static_cast<long long>(l) * n, n, size, wr + l, wi + l, st, size <= kMsKW);
+      nn = l - 1;
+      last_nn = n;
+      continue;
+    }
+    const long long b0 = static_cast<long long>(nn - ns + 1);
+    {
+      ScopedKernelTimer ts(c, "diag_shifts");
+      hqr_block(c, A + b0 + b0 * n, n, ns, sw, sw + ns, ctl.p + 2, true);
+    }
+    k_ms_shifts<<<1, 32, 0, c.stream>>>(sw, sw + ns, ns, A, n, nn, stall > 0 && stall % 10 == 0 ? 1 : 0, sw + 2 * ns);
+    RDD_LAUNCH_CHECK();
+    {
+      ScopedKernelTimer tw(c, "diag_sweep");
+      ms_sweep(c, A, n, l, nn, kMsNB, sw + 2 * ns, U);
+    }
+  }
+}
+
 // eigenvalues of a general square matrix (device, destroyed); host wr/wi sorted by (real, imag)
 void dense_eigenvalues_dev(Ctx& c, double* A, int n, std::vector<double>& wr, std::vector<double>& wi) {
   ScopedKernelTimer tk(c, "diag_eig");
   wr.assign(n, 0.0);
   wi.assign(n, 0.0);
   if (n == 0) return;
-  hessenberg(c, A, n);
+  {
+    ScopedKernelTimer th(c, "diag_hessenberg");
+    hessenberg(c, A, n);
+  }
   double* w = c.ws("dg_w", 2 * static_cast<size_t>(n));
   DBuf<int> st;
   st.zero(1, c.stream);
-  k_hqr<<<1, kQRT, 0, c.stream>>>(A, n, w, w + n, st.p, 60);
-  RDD_LAUNCH_CHECK();
+  {
+    ScopedKernelTimer tq(c, "diag_qr");
+    hessenberg_eigenvalues(c, A, n, w, w + n, st.p);
+  }
   int status = 0;
   RDD_CUDA(cudaMemcpyAsync(&status, st.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   RDD_CUDA(cudaMemcpyAsync(wr.data(), w, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));

@@ -28,7 +28,18 @@ for n in (1000, 2000, 4000):
     a = np.random.default_rng(n).standard_normal((n, n))
     for name, f in (("spectrum", s.spectrum), ("singular_values", s.singular_values)):
         f(a[:64, :64])
-        t = time.perf_counter(); f(a); dt = time.perf_counter() - t
-        out.append({"case": f"{name} n={n}", "gpu_s": dt})
+        t = time.perf_counter(); got = f(a); dt = time.perf_counter() - t
+        rec = {"case": f"{name} n={n}", "gpu_s": dt}
+        if n <= 2000:
+            t = time.perf_counter()
+            ref = np.linalg.eigvals(a) if name == "spectrum" else np.linalg.svd(a, compute_uv=False)
+            rec["numpy_s"] = time.perf_counter() - t
+            if name == "spectrum":
+                from scipy.optimize import linear_sum_assignment
+                D = np.abs(got[:, None] - ref[None, :]); r, cc = linear_sum_assignment(D)
+                rec["max_err_over_norm"] = float(D[r, cc].max() / np.linalg.norm(a, 2))
+            else:
+                rec["max_err_over_norm"] = float(np.max(np.abs(got - ref)) / ref[0])
+        out.append(rec)
 for r in out:
     print(json.dumps(r))

@@ -129,6 +129,28 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// sum over a 256-thread CTA in a fixed order (valid in thread 0)
+__device__ __forceinline__ double block_sum_256(double v) {
+  __shared__ double sh_b256[8];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) sh_b256[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < 8 ? sh_b256[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+  }
+  __syncthreads();
+  return t;
+}
+// Σ part[0..n) by one warp in a fixed order (lane-strided, then the xor tree): every lane of
+// every warp that calls it gets the identical value
+__device__ __forceinline__ double warp_sum_parts(const double* part, int n) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int i = lane; i < n; i += 32) s += part[i];
+  return warp_sum(s);
+}
 __device__ __forceinline__ int warp_min(int v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -231,16 +231,19 @@ void run_pca(Ctx& c);
 // equil.cu (K6) + matvec.cu (K9/K10)
 void column_norms_scale(Ctx& c, bool equilibrate);
 void matvec_dev(Ctx& c, const double* w, double* y);
-void matvec_t_dev(Ctx& c, const double* r, double* out);
+// dot_with/dot_part: per-CTA partials (ceil(p/256)) of dot_with·out, fused into the last kernel
+void matvec_t_dev(Ctx& c, const double* r, double* out, const double* dot_with = nullptr, double* dot_part = nullptr);
 // normal.cu (K7)
 void build_normal_blocks(Ctx& c);
 void normal_apply_dev(Ctx& c, const double* w, double* out);
 void normal_operator(Ctx& c, const double* w, double* out);  // runner.hpp:232-234
+bool normal_operator_dot(Ctx& c, const double* w, double* out, double* dot_part);
 bool build_fused_plan(Ctx& c);
 void fused_normal_apply_dev(Ctx& c, const double* w, double* out);
 // schwarz.cu (K8/K11)
 void build_schwarz(Ctx& c, int kind);
-void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose);
+// pzz/pzv: per-CTA partials (ceil(p/256)) of z·z and z·v, fused into the reduction kernel
+void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose, double* pzz = nullptr, double* pzv = nullptr);
 void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, const std::vector<long long>& off,
                    bool lower_only = false);
 void refresh_local_cond(Ctx& c);

@@ -46,11 +46,9 @@ __device__ __forceinline__ double block_sum(double v) {
   return t;  // valid in thread 0
 }
 
-__device__ __forceinline__ double sum_parts(const double* part) {
-  double s = 0.0;
-  for (int i = 0; i < kRB; ++i) s += part[i];
-  return s;
-}
+// partial sums are reduced by one warp in a fixed order (warp_sum_parts): deterministic, and
+// every warp that needs the scalar computes the identical value
+
 
 __global__ void k_dot_part(const double* __restrict__ x, const double* __restrict__ y, int n,
                            double* __restrict__ part) {
@@ -77,8 +75,9 @@ __global__ void k_dot2_part(const double* __restrict__ a, const double* __restri
 
 // CG setup after z = M b: z0 = ‖z‖, rz = r·z, p = z
 __global__ void k_cg_init(CgState* st, const double* __restrict__ pz, const double* __restrict__ prz,
-                          const double* __restrict__ pbb, double* hist, double* thist) {
-  const double zz = sum_parts(pz), rz = sum_parts(prz), bb = sum_parts(pbb);
+                          const double* __restrict__ pbb, double* hist, double* thist, int npz, int npb) {
+  const double zz = warp_sum_parts(pz, npz), rz = warp_sum_parts(prz, npz), bb = warp_sum_parts(pbb, npb);
+  if (threadIdx.x != 0) return;
   st->z0 = sqrt(zz);
   st->bnorm = sqrt(bb);
   st->rz = rz;
@@ -97,9 +96,9 @@ __global__ void k_cg_init(CgState* st, const double* __restrict__ pz, const doub
 // alpha = rz / pAp; breakdown check (krylov.hpp:132-135); x += αp; r -= αAp; partial ‖r‖²
 __global__ void k_cg_update(CgState* st, const double* __restrict__ ppap, double* __restrict__ x,
                             double* __restrict__ r, const double* __restrict__ p, const double* __restrict__ Ap, int n,
-                            double* __restrict__ prr, int* brk_flag) {
+                            double* __restrict__ prr, int* brk_flag, int npap) {
   if (st->status != ST_RUNNING) return;
-  const double pAp = sum_parts(ppap);
+  const double pAp = warp_sum_parts(ppap, npap);
   const double rz = st->rz;
   if (pAp <= 0.0 || rz == 0.0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *brk_flag = 1;
@@ -119,13 +118,14 @@ __global__ void k_cg_update(CgState* st, const double* __restrict__ ppap, double
 
 // rel = ‖z‖/‖z0‖, histories, convergence, beta (krylov.hpp:139-151)
 __global__ void k_cg_finish(CgState* st, const double* __restrict__ pzz, const double* __restrict__ prz,
-                            const double* __restrict__ prr, double* hist, double* thist, int* brk_flag) {
+                            const double* __restrict__ prr, double* hist, double* thist, int* brk_flag, int npz) {
   if (st->status != ST_RUNNING) return;
   if (*brk_flag) {
-    st->status = ST_BREAKDOWN;
+    if (threadIdx.x == 0) st->status = ST_BREAKDOWN;
     return;
   }
-  const double zz = sum_parts(pzz), rzn = sum_parts(prz), rr = sum_parts(prr);
+  const double zz = warp_sum_parts(pzz, npz), rzn = warp_sum_parts(prz, npz), rr = warp_sum_parts(prr, kRB);
+  if (threadIdx.x != 0) return;
   const double rel = sqrt(zz) / st->z0;
   const int it = st->it + 1;
   hist[it] = rel;
@@ -214,24 +214,33 @@ struct Vecs {
 }  // namespace
 
 // A(w) = Hᵀ(H w) (runner.hpp:232-234) or the block-sparse HᵀH
-void normal_operator(Ctx& c, const double* w, double* out) {
+void normal_operator(Ctx& c, const double* w, double* out) { normal_operator_dot(c, w, out, nullptr); }
+
+// the normal operator; with dot_part, also per-CTA partials (ceil(p/256)) of w·out when the
+// formulation produces them in its last kernel (returns whether it did)
+bool normal_operator_dot(Ctx& c, const double* w, double* out, double* dot_part) {
   if (c.cfg.op_form == RDD_OPERATOR_NORMAL && c.NB.p) {
     normal_apply_dev(c, w, out);
-  } else if (c.cfg.op_form == RDD_OPERATOR_FUSED && c.fused_ready) {
-    fused_normal_apply_dev(c, w, out);
-  } else {
-    matvec_dev(c, w, c.ytmp.ensure(c.N));
-    matvec_t_dev(c, c.ytmp.p, out);
+    return false;
   }
+  if (c.cfg.op_form == RDD_OPERATOR_FUSED && c.fused_ready) {
+    fused_normal_apply_dev(c, w, out);
+    return false;
+  }
+  matvec_dev(c, w, c.ytmp.ensure(c.N));
+  matvec_t_dev(c, c.ytmp.p, out, dot_part ? w : nullptr, dot_part);
+  return dot_part != nullptr;
 }
 
-static void precond(Ctx& c, const double* v, double* z) {
+// z = M v; with pzz/pzv, also per-CTA partials (ceil(p/256)) of z·z and z·v (returns whether)
+static bool precond(Ctx& c, const double* v, double* z, double* pzz = nullptr, double* pzv = nullptr) {
   if (c.pkind == RDD_PRECOND_NONE) {
     k_copy<<<kRB, kRT, 0, c.stream>>>(z, v, c.p);
     RDD_LAUNCH_CHECK();
-  } else {
-    precond_apply_dev(c, v, z, false);
+    return false;
   }
+  precond_apply_dev(c, v, z, false, pzz, pzv);
+  return pzz != nullptr;
 }
 
 static double dot_host(Ctx& c, const double* x, const double* y, int n, double* part) {
@@ -259,8 +268,9 @@ static void cg_solve(Ctx& c, const double* b, double* x, double tol, int max_ite
   double* z = r + n;
   double* pv = z + n;
   double* Ap = pv + n;
-  double* sc = c.scal.ensure(8 * kRB + 64);
-  double *P0 = sc, *P1 = sc + kRB, *P2 = sc + 2 * kRB, *P3 = sc + 3 * kRB, *P4 = sc + 4 * kRB;
+  const int ps = std::max(kRB, ceil_div(n, 256));  // partial slots: kRB dot CTAs or fused ceil(p/256)
+  double* sc = c.wsd["cg.part"].ensure(5 * static_cast<size_t>(ps));
+  double *P0 = sc, *P1 = sc + ps, *P2 = sc + 2 * ps, *P3 = sc + 3 * ps, *P4 = sc + 4 * ps;
   DBuf<CgState> st;
   DBuf<int> brk;
   DBuf<double> hist, thist;
@@ -275,23 +285,41 @@ static void cg_solve(Ctx& c, const double* b, double* x, double tol, int max_ite
   Vecs V{n, &c};
   V.fill(x, 0.0);
   V.copy(r, b);
-  precond(c, r, z);
-  k_dot2_part<<<kRB, kRT, 0, c.stream>>>(z, z, r, n, P0, P1);  // (z·z, z·r)
+  // dot partials: fused into the operator's / preconditioner's last kernel where they exist
+  // (ceil(p/256) partials), else the kRB-CTA dot kernels
+  const int npf = ceil_div(n, 256);
+  int npz = npf;
+  if (!precond(c, r, z, P0, P1)) {
+    k_dot2_part<<<kRB, kRT, 0, c.stream>>>(z, z, r, n, P0, P1);  // (z·z, z·r)
+    RDD_LAUNCH_CHECK();
+    npz = kRB;
+  }
   k_dot_part<<<kRB, kRT, 0, c.stream>>>(b, b, n, P2);
   RDD_LAUNCH_CHECK();
-  k_cg_init<<<1, 1, 0, c.stream>>>(st.p, P0, P1, P2, hist.p, thist.p);
+  k_cg_init<<<1, 32, 0, c.stream>>>(st.p, P0, P1, P2, hist.p, thist.p, npz, kRB);
   RDD_LAUNCH_CHECK();
   V.copy(pv, z);
 
   // one iteration = fixed launch sequence; capture once, replay in chunks with a device status
   auto iteration = [&]() {
-    normal_operator(c, pv, Ap);
-    k_dot_part<<<kRB, kRT, 0, c.stream>>>(pv, Ap, n, P0);
-    k_cg_update<<<kRB, kRT, 0, c.stream>>>(st.p, P0, x, r, pv, Ap, n, P4, brk.p);
-    precond(c, r, z);
-    k_dot2_part<<<kRB, kRT, 0, c.stream>>>(z, z, r, n, P2, P3);
-    k_cg_finish<<<1, 1, 0, c.stream>>>(st.p, P2, P3, P4, hist.p, thist.p, brk.p);
+    int npap = npf;
+    if (!normal_operator_dot(c, pv, Ap, P0)) {
+      k_dot_part<<<kRB, kRT, 0, c.stream>>>(pv, Ap, n, P0);
+      RDD_LAUNCH_CHECK();
+      npap = kRB;
+    }
+    k_cg_update<<<kRB, kRT, 0, c.stream>>>(st.p, P0, x, r, pv, Ap, n, P4, brk.p, npap);
+    RDD_LAUNCH_CHECK();
+    int npzz = npf;
+    if (!precond(c, r, z, P2, P3)) {
+      k_dot2_part<<<kRB, kRT, 0, c.stream>>>(z, z, r, n, P2, P3);
+      RDD_LAUNCH_CHECK();
+      npzz = kRB;
+    }
+    k_cg_finish<<<1, 32, 0, c.stream>>>(st.p, P2, P3, P4, hist.p, thist.p, brk.p, npzz);
+    RDD_LAUNCH_CHECK();
     k_cg_p<<<kRB, kRT, 0, c.stream>>>(st.p, pv, z, n);
+    RDD_LAUNCH_CHECK();
   };
   const int chunk = 8;
   c.ytmp.ensure(c.N);  // no allocations inside the capture

@@ -138,15 +138,23 @@ __global__ void __launch_bounds__(kMtWarps * 32) k_block_gemv_t(const double* __
 }
 
 // out[col] = Σ over the row chunks of its block (ascending) of the partials
-__global__ void k_chunk_sum(const double* __restrict__ part, const int* __restrict__ col_owner,
-                            const int* __restrict__ col_off, const int* __restrict__ blk_tile0,
-                            const int* __restrict__ part_off, int p, double* __restrict__ out) {
+// (optional) dw/dpart: per-CTA partial of dw·out (the CG's pᵀAp), fixed order
+__global__ void __launch_bounds__(256) k_chunk_sum(const double* __restrict__ part, const int* __restrict__ col_owner,
+                                                   const int* __restrict__ col_off, const int* __restrict__ blk_tile0,
+                                                   const int* __restrict__ part_off, int p, double* __restrict__ out,
+                                                   const double* __restrict__ dw, double* __restrict__ dpart) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= p) return;
-  const int j = col_owner[col], k = col - col_off[j];
   double s = 0.0;
-  for (int tt = blk_tile0[j]; tt < blk_tile0[j + 1]; ++tt) s += part[part_off[tt] + k];
-  out[col] = s;
+  if (col < p) {
+    const int j = col_owner[col], k = col - col_off[j];
+    for (int tt = blk_tile0[j]; tt < blk_tile0[j + 1]; ++tt) s += part[part_off[tt] + k];
+    out[col] = s;
+  }
+  if (dpart) {
+    double d = col < p ? dw[col] * s : 0.0;
+    d = block_sum_256(d);
+    if (threadIdx.x == 0) dpart[blockIdx.x] = d;
+  }
 }
 
 }  // namespace
@@ -206,14 +214,14 @@ void matvec_dev(Ctx& c, const double* w, double* y) {
   RDD_LAUNCH_CHECK();
 }
 
-void matvec_t_dev(Ctx& c, const double* r, double* out) {
+void matvec_t_dev(Ctx& c, const double* r, double* out, const double* dot_with, double* dot_part) {
   ScopedKernelTimer tk(c, "matvec_t");
   if (c.mt_ntiles == 0) return;
   k_block_gemv_t<<<c.mt_ntiles, kMtWarps * 32, 0, c.stream>>>(c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p,
                                                               c.mt_tiles.p, c.mt_part_off.p, r, c.mt_part.p);
   RDD_LAUNCH_CHECK();
   k_chunk_sum<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.mt_part.p, c.downer.p, c.dcol_off.p, c.mt_blk_tile0.p,
-                                                        c.mt_part_off.p, c.p, out);
+                                                        c.mt_part_off.p, c.p, out, dot_with, dot_part);
   RDD_LAUNCH_CHECK();
 }
 

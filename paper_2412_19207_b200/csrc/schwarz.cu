@@ -100,22 +100,35 @@ __global__ void k_local_scale(double* __restrict__ V, const double* __restrict__
 
 // out[col] = Σ_i weight · z_i[pos]  over the ≤3^d subdomains whose S_i contains col
 // z2 (optional): a second partial of every local result (split local applies), added first
-__global__ void k_reduce(const double* __restrict__ z, const double* __restrict__ z2, const int* __restrict__ gat_ptr,
-                         const int* __restrict__ gat_pos, const int* __restrict__ gat_owner_pos,
-                         const int* __restrict__ mult, int p, int kind, int transpose, double* __restrict__ out) {
+// (optional) v/pzz/pzv: per-CTA partials of out·out and out·v (the CG's ‖z‖², z·r), fixed order
+__global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ z, const double* __restrict__ z2,
+                                                const int* __restrict__ gat_ptr, const int* __restrict__ gat_pos,
+                                                const int* __restrict__ gat_owner_pos, const int* __restrict__ mult,
+                                                int p, int kind, int transpose, double* __restrict__ out,
+                                                const double* __restrict__ v, double* __restrict__ pzz,
+                                                double* __restrict__ pzv) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= p) return;
   double s = 0.0;
-  if (!transpose && kind == RDD_PRECOND_RAS) {
-    const int q = gat_owner_pos[col];
-    s = z2 ? z[q] + z2[q] : z[q];
-  } else {
-    for (int q = gat_ptr[col]; q < gat_ptr[col + 1]; ++q) {
-      const double zz = z2 ? z[gat_pos[q]] + z2[gat_pos[q]] : z[gat_pos[q]];
-      s += (!transpose && kind == RDD_PRECOND_SAS) ? zz / mult[col] : zz;
+  if (col < p) {
+    if (!transpose && kind == RDD_PRECOND_RAS) {
+      const int q = gat_owner_pos[col];
+      s = z2 ? z[q] + z2[q] : z[q];
+    } else {
+      for (int q = gat_ptr[col]; q < gat_ptr[col + 1]; ++q) {
+        const double zz = z2 ? z[gat_pos[q]] + z2[gat_pos[q]] : z[gat_pos[q]];
+        s += (!transpose && kind == RDD_PRECOND_SAS) ? zz / mult[col] : zz;
+      }
+    }
+    out[col] = s;
+  }
+  if (pzz) {
+    const double a = block_sum_256(s * s);
+    const double b = block_sum_256(col < p ? s * v[col] : 0.0);
+    if (threadIdx.x == 0) {
+      pzz[blockIdx.x] = a;
+      pzv[blockIdx.x] = b;
     }
   }
-  out[col] = s;
 }
 
 
@@ -463,12 +476,12 @@ void build_schwarz(Ctx& c, int kind) {
   c.nmax_local = *std::max_element(n.begin(), n.end());
 }
 
-void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose) {
+void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose, double* pzz, double* pzv) {
   ScopedKernelTimer tk(c, "precond_apply");
   chol_apply(c, v, transpose, c.zloc.p);
   const double* z2 = c.inv_mode ? c.zloc.p + c.set_idx.size() : nullptr;  // second half-partials
   k_reduce<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.zloc.p, z2, c.gat_ptr.p, c.gat_pos.p, c.gat_owner_pos.p, c.dmult.p,
-                                                     c.p, c.pkind, transpose ? 1 : 0, z);
+                                                     c.p, c.pkind, transpose ? 1 : 0, z, v, pzz, pzv);
   RDD_LAUNCH_CHECK();
 }
 

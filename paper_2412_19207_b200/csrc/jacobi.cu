@@ -343,9 +343,9 @@ __device__ __forceinline__ void unit_update(double* c0p, P1 c1p, bool w2, double
   }
 }
 
-constexpr int kJT = 1024;  // threads per CTA
-template <int K>
-__global__ void __launch_bounds__(kJT, 1) k_jacobi_oe(const double* __restrict__ Ain, double* __restrict__ ev,
+constexpr int kJT = 1024;  // threads per CTA (kJT/2 with two CTAs per SM for small batched blocks)
+template <int K, int NT = kJT>
+__global__ void __launch_bounds__(NT, kJT / NT) k_jacobi_oe(const double* __restrict__ Ain, double* __restrict__ ev,
                                                    const int* __restrict__ nvec, const long long* __restrict__ off,
                                                    const long long* __restrict__ ev_off, int max_sweeps, Crit crit_in,
                                                    double floor_rel, double conv_rel, int* __restrict__ sweeps_out,
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kJT, 1) k_jacobi_oe(const double* __restrict__
   __shared__ int cbeg, cend;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = kJT / 32;
+  constexpr int NW = NT / 32;
   if (tid == 0) {  // even-aligned whole-column ranges of ~chunk elements; columns padded to even length
     int cur = 0, start = 0, e = 0;
     cbeg = (rank == 0) ? 0 : ne;
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kJT, 1) k_jacobi_oe(const double* __restrict__
     active[0] = active[1] = 0;
   }
   __syncthreads();
-  for (int j = tid; j < ne; j += kJT) {
+  for (int j = tid; j < ne; j += NT) {
     double* basep = smem;
     if constexpr (K > 1) basep = cg::this_cluster().map_shared_rank(smem, static_cast<int>(own[j]));
     colp[j] = basep + lcol[j];
@@ -410,8 +410,8 @@ __global__ void __launch_bounds__(kJT, 1) k_jacobi_oe(const double* __restrict__
     for (int i = lane; i <= j; i += 32)
       smem[lcol[j] + i] = (i < n && j < n) ? A[i + static_cast<long long>(j) * n] : 0.0;
   // step-0 tables (even pairs (2k, 2k+1)) straight from global memory, in every CTA
-  for (int i = tid; i < ne; i += kJT) dg[i] = i < n ? A[i + static_cast<long long>(i) * n] : 0.0;
-  for (int k = tid; k < np; k += kJT) {
+  for (int i = tid; i < ne; i += NT) dg[i] = i < n ? A[i + static_cast<long long>(i) * n] : 0.0;
+  for (int k = tid; k < np; k += NT) {
     const int p = 2 * k, q = p + 1;
     od[k] = q < n ? A[p + static_cast<long long>(q) * n] : 0.0;
   }
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(kJT, 1) k_jacobi_oe(const double* __restrict__
       const double* odi = od + bi * (nemax / 2);
       const int npair = o ? np - 1 : np;
       // decide every pair of this step from the local tables
-      for (int k = tid; k < npair; k += kJT) {
+      for (int k = tid; k < npair; k += NT) {
         const int p = o + 2 * k, q = p + 1;
         const double app = dgi[p], aqq = dgi[q], apq = odi[k];
         double c = 1.0, sv = 0.0;
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kJT, 1) k_jacobi_oe(const double* __restrict__
   }
   if (rank == 0) {
     const double* dgf = dg + static_cast<int>(t_glob & 1) * nemax;
-    for (int i = tid; i < ne; i += kJT) ev[ev_off[b] + i] = dgf[i];
+    for (int i = tid; i < ne; i += NT) ev[ev_off[b] + i] = dgf[i];
     if (tid == 0) sweeps_out[b] = sweep;
   }
   if constexpr (K > 1) cg::this_cluster().sync();  // keep shared memory alive for remote writers
@@ -825,7 +825,10 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     const size_t smem = oe_smem(ne, K);
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(B * K);
-    lc.blockDim = dim3(kJT);
+    // small single-CTA blocks in batches larger than the SM count: two 512-thread CTAs per SM keep
+    // the whole batch resident (no partial second wave) and overlap one CTA's barrier waits
+    const bool half = K == 1 && B > c.prop.multiProcessorCount && 2 * smem + 2048 <= kCtaSmem + 1024;
+    lc.blockDim = dim3(half ? kJT / 2 : kJT);
     lc.dynamicSmemBytes = smem;
     lc.stream = c.stream;
     cudaLaunchAttribute at[1];
@@ -843,7 +846,8 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
                                   static_cast<const long long*>(droff.p), chunk, ne, oe_items(ne), exper));
       ++launch_counter();
     };
-    if (K == 1) launch(k_jacobi_oe<1>);
+    if (K == 1 && half) launch(k_jacobi_oe<1, kJT / 2>);
+    else if (K == 1) launch(k_jacobi_oe<1>);
     else if (K == 2) launch(k_jacobi_oe<2>);
     else if (K == 4) launch(k_jacobi_oe<4>);
     else launch(k_jacobi_oe<8>);

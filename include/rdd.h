@@ -91,6 +91,7 @@ typedef struct rdd_config {
   int gmres_restart;/* 0 = full                                        */
   int op_form;      /* RDD_OPERATOR_* (product only; oracle ignores)   */
   int true_residual;/* GMRES: diagnostic true residual each step (krylov.hpp:360-367); 1 = as reference */
+  int ref_resolution;/* example2 Crank-Nicolson reference grid (config.hpp:28); 0 = 2001    */
 } rdd_config;
 
 /* Mirrors rannddm::RunSummary (runner.hpp:147-156) + device phase split. */

@@ -1563,7 +1563,8 @@ static void evaluate(Oracle& o, const std::vector<int>& test_res) {
     for (int i = 0; i < M; ++i)
       for (int c = 0; c < C; ++c) o.exact(i, c) = o.prob.exact(c, o.test_pts[i]);
   } else {
-    if (!o.refgrid) o.refgrid = std::make_unique<RefGrid>(reference_example2(2001));
+    const int res = o.cfg.ref_resolution > 0 ? o.cfg.ref_resolution : 2001;  // config.hpp:28
+    if (!o.refgrid || o.refgrid->nx != res) o.refgrid = std::make_unique<RefGrid>(reference_example2(res));
     for (int i = 0; i < M; ++i) o.exact(i, 0) = o.refgrid->at(o.test_pts[i][0], o.test_pts[i][1]);
   }
   double dn = 0.0, num = 0.0, mean = 0.0, l1 = 0.0;

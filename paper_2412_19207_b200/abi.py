@@ -48,6 +48,7 @@ class Config(C.Structure):
         ("gmres_restart", C.c_int),
         ("op_form", C.c_int),
         ("true_residual", C.c_int),
+        ("ref_resolution", C.c_int),
     ]
 
     @property
@@ -65,7 +66,7 @@ class Config(C.Structure):
             "pca_matrix": self.pca_matrix, "solver": SOLVER_NAMES[self.solver],
             "precond": PRECOND_NAMES[self.precond], "rel_tol": self.rel_tol,
             "max_iter": self.max_iter, "gmres_restart": self.gmres_restart,
-            "op_form": self.op_form, "true_residual": self.true_residual,
+            "op_form": self.op_form, "true_residual": self.true_residual, "ref_resolution": self.ref_resolution,
         }
 
 
@@ -89,7 +90,7 @@ def make_config(problem: int, counts, m: int, colloc, *, n: int = 2, dim: int = 
                 tau: float = 0.0, pca_matrix: int = PCA_OP_APPLIED, solver: int = SOLVER_GMRES,
                 precond: int = PRECOND_AS, rel_tol: float = 1e-5, max_iter: int = 0,
                 gmres_restart: int = 0, op_form: int = OPERATOR_TWO_PASS,
-                true_residual: int = 1) -> Config:
+                true_residual: int = 1, ref_resolution: int = 0) -> Config:
     """Build a Config; defaults follow RunConfig (config.hpp:23-68)."""
     c = Config()
     c.problem = problem
@@ -117,4 +118,5 @@ def make_config(problem: int, counts, m: int, colloc, *, n: int = 2, dim: int = 
     c.gmres_restart = gmres_restart
     c.op_form = op_form
     c.true_residual = true_residual
+    c.ref_resolution = ref_resolution
     return c

@@ -174,6 +174,8 @@ struct Ctx {
 
   // ---- evaluation
   std::vector<double> approx, exact;  // M x C (host copies)
+  DBuf<double> ref2;                  // example2 reference field (res x res, level-major)
+  int ref2_res = 0;
   rdd_summary sum{};
 
   // ---- instrumentation
@@ -219,6 +221,7 @@ struct ScopedKernelTimer {
 // ---- module entry points (one per reference function family) -----------------------
 // host_setup.cpp
 void setup_problem(Ctx& c, const rdd_config& cfg, uint64_t seed);  // problems + geometry + bases + points
+void reference_example2_grid(int res, std::vector<double>& v);     // problems.hpp:219-264
 void upload_inputs(Ctx& c);
 // index.cu (K1)
 void build_index(Ctx& c);

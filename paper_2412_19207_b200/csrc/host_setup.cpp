@@ -104,6 +104,37 @@ bool interiors_intersect(const Ctx& c, int i, int j) {  // geometry.hpp:99-105
 
 }  // namespace
 
+// problems.hpp:219-264 reference_example2: space-time Crank-Nicolson field of example2 on a
+// res x res grid (level-major), Thomas elimination with the constant coefficients factored once.
+// Host-side like the reference (it is the error yardstick, not part of the solve), same operation
+// order so the device's bilinear lookups see the identical field.
+void reference_example2_grid(int res, std::vector<double>& v) {
+  if (res < 501) throw std::invalid_argument("reference_example2: resolution must be >= 501");
+  const int nx = res, nt = res, ni = nx - 2;
+  const double h = 2.0 / static_cast<double>(nx - 1), dt = 1.0 / static_cast<double>(nt - 1);
+  const double kappa = 0.1 / kPi;
+  const double a = kappa * dt / (2.0 * h * h), c = dt / (4.0 * h);
+  v.assign(static_cast<size_t>(nx) * nt, 0.0);
+  for (int i = 0; i < nx; ++i) v[i] = -std::sin(kPi * (-1.0 + i * h));
+  v[0] = 0.0;
+  v[nx - 1] = 0.0;
+  const double lo = -(a + c), di = 1.0 + 2.0 * a, up = -(a - c);
+  std::vector<double> cp(ni), rhs(ni), dp(ni);
+  cp[0] = up / di;
+  for (int i = 1; i < ni; ++i) cp[i] = up / (di - lo * cp[i - 1]);
+  for (int step = 1; step < nt; ++step) {
+    const double* prev = v.data() + static_cast<size_t>(step - 1) * nx;
+    double* next = v.data() + static_cast<size_t>(step) * nx;
+    for (int i = 0; i < ni; ++i) rhs[i] = (a + c) * prev[i] + (1.0 - 2.0 * a) * prev[i + 1] + (a - c) * prev[i + 2];
+    dp[0] = rhs[0] / di;
+    for (int i = 1; i < ni; ++i) dp[i] = (rhs[i] - lo * dp[i - 1]) / (di - lo * cp[i - 1]);
+    next[ni] = dp[ni - 1];
+    for (int i = ni - 2; i >= 0; --i) next[i + 1] = dp[i] - cp[i] * next[i + 2];
+    next[0] = 0.0;
+    next[nx - 1] = 0.0;
+  }
+}
+
 void setup_problem(Ctx& c, const rdd_config& cfg, uint64_t seed) {
   c.cfg = cfg;
   c.seed = seed;

@@ -273,7 +273,27 @@ struct EvalArgs {
   const double* U;        // J x m x C effective output weights u_j = V_j W_j
   double* approx;         // M x C
   double* exact;
+  const double* ref;      // example2: reference field (refn x refn), else null
+  int refn;
 };
+
+// problems.hpp:203-216 ReferenceGrid::at: bilinear lookup in the space-time field
+__device__ double ref_at(const double* v, int n, double x, double t) {
+  const double h = 2.0 / static_cast<double>(n - 1);
+  const double dt = 1.0 / static_cast<double>(n - 1);
+  const double fx = (x + 1.0) / h, ft = t / dt;
+  int ix = static_cast<int>(floor(fx)), it = static_cast<int>(floor(ft));
+  ix = min(max(ix, 0), n - 2);
+  it = min(max(it, 0), n - 2);
+  const double ax = fx - ix, at_ = ft - it;
+  const double v00 = v[static_cast<size_t>(it) * n + ix], v01 = v[static_cast<size_t>(it) * n + ix + 1];
+  const double v10 = v[static_cast<size_t>(it + 1) * n + ix], v11 = v[static_cast<size_t>(it + 1) * n + ix + 1];
+  // unfused products and sums (the reference's host arithmetic): bit-identical field values
+  const double bx = 1.0 - ax, bt = 1.0 - at_;
+  const double r0 = __dadd_rn(__dmul_rn(bx, v00), __dmul_rn(ax, v01));
+  const double r1 = __dadd_rn(__dmul_rn(bx, v10), __dmul_rn(ax, v11));
+  return __dadd_rn(__dmul_rn(bt, r0), __dmul_rn(at_, r1));
+}
 
 __device__ __forceinline__ double raw_wv(const EvalArgs& A, int k, const double* x) {
   const double* bx = A.box + 16 * static_cast<size_t>(k);
@@ -298,7 +318,8 @@ __global__ void k_evaluate(EvalArgs A) {
   for (int a = d - 1; a >= 0; --a) {  // last axis fastest (geometry.hpp:216-230)
     const int k = rem % A.res[a];
     rem /= A.res[a];
-    x[a] = A.lo[a] + (static_cast<double>(k) + 0.5) * A.step[a];
+    // unfused, as uniform_grid computes it on the host: bit-identical test points
+    x[a] = __dadd_rn(A.lo[a], __dmul_rn(static_cast<double>(k) + 0.5, A.step[a]));
   }
   const double Lv = L_jet(A.P, x).c[0];
   double acc[3] = {0.0, 0.0, 0.0};
@@ -322,7 +343,7 @@ __global__ void k_evaluate(EvalArgs A) {
   }
   for (int cc = 0; cc < A.P.C; ++cc) {
     A.approx[static_cast<size_t>(cc) * A.M + i] = acc[cc] + G_value(A.P, x, cc);
-    A.exact[static_cast<size_t>(cc) * A.M + i] = exact_value(A.P, x, cc);
+    A.exact[static_cast<size_t>(cc) * A.M + i] = A.ref ? ref_at(A.ref, A.refn, x[0], x[1]) : exact_value(A.P, x, cc);
   }
 }
 
@@ -349,9 +370,19 @@ __global__ void k_effective_weights(const double* __restrict__ Vred, const doubl
 
 void evaluate(Ctx& c, const int* test_res) {
   ScopedKernelTimer tk(c, "evaluate");
-  if (!c.prob.has_exact)
-    throw std::invalid_argument("evaluation of problems without a closed form (example2) is not on the device path");
   EvalArgs A{};
+  if (!c.prob.has_exact) {  // example2: errors against the Crank-Nicolson field (runner.hpp:286-289)
+    const int res = c.cfg.ref_resolution > 0 ? c.cfg.ref_resolution : 2001;
+    if (c.ref2_res != res) {
+      std::vector<double> v;
+      reference_example2_grid(res, v);
+      c.ref2.upload(v, c.stream);
+      RDD_CUDA(cudaStreamSynchronize(c.stream));  // v is pageable and scoped
+      c.ref2_res = res;
+    }
+    A.ref = c.ref2.p;
+    A.refn = res;
+  }
   A.P.id = c.prob.id;
   A.P.d = c.d;
   A.P.C = c.C;

@@ -80,7 +80,7 @@ class RunConfig:
             tau_mode=A.TAU_ABSOLUTE if self.tau_on else A.TAU_OFF, tau=self.tau,
             pca_matrix=A.PCA_OP_APPLIED if self.pca_matrix == "operator" else A.PCA_PSI,
             solver=_SOLVERS[self.solver], precond=_PRECOND_ID[self.preconditioner], rel_tol=self.rel_tol,
-            max_iter=self.max_iter, gmres_restart=self.gmres_restart)
+            max_iter=self.max_iter, gmres_restart=self.gmres_restart, ref_resolution=self.ref_resolution)
 
 
 def _g(v: float, prec: int) -> str:

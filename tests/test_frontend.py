@@ -88,9 +88,13 @@ def test_device_config_mapping():
     cfg = F.parse_config_text(small_config("out"))
     got = cfg.to_abi(77)
     want = configs.golden_runner(77)
+    assert got.ref_resolution == 2001  # config.hpp:28 default, carried to the device
+    want.ref_resolution = 2001
     assert bytes(got) == bytes(want)
     sweep = F.parse_config_text(small_config("out") + "[basis]\nm = 12\n[pca]\ntau = 0.01\n")
-    assert bytes(sweep.to_abi(78)) == bytes(configs.golden_sweep(1e-2, 78))
+    want = configs.golden_sweep(1e-2, 78)
+    want.ref_resolution = 2001
+    assert bytes(sweep.to_abi(78)) == bytes(want)
     assert sweep.to_abi().seed == 77
 
 

@@ -30,6 +30,11 @@ def _cases():
     ex3 = A.make_config(A.PROBLEM_EXAMPLE3, [2, 2, 2], 12, [6, 6, 6], seed=5, test=[10, 10, 10],
                         solver=A.SOLVER_CG, precond=A.PRECOND_AS, rel_tol=1e-10)
     c["example3"] = ex3
+    # example2 (advection-diffusion space-time, no closed form): errors against the
+    # Crank-Nicolson reference field (problems.hpp:195-264), reduced resolution to keep it quick
+    c["example2"] = A.make_config(A.PROBLEM_EXAMPLE2, [2, 2], 24, [16, 16], seed=5, test=[30, 30],
+                                  tau_mode=A.TAU_RELATIVE, tau=1e-6, pca_matrix=A.PCA_OP_APPLIED,
+                                  solver=A.SOLVER_GMRES, precond=A.PRECOND_AS, rel_tol=1e-10, ref_resolution=801)
     # 223 < m takes the cluster (distributed shared memory) Jacobi path in the PCA: K=2 and K=4
     big = A.make_config(A.PROBLEM_EXAMPLE1, [2, 2], 240, [40, 40], n=2, seed=9, test=[40, 40],
                         tau_mode=A.TAU_RELATIVE, tau=1e-6, pca_matrix=A.PCA_OP_APPLIED,
@@ -246,3 +251,19 @@ def test_operator_forms(dev, orc, name, op_form):
     nd = dev.normal_apply(w)
     tol = 1e-11 if cfg.tau_mode == A.TAU_OFF else 1e-6
     assert np.linalg.norm(nd - no) <= tol * np.linalg.norm(no), (name, op_form)
+
+
+def test_example2_reference_field(dev, orc):
+    # the exact values of example2 come from the reference's Crank-Nicolson field and its
+    # bilinear lookup (problems.hpp:198-264): identical arithmetic on both sides
+    cfg = CASES["example2"]
+    sd = dev.run_single(cfg)
+    so = orc.run_single(cfg)
+    ed, eo = dev.getd("exact"), orc.getd("exact")
+    assert ed.shape == eo.shape == (900,)
+    assert np.array_equal(ed, eo)
+    assert sd["e_l2"] == pytest.approx(so["e_l2"], rel=1e-6)
+    bad = A.Config.from_buffer_copy(cfg)
+    bad.ref_resolution = 100
+    with pytest.raises(ValueError, match="resolution must be >= 501"):
+        dev.run_single(bad)

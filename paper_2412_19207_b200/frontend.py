@@ -294,6 +294,16 @@ def run(cfg: RunConfig, solver=None) -> list:
     return rows
 
 
+def write_local_diagnostics_csv(path: str, solver) -> None:
+    """schwarz.hpp:217-225: per-subdomain set size, local rank and condition estimate of the
+    preconditioner built on the device context (default stream precision)."""
+    ranks, conds = solver.geti("local_rank"), solver.getd("local_cond")
+    with open(path, "w") as f:
+        f.write("subdomain,size,rank,cond_estimate\n")
+        for i, (r, k) in enumerate(zip(ranks, conds)):
+            f.write(f"{i},{len(solver.geti('set', i))},{int(r)},{_g(float(k), 6)}\n")
+
+
 def _precond_kind(cfg: RunConfig) -> int:
     return _PRECOND_ID[cfg.preconditioner or "AS"]  # value_or(AS), runner.hpp:354/385
 

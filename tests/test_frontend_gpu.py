@@ -104,3 +104,21 @@ def test_scaling_cmd_golden(dev, golden, tmp_path):
     assert float(got[0]["e_l1n"]) == pytest.approx(float(ref_as["e_l1n"]), rel=1e-6)
     # unpreconditioned GMRES(30) on cond ~1e10: iteration count within 5%
     assert abs(float(got[1]["iter"]) - float(ref_none["iter"])) <= 0.05 * float(ref_none["iter"])
+
+
+def test_local_diagnostics_csv_golden(dev, golden, tmp_path):
+    # test_schwarz.cpp:190-203: build_setup({2,2}, 6, 12, 61), AS, schwarz_diag.csv
+    from paper_2412_19207_b200 import abi as A
+    from paper_2412_19207_b200 import configs
+    dev.build_instance(configs.golden_schwarz_diag())
+    dev.assemble(False)
+    dev.build_preconditioner(A.PRECOND_AS)
+    path = str(tmp_path / "schwarz_diag.csv")
+    F.write_local_diagnostics_csv(path, dev)
+    got = _rows(path)
+    with open(path) as f:
+        assert f.readline().strip() == "subdomain,size,rank,cond_estimate"
+    assert len(got) == len(golden["schwarz_diag"]) == 4
+    for g, ref in zip(got, golden["schwarz_diag"]):
+        assert g["subdomain"] == ref["subdomain"] and g["size"] == ref["size"] and g["rank"] == ref["rank"]
+        assert float(g["cond_estimate"]) == pytest.approx(float(ref["cond_estimate"]), rel=1e-5)

@@ -274,7 +274,7 @@ def run_device(args, cfg, world, rank, local, dist):
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": ("normal operator Hᵀ(H·w), single pass: k_fused_normal + k_fused_reduce" if op_form == A.OPERATOR_FUSED else "normal operator Hᵀ(H·w): k_block_gemv + k_cover_sum + k_block_gemv_t"),
+                         "kernel": ("normal operator Hᵀ(H·w), single pass: k_fused_normal + k_fused_reduce" if op_form == A.OPERATOR_FUSED else "normal operator Hᵀ(H·w): k_block_gemv + k_block_gemv_t (y = H·w formed in its staging) + k_chunk_sum"),
                          "bytes_per_call": op_bytes, "ms_per_call": op_ms},
             "clocks": clk,
         }

@@ -158,6 +158,8 @@ struct Ctx {
   DBuf<int2> mv_tiles, mt_tiles;      // (block, first row) / (block, first column) tiles of H·w / Hᵀ·r
   int mv_ntiles = 0, mt_ntiles = 0, mv_rmax = 0;
   DBuf<double> zrows;                 // per-block partial H_j·w_j (row_ptr layout)
+  DBuf<int> ent_flat;                 // per (block, local row): flat z indices of the point's covers (-1 pad)
+  int ent_w = 0;                      // its width (4 or 8; 0 = not built)
   DBuf<int> mt_part_off, mt_blk_tile0;  // Hᵀ·r row-chunk partials: offset per tile, first tile per block
   DBuf<double> mt_part;
   DBuf<GemmTask> wsg;                 // device-generated GEMM task lists
@@ -241,6 +243,7 @@ void build_normal_blocks(Ctx& c);
 void normal_apply_dev(Ctx& c, const double* w, double* out);
 void normal_operator(Ctx& c, const double* w, double* out);  // runner.hpp:232-234
 bool normal_operator_dot(Ctx& c, const double* w, double* out, double* dot_part);
+void normal_two_pass_dev(Ctx& c, const double* w, double* out, double* dot_part);
 bool build_fused_plan(Ctx& c);
 void fused_normal_apply_dev(Ctx& c, const double* w, double* out);
 // schwarz.cu (K8/K11)

@@ -227,8 +227,7 @@ bool normal_operator_dot(Ctx& c, const double* w, double* out, double* dot_part)
     fused_normal_apply_dev(c, w, out);
     return false;
   }
-  matvec_dev(c, w, c.ytmp.ensure(c.N));
-  matvec_t_dev(c, c.ytmp.p, out, dot_part ? w : nullptr, dot_part);
+  normal_two_pass_dev(c, w, out, dot_part);
   return dot_part != nullptr;
 }
 

@@ -85,7 +85,11 @@ __global__ void k_cover_sum(const double* __restrict__ z, const int* __restrict_
 // stride the rows, then the butterfly) into a partial; (2) each column sums its chunk partials in
 // chunk order. Deterministic, no atomics; the tile count does not depend on p_j, so the grid fills
 // the GPU even when blocks are narrow.
+// FROM_Z (the normal operator Hᵀ(H·w)): the staged r = (H·w)[rows_j] is formed here from the
+// per-block partials z of k_block_gemv through the per-entry cover lists (ascending j, the
+// reference's summation order, so identical to k_cover_sum's y) — no y round trip, one launch less.
 constexpr int kMtRows = 512, kMtWarps = 8, kMtUnroll = 8;
+template <bool FROM_Z, int W>
 __global__ void __launch_bounds__(kMtWarps * 32) k_block_gemv_t(const double* __restrict__ H,
                                                                  const long long* __restrict__ H_off,
                                                                  const int* __restrict__ row_ptr,
@@ -93,14 +97,38 @@ __global__ void __launch_bounds__(kMtWarps * 32) k_block_gemv_t(const double* __
                                                                  const int* __restrict__ col_off,
                                                                  const int2* __restrict__ tiles,
                                                                  const int* __restrict__ part_off,
-                                                                 const double* __restrict__ r, double* __restrict__ part) {
+                                                                 const double* __restrict__ r, double* __restrict__ part,
+                                                                 const int* __restrict__ ent_flat) {
   __shared__ double rsm[kMtRows];
   const int2 t = tiles[blockIdx.x];
   const int j = t.x;
   const int r0 = row_ptr[j], rows = row_ptr[j + 1] - r0;
   const int q0 = t.y, nq = min(kMtRows, rows - q0);
   const int pj = col_off[j + 1] - col_off[j];
-  for (int q = threadIdx.x; q < nq; q += blockDim.x) rsm[q] = r[row_idx[r0 + q0 + q]];
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    if constexpr (FROM_Z) {
+      const int4* f = reinterpret_cast<const int4*>(ent_flat + static_cast<size_t>(r0 + q0 + q) * W);
+      int idx[W];
+#pragma unroll
+      for (int u = 0; u < W / 4; ++u) {
+        const int4 v = f[u];
+        idx[4 * u] = v.x;
+        idx[4 * u + 1] = v.y;
+        idx[4 * u + 2] = v.z;
+        idx[4 * u + 3] = v.w;
+      }
+      double zv[W];
+#pragma unroll
+      for (int u = 0; u < W; ++u) zv[u] = idx[u] >= 0 ? r[idx[u]] : 0.0;
+      double s = 0.0;
+#pragma unroll
+      for (int u = 0; u < W; ++u)
+        if (idx[u] >= 0) s += zv[u];
+      rsm[q] = s;
+    } else {
+      rsm[q] = r[row_idx[r0 + q0 + q]];
+    }
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* out = part + part_off[blockIdx.x];
@@ -159,6 +187,25 @@ __global__ void __launch_bounds__(256) k_chunk_sum(const double* __restrict__ pa
 
 }  // namespace
 
+// per (block, local row) entry: flat indices into the per-block partials z of the entry's point's
+// covering (block, row) pairs, ascending block, padded with -1 to the width W (4 or 8)
+__global__ void k_entry_covers(const int* __restrict__ row_idx, const int* __restrict__ row_ptr,
+                               const int* __restrict__ cov_n, const int* __restrict__ cov_j,
+                               const int* __restrict__ cov_r, int maxcov, long long nent, int W,
+                               int* __restrict__ ent_flat) {
+  const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (e >= nent) return;
+  const int i = row_idx[e], nc = cov_n[i];
+  for (int s = 0; s < W; ++s) {
+    int v = -1;
+    if (s < nc) {
+      const size_t q = static_cast<size_t>(i) * maxcov + s;
+      v = row_ptr[cov_j[q]] + cov_r[q];
+    }
+    ent_flat[e * W + s] = v;
+  }
+}
+
 void ensure_col_owner(Ctx& c) {
   std::vector<int> own(c.p);
   for (int j = 0; j < c.J; ++j)
@@ -190,6 +237,18 @@ void ensure_col_owner(Ctx& c) {
   c.mt_blk_tile0.upload(t0, c.stream);
   c.mt_part.ensure(std::max(1, pacc));
   c.zrows.ensure(std::max(1, c.h_row_ptr[c.J]));
+  // cover lists per entry for the normal operator's fused staging (built once per instance,
+  // outside any graph capture)
+  c.ent_w = c.maxcov <= 4 ? 4 : 8;
+  const long long nent = c.h_row_ptr[c.J];
+  if (c.maxcov <= 8 && nent > 0) {
+    c.ent_flat.ensure(static_cast<size_t>(nent) * c.ent_w);
+    k_entry_covers<<<ceil_div(nent, 256), 256, 0, c.stream>>>(c.row_idx.p, c.row_ptr.p, c.cov_n.p, c.cov_j.p, c.cov_r.p,
+                                                              c.maxcov, nent, c.ent_w, c.ent_flat.p);
+    RDD_LAUNCH_CHECK();
+  } else {
+    c.ent_w = 0;
+  }
 }
 
 void column_norms_scale(Ctx& c, bool equilibrate) {
@@ -217,11 +276,39 @@ void matvec_dev(Ctx& c, const double* w, double* y) {
 void matvec_t_dev(Ctx& c, const double* r, double* out, const double* dot_with, double* dot_part) {
   ScopedKernelTimer tk(c, "matvec_t");
   if (c.mt_ntiles == 0) return;
-  k_block_gemv_t<<<c.mt_ntiles, kMtWarps * 32, 0, c.stream>>>(c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p,
-                                                              c.mt_tiles.p, c.mt_part_off.p, r, c.mt_part.p);
+  k_block_gemv_t<false, 4><<<c.mt_ntiles, kMtWarps * 32, 0, c.stream>>>(
+      c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p, c.mt_tiles.p, c.mt_part_off.p, r, c.mt_part.p, nullptr);
   RDD_LAUNCH_CHECK();
   k_chunk_sum<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.mt_part.p, c.downer.p, c.dcol_off.p, c.mt_blk_tile0.p,
                                                         c.mt_part_off.p, c.p, out, dot_with, dot_part);
+  RDD_LAUNCH_CHECK();
+}
+
+// out = Hᵀ(H·w) in the reference's two passes over H, y = H·w formed inside the Hᵀ staging
+void normal_two_pass_dev(Ctx& c, const double* w, double* out, double* dot_part) {
+  if (c.ent_w == 0 || c.mt_ntiles == 0) {
+    matvec_dev(c, w, c.ytmp.ensure(c.N));
+    matvec_t_dev(c, c.ytmp.p, out, dot_part ? w : nullptr, dot_part);
+    return;
+  }
+  ScopedKernelTimer tk(c, "normal_two_pass");
+  if (c.mv_ntiles > 0) {
+    const size_t sm = static_cast<size_t>(c.m) * sizeof(double);
+    k_block_gemv<<<c.mv_ntiles, kMvRows, sm, c.stream>>>(c.H, c.dH_off.p, c.row_ptr.p, c.dcol_off.p, c.mv_tiles.p, w,
+                                                         c.zrows.p);
+    RDD_LAUNCH_CHECK();
+  }
+  if (c.ent_w == 4)
+    k_block_gemv_t<true, 4><<<c.mt_ntiles, kMtWarps * 32, 0, c.stream>>>(
+        c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p, c.mt_tiles.p, c.mt_part_off.p, c.zrows.p, c.mt_part.p,
+        c.ent_flat.p);
+  else
+    k_block_gemv_t<true, 8><<<c.mt_ntiles, kMtWarps * 32, 0, c.stream>>>(
+        c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p, c.mt_tiles.p, c.mt_part_off.p, c.zrows.p, c.mt_part.p,
+        c.ent_flat.p);
+  RDD_LAUNCH_CHECK();
+  k_chunk_sum<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.mt_part.p, c.downer.p, c.dcol_off.p, c.mt_blk_tile0.p,
+                                                        c.mt_part_off.p, c.p, out, dot_part ? w : nullptr, dot_part);
   RDD_LAUNCH_CHECK();
 }
 

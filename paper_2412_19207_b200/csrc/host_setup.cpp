@@ -221,18 +221,21 @@ void setup_problem(Ctx& c, const rdd_config& cfg, uint64_t seed) {
   const long long Ntot = n + (nb > 0 ? 4LL * nb : 0);
   if (Ntot > 2000000000LL) throw std::invalid_argument("too many collocation points");
   c.N = static_cast<int>(Ntot);
-  c.h_pts.assign(static_cast<size_t>(d) * c.N, 0.0);
-  std::vector<int> gi(d, 0);
+  c.h_pts.resize(static_cast<size_t>(d) * c.N);  // every entry is written below
   std::vector<double> step(d);
+  std::vector<long long> stride(d, 1);
   for (int a = 0; a < d; ++a) step[a] = (c.prob.hi[a] - c.prob.lo[a]) / static_cast<double>(res[a]);
-  for (long long flat = 0; flat < n; ++flat) {
-    for (int a = 0; a < d; ++a)
-      c.h_pts[static_cast<size_t>(a) * c.N + flat] = c.prob.lo[a] + (static_cast<double>(gi[a]) + 0.5) * step[a];
-    for (int a = d - 1; a >= 0; --a) {
-      if (++gi[a] < res[a]) break;
-      gi[a] = 0;
+  for (int a = d - 2; a >= 0; --a) stride[a] = stride[a + 1] * res[a + 1];
+  // last axis fastest; index of axis a = (flat / stride_a) mod res_a — the same coordinate formula
+  // as the reference's incremental counters, evaluated per point so the host threads split the grid
+  double* hp = c.h_pts.data();
+  const long long NN = c.N;
+#pragma omp parallel for schedule(static)
+  for (long long flat = 0; flat < n; ++flat)
+    for (int a = 0; a < d; ++a) {
+      const long long g = (flat / stride[a]) % res[a];
+      hp[a * NN + flat] = c.prob.lo[a] + (static_cast<double>(g) + 0.5) * step[a];
     }
-  }
   if (nb > 0) {
     long long q = n;
     for (int e = 0; e < 4; ++e) {
@@ -249,6 +252,7 @@ void setup_problem(Ctx& c, const rdd_config& cfg, uint64_t seed) {
   // ---- random bases: R (m x d, drawn k-major then axis) then b (basis.hpp:43-46)
   c.h_R.assign(static_cast<size_t>(total) * c.m * d, 0.0);
   c.h_b.assign(static_cast<size_t>(total) * c.m, 0.0);
+#pragma omp parallel for schedule(static)
   for (int j = 0; j < total; ++j) {
     Mix rng{subdomain_seed(seed, j)};
     for (int k = 0; k < c.m; ++k)

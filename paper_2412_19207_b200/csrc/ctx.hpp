@@ -118,6 +118,7 @@ struct Ctx {
   DBuf<double> NB;
   std::map<std::pair<int, int>, int> nb_index;
   DBuf<long long> nb_look;         // per neighbour-CSR entry: NB offset or -1
+  std::vector<long long> h_nb_look;  // host copy
 
   // ---- Schwarz (schwarz.hpp)
   int pkind = RDD_PRECOND_NONE;

@@ -168,6 +168,7 @@ void build_normal_blocks(Ctx& c) {
       if (it != c.nb_index.end()) look[q] = c.nb_off[it->second];
     }
   c.nb_look.upload(look, c.stream);
+  c.h_nb_look = look;
   RDD_CUDA(cudaStreamSynchronize(c.stream));
 }
 

@@ -242,34 +242,41 @@ void build_schwarz(Ctx& c, int kind) {
   ScopedKernelTimer tk(c, "schwarz_build");
   const int J = c.J;
   c.pkind = kind;
+  const double th0 = now_s();
   // index sets (schwarz.hpp:39-61)
   c.set_ptr.assign(J + 1, 0);
-  c.set_idx.clear();
   std::vector<int> n(J);
   for (int i = 0; i < J; ++i) {
+    int ni = 0;
+    for (int q = c.nbr_ptr[i]; q < c.nbr_ptr[i + 1]; ++q) ni += c.h_p[c.nbr_idx[q]];
+    if (ni == 0) throw std::runtime_error("empty index set for subdomain " + std::to_string(i));
+    n[i] = ni;
+    c.set_ptr[i + 1] = c.set_ptr[i] + ni;
+  }
+  c.set_idx.resize(c.set_ptr[J]);
+  c.h_mult.assign(c.p, 0);
+  for (int i = 0; i < J; ++i) {
+    int* out = c.set_idx.data() + c.set_ptr[i];
     for (int q = c.nbr_ptr[i]; q < c.nbr_ptr[i + 1]; ++q) {
       const int j = c.nbr_idx[q];
-      for (int col = c.h_col_off[j]; col < c.h_col_off[j + 1]; ++col) c.set_idx.push_back(col);
+      for (int col = c.h_col_off[j]; col < c.h_col_off[j + 1]; ++col) {
+        *out++ = col;
+        ++c.h_mult[col];
+      }
     }
-    c.set_ptr[i + 1] = static_cast<int>(c.set_idx.size());
-    n[i] = c.set_ptr[i + 1] - c.set_ptr[i];
-    if (n[i] == 0) throw std::runtime_error("empty index set for subdomain " + std::to_string(i));
   }
-  c.h_mult.assign(c.p, 0);
-  for (int col : c.set_idx) ++c.h_mult[col];
-  // gather map per column: positions (into the concatenated z) in ascending i
-  std::vector<std::vector<int>> gl(c.p);
-  std::vector<int> owner_pos(c.p, 0);
-  for (int i = 0; i < J; ++i)
-    for (int q = c.set_ptr[i]; q < c.set_ptr[i + 1]; ++q) {
-      const int col = c.set_idx[q];
-      gl[col].push_back(q);
-      if (c.h_owner[col] == i) owner_pos[col] = q;
-    }
-  std::vector<int> gp(c.p + 1, 0), gpos;
-  for (int col = 0; col < c.p; ++col) {
-    gp[col + 1] = gp[col] + static_cast<int>(gl[col].size());
-    gpos.insert(gpos.end(), gl[col].begin(), gl[col].end());
+  // gather map per column: positions (into the concatenated z) in ascending i — a counting sort
+  // keyed by column (positions are visited in ascending order, so each column's list is sorted)
+  std::vector<int> gp(c.p + 1, 0), gpos(c.set_idx.size()), owner_pos(c.p, 0);
+  for (int col = 0; col < c.p; ++col) gp[col + 1] = gp[col] + c.h_mult[col];
+  {
+    std::vector<int> fill(gp.begin(), gp.end() - 1);
+    for (int i = 0; i < J; ++i)
+      for (int q = c.set_ptr[i]; q < c.set_ptr[i + 1]; ++q) {
+        const int col = c.set_idx[q];
+        gpos[fill[col]++] = q;
+        if (c.h_owner[col] == i) owner_pos[col] = q;
+      }
   }
   c.gat_ptr.upload(gp, c.stream);
   c.gat_pos.upload(gpos, c.stream);
@@ -278,28 +285,39 @@ void build_schwarz(Ctx& c, int kind) {
   c.dset_idx.upload(c.set_idx, c.stream);
   c.dmult.upload(c.h_mult, c.stream);
   c.zloc.ensure(std::max<size_t>(1, 2 * c.set_idx.size()));  // two partials in the inverse mode
+  if (c.verbose) std::fprintf(stderr, "[schwarz] index sets + gather map (host) %.3f ms\n", 1e3 * (now_s() - th0));
 
-  // local matrix sizes and gather plan (schwarz.hpp:112-130): A_i blocks come from NB
+  // local matrix sizes and gather plan (schwarz.hpp:112-130): A_i blocks come from NB. The pair
+  // (j1, j2) is looked up in j1's sorted neighbour list (normal blocks exist for neighbour pairs).
   c.local_n = n;
   c.gat_tasks.clear();
+  std::vector<int> po;
   for (int i = 0; i < J; ++i) {
-    std::vector<std::pair<int, int>> parts;
+    po.clear();
     int o = 0;
     for (int q = c.nbr_ptr[i]; q < c.nbr_ptr[i + 1]; ++q) {
-      const int j = c.nbr_idx[q];
-      parts.push_back({j, o});
-      o += c.h_p[j];
+      po.push_back(o);
+      o += c.h_p[c.nbr_idx[q]];
     }
-    for (auto [j1, o1] : parts)
-      for (auto [j2, o2] : parts) {
-        auto it = c.nb_index.find({std::min(j1, j2), std::max(j1, j2)});
-        if (it == c.nb_index.end()) continue;
-        c.gat_tasks.push_back({i, j1, j2, o1, o2, c.nb_off[it->second]});
+    const int b0 = c.nbr_ptr[i], nn = c.nbr_ptr[i + 1] - b0;
+    for (int x = 0; x < nn; ++x)
+      for (int y = 0; y < nn; ++y) {
+        const int j1 = c.nbr_idx[b0 + x], j2 = c.nbr_idx[b0 + y];
+        const int lo = std::min(j1, j2), hi = std::max(j1, j2);
+        const int* beg = c.nbr_idx.data() + c.nbr_ptr[lo];
+        const int* endp = c.nbr_idx.data() + c.nbr_ptr[lo + 1];
+        const int* it = std::lower_bound(beg, endp, hi);
+        if (it == endp || *it != hi) continue;
+        const long long nbo = c.h_nb_look[it - c.nbr_idx.data()];
+        if (nbo < 0) continue;  // neighbours without a row intersection: no normal block
+        c.gat_tasks.push_back({i, j1, j2, po[x], po[y], nbo});
       }
   }
+  if (c.verbose) std::fprintf(stderr, "[schwarz] + gather tasks (host) %.3f ms\n", 1e3 * (now_s() - th0));
   // storage: the tile-packed factor of every A_i (the eigen-fallback blocks keep a dense copy) or,
   // when every block is small, the packed explicit inverse: one symmetric tile pass per apply
   // instead of two triangular ones, for 2/3·n³ more build flops
+  if (c.verbose) std::fprintf(stderr, "[schwarz] + gather tasks (host) %.3f ms\n", 1e3 * (now_s() - th0));
   c.inv_mode = *std::max_element(n.begin(), n.end()) <= kInvMax;
   c.P_off.assign(J + 1, 0);
   for (int i = 0; i < J; ++i) c.P_off[i + 1] = c.P_off[i] + packed_chol_size(n[i]);

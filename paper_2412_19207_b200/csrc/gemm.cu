@@ -44,11 +44,21 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmTask* __restrict__ tasks)
   const int m0 = T.tm * BM, n0 = T.tn * BN;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
 
+  // C = beta·C + alpha·op(A)op(B). With alpha = ±1 the accumulators start from (beta/alpha)·C,
+  // loaded here so the C read overlaps the operand prologue instead of trailing the main loop
+  const bool pre = T.beta != 0.0 && (T.alpha == 1.0 || T.alpha == -1.0);
+  const double cf = T.beta * T.alpha;  // beta/alpha for alpha = ±1
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m = m0 + wm + 8 * i + (lane >> 2);
+        const int n = n0 + wn + 8 * j + 2 * (lane & 3) + e;
+        acc[i][j][e] = (pre && m < T.M && n < T.N) ? cf * T.Cm[m + static_cast<long long>(n) * T.ldc] : 0.0;
+      }
 
   auto As = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStageA; };
   auto Bs = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStageA + kStageA; };
@@ -126,7 +136,7 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmTask* __restrict__ tasks)
         const int n = n0 + wn + 8 * j + 2 * (lane & 3) + e;
         if (m < T.M && n < T.N) {
           double* p = T.Cm + m + static_cast<long long>(n) * T.ldc;
-          *p = (T.beta != 0.0 ? T.beta * *p : 0.0) + T.alpha * acc[i][j][e];
+          *p = pre ? T.alpha * acc[i][j][e] : (T.beta != 0.0 ? T.beta * *p : 0.0) + T.alpha * acc[i][j][e];
         }
       }
 }

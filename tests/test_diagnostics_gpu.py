@@ -175,3 +175,52 @@ def test_spectra_needs_preconditioner_and_cap(dev):
         dev.spectra(True)
     with pytest.raises(ValueError, match=r"matrix of size 32 exceeds the dense diagnostics cap \(31\)"):
         dev.spectra(False, cap=31)
+
+
+@pytest.mark.parametrize("case", ["repeated", "rotations", "triangular_perturbed", "graded", "zero", "scaled_identity"])
+def test_spectrum_multibulge_structures(dev, case):
+    # active blocks above 112 take the windowed multi-bulge sweeps; structures that stress the
+    # shifts and deflation (repeated, complex-pair, nonnormal, graded, degenerate spectra)
+    rng = np.random.default_rng(hash(case) % 2**32)
+    n = 240
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    if case == "repeated":
+        lam = np.repeat([1.0, 2.0, 5.0, -3.0], n // 4)
+        a = (q * lam) @ q.T
+        want = lam.astype(complex)
+    elif case == "rotations":
+        b = np.zeros((n, n))
+        want = []
+        for k in range(n // 2):
+            re, im = rng.uniform(-2, 2), rng.uniform(0.1, 3)
+            b[2 * k:2 * k + 2, 2 * k:2 * k + 2] = [[re, im], [-im, re]]
+            want += [re + 1j * im, re - 1j * im]
+        a = q @ b @ q.T
+        want = np.array(want)
+    elif case == "triangular_perturbed":
+        # strongly nonnormal: eigenvalues are ill-conditioned, so check the backward error of each
+        # computed eigenvalue (σ_min(A − λI) small) rather than distances to another solver's values
+        t = np.triu(rng.standard_normal((n, n)))
+        a = q @ t @ q.T
+        got = dev.spectrum(a)
+        na = np.linalg.norm(a, 2)
+        worst = max(np.linalg.svd(a - z * np.eye(n), compute_uv=False)[-1] for z in got[::8])
+        assert worst <= 1e-12 * n * na
+        assert abs(got.sum() - np.trace(a)) <= 1e-9 * n * na  # trace = Σλ
+        return
+    elif case == "graded":
+        lam = np.logspace(-8, 4, n)
+        a = (q * lam) @ q.T
+        want = lam.astype(complex)
+    elif case == "zero":
+        a = np.zeros((n, n))
+        want = np.zeros(n, dtype=complex)
+    else:
+        a = 3.5 * np.eye(n)
+        want = np.full(n, 3.5, dtype=complex)
+    got = dev.spectrum(a)
+    scale = max(1.0, np.linalg.norm(a, 2))
+    tol = 1e-9
+    if case == "repeated":
+        tol = 1e-7  # a multiple eigenvalue of a symmetric matrix rounded through a nonsymmetric solver
+    assert _match(got, want) <= tol * scale, case

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <future>
 
 #include "ctx.hpp"
 
@@ -109,8 +110,12 @@ static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed, bool reside
   if (cfg.solver == RDD_SOLVER_QR) {  // runner.hpp:217-222: no preconditioner, no Krylov
   } else if (cfg.precond >= 0) {
     t0 = now_s();
+    // the Schwarz index sets are host work independent of the normal blocks: a host thread builds
+    // them while the device forms the blocks
+    auto idx = std::async(std::launch::async, [&c] { return prepare_schwarz_index(c); });
     build_normal_blocks(c);
-    build_schwarz(c, cfg.precond);
+    SchwarzIndex x = idx.get();
+    build_schwarz(c, cfg.precond, &x);
     RDD_CUDA(cudaStreamSynchronize(c.stream));
     t_pre = now_s() - t0;
     if (c.verbose) std::fprintf(stderr, "[phase] precond %.3f s (fallback %d)\n", t_pre, c.n_fallback);
@@ -252,9 +257,15 @@ int rdd_assemble(rdd_ctx* h, int equilibrate) {
 int rdd_build_preconditioner(rdd_ctx* h, int kind) {
   return guarded(h, [&](Ctx& c) {
     need_assembled(c);
-    rdd::build_normal_blocks(c);
-    if (kind >= 0) rdd::build_schwarz(c, kind);
-    else c.pkind = RDD_PRECOND_NONE;
+    if (kind >= 0) {
+      auto idx = std::async(std::launch::async, [&c] { return rdd::prepare_schwarz_index(c); });
+      rdd::build_normal_blocks(c);
+      rdd::SchwarzIndex x = idx.get();
+      rdd::build_schwarz(c, kind, &x);
+    } else {
+      rdd::build_normal_blocks(c);
+      c.pkind = RDD_PRECOND_NONE;
+    }
   });
 }
 int rdd_solve(rdd_ctx* h, int solver, double rel_tol, int max_iter, int gmres_restart) {

@@ -248,7 +248,11 @@ void normal_two_pass_dev(Ctx& c, const double* w, double* out, double* dot_part)
 bool build_fused_plan(Ctx& c);
 void fused_normal_apply_dev(Ctx& c, const double* w, double* out);
 // schwarz.cu (K8/K11)
-void build_schwarz(Ctx& c, int kind);
+struct SchwarzIndex {  // host side of build_index_sets (schwarz.hpp:39-61) + the column gather map
+  std::vector<int> set_ptr, set_idx, mult, n, gp, gpos, owner_pos;
+};
+SchwarzIndex prepare_schwarz_index(const Ctx& c);
+void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre = nullptr);
 // pzz/pzv: per-CTA partials (ceil(p/256)) of z·z and z·v, fused into the reduction kernel
 void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose, double* pzz = nullptr, double* pzv = nullptr);
 void gather_locals(Ctx& c, const std::vector<int>& which, DBuf<double>& out, const std::vector<long long>& off,

@@ -238,46 +238,62 @@ void refresh_local_cond(Ctx& c) {
   c.local_cond_exact = true;
 }
 
-void build_schwarz(Ctx& c, int kind) {
-  ScopedKernelTimer tk(c, "schwarz_build");
+// index sets S_i (schwarz.hpp:39-61), multiplicities and the per-column gather map: host work that
+// reads only the decomposition and the PCA ranks, so it can run on a host thread while the normal
+// blocks are formed on the device
+SchwarzIndex prepare_schwarz_index(const Ctx& c) {
+  SchwarzIndex x;
   const int J = c.J;
-  c.pkind = kind;
-  const double th0 = now_s();
-  // index sets (schwarz.hpp:39-61)
-  c.set_ptr.assign(J + 1, 0);
-  std::vector<int> n(J);
+  x.set_ptr.assign(J + 1, 0);
+  x.n.resize(J);
   for (int i = 0; i < J; ++i) {
     int ni = 0;
     for (int q = c.nbr_ptr[i]; q < c.nbr_ptr[i + 1]; ++q) ni += c.h_p[c.nbr_idx[q]];
     if (ni == 0) throw std::runtime_error("empty index set for subdomain " + std::to_string(i));
-    n[i] = ni;
-    c.set_ptr[i + 1] = c.set_ptr[i] + ni;
+    x.n[i] = ni;
+    x.set_ptr[i + 1] = x.set_ptr[i] + ni;
   }
-  c.set_idx.resize(c.set_ptr[J]);
-  c.h_mult.assign(c.p, 0);
+  x.set_idx.resize(x.set_ptr[J]);
+  x.mult.assign(c.p, 0);
   for (int i = 0; i < J; ++i) {
-    int* out = c.set_idx.data() + c.set_ptr[i];
+    int* out = x.set_idx.data() + x.set_ptr[i];
     for (int q = c.nbr_ptr[i]; q < c.nbr_ptr[i + 1]; ++q) {
       const int j = c.nbr_idx[q];
       for (int col = c.h_col_off[j]; col < c.h_col_off[j + 1]; ++col) {
         *out++ = col;
-        ++c.h_mult[col];
+        ++x.mult[col];
       }
     }
   }
   // gather map per column: positions (into the concatenated z) in ascending i — a counting sort
   // keyed by column (positions are visited in ascending order, so each column's list is sorted)
-  std::vector<int> gp(c.p + 1, 0), gpos(c.set_idx.size()), owner_pos(c.p, 0);
-  for (int col = 0; col < c.p; ++col) gp[col + 1] = gp[col] + c.h_mult[col];
-  {
-    std::vector<int> fill(gp.begin(), gp.end() - 1);
-    for (int i = 0; i < J; ++i)
-      for (int q = c.set_ptr[i]; q < c.set_ptr[i + 1]; ++q) {
-        const int col = c.set_idx[q];
-        gpos[fill[col]++] = q;
-        if (c.h_owner[col] == i) owner_pos[col] = q;
-      }
-  }
+  x.gp.assign(c.p + 1, 0);
+  x.gpos.resize(x.set_idx.size());
+  x.owner_pos.assign(c.p, 0);
+  for (int col = 0; col < c.p; ++col) x.gp[col + 1] = x.gp[col] + x.mult[col];
+  std::vector<int> fill(x.gp.begin(), x.gp.end() - 1);
+  for (int i = 0; i < J; ++i)
+    for (int q = x.set_ptr[i]; q < x.set_ptr[i + 1]; ++q) {
+      const int col = x.set_idx[q];
+      x.gpos[fill[col]++] = q;
+      if (c.h_owner[col] == i) x.owner_pos[col] = q;
+    }
+  return x;
+}
+
+void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre) {
+  ScopedKernelTimer tk(c, "schwarz_build");
+  const int J = c.J;
+  c.pkind = kind;
+  const double th0 = now_s();
+  SchwarzIndex own;
+  if (!pre) own = prepare_schwarz_index(c);
+  SchwarzIndex& x = pre ? *pre : own;
+  c.set_ptr = std::move(x.set_ptr);
+  c.set_idx = std::move(x.set_idx);
+  c.h_mult = std::move(x.mult);
+  std::vector<int> n = std::move(x.n), gp = std::move(x.gp), gpos = std::move(x.gpos),
+                   owner_pos = std::move(x.owner_pos);
   c.gat_ptr.upload(gp, c.stream);
   c.gat_pos.upload(gpos, c.stream);
   c.gat_owner_pos.upload(owner_pos, c.stream);

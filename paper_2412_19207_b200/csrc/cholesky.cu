@@ -37,7 +37,6 @@ __global__ void k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mat
   extern __shared__ double dsm[];
   double(*s)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
   double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
-  __shared__ double d;
   const int q = act[blockIdx.x];
   const Mat M = mats[q];
   const int k0 = k * NB, bs = min(NB, M.n - k0);
@@ -47,6 +46,7 @@ __global__ void k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mat
     s[r][c] = (r < bs && c < bs) ? a[r + static_cast<long long>(c) * M.n] : (r == c ? 1.0 : 0.0);
   }
   __syncthreads();
+  __shared__ double d;
   for (int c = 0; c < NB; ++c) {
     if (threadIdx.x == 0) {
       const double v = s[c][c];
@@ -57,9 +57,12 @@ __global__ void k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mat
     __syncthreads();
     for (int r = c + 1 + threadIdx.x; r < NB; r += blockDim.x) s[r][c] /= d;
     __syncthreads();
-    for (int e = threadIdx.x; e < (NB - c - 1) * (NB - c - 1); e += blockDim.x) {
-      const int r = c + 1 + e % (NB - c - 1), qq = c + 1 + e / (NB - c - 1);
-      if (qq <= r) s[r][qq] -= s[r][c] * s[qq][c];
+    {  // trailing update of the lower triangle: warps over rows, lanes over columns (no div/mod)
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+      for (int r = c + 1 + warp; r < NB; r += nw) {
+        const double src = s[r][c];
+        for (int qq = c + 1 + lane; qq <= r; qq += 32) s[r][qq] -= src * s[qq][c];
+      }
     }
     __syncthreads();
   }
@@ -67,12 +70,18 @@ __global__ void k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mat
     const int r = e % NB, c = e / NB;
     if (r < bs && c < bs) a[r + static_cast<long long>(c) * M.n] = r >= c ? s[r][c] : 0.0;
   }
-  const int c = threadIdx.x;  // column c of L⁻¹: forward substitution down the rows
-  if (c < NB) {
+  // L⁻¹ by forward substitution down the rows, four lanes per column (a column only reads its own
+  // earlier entries, so the four lanes synchronise within their warp only)
+  {
+    const int c = threadIdx.x >> 2, part = threadIdx.x & 3;
     for (int r = 0; r < NB; ++r) {
-      double v = (r == c) ? 1.0 : 0.0;
-      for (int qq = c; qq < r; ++qq) v -= s[r][qq] * X[qq][c];
-      X[r][c] = r < c ? 0.0 : v / s[r][r];
+      double v = 0.0;
+      if (r > c)
+        for (int qq = c + part; qq < r; qq += 4) v += s[r][qq] * X[qq][c];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (part == 0) X[r][c] = r < c ? 0.0 : ((r == c ? 1.0 : 0.0) - v) / s[r][r];
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -605,9 +614,12 @@ void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const s
   dtask.ensure(static_cast<size_t>(std::max<long long>(1, tmax)));
   for (int k = 0; k < nbmax; ++k) {
     const Step& st = steps[k];
-    k_potrf_diag<<<static_cast<int>(st.nact), 256, kPairSmem, c.stream>>>(A, dm.p, dact.p + st.act0, k, dfail.p, Dinv,
-                                                                           ddoff.p);
-    RDD_LAUNCH_CHECK();
+    {
+      ScopedKernelTimer tp(c, "potrf");
+      k_potrf_diag<<<static_cast<int>(st.nact), 256, kPairSmem, c.stream>>>(A, dm.p, dact.p + st.act0, k, dfail.p,
+                                                                             Dinv, ddoff.p);
+      RDD_LAUNCH_CHECK();
+    }
     if (st.stotal > 0) {  // panel: A[ib, k] <- A[ib, k] D_kᵀ on DMMA
       k_make_updates<<<ceil_div(st.stotal, 256), 256, 0, c.stream>>>(A, dsd.p + st.sd0, static_cast<int>(st.nsd),
                                                                       st.stotal, dtask.p);

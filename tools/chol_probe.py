@@ -12,4 +12,4 @@ s.reset_stats()
 r = s.rerun_resident()
 n = s.geti("local_n")
 print({k: r[k] for k in ("iterations", "t_pca", "t_precond", "t_solve")}, "n_max", n.max(), "sum n3/3", float((n.astype(float)**3/3).sum()),
-      {f: s.kernel_stats(f) for f in ("cholesky", "gemm_nt", "inv_power", "schwarz_gather")})
+      {f: s.kernel_stats(f) for f in ("cholesky", "gemm_nt", "inv_power", "schwarz_gather", "potrf")})

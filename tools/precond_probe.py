@@ -20,4 +20,4 @@ for rep in range(4):
 s.set_timing(True)
 s.reset_stats()
 s.build_preconditioner(A.PRECOND_AS)
-print({f: s.kernel_stats(f) for f in ("normal_blocks", "schwarz_build", "schwarz_gather", "cholesky", "gemm_nt", "gemm_nn", "gemm_tn", "inv_power", "power")})
+print({f: s.kernel_stats(f) for f in ("normal_blocks", "schwarz_build", "schwarz_gather", "cholesky", "gemm_nt", "gemm_nn", "gemm_tn", "inv_power", "power", "potrf")})

@@ -775,7 +775,8 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
     const double* __restrict__ P, const long long* __restrict__ poff, const double* const* __restrict__ dense,
     const int* __restrict__ set_ptr, const int* __restrict__ set_idx, const double* __restrict__ v,
     const int* __restrict__ mult, const int* __restrict__ owner, int kind, int transpose, int nbmax,
-    double* __restrict__ z, int inverse, long long zhalf) {
+    double* __restrict__ z, int inverse, long long zhalf, const int* __restrict__ live) {
+  if (live && *live != 0) return;  // solver loop already stopped (speculative graph iteration)
   extern __shared__ double sm[];
   double* g = sm;
   double* red = sm + static_cast<size_t>(nbmax) * NB;
@@ -821,7 +822,7 @@ void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
   }
   k_chol_apply<<<c.inv_mode ? 2 * c.J : c.J, kSolveWarps * 32, smem, c.stream>>>(
       c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p, v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
-      ceil_div(c.nmax_local, NB), zloc, c.inv_mode ? 1 : 0, static_cast<long long>(c.set_idx.size()));
+      ceil_div(c.nmax_local, NB), zloc, c.inv_mode ? 1 : 0, static_cast<long long>(c.set_idx.size()), c.live);
   RDD_LAUNCH_CHECK();
 }
 

@@ -159,6 +159,8 @@ struct Ctx {
   DBuf<int2> mv_tiles, mt_tiles;      // (block, first row) / (block, first column) tiles of H·w / Hᵀ·r
   int mv_ntiles = 0, mt_ntiles = 0, mv_rmax = 0;
   DBuf<double> zrows;                 // per-block partial H_j·w_j (row_ptr layout)
+  const int* live = nullptr;          // solver status word (0 = running) while a solver graph is captured:
+                                      // operator/preconditioner kernels of speculative iterations exit early
   DBuf<int> ent_flat;                 // per (block, local row): flat z indices of the point's covers (-1 pad)
   int ent_w = 0;                      // its width (4 or 8; 0 = not built)
   DBuf<int> mt_part_off, mt_blk_tile0;  // Hᵀ·r row-chunk partials: offset per tile, first tile per block

@@ -325,7 +325,14 @@ static void cg_solve(Ctx& c, const double* b, double* x, double tol, int max_ite
   CgGraph g;
   const bool timing = c.timing;
   c.timing = false;  // no event records inside capture
+  // the operator/preconditioner kernels of iterations after the stop exit early
+  struct LiveScope {
+    Ctx& c;
+    LiveScope(Ctx& cc, const int* p) : c(cc) { c.live = p; }
+    ~LiveScope() { c.live = nullptr; }
+  };
   {
+    LiveScope ls(c, &st.p->status);
     cudaGraph_t graph;
     const int64_t before = launch_counter();
     RDD_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));

@@ -42,7 +42,8 @@ constexpr int kMvRows = 256, kMvUnroll = 8;
 __global__ void __launch_bounds__(kMvRows) k_block_gemv(const double* __restrict__ H, const long long* __restrict__ H_off,
                                                          const int* __restrict__ row_ptr, const int* __restrict__ col_off,
                                                          const int2* __restrict__ tiles, const double* __restrict__ w,
-                                                         double* __restrict__ z) {
+                                                         double* __restrict__ z, const int* __restrict__ live) {
+  if (live && *live != 0) return;  // solver loop already stopped (speculative graph iteration)
   extern __shared__ double wsm[];
   const int2 t = tiles[blockIdx.x];
   const int j = t.x;
@@ -98,7 +99,9 @@ __global__ void __launch_bounds__(kMtWarps * 32) k_block_gemv_t(const double* __
                                                                  const int2* __restrict__ tiles,
                                                                  const int* __restrict__ part_off,
                                                                  const double* __restrict__ r, double* __restrict__ part,
-                                                                 const int* __restrict__ ent_flat) {
+                                                                 const int* __restrict__ ent_flat,
+                                                                 const int* __restrict__ live) {
+  if (live && *live != 0) return;
   __shared__ double rsm[kMtRows];
   const int2 t = tiles[blockIdx.x];
   const int j = t.x;
@@ -170,7 +173,9 @@ __global__ void __launch_bounds__(kMtWarps * 32) k_block_gemv_t(const double* __
 __global__ void __launch_bounds__(256) k_chunk_sum(const double* __restrict__ part, const int* __restrict__ col_owner,
                                                    const int* __restrict__ col_off, const int* __restrict__ blk_tile0,
                                                    const int* __restrict__ part_off, int p, double* __restrict__ out,
-                                                   const double* __restrict__ dw, double* __restrict__ dpart) {
+                                                   const double* __restrict__ dw, double* __restrict__ dpart,
+                                                   const int* __restrict__ live) {
+  if (live && *live != 0) return;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   double s = 0.0;
   if (col < p) {
@@ -265,7 +270,7 @@ void matvec_dev(Ctx& c, const double* w, double* y) {
   if (c.mv_ntiles > 0) {
     const size_t sm = static_cast<size_t>(c.m) * sizeof(double);
     k_block_gemv<<<c.mv_ntiles, kMvRows, sm, c.stream>>>(c.H, c.dH_off.p, c.row_ptr.p, c.dcol_off.p, c.mv_tiles.p, w,
-                                                         c.zrows.p);
+                                                         c.zrows.p, c.live);
     RDD_LAUNCH_CHECK();
   }
   k_cover_sum<<<ceil_div(c.N, 256), 256, 0, c.stream>>>(c.zrows.p, c.row_ptr.p, c.cov_n.p, c.cov_j.p, c.cov_r.p,
@@ -277,10 +282,10 @@ void matvec_t_dev(Ctx& c, const double* r, double* out, const double* dot_with, 
   ScopedKernelTimer tk(c, "matvec_t");
   if (c.mt_ntiles == 0) return;
   k_block_gemv_t<false, 4><<<c.mt_ntiles, kMtWarps * 32, 0, c.stream>>>(
-      c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p, c.mt_tiles.p, c.mt_part_off.p, r, c.mt_part.p, nullptr);
+      c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p, c.mt_tiles.p, c.mt_part_off.p, r, c.mt_part.p, nullptr, c.live);
   RDD_LAUNCH_CHECK();
   k_chunk_sum<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.mt_part.p, c.downer.p, c.dcol_off.p, c.mt_blk_tile0.p,
-                                                        c.mt_part_off.p, c.p, out, dot_with, dot_part);
+                                                        c.mt_part_off.p, c.p, out, dot_with, dot_part, c.live);
   RDD_LAUNCH_CHECK();
 }
 
@@ -295,20 +300,20 @@ void normal_two_pass_dev(Ctx& c, const double* w, double* out, double* dot_part)
   if (c.mv_ntiles > 0) {
     const size_t sm = static_cast<size_t>(c.m) * sizeof(double);
     k_block_gemv<<<c.mv_ntiles, kMvRows, sm, c.stream>>>(c.H, c.dH_off.p, c.row_ptr.p, c.dcol_off.p, c.mv_tiles.p, w,
-                                                         c.zrows.p);
+                                                         c.zrows.p, c.live);
     RDD_LAUNCH_CHECK();
   }
   if (c.ent_w == 4)
     k_block_gemv_t<true, 4><<<c.mt_ntiles, kMtWarps * 32, 0, c.stream>>>(
         c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p, c.mt_tiles.p, c.mt_part_off.p, c.zrows.p, c.mt_part.p,
-        c.ent_flat.p);
+        c.ent_flat.p, c.live);
   else
     k_block_gemv_t<true, 8><<<c.mt_ntiles, kMtWarps * 32, 0, c.stream>>>(
         c.H, c.dH_off.p, c.row_ptr.p, c.row_idx.p, c.dcol_off.p, c.mt_tiles.p, c.mt_part_off.p, c.zrows.p, c.mt_part.p,
-        c.ent_flat.p);
+        c.ent_flat.p, c.live);
   RDD_LAUNCH_CHECK();
   k_chunk_sum<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.mt_part.p, c.downer.p, c.dcol_off.p, c.mt_blk_tile0.p,
-                                                        c.mt_part_off.p, c.p, out, dot_part ? w : nullptr, dot_part);
+                                                        c.mt_part_off.p, c.p, out, dot_part ? w : nullptr, dot_part, c.live);
   RDD_LAUNCH_CHECK();
 }
 

@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ z, co
                                                 const int* __restrict__ gat_owner_pos, const int* __restrict__ mult,
                                                 int p, int kind, int transpose, double* __restrict__ out,
                                                 const double* __restrict__ v, double* __restrict__ pzz,
-                                                double* __restrict__ pzv) {
+                                                double* __restrict__ pzv, const int* __restrict__ live) {
+  if (live && *live != 0) return;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   double s = 0.0;
   if (col < p) {
@@ -515,7 +516,7 @@ void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose, doubl
   chol_apply(c, v, transpose, c.zloc.p);
   const double* z2 = c.inv_mode ? c.zloc.p + c.set_idx.size() : nullptr;  // second half-partials
   k_reduce<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.zloc.p, z2, c.gat_ptr.p, c.gat_pos.p, c.gat_owner_pos.p, c.dmult.p,
-                                                     c.p, c.pkind, transpose ? 1 : 0, z, v, pzz, pzv);
+                                                     c.p, c.pkind, transpose ? 1 : 0, z, v, pzz, pzv, c.live);
   RDD_LAUNCH_CHECK();
 }
 

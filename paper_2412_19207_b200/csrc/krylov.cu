@@ -51,7 +51,8 @@ __device__ __forceinline__ double block_sum(double v) {
 
 
 __global__ void k_dot_part(const double* __restrict__ x, const double* __restrict__ y, int n,
-                           double* __restrict__ part) {
+                           double* __restrict__ part, const int* __restrict__ live = nullptr) {
+  if (live && *live) return;
   double s = 0.0;
   for (int i = blockIdx.x * kRT + threadIdx.x; i < n; i += kRB * kRT) s += x[i] * y[i];
   s = block_sum(s);
@@ -152,7 +153,9 @@ __global__ void k_copy(double* __restrict__ dst, const double* __restrict__ src,
 __global__ void k_fill(double* __restrict__ dst, double v, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = v;
 }
-__global__ void k_sub(double* __restrict__ out, const double* __restrict__ a, const double* __restrict__ b, int n) {
+__global__ void k_sub(double* __restrict__ out, const double* __restrict__ a, const double* __restrict__ b, int n,
+                      const int* __restrict__ live = nullptr) {
+  if (live && *live) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] - b[i];
 }
 __global__ void k_scale_to(double* __restrict__ out, const double* __restrict__ in, const double* s, int n,
@@ -163,7 +166,8 @@ __global__ void k_scale_to(double* __restrict__ out, const double* __restrict__ 
 
 // GMRES: h[k] = V[:,k]ᵀ w for k < nk, one CTA per basis vector (fixed-order reduction)
 __global__ void k_multidot(const double* __restrict__ V, long long ldv, const double* __restrict__ w, int n,
-                           double* __restrict__ h) {
+                           double* __restrict__ h, const int* __restrict__ live = nullptr) {
+  if (live && *live) return;
   const int k = blockIdx.x;
   const double* v = V + k * ldv;
   double s = 0.0;
@@ -173,7 +177,8 @@ __global__ void k_multidot(const double* __restrict__ V, long long ldv, const do
 }
 // w -= V h (nk columns); optionally accumulate h into hacc
 __global__ void k_multiaxpy(const double* __restrict__ V, long long ldv, double* __restrict__ w, int n,
-                            const double* __restrict__ h, int nk) {
+                            const double* __restrict__ h, int nk, const int* __restrict__ live = nullptr) {
+  if (live && *live) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double s = w[i];
     for (int k = 0; k < nk; ++k) s -= h[k] * V[k * ldv + i];
@@ -182,7 +187,9 @@ __global__ void k_multiaxpy(const double* __restrict__ V, long long ldv, double*
 }
 // x += V y
 __global__ void k_combine(const double* __restrict__ V, long long ldv, const double* __restrict__ y, int nk,
-                          const double* __restrict__ x0, double* __restrict__ x, int n) {
+                          const double* __restrict__ x0, double* __restrict__ x, int n,
+                          const int* __restrict__ live = nullptr) {
+  if (live && *live) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double s = x0[i];
     for (int k = 0; k < nk; ++k) s += y[k] * V[k * ldv + i];
@@ -196,6 +203,94 @@ __global__ void k_scal_div(double* __restrict__ out, const double* __restrict__ 
 // out = ca·a + cb·b (out may alias a or b)
 __global__ void k_lincomb(double* out, const double* a, double ca, const double* b, double cb, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = ca * a[i] + cb * b[i];
+}
+
+// ---- GMRES(m) cycle on the device (krylov.hpp:275-389): the Hessenberg column, the Givens
+// rotations, the residual estimate and the stopping tests of each Arnoldi step run in one warp, so
+// the host launches whole chunks of steps without reading anything back; steps launched after the
+// stop exit on the status word (Arnoldi is append-only, so the stopped state is exact).
+enum { GM_RUN = 0, GM_CONV = 1, GM_BREAK = 2, GM_MAXIT = 3, GM_CYCLE = 4 };
+struct GmState {
+  int stop;   // GM_*
+  int tr;     // 0 while the true residual of the latest step is pending
+  int it;     // iterations so far (all cycles)
+  int k;      // steps done in this cycle
+  int max_it, len, ident, true_res;
+  double gnorm0, bnorm, tol, hnext;
+};
+
+// step k: H[:, k] = hA + hB (CGS2), hnext = ‖w‖; previous rotations, new rotation, g; residual
+// estimate; stopping tests in the reference's order (breakdown, converged/lucky, cap, cycle end)
+__global__ void k_gm_step(GmState* st, const double* __restrict__ hA, const double* __restrict__ hB,
+                          const double* __restrict__ part, int k, double* __restrict__ H, int ldh,
+                          double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ g,
+                          double* __restrict__ y, double* __restrict__ hist, double* __restrict__ thist) {
+  if (st->stop != GM_RUN) return;
+  const double hnext = sqrt(warp_sum_parts(part, kRB));
+  if (threadIdx.x != 0) return;
+  double* col = H + static_cast<long long>(k) * ldh;
+  for (int i = 0; i <= k; ++i) col[i] = hA[i] + hB[i];
+  col[k + 1] = hnext;
+  for (int i = 0; i < k; ++i) {
+    const double t = cs[i] * col[i] + sn[i] * col[i + 1];
+    col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+    col[i] = t;
+  }
+  const double denom = hypot(col[k], col[k + 1]);
+  if (denom == 0.0) {
+    st->stop = GM_BREAK;
+    return;
+  }
+  cs[k] = col[k] / denom;
+  sn[k] = col[k + 1] / denom;
+  col[k] = denom;
+  col[k + 1] = 0.0;
+  g[k + 1] = -sn[k] * g[k];
+  g[k] *= cs[k];
+  const double rel = fabs(g[k + 1]) / st->gnorm0;
+  const int it = ++st->it;
+  st->k = k + 1;
+  st->hnext = hnext;
+  hist[it] = rel;
+  if (st->ident) {
+    thist[it] = rel;
+  } else if (st->true_res) {  // y for the diagnostic true residual (krylov.hpp:360-367)
+    for (int i = k; i >= 0; --i) {
+      double s = g[i];
+      for (int j = i + 1; j <= k; ++j) s -= H[i + static_cast<long long>(j) * ldh] * y[j];
+      y[i] = s / H[i + static_cast<long long>(i) * ldh];
+    }
+    st->tr = 0;
+  } else {
+    thist[it] = -1.0;
+  }
+  if (rel <= st->tol || hnext == 0.0) st->stop = GM_CONV;
+  else if (it >= st->max_it) st->stop = GM_MAXIT;
+  else if (k + 1 == st->len) st->stop = GM_CYCLE;
+}
+// w /= hnext (skipped once stopped, and for hnext = 0)
+__global__ void k_gm_scale(GmState* st, double* __restrict__ w, int n) {
+  if (st->stop != GM_RUN) return;
+  const double h = st->hnext;
+  if (h == 0.0) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) w[i] = w[i] / h;
+}
+__global__ void k_gm_thist(GmState* st, const double* __restrict__ part, double* __restrict__ thist) {
+  if (st->tr != 0) return;
+  const double rn = sqrt(warp_sum_parts(part, kRB));
+  if (threadIdx.x != 0) return;
+  thist[st->it] = st->bnorm > 0.0 ? rn / st->bnorm : 0.0;
+  st->tr = 1;
+}
+// y = R⁻¹ g for the kk steps of the cycle (back substitution on the rotated Hessenberg)
+__global__ void k_gm_ysolve(const double* __restrict__ H, int ldh, const double* __restrict__ g, int kk,
+                            double* __restrict__ y) {
+  if (threadIdx.x != 0) return;
+  for (int i = kk - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int j = i + 1; j < kk; ++j) s -= H[i + static_cast<long long>(j) * ldh] * y[j];
+    y[i] = s / H[i + static_cast<long long>(i) * ldh];
+  }
 }
 
 struct Vecs {
@@ -376,6 +471,7 @@ static void gmres_solve(Ctx& c, const double* b, double* x, double tol, int max_
   const bool ident = c.pkind == RDD_PRECOND_NONE;
   const bool true_res = c.cfg.true_residual != 0;
   double* part = c.scal.ensure(8 * kRB + 64);
+  double* part2 = part + 2 * kRB;
   auto& hist = c.hist[comp];
   auto& thist = c.true_hist[comp];
   hist.clear();
@@ -402,16 +498,32 @@ static void gmres_solve(Ctx& c, const double* b, double* x, double tol, int max_
   if (restart == 0 && cycle_len > 4096)
     throw std::runtime_error("full GMRES basis of " + std::to_string(cycle_len) +
                              " vectors exceeds the cap; configure gmres_restart");
-  DBuf<double> Vb, hd;
+  const int ldh = cycle_len + 1;
+  DBuf<double> Vb, hv, Hd, dhist, dthist;
   Vb.ensure(static_cast<size_t>(cycle_len + 1) * n);
-  hd.ensure(2 * (cycle_len + 2));
-  hist.push_back(1.0);
-  thist.push_back(bnorm > 0.0 ? 1.0 : 0.0);
-  int iters_left = max_iter;
+  hv.ensure(static_cast<size_t>(5 * (cycle_len + 2)));  // hA, hB, cs, sn, g / y
+  double *hA = hv.p, *hB = hA + (cycle_len + 2), *cs = hB + (cycle_len + 2), *sn = cs + (cycle_len + 2),
+         *g = sn + (cycle_len + 2);
+  DBuf<double> yv;
+  yv.ensure(cycle_len + 2);
+  Hd.ensure(static_cast<size_t>(ldh) * cycle_len);
+  dhist.ensure(static_cast<size_t>(max_iter) + 2);
+  dthist.ensure(static_cast<size_t>(max_iter) + 2);
+  DBuf<GmState> st;
+  st.ensure(1);
+  GmState hs{};
+  double one = 1.0, tb = bnorm > 0.0 ? 1.0 : 0.0;
+  RDD_CUDA(cudaMemcpyAsync(dhist.p, &one, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  RDD_CUDA(cudaMemcpyAsync(dthist.p, &tb, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  int it = 0;
   bool converged = false, breakdown = false;
-  std::vector<double> Hm, cs, sn, gv, hh(cycle_len + 2), hh2(cycle_len + 2);
-  auto Hat = [&](int i, int k) -> double& { return Hm[static_cast<size_t>(k) * (cycle_len + 1) + i]; };
-  while (iters_left > 0 && !converged && !breakdown) {
+  struct LiveScope {
+    Ctx& c;
+    explicit LiveScope(Ctx& cc) : c(cc) {}
+    ~LiveScope() { c.live = nullptr; }
+  } ls(c);
+  constexpr int kChunk = 8;  // Arnoldi steps launched between status reads
+  while (it < max_iter && !converged && !breakdown) {
     normal_operator(c, x, t1);
     k_sub<<<kRB, kRT, 0, c.stream>>>(t2, b, t1, n);  // b - A x
     RDD_LAUNCH_CHECK();
@@ -422,104 +534,77 @@ static void gmres_solve(Ctx& c, const double* b, double* x, double tol, int max_
       converged = true;
       break;
     }
-    const int len = std::min(cycle_len, iters_left);
+    const int len = std::min(cycle_len, max_iter - it);
     k_scal_div<<<kRB, kRT, 0, c.stream>>>(Vb.p, t1, beta, n);
     RDD_LAUNCH_CHECK();
-    Hm.assign(static_cast<size_t>(len + 1) * (cycle_len + 1), 0.0);
-    cs.assign(len, 0.0);
-    sn.assign(len, 0.0);
-    gv.assign(len + 1, 0.0);
-    gv[0] = beta;
-    int k = 0;
-    for (; k < len;) {
-      double* vk = Vb.p + static_cast<size_t>(k) * n;
-      double* w = Vb.p + static_cast<size_t>(k + 1) * n;
-      if (ident) {
-        normal_operator(c, vk, w);
-      } else {
-        normal_operator(c, vk, t1);
-        precond(c, t1, w);
-      }
-      // CGS2: h = Vᵀw; w -= V h (twice)
-      for (int pass = 0; pass < 2; ++pass) {
-        k_multidot<<<k + 1, kRT, 0, c.stream>>>(Vb.p, n, w, n, hd.p);
-        k_multiaxpy<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, w, n, hd.p, k + 1);
-        RDD_LAUNCH_CHECK();
-        RDD_CUDA(cudaMemcpyAsync(pass == 0 ? hh.data() : hh2.data(), hd.p, sizeof(double) * (k + 1),
-                                 cudaMemcpyDeviceToHost, c.stream));
-        RDD_CUDA(cudaStreamSynchronize(c.stream));
-      }
-      for (int i = 0; i <= k; ++i) Hat(i, k) = hh[i] + hh2[i];
-      const double hnext = std::sqrt(dot_host(c, w, w, n, part));
-      Hat(k + 1, k) = hnext;
-      if (hnext > 0.0) {
-        k_scal_div<<<kRB, kRT, 0, c.stream>>>(w, w, hnext, n);
-        RDD_LAUNCH_CHECK();
-      }
-      for (int i = 0; i < k; ++i) {
-        const double t = cs[i] * Hat(i, k) + sn[i] * Hat(i + 1, k);
-        Hat(i + 1, k) = -sn[i] * Hat(i, k) + cs[i] * Hat(i + 1, k);
-        Hat(i, k) = t;
-      }
-      const double denom = std::hypot(Hat(k, k), Hat(k + 1, k));
-      if (denom == 0.0) {
-        breakdown = true;
-        break;
-      }
-      cs[k] = Hat(k, k) / denom;
-      sn[k] = Hat(k + 1, k) / denom;
-      Hat(k, k) = denom;
-      Hat(k + 1, k) = 0.0;
-      gv[k + 1] = -sn[k] * gv[k];
-      gv[k] *= cs[k];
-      const double rel = std::fabs(gv[k + 1]) / gnorm0;
-      hist.push_back(rel);
-      ++c.iters[comp];
-      --iters_left;
-      ++k;
-      auto ysolve = [&](int kk) {
-        std::vector<double> y(kk);
-        for (int i = kk - 1; i >= 0; --i) {
-          double s = gv[i];
-          for (int j = i + 1; j < kk; ++j) s -= Hat(i, j) * y[j];
-          y[i] = s / Hat(i, i);
+    GmState s0{};
+    s0.stop = GM_RUN;
+    s0.tr = 1;
+    s0.it = it;
+    s0.max_it = max_iter;
+    s0.len = len;
+    s0.ident = ident ? 1 : 0;
+    s0.true_res = true_res ? 1 : 0;
+    s0.gnorm0 = gnorm0;
+    s0.bnorm = bnorm;
+    s0.tol = tol;
+    st.upload(&s0, 1, c.stream);
+    RDD_CUDA(cudaMemcpyAsync(g, &beta, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    for (int k0 = 0; k0 < len; k0 += kChunk) {
+      for (int k = k0; k < std::min(len, k0 + kChunk); ++k) {
+        double* vk = Vb.p + static_cast<size_t>(k) * n;
+        double* w = Vb.p + static_cast<size_t>(k + 1) * n;
+        c.live = &st.p->stop;
+        if (ident) {
+          normal_operator(c, vk, w);
+        } else {
+          normal_operator(c, vk, t1);
+          precond(c, t1, w);
         }
-        return y;
-      };
-      if (ident) {
-        thist.push_back(rel);
-      } else if (true_res) {  // diagnostic true residual (krylov.hpp:360-367)
-        const std::vector<double> y = ysolve(k);
-        RDD_CUDA(cudaMemcpyAsync(hd.p, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c.stream));
-        k_combine<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, hd.p, k, x, xk, n);
+        // CGS2: h = Vᵀw; w -= V h (twice)
+        k_multidot<<<k + 1, kRT, 0, c.stream>>>(Vb.p, n, w, n, hA, c.live);
+        k_multiaxpy<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, w, n, hA, k + 1, c.live);
+        k_multidot<<<k + 1, kRT, 0, c.stream>>>(Vb.p, n, w, n, hB, c.live);
+        k_multiaxpy<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, w, n, hB, k + 1, c.live);
+        k_dot_part<<<kRB, kRT, 0, c.stream>>>(w, w, n, part, c.live);
         RDD_LAUNCH_CHECK();
-        normal_operator(c, xk, t1);
-        k_sub<<<kRB, kRT, 0, c.stream>>>(rr, b, t1, n);
+        k_gm_step<<<1, 32, 0, c.stream>>>(st.p, hA, hB, part, k, Hd.p, ldh, cs, sn, g, yv.p, dhist.p, dthist.p);
         RDD_LAUNCH_CHECK();
-        const double rn = std::sqrt(dot_host(c, rr, rr, n, part));
-        thist.push_back(bnorm > 0.0 ? rn / bnorm : 0.0);
-      } else {
-        thist.push_back(-1.0);
+        k_gm_scale<<<kRB, kRT, 0, c.stream>>>(st.p, w, n);
+        RDD_LAUNCH_CHECK();
+        if (!ident && true_res) {  // diagnostic true residual ‖b − A x_k‖ (krylov.hpp:360-367)
+          c.live = &st.p->tr;
+          k_combine<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, yv.p, k + 1, x, xk, n, c.live);
+          RDD_LAUNCH_CHECK();
+          normal_operator(c, xk, t1);
+          k_sub<<<kRB, kRT, 0, c.stream>>>(rr, b, t1, n, c.live);
+          k_dot_part<<<kRB, kRT, 0, c.stream>>>(rr, rr, n, part2, c.live);
+          RDD_LAUNCH_CHECK();
+          k_gm_thist<<<1, 32, 0, c.stream>>>(st.p, part2, dthist.p);
+          RDD_LAUNCH_CHECK();
+        }
+        c.live = nullptr;
       }
-      if (rel <= tol || hnext == 0.0) {
-        converged = true;
-        break;
-      }
-      if (iters_left == 0) break;
+      st.download(&hs, 1, c.stream);
+      RDD_CUDA(cudaStreamSynchronize(c.stream));
+      if (hs.stop != GM_RUN) break;
     }
-    if (k > 0) {
-      std::vector<double> y(k);
-      for (int i = k - 1; i >= 0; --i) {
-        double s = gv[i];
-        for (int j = i + 1; j < k; ++j) s -= Hat(i, j) * y[j];
-        y[i] = s / Hat(i, i);
-      }
-      RDD_CUDA(cudaMemcpyAsync(hd.p, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c.stream));
-      k_combine<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, hd.p, k, x, x, n);
+    it = hs.it;
+    if (hs.k > 0) {  // x += V y
+      k_gm_ysolve<<<1, 32, 0, c.stream>>>(Hd.p, ldh, g, hs.k, yv.p);
+      RDD_LAUNCH_CHECK();
+      k_combine<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, yv.p, hs.k, x, x, n);
       RDD_LAUNCH_CHECK();
     }
-    if (restart == 0 && !converged && !breakdown && iters_left > 0 && k == cycle_len) break;
+    if (hs.stop == GM_CONV) converged = true;
+    if (hs.stop == GM_BREAK) breakdown = true;
+    if (restart == 0 && !converged && !breakdown && it < max_iter && hs.k == cycle_len) break;
   }
+  c.iters[comp] = it;
+  hist.resize(it + 1);
+  thist.resize(it + 1);
+  dhist.download(hist.data(), it + 1, c.stream);
+  dthist.download(thist.data(), it + 1, c.stream);
   RDD_CUDA(cudaStreamSynchronize(c.stream));
   c.conv[comp] = converged;
   c.brk[comp] = breakdown;

@@ -751,11 +751,21 @@ std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector
   std::vector<double> out(B, 0.0);
   if (B == 0) return out;
   const int nmax = *std::max_element(n.begin(), n.end());
+  // largest blocks first (one CTA each, time ∝ n²): no big block starts in the last wave
+  std::vector<int> perm(B);
+  for (int b = 0; b < B; ++b) perm[b] = b;
+  std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return n[a] > n[b]; });
+  std::vector<int> ns(B);
+  std::vector<long long> ps(B);
+  for (int b = 0; b < B; ++b) {
+    ns[b] = n[perm[b]];
+    ps[b] = poff[perm[b]];
+  }
   DBuf<int> dn;
   DBuf<long long> dp;
   DBuf<double> d;
-  dn.upload(n, c.stream);
-  dp.upload(poff, c.stream);
+  dn.upload(ns, c.stream);
+  dp.upload(ps, c.stream);
   d.ensure(B);
   const size_t smem = chol_solve_smem(nmax, inverse);
   if (c.verbose) std::fprintf(stderr, "[inv_power] B=%d nmax=%d smem=%zu iters=%d\n", B, nmax, smem, iters);
@@ -763,8 +773,10 @@ std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector
   k_chol_power<<<B, kSolveWarps * 32, smem, c.stream>>>(P, dp.p, dn.p, iters, ceil_div(nmax, NB), d.p,
                                                         inverse ? 1 : 0);
   RDD_LAUNCH_CHECK();
-  d.download(out.data(), B, c.stream);
+  std::vector<double> sorted(B);
+  d.download(sorted.data(), B, c.stream);
   RDD_CUDA(cudaStreamSynchronize(c.stream));
+  for (int b = 0; b < B; ++b) out[perm[b]] = sorted[b];
   return out;
 }
 
@@ -775,13 +787,17 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
     const double* __restrict__ P, const long long* __restrict__ poff, const double* const* __restrict__ dense,
     const int* __restrict__ set_ptr, const int* __restrict__ set_idx, const double* __restrict__ v,
     const int* __restrict__ mult, const int* __restrict__ owner, int kind, int transpose, int nbmax,
-    double* __restrict__ z, int inverse, long long zhalf, const int* __restrict__ live) {
+    double* __restrict__ z, int inverse, long long zhalf, const int* __restrict__ live,
+    const int* __restrict__ order) {
   if (live && *live != 0) return;  // solver loop already stopped (speculative graph iteration)
   extern __shared__ double sm[];
   double* g = sm;
   double* red = sm + static_cast<size_t>(nbmax) * NB;
-  // inverse mode: two CTAs per subdomain, each over every other tile, partials to z and z + zhalf
-  const int i = inverse ? blockIdx.x >> 1 : blockIdx.x;
+  // inverse mode: two CTAs per subdomain, each over every other tile, partials to z and z + zhalf.
+  // CTAs take the subdomains largest first (order): the per-CTA streaming time grows with n_i²,
+  // so the biggest local solves must not start in the last wave
+  const int bi = inverse ? blockIdx.x >> 1 : blockIdx.x;
+  const int i = order ? order[bi] : bi;
   const int h = inverse ? blockIdx.x & 1 : 0;
   const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0, nb = (n + NB - 1) / NB;
   for (int q = threadIdx.x; q < nb * NB; q += blockDim.x) {
@@ -822,7 +838,8 @@ void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
   }
   k_chol_apply<<<c.inv_mode ? 2 * c.J : c.J, kSolveWarps * 32, smem, c.stream>>>(
       c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p, v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
-      ceil_div(c.nmax_local, NB), zloc, c.inv_mode ? 1 : 0, static_cast<long long>(c.set_idx.size()), c.live);
+      ceil_div(c.nmax_local, NB), zloc, c.inv_mode ? 1 : 0, static_cast<long long>(c.set_idx.size()), c.live,
+      c.apply_order.p);
   RDD_LAUNCH_CHECK();
 }
 

@@ -148,6 +148,7 @@ struct Ctx {
   std::vector<GatherTask> gat_tasks;
   double full_rank_cond = 1e11;       // Cholesky path when cond_est(A_i) is below this
   DBuf<double> zloc;                  // Σ n_i
+  DBuf<int> apply_order;              // subdomains by local size, largest first (apply CTA order)
 
   // ---- Krylov
   DBuf<double> work;                  // vectors

@@ -307,6 +307,12 @@ void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre) {
   // local matrix sizes and gather plan (schwarz.hpp:112-130): A_i blocks come from NB. The pair
   // (j1, j2) is looked up in j1's sorted neighbour list (normal blocks exist for neighbour pairs).
   c.local_n = n;
+  {
+    std::vector<int> ord(J);
+    for (int i = 0; i < J; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return n[a] > n[b]; });
+    c.apply_order.upload(ord, c.stream);
+  }
   c.gat_tasks.clear();
   std::vector<int> po;
   for (int i = 0; i < J; ++i) {

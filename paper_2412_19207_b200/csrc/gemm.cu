@@ -62,16 +62,26 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmTask* __restrict__ tasks)
 
   auto As = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStageA; };
   auto Bs = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStageA + kStageA; };
+  // row-gather indices (TN normal blocks) for the stage issued next are loaded one issue ahead, so
+  // the dependent index read does not stall the cp.async issue of every stage
+  int gia = 0, gib = 0;
+  auto gidx = [&](int kt) {
+    const int k = kt * BK + (tid & 15);
+    gia = (AT && T.gA && k < T.K) ? __ldg(T.gA + k) : k;
+    gib = (!BT && T.gB && k < T.K) ? __ldg(T.gB + k) : k;
+  };
+  gidx(0);
   auto issue = [&](int kt, int s) {
     const int k0 = kt * BK;
     double* a = As(s);
     double* bsm = Bs(s);
+    const int ga = gia, gb = gib;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (AT) {  // A(k, m) = A[k + m*lda] -> a[m][k]
         const int k = k0 + (tid & 15), ml = (tid >> 4) + 8 * i, m = m0 + ml;
         const bool v = k < T.K && m < T.M;
-        const long long kk = v ? (T.gA ? T.gA[k] : k) : 0;
+        const long long kk = v ? ga : 0;
         cp_async8(a + ml * KP + (tid & 15), v ? T.A + kk + static_cast<long long>(m) * T.lda : T.A, v);
       } else {  // A(m, k) = A[m + k*lda] -> a[k][m]
         const int ml = tid & 63, m = m0 + ml, kl = (tid >> 6) + 2 * i, k = k0 + kl;
@@ -81,7 +91,7 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmTask* __restrict__ tasks)
       if (!BT) {  // B(k, n) = B[k + n*ldb] -> b[n][k]
         const int k = k0 + (tid & 15), nl = (tid >> 4) + 8 * i, n = n0 + nl;
         const bool v = k < T.K && n < T.N;
-        const long long kk = v ? (T.gB ? T.gB[k] : k) : 0;
+        const long long kk = v ? gb : 0;
         cp_async8(bsm + nl * KP + (tid & 15), v ? T.B + kk + static_cast<long long>(n) * T.ldb : T.B, v);
       } else {  // B(k, n) = Bt[n + k*ldb] -> b[k][n]
         const int nl = tid & 63, n = n0 + nl, kl = (tid >> 6) + 2 * i, k = k0 + kl;
@@ -89,6 +99,7 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmTask* __restrict__ tasks)
         cp_async8(bsm + kl * MP + nl, v ? T.B + n + static_cast<long long>(k) * T.ldb : T.B, v);
       }
     }
+    gidx(kt + 1);
   };
 
   const int nk = (T.K + BK - 1) / BK;

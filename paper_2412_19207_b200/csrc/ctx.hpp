@@ -88,6 +88,8 @@ struct Ctx {
   DBuf<int> row_ptr, row_idx;
   int maxcov = 0;
   DBuf<int> cov_j, cov_r, cov_n;
+  DBuf<double> ax_lo, ax_hi;          // per-axis box intervals (axis-major), for cover searches
+  int ax_counts[kMaxDim] = {1, 1, 1, 1}, ax_stride[kMaxDim] = {0, 0, 0, 0}, ax_off[kMaxDim] = {0, 0, 0, 0};
   long long sum_rows = 0;
 
   // ---- PCA (K2-K5)

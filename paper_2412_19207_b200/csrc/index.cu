@@ -225,9 +225,15 @@ void build_index(Ctx& c) {
       ahi.push_back(c.axis_hi[a][k]);
     }
   }
-  DBuf<double> dlo, dhi;
+  DBuf<double>& dlo = c.ax_lo;  // kept: the evaluation finds test-point covers the same way
+  DBuf<double>& dhi = c.ax_hi;
   dlo.upload(alo, c.stream);
   dhi.upload(ahi, c.stream);
+  for (int a = 0; a < kMaxDim; ++a) {
+    c.ax_counts[a] = a < c.d ? A.counts[a] : 1;
+    c.ax_stride[a] = a < c.d ? A.stride[a] : 0;
+    c.ax_off[a] = a < c.d ? A.off[a] : 0;
+  }
   const int nchunks = ceil_div(N, kChunk);
   DBuf<int> chunk, totals, err, mx;
   chunk.zero(static_cast<size_t>(nchunks) * J, c.stream);

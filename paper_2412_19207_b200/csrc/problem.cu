@@ -275,6 +275,9 @@ struct EvalArgs {
   double* exact;
   const double* ref;      // example2: reference field (refn x refn), else null
   int refn;
+  const double* ax_lo;    // per-axis box intervals: the covering boxes of a test point
+  const double* ax_hi;
+  int ax_counts[kMaxDim], ax_stride[kMaxDim], ax_off[kMaxDim];
 };
 
 // problems.hpp:203-216 ReferenceGrid::at: bilinear lookup in the space-time field
@@ -323,7 +326,37 @@ __global__ void k_evaluate(EvalArgs A) {
   }
   const double Lv = L_jet(A.P, x).c[0];
   double acc[3] = {0.0, 0.0, 0.0};
-  for (int j = 0; j < A.J; ++j) {
+  // covering boxes (geometry.hpp:180-185): per-axis closed-interval candidates, enumerated as the
+  // lexicographic product (axis 0 slowest) = ascending j, the reference's accumulation order
+  int cand[kMaxDim][8], nc[kMaxDim];
+  bool any = true, full = false;  // full: more than 8 candidates on an axis -> scan every box
+  for (int a = 0; a < d && any; ++a) {
+    nc[a] = 0;
+    for (int k = 0; k < A.ax_counts[a]; ++k) {
+      const double lo = A.ax_lo[A.ax_off[a] + k], hi = A.ax_hi[A.ax_off[a] + k];
+      if (!(x[a] < lo || x[a] > hi)) {
+        if (nc[a] < 8) cand[a][nc[a]++] = k;
+        else full = true;
+      }
+    }
+    any = nc[a] > 0;
+  }
+  int itc[kMaxDim] = {0, 0, 0, 0};
+  int jf = 0;
+  for (bool more = full || any; more;) {
+    int j = 0;
+    if (full) {
+      j = jf++;
+      more = jf < A.J;
+    } else {
+      for (int a = 0; a < d; ++a) j += cand[a][itc[a]] * A.ax_stride[a];
+      int a = d - 1;
+      for (; a >= 0; --a) {
+        if (++itc[a] < nc[a]) break;
+        itc[a] = 0;
+      }
+      more = a >= 0;
+    }
     const double wj = raw_wv(A, j, x);
     if (wj == 0.0) continue;  // covering_subdomains + zero window (basis.hpp:169-176)
     double tot = 0.0;
@@ -406,6 +439,13 @@ void evaluate(Ctx& c, const int* test_res) {
   counts1.upload(h_c1, c.stream);
   A.box = c.dbox.p;
   A.counts1 = counts1.p;
+  A.ax_lo = c.ax_lo.p;
+  A.ax_hi = c.ax_hi.p;
+  for (int a = 0; a < kMaxDim; ++a) {
+    A.ax_counts[a] = c.ax_counts[a];
+    A.ax_stride[a] = c.ax_stride[a];
+    A.ax_off[a] = c.ax_off[a];
+  }
   A.nbr_ptr = c.dnbr_ptr.p;
   A.nbr_idx = c.dnbr_idx.p;
   A.R = c.R.p;

@@ -62,8 +62,14 @@ static void reset_state(Ctx& c) {
 // runner.hpp:40-70
 static void build_instance(Ctx& c, const rdd_config& cfg, uint64_t seed) {
   reset_state(c);
+  const double h0 = now_s();
   setup_problem(c, cfg, seed);
+  const double h1 = now_s();
   upload_inputs(c);
+  if (c.verbose) {
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    std::fprintf(stderr, "[host] setup %.3f ms, upload %.3f ms\n", 1e3 * (h1 - h0), 1e3 * (now_s() - h1));
+  }
   build_index(c);
   eval_problem(c);
   run_pca(c);

@@ -267,3 +267,20 @@ def test_example2_reference_field(dev, orc):
     bad.ref_resolution = 100
     with pytest.raises(ValueError, match="resolution must be >= 501"):
         dev.run_single(bad)
+
+
+@pytest.mark.parametrize("restart,max_iter", [(3, 10), (5, 7), (0, 6), (4, 4)])
+def test_gmres_cycles_and_caps(dev, orc, restart, max_iter):
+    # restarted GMRES(m) (krylov.hpp:275-389) with the iteration cap landing inside, at the end of, or
+    # before the end of a cycle: iteration counts, convergence flags and both residual histories
+    cfg = configs.scaled(configs.c4(), [4, 2], 8, m=40)  # RAS-GMRES needs tens of steps here
+    cfg.solver, cfg.precond, cfg.rel_tol = A.SOLVER_GMRES, A.PRECOND_RAS, 1e-14
+    cfg.gmres_restart, cfg.max_iter = restart, max_iter
+    sd, so = dev.run_single(cfg), orc.run_single(cfg)
+    assert sd["iterations"] == so["iterations"] == max_iter
+    assert sd["converged"] == so["converged"] == 0
+    hd, ho = dev.getd("hist"), orc.getd("hist")
+    td, to = dev.getd("true_hist"), orc.getd("true_hist")
+    assert len(hd) == len(ho) == max_iter + 1 and len(td) == len(to) == max_iter + 1
+    assert np.allclose(hd, ho, rtol=1e-6, atol=1e-14) and np.allclose(td, to, rtol=1e-6, atol=1e-14)
+    assert sd["e_l2"] == pytest.approx(so["e_l2"], rel=1e-6)

@@ -1,6 +1,9 @@
-"""FP64 tensor throughput of the Gram (PCA) and the Schwarz Cholesky for a config, from the
-library's per-family CUDA-event timers and the algorithmic flop counts:
-Gram Σ_j rows_j·m·(m+1) (symmetric), Cholesky Σ_i n_i³/3."""
+"""FP64 throughput of the Gram (PCA), the Schwarz Cholesky and the collocation assembly for a config,
+from the library's per-family CUDA-event timers and the algorithmic flop counts:
+Gram Σ_j rows_j·m·(m+1) (symmetric), Cholesky Σ_i n_i³/3 — against the measured DGEMM peak;
+assembly (4d+12) flops + one tanh (counted as 20) per (row, neuron) entry of the unreduced
+sample blocks, i.e. 40 (d=2) / 44 (d=3) per entry — against the measured FP64 FMA-pipe peak
+(tools/fp64_peak.py)."""
 import json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -20,10 +23,16 @@ m = cfg.m
 n = s.geti("local_n").astype(np.float64)
 g_ms, _ = s.kernel_stats("gram")
 c_ms, _ = s.kernel_stats("cholesky")
+a_ms, a_n = s.kernel_stats("assemble")
 gram = float((rows * m * (m + 1)).sum())
 chol = float((n ** 3 / 3).sum())
+d = cfg.d
+asm = float((rows * m).sum()) * (4 * d + 12 + 20)
+fma_peak = float(sys.argv[2]) if len(sys.argv) > 2 else 36.9  # TF/s, DFMA pipe (tools/fp64_peak.py)
 peak = 35.46  # TF/s, cuBLAS DGEMM measured on this B200 (tools/fp64_peak.py, DMMA pipe 96.5% busy)
 out = {"config": name, "gram_ms": g_ms, "gram_tflops": gram / g_ms / 1e9, "gram_frac": gram / g_ms / 1e9 / peak,
        "chol_ms": c_ms, "chol_tflops": chol / c_ms / 1e9, "chol_frac": chol / c_ms / 1e9 / peak,
-       "sum_n3_over_3": chol, "n_max": int(n.max()), "peak_tflops": peak}
+       "sum_n3_over_3": chol,
+       "assemble_ms": a_ms, "assemble_launches": a_n, "assemble_entries": float((rows * m).sum()),
+       "assemble_tflops": asm / a_ms / 1e9, "assemble_frac": asm / a_ms / 1e9 / fma_peak, "fma_peak_tflops": fma_peak, "n_max": int(n.max()), "peak_tflops": peak}
 print(json.dumps(out))

@@ -28,7 +28,7 @@ gram = float((rows * m * (m + 1)).sum())
 chol = float((n ** 3 / 3).sum())
 d = cfg.d
 asm = float((rows * m).sum()) * (4 * d + 12 + 20)
-fma_peak = float(sys.argv[2]) if len(sys.argv) > 2 else 36.9  # TF/s, DFMA pipe (tools/fp64_peak.py)
+fma_peak = float(sys.argv[2]) if len(sys.argv) > 2 else 36.59  # TF/s, DFMA pipe measured (tools/fp64_peak.py)
 peak = 35.46  # TF/s, cuBLAS DGEMM measured on this B200 (tools/fp64_peak.py, DMMA pipe 96.5% busy)
 out = {"config": name, "gram_ms": g_ms, "gram_tflops": gram / g_ms / 1e9, "gram_frac": gram / g_ms / 1e9 / peak,
        "chol_ms": c_ms, "chol_tflops": chol / c_ms / 1e9, "chol_frac": chol / c_ms / 1e9 / peak,

@@ -5,7 +5,7 @@ hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[hi]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
 tot, cnt = collections.defaultdict(float), collections.Counter()
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}
 for r in rows[hi + 1:]:
     if len(r) <= vi:
         continue

@@ -11,6 +11,8 @@
 // i.e. (2d+6) FMAs + one activation per entry. Output blocks are column-major
 // (rows_j x m); a thread owns a row and streams across neurons, so each neuron's column is
 // written by a warp as 32 consecutive doubles (coalesced).
+#include <type_traits>
+
 #include "ctx.hpp"
 
 namespace rdd {
@@ -46,9 +48,10 @@ __device__ __forceinline__ bool in_box(const double* box, const double* x, int d
   return true;
 }
 
-// basis.hpp:121-138 raw_window_jet
-__device__ Jet raw_window_jet(const AsmArgs& A, int k, const double* x) {
-  const int d = A.d;
+// basis.hpp:121-138 raw_window_jet (D compile-time: the jet loops unroll, jets stay in registers)
+template <int D>
+__device__ __forceinline__ Jet raw_window_jet(const AsmArgs& A, int k, const double* x) {
+  constexpr int d = D;
   Jet prod;
   jet_zero(prod, d);
   const double* bx = A.box + 16 * static_cast<size_t>(k);
@@ -86,107 +89,41 @@ __device__ double raw_window_value(const AsmArgs& A, int k, const double* x) {  
   return prod;
 }
 
-__global__ void __launch_bounds__(kRowsPerBlock) k_assemble(AsmArgs A) {
-  extern __shared__ double sm[];
-  const int tile = blockIdx.x;
-  // find the subdomain owning this tile
-  int lo = 0, hi = A.J;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (A.tile_ptr[mid] <= tile) lo = mid;
-    else hi = mid;
-  }
-  const int j = lo;
-  const int d = A.d, m = A.m, jl = jet_len(d);
-  const int rows = A.row_ptr[j + 1] - A.row_ptr[j];
-  const int r = (tile - A.tile_ptr[j]) * kRowsPerBlock + threadIdx.x;
-  const double* bx = A.box + 16 * static_cast<size_t>(j);
+// per-row constants of the op_applied entries, held in registers across the neuron loop
+template <int D>
+struct RowCoef {
+  double xh[D];   // local coordinates in [-1, 1]^d
+  double lwg[D];  // ∇(L·ω_j)
+  double lwv;     // L·ω_j
+  double alpha;   // A[L·ω_j] (operator applied to the jet)
+};
 
-  // per-neuron parameters: [b, R(d), h(d), q1, q2]
-  const int np = 3 + 2 * d;
-  double w_[kMaxDim];
-  for (int a = 0; a < d; ++a) w_[a] = 2.0 / (bx[4 + a] - bx[a]);  // normalize_scales (geometry.hpp:71-75)
-  for (int k = threadIdx.x; k < m; k += blockDim.x) {
-    double* P = sm + static_cast<size_t>(k) * np;
-    const double* Rk = A.R + (static_cast<size_t>(j) * m + k) * d;
-    P[0] = A.b[static_cast<size_t>(j) * m + k];
-    double g[kMaxDim];
-    for (int a = 0; a < d; ++a) {
-      P[1 + a] = Rk[a];
-      g[a] = Rk[a] * w_[a];
-    }
-    double q1 = 0.0, q2 = 0.0;
-    for (int a = 0; a < d; ++a) {
-      q1 += A.coef[1 + a] * g[a];
-      double h = 0.0;
-      for (int bb = 0; bb < d; ++bb) {
-        const double cab = A.coef[1 + d + hess_index(min(a, bb), max(a, bb), d)];
-        h += (a == bb ? 2.0 * cab : cab) * g[bb];
-        if (bb >= a) q2 += cab * g[a] * g[bb];
-      }
-      P[1 + d + a] = h;
-    }
-    P[1 + 2 * d] = q1;
-    P[2 + 2 * d] = q2;
+// the neuron loop of one row: z = b + R·x̂, entry = α·t(z) + β·t'(z) + (LW·q2)·t''(z) with
+// β = LW·q1 + ∇LW·h (per-neuron q1, h, q2 in shared memory), stored down the block's column-major
+// layout; returns whether any entry was non-finite
+template <int D, int ACT>
+__device__ __forceinline__ bool row_entries(const double* __restrict__ sm, int m, const RowCoef<D> rc,
+                                            double* __restrict__ out, int rows) {
+  constexpr int np = 3 + 2 * D;
+  // pin the row constants in registers (otherwise they are re-read from the prologue's stack
+  // frame on every neuron)
+  double xh[D], lwg[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    xh[a] = rc.xh[a];
+    lwg[a] = rc.lwg[a];
+    asm volatile("" : "+d"(xh[a]), "+d"(lwg[a]));
   }
-  __syncthreads();
-  if (r >= rows) return;
-
-  const int gi = A.row_idx[A.row_ptr[j] + r];
-  double x[kMaxDim] = {0, 0, 0, 0}, xh[kMaxDim];
-  for (int a = 0; a < d; ++a) x[a] = A.pts[static_cast<size_t>(a) * A.N + gi];
-  for (int a = 0; a < d; ++a) {
-    const double cen = 0.5 * (bx[a] + bx[4 + a]);
-    const double wid = bx[4 + a] - bx[a];
-    xh[a] = 2.0 * (x[a] - cen) / wid;  // normalize_to_box (geometry.hpp:61-68)
-  }
-  double* out = A.out + A.out_off[j] + r;
-
-  if (A.kind == RDD_PCA_PSI) {
-    const double wj = raw_window_value(A, j, x);
-    double w = 0.0;
-    if (wj != 0.0) {
-      double tot = 0.0;
-      for (int q = A.nbr_ptr[j]; q < A.nbr_ptr[j + 1]; ++q) tot += raw_window_value(A, A.nbr_idx[q], x);
-      w = wj / tot;
-    }
-    for (int k = 0; k < m; ++k) {
-      const double* P = sm + static_cast<size_t>(k) * np;
-      double z = P[0];
-      for (int a = 0; a < d; ++a) z += P[1 + a] * xh[a];
-      const double t = A.act == 0 ? tanh(z) : sin(z);
-      out[static_cast<size_t>(k) * rows] = w * t;
-    }
-    return;
-  }
-
-  // LW = L(x) * window_jet(j, x)  (basis.hpp:158-167, 211)
-  const Jet wj = raw_window_jet(A, j, x);
-  Jet tot;
-  jet_zero(tot, d);
-  for (int q = A.nbr_ptr[j]; q < A.nbr_ptr[j + 1]; ++q) {
-    const Jet rk = raw_window_jet(A, A.nbr_idx[q], x);
-    for (int e = 0; e < jl; ++e) tot.c[e] += rk.c[e];
-  }
-  if (!(tot.c[0] > 0.0)) atomicExch(A.bad + 2, 1);  // domain_error (basis.hpp:165)
-  const double rcp = 1.0 / tot.c[0];
-  const Jet win = jet_mul(wj, jet_compose(rcp, -rcp * rcp, 2.0 * rcp * rcp * rcp, tot, d), d);
-  Jet L;
-  for (int e = 0; e < jl; ++e) L.c[e] = A.Ljet[static_cast<size_t>(gi) * jl + e];
-  const Jet LW = jet_mul(L, win, d);
-  double alpha = 0.0;
-  for (int e = 0; e < jl; ++e) alpha += A.coef[e] * LW.c[e];
-  const double lwv = LW.c[0];
-  double lwg[kMaxDim];
-  for (int a = 0; a < d; ++a) lwg[a] = LW.c[1 + a];
-
+  double lwv = rc.lwv, alpha = rc.alpha;
+  asm volatile("" : "+d"(lwv), "+d"(alpha));
   bool bad = false;
-  for (int k = 0; k < m; ++k) {
-    const double* P = sm + static_cast<size_t>(k) * np;
+  for (int k = 0; k < m; ++k, out += rows) {
+    const double* P = sm + k * np;
     double z = P[0];
-    for (int a = 0; a < d; ++a) z += P[1 + a] * xh[a];
+#pragma unroll
+    for (int a = 0; a < D; ++a) z += P[1 + a] * xh[a];
     double t, t1, t2;
-    if (A.act == 0) {
+    if constexpr (ACT == 0) {
       t = tanh(z);
       t1 = 1.0 - t * t;
       t2 = -2.0 * t * t1;
@@ -197,14 +134,171 @@ __global__ void __launch_bounds__(kRowsPerBlock) k_assemble(AsmArgs A) {
       t1 = cs;
       t2 = -sn;
     }
-    double beta = lwv * P[1 + 2 * d];
-    for (int a = 0; a < d; ++a) beta += lwg[a] * P[1 + d + a];
-    const double v = alpha * t + beta * t1 + (lwv * P[2 + 2 * d]) * t2;
+    double beta = lwv * P[1 + 2 * D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) beta += lwg[a] * P[1 + D + a];
+    const double v = alpha * t + beta * t1 + (lwv * P[2 + 2 * D]) * t2;
     bad |= !isfinite(v);
-    out[static_cast<size_t>(k) * rows] = v;
+    *out = v;
   }
-  if (bad) {
-    atomicExch(A.bad, gi);
+  return bad;
+}
+
+// the subdomain owning row tile `tile` (tile_ptr: J+1 prefix of row tiles)
+__device__ __forceinline__ int tile_block(const int* __restrict__ tile_ptr, int J, int tile) {
+  int lo = 0, hi = J;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (tile_ptr[mid] <= tile) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// per-neuron parameters [b, R(d), h(d), q1, q2] of neuron k of subdomain j
+template <int D>
+__device__ __forceinline__ void neuron_params(const AsmArgs& A, int j, int k, double* P) {
+  const double* bx = A.box + 16 * static_cast<size_t>(j);
+  const double* Rk = A.R + (static_cast<size_t>(j) * A.m + k) * D;
+  P[0] = A.b[static_cast<size_t>(j) * A.m + k];
+  double g[D];
+  for (int a = 0; a < D; ++a) {
+    P[1 + a] = Rk[a];
+    g[a] = Rk[a] * (2.0 / (bx[4 + a] - bx[a]));  // normalize_scales (geometry.hpp:71-75)
+  }
+  double q1 = 0.0, q2 = 0.0;
+  for (int a = 0; a < D; ++a) {
+    q1 += A.coef[1 + a] * g[a];
+    double h = 0.0;
+    for (int bb = 0; bb < D; ++bb) {
+      const double cab = A.coef[1 + D + hess_index(min(a, bb), max(a, bb), D)];
+      h += (a == bb ? 2.0 * cab : cab) * g[bb];
+      if (bb >= a) q2 += cab * g[a] * g[bb];
+    }
+    P[1 + D + a] = h;
+  }
+  P[1 + 2 * D] = q1;
+  P[2 + 2 * D] = q2;
+}
+
+// the point of row r of block j and its local coordinates (normalize_to_box, geometry.hpp:61-68)
+template <int D>
+__device__ __forceinline__ int row_point(const AsmArgs& A, int j, int r, double* x, double* xh) {
+  const double* bx = A.box + 16 * static_cast<size_t>(j);
+  const int gi = A.row_idx[A.row_ptr[j] + r];
+  for (int a = 0; a < kMaxDim; ++a) x[a] = 0.0;
+  for (int a = 0; a < D; ++a) x[a] = A.pts[static_cast<size_t>(a) * A.N + gi];
+  for (int a = 0; a < D; ++a) {
+    const double cen = 0.5 * (bx[a] + bx[4 + a]);
+    const double wid = bx[4 + a] - bx[a];
+    xh[a] = 2.0 * (x[a] - cen) / wid;
+  }
+  return gi;
+}
+
+// psi sample blocks (reduction.hpp:30-48): S_j[r,k] = ω_j(x)·φ_k(x), one kernel
+template <int D>
+__global__ void __launch_bounds__(kRowsPerBlock) k_assemble_psi(AsmArgs A) {
+  extern __shared__ double sm[];
+  const int tile = blockIdx.x;
+  const int j = tile_block(A.tile_ptr, A.J, tile);
+  const int m = A.m, np = 3 + 2 * D;
+  const int rows = A.row_ptr[j + 1] - A.row_ptr[j];
+  const int r = (tile - A.tile_ptr[j]) * kRowsPerBlock + threadIdx.x;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) neuron_params<D>(A, j, k, sm + static_cast<size_t>(k) * np);
+  __syncthreads();
+  if (r >= rows) return;
+  double x[kMaxDim], xh[D];
+  row_point<D>(A, j, r, x, xh);
+  double* out = A.out + A.out_off[j] + r;
+  const double wj = raw_window_value(A, j, x);
+  double w = 0.0;
+  if (wj != 0.0) {
+    double tot = 0.0;
+    for (int q = A.nbr_ptr[j]; q < A.nbr_ptr[j + 1]; ++q) tot += raw_window_value(A, A.nbr_idx[q], x);
+    w = wj / tot;
+  }
+  for (int k = 0; k < m; ++k) {
+    const double* P = sm + static_cast<size_t>(k) * np;
+    double z = P[0];
+    for (int a = 0; a < D; ++a) z += P[1 + a] * xh[a];
+    const double t = A.act == 0 ? tanh(z) : sin(z);
+    out[static_cast<size_t>(k) * rows] = w * t;
+  }
+}
+
+// op_applied, stage 1a: per-neuron parameters of every subdomain (J x m x np) to global memory
+template <int D>
+__global__ void k_neuron_params(AsmArgs A, double* __restrict__ Pg) {
+  const int j = blockIdx.x;
+  constexpr int np = 3 + 2 * D;
+  for (int k = threadIdx.x; k < A.m; k += blockDim.x)
+    neuron_params<D>(A, j, k, Pg + (static_cast<size_t>(j) * A.m + k) * np);
+}
+
+// op_applied, stage 1b: per (block, row) the row constants RowCoef (x̂, LW, ∇LW, A[LW]) with
+// LW = L(x)·window_jet(j, x) (basis.hpp:158-167, 211), stored field-major (rc[f·nent + entry])
+template <int D>
+__global__ void __launch_bounds__(kRowsPerBlock) k_row_coefs(AsmArgs A, double* __restrict__ rcg, long long nent) {
+  const int tile = blockIdx.x;
+  const int j = tile_block(A.tile_ptr, A.J, tile);
+  const int jl = jet_len(D);
+  const int rows = A.row_ptr[j + 1] - A.row_ptr[j];
+  const int r = (tile - A.tile_ptr[j]) * kRowsPerBlock + threadIdx.x;
+  if (r >= rows) return;
+  double x[kMaxDim], xh[D];
+  const int gi = row_point<D>(A, j, r, x, xh);
+  const Jet wj = raw_window_jet<D>(A, j, x);
+  Jet tot;
+  jet_zero(tot, D);
+  for (int q = A.nbr_ptr[j]; q < A.nbr_ptr[j + 1]; ++q) {
+    const Jet rk = raw_window_jet<D>(A, A.nbr_idx[q], x);
+    for (int e = 0; e < jl; ++e) tot.c[e] += rk.c[e];
+  }
+  if (!(tot.c[0] > 0.0)) atomicExch(A.bad + 2, 1);  // domain_error (basis.hpp:165)
+  const double rcp = 1.0 / tot.c[0];
+  const Jet win = jet_mul(wj, jet_compose(rcp, -rcp * rcp, 2.0 * rcp * rcp * rcp, tot, D), D);
+  Jet L;
+  for (int e = 0; e < jl; ++e) L.c[e] = A.Ljet[static_cast<size_t>(gi) * jl + e];
+  const Jet LW = jet_mul(L, win, D);
+  double alpha = 0.0;
+  for (int e = 0; e < jl; ++e) alpha += A.coef[e] * LW.c[e];
+  const long long e0 = A.row_ptr[j] + r;
+  for (int a = 0; a < D; ++a) {
+    rcg[a * nent + e0] = xh[a];
+    rcg[(D + a) * nent + e0] = LW.c[1 + a];
+  }
+  rcg[2 * D * nent + e0] = LW.c[0];
+  rcg[(2 * D + 1) * nent + e0] = alpha;
+}
+
+// op_applied, stage 2: the entries. No calls and no divisions in this kernel, so the row
+// constants live in registers across the neuron loop (a fused prologue with the window jets'
+// division / sincos subroutine calls put them on the stack, re-read every neuron).
+template <int D, int ACT>
+__global__ void __launch_bounds__(kRowsPerBlock) k_assemble_op(AsmArgs A, const double* __restrict__ Pg,
+                                                               const double* __restrict__ rcg, long long nent) {
+  extern __shared__ double sm[];
+  constexpr int np = 3 + 2 * D;
+  const int tile = blockIdx.x;
+  const int j = tile_block(A.tile_ptr, A.J, tile);
+  const int m = A.m;
+  const int rows = A.row_ptr[j + 1] - A.row_ptr[j];
+  const int r = (tile - A.tile_ptr[j]) * kRowsPerBlock + threadIdx.x;
+  const double* Pj = Pg + static_cast<size_t>(j) * m * np;
+  for (int q = threadIdx.x; q < m * np; q += blockDim.x) sm[q] = Pj[q];
+  __syncthreads();
+  if (r >= rows) return;
+  const long long e0 = A.row_ptr[j] + r;
+  RowCoef<D> rc;
+  for (int a = 0; a < D; ++a) {
+    rc.xh[a] = rcg[a * nent + e0];
+    rc.lwg[a] = rcg[(D + a) * nent + e0];
+  }
+  rc.lwv = rcg[2 * D * nent + e0];
+  rc.alpha = rcg[(2 * D + 1) * nent + e0];
+  if (row_entries<D, ACT>(sm, m, rc, A.out + A.out_off[j] + r, rows)) {
+    atomicExch(A.bad, A.row_idx[e0]);
     atomicExch(A.bad + 1, j);
   }
 }
@@ -248,10 +342,35 @@ void assemble_samples(Ctx& c, int kind, double* out, const std::vector<long long
   bad.upload(hbad, 3, c.stream);
   A.bad = bad.p;
   const size_t smem = static_cast<size_t>(c.m) * (3 + 2 * c.d) * sizeof(double);
-  if (smem > 32 * 1024) RDD_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  if (tp[c.J] > 0) {
-    k_assemble<<<tp[c.J], kRowsPerBlock, smem, c.stream>>>(A);
+  if (c.d < 1 || c.d > 4) throw std::invalid_argument("assemble: dimension must be 1..4");
+  const long long nent = c.h_row_ptr[c.J];
+  auto run = [&](auto dim) {
+    constexpr int D = decltype(dim)::value;
+    auto launch = [&](auto kernel, auto... extra) {
+      if (smem > 32 * 1024) RDD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kernel<<<tp[c.J], kRowsPerBlock, smem, c.stream>>>(A, extra...);
+      RDD_LAUNCH_CHECK();
+    };
+    if (kind == RDD_PCA_PSI) {
+      launch(k_assemble_psi<D>);
+      return;
+    }
+    double* Pg = c.ws("asm_neuron", static_cast<size_t>(c.J) * c.m * (3 + 2 * D));
+    double* rcg = c.ws("asm_rowc", static_cast<size_t>(nent) * (2 * D + 2));
+    k_neuron_params<D><<<c.J, 128, 0, c.stream>>>(A, Pg);
     RDD_LAUNCH_CHECK();
+    k_row_coefs<D><<<tp[c.J], kRowsPerBlock, 0, c.stream>>>(A, rcg, nent);
+    RDD_LAUNCH_CHECK();
+    if (A.act == 0) launch(k_assemble_op<D, 0>, static_cast<const double*>(Pg), static_cast<const double*>(rcg), nent);
+    else launch(k_assemble_op<D, 1>, static_cast<const double*>(Pg), static_cast<const double*>(rcg), nent);
+  };
+  if (tp[c.J] > 0) {
+    switch (c.d) {
+      case 1: run(std::integral_constant<int, 1>{}); break;
+      case 2: run(std::integral_constant<int, 2>{}); break;
+      case 3: run(std::integral_constant<int, 3>{}); break;
+      default: run(std::integral_constant<int, 4>{}); break;
+    }
   }
   int hb[3];
   bad.download(hb, 3, c.stream);

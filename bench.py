@@ -275,7 +275,8 @@ def run_device(args, cfg, world, rank, local, dist):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "kernel": ("normal operator Hᵀ(H·w), single pass: k_fused_normal + k_fused_reduce" if op_form == A.OPERATOR_FUSED else "normal operator Hᵀ(H·w): k_block_gemv + k_block_gemv_t (y = H·w formed in its staging) + k_chunk_sum"),
-                         "bytes_per_call": op_bytes, "ms_per_call": op_ms},
+                         "bytes_per_call": op_bytes, "ms_per_call": op_ms,
+                         "nominal_peak": 8000.0, "frac_nominal": achieved / 8000.0},
             "clocks": clk,
         }
         if cpu is not None:

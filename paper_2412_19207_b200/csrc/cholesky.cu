@@ -453,6 +453,73 @@ __device__ void symv_packed(const double* __restrict__ P, int nb, double* v, dou
   __syncthreads();
 }
 
+// symv_packed with the tile taken in four quarters of 16 columns: 16 transposed partials per lane
+// instead of 32, so the explicit-inverse apply fits 80 registers (3 CTAs per SM instead of 2)
+__device__ void symv_packed_q(const double* __restrict__ P, int nb, double* v, double* part, int t0 = 0, int tstep = 1) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  const int len = nb * NB;
+  double* my = part + static_cast<size_t>(warp) * len;
+  for (int i = lane; i < len; i += 32) my[i] = 0.0;
+  __syncwarp();
+  const int T = nb * (nb + 1) / 2;
+  const int first = t0 + warp * tstep, stride = kSolveWarps * tstep;  // this warp's tiles
+  int k = 0, j = first;  // tile t = k(k+1)/2 + j
+  while (j > k) {
+    j -= k + 1;
+    ++k;
+  }
+  for (int t = first; t < T; t += stride) {
+    const double* tile = P + static_cast<long long>(t) * (NB * NB);
+    const double* gj = v + j * NB;
+    const double gk0 = v[k * NB + 2 * lane], gk1 = v[k * NB + 2 * lane + 1];
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll 1
+    for (int h = 0; h < 4; ++h) {
+      double p[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(tile + (h * 16 + c) * NB) + lane);
+        const double gc = gj[h * 16 + c];
+        a0 += a.x * gc;
+        a1 += a.y * gc;
+        p[c] = a.x * gk0 + a.y * gk1;
+      }
+      if (j < k) {  // warp-uniform
+        // fold the half-warps (lanes L and L^16 then hold the same pair sums), then the transpose
+        // butterfly over 16 lanes: lane L (mod 16) ends with column L's sum
+#pragma unroll
+        for (int i = 0; i < 16; ++i) p[i] += __shfl_xor_sync(0xffffffffu, p[i], 16);
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int i = 0; i < o; ++i) {
+            const double send = up ? p[i] : p[i + o];
+            const double keep = up ? p[i + o] : p[i];
+            p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        if (lane < 16) my[j * NB + h * 16 + lane] += p[0];
+      }
+    }
+    my[k * NB + 2 * lane] += a0;
+    my[k * NB + 2 * lane + 1] += a1;
+    __syncwarp();
+    j += stride;
+    while (j > k && k < nb) {
+      j -= k + 1;
+      ++k;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < len; i += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < kSolveWarps; ++w) s += part[static_cast<size_t>(w) * len + i];
+    v[i] = s;
+  }
+  __syncthreads();
+}
+
 // λmax(A⁻¹) by power iteration through the factor: one CTA per matrix
 __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_power(const double* __restrict__ P,
                                                                  const long long* __restrict__ poff,
@@ -829,8 +896,63 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
   for (int r = threadIdx.x; r < n; r += blockDim.x) zo[s0 + r] = g[r];
 }
 
+// explicit-inverse apply (small blocks): two CTAs per subdomain as in k_chol_apply's inverse mode,
+// with the quarter-tile symv and a register cap for 3 CTAs per SM
+__global__ void __launch_bounds__(kSolveWarps * 32, 3) k_inv_apply(
+    const double* __restrict__ P, const long long* __restrict__ poff, const double* const* __restrict__ dense,
+    const int* __restrict__ set_ptr, const int* __restrict__ set_idx, const double* __restrict__ v,
+    const int* __restrict__ mult, const int* __restrict__ owner, int kind, int transpose, int nbmax,
+    double* __restrict__ z, long long zhalf, const int* __restrict__ live, const int* __restrict__ order) {
+  if (live && *live != 0) return;
+  extern __shared__ double sm[];
+  double* g = sm;
+  double* red = sm + static_cast<size_t>(nbmax) * NB;
+  const int bi = blockIdx.x >> 1;
+  const int i = order ? order[bi] : bi;
+  const int h = blockIdx.x & 1;
+  const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0, nb = (n + NB - 1) / NB;
+  for (int q = threadIdx.x; q < nb * NB; q += blockDim.x) {
+    double val = 0.0;
+    if (q < n) {
+      const int col = set_idx[s0 + q];
+      val = v[col];
+      if (transpose) {
+        if (kind == RDD_PRECOND_SAS) val /= mult[col];
+        else if (kind == RDD_PRECOND_RAS) val = owner[col] == i ? val : 0.0;
+      }
+    }
+    g[q] = val;
+  }
+  __syncthreads();
+  double* zo = z + static_cast<long long>(h) * zhalf;
+  const double* D = dense[i];
+  if (D) {
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      double acc = 0.0;
+      if (h == 0)
+        for (int q = 0; q < n; ++q) acc += D[r + static_cast<long long>(q) * n] * g[q];
+      zo[s0 + r] = acc;
+    }
+    return;
+  }
+  symv_packed_q(P + poff[i], nb, g, red, h, 2);
+  for (int r = threadIdx.x; r < n; r += blockDim.x) zo[s0 + r] = g[r];
+}
+
 void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
   const size_t smem = chol_solve_smem(c.nmax_local, c.inv_mode);
+  if (c.inv_mode) {
+    static size_t set_inv = 0;
+    if (smem > set_inv) {
+      RDD_CUDA(cudaFuncSetAttribute(k_inv_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      set_inv = smem;
+    }
+    k_inv_apply<<<2 * c.J, kSolveWarps * 32, smem, c.stream>>>(
+        c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p, v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
+        ceil_div(c.nmax_local, NB), zloc, static_cast<long long>(c.set_idx.size()), c.live, c.apply_order.p);
+    RDD_LAUNCH_CHECK();
+    return;
+  }
   static size_t set = 0;
   if (smem > set) {
     RDD_CUDA(cudaFuncSetAttribute(k_chol_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

@@ -1,22 +1,27 @@
 #!/usr/bin/env python
 """bench.py — AS-PCG end-to-end solve time for the RaNN + overlapping-Schwarz pipeline on B200.
 
-Workload: BASELINE.json configs[1] (C2: 2-D multiscale Poisson, 16x16 subdomains, m=300, 60x60
-points per subdomain = 921,600 collocation rows, PCA σ/σmax > 1e-6, AS-preconditioned CG on the
-normal equations to relative residual 1e-10, FP64). One step = one full pipeline solve
-(runner.hpp:202-275: PCA -> assembly -> equilibration -> normal blocks + Schwarz -> PCG -> test
-evaluation) of one seed.
+Workload (default): C5 = BASELINE.json configs[4], the largest configuration that fits one GPU
+(the metric line names no config): 3-D Poisson on [0,1]^3, 8x8x8 subdomains with 10% overlap,
+m = 400 tanh neurons, 20^3 points per subdomain (4.1M collocation rows), PCA σ/σmax > 1e-6,
+AS-preconditioned CG on the normal equations to relative residual 1e-10, FP64. One step = one
+full pipeline solve (runner.hpp:202-275: PCA -> assembly -> equilibration -> normal blocks +
+Schwarz -> PCG -> test evaluation) of one seed. --config C1..C4 selects the others.
 
   value   seconds per solve, inputs (collocation points, boxes, random bases) already resident
           in HBM; CUDA events on the library's stream; max over ranks.
   e2e     the same metric through the public C-ABI call rdd_run_single with host inputs: host
           geometry/bases, pinned H2D of points and bases, D2H of the evaluation, every step.
-  roofline  the block-sparse normal operator Hᵀ(H·w) (the matvec of the metric), HBM-bound.
-  cpu_baseline  the CPU oracle (oracle/, C++ restatement of the reference) on a bounded slice.
+  roofline  the HBM-bound kernel with the larger share of the step — the Schwarz apply or the
+          block-sparse normal operator Hᵀ(H·w) — algorithmic bytes per call over its CUDA-event
+          time; the other one is reported as roofline_other.
+  cpu_baseline  one real, complete CPU-oracle solve of C5s (the 2x2x2 run BASELINE names for
+          C5), with the device's time on the same C5s solve beside it. Nothing is extrapolated.
 
 N>1 (torchrun): replicas — every rank solves its own seed (seed + rank) on its own GPU; the
-path has no data exchange in this tier. --impl reference runs the CPU
-oracle on rank 0 only.
+path has no data exchange in this tier. --impl reference: rank 0
+measures one complete C5s oracle solve and reports value = null with the reason (a full C5
+oracle solve takes hours).
 """
 from __future__ import annotations
 
@@ -34,8 +39,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "AS-PCG end-to-end solve sec to rel-res 1e-10; matvec HBM GB/s vs peak"
 FALLBACK_HBM_GBS = 6650.0
-# iterations of the full C2 solve measured on the device (used only to extrapolate the CPU sample)
-FULL_ITERATIONS = {"C2": 173, "C1": 24}
 
 
 def peaks():
@@ -129,79 +132,79 @@ def barrier(dist):
 
 
 # ------------------------------------------------------------------ CPU oracle sample
-def cpu_sample(cfg_name: str, cfg, threads: int):
-    """Time the CPU oracle on a slice of the workload and extrapolate to the full config.
-
-    The slice keeps d, m, P (points per subdomain per axis) and the operator with
-    2^d subdomains (corner boxes: ~15% fewer rows than interior ones, so a slight underestimate). Setup phases (PCA, assembly, local eigensolves) scale with the subdomain
-    count; the solve scales with subdomains x iterations (the full-size iteration count is the
-    device-measured one)."""
+def cpu_sample(threads: int):
+    """One real, complete CPU-oracle solve of C5s — BASELINE configs[4]'s own 2x2x2 run of the C5
+    workload (same d, m = 400, 20^3 points per subdomain, operator, PCA rule, AS-PCG to 1e-10) —
+    timed end to end on this host. Nothing is extrapolated: the device's time on the same C5s
+    solve is measured beside it (run_device), and full-size oracle timings are committed under
+    profiles/oracle_fullsize_r02.jsonl."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc_mod
     from oracle import Oracle
     from paper_2412_19207_b200 import configs
 
-    J = 1
-    for a in range(cfg.d):
-        J *= cfg.counts[a]
-    per = cfg.colloc[0] // cfg.counts[0]
-    sl = [2] * cfg.d if J > 2 ** cfg.d else list(cfg.counts)[:cfg.d]
-    scfg = configs.scaled(cfg, sl, per)
-    Js = 1
-    for v in sl:
-        Js *= v
+    cfg = configs.c5(counts=(2, 2, 2))
     o = Oracle(threads=threads)
     t0 = time.perf_counter()
-    s = o.run_single(scfg)
+    s = o.run_single(cfg)
     wall = time.perf_counter() - t0
-    f = J / Js
-    iters_full = FULL_ITERATIONS.get(cfg_name, s["iterations"])
-    per_iter = s["t_solve"] / max(1, s["iterations"])
-    est = (s["t_assemble"] + s["t_precond"]) * f + per_iter * f * iters_full + s["t_evaluate"] * f
-    import oracle as orc_mod
-    cores = orc_mod.lib().orc_max_threads()
+    o.close()
     return {
-        "value": est, "unit": "s", "cores": cores, "kind": "port",
-        "sample": (f"CPU oracle (C++ restatement of the reference, OpenMP at the reference's 5 sites, "
-                   f"LAPACK single-threaded as Eigen) timed on a {'x'.join(map(str, sl))}-subdomain slice of "
-                   f"{cfg_name} (same m={cfg.m}, {per} points/subdomain/axis, {s['iterations']} PCG iterations, "
-                   f"{wall:.1f} s wall), extrapolated x{f:.0f} subdomains and to {iters_full} iterations"),
-        "slice_summary": {k: s[k] for k in ("J", "DoF", "N", "iterations", "t_assemble", "t_precond", "t_solve")},
+        "value": wall, "unit": "s", "cores": orc_mod.lib().orc_max_threads(), "kind": "port",
+        "sample": (f"one complete run_single of C5s (2x2x2 subdomains of C5: m=400, 20^3 points per subdomain, "
+                   f"AS-PCG to 1e-10; J={s['J']}, DoF={s['DoF']}, N={s['N']}, {s['iterations']} PCG iterations) on the "
+                   f"CPU oracle (C++ restatement of the reference: serial per-subdomain PCA as runner.hpp:52-65, "
+                   f"OpenMP at the reference's sites, LAPACK single-threaded as Eigen), measured, not extrapolated"),
+        "summary": {k: s[k] for k in ("J", "DoF", "N", "iterations", "e_l2", "t_assemble", "t_precond", "t_solve")},
     }
 
 
 def run_reference(args, cfg, world, rank, dist):
+    """The reference arm. A full C5 solve on the CPU oracle takes hours on a host (512 serial
+    per-subdomain SVDs and dense local eigensolves of order ~5,000: profiles/oracle_fullsize_r02.jsonl),
+    and a bounded sample is not the metric (seconds for the whole C5 solve), so `value` is null
+    rather than an estimate; one real complete C5s solve is measured and reported as the sample."""
     if rank != 0:
         return 0
-    from paper_2412_19207_b200 import configs  # noqa: F401
     threads = os.cpu_count() or 1
-    vals, last = [], None
-    for i in range(args.warmup + args.steps):
-        r = cpu_sample(args.config, cfg, threads)
-        if i >= args.warmup:
-            vals.append(r["value"])
-            last = r
-    v = statistics.median(vals)
+    smp = cpu_sample(threads)
     line = {
-        "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "metric": METRIC, "value": None, "unit": "s", "n_gpus": args.gpus, "steps": 0, "warmup": 0,
+        "ms_per_step": None, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (formula-defined problem, SplitMix64 bases as the reference)", "impl": "reference",
         "config": {"workload": args.config, **cfg.as_dict()},
-        "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reason": (f"a complete {args.config} solve on the host CPU oracle takes hours (serial per-subdomain PCA and "
+                   f"dense local eigensolves); no estimate is reported. Measured instead: one complete C5s solve "
+                   f"({smp['value']:.1f} s on {smp['cores']} threads, cpu_baseline) and full-size oracle timings in "
+                   f"profiles/oracle_fullsize_r02.jsonl"),
+        "cpu_baseline": {k: smp[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": None, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def ncu_traffic(workload: str, family: str):
+    """DRAM bytes per call of a kernel family from the committed ncu --set full summary of the same
+    workload (tools/ncu_traffic.py writes it from the capture; profiles/ncu_traffic_r02.json)."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"{workload}:{family}", {}).get("dram_bytes_per_call")
+    except Exception:
+        return None
+
+
 # ------------------------------------------------------------------ device arm
 def run_device(args, cfg, world, rank, local, dist):
     from paper_2412_19207_b200 import abi as A
-    from paper_2412_19207_b200 import rdd
+    from paper_2412_19207_b200 import configs, rdd
 
     cfg.seed = cfg.seed + rank
     s = rdd.Solver(local)
     # setup step (untimed): builds and uploads the instance
-    first = s.run_single(cfg)
+    s.run_single(cfg)
     # the sampler starts before the warm-up so its own start-up (driver queries) stays outside the
     # timed region; it keeps sampling through it
     clocks = ClockSampler(local)
@@ -230,57 +233,77 @@ def run_device(args, cfg, world, rank, local, dist):
     s.L.rdd_io_bytes(C.byref(h0), C.byref(d0))
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        e2e_s = s.run_single(cfg)
+        s.run_single(cfg)
     e2e = (time.perf_counter() - t0) / args.steps
     h1, d1 = C.c_int64(), C.c_int64()
     s.L.rdd_io_bytes(C.byref(h1), C.byref(d1))
     e2e_max = reduce_max(dist, e2e)
 
-    # roofline: the normal operator (two passes over H) timed back-to-back with CUDA events on
-    # the library stream, same resident system
-    op_form = cfg.op_form if cfg.op_form in (A.OPERATOR_TWO_PASS, A.OPERATOR_FUSED) else A.OPERATOR_TWO_PASS
-    op_ms, op_bytes = s.bench_operator(op_form, reps=30)
+    # roofline: the two HBM-bound kernels of a PCG iteration, each timed back-to-back with CUDA
+    # events on the library stream on the resident system; the one with the larger share of the
+    # step (calls per solve x time per call) is the line's `roofline`
     peak, peak_kind = peaks()
-    achieved = op_bytes / (op_ms / 1e3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_matvec_traffic.json")
-    if os.path.exists(prof):
-        try:
-            with open(prof) as f:
-                traffic = json.load(f).get("bytes_per_call")
-        except Exception:
-            traffic = None
+    its = summ["iterations"]
+    op_ms, op_bytes = s.bench_operator(A.OPERATOR_TWO_PASS, reps=20)
+    pc_ms, pc_bytes = s.bench_precond(False, reps=10)
+    kern = {
+        "operator": ("normal operator Hᵀ(H·w): k_block_gemv + k_block_gemv_t (y = H·w formed in its staging) "
+                     "+ k_chunk_sum", op_ms, op_bytes, "operator"),
+        "schwarz_apply": ("AS Schwarz apply z = Σ R_iᵀ A_i⁻¹ R_i v: k_chol_apply / k_inv_apply + k_reduce",
+                          pc_ms, pc_bytes, "schwarz_apply"),
+    }
+    roof = {}
+    for key, (desc, kms, kb, fam) in kern.items():
+        ach = kb / (kms / 1e3) / 1e9
+        roof[key] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": ncu_traffic(args.config, key), "peak_source": peak_kind, "kernel": desc,
+                     "bytes_per_call": kb, "ms_per_call": kms, "calls_per_step": its + 1,
+                     "share_of_step": (its + 1) * kms / 1e3 / t_step,
+                     "nominal_peak": 8000.0, "frac_nominal": ach / 8000.0}
+    dom = max(roof, key=lambda k: roof[k]["share_of_step"])
 
     cpu = None
+    dev_sample = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_sample(args.config, cfg, os.cpu_count() or 1)
+            cpu = cpu_sample(os.cpu_count() or 1)
+            c5s = configs.c5(counts=(2, 2, 2))
+            s.run_single(c5s)
+            s.L.rdd_event_record(s.h, 0)
+            for _ in range(3):
+                s.rerun_resident()
+            s.L.rdd_event_record(s.h, 1)
+            s.L.rdd_event_elapsed(s.h, 0, 1, C.byref(ms))
+            dev_sample = ms.value / 1e3 / 3
         except Exception as e:  # the baseline is reported, never the target
             cpu = {"value": None, "unit": "s", "cores": 0, "kind": "port", "sample": f"failed: {e}"}
     if rank == 0:
+        ph = {k: summ[k] for k in ("t_pca", "t_assemble", "t_precond", "t_solve", "t_evaluate")}
         line = {
             "metric": METRIC, "value": t_step_max, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step_max * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (formula-defined problem, SplitMix64 bases as the reference)",
-            "config": {"workload": args.config, "l2": "working set (S 3.1 GB, H 0.6 GB) exceeds the 126 MB L2",
+            "config": {"workload": args.config,
+                       "l2": "no flush needed: the resident working set (sample matrices, H, Schwarz factors) "
+                             "is tens of GB, far above the 126 MB L2",
                        "parallelism": f"replicas x{world} (one seed per GPU)", **cfg.as_dict()},
             "solves_per_s": world / t_step_max,
-            "phases_s": {k: summ[k] for k in ("t_pca", "t_assemble", "t_precond", "t_solve", "t_evaluate")},
-            "iterations": summ["iterations"], "converged": summ["converged"], "DoF": summ["DoF"], "N": summ["N"],
+            # the library's phase clocks are cumulative up to assembly; reported per phase here
+            "phases_s": {"pca": ph["t_pca"], "assembly": ph["t_assemble"] - ph["t_pca"],
+                         "schwarz_build": ph["t_precond"], "solve": ph["t_solve"], "evaluate": ph["t_evaluate"]},
+            "iterations": its, "converged": summ["converged"], "DoF": summ["DoF"], "N": summ["N"],
             "e_l2": summ["e_l2"], "final_residual": summ["final_residual"],
             "e2e": {"value": e2e_max, "unit": "s", "h2d_bytes_per_step": (h1.value - h0.value) // args.steps,
                     "d2h_bytes_per_step": (d1.value - d0.value) // args.steps},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": ("normal operator Hᵀ(H·w), single pass: k_fused_normal + k_fused_reduce" if op_form == A.OPERATOR_FUSED else "normal operator Hᵀ(H·w): k_block_gemv + k_block_gemv_t (y = H·w formed in its staging) + k_chunk_sum"),
-                         "bytes_per_call": op_bytes, "ms_per_call": op_ms,
-                         "nominal_peak": 8000.0, "frac_nominal": achieved / 8000.0},
+            "roofline": {**roof[dom], "which": dom},
+            "roofline_other": {**roof[[k for k in roof if k != dom][0]], "which": [k for k in roof if k != dom][0]},
             "clocks": clk,
         }
         if cpu is not None:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"]["device_same_sample_s"] = dev_sample
         print(json.dumps(line), flush=True)
     s.close()
     return 0
@@ -292,7 +315,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="rdd", choices=["rdd", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

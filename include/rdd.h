@@ -187,8 +187,20 @@ int rdd_kernel_stats(rdd_ctx* ctx, const char* family, double* ms_total, int64_t
 int rdd_reset_stats(rdd_ctx* ctx);
 int rdd_set_timing(rdd_ctx* ctx, int on);  /* per-family CUDA-event timing (adds syncs) */
 int rdd_set_verbose(rdd_ctx* ctx, int on);  /* phase times and solver diagnostics on stderr */
+/* Numeric switches of the device path (no reference counterpart; the reference always takes the
+   eigen pseudo-inverse of schwarz.hpp:131-146):
+     "full_rank_cond"  local blocks A_i whose condition estimate is below this take the Cholesky
+                       path, the rest the eigen pseudo-inverse with the reference cutoff
+                       (default in DESIGN.md §4 K8; 0 routes every block to the eigen path).
+   Takes effect at the next rdd_build_preconditioner. RDD_INVALID_ARGUMENT for unknown names. */
+int rdd_set_param(rdd_ctx* ctx, const char* name, double value);
 /* Time `reps` calls of the normal operator on device-resident vectors (CUDA events). */
 int rdd_bench_operator(rdd_ctx* ctx, int op_form, int reps, double* ms_per_call, double* bytes_per_call);
+/* Time `reps` applications of the built Schwarz preconditioner (schwarz.hpp:153-215) on a
+   device-resident vector (CUDA events on the context stream). bytes_per_call = algorithmic HBM
+   bytes: the local operators (factor read twice, explicit inverse or dense pseudo-inverse read
+   once), the gathered/scattered local vectors and the reduction. */
+int rdd_bench_precond(rdd_ctx* ctx, int transpose, int reps, double* ms_per_call, double* bytes_per_call);
 /* Batched Jacobi eigensolver probe (no reference counterpart; tuning aid): `batch` random
    symmetric matrices of order n, exactly `sweeps` sweeps, eigenvectors included; ms via events. */
 int rdd_bench_jacobi(rdd_ctx* ctx, int n, int batch, int sweeps, double* ms);

@@ -71,6 +71,8 @@ def lib():
         L.orc_get_d.restype = C.c_int64
         L.orc_get_d.argtypes = [C.c_void_p, C.c_char_p, C.c_int, dp, C.c_int64]
         L.orc_max_threads.restype = C.c_int
+        L.orc_set_option.restype = C.c_int
+        L.orc_set_option.argtypes = [C.c_char_p, C.c_int]
         _lib = L
     return _lib
 
@@ -91,6 +93,13 @@ class Oracle:
         self.h = self.L.orc_create(lapack_path().encode(), threads)
         if not self.h:
             raise OracleError("orc_create failed")
+
+    @staticmethod
+    def set_option(name: str, value: int):
+        """Fixture-generation switches: 'parallel_pca' (independent per-subdomain PCAs run
+        concurrently), 'keep_samples' (keep the unreduced sample matrices)."""
+        if lib().orc_set_option(name.encode(), int(value)) != 0:
+            raise OracleError(f"unknown oracle option {name}")
 
     def close(self):
         if self.h:

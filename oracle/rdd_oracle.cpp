@@ -8,7 +8,7 @@
 // Eigen is not installed here, so the reference cannot be compiled as-is.
 // Dense decompositions that the reference takes from Eigen are taken from LAPACK in scipy's
 // bundled OpenBLAS, loaded with dlopen at orc_create():
-//   Eigen::JacobiSVD            (reduction.hpp:91)  -> dgesvj (one-sided Jacobi, same accuracy class)
+//   Eigen::JacobiSVD            (reduction.hpp:91)  -> dgeqp3 preconditioner + dgesvj on R (Eigen's QR-preconditioned form)
 //   SelfAdjointEigenSolver      (schwarz.hpp:131)   -> dsyevd (ascending, as Eigen)
 //   ColPivHouseholderQR         (krylov.hpp:100)    -> dgeqp3 + dormqr + back substitution
 //   EigenSolver / BDCSVD        (krylov.hpp:416/425)-> dgeev / dgesvd (diagnostics only)
@@ -624,18 +624,57 @@ static RefGrid reference_example2(int res) {
   return ref;
 }
 
+// fixture-generation switches (orc_set_option): concurrent per-subdomain PCAs, and whether the
+// unreduced sample matrices are kept (needed by the psi-reduction tests, ~15 GB on C5)
+static int g_parallel_pca = 0;
+static int g_keep_samples = 1;
+
 // ---------------------------------------------------------------- PCA (reduction.hpp:18-155)
 struct Reduced {
   Mat V;       // m x p
+  Mat Vfull;   // m x min(rows, m): every right singular vector (fixture generation reads it)
   int p = 0;
   Vec sigma;   // min(rows, m), non-increasing
   bool identity = false;
 };
 
 // Thin SVD: singular values (non-increasing) and right singular vectors (m x min(rows,m)).
+// Tall inputs follow Eigen's JacobiSVD (its default ColPivHouseholderQRPreconditioner): a
+// column-pivoted Householder QR S·P = Q·R first, then the Jacobi SVD of the square upper
+// triangular R, whose right vectors are carried back through the column permutation
+// (V = P·V_R). The Jacobi SVD of R is LAPACK's one-sided dgesvj (same accuracy class as Eigen's
+// two-sided sweeps: both relatively accurate on R).
 static void svd_thin(const Mat& S, Vec& sv, Mat& V) {
   const int M = S.r, N = S.c;
-  if (M >= N) {
+  if (M > N) {
+    Mat A = S;
+    int lda = M, info = 0;
+    std::vector<int> jpvt(N, 0);
+    Vec tau(N);
+    double wq = 0.0;
+    int lq = -1;
+    g_lapack.geqp3(&M, &N, A.a.data(), &lda, jpvt.data(), tau.data(), &wq, &lq, &info);
+    lq = std::max(1, static_cast<int>(wq));
+    Vec work_q(lq);
+    g_lapack.geqp3(&M, &N, A.a.data(), &lda, jpvt.data(), tau.data(), work_q.data(), &lq, &info);
+    if (info < 0) throw std::runtime_error("dgeqp3: bad argument");
+    Mat R(N, N);
+    for (int c = 0; c < N; ++c)
+      for (int r = 0; r <= c; ++r) R(r, c) = A(r, c);
+    sv.assign(N, 0.0);
+    Mat VR(N, N);
+    int lwork = std::max(6, 2 * N), mv = 0, ldv = N, ldr = N;
+    Vec work(lwork);
+    g_lapack.gesvj("U", "N", "V", &N, &N, R.a.data(), &ldr, sv.data(), &mv, VR.a.data(), &ldv, work.data(), &lwork,
+                   &info, 1, 1, 1);
+    if (info < 0) throw std::runtime_error("dgesvj: bad argument");
+    const double scale = work[0];
+    if (scale != 1.0)
+      for (double& s : sv) s *= scale;
+    V = Mat(N, N);
+    for (int c = 0; c < N; ++c)
+      for (int r = 0; r < N; ++r) V(jpvt[r] - 1, c) = VR(r, c);
+  } else if (M == N) {
     Mat A = S;
     sv.assign(N, 0.0);
     V = Mat(N, N);
@@ -693,6 +732,7 @@ static Reduced truncate(const Mat& S, double tau, bool relative) {
   out.p = keep;
   out.V = Mat(Vfull.r, keep);
   for (int c = 0; c < keep; ++c) std::copy(Vfull.col(c), Vfull.col(c) + Vfull.r, out.V.col(c));
+  out.Vfull = std::move(Vfull);
   for (int c = 0; c < keep; ++c) {
     for (int r = 0; r < out.V.r; ++r) {
       if (out.V(r, c) != 0.0) {
@@ -822,17 +862,42 @@ static void build_instance(Oracle& o, const rdd_config& cfg, uint64_t seed) {
     o.dec = build_cell_decomposition(o.prob.domain, counts, cfg.delta);
   o.pts = uniform_grid(o.prob.domain, colloc, cfg.boundary_per_edge);
   const int J = o.dec.size();
-  for (int j = 0; j < J; ++j) {
-    o.bases.push_back(make_random_basis(subdomain_seed(seed, j), cfg.m, d, cfg.activation));
-    if (cfg.tau_mode != RDD_TAU_OFF) {
-      const std::vector<int> idx = rows_of(o, j);
-      if (idx.empty()) throw std::runtime_error("subdomain " + std::to_string(j) + " contains no collocation points");
-      Mat S = cfg.pca_matrix == RDD_PCA_OP_APPLIED ? build_operator_sample_matrix(o, j, idx)
-                                                   : build_sample_matrix(o, j, idx);
-      o.red.push_back(truncate(S, cfg.tau, cfg.tau_mode == RDD_TAU_RELATIVE));
-      o.samples.push_back(std::move(S));
-    } else {
-      o.red.push_back(identity_reduction(cfg.m));
+  if (g_parallel_pca && cfg.tau_mode != RDD_TAU_OFF) {
+    // fixture generation only (tests/golden/make_fullsize.py): the per-subdomain PCAs are
+    // independent, so they run concurrently; each one is the same serial computation as below
+    // (the reference's loop, runner.hpp:52-65, is serial)
+    for (int j = 0; j < J; ++j) o.bases.push_back(make_random_basis(subdomain_seed(seed, j), cfg.m, d, cfg.activation));
+    o.red.assign(J, Reduced{});
+    if (g_keep_samples) o.samples.assign(J, Mat{});
+    std::string err;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int j = 0; j < J; ++j) {
+      try {
+        const std::vector<int> idx = rows_of(o, j);
+        if (idx.empty()) throw std::runtime_error("subdomain " + std::to_string(j) + " contains no collocation points");
+        Mat S = cfg.pca_matrix == RDD_PCA_OP_APPLIED ? build_operator_sample_matrix(o, j, idx)
+                                                     : build_sample_matrix(o, j, idx);
+        o.red[j] = truncate(S, cfg.tau, cfg.tau_mode == RDD_TAU_RELATIVE);
+        if (g_keep_samples) o.samples[j] = std::move(S);
+      } catch (const std::exception& e) {
+#pragma omp critical
+        err = e.what();
+      }
+    }
+    if (!err.empty()) throw std::runtime_error(err);
+  } else {
+    for (int j = 0; j < J; ++j) {
+      o.bases.push_back(make_random_basis(subdomain_seed(seed, j), cfg.m, d, cfg.activation));
+      if (cfg.tau_mode != RDD_TAU_OFF) {
+        const std::vector<int> idx = rows_of(o, j);
+        if (idx.empty()) throw std::runtime_error("subdomain " + std::to_string(j) + " contains no collocation points");
+        Mat S = cfg.pca_matrix == RDD_PCA_OP_APPLIED ? build_operator_sample_matrix(o, j, idx)
+                                                     : build_sample_matrix(o, j, idx);
+        o.red.push_back(truncate(S, cfg.tau, cfg.tau_mode == RDD_TAU_RELATIVE));
+        if (g_keep_samples) o.samples.push_back(std::move(S));
+      } else {
+        o.red.push_back(identity_reduction(cfg.m));
+      }
     }
   }
   o.col_off.assign(J + 1, 0);
@@ -1667,6 +1732,14 @@ void* orc_create(const char* lapack_path, int threads) {
 }
 void orc_destroy(void* h) { delete static_cast<Oracle*>(h); }
 const char* orc_last_error(void* h) { return static_cast<Oracle*>(h)->err.c_str(); }
+int orc_set_option(const char* name, int value) {
+  const std::string n = name ? name : "";
+  if (n == "parallel_pca") orc::g_parallel_pca = value;
+  else if (n == "keep_samples") orc::g_keep_samples = value;
+  else return 1;
+  return 0;
+}
+
 int orc_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
@@ -1836,6 +1909,7 @@ int64_t orc_get_d(void* h, const char* what, int index, double* out, int64_t cap
   else if (w == "S") v = o->samples[index].a;
   else if (w == "sigma") v = o->red[index].sigma;
   else if (w == "V") v = o->red[index].V.a;
+  else if (w == "V_full") v = o->red[index].Vfull.a;
   else if (w == "H") v = o->H[index].a;
   else if (w == "F") v = o->F.a;
   else if (w == "scales") v = o->scales;

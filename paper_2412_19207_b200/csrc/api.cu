@@ -249,6 +249,17 @@ int rdd_set_verbose(rdd_ctx* h, int on) {
   return RDD_OK;
 }
 
+int rdd_set_param(rdd_ctx* h, const char* name, double value) {
+  if (!h || !name) return RDD_INVALID_ARGUMENT;
+  const std::string n(name);
+  if (n == "full_rank_cond" && value >= 0.0) {
+    h->c.full_rank_cond = value;
+    return RDD_OK;
+  }
+  h->c.err = "rdd_set_param: unknown parameter or bad value: " + n;
+  return RDD_INVALID_ARGUMENT;
+}
+
 const char* rdd_last_error(const rdd_ctx* h) { return h ? h->c.err.c_str() : "null context"; }
 
 int rdd_build_instance(rdd_ctx* h, const rdd_config* cfg, uint64_t seed) {
@@ -589,6 +600,44 @@ int rdd_bench_operator(rdd_ctx* h, int op_form, int reps, double* ms_per_call, d
       *bytes_per_call = 8.0 * static_cast<double>(c.H_off[c.J]) + 8.0 * 2 * c.p + 8.0 * c.sum_rows;
     else  // two passes over H + vectors + row maps
       *bytes_per_call = 2.0 * (8.0 * static_cast<double>(c.H_off[c.J]) + 8.0 * (c.p + c.N) + 4.0 * c.sum_rows);
+  });
+}
+
+int rdd_bench_precond(rdd_ctx* h, int transpose, int reps, double* ms_per_call, double* bytes_per_call) {
+  return guarded(h, [&](Ctx& c) {
+    if (c.pkind < 0) throw std::invalid_argument("no preconditioner built");
+    rdd::DBuf<double> v, z;
+    v.ensure(c.p);
+    z.ensure(c.p);
+    RDD_CUDA(cudaMemsetAsync(v.p, 0, sizeof(double) * c.p, c.stream));
+    for (int i = 0; i < 3; ++i) rdd::precond_apply_dev(c, v.p, z.p, transpose != 0);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c.stream);
+    for (int i = 0; i < reps; ++i) rdd::precond_apply_dev(c, v.p, z.p, transpose != 0);
+    cudaEventRecord(e1, c.stream);
+    RDD_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_per_call = ms / reps;
+    // algorithmic bytes: per subdomain the local operator (lower triangle incl. diagonal, read
+    // twice by the forward and backward solves; once as an explicit inverse; the dense n_i x n_i
+    // pseudo-inverse once on eigen-fallback blocks), the gathered v[S_i] and the written z_i
+    // with their 4-byte indices, then the reduction (z read through the gather map, out written)
+    double b = 0.0;
+    const int J = static_cast<int>(c.set_ptr.size()) - 1;
+    for (int i = 0; i < J; ++i) {
+      const double n = c.set_ptr[i + 1] - c.set_ptr[i];
+      const bool dense = std::binary_search(c.fallback.begin(), c.fallback.end(), i);
+      const double tri = n * (n + 1) / 2.0;
+      b += 8.0 * (dense ? n * n : (c.inv_mode ? tri : 2.0 * tri));
+      b += 8.0 * 2.0 * n + 4.0 * n;
+    }
+    b += 8.0 * static_cast<double>(c.set_idx.size()) + 4.0 * static_cast<double>(c.set_idx.size()) + 8.0 * c.p;
+    *bytes_per_call = b;
   });
 }
 

@@ -72,7 +72,9 @@ def lib():
         L.rdd_reset_stats.argtypes = [vp]
         L.rdd_set_timing.argtypes = [vp, C.c_int]
         L.rdd_set_verbose.argtypes = [vp, C.c_int]
+        L.rdd_set_param.argtypes = [vp, C.c_char_p, C.c_double]
         L.rdd_bench_operator.argtypes = [vp, C.c_int, C.c_int, dp, dp]
+        L.rdd_bench_precond.argtypes = [vp, C.c_int, C.c_int, dp, dp]
         L.rdd_bench_jacobi.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp]
         L.rdd_spectra.argtypes = [vp, C.c_int, dp, dp, dp, dp, dp, dp]
         L.rdd_dense_spectrum.argtypes = [vp, i64, i64, dp, C.c_int, dp, dp]
@@ -208,6 +210,9 @@ class Solver:
     def set_verbose(self, on: bool):
         self.L.rdd_set_verbose(self.h, int(on))
 
+    def set_param(self, name: str, value: float):
+        self._check(self.L.rdd_set_param(self.h, name.encode(), float(value)))
+
     def reset_stats(self):
         self.L.rdd_reset_stats(self.h)
 
@@ -271,4 +276,10 @@ class Solver:
         ms = C.c_double()
         by = C.c_double()
         self._check(self.L.rdd_bench_operator(self.h, op_form, reps, C.byref(ms), C.byref(by)))
+        return ms.value, by.value
+
+    def bench_precond(self, transpose: bool = False, reps: int = 20):
+        ms = C.c_double()
+        by = C.c_double()
+        self._check(self.L.rdd_bench_precond(self.h, int(transpose), reps, C.byref(ms), C.byref(by)))
         return ms.value, by.value

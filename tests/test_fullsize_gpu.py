@@ -1,14 +1,24 @@
-"""BASELINE.json's configurations at full size.
+"""BASELINE.json's configurations at full size, against the CPU oracle.
 
-C1 and C5s (the 2×2×2 run of C5, m = 400, 40³ points) are compared with the CPU oracle directly:
-ranks bit-exact, iterations within 5%, e_L2 within the solve's resolution. C2 and C4 are too
-large for the oracle within a test (its serial SVDs and eigensolves take minutes), so they are
-checked through size-independent properties of the domain: covering and ordering of the
-point-to-subdomain index, the PCA threshold rule on the exported spectra, orthonormal kept
-bases, the operator's adjoint identity and linearity, symmetry and positivity of the AS
-preconditioner, a converged solve with bit-identical reruns, and the true normal-equation
-residual of the returned coefficients.
+* C1 and C5s (the 2x2x2 run of C5) are run on the oracle inside the test.
+* C2, C3, C4 and C5 are compared with committed full-size oracle fixtures
+  (tests/golden/fullsize/*.npz, written by tests/golden/make_fullsize.py; the oracle needs
+  minutes to hours for these, so it is not run on the GPU box):
+    - PCA of every subdomain (reduction.hpp:89-109): ranks p_j bit-exact; σ_i within 1e-9
+      relative above 20% of the threshold; one seeded probe per subdomain through the kept
+      projector, ‖(P_dev − P_ref)x‖ ≤ 1e-8‖x‖; the exact projector 2-norm ‖P_dev − P_ref‖₂ ≤ 1e-8 on
+      four subdomains per config (from the stored basis or its complement).
+    - full run_single with AS-PCG to 1e-10 on C2 and C4 (runner.hpp:202-275): iterations within
+      5%, e_L2 and e_L1n within 1e-8 relative, the final relative residual within 1e-8 relative,
+      the approximation at the test points ‖u_dev − u_ref‖ ≤ 1e-8‖u_exact‖.
+* C2 and C4 are also checked through size-independent properties of the domain: covering and
+  ordering of the point-to-subdomain index, the PCA threshold rule on the exported spectra,
+  orthonormal kept bases, the operator's adjoint identity and linearity, symmetry and positivity
+  of the AS preconditioner, a converged solve with bit-identical reruns, and the true
+  normal-equation residual of the returned coefficients.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -38,10 +48,11 @@ def test_full_size_vs_oracle(dev, orc, name):
     assert np.array_equal(pd, orc.geti("p_j"))  # PCA ranks bit-exact
     assert sd["DoF"] == so["DoF"] and sd["N"] == so["N"] and sd["J"] == so["J"]
     assert sd["converged"] == so["converged"] == 1
-    assert abs(sd["iterations"] - so["iterations"]) <= max(1, round(0.05 * so["iterations"])), (sd, so)
-    # rel_tol 1e-10 on the preconditioned residual: the errors agree far below the 1e-6 bar
-    assert sd["e_l2"] == pytest.approx(so["e_l2"], rel=1e-6), (sd["e_l2"], so["e_l2"])
-    assert sd["e_l1n"] == pytest.approx(so["e_l1n"], rel=1e-6)
+    assert abs(sd["iterations"] - so["iterations"]) <= int(0.05 * so["iterations"]), (sd, so)
+    assert sd["e_l2"] == pytest.approx(so["e_l2"], rel=1e-8), (sd["e_l2"], so["e_l2"])
+    assert sd["e_l1n"] == pytest.approx(so["e_l1n"], rel=1e-8)
+    ua, ue = dev.getd("approx"), dev.getd("exact")
+    assert np.linalg.norm(ua - orc.getd("approx")) <= 1e-8 * np.linalg.norm(ue)
 
 
 def _properties(dev, cfg, precond_symmetric):
@@ -113,3 +124,67 @@ def test_c4_full_size_properties(dev):
     v, w = rng.standard_normal(p), rng.standard_normal(p)
     z, zt = dev.precond_apply(v), dev.precond_apply(w, transpose=True)
     assert abs(z @ w - v @ zt) <= 1e-10 * np.linalg.norm(z) * np.linalg.norm(w)
+
+
+# ---------------------------------------------------------------- committed full-size oracle fixtures
+FIX = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "fullsize")
+PROBE_SEED = 20250  # tests/golden/make_fullsize.py
+
+
+def _fixture(kind, name):
+    path = os.path.join(FIX, f"{kind}_{name}.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"missing fixture {path} (tests/golden/make_fullsize.py)")
+    return np.load(path)
+
+
+def _check_pca(dev, cfg, fx):
+    m = cfg.m
+    pd = dev.geti("p_j")
+    assert np.array_equal(pd, fx["p_j"]), np.flatnonzero(pd != fx["p_j"])[:10]  # bit-exact ranks
+    off, sig_ref = fx["sigma_off"], fx["sigma"]
+    worst_probe = 0.0
+    for j in range(len(pd)):
+        so = sig_ref[off[j]:off[j + 1]]
+        sd = dev.getd("sigma", j)[:len(so)]
+        big = so > 0.2 * cfg.tau * so[0]
+        np.testing.assert_allclose(sd[big], so[big], rtol=1e-9, atol=0, err_msg=f"sigma j={j}")
+        V = dev.getd("V", j).reshape(int(pd[j]), m).T
+        x = np.random.default_rng(PROBE_SEED + j).standard_normal(m)
+        worst_probe = max(worst_probe, np.linalg.norm(V @ (V.T @ x) - fx["probe_px"][j]) / np.linalg.norm(x))
+    assert worst_probe <= 1e-8, worst_probe
+    for j in fx["subset"]:
+        B = fx[f"basis_{j}"]
+        Pr = B @ B.T
+        if int(fx[f"basis_kind_{j}"]) == 1:
+            Pr = np.eye(m) - Pr
+        V = dev.getd("V", int(j)).reshape(int(pd[j]), m).T
+        assert np.linalg.norm(V @ V.T - Pr, 2) <= 1e-8, int(j)
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_full_size_pca_vs_oracle_fixture(dev, name):
+    cfg = configs.BASELINE[name]()
+    dev.build_instance(cfg)
+    _check_pca(dev, cfg, _fixture("pca", name))
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_full_size_run_vs_oracle_fixture(dev, name):
+    cfg = configs.aspcg(name)
+    fx = _fixture("run", name)
+    sd = dev.run_single(cfg)
+    _check_pca(dev, cfg, fx)
+    assert sd["DoF"] == int(fx["DoF"]) and sd["N"] == int(fx["N"])
+    assert sd["converged"] == int(fx["converged"]) == 1
+    its = int(fx["iterations"])
+    assert abs(sd["iterations"] - its) <= int(0.05 * its), (sd["iterations"], its)
+    assert sd["e_l2"] == pytest.approx(float(fx["e_l2"]), rel=1e-8), (sd["e_l2"], float(fx["e_l2"]))
+    assert sd["e_l1n"] == pytest.approx(float(fx["e_l1n"]), rel=1e-8)
+    assert sd["final_residual"] == pytest.approx(float(fx["final_residual"]), rel=1e-8)
+    ue = dev.getd("exact")
+    assert np.linalg.norm(dev.getd("approx") - fx["approx"]) <= 1e-8 * np.linalg.norm(ue)
+    # the residual histories follow each other while they are far above rounding
+    hd, ho = dev.getd("hist", 0), fx["hist"]
+    k = min(len(hd), len(ho))
+    np.testing.assert_allclose(hd[:k][ho[:k] > 1e-6], ho[:k][ho[:k] > 1e-6], rtol=1e-6)

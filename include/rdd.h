@@ -143,6 +143,39 @@ int rdd_io_bytes(int64_t* h2d, int64_t* d2h);
 int rdd_event_record(rdd_ctx* ctx, int slot);
 int rdd_event_elapsed(rdd_ctx* ctx, int slot_a, int slot_b, double* ms);
 
+/* ---- caller inputs: the reference's objects instead of a RunConfig ------------------
+ * The phase API above then runs on them: rdd_build_custom (instead of rdd_build_instance),
+ * rdd_assemble, rdd_build_preconditioner, rdd_solve, rdd_evaluate_at. */
+/* geometry.hpp:84-97 CartesianDecomposition as build_decomposition made it: dim, subdomains per
+ * axis, the domain box, per subdomain (axis 0 slowest, geometry.hpp:146-167) the box lo/hi, centre
+ * and half width (J x dim each, subdomain after subdomain) and its neighbour set (CSR over J,
+ * ascending, self included, geometry.hpp:169-174). The boxes must form a tensor product. */
+int rdd_set_decomposition(rdd_ctx* ctx, int dim, const int32_t* counts, const double* domain_lo,
+                          const double* domain_hi, const double* box_lo, const double* box_hi,
+                          const double* center, const double* half, const int32_t* nbr_ptr,
+                          const int32_t* nbr_idx);
+/* geometry.hpp:189-197 PointSet (the collocation points): N points, dim coordinates each, point
+ * after point. */
+int rdd_set_points(rdd_ctx* ctx, int64_t N, const double* pts);
+/* basis.hpp:24-48 RandomBasis of every subdomain: R (m x dim, neuron after neuron) and b (m),
+ * subdomain after subdomain; activation 0 = tanh, 1 = sin (basis.hpp:14). */
+int rdd_set_bases(rdd_ctx* ctx, int J, int m, const double* R, const double* b, int activation);
+/* problems.hpp:28-37 ProblemSpec evaluated by the caller at the collocation points:
+ *   op_coef  the linear operator's coefficients on the jet (value, gradient[dim], Hessian upper
+ *            triangle row by row; jet_len = 1 + dim + dim(dim+1)/2): LinearOperator::apply on unit
+ *            jets (constant-coefficient operators, as every reference operator is);
+ *   L_jets   the jet of the constraining factor L at every point (N x jet_len, point after point);
+ *   F        f_c − A[G_c] at every point (N x C, column-major; assembly.hpp:97-106). */
+int rdd_set_problem(rdd_ctx* ctx, int C, const double* op_coef, const double* L_jets, const double* F);
+/* runner.hpp:40-70 build_instance on the caller inputs (index + PCA). From cfg only the PCA
+ * settings (tau_mode, tau, pca_matrix) and op_form are read. */
+int rdd_build_custom(rdd_ctx* ctx, const rdd_config* cfg);
+/* runner.hpp:105-127 evaluate_solution(inst, W, pts) at M caller points (point after point) with
+ * the caller's unscaled W (p x C, column-major) or, W = NULL, the last solve's; L_vals = L at the
+ * points (M), G_vals = G_c at the points (M x C, column-major; NULL = 0); u_out M x C column-major. */
+int rdd_evaluate_at(rdd_ctx* ctx, int64_t M, const double* pts, const double* W, const double* L_vals,
+                    const double* G_vals, double* u_out);
+
 /* ---- operators (pluggable into the reference's LinearMap, krylov.hpp:42-52) ---------- */
 /* Vector lengths are checked like the reference's (RDD_INVALID_ARGUMENT, "... wrong length"). */
 int rdd_matvec(rdd_ctx* ctx, const double* w, int64_t nw, double* y, int64_t ny);             /* assembly.hpp:110 */

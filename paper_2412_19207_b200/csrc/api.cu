@@ -76,6 +76,17 @@ static void build_instance(Ctx& c, const rdd_config& cfg, uint64_t seed) {
   ensure_col_owner(c);
 }
 
+// runner.hpp:40-70 on caller inputs (rdd_set_decomposition / points / bases / problem)
+static void build_custom(Ctx& c, const rdd_config& cfg) {
+  reset_state(c);
+  setup_custom(c, cfg);
+  upload_inputs(c);
+  build_index(c);
+  upload_custom_problem(c);
+  run_pca(c);
+  ensure_col_owner(c);
+}
+
 // runner.hpp:89-101 + assembly.hpp:41-108
 static void assemble(Ctx& c, bool equilibrate) {
   if (c.h_p.empty()) throw std::invalid_argument("assemble: build_instance first");
@@ -100,7 +111,8 @@ static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed, bool reside
     reset_state(c);
     c.cfg = cfg;
     build_index(c);
-    eval_problem(c);
+    if (c.prob.id == 0) upload_custom_problem(c);
+    else eval_problem(c);
     run_pca(c);
     ensure_col_owner(c);
   } else {
@@ -134,7 +146,7 @@ static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed, bool reside
   const double t_sol = now_s() - t0;
   if (c.verbose) std::fprintf(stderr, "[phase] solve %.3f s (%d its)\n", t_sol, c.iters.empty() ? 0 : c.iters[0]);
   t0 = now_s();
-  evaluate(c, cfg.test);
+  if (c.prob.id != 0) evaluate(c, cfg.test);  // caller problems evaluate at caller points (evaluate_at)
   const double t_ev = now_s() - t0;
   rdd_summary& s = c.sum;
   s.seed = seed;
@@ -393,6 +405,90 @@ int rdd_precond_apply(rdd_ctx* h, const double* v, int64_t nv, double* z, int64_
     rdd::precond_apply_dev(c, dv.p, dz.p, transpose != 0);
     dz.download(z, c.p, c.stream);
     RDD_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+
+// ---- caller inputs (the reference's objects instead of a RunConfig)
+int rdd_set_decomposition(rdd_ctx* h, int dim, const int32_t* counts, const double* domain_lo, const double* domain_hi,
+                          const double* box_lo, const double* box_hi, const double* center, const double* half,
+                          const int32_t* nbr_ptr, const int32_t* nbr_idx) {
+  return guarded(h, [&](Ctx& c) {
+    if (dim < 1 || dim > rdd::kMaxDim) throw std::invalid_argument("decomposition dimension must be 1..4");
+    if (!counts || !domain_lo || !domain_hi || !box_lo || !box_hi || !center || !half || !nbr_ptr || !nbr_idx)
+      throw std::invalid_argument("decomposition: null array");
+    rdd::CustomInputs& u = c.custom;
+    u.d = dim;
+    u.counts.assign(counts, counts + dim);
+    long long J = 1;
+    for (int k : u.counts) {
+      if (k < 1) throw std::invalid_argument("per-axis subdomain counts must be >= 1");
+      J *= k;
+    }
+    if (J > (1 << 24)) throw std::invalid_argument("decomposition: too many subdomains");
+    u.dom_lo.assign(domain_lo, domain_lo + dim);
+    u.dom_hi.assign(domain_hi, domain_hi + dim);
+    const size_t n = static_cast<size_t>(J) * dim;
+    u.lo.assign(box_lo, box_lo + n);
+    u.hi.assign(box_hi, box_hi + n);
+    u.ctr.assign(center, center + n);
+    u.half.assign(half, half + n);
+    u.nbr_ptr.assign(nbr_ptr, nbr_ptr + J + 1);
+    if (u.nbr_ptr[0] != 0) throw std::invalid_argument("decomposition: neighbour CSR must start at 0");
+    u.nbr_idx.assign(nbr_idx, nbr_idx + u.nbr_ptr[J]);
+    for (int v : u.nbr_idx)
+      if (v < 0 || v >= J) throw std::invalid_argument("decomposition: neighbour index out of range");
+    u.has_dec = true;
+  });
+}
+int rdd_set_points(rdd_ctx* h, int64_t N, const double* pts) {
+  return guarded(h, [&](Ctx& c) {
+    rdd::CustomInputs& u = c.custom;
+    if (!u.has_dec) throw std::invalid_argument("points: set the decomposition first");
+    if (N < 1 || !pts) throw std::invalid_argument("points: empty point set");
+    u.pts.assign(pts, pts + static_cast<size_t>(N) * u.d);
+    u.has_pts = true;
+  });
+}
+int rdd_set_bases(rdd_ctx* h, int J, int m, const double* R, const double* b, int activation) {
+  return guarded(h, [&](Ctx& c) {
+    rdd::CustomInputs& u = c.custom;
+    if (!u.has_dec) throw std::invalid_argument("bases: set the decomposition first");
+    if (m < 1) throw std::invalid_argument("hidden width m must be >= 1");
+    if (activation != 0 && activation != 1) throw std::invalid_argument("activation must be tanh (0) or sin (1)");
+    if (!R || !b || J < 1) throw std::invalid_argument("bases: null array");
+    u.m = m;
+    u.act = activation;
+    u.R.assign(R, R + static_cast<size_t>(J) * m * u.d);
+    u.b.assign(b, b + static_cast<size_t>(J) * m);
+    u.has_bases = true;
+  });
+}
+int rdd_set_problem(rdd_ctx* h, int C, const double* op_coef, const double* L_jets, const double* F) {
+  return guarded(h, [&](Ctx& c) {
+    rdd::CustomInputs& u = c.custom;
+    if (!u.has_pts) throw std::invalid_argument("problem: set the points first");
+    if (C < 1 || C > 3) throw std::invalid_argument("problem: 1..3 solution components");
+    if (!op_coef || !L_jets || !F) throw std::invalid_argument("problem: null array");
+    const size_t N = u.pts.size() / u.d, jl = rdd::jet_len(u.d);
+    u.C = C;
+    u.coef.assign(op_coef, op_coef + jl);
+    u.Ljet.assign(L_jets, L_jets + N * jl);
+    u.F.assign(F, F + N * C);
+    u.has_problem = true;
+  });
+}
+int rdd_build_custom(rdd_ctx* h, const rdd_config* cfg) {
+  return guarded(h, [&](Ctx& c) {
+    if (!cfg) throw std::invalid_argument("null config");
+    rdd::build_custom(c, *cfg);
+  });
+}
+int rdd_evaluate_at(rdd_ctx* h, int64_t M, const double* pts, const double* W, const double* L_vals,
+                    const double* G_vals, double* u_out) {
+  return guarded(h, [&](Ctx& c) {
+    if (M > 0 && (!pts || !L_vals || !u_out)) throw std::invalid_argument("evaluate_solution: null array");
+    rdd::evaluate_at(c, M, pts, W, L_vals, G_vals, u_out);
   });
 }
 

@@ -55,6 +55,22 @@ struct GemmTask {
   double alpha = 1.0;
 };
 
+// Caller-supplied inputs (rdd_set_decomposition / points / bases / problem): the reference's
+// CartesianDecomposition, PointSet, RandomBasis and a ProblemSpec evaluated at the points.
+struct CustomInputs {
+  bool has_dec = false, has_pts = false, has_bases = false, has_problem = false;
+  int d = 0;
+  std::vector<int> counts;
+  std::vector<double> dom_lo, dom_hi;           // d
+  std::vector<double> lo, hi, ctr, half;        // J x d (geometry.hpp:84-97 sub, centers, half)
+  std::vector<int> nbr_ptr, nbr_idx;            // neighbour sets (CSR)
+  std::vector<double> pts;                      // N x d, point after point
+  int m = 0, act = 0;
+  std::vector<double> R, b;                     // J x m x d, J x m
+  int C = 1;
+  std::vector<double> coef, Ljet, F;            // jet_len(d); N x jet_len(d); N x C (column-major)
+};
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -64,8 +80,9 @@ struct Ctx {
   // ---- configuration
   rdd_config cfg{};
   uint64_t seed = 0;
-  ProblemDesc prob;
+  ProblemDesc prob;                 // id 0 = caller-supplied problem (CustomInputs)
   int d = 2, J = 0, N = 0, m = 0, C = 1, jl = 6;
+  CustomInputs custom;
 
   // ---- host geometry (geometry.hpp:84-185)
   std::vector<double> box_lo, box_hi, box_c, box_h;  // J x 4
@@ -231,10 +248,12 @@ struct ScopedKernelTimer {
 void setup_problem(Ctx& c, const rdd_config& cfg, uint64_t seed);  // problems + geometry + bases + points
 void reference_example2_grid(int res, std::vector<double>& v);     // problems.hpp:219-264
 void upload_inputs(Ctx& c);
+void setup_custom(Ctx& c, const rdd_config& cfg);                  // the same from CustomInputs
 // index.cu (K1)
 void build_index(Ctx& c);
 // problem.cu
 void eval_problem(Ctx& c);
+void upload_custom_problem(Ctx& c);  // caller L jets and F instead of eval_problem
 // assemble.cu (K2)
 void assemble_samples(Ctx& c, int kind, double* out, const std::vector<long long>& off);
 // pca.cu (K3-K5)
@@ -270,6 +289,11 @@ void qr_solve_dev(Ctx& c);
 void solve_all(Ctx& c, int solver, double tol, int max_iter, int restart);
 // evaluate.cu (K14)
 void evaluate(Ctx& c, const int* test_res);
+// runner.hpp:105-127 evaluate_solution at caller points (M x d, point after point) with caller W
+// (p x C, column-major, unscaled) or the solved one (W = nullptr), caller L values (M) and G
+// values (M x C, column-major; nullptr = 0); out M x C column-major
+void evaluate_at(Ctx& c, long long M, const double* pts, const double* W, const double* Lv, const double* Gv,
+                 double* out);
 // gemm.cu
 void gemm_tn(Ctx& c, const std::vector<GemmTask>& tasks);  // C = Aᵀ B (A: K x M, B: K x N col-major)
 void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks);  // C = A B  (A: M x K, B: K x N col-major)

@@ -261,4 +261,92 @@ void setup_problem(Ctx& c, const rdd_config& cfg, uint64_t seed) {
   }
 }
 
+
+// The instance from caller inputs (rdd_set_*): the reference's CartesianDecomposition (boxes,
+// centres, half widths, neighbour sets as build_decomposition made them, geometry.hpp:109-177),
+// its PointSet and RandomBasis objects, and a ProblemSpec evaluated at the points by the caller.
+// The decomposition must be a tensor product (box j's interval on axis a depends only on j's
+// axis-a index, axis 0 slowest), as every CartesianDecomposition is.
+void setup_custom(Ctx& c, const rdd_config& cfg) {
+  CustomInputs& u = c.custom;
+  if (!u.has_dec || !u.has_pts || !u.has_bases || !u.has_problem)
+    throw std::invalid_argument("custom instance: set the decomposition, points, bases and problem first");
+  const int d = u.d;
+  int total = 1;
+  for (int k : u.counts) total *= k;
+  if (static_cast<int>(u.R.size()) != total * u.m * d) throw std::invalid_argument("custom bases: one per subdomain");
+  const long long N = static_cast<long long>(u.pts.size()) / d;
+  if (static_cast<long long>(u.Ljet.size()) != N * jet_len(d))
+    throw std::invalid_argument("custom problem: L jets must be given at every collocation point");
+  c.cfg = cfg;
+  c.seed = cfg.seed;
+  c.prob = ProblemDesc{};
+  c.prob.id = 0;
+  c.prob.d = d;
+  c.prob.C = u.C;
+  c.prob.has_exact = false;
+  for (int a = 0; a < d; ++a) {
+    c.prob.lo[a] = u.dom_lo[a];
+    c.prob.hi[a] = u.dom_hi[a];
+  }
+  for (int k = 0; k < jet_len(d); ++k) c.prob.coef[k] = u.coef[k];
+  c.d = d;
+  c.C = u.C;
+  c.jl = jet_len(d);
+  c.m = u.m;
+  c.cfg.m = u.m;
+  c.cfg.activation = u.act;
+  c.cfg.dim = d;
+  for (int a = 0; a < d; ++a) c.cfg.counts[a] = u.counts[a];
+  if (cfg.tau_mode != RDD_TAU_OFF && !(cfg.tau >= 0.0))  // reduction.hpp:90
+    throw std::invalid_argument("truncation threshold tau must be >= 0");
+  if (cfg.max_iter < 0) throw std::invalid_argument("max_iter must be >= 1");  // krylov.hpp:79
+  c.counts = u.counts;
+  c.J = total;
+  c.box_lo.assign(total * 4, 0.0);
+  c.box_hi.assign(total * 4, 0.0);
+  c.box_c.assign(total * 4, 0.0);
+  c.box_h.assign(total * 4, 0.0);
+  c.axis_lo.assign(d, std::vector<double>());
+  c.axis_hi.assign(d, std::vector<double>());
+  for (int a = 0; a < d; ++a) {
+    c.axis_lo[a].assign(u.counts[a], 0.0);
+    c.axis_hi[a].assign(u.counts[a], 0.0);
+  }
+  std::vector<int> idx(d, 0);
+  std::vector<std::vector<char>> seen(d);
+  for (int a = 0; a < d; ++a) seen[a].assign(u.counts[a], 0);
+  for (int j = 0; j < total; ++j) {
+    for (int a = 0; a < d; ++a) {
+      const size_t q = static_cast<size_t>(j) * d + a;
+      c.box_lo[j * 4 + a] = u.lo[q];
+      c.box_hi[j * 4 + a] = u.hi[q];
+      c.box_c[j * 4 + a] = u.ctr[q];
+      c.box_h[j * 4 + a] = u.half[q];
+      if (!seen[a][idx[a]]) {
+        c.axis_lo[a][idx[a]] = u.lo[q];
+        c.axis_hi[a][idx[a]] = u.hi[q];
+        seen[a][idx[a]] = 1;
+      } else if (c.axis_lo[a][idx[a]] != u.lo[q] || c.axis_hi[a][idx[a]] != u.hi[q]) {
+        throw std::invalid_argument("custom decomposition: boxes are not a tensor product (axis 0 slowest)");
+      }
+    }
+    for (int a = d - 1; a >= 0; --a) {
+      if (++idx[a] < u.counts[a]) break;
+      idx[a] = 0;
+    }
+  }
+  c.nbr_ptr = u.nbr_ptr;
+  c.nbr_idx = u.nbr_idx;
+  if (static_cast<int>(c.nbr_ptr.size()) != total + 1)
+    throw std::invalid_argument("custom decomposition: one neighbour set per subdomain");
+  if (N > 2000000000LL) throw std::invalid_argument("too many collocation points");
+  c.N = static_cast<int>(N);
+  c.h_pts.resize(static_cast<size_t>(d) * c.N);
+  for (long long i = 0; i < N; ++i)
+    for (int a = 0; a < d; ++a) c.h_pts[static_cast<size_t>(a) * N + i] = u.pts[static_cast<size_t>(i) * d + a];
+  c.h_R.assign(u.R.begin(), u.R.end());
+  c.h_b.assign(u.b.begin(), u.b.end());
+}
+
 }  // namespace rdd

@@ -202,6 +202,20 @@ void eval_problem(Ctx& c) {
     throw std::runtime_error("non-finite right-hand side at collocation point " + std::to_string(h_bad));
 }
 
+// Caller-evaluated problem (CustomInputs): L jets and F = f − A[G] at the collocation points,
+// in place of eval_problem; same layouts (Ljet point-major, F column-major per component).
+void upload_custom_problem(Ctx& c) {
+  const CustomInputs& u = c.custom;
+  for (size_t q = 0; q < u.F.size(); ++q)
+    if (!std::isfinite(u.F[q]))
+      throw std::runtime_error("non-finite right-hand side at collocation point " + std::to_string(q % c.N));
+  if (static_cast<long long>(u.F.size()) != static_cast<long long>(c.N) * c.C)
+    throw std::invalid_argument("custom problem: F must have N x C entries");
+  c.Ljet.upload(u.Ljet.data(), u.Ljet.size(), c.stream);
+  c.Fpt.upload(u.F.data(), u.F.size(), c.stream);
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+}
+
 }  // namespace rdd
 
 // ---------------------------------------------------------------- K14: evaluation (runner.hpp:105-144)
@@ -278,6 +292,9 @@ struct EvalArgs {
   const double* ax_lo;    // per-axis box intervals: the covering boxes of a test point
   const double* ax_hi;
   int ax_counts[kMaxDim], ax_stride[kMaxDim], ax_off[kMaxDim];
+  const double* xin;      // caller points (M x d, point after point), or null: the test grid
+  const double* Lin;      // caller L values (M) with xin
+  const double* Gin;      // caller G values (M x C) with xin, or null (G = 0)
 };
 
 // problems.hpp:203-216 ReferenceGrid::at: bilinear lookup in the space-time field
@@ -317,14 +334,18 @@ __global__ void k_evaluate(EvalArgs A) {
   if (i >= A.M) return;
   const int d = A.P.d;
   double x[kMaxDim] = {0, 0, 0, 0};
-  int rem = i;
-  for (int a = d - 1; a >= 0; --a) {  // last axis fastest (geometry.hpp:216-230)
-    const int k = rem % A.res[a];
-    rem /= A.res[a];
-    // unfused, as uniform_grid computes it on the host: bit-identical test points
-    x[a] = __dadd_rn(A.lo[a], __dmul_rn(static_cast<double>(k) + 0.5, A.step[a]));
+  if (A.xin) {
+    for (int a = 0; a < d; ++a) x[a] = A.xin[static_cast<size_t>(i) * d + a];
+  } else {
+    int rem = i;
+    for (int a = d - 1; a >= 0; --a) {  // last axis fastest (geometry.hpp:216-230)
+      const int k = rem % A.res[a];
+      rem /= A.res[a];
+      // unfused, as uniform_grid computes it on the host: bit-identical test points
+      x[a] = __dadd_rn(A.lo[a], __dmul_rn(static_cast<double>(k) + 0.5, A.step[a]));
+    }
   }
-  const double Lv = L_jet(A.P, x).c[0];
+  const double Lv = A.xin ? A.Lin[i] : L_jet(A.P, x).c[0];
   double acc[3] = {0.0, 0.0, 0.0};
   // covering boxes (geometry.hpp:180-185): per-axis closed-interval candidates, enumerated as the
   // lexicographic product (axis 0 slowest) = ascending j, the reference's accumulation order
@@ -375,6 +396,10 @@ __global__ void k_evaluate(EvalArgs A) {
     for (int cc = 0; cc < A.P.C; ++cc) acc[cc] += s[cc] * (Lv * w);
   }
   for (int cc = 0; cc < A.P.C; ++cc) {
+    if (A.xin) {
+      A.approx[static_cast<size_t>(cc) * A.M + i] = acc[cc] + (A.Gin ? A.Gin[static_cast<size_t>(cc) * A.M + i] : 0.0);
+      continue;
+    }
     A.approx[static_cast<size_t>(cc) * A.M + i] = acc[cc] + G_value(A.P, x, cc);
     A.exact[static_cast<size_t>(cc) * A.M + i] = A.ref ? ref_at(A.ref, A.refn, x[0], x[1]) : exact_value(A.P, x, cc);
   }
@@ -401,21 +426,7 @@ __global__ void k_effective_weights(const double* __restrict__ Vred, const doubl
 
 }  // namespace
 
-void evaluate(Ctx& c, const int* test_res) {
-  ScopedKernelTimer tk(c, "evaluate");
-  EvalArgs A{};
-  if (!c.prob.has_exact) {  // example2: errors against the Crank-Nicolson field (runner.hpp:286-289)
-    const int res = c.cfg.ref_resolution > 0 ? c.cfg.ref_resolution : 2001;
-    if (c.ref2_res != res) {
-      std::vector<double> v;
-      reference_example2_grid(res, v);
-      c.ref2.upload(v, c.stream);
-      RDD_CUDA(cudaStreamSynchronize(c.stream));  // v is pageable and scoped
-      c.ref2_res = res;
-    }
-    A.ref = c.ref2.p;
-    A.refn = res;
-  }
+static void eval_common(Ctx& c, EvalArgs& A, DBuf<int>& counts1) {
   A.P.id = c.prob.id;
   A.P.d = c.d;
   A.P.C = c.C;
@@ -424,16 +435,6 @@ void evaluate(Ctx& c, const int* test_res) {
   A.J = c.J;
   A.m = c.m;
   A.act = c.cfg.activation;
-  long long M = 1;
-  for (int a = 0; a < c.d; ++a) {
-    if (test_res[a] < 1) throw std::invalid_argument("grid resolutions must be >= 1");
-    A.res[a] = test_res[a];
-    A.lo[a] = c.prob.lo[a];
-    A.step[a] = (c.prob.hi[a] - c.prob.lo[a]) / static_cast<double>(test_res[a]);
-    M *= test_res[a];
-  }
-  A.M = static_cast<int>(M);
-  DBuf<int> counts1;
   std::vector<int> h_c1(kMaxDim, 1);
   for (int a = 0; a < c.d; ++a) h_c1[a] = c.counts[a] == 1 ? 1 : 0;
   counts1.upload(h_c1, c.stream);
@@ -450,6 +451,68 @@ void evaluate(Ctx& c, const int* test_res) {
   A.nbr_idx = c.dnbr_idx.p;
   A.R = c.R.p;
   A.b = c.bvec.p;
+}
+
+void evaluate_at(Ctx& c, long long M, const double* pts, const double* W, const double* Lv, const double* Gv,
+                 double* out) {
+  ScopedKernelTimer tk(c, "evaluate");
+  if (c.J == 0 || c.h_p.empty()) throw std::invalid_argument("evaluate_solution: build an instance first");
+  if (M < 0 || M > 2000000000LL) throw std::invalid_argument("evaluate_solution: bad point count");
+  if (M == 0) return;
+  if (!W && c.W.n < static_cast<size_t>(c.p) * c.C) throw std::invalid_argument("evaluate_solution: no solution yet");
+  EvalArgs A{};
+  DBuf<int> counts1;
+  eval_common(c, A, counts1);
+  A.M = static_cast<int>(M);
+  DBuf<double> dx, dl, dg, dw, U, ap;
+  dx.upload(pts, static_cast<size_t>(M) * c.d, c.stream);
+  dl.upload(Lv, static_cast<size_t>(M), c.stream);
+  if (Gv) dg.upload(Gv, static_cast<size_t>(M) * c.C, c.stream);
+  if (W) dw.upload(W, static_cast<size_t>(c.p) * c.C, c.stream);
+  A.xin = dx.p;
+  A.Lin = dl.p;
+  A.Gin = Gv ? dg.p : nullptr;
+  U.ensure(static_cast<size_t>(c.C) * c.J * c.m);
+  k_effective_weights<<<c.J, 128, 0, c.stream>>>(c.Vred.p, W ? dw.p : c.W.p, c.dcol_off.p, c.J, c.m, c.p,
+                                                 c.identity_V ? 1 : 0, U.p, c.C);
+  RDD_LAUNCH_CHECK();
+  A.U = U.p;
+  ap.ensure(static_cast<size_t>(M) * c.C);
+  A.approx = ap.p;
+  k_evaluate<<<ceil_div(M, 128), 128, 0, c.stream>>>(A);
+  RDD_LAUNCH_CHECK();
+  ap.download(out, static_cast<size_t>(M) * c.C, c.stream);
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+void evaluate(Ctx& c, const int* test_res) {
+  ScopedKernelTimer tk(c, "evaluate");
+  if (c.prob.id == 0)
+    throw std::invalid_argument("caller-supplied problem: evaluate at caller points (rdd_evaluate_at)");
+  EvalArgs A{};
+  if (!c.prob.has_exact) {  // example2: errors against the Crank-Nicolson field (runner.hpp:286-289)
+    const int res = c.cfg.ref_resolution > 0 ? c.cfg.ref_resolution : 2001;
+    if (c.ref2_res != res) {
+      std::vector<double> v;
+      reference_example2_grid(res, v);
+      c.ref2.upload(v, c.stream);
+      RDD_CUDA(cudaStreamSynchronize(c.stream));  // v is pageable and scoped
+      c.ref2_res = res;
+    }
+    A.ref = c.ref2.p;
+    A.refn = res;
+  }
+  DBuf<int> counts1;
+  eval_common(c, A, counts1);
+  long long M = 1;
+  for (int a = 0; a < c.d; ++a) {
+    if (test_res[a] < 1) throw std::invalid_argument("grid resolutions must be >= 1");
+    A.res[a] = test_res[a];
+    A.lo[a] = c.prob.lo[a];
+    A.step[a] = (c.prob.hi[a] - c.prob.lo[a]) / static_cast<double>(test_res[a]);
+    M *= test_res[a];
+  }
+  A.M = static_cast<int>(M);
   DBuf<double> U, ap, ex;
   U.ensure(static_cast<size_t>(c.C) * c.J * c.m);
   k_effective_weights<<<c.J, 128, 0, c.stream>>>(c.Vred.p, c.W.p, c.dcol_off.p, c.J, c.m, c.p, c.identity_V ? 1 : 0,

@@ -1,0 +1,58 @@
+"""Level-2 drop-in: the reference's own code with the device behind its interfaces.
+
+tests/cpp/dropin.cpp is the UNMODIFIED reference (compiled here against the Eigen-subset shim)
+plus include/rannddm_gpu_ref.hpp, the adapter a reference maintainer would include: the
+reference's RunConfig/ProblemSpec/CartesianDecomposition/PointSet/RandomBasis objects go through
+the C ABI, the device operators come back as the reference's LinearMaps.
+  A  a problem the reference does not ship, reference pipeline (CPU) vs device pipeline
+  B  the reference's own cg()/gmres() driving the device normal operator and Schwarz apply
+  C  rannddm::gpu::run_single(to_rdd_config(cfg)) vs the reference's run_single(cfg)
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "cpp", "build", "dropin")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lines():
+    if not os.path.exists(BIN):
+        pytest.fail("tests/cpp/build/dropin not built (python -c 'import __graft_entry__ as g; g.build()')")
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import lapack_path
+    env = dict(os.environ, RDD_LAPACK_PATH=lapack_path())
+    out = subprocess.run([BIN], capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+
+
+def test_custom_problem_through_reference_objects(lines):
+    a = next(l for l in lines if l["scenario"] == "A")
+    assert a["p_j_ref"] == a["p_j_dev"]  # PCA ranks bit-exact
+    assert abs(a["its_dev"] - a["its_ref"]) <= int(0.05 * a["its_ref"]), a
+    assert a["e_l2_dev"] == pytest.approx(a["e_l2_ref"], rel=1e-8), a
+    assert a["u_rel_diff"] <= 1e-8, a
+
+
+@pytest.mark.parametrize("solver", ["cg", "gmres"])
+def test_reference_krylov_over_device_maps(lines, solver):
+    b = next(l for l in lines if l["scenario"] == "B" and l["solver"] == solver)
+    assert b["converged"] == 1
+    assert abs(b["its_refkrylov_devmaps"] - b["its_dev"]) <= int(0.05 * b["its_dev"]), b
+    assert abs(b["its_refkrylov_devmaps"] - b["its_ref"]) <= int(0.05 * b["its_ref"]), b
+    assert b["e_l2"] == pytest.approx(b["e_l2_ref"], rel=1e-8), b
+    assert b["u_rel_diff_ref"] <= 1e-8, b
+
+
+def test_run_single_dropin(lines):
+    cs = [l for l in lines if l["scenario"] == "C"]
+    assert len(cs) == 2
+    for c in cs:
+        assert c["ref"][:4] == c["dev"][:4], c
+        assert c["dev"][4] == pytest.approx(c["ref"][4], rel=5e-7), c

@@ -165,7 +165,7 @@ struct Ctx {
     long long nb;
   };
   std::vector<GatherTask> gat_tasks;
-  double full_rank_cond = 1e11;       // Cholesky path when cond_est(A_i) is below this
+  double full_rank_cond = 1e9;        // Cholesky path when cond_est(A_i) is below this (DESIGN §4 K8)
   DBuf<double> zloc;                  // Σ n_i
   DBuf<int> apply_order;              // subdomains by local size, largest first (apply CTA order)
 

@@ -36,7 +36,10 @@ def test_custom_problem_through_reference_objects(lines):
     a = next(l for l in lines if l["scenario"] == "A")
     assert a["p_j_ref"] == a["p_j_dev"]  # PCA ranks bit-exact
     assert abs(a["its_dev"] - a["its_ref"]) <= int(0.05 * a["its_ref"]), a
-    assert a["e_l2_dev"] == pytest.approx(a["e_l2_ref"], rel=1e-8), a
+    # e_L2 = ‖u − u*‖/‖u*‖: the two relative errors agree within 1e-8, and so do the solutions
+    # themselves (‖u_dev − u_ref‖ ≤ 1e-8‖u*‖ bounds |Δe_L2| by the triangle inequality); a bar
+    # relative to e_L2 itself would be ill-posed here, where e_L2 ~ 1e-7
+    assert abs(a["e_l2_dev"] - a["e_l2_ref"]) <= 1e-8, a
     assert a["u_rel_diff"] <= 1e-8, a
 
 
@@ -46,7 +49,7 @@ def test_reference_krylov_over_device_maps(lines, solver):
     assert b["converged"] == 1
     assert abs(b["its_refkrylov_devmaps"] - b["its_dev"]) <= int(0.05 * b["its_dev"]), b
     assert abs(b["its_refkrylov_devmaps"] - b["its_ref"]) <= int(0.05 * b["its_ref"]), b
-    assert b["e_l2"] == pytest.approx(b["e_l2_ref"], rel=1e-8), b
+    assert abs(b["e_l2"] - b["e_l2_ref"]) <= 1e-8, b
     assert b["u_rel_diff_ref"] <= 1e-8, b
 
 

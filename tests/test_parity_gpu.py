@@ -1,8 +1,15 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeds.
 
 Bars (BASELINE.json north_star): point->subdomain indexing and PCA ranks bit-exact; PCA
-subspaces within a projector difference of 1e-8; iteration counts within 5%; floating-point
-results within the stated relative tolerances below.
+subspaces within a projector difference of 1e-8; iteration counts within 5% (no ±1 slack: below
+20 iterations they must be equal); H, the operators and the normal blocks within 1e-9 relative
+(1e-12 with PCA off); the relative L2 error on the test points within 1e-8 and the solutions
+themselves within ‖u_dev − u_ref‖ ≤ 1e-8‖u*‖ (solves to rel_tol 1e-10).
+
+e_L2 = ‖u − u*‖/‖u*‖ is itself a relative quantity; the bar is on its difference (|Δe_L2| ≤ 1e-8,
+implied by the solution bar through the triangle inequality). A bar relative to e_L2 would be
+ill-posed where e_L2 ≪ 1 (1e-7 on some cases): it would ask the two solutions to agree to
+1e-15 relative, below the rounding of the local solves (ε·cond(A_i)).
 """
 import numpy as np
 import pytest
@@ -104,7 +111,7 @@ def test_assembly_and_operators(dev, orc, name):
     dev.build_instance(cfg).assemble(eq)
     orc.build_instance(cfg).assemble(eq)
     J = int(orc.geti("J")[0])
-    tol = 1e-12 if cfg.tau_mode == A.TAU_OFF else 1e-7
+    tol = 1e-12 if cfg.tau_mode == A.TAU_OFF else 1e-9
     for j in range(J):
         Hd, Ho = dev.block(j), orc.block(j)
         assert Hd.shape == Ho.shape
@@ -134,7 +141,7 @@ def test_normal_blocks_and_schwarz(dev, orc, name):
     orc.build_instance(cfg).assemble(True).build_preconditioner(cfg.precond)
     assert np.array_equal(dev.geti("nb_pairs"), orc.geti("nb_pairs"))
     Ad, Ao = dev.getd("nb_dense"), orc.getd("nb_dense")
-    tol = 1e-12 if cfg.tau_mode == A.TAU_OFF else 1e-7
+    tol = 1e-12 if cfg.tau_mode == A.TAU_OFF else 1e-9
     assert np.linalg.norm(Ad - Ao) <= tol * np.linalg.norm(Ao)
     assert np.array_equal(dev.geti("local_rank"), orc.geti("local_rank")), name
     rng = np.random.default_rng(7)
@@ -150,6 +157,7 @@ def test_normal_blocks_and_schwarz(dev, orc, name):
 
 @pytest.mark.parametrize("name", list(CASES))
 def test_run_single(dev, orc, name):
+    # at the case's own tolerance: iterations, convergence and the residual history
     cfg = A.Config.from_buffer_copy(CASES[name])
     if cfg.precond < 0:
         cfg.precond = A.PRECOND_AS
@@ -157,10 +165,21 @@ def test_run_single(dev, orc, name):
     sd = dev.run_single(cfg)
     assert sd["DoF"] == so["DoF"] and sd["N"] == so["N"] and sd["J"] == so["J"]
     assert sd["converged"] == so["converged"]
-    assert abs(sd["iterations"] - so["iterations"]) <= max(1, round(0.05 * so["iterations"])), (sd, so)
-    # the solve stops at rel_tol; errors agree to the level the solve resolves
-    tol = max(1e-6, 100 * cfg.rel_tol)
-    assert sd["e_l2"] == pytest.approx(so["e_l2"], rel=tol), (name, sd["e_l2"], so["e_l2"])
+    assert abs(sd["iterations"] - so["iterations"]) <= int(0.05 * so["iterations"]), (sd, so)
+    hd, ho = dev.getd("hist", 0), orc.getd("hist", 0)
+    keep = ho[:len(hd)] > 1e-6  # above the rounding of the local solves
+    np.testing.assert_allclose(hd[:len(ho)][keep[:len(hd)]], ho[:len(hd)][keep[:len(hd)]], rtol=1e-6)
+    # solved to rel_tol 1e-10: the relative L2 errors and the solutions at the test points
+    cfg.rel_tol = 1e-10
+    so = orc.run_single(cfg)
+    uo = orc.getd("approx")
+    sd = dev.run_single(cfg)
+    ud, ue = dev.getd("approx"), dev.getd("exact")
+    assert abs(sd["iterations"] - so["iterations"]) <= int(0.05 * so["iterations"]), (name, sd, so)
+    assert abs(sd["e_l2"] - so["e_l2"]) <= 1e-8, (name, sd["e_l2"], so["e_l2"])
+    assert np.linalg.norm(ud - uo) <= 1e-8 * np.linalg.norm(ue), name
+    assert sd["final_residual"] <= 1e-10 and so["final_residual"] <= 1e-10
+    assert abs(sd["final_residual"] - so["final_residual"]) <= 1e-8
 
 
 # CGS and BiCG (krylov.hpp:159-270): the paper's Table 1b variants; BiCG exercises
@@ -195,13 +214,13 @@ def test_cgs_bicg(dev, orc, name):
     so = orc.run_single(cfg)
     sd = dev.run_single(cfg)
     assert sd["converged"] == so["converged"] and sd["breakdown"] == so["breakdown"], (name, sd, so)
-    assert abs(sd["iterations"] - so["iterations"]) <= max(1, round(0.05 * so["iterations"])), (name, sd, so)
+    assert abs(sd["iterations"] - so["iterations"]) <= int(0.05 * so["iterations"]), (name, sd, so)
     hd, ho = dev.getd("hist", 0), orc.getd("hist", 0)
     k = min(len(hd), len(ho), 5)
     keep = ho[:k] > 1e-6  # residuals near ε·cond(M⁻¹A) are rounding
     np.testing.assert_allclose(hd[:k][keep], ho[:k][keep], rtol=1e-6)
-    tol = max(1e-6, 100 * cfg.rel_tol)
-    assert sd["e_l2"] == pytest.approx(so["e_l2"], rel=tol), (name, sd["e_l2"], so["e_l2"])
+    # these stop at the cases' tol 1e-5: the solutions agree to the level the solves resolve
+    assert np.linalg.norm(dev.getd("approx") - orc.getd("approx")) <= 1e-6 * np.linalg.norm(dev.getd("exact"))
 
 
 # dense column-pivoted QR least squares (krylov.hpp:97-101, runner.hpp:217-222)
@@ -284,3 +303,59 @@ def test_gmres_cycles_and_caps(dev, orc, restart, max_iter):
     assert len(hd) == len(ho) == max_iter + 1 and len(td) == len(to) == max_iter + 1
     assert np.allclose(hd, ho, rtol=1e-6, atol=1e-14) and np.allclose(td, to, rtol=1e-6, atol=1e-14)
     assert sd["e_l2"] == pytest.approx(so["e_l2"], rel=1e-6)
+
+
+# The eigen pseudo-inverse path of the Schwarz build (schwarz.hpp:131-146: local eigen-
+# decomposition, cutoff 1e-12·λmax, A_i⁺ = V diag(1/λ) Vᵀ), which the reference takes for every
+# block and the device for blocks whose condition estimate reaches full_rank_cond. The
+# reference's default RunConfig (config.hpp:23-68: example1 n=2, 4x4 subdomains, delta 2, m 16,
+# PCA off, GMRES + AS, tol 1e-5) has rank-deficient local blocks, so it takes that path.
+def _reference_default():
+    return A.make_config(A.PROBLEM_EXAMPLE1, [4, 4], 16, [40, 40], n=2, seed=1000, test=[350, 350],
+                         solver=A.SOLVER_GMRES, precond=A.PRECOND_AS, rel_tol=1e-5)
+
+
+@pytest.mark.parametrize("kind", [A.PRECOND_AS, A.PRECOND_SAS, A.PRECOND_RAS])
+def test_eigen_fallback_reference_default(dev, orc, kind):
+    cfg = _reference_default()
+    cfg.precond = kind
+    dev.build_instance(cfg).assemble(True).build_preconditioner(kind)
+    orc.build_instance(cfg).assemble(True).build_preconditioner(kind)
+    assert int(dev.geti("n_fallback")[0]) > 0  # the eigen path is exercised
+    assert np.array_equal(dev.geti("local_rank"), orc.geti("local_rank"))
+    # cond estimates of the kept spectrum (λmax/λmin over λ > 1e-12·λmax): both backward stable
+    np.testing.assert_allclose(dev.getd("local_cond"), orc.getd("local_cond"), rtol=1e-3)
+    rng = np.random.default_rng(17)
+    p = int(orc.geti("p")[0])
+    for tr in (False, True):
+        v = rng.standard_normal(p)
+        zo, zd = orc.precond_apply(v, tr), dev.precond_apply(v, tr)
+        # pseudo-inverses of rank-deficient blocks: the kept eigenvectors are accurate to
+        # ε·λmax/gap; the applies agree to ε·cond of the kept spectrum
+        tol = max(1e-9, 1e-14 * float(orc.getd("local_cond").max()))
+        assert np.linalg.norm(zd - zo) <= tol * np.linalg.norm(zo), (kind, tr)
+    so, sd = orc.run_single(cfg), dev.run_single(cfg)
+    assert sd["DoF"] == so["DoF"] and sd["converged"] == so["converged"]
+    assert abs(sd["iterations"] - so["iterations"]) <= int(0.05 * so["iterations"]), (sd, so)
+
+
+@pytest.mark.parametrize("name", ["runner77", "c2_slice", "c4_slice", "example3"])
+def test_all_blocks_eigen_path(dev, orc, name):
+    # full_rank_cond = 0 routes every local block to the eigen pseudo-inverse (the reference's
+    # own method): the applies then agree with the oracle's to rounding of the eigensolvers
+    cfg = CASES[name]
+    dev.set_param("full_rank_cond", 0.0)
+    try:
+        dev.build_instance(cfg).assemble(True).build_preconditioner(A.PRECOND_AS)
+        orc.build_instance(cfg).assemble(True).build_preconditioner(A.PRECOND_AS)
+        assert int(dev.geti("n_fallback")[0]) == int(dev.geti("J")[0])
+        assert np.array_equal(dev.geti("local_rank"), orc.geti("local_rank"))
+        p = int(orc.geti("p")[0])
+        v = np.random.default_rng(23).standard_normal(p)
+        zo, zd = orc.precond_apply(v), dev.precond_apply(v)
+        tol = max(1e-10, 1e-14 * float(orc.getd("local_cond").max()))
+        assert np.linalg.norm(zd - zo) <= tol * np.linalg.norm(zo), name
+        so, sd = orc.run_single(cfg), dev.run_single(cfg)
+        assert sd["iterations"] == so["iterations"], (name, sd["iterations"], so["iterations"])
+    finally:
+        dev.set_param("full_rank_cond", 1e9)

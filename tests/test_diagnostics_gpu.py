@@ -154,7 +154,9 @@ def test_spectra_vs_oracle(dev, orc, kind):
     p = len(o_n)
     assert len(normal) == p
     lmax = o_n.max()
-    assert np.max(np.abs(normal.real - o_n)) <= 1e-11 * lmax
+    # Weyl: |λ_i(A_dev) − λ_i(A_ref)| ≤ ‖A_dev − A_ref‖₂ (A = HᵀH, the two PCAs differ by ~1e-11)
+    dA = np.linalg.norm(dev.getd("nb_dense").reshape(p, p) - orc.getd("nb_dense").reshape(p, p), 2)
+    assert np.max(np.abs(np.sort(normal.real) - o_n)) <= dA + 1e-13 * lmax
     # full complex spectrum of the oracle's own M⁻¹HᵀH (dense, numpy) and the sorted real parts
     AtA = orc.getd("nb_dense").reshape(p, p)
     MA = np.stack([orc.precond_apply(AtA[:, c]) for c in range(p)], axis=1)

@@ -67,8 +67,9 @@ def test_scaling_row(orc, golden):
     assert s["e_l1n"] == pytest.approx(float(ref_as["e_l1n"]), rel=1e-6)
     s = orc.run_single(configs.golden_scaling(A.PRECOND_NONE))
     assert s["DoF"] == 87
-    # unpreconditioned GMRES(30) on cond ~1e10: iteration count is rounding-sensitive (within 5%)
-    assert abs(s["iterations"] - int(float(ref_none["iter"]))) <= 0.05 * int(float(ref_none["iter"]))
+    # unpreconditioned GMRES(30) on cond ~1e10 is rounding-sensitive; with the PCA in Eigen's
+    # QR-preconditioned Jacobi form the oracle reproduces the reference's 86 iterations exactly
+    assert s["iterations"] == int(float(ref_none["iter"])) == 86
     assert s["e_l1n"] == pytest.approx(float(ref_none["e_l1n"]), rel=1e-3)
 
 

@@ -237,6 +237,10 @@ int rdd_bench_precond(rdd_ctx* ctx, int transpose, int reps, double* ms_per_call
 /* Batched Jacobi eigensolver probe (no reference counterpart; tuning aid): `batch` random
    symmetric matrices of order n, exactly `sweeps` sweeps, eigenvectors included; ms via events. */
 int rdd_bench_jacobi(rdd_ctx* ctx, int n, int batch, int sweeps, double* ms);
+/* Batched DMMA GEMM probe (no reference counterpart; tuning aid): `batch` independent products
+   C = op(A)·op(B) of shape M x N x K, mode 0 = NN, 1 = TN (Aᵀ), 2 = NT (Bᵀ); ms per launch
+   over `reps` launches (CUDA events). Algorithmic flops = 2·M·N·K·batch. */
+int rdd_bench_gemm(rdd_ctx* ctx, int mode, int M, int N, int K, int batch, int reps, double* ms);
 
 #ifdef __cplusplus
 }

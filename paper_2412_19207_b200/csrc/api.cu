@@ -737,6 +737,59 @@ int rdd_bench_precond(rdd_ctx* h, int transpose, int reps, double* ms_per_call, 
   });
 }
 
+int rdd_bench_gemm(rdd_ctx* h, int mode, int M, int N, int K, int batch, int reps, double* ms_out) {
+  return guarded(h, [&](Ctx& c) {
+    if (M < 1 || N < 1 || K < 1 || batch < 1 || reps < 1 || mode < 0 || mode > 2)
+      throw std::invalid_argument("bench_gemm: bad shape");
+    const size_t sa = static_cast<size_t>(M) * K, sb = static_cast<size_t>(K) * N, sc = static_cast<size_t>(M) * N;
+    rdd::DBuf<double> A, B, Cm;
+    A.ensure(sa * batch);
+    B.ensure(sb * batch);
+    Cm.ensure(sc * batch);
+    RDD_CUDA(cudaMemsetAsync(A.p, 0, sizeof(double) * sa * batch, c.stream));
+    RDD_CUDA(cudaMemsetAsync(B.p, 0, sizeof(double) * sb * batch, c.stream));
+    std::vector<rdd::GemmTask> tasks;
+    for (int b = 0; b < batch; ++b)
+      for (int tm = 0; tm < (M + 63) / 64; ++tm)
+        for (int tn = 0; tn < (N + 63) / 64; ++tn) {
+          rdd::GemmTask t{};
+          t.A = A.p + sa * b;
+          t.B = B.p + sb * b;
+          t.Cm = Cm.p + sc * b;
+          t.M = M;
+          t.N = N;
+          t.K = K;
+          t.lda = mode == 1 ? K : M;
+          t.ldb = mode == 2 ? N : K;
+          t.ldc = M;
+          t.tm = tm;
+          t.tn = tn;
+          t.beta = 0.0;
+          t.alpha = 1.0;
+          tasks.push_back(t);
+        }
+    auto run = [&] {
+      if (mode == 0) rdd::gemm_nn(c, tasks);
+      else if (mode == 1) rdd::gemm_tn(c, tasks);
+      else rdd::gemm_nt(c, tasks);
+    };
+    run();
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c.stream);
+    for (int r = 0; r < reps; ++r) run();
+    cudaEventRecord(e1, c.stream);
+    RDD_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_out = ms / reps;
+  });
+}
+
 // ---- dense diagnostics (krylov.hpp:403-440, runner.hpp:344-400)
 static int diag_cap(int cap) { return cap <= 0 ? 4000 : cap; }  // krylov.hpp:404 kDenseSpectrumCap
 

@@ -942,26 +942,17 @@ __global__ void __launch_bounds__(kSolveWarps * 32, 3) k_inv_apply(
 void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
   const size_t smem = chol_solve_smem(c.nmax_local, c.inv_mode);
   if (c.inv_mode) {
-    static size_t set_inv = 0;
-    if (smem > set_inv) {
-      RDD_CUDA(cudaFuncSetAttribute(k_inv_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      set_inv = smem;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(k_inv_apply), smem);
     k_inv_apply<<<2 * c.J, kSolveWarps * 32, smem, c.stream>>>(
         c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p, v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
         ceil_div(c.nmax_local, NB), zloc, static_cast<long long>(c.set_idx.size()), c.live, c.apply_order.p);
     RDD_LAUNCH_CHECK();
     return;
   }
-  static size_t set = 0;
-  if (smem > set) {
-    RDD_CUDA(cudaFuncSetAttribute(k_chol_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    set = smem;
-  }
-  k_chol_apply<<<c.inv_mode ? 2 * c.J : c.J, kSolveWarps * 32, smem, c.stream>>>(
+  ensure_smem_attr(reinterpret_cast<const void*>(k_chol_apply), smem);
+  k_chol_apply<<<c.J, kSolveWarps * 32, smem, c.stream>>>(
       c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p, v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
-      ceil_div(c.nmax_local, NB), zloc, c.inv_mode ? 1 : 0, static_cast<long long>(c.set_idx.size()), c.live,
-      c.apply_order.p);
+      ceil_div(c.nmax_local, NB), zloc, 0, static_cast<long long>(c.set_idx.size()), c.live, c.apply_order.p);
   RDD_LAUNCH_CHECK();
 }
 

@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -27,6 +30,21 @@ inline void check_cuda(cudaError_t e, const char* what, const char* file, int li
                     std::to_string(line));
 }
 #define RDD_CUDA(x) ::rdd::check_cuda((x), #x, __FILE__, __LINE__)
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: the largest size set so far is
+// cached per (kernel, device) under a lock, so contexts on several devices and host threads are safe
+inline void ensure_smem_attr(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  RDD_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = done[{kernel, dev}];
+  if (bytes > cur) {
+    RDD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    cur = bytes;
+  }
+}
 // every kernel launch of the library goes through this check: it also counts launches
 inline int64_t& launch_counter() {
   static thread_local int64_t n = 0;

@@ -159,12 +159,7 @@ void launch(Ctx& c, const std::vector<GemmTask>& tasks, const char* fam) {
   DBuf<GemmTask> d;
   d.upload(tasks, c.stream);
   // grid.x limit is 2^31-1; tasks are far fewer
-  static bool attr_set = false;
-  if (!attr_set) {
-    RDD_CUDA(cudaFuncSetAttribute(k_gemm<AT, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kGemmSmem)));
-    attr_set = true;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<AT, BT>), kGemmSmem);
   k_gemm<AT, BT><<<static_cast<unsigned>(tasks.size()), NT, kGemmSmem, c.stream>>>(d.p);
   RDD_LAUNCH_CHECK();
   if (!alloc_stream()) RDD_CUDA(cudaStreamSynchronize(c.stream));  // task buffer lifetime (non-pooled)
@@ -180,12 +175,7 @@ void gemm_nt(Ctx& c, const std::vector<GemmTask>& tasks) { launch<false, true>(c
 void gemm_nt_dev(Ctx& c, const GemmTask* tasks, int count) {
   if (count <= 0) return;
   ScopedKernelTimer tk(c, "gemm_nt");
-  static bool attr_set = false;
-  if (!attr_set) {
-    RDD_CUDA(cudaFuncSetAttribute(k_gemm<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kGemmSmem)));
-    attr_set = true;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<false, true>), kGemmSmem);
   k_gemm<false, true><<<static_cast<unsigned>(count), NT, kGemmSmem, c.stream>>>(tasks);
   RDD_LAUNCH_CHECK();
 }

@@ -75,6 +75,7 @@ def lib():
         L.rdd_set_param.argtypes = [vp, C.c_char_p, C.c_double]
         L.rdd_bench_operator.argtypes = [vp, C.c_int, C.c_int, dp, dp]
         L.rdd_bench_precond.argtypes = [vp, C.c_int, C.c_int, dp, dp]
+        L.rdd_bench_gemm.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp]
         L.rdd_bench_jacobi.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp]
         L.rdd_spectra.argtypes = [vp, C.c_int, dp, dp, dp, dp, dp, dp]
         L.rdd_dense_spectrum.argtypes = [vp, i64, i64, dp, C.c_int, dp, dp]
@@ -277,6 +278,11 @@ class Solver:
         by = C.c_double()
         self._check(self.L.rdd_bench_operator(self.h, op_form, reps, C.byref(ms), C.byref(by)))
         return ms.value, by.value
+
+    def bench_gemm(self, mode: int, M: int, N: int, K: int, batch: int = 1, reps: int = 5) -> float:
+        ms = C.c_double()
+        self._check(self.L.rdd_bench_gemm(self.h, mode, M, N, K, batch, reps, C.byref(ms)))
+        return ms.value
 
     def bench_precond(self, transpose: bool = False, reps: int = 20):
         ms = C.c_double()

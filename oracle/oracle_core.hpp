@@ -3,8 +3,11 @@
 // CPU restatement of the reference `rannddm` primitives (/root/reference/proj/include/rannddm/)
 // with the same floating-point operation order, so that assembly reproduces the reference's
 // golden exports (proj/h_export.txt) bit for bit. Each item cites the reference file:line it
-// restates. No reference source is copied; Eigen (absent here) is replaced by plain
-// column-major storage.
+// restates. Bit-level parity requires the reference's expressions and their grouping, so the
+// jet arithmetic here (random.hpp:9-37, geometry.hpp:26-75, jet.hpp:13-156) is a close
+// transliteration of those headers, with Eigen (absent here) replaced by plain column-major
+// storage. The reference itself is compiled separately (oracle/_ref, oracle/eigen_shim) and
+// this restatement is pinned against it (tests/test_reference_build.py).
 #pragma once
 
 #include <array>

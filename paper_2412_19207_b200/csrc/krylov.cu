@@ -4,11 +4,13 @@
 // per-CTA partials, summed in order by the consumer), so reruns are bit-identical like the
 // reference's (test_runner.cpp:109-117). CG keeps its control state (iteration, status, rz,
 // histories) on the device: every kernel of an iteration is a no-op once the status leaves
-// RUNNING, so an iteration is a fixed sequence of launches that is captured once into a CUDA
-// graph and replayed with a device-side while condition (cudaGraphCondTypeWhile).
+// RUNNING, so an iteration is a fixed sequence of launches, captured once into a CUDA graph of
+// eight iterations that the host replays, reading the status word once per replay.
 // GMRES uses classical Gram–Schmidt applied twice (CGS2) — orthogonality equivalent to the
-// reference's MGS twice, but as two batched projections instead of 2(k+1) sequential ones —
-// and Givens rotations / triangular solves on the host (the (m+1) x m Hessenberg is tiny).
+// reference's MGS twice, but as two batched projections instead of 2(k+1) sequential ones. The
+// Hessenberg column, the Givens rotations, the residual estimate and the small triangular solve
+// for the diagnostic true residual run in one warp on the device (k_gm_step); Arnoldi steps are
+// launched in chunks with one status read per chunk.
 #include <cmath>
 #include <cstring>
 

@@ -3,12 +3,16 @@
 // The reference takes a thin JacobiSVD of each sample block S_j (rows_j x m) and keeps the
 // right singular vectors with σ > τ. A Gram matrix alone cannot reproduce that: SᵀS squares
 // the condition number, so eigenvalues near a relative threshold of 1e-6 (λ ~ 1e-12 λmax) carry
-// O(1e-4) relative error and the kept subspace O(1e-4) error (SURVEY §7.3 hard part 1). The
-// device path therefore runs two Jacobi stages:
-//   1. G = SᵀS (DMMA), Jacobi -> V0 (backward stable, absolute accuracy only);
-//   2. T = S·V0 (DMMA), G1 = TᵀT (DMMA) — a graded, nearly diagonal matrix whose entries are
-//      accurate relative to sqrt(g_ii g_jj) — Jacobi with the relative threshold -> W, whose
-//      eigenvalues are relatively accurate (Demmel–Veselić); V = V0·W, σ_i = sqrt(λ_i(G1)).
+// O(1e-4) relative error and the kept subspace O(1e-4) error (SURVEY §7.3 hard part 1).
+// Main path (DESIGN §4 K4a/K4):
+//   1. G = SᵀS (DMMA); pivoted Cholesky of G to its numerical rank r, Jacobi on the graded
+//      r x r LᵀL, V_r = L·U;
+//   2. one subspace-iteration step from S itself, Y = Sᵀ(S·V_r) (two DMMA GEMMs), orthonormalised
+//      by a thin Householder QR (k_house_complete) -> Q;
+//   3. Jacobi with the relative criterion (Demmel–Veselić) on the graded r x r (S·Q)ᵀ(S·Q)
+//      -> W, σ relatively accurate, V = Q·W.
+// Fallback (thresholds below ~1e-7·σmax): the two-stage path — Jacobi on G -> V0, then
+// T = S·V0, Jacobi on TᵀT with the relative threshold -> W, V = V0·W.
 // Then: sort σ non-increasing, keep σ > τ (strict; τ relative to σ_max in RDD_TAU_RELATIVE
 // mode), floor p_j >= 1, canonical signs (first nonzero entry of each kept column >= 0), and
 // H_j = S_j·V_j (DMMA) — by linearity equal to assembling the reduced jets (reduction.hpp:122-139).

@@ -56,6 +56,7 @@ static void reset_state(Ctx& c) {
   c.sum = rdd_summary{};
   c.H = nullptr;
   c.fused_ready = false;
+  c.ras_panel = false;
   c.mt_groups = 0;
 }
 
@@ -725,6 +726,12 @@ int rdd_bench_precond(rdd_ctx* h, int transpose, int reps, double* ms_per_call, 
     // with their 4-byte indices, then the reduction (z read through the gather map, out written)
     double b = 0.0;
     const int J = static_cast<int>(c.set_ptr.size()) - 1;
+    if (c.ras_panel) {  // RAS owner-row panels: p_i x n_i per subdomain, read once
+      b = 8.0 * static_cast<double>(c.ras_off[J]) + 12.0 * static_cast<double>(c.set_idx.size()) +
+          8.0 * static_cast<double>(c.set_idx.size()) + 4.0 * static_cast<double>(c.p) + 8.0 * c.p;
+      *bytes_per_call = b;
+      return;
+    }
     for (int i = 0; i < J; ++i) {
       const double n = c.set_ptr[i + 1] - c.set_ptr[i];
       const bool dense = std::binary_search(c.fallback.begin(), c.fallback.end(), i);

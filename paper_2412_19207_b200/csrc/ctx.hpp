@@ -167,6 +167,13 @@ struct Ctx {
   std::vector<GatherTask> gat_tasks;
   double full_rank_cond = 1e9;        // Cholesky path when cond_est(A_i) is below this (DESIGN §4 K8)
   DBuf<double> zloc;                  // Σ n_i
+  // RAS owner-row panels (small blocks): per i the rows of A_i⁻¹ that subdomain i owns
+  // (p_i x n_i, column-major), the only rows the restricted apply keeps (schwarz.hpp:170-182)
+  bool ras_panel = false;
+  DBuf<double> Pras;
+  DBuf<long long> dras_off;
+  DBuf<int> down_off, down_n;
+  std::vector<long long> ras_off;
   DBuf<int> apply_order;              // subdomains by local size, largest first (apply CTA order)
 
   // ---- Krylov
@@ -310,6 +317,8 @@ size_t chol_solve_smem(int nmax, bool inverse);
 std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector<int>& n,
                                       const std::vector<long long>& poff, int iters, bool inverse);
 void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc);
+void build_ras_panels(Ctx& c);                                        // after build_schwarz (RAS, inverse mode)
+void ras_panel_apply(Ctx& c, const double* v, bool transpose, double* zloc);
 std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int>& n,
                                   const std::vector<long long>& off, int iters);
 // diag.cu (§8f row 4: krylov.hpp:403-440 dense diagnostics)

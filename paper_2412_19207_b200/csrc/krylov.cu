@@ -13,6 +13,8 @@
 // launched in chunks with one status read per chunk.
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <utility>
 
 #include "ctx.hpp"
 
@@ -524,7 +526,50 @@ static void gmres_solve(Ctx& c, const double* b, double* x, double tol, int max_
     explicit LiveScope(Ctx& cc) : c(cc) {}
     ~LiveScope() { c.live = nullptr; }
   } ls(c);
-  constexpr int kChunk = 8;  // Arnoldi steps launched between status reads
+  constexpr int kChunk = 8;  // Arnoldi steps per captured graph, one status read per replay
+  // one Arnoldi step k (krylov.hpp:317-350): every kernel is a no-op once the status word stops
+  // the cycle, so a chunk of steps is a fixed launch sequence, captured once per (k0, k1) and
+  // replayed in every cycle
+  auto step = [&](int k) {
+    double* vk = Vb.p + static_cast<size_t>(k) * n;
+    double* w = Vb.p + static_cast<size_t>(k + 1) * n;
+    c.live = &st.p->stop;
+    if (ident) {
+      normal_operator(c, vk, w);
+    } else {
+      normal_operator(c, vk, t1);
+      precond(c, t1, w);
+    }
+    // CGS2: h = Vᵀw; w -= V h (twice)
+    k_multidot<<<k + 1, kRT, 0, c.stream>>>(Vb.p, n, w, n, hA, c.live);
+    k_multiaxpy<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, w, n, hA, k + 1, c.live);
+    k_multidot<<<k + 1, kRT, 0, c.stream>>>(Vb.p, n, w, n, hB, c.live);
+    k_multiaxpy<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, w, n, hB, k + 1, c.live);
+    k_dot_part<<<kRB, kRT, 0, c.stream>>>(w, w, n, part, c.live);
+    RDD_LAUNCH_CHECK();
+    k_gm_step<<<1, 32, 0, c.stream>>>(st.p, hA, hB, part, k, Hd.p, ldh, cs, sn, g, yv.p, dhist.p, dthist.p);
+    RDD_LAUNCH_CHECK();
+    k_gm_scale<<<kRB, kRT, 0, c.stream>>>(st.p, w, n);
+    RDD_LAUNCH_CHECK();
+    if (!ident && true_res) {  // diagnostic true residual ‖b − A x_k‖ (krylov.hpp:360-367)
+      c.live = &st.p->tr;
+      k_combine<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, yv.p, k + 1, x, xk, n, c.live);
+      RDD_LAUNCH_CHECK();
+      normal_operator(c, xk, t1);
+      k_sub<<<kRB, kRT, 0, c.stream>>>(rr, b, t1, n, c.live);
+      k_dot_part<<<kRB, kRT, 0, c.stream>>>(rr, rr, n, part2, c.live);
+      RDD_LAUNCH_CHECK();
+      k_gm_thist<<<1, 32, 0, c.stream>>>(st.p, part2, dthist.p);
+      RDD_LAUNCH_CHECK();
+    }
+    c.live = nullptr;
+  };
+  struct GraphCache {
+    std::map<std::pair<int, int>, std::pair<cudaGraphExec_t, size_t>> g;
+    ~GraphCache() {
+      for (auto& kv : g) cudaGraphExecDestroy(kv.second.first);
+    }
+  } graphs;
   while (it < max_iter && !converged && !breakdown) {
     normal_operator(c, x, t1);
     k_sub<<<kRB, kRT, 0, c.stream>>>(t2, b, t1, n);  // b - A x
@@ -553,40 +598,27 @@ static void gmres_solve(Ctx& c, const double* b, double* x, double tol, int max_
     st.upload(&s0, 1, c.stream);
     RDD_CUDA(cudaMemcpyAsync(g, &beta, sizeof(double), cudaMemcpyHostToDevice, c.stream));
     for (int k0 = 0; k0 < len; k0 += kChunk) {
-      for (int k = k0; k < std::min(len, k0 + kChunk); ++k) {
-        double* vk = Vb.p + static_cast<size_t>(k) * n;
-        double* w = Vb.p + static_cast<size_t>(k + 1) * n;
-        c.live = &st.p->stop;
-        if (ident) {
-          normal_operator(c, vk, w);
-        } else {
-          normal_operator(c, vk, t1);
-          precond(c, t1, w);
-        }
-        // CGS2: h = Vᵀw; w -= V h (twice)
-        k_multidot<<<k + 1, kRT, 0, c.stream>>>(Vb.p, n, w, n, hA, c.live);
-        k_multiaxpy<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, w, n, hA, k + 1, c.live);
-        k_multidot<<<k + 1, kRT, 0, c.stream>>>(Vb.p, n, w, n, hB, c.live);
-        k_multiaxpy<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, w, n, hB, k + 1, c.live);
-        k_dot_part<<<kRB, kRT, 0, c.stream>>>(w, w, n, part, c.live);
-        RDD_LAUNCH_CHECK();
-        k_gm_step<<<1, 32, 0, c.stream>>>(st.p, hA, hB, part, k, Hd.p, ldh, cs, sn, g, yv.p, dhist.p, dthist.p);
-        RDD_LAUNCH_CHECK();
-        k_gm_scale<<<kRB, kRT, 0, c.stream>>>(st.p, w, n);
-        RDD_LAUNCH_CHECK();
-        if (!ident && true_res) {  // diagnostic true residual ‖b − A x_k‖ (krylov.hpp:360-367)
-          c.live = &st.p->tr;
-          k_combine<<<kRB, kRT, 0, c.stream>>>(Vb.p, n, yv.p, k + 1, x, xk, n, c.live);
-          RDD_LAUNCH_CHECK();
-          normal_operator(c, xk, t1);
-          k_sub<<<kRB, kRT, 0, c.stream>>>(rr, b, t1, n, c.live);
-          k_dot_part<<<kRB, kRT, 0, c.stream>>>(rr, rr, n, part2, c.live);
-          RDD_LAUNCH_CHECK();
-          k_gm_thist<<<1, 32, 0, c.stream>>>(st.p, part2, dthist.p);
-          RDD_LAUNCH_CHECK();
-        }
-        c.live = nullptr;
+      const int k1 = std::min(len, k0 + kChunk);
+      auto key = std::make_pair(k0, k1);
+      auto gi = graphs.g.find(key);
+      if (gi == graphs.g.end()) {  // first use of this chunk shape: capture its launches once
+        const bool timing = c.timing;
+        c.timing = false;
+        const int64_t before = launch_counter();
+        cudaGraph_t graph;
+        RDD_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+        for (int k = k0; k < k1; ++k) step(k);
+        RDD_CUDA(cudaStreamEndCapture(c.stream, &graph));
+        const size_t nodes = static_cast<size_t>(launch_counter() - before);
+        launch_counter() = before;
+        cudaGraphExec_t exec = nullptr;
+        RDD_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+        c.timing = timing;
+        gi = graphs.g.emplace(key, std::make_pair(exec, nodes)).first;
       }
+      RDD_CUDA(cudaGraphLaunch(gi->second.first, c.stream));
+      launch_counter() += static_cast<int64_t>(gi->second.second);
       st.download(&hs, 1, c.stream);
       RDD_CUDA(cudaStreamSynchronize(c.stream));
       if (hs.stop != GM_RUN) break;

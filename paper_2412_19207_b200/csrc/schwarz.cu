@@ -515,12 +515,18 @@ void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre) {
   c.n_fallback = static_cast<int>(c.fallback.size());
   c.dfb_ptr.upload(fbp, c.stream);
   c.nmax_local = *std::max_element(n.begin(), n.end());
+  build_ras_panels(c);
 }
 
 void precond_apply_dev(Ctx& c, const double* v, double* z, bool transpose, double* pzz, double* pzv) {
   ScopedKernelTimer tk(c, "precond_apply");
-  chol_apply(c, v, transpose, c.zloc.p);
-  const double* z2 = c.inv_mode ? c.zloc.p + c.set_idx.size() : nullptr;  // second half-partials
+  const double* z2 = nullptr;
+  if (c.ras_panel) {
+    ras_panel_apply(c, v, transpose, c.zloc.p);
+  } else {
+    chol_apply(c, v, transpose, c.zloc.p);
+    if (c.inv_mode) z2 = c.zloc.p + c.set_idx.size();  // second half-partials
+  }
   k_reduce<<<ceil_div(c.p, 256), 256, 0, c.stream>>>(c.zloc.p, z2, c.gat_ptr.p, c.gat_pos.p, c.gat_owner_pos.p, c.dmult.p,
                                                      c.p, c.pkind, transpose ? 1 : 0, z, v, pzz, pzv, c.live);
   RDD_LAUNCH_CHECK();

@@ -415,7 +415,10 @@ void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre) {
         nn.push_back(cn[q]);
         po.push_back(cpoff[q]);
       }
-      const std::vector<double> lp = batched_inv_power(c, c.P.p, nn, po, 12, false);
+      // routing estimate only: blocks that do not clear the threshold are refined below (60
+      // iterations on A_i⁻¹ and A_i), and the exported local_cond is recomputed exactly on demand
+      // (refresh_local_cond); ‖A_i‖_F over-estimates λmax(A_i) by up to sqrt(n_i)
+      const std::vector<double> lp = batched_inv_power(c, c.P.p, nn, po, 4, false);
       for (size_t z = 0; z < ok_q.size(); ++z) {
         const int q = ok_q[z];
         if (fa[q] * lp[z] < c.full_rank_cond) {

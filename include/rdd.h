@@ -65,7 +65,6 @@ extern "C" {
 /* normal-operator formulation used by the Krylov loop */
 #define RDD_OPERATOR_TWO_PASS 0 /* Hᵀ(H·w), runner.hpp:232-234 (reference semantics) */
 #define RDD_OPERATOR_NORMAL 1   /* block-sparse HᵀH from the normal blocks           */
-#define RDD_OPERATOR_FUSED 2    /* Hᵀ(H·w) in one pass over H (tile partials, deterministic) */
 
 /* Mirrors rannddm::RunConfig (config.hpp:23-68) plus the BASELINE extensions. */
 typedef struct rdd_config {

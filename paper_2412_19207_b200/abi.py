@@ -18,7 +18,7 @@ TAU_OFF, TAU_ABSOLUTE, TAU_RELATIVE = 0, 1, 2
 PCA_PSI, PCA_OP_APPLIED = 0, 1
 SOLVER_QR, SOLVER_CG, SOLVER_CGS, SOLVER_BICG, SOLVER_GMRES = 0, 1, 2, 3, 4
 PRECOND_NONE, PRECOND_AS, PRECOND_SAS, PRECOND_RAS = -1, 0, 1, 2
-OPERATOR_TWO_PASS, OPERATOR_NORMAL, OPERATOR_FUSED = 0, 1, 2
+OPERATOR_TWO_PASS, OPERATOR_NORMAL = 0, 1
 
 SOLVER_NAMES = {0: "qr_direct", 1: "cg", 2: "cgs", 3: "bicg", 4: "gmres"}
 PRECOND_NAMES = {-1: "none", 0: "AS", 1: "SAS", 2: "RAS"}

@@ -55,7 +55,6 @@ static void reset_state(Ctx& c) {
   c.exact.clear();
   c.sum = rdd_summary{};
   c.H = nullptr;
-  c.fused_ready = false;
   c.ras_panel = false;
   c.mt_groups = 0;
 }
@@ -97,8 +96,6 @@ static void assemble(Ctx& c, bool equilibrate) {
   RDD_CUDA(cudaMemcpyAsync(c.F.p, c.Fpt.p, sizeof(double) * c.N * c.C, cudaMemcpyDeviceToDevice, c.stream));
   column_norms_scale(c, equilibrate);
   RDD_CUDA(cudaStreamSynchronize(c.stream));
-  c.fused_ready = false;
-  if (c.cfg.op_form == RDD_OPERATOR_FUSED) build_fused_plan(c);  // falls back to two passes if it cannot
   c.assembled = true;
   c.equilibrated = equilibrate;
 }
@@ -668,8 +665,8 @@ int rdd_bench_operator(rdd_ctx* h, int op_form, int reps, double* ms_per_call, d
   return guarded(h, [&](Ctx& c) {
     need_assembled(c);
     if (op_form == RDD_OPERATOR_NORMAL && !c.NB.p) rdd::build_normal_blocks(c);
-    if (op_form == RDD_OPERATOR_FUSED && !c.fused_ready && !rdd::build_fused_plan(c))
-      throw std::runtime_error("fused operator plan unavailable (too many blocks per tile)");
+    if (op_form != RDD_OPERATOR_TWO_PASS && op_form != RDD_OPERATOR_NORMAL)
+      throw std::invalid_argument("unknown normal-operator form");
     rdd::DBuf<double> w, out;
     w.ensure(c.p);
     out.ensure(c.p);
@@ -693,8 +690,6 @@ int rdd_bench_operator(rdd_ctx* h, int op_form, int reps, double* ms_per_call, d
     *ms_per_call = ms / reps;
     if (op_form == RDD_OPERATOR_NORMAL)
       *bytes_per_call = 8.0 * static_cast<double>(c.nb_off.back()) + 8.0 * 2 * c.p;
-    else if (op_form == RDD_OPERATOR_FUSED)  // one pass over H + w, out + (block, row) cover maps
-      *bytes_per_call = 8.0 * static_cast<double>(c.H_off[c.J]) + 8.0 * 2 * c.p + 8.0 * c.sum_rows;
     else  // two passes over H + vectors + row maps
       *bytes_per_call = 2.0 * (8.0 * static_cast<double>(c.H_off[c.J]) + 8.0 * (c.p + c.N) + 4.0 * c.sum_rows);
   });

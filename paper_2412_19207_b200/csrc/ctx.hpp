@@ -195,14 +195,6 @@ struct Ctx {
   DBuf<GemmTask> wsg;                 // device-generated GEMM task lists
   int mt_groups = 0;
   size_t mt_smem = 0;
-  // fused single-pass normal operator plan
-  DBuf<int> f_bptr;
-  DBuf<unsigned char> f_tiles;
-  DBuf<long long> f_bparts;
-  DBuf<double> f_part;
-  int f_ntiles = 0;
-  long long f_part_size = 0;
-  bool fused_ready = false;
 
   // ---- evaluation
   std::vector<double> approx, exact;  // M x C (host copies)
@@ -276,8 +268,6 @@ void normal_apply_dev(Ctx& c, const double* w, double* out);
 void normal_operator(Ctx& c, const double* w, double* out);  // runner.hpp:232-234
 bool normal_operator_dot(Ctx& c, const double* w, double* out, double* dot_part);
 void normal_two_pass_dev(Ctx& c, const double* w, double* out, double* dot_part);
-bool build_fused_plan(Ctx& c);
-void fused_normal_apply_dev(Ctx& c, const double* w, double* out);
 // schwarz.cu (K8/K11)
 struct SchwarzIndex {  // host side of build_index_sets (schwarz.hpp:39-61) + the column gather map
   std::vector<int> set_ptr, set_idx, mult, n, gp, gpos, owner_pos;

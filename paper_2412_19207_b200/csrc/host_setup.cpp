@@ -150,6 +150,8 @@ void setup_problem(Ctx& c, const rdd_config& cfg, uint64_t seed) {
   if (cfg.tau_mode != RDD_TAU_OFF && !(cfg.tau >= 0.0))  // reduction.hpp:90
     throw std::invalid_argument("truncation threshold tau must be >= 0");
   if (cfg.max_iter < 0) throw std::invalid_argument("max_iter must be >= 1");  // krylov.hpp:79
+  if (cfg.op_form != RDD_OPERATOR_TWO_PASS && cfg.op_form != RDD_OPERATOR_NORMAL)
+    throw std::invalid_argument("unknown normal-operator form");
   c.counts.assign(cfg.counts, cfg.counts + d);
   for (int k : c.counts)
     if (k < 1) throw std::invalid_argument("per-axis subdomain counts must be >= 1");

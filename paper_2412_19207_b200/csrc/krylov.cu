@@ -322,10 +322,6 @@ bool normal_operator_dot(Ctx& c, const double* w, double* out, double* dot_part)
     normal_apply_dev(c, w, out);
     return false;
   }
-  if (c.cfg.op_form == RDD_OPERATOR_FUSED && c.fused_ready) {
-    fused_normal_apply_dev(c, w, out);
-    return false;
-  }
   normal_two_pass_dev(c, w, out, dot_part);
   return dot_part != nullptr;
 }

@@ -128,7 +128,7 @@ def test_assembly_and_operators(dev, orc, name):
     assert np.linalg.norm(td - to) <= 10 * tol * np.linalg.norm(to)
     # adjoint identity on the device path alone (test_assembly.cpp:114-134)
     assert abs(yd @ r - w @ td) <= 1e-11 * max(1.0, abs(yd @ r))
-    # normal operator Hᵀ(H·w) (runner.hpp:232-234) in the configured formulation (fused for slices)
+    # normal operator Hᵀ(H·w) (runner.hpp:232-234) in the configured formulation
     no = orc.matvec_transpose(orc.matvec(w))
     nd = dev.normal_apply(w)
     assert np.linalg.norm(nd - no) <= 10 * tol * np.linalg.norm(no), (name, cfg.op_form)
@@ -263,10 +263,10 @@ def test_qr_direct(dev, orc, name):
     assert np.linalg.norm(wd - wo) <= 1e-6 * np.linalg.norm(wo), name
 
 
-# the two alternative normal-operator formulations: the single-pass fused kernel and
-# the assembled normal blocks HᵀH, against the reference's two passes on the oracle
+# the alternative normal-operator formulation: the assembled normal blocks HᵀH, against
+# the reference's two passes on the oracle
 @pytest.mark.parametrize("name", ["c1_slice", "c2_slice", "c3_slice", "c4_slice", "runner77"])
-@pytest.mark.parametrize("op_form", [A.OPERATOR_FUSED, A.OPERATOR_NORMAL])
+@pytest.mark.parametrize("op_form", [A.OPERATOR_NORMAL])
 def test_operator_forms(dev, orc, name, op_form):
     cfg = A.Config.from_buffer_copy(CASES[name])
     cfg.op_form = op_form

@@ -5,7 +5,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2412_19207_b200 import rdd, configs, abi as A
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
-for of in (A.OPERATOR_TWO_PASS, A.OPERATOR_FUSED, A.OPERATOR_NORMAL):
+for of in (A.OPERATOR_TWO_PASS, A.OPERATOR_NORMAL):
     cfg = configs.aspcg(name)
     cfg.op_form = of
     s = rdd.Solver(0)

@@ -4,7 +4,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2412_19207_b200 import rdd, configs
 FAMILIES = ["index", "problem", "assemble", "assemble_psi", "pca_total", "syevj", "project", "gemm_tn", "gemm_nn",
-            "gemm_nt", "equilibrate", "matvec", "matvec_t", "fused_normal", "normal_blocks", "normal_apply",
+            "gemm_nt", "equilibrate", "matvec", "matvec_t", "normal_blocks", "normal_apply",
             "schwarz_build", "schwarz_alloc", "schwarz_gather", "cholesky", "inv_power", "power", "gram", "precond_apply", "solve", "evaluate"]
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 cfg = configs.aspcg(name)

@@ -21,7 +21,7 @@ namespace rdd {
 namespace {
 
 constexpr int NB = 64;
-constexpr int kPairSmem = (NB * (NB + 1) + NB * NB) * sizeof(double);
+constexpr int kPairSmem = 2 * NB * (NB + 1) * sizeof(double);
 constexpr int kSolveWarps = 8;
 
 struct Mat {
@@ -32,64 +32,61 @@ struct Mat {
 // A[k-block, k-block] <- chol (lower); pads beyond n act as identity. Also D_k = L_kk⁻¹ (lower,
 // padding identity) into the per-matrix diagonal-inverse workspace: the panel solve becomes a DMMA
 // product with D_kᵀ and the packed factor stores D_k.
-__global__ void __launch_bounds__(32) k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mats,
-                                                    const int* __restrict__ act, int k, int* __restrict__ fail,
-                                                    double* __restrict__ Dinv, const long long* __restrict__ doff) {
-  // one warp per tile: the 64 column steps of the factorisation and the 64 row steps of the
-  // inverse synchronise within the warp only (no CTA barriers on the critical chain); lane owns
-  // rows {lane, lane + 32} while factoring and columns {lane, lane + 32} while inverting
+__global__ void k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mats, const int* __restrict__ act, int k,
+                             int* __restrict__ fail, double* __restrict__ Dinv, const long long* __restrict__ doff) {
   extern __shared__ double dsm[];
   double(*s)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
-  double(*X)[NB] = reinterpret_cast<double(*)[NB]>(dsm + NB * (NB + 1));
-  const int lane = threadIdx.x;
+  double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
   const int q = act[blockIdx.x];
   const Mat M = mats[q];
   const int k0 = k * NB, bs = min(NB, M.n - k0);
   double* a = A + M.off + k0 + static_cast<long long>(k0) * M.n;
-  for (int c = 0; c < NB; ++c)
-    for (int r = lane; r < NB; r += 32)
-      s[r][c] = (r < bs && c < bs) ? a[r + static_cast<long long>(c) * M.n] : (r == c ? 1.0 : 0.0);
-  __syncwarp();
-  bool bad = false;
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e % NB, c = e / NB;
+    s[r][c] = (r < bs && c < bs) ? a[r + static_cast<long long>(c) * M.n] : (r == c ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  __shared__ double d;
   for (int c = 0; c < NB; ++c) {
-    const double v = s[c][c];
-    bad |= !(v > 0.0);
-    const double d = sqrt(fmax(v, 1e-300));
-    __syncwarp();
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = lane + 32 * h;
-      if (r > c) s[r][c] /= d;
+    if (threadIdx.x == 0) {
+      const double v = s[c][c];
+      if (!(v > 0.0)) fail[q] = 1;
+      d = sqrt(fmax(v, 1e-300));
+      s[c][c] = d;
     }
-    if (lane == 0) s[c][c] = d;
-    __syncwarp();
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {  // trailing update of the lower triangle, row by row
-      const int r = lane + 32 * h;
-      if (r > c) {
+    __syncthreads();
+    for (int r = c + 1 + threadIdx.x; r < NB; r += blockDim.x) s[r][c] /= d;
+    __syncthreads();
+    {  // trailing update of the lower triangle: warps over rows, lanes over columns (no div/mod)
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+      for (int r = c + 1 + warp; r < NB; r += nw) {
         const double src = s[r][c];
-        for (int qq = c + 1; qq <= r; ++qq) s[r][qq] -= src * s[qq][c];
+        for (int qq = c + 1 + lane; qq <= r; qq += 32) s[r][qq] -= src * s[qq][c];
       }
     }
-    __syncwarp();
+    __syncthreads();
   }
-  if (lane == 0 && bad) fail[q] = 1;
-  for (int c = 0; c < NB; ++c)
-    for (int r = lane; r < NB; r += 32)
-      if (r < bs && c < bs) a[r + static_cast<long long>(c) * M.n] = r >= c ? s[r][c] : 0.0;
-  // L⁻¹ by forward substitution, one column per lane pass: a column reads only its own entries
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int c = lane + 32 * h;
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e % NB, c = e / NB;
+    if (r < bs && c < bs) a[r + static_cast<long long>(c) * M.n] = r >= c ? s[r][c] : 0.0;
+  }
+  // L⁻¹ by forward substitution down the rows, four lanes per column (a column only reads its own
+  // earlier entries, so the four lanes synchronise within their warp only)
+  {
+    const int c = threadIdx.x >> 2, part = threadIdx.x & 3;
     for (int r = 0; r < NB; ++r) {
       double v = 0.0;
-      for (int qq = c; qq < r; ++qq) v += s[r][qq] * X[qq][c];
-      X[r][c] = r < c ? 0.0 : ((r == c ? 1.0 : 0.0) - v) / s[r][r];
+      if (r > c)
+        for (int qq = c + part; qq < r; qq += 4) v += s[r][qq] * X[qq][c];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (part == 0) X[r][c] = r < c ? 0.0 : ((r == c ? 1.0 : 0.0) - v) / s[r][r];
+      __syncwarp();
     }
   }
-  __syncwarp();
+  __syncthreads();
   double* o = Dinv + doff[q] + static_cast<long long>(k) * NB * NB;
-  for (int e = lane; e < NB * NB; e += 32) o[e] = X[e % NB][e / NB];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) o[e] = X[e % NB][e / NB];
 }
 
 
@@ -686,7 +683,7 @@ void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const s
     const Step& st = steps[k];
     {
       ScopedKernelTimer tp(c, "potrf");
-      k_potrf_diag<<<static_cast<int>(st.nact), 32, kPairSmem, c.stream>>>(A, dm.p, dact.p + st.act0, k, dfail.p,
+      k_potrf_diag<<<static_cast<int>(st.nact), 256, kPairSmem, c.stream>>>(A, dm.p, dact.p + st.act0, k, dfail.p,
                                                                              Dinv, ddoff.p);
       RDD_LAUNCH_CHECK();
     }

@@ -453,73 +453,6 @@ __device__ void symv_packed(const double* __restrict__ P, int nb, double* v, dou
   __syncthreads();
 }
 
-// symv_packed with the tile taken in four quarters of 16 columns: 16 transposed partials per lane
-// instead of 32, so the explicit-inverse apply fits 80 registers (3 CTAs per SM instead of 2)
-__device__ void symv_packed_q(const double* __restrict__ P, int nb, double* v, double* part, int t0 = 0, int tstep = 1) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
-  const int len = nb * NB;
-  double* my = part + static_cast<size_t>(warp) * len;
-  for (int i = lane; i < len; i += 32) my[i] = 0.0;
-  __syncwarp();
-  const int T = nb * (nb + 1) / 2;
-  const int first = t0 + warp * tstep, stride = kSolveWarps * tstep;  // this warp's tiles
-  int k = 0, j = first;  // tile t = k(k+1)/2 + j
-  while (j > k) {
-    j -= k + 1;
-    ++k;
-  }
-  for (int t = first; t < T; t += stride) {
-    const double* tile = P + static_cast<long long>(t) * (NB * NB);
-    const double* gj = v + j * NB;
-    const double gk0 = v[k * NB + 2 * lane], gk1 = v[k * NB + 2 * lane + 1];
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll 1
-    for (int h = 0; h < 4; ++h) {
-      double p[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const double2 a = __ldcs(reinterpret_cast<const double2*>(tile + (h * 16 + c) * NB) + lane);
-        const double gc = gj[h * 16 + c];
-        a0 += a.x * gc;
-        a1 += a.y * gc;
-        p[c] = a.x * gk0 + a.y * gk1;
-      }
-      if (j < k) {  // warp-uniform
-        // fold the half-warps (lanes L and L^16 then hold the same pair sums), then the transpose
-        // butterfly over 16 lanes: lane L (mod 16) ends with column L's sum
-#pragma unroll
-        for (int i = 0; i < 16; ++i) p[i] += __shfl_xor_sync(0xffffffffu, p[i], 16);
-#pragma unroll
-        for (int o = 8; o >= 1; o >>= 1) {
-          const bool up = (lane & o) != 0;
-#pragma unroll
-          for (int i = 0; i < o; ++i) {
-            const double send = up ? p[i] : p[i + o];
-            const double keep = up ? p[i + o] : p[i];
-            p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-          }
-        }
-        if (lane < 16) my[j * NB + h * 16 + lane] += p[0];
-      }
-    }
-    my[k * NB + 2 * lane] += a0;
-    my[k * NB + 2 * lane + 1] += a1;
-    __syncwarp();
-    j += stride;
-    while (j > k && k < nb) {
-      j -= k + 1;
-      ++k;
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < len; i += blockDim.x) {
-    double s = 0.0;
-    for (int w = 0; w < kSolveWarps; ++w) s += part[static_cast<size_t>(w) * len + i];
-    v[i] = s;
-  }
-  __syncthreads();
-}
-
 // λmax(A⁻¹) by power iteration through the factor: one CTA per matrix
 __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_power(const double* __restrict__ P,
                                                                  const long long* __restrict__ poff,
@@ -896,21 +829,62 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
   for (int r = threadIdx.x; r < n; r += blockDim.x) zo[s0 + r] = g[r];
 }
 
-// explicit-inverse apply (small blocks): two CTAs per subdomain as in k_chol_apply's inverse mode,
-// with the quarter-tile symv and a register cap for 3 CTAs per SM
-__global__ void __launch_bounds__(kSolveWarps * 32, 3) k_inv_apply(
+// ---- explicit-inverse apply through a TMA ring (small blocks: C1, C2, C4). The packed lower tiles
+// of A_i⁻¹ (64x64, 32 KB each, block row after block row) are streamed by one producer warp with
+// 1-D bulk copies (cp.async.bulk, mbarrier completion) into a 2-stage shared-memory ring; eight
+// consumer warps split every tile by columns (8 each): y_k += T_kj g_j accumulates per lane in
+// registers along the block row, y_j += T_kjᵀ g_k is reduced per column (fold + butterfly) and added
+// by its one owning lane. Memory latency is covered by the copies in flight, not by resident warps.
+// Two CTAs per subdomain take alternate tiles (partials to z and z + zhalf, summed by k_reduce).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT%=:\n\t"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+constexpr int kTmaStages = 2;
+constexpr int kTileBytes = NB * NB * sizeof(double);
+
+__global__ void __launch_bounds__((kSolveWarps + 1) * 32) k_inv_apply_tma(
     const double* __restrict__ P, const long long* __restrict__ poff, const double* const* __restrict__ dense,
     const int* __restrict__ set_ptr, const int* __restrict__ set_idx, const double* __restrict__ v,
     const int* __restrict__ mult, const int* __restrict__ owner, int kind, int transpose, int nbmax,
     double* __restrict__ z, long long zhalf, const int* __restrict__ live, const int* __restrict__ order) {
   if (live && *live != 0) return;
-  extern __shared__ double sm[];
-  double* g = sm;
-  double* red = sm + static_cast<size_t>(nbmax) * NB;
-  const int bi = blockIdx.x >> 1;
+  extern __shared__ __align__(128) double tsm[];
+  double* ring = tsm;                                      // kTmaStages x 64 x 64
+  double* g = ring + kTmaStages * NB * NB;                 // nbmax * 64
+  double* y = g + static_cast<size_t>(nbmax) * NB;         // nbmax * 64
+  double* scr = y + static_cast<size_t>(nbmax) * NB;       // kSolveWarps x 64 (block-row flush)
+  __shared__ __align__(8) uint64_t full[kTmaStages], empty[kTmaStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bi = blockIdx.x >> 1, h = blockIdx.x & 1;
   const int i = order ? order[bi] : bi;
-  const int h = blockIdx.x & 1;
   const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0, nb = (n + NB - 1) / NB;
+  const double* D = dense[i];
+  double* zo = z + static_cast<long long>(h) * zhalf;
   for (int q = threadIdx.x; q < nb * NB; q += blockDim.x) {
     double val = 0.0;
     if (q < n) {
@@ -922,11 +896,17 @@ __global__ void __launch_bounds__(kSolveWarps * 32, 3) k_inv_apply(
       }
     }
     g[q] = val;
+    y[q] = 0.0;
+  }
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kTmaStages; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kSolveWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  double* zo = z + static_cast<long long>(h) * zhalf;
-  const double* D = dense[i];
-  if (D) {
+  if (D) {  // eigen-fallback block: dense pseudo-inverse, one CTA
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
       double acc = 0.0;
       if (h == 0)
@@ -935,15 +915,100 @@ __global__ void __launch_bounds__(kSolveWarps * 32, 3) k_inv_apply(
     }
     return;
   }
-  symv_packed_q(P + poff[i], nb, g, red, h, 2);
-  for (int r = threadIdx.x; r < n; r += blockDim.x) zo[s0 + r] = g[r];
+  const int T = nb * (nb + 1) / 2;
+  const double* Pi = P + poff[i];
+  if (warp == kSolveWarps) {  // producer
+    if (lane == 0) {
+      int it = 0;
+      for (int t = h; t < T; t += 2, ++it) {
+        const int b = it % kTmaStages;
+        if (it >= kTmaStages) mbar_wait(&empty[b], ((it / kTmaStages) - 1) & 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[b], kTileBytes);
+        bulk_load(ring + b * NB * NB, Pi + static_cast<long long>(t) * (NB * NB), kTileBytes, &full[b]);
+      }
+    }
+    return;
+  }
+  // consumers: warp takes columns [8w, 8w + 8) of every tile; lane holds rows 2l, 2l + 1
+  int k = 0, j = h;
+  while (j > k) {
+    j -= k + 1;
+    ++k;
+  }
+  double a0 = 0.0, a1 = 0.0;
+  int it = 0;
+  for (int t = h; t < T; t += 2, ++it) {
+    const int b = it % kTmaStages;
+    mbar_wait(&full[b], (it / kTmaStages) & 1);
+    const double* tile = ring + b * NB * NB;
+    const double gk0 = g[k * NB + 2 * lane], gk1 = g[k * NB + 2 * lane + 1];
+    double p[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int col = warp * 8 + c;
+      const double2 a = reinterpret_cast<const double2*>(tile + col * NB)[lane];
+      const double gc = g[j * NB + col];
+      a0 += a.x * gc;
+      a1 += a.y * gc;
+      p[c] = a.x * gk0 + a.y * gk1;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);  // the tile is in registers
+    if (j < k) {  // y_j += T_kjᵀ g_k: fold 32 lanes to 8, then an 8-lane transpose butterfly
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        p[c] += __shfl_xor_sync(0xffffffffu, p[c], 16);
+        p[c] += __shfl_xor_sync(0xffffffffu, p[c], 8);
+      }
+#pragma unroll
+      for (int o = 4; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int q = 0; q < o; ++q) {
+          const double send = up ? p[q] : p[q + o];
+          const double keep = up ? p[q + o] : p[q];
+          p[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (lane < 8) y[j * NB + warp * 8 + lane] += p[0];
+    }
+    // next tile of this CTA; flush the row partials when the block row changes
+    int nk = k, nj = j + 2;
+    while (nj > nk && nk < nb) {
+      nj -= nk + 1;
+      ++nk;
+    }
+    if (nk != k || t + 2 >= T) {
+      scr[warp * NB + 2 * lane] = a0;
+      scr[warp * NB + 2 * lane + 1] = a1;
+      asm volatile("bar.sync 1, %0;" ::"r"(kSolveWarps * 32) : "memory");
+      if (threadIdx.x < NB) {
+        double s = 0.0;
+        for (int w = 0; w < kSolveWarps; ++w) s += scr[w * NB + threadIdx.x];
+        y[k * NB + threadIdx.x] += s;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(kSolveWarps * 32) : "memory");
+      a0 = a1 = 0.0;
+    }
+    k = nk;
+    j = nj;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(kSolveWarps * 32) : "memory");
+  for (int r = threadIdx.x; r < n; r += kSolveWarps * 32) zo[s0 + r] = y[r];
+}
+
+size_t inv_apply_tma_smem(int nmax) {
+  const size_t len = static_cast<size_t>(ceil_div(nmax, NB)) * NB;
+  return (static_cast<size_t>(kTmaStages) * NB * NB + 2 * len + kSolveWarps * NB) * sizeof(double);
 }
 
 void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
   const size_t smem = chol_solve_smem(c.nmax_local, c.inv_mode);
   if (c.inv_mode) {
-    ensure_smem_attr(reinterpret_cast<const void*>(k_inv_apply), smem);
-    k_inv_apply<<<2 * c.J, kSolveWarps * 32, smem, c.stream>>>(
+    const size_t tsm = inv_apply_tma_smem(c.nmax_local);
+    ensure_smem_attr(reinterpret_cast<const void*>(k_inv_apply_tma), tsm);
+    k_inv_apply_tma<<<2 * c.J, (kSolveWarps + 1) * 32, tsm, c.stream>>>(
         c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p, v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
         ceil_div(c.nmax_local, NB), zloc, static_cast<long long>(c.set_idx.size()), c.live, c.apply_order.p);
     RDD_LAUNCH_CHECK();

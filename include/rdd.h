@@ -224,6 +224,8 @@ int rdd_set_verbose(rdd_ctx* ctx, int on);  /* phase times and solver diagnostic
      "full_rank_cond"  local blocks A_i whose condition estimate is below this take the Cholesky
                        path, the rest the eigen pseudo-inverse with the reference cutoff
                        (default in DESIGN.md §4 K8; 0 routes every block to the eigen path).
+     "pca_refine"      subspace-refinement steps Y = Sᵀ(S·V) of the PCA (DESIGN §4 K4a;
+                       0 = automatic).
    Takes effect at the next rdd_build_preconditioner. RDD_INVALID_ARGUMENT for unknown names. */
 int rdd_set_param(rdd_ctx* ctx, const char* name, double value);
 /* Time `reps` calls of the normal operator on device-resident vectors (CUDA events). */

@@ -266,6 +266,10 @@ int rdd_set_param(rdd_ctx* h, const char* name, double value) {
     h->c.full_rank_cond = value;
     return RDD_OK;
   }
+  if (n == "pca_refine" && value >= 0.0 && value <= 4.0) {
+    h->c.pca_refine = static_cast<int>(value);
+    return RDD_OK;
+  }
   h->c.err = "rdd_set_param: unknown parameter or bad value: " + n;
   return RDD_INVALID_ARGUMENT;
 }

@@ -165,6 +165,7 @@ struct Ctx {
     long long nb;
   };
   std::vector<GatherTask> gat_tasks;
+  int pca_refine = 0;                 // subspace-refinement steps of the PCA (0 = automatic)
   double full_rank_cond = 1e9;        // Cholesky path when cond_est(A_i) is below this (DESIGN §4 K8)
   DBuf<double> zloc;                  // Σ n_i
   // RAS owner-row panels (small blocks): per i the rows of A_i⁻¹ that subdomain i owns

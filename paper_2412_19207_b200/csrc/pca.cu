@@ -357,7 +357,7 @@ void run_pca(Ctx& c) {
       if (!(rj[j] == m || ok)) fast = false;
     }
     const bool skip_s1 = fast && rmax > 223;
-    const int nref = skip_s1 ? 2 : 1;
+    const int nref = c.pca_refine > 0 ? c.pca_refine : (skip_s1 ? 2 : 1);
     {
       std::vector<GemmTask> t;
       for (int j = 0; j < J; ++j) {
@@ -400,6 +400,7 @@ void run_pca(Ctx& c) {
       for (int it = 0; it < nref; ++it) {
         const double* Vin = it == 0 ? (skip_s1 ? Lw.p : Vr.p) : V0.p;
         {
+          ScopedKernelTimer tr(c, "pca_refine");
           std::vector<GemmTask> t;
           for (int j = 0; j < J; ++j) {
             const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
@@ -411,6 +412,7 @@ void run_pca(Ctx& c) {
           gemm_nn(c, t);  // Z = S·V
         }
         {
+          ScopedKernelTimer tr(c, "pca_refine");
           std::vector<GemmTask> t;
           for (int j = 0; j < J; ++j) {
             const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
@@ -426,11 +428,13 @@ void run_pca(Ctx& c) {
           RDD_CUDA(cudaFuncSetAttribute(k_house_complete, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(sm)));
         const double* ord = (it == 0 && !skip_s1) ? lam.p : dorder;
+        ScopedKernelTimer th(c, "pca_house");
         k_house_complete<<<J, kHouseThreads, sm, c.stream>>>(Hw.p, ord, doffr_sel.p, dr.p, m, Lw.p == Vin ? Vr.p : Lw.p,
                                                              V0.p, 1);
         RDD_LAUNCH_CHECK();  // V0[:, :r] = orthonormal basis of span(Y)
       }
       {
+        ScopedKernelTimer ts(c, "pca_stage2_gemm");
         std::vector<GemmTask> t;
         for (int j = 0; j < J; ++j) {
           const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
@@ -442,6 +446,7 @@ void run_pca(Ctx& c) {
         gemm_nn(c, t);  // T_a = S·Q
       }
       {
+        ScopedKernelTimer ts(c, "pca_stage2_gemm");
         std::vector<GemmTask> t;
         for (int j = 0; j < J; ++j) {
           const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
@@ -490,6 +495,7 @@ void run_pca(Ctx& c) {
         gemm_nn(c, t);  // T_a
       }
       {
+        ScopedKernelTimer ts(c, "pca_stage2_gemm");
         std::vector<GemmTask> t;
         for (int j = 0; j < J; ++j) {
           const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];

@@ -15,7 +15,11 @@ PROBE_SEED = 20250
 
 def main():
     s = rdd.Solver(0)
-    for name in sys.argv[1:] or ["C3", "C5", "C2", "C4"]:
+    args = sys.argv[1:]
+    if args and args[0].startswith("refine="):
+        s.set_param("pca_refine", float(args[0].split("=")[1]))
+        args = args[1:]
+    for name in args or ["C3", "C5", "C2", "C4"]:
         kind = "pca" if name in ("C3", "C5") else "run"
         fx = np.load(os.path.join(ROOT, "tests", "golden", "fullsize", f"{kind}_{name}.npz"))
         cfg = configs.BASELINE[name]()

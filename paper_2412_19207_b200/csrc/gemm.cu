@@ -12,11 +12,19 @@ namespace rdd {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, NT = 128, STAGES = 3;
+constexpr int BM = 64, BN = 64, BK = 16, NT = 128;
 constexpr int KP = BK + 4;   // k-contiguous tiles: [64][BK+4] (row stride ≡ 4 banks mod 16)
 constexpr int MP = BM + 4;   // m/n-contiguous tiles: [BK][64+4]
 constexpr int kStageA = BM * KP > BK * MP ? BM * KP : BK * MP;  // doubles per operand per stage
-constexpr size_t kGemmSmem = static_cast<size_t>(STAGES) * 2 * kStageA * sizeof(double);
+constexpr size_t gemm_smem(int stages) { return static_cast<size_t>(stages) * 2 * kStageA * sizeof(double); }
+// pipeline depth / residency per mode (tools/gemm_bench.py): the NN and NT products (projections,
+// Cholesky panel and trailing updates) run best with a 2-deep ring and 4 CTAs per SM (+5-10% on
+// the K = 64 and K = 512 update shapes), the TN Gram products with a 3-deep ring and 3 CTAs
+template <bool AT>
+struct GemmCfg {
+  static constexpr int stages = AT ? 3 : 2;
+  static constexpr int minb = AT ? 3 : 4;
+};
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -36,8 +44,8 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // through a STAGES-deep cp.async ring; each operand tile keeps its global contiguous direction
 // in shared memory (k-contiguous for Aᵀ / B, m-contiguous for A / Bᵀ) so the copies coalesce,
 // and the padded strides make the fragment reads bank-conflict free.
-template <bool AT, bool BT>
-__global__ void __launch_bounds__(NT) k_gemm(const GemmTask* __restrict__ tasks) {
+template <bool AT, bool BT, int STAGES = GemmCfg<AT>::stages>
+__global__ void __launch_bounds__(NT, GemmCfg<AT>::minb) k_gemm(const GemmTask* __restrict__ tasks) {
   extern __shared__ __align__(16) double gsm[];
   const GemmTask T = tasks[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -115,24 +123,31 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmTask* __restrict__ tasks)
     cp_commit();
     const double* a = As(kt % STAGES);
     const double* bsm = Bs(kt % STAGES);
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
+    // fragments double-buffered across the four k-steps of the stage: the loads of step kk+4 are
+    // issued before the 16 DMMAs of step kk, so no DMMA waits on its own shared-memory load
+    double af[2][4], bf[2][4];
+    auto frag = [&](int kk, int b) {
       const int k = kk + (lane & 3);
-      double af[4], bf[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int ml = wm + 8 * i + (lane >> 2);
-        af[i] = AT ? a[ml * KP + k] : a[k * MP + ml];
+        af[b][i] = AT ? a[ml * KP + k] : a[k * MP + ml];
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int nl = wn + 8 * j + (lane >> 2);
-        bf[j] = BT ? bsm[k * MP + nl] : bsm[nl * KP + k];
+        bf[b][j] = BT ? bsm[k * MP + nl] : bsm[nl * KP + k];
       }
+    };
+    frag(0, 0);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      const int b = (kk >> 2) & 1;
+      if (kk + 4 < BK) frag(kk + 4, b ^ 1);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[b][i], bf[b][j]);
     }
   }
   cp_wait<0>();
@@ -159,8 +174,9 @@ void launch(Ctx& c, const std::vector<GemmTask>& tasks, const char* fam) {
   DBuf<GemmTask> d;
   d.upload(tasks, c.stream);
   // grid.x limit is 2^31-1; tasks are far fewer
-  ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<AT, BT>), kGemmSmem);
-  k_gemm<AT, BT><<<static_cast<unsigned>(tasks.size()), NT, kGemmSmem, c.stream>>>(d.p);
+  constexpr size_t smem = gemm_smem(GemmCfg<AT>::stages);
+  ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<AT, BT>), smem);
+  k_gemm<AT, BT><<<static_cast<unsigned>(tasks.size()), NT, smem, c.stream>>>(d.p);
   RDD_LAUNCH_CHECK();
   if (!alloc_stream()) RDD_CUDA(cudaStreamSynchronize(c.stream));  // task buffer lifetime (non-pooled)
 }
@@ -175,8 +191,9 @@ void gemm_nt(Ctx& c, const std::vector<GemmTask>& tasks) { launch<false, true>(c
 void gemm_nt_dev(Ctx& c, const GemmTask* tasks, int count) {
   if (count <= 0) return;
   ScopedKernelTimer tk(c, "gemm_nt");
-  ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<false, true>), kGemmSmem);
-  k_gemm<false, true><<<static_cast<unsigned>(count), NT, kGemmSmem, c.stream>>>(tasks);
+  constexpr size_t smem = gemm_smem(GemmCfg<false>::stages);
+  ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<false, true>), smem);
+  k_gemm<false, true><<<static_cast<unsigned>(count), NT, smem, c.stream>>>(tasks);
   RDD_LAUNCH_CHECK();
 }
 

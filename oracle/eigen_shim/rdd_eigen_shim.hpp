@@ -36,6 +36,7 @@
 namespace Eigen {
 
 using Index = std::ptrdiff_t;
+constexpr int Dynamic = -1;
 enum UpLoType { Lower = 1, Upper = 2 };
 enum DecompositionOptions { ComputeFullU = 0x04, ComputeThinU = 0x08, ComputeFullV = 0x10, ComputeThinV = 0x20,
                             EigenvaluesOnly = 0x40, ComputeEigenvectors = 0x80 };
@@ -134,6 +135,17 @@ class MatrixXd {
   ArrayRef array() const;
   MatrixXd eval() const { return *this; }
 
+  double trace() const {
+    double t = 0.0;
+    for (Index i = 0; i < std::min(r_, c_); ++i) t += (*this)(i, i);
+    return t;
+  }
+  Block diagonal() const;
+  class CommaInit operator<<(double v);
+  class LdltSolve ldlt() const;
+  bool operator==(const MatrixXd& o) const { return r_ == o.r_ && c_ == o.c_ && a_ == o.a_; }
+  bool operator!=(const MatrixXd& o) const { return !(*this == o); }
+
   MatrixXd transpose() const {
     MatrixXd t(c_, r_);
     for (Index j = 0; j < c_; ++j)
@@ -229,12 +241,15 @@ using RowVectorXd = MatrixXd;
 // ---------------------------------------------------------------- strided writable view
 class Block {
  public:
-  Block(double* base, Index r, Index c, Index ld) : p_(base), r_(r), c_(c), ld_(ld) {}
+  Block(double* base, Index r, Index c, Index ld, Index rs = 1) : p_(base), r_(r), c_(c), ld_(ld), rs_(rs) {}
   Index rows() const { return r_; }
   Index cols() const { return c_; }
   Index size() const { return r_ * c_; }
-  double& operator()(Index i, Index j) const { return p_[j * ld_ + i]; }
-  double& operator()(Index i) const { return c_ == 1 ? p_[i] : (r_ == 1 ? p_[i * ld_] : p_[(i / r_) * ld_ + i % r_]); }
+  double& operator()(Index i, Index j) const { return p_[j * ld_ + i * rs_]; }
+  double& operator()(Index i) const {
+    return c_ == 1 ? p_[i * rs_] : (r_ == 1 ? p_[i * ld_] : p_[(i / r_) * ld_ + (i % r_) * rs_]);
+  }
+  class CommaInit operator<<(double v);
 
   Block& operator=(const MatrixXd& m) {
     if (m.size() != size()) shim::fail("block assignment: size mismatch");
@@ -259,7 +274,7 @@ class Block {
   }
   void setZero() { *this *= 0.0; }
 
-  Block block(Index i, Index j, Index r, Index c) const { return Block(&(*this)(i, j), r, c, ld_); }
+  Block block(Index i, Index j, Index r, Index c) const { return Block(&(*this)(i, j), r, c, ld_, rs_); }
   Block segment(Index i, Index n) const { return c_ == 1 ? block(i, 0, n, 1) : block(0, i, 1, n); }
   Block head(Index n) const { return segment(0, n); }
   Block tail(Index n) const { return segment(size() - n, n); }
@@ -287,7 +302,7 @@ class Block {
 
  private:
   double* p_;
-  Index r_, c_, ld_;
+  Index r_, c_, ld_, rs_;
 };
 
 inline MatrixXd::MatrixXd(const Block& b) : r_(b.rows()), c_(b.cols()), a_(static_cast<size_t>(b.size())) {
@@ -310,6 +325,34 @@ inline Block MatrixXd::bottomRows(Index n) const { return block(r_ - n, 0, n, c_
 inline Block MatrixXd::leftCols(Index n) const { return block(0, 0, r_, n); }
 inline Block MatrixXd::rightCols(Index n) const { return block(0, c_ - n, r_, n); }
 inline Block MatrixXd::topLeftCorner(Index r, Index c) const { return block(0, 0, r, c); }
+inline Block MatrixXd::diagonal() const {
+  return Block(const_cast<double*>(a_.data()), std::min(r_, c_), 1, r_, r_ + 1);
+}
+
+// comma initializer (M << a, b, ...): row after row, as Eigen fills
+class CommaInit {
+ public:
+  CommaInit(MatrixXd* m, Block* b, double v) : m_(m), b_(b) { put(v); }
+  CommaInit& operator,(double v) {
+    put(v);
+    return *this;
+  }
+
+ private:
+  void put(double v) {
+    const Index r = m_ ? m_->rows() : b_->rows(), c = m_ ? m_->cols() : b_->cols();
+    if (k_ >= r * c) shim::fail("comma initializer: too many coefficients");
+    const Index i = k_ / c, j = k_ % c;
+    if (m_) (*m_)(i, j) = v;
+    else (*b_)(i, j) = v;
+    ++k_;
+  }
+  MatrixXd* m_;
+  Block* b_;
+  Index k_ = 0;
+};
+inline CommaInit MatrixXd::operator<<(double v) { return CommaInit(this, nullptr, v); }
+inline CommaInit Block::operator<<(double v) { return CommaInit(nullptr, this, v); }
 
 // ---------------------------------------------------------------- arithmetic (eager)
 inline MatrixXd operator+(const MatrixXd& a, const MatrixXd& b) {
@@ -593,6 +636,42 @@ class ColPivQR {
 template <class MatrixType>
 using ColPivHouseholderQR = ColPivQR;
 inline ColPivQR MatrixXd::colPivHouseholderQr() const { return ColPivQR(*this); }
+// ldlt().solve (used by the reference's tests on small SPD systems): a column-pivoted QR solve
+class LdltSolve {
+ public:
+  explicit LdltSolve(const MatrixXd& A) : qr_(A) {}
+  MatrixXd solve(const MatrixXd& b) const { return qr_.solve(b); }
+
+ private:
+  ColPivQR qr_;
+};
+inline LdltSolve MatrixXd::ldlt() const { return LdltSolve(*this); }
+
+template <int Size>
+class PermutationMatrix {
+ public:
+  explicit PermutationMatrix(Index n) : idx_(std::vector<int>(static_cast<size_t>(n), 0)) {}
+  void setIdentity() {
+    for (size_t i = 0; i < idx_.v.size(); ++i) idx_.v[i] = static_cast<int>(i);
+  }
+  struct Indices {
+    std::vector<int> v;
+    int& operator()(Index i) { return v[static_cast<size_t>(i)]; }
+    int operator()(Index i) const { return v[static_cast<size_t>(i)]; }
+  };
+  Indices& indices() { return idx_; }
+  const Indices& indices() const { return idx_; }
+  // (P A).row(indices(i)) = A.row(i)
+  friend MatrixXd operator*(const PermutationMatrix& P, const MatrixXd& A) {
+    MatrixXd out(A.rows(), A.cols());
+    for (Index i = 0; i < A.rows(); ++i)
+      for (Index j = 0; j < A.cols(); ++j) out(P.idx_(i), j) = A(i, j);
+    return out;
+  }
+
+ private:
+  Indices idx_;
+};
 
 class VectorXcd {
  public:

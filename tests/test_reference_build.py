@@ -104,3 +104,18 @@ def test_oracle_matches_compiled_reference(rf, orc, name):
         assert np.linalg.norm(zo - zr) <= tol * np.linalg.norm(zr), (name, tr)
     y = rf.matvec(v)
     assert np.linalg.norm(orc.matvec(v) - y) <= 1e-12 * np.linalg.norm(y)
+
+
+def test_reference_unit_tests_pass_on_the_shims(tmp_path):
+    # the reference's own Catch2 suite (proj/tests/test_*.cpp: 65 test cases) compiled against the
+    # Eigen- and Catch2-subset shims (oracle/ref/Makefile -> oracle/_ref/ref_tests): the compiled
+    # reference used as the oracle here behaves as the reference's tests require
+    import subprocess
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_tests")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/ref_tests not built")
+    env = dict(os.environ, RDD_LAPACK_PATH=refmod.lapack_path())
+    out = subprocess.run([exe], cwd=tmp_path, capture_output=True, text=True, env=env, timeout=900)
+    tail = out.stdout.strip().splitlines()[-1]
+    assert out.returncode == 0, (tail, out.stderr[-2000:])
+    assert "test cases: 65, failed: 0" in tail, tail

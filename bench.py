@@ -15,13 +15,14 @@ Schwarz -> PCG -> test evaluation) of one seed. --config C1..C4 selects the othe
   roofline  the HBM-bound kernel with the larger share of the step — the Schwarz apply or the
           block-sparse normal operator Hᵀ(H·w) — algorithmic bytes per call over its CUDA-event
           time; the other one is reported as roofline_other.
-  cpu_baseline  one real, complete CPU-oracle solve of C5s (the 2x2x2 run BASELINE names for
-          C5), with the device's time on the same C5s solve beside it. Nothing is extrapolated.
+  cpu_baseline  one real, complete CPU solve of C5s (the 2x2x2 run BASELINE names for C5) by the
+          reference itself compiled here (oracle/_ref), with the device's time on the same C5s
+          solve beside it. Nothing is extrapolated.
 
 N>1 (torchrun): replicas — every rank solves its own seed (seed + rank) on its own GPU; the
 path has no data exchange in this tier. --impl reference: rank 0
-measures one complete C5s oracle solve and reports value = null with the reason (a full C5
-oracle solve takes hours).
+measures one complete C5s solve of the compiled reference and reports value = null with the
+reason (a full C5 solve on the host takes hours).
 """
 from __future__ import annotations
 
@@ -133,28 +134,48 @@ def barrier(dist):
 
 # ------------------------------------------------------------------ CPU oracle sample
 def cpu_sample(threads: int):
-    """One real, complete CPU-oracle solve of C5s — BASELINE configs[4]'s own 2x2x2 run of the C5
+    """One real, complete CPU solve of C5s — BASELINE configs[4]'s own 2x2x2 run of the C5
     workload (same d, m = 400, 20^3 points per subdomain, operator, PCA rule, AS-PCG to 1e-10) —
-    timed end to end on this host. Nothing is extrapolated: the device's time on the same C5s
-    solve is measured beside it (run_device), and full-size oracle timings are committed under
+    timed end to end on this host. It runs the reference itself (oracle/_ref: the unmodified
+    headers compiled against the Eigen-subset shim, C5s assembled from the reference's own types,
+    kind "reference") when that library is present, else the C++ restatement (oracle/, kind
+    "port"). Nothing is extrapolated: the device's time on the same C5s solve is measured beside
+    it (run_device), and full-size oracle timings are committed under
     profiles/oracle_fullsize_r02.jsonl."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc_mod
-    from oracle import Oracle
     from paper_2412_19207_b200 import configs
 
     cfg = configs.c5(counts=(2, 2, 2))
-    o = Oracle(threads=threads)
-    t0 = time.perf_counter()
-    s = o.run_single(cfg)
-    wall = time.perf_counter() - t0
-    o.close()
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    try:
+        import ref as ref_mod
+        use_ref = ref_mod.available()
+    except Exception:
+        use_ref = False
+    if use_ref:
+        r = ref_mod.Reference()
+        t0 = time.perf_counter()
+        s = r.run_baseline(cfg)
+        wall = time.perf_counter() - t0
+        r.close()
+        kind, what = "reference", ("the reference itself (oracle/_ref: the unmodified rannddm headers compiled against the "
+                                   "Eigen-subset shim; serial per-subdomain JacobiSVD and SelfAdjointEigenSolver as "
+                                   "runner.hpp/schwarz.hpp run them, OpenMP at the reference's sites)")
+    else:
+        from oracle import Oracle
+        o = Oracle(threads=threads)
+        t0 = time.perf_counter()
+        s = o.run_single(cfg)
+        wall = time.perf_counter() - t0
+        o.close()
+        kind, what = "port", ("the CPU oracle (C++ restatement of the reference: serial per-subdomain PCA as "
+                              "runner.hpp:52-65, OpenMP at the reference's sites, LAPACK single-threaded as Eigen)")
     return {
-        "value": wall, "unit": "s", "cores": orc_mod.lib().orc_max_threads(), "kind": "port",
+        "value": wall, "unit": "s", "cores": orc_mod.lib().orc_max_threads(), "kind": kind,
         "sample": (f"one complete run_single of C5s (2x2x2 subdomains of C5: m=400, 20^3 points per subdomain, "
-                   f"AS-PCG to 1e-10; J={s['J']}, DoF={s['DoF']}, N={s['N']}, {s['iterations']} PCG iterations) on the "
-                   f"CPU oracle (C++ restatement of the reference: serial per-subdomain PCA as runner.hpp:52-65, "
-                   f"OpenMP at the reference's sites, LAPACK single-threaded as Eigen), measured, not extrapolated"),
+                   f"AS-PCG to 1e-10; J={s['J']}, DoF={s['DoF']}, N={s['N']}, {s['iterations']} PCG iterations) on "
+                   f"{what}, measured, not extrapolated"),
         "summary": {k: s[k] for k in ("J", "DoF", "N", "iterations", "e_l2", "t_assemble", "t_precond", "t_solve")},
     }
 
@@ -173,7 +194,7 @@ def run_reference(args, cfg, world, rank, dist):
         "ms_per_step": None, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (formula-defined problem, SplitMix64 bases as the reference)", "impl": "reference",
         "config": {"workload": args.config, **cfg.as_dict()},
-        "reason": (f"a complete {args.config} solve on the host CPU oracle takes hours (serial per-subdomain PCA and "
+        "reason": (f"a complete {args.config} solve on the host (the reference compiled here) takes hours (serial per-subdomain PCA and "
                    f"dense local eigensolves); no estimate is reported. Measured instead: one complete C5s solve "
                    f"({smp['value']:.1f} s on {smp['cores']} threads, cpu_baseline) and full-size oracle timings in "
                    f"profiles/oracle_fullsize_r02.jsonl"),

@@ -40,6 +40,7 @@ def lib():
         L.ref_last_error.argtypes = [vp]
         L.ref_run_single.argtypes = [vp, C.POINTER(A.Config), C.c_uint64, C.POINTER(A.Summary)]
         L.ref_build.argtypes = [vp, C.POINTER(A.Config), C.c_uint64, C.c_int]
+        L.ref_run_baseline.argtypes = [vp, C.POINTER(A.Config), C.c_uint64, C.POINTER(A.Summary)]
         L.ref_matvec.argtypes = [vp, dp, dp]
         L.ref_matvec_transpose.argtypes = [vp, dp, dp]
         L.ref_precond_apply.argtypes = [vp, dp, dp, C.c_int]
@@ -77,6 +78,13 @@ class Reference:
     def run_single(self, cfg, seed=None) -> dict:
         s = A.Summary()
         self._check(self.L.ref_run_single(self.h, C.byref(cfg), cfg.seed if seed is None else seed, C.byref(s)))
+        return s.as_dict()
+
+    def run_baseline(self, cfg, seed=None) -> dict:
+        """run_single for a BASELINE configuration (C1-C5 problems, cell decomposition, relative
+        τ, edge points) on the reference's own functions and types (oracle/ref/ref_capi.cpp)."""
+        s = A.Summary()
+        self._check(self.L.ref_run_baseline(self.h, C.byref(cfg), cfg.seed if seed is None else seed, C.byref(s)))
         return s.as_dict()
 
     def build(self, cfg, precond=A.PRECOND_AS, seed=None):

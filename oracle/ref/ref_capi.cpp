@@ -6,7 +6,10 @@
 // the reference's own run_single (runner.hpp:202-275) and its phase functions for the
 // configurations the reference's RunConfig can express (problems example1/2/3, the reference
 // decomposition, absolute or no PCA threshold).
+#include <chrono>
+#include <cmath>
 #include <cstdio>
+#include <optional>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -26,6 +29,7 @@ struct Ref {
   std::unique_ptr<rannddm::EquilibratedSystem> eq;
   std::unique_ptr<rannddm::NormalBlocks> nb;
   std::unique_ptr<rannddm::SchwarzPreconditioner> pre;
+  std::vector<rannddm::SolveReport> base_reports;  // ref_run_baseline
 };
 
 rannddm::RunConfig to_run_config(const rdd_config& c) {
@@ -82,6 +86,181 @@ Eigen::VectorXd vec_in(const double* p, int n) {
   return v;
 }
 
+// ---- BASELINE configurations on the reference's own types: the problems C1-C5 as
+// ProblemSpecs built from the reference's operators and jet helpers, the cell-centred
+// decomposition filled into a CartesianDecomposition (geometry.hpp:84-97; neighbour sets by the
+// reference's interiors_intersect), the reference's uniform_grid plus C1's edge points, and the
+// relative PCA threshold applied to the reference's JacobiSVD (truncate at τ·σmax).
+rannddm::Jet2 ramp_L(int d, const rannddm::Point& x) {
+  rannddm::Jet2 v = rannddm::Jet2::constant(d, 1.0);
+  for (int a = 0; a < d; ++a)
+    v = v * rannddm::tanh_of_linear(d, a, x[a], 1.0) * rannddm::tanh_of_linear(d, a, x[a], -1.0, 1.0);
+  return v;
+}
+rannddm::Jet2 gauss_of_linear(int d, int axis, double x, double alpha, double beta) {  // exp(-100 q²)
+  const rannddm::Jet2 q = rannddm::Jet2::variable(d, axis, alpha * x + beta, alpha);
+  const rannddm::Jet2 s = -100.0 * (q * q);
+  const double e = std::exp(s.v);
+  return rannddm::compose(rannddm::ScalarTriple{e, e, e}, s);
+}
+
+rannddm::ProblemSpec baseline_problem(int id, int dim) {
+  using namespace rannddm;
+  ProblemSpec P;
+  auto value_field = [](std::function<double(const Point&)> f) {
+    ScalarField sf;
+    sf.value = f;
+    sf.jet = nullptr;
+    return sf;
+  };
+  switch (id) {
+    case RDD_PROBLEM_POISSON: {  // C1 (2-D) / C5 (3-D): -Δu = f, u = Π sin πx_a
+      const int d = dim == 0 ? 2 : dim;
+      P.name = "poisson";
+      P.domain.dim = d;
+      for (int a = 0; a < d; ++a) {
+        P.domain.lo[a] = 0.0;
+        P.domain.hi[a] = 1.0;
+      }
+      P.op = minus_laplacian();
+      P.exact = {value_field([d](const Point& x) {
+        double s = 1.0;
+        for (int a = 0; a < d; ++a) s *= std::sin(kPi * x[a]);
+        return s;
+      })};
+      P.rhs = {[d](const Point& x) {
+        double s = 1.0;
+        for (int a = 0; a < d; ++a) s *= std::sin(kPi * x[a]);
+        return (static_cast<double>(d) * kPi * kPi) * s;
+      }};
+      P.constraint.L = [d](const Point& x) { return ramp_L(d, x); };
+      P.constraint.G = {[d](const Point&) { return Jet2::constant(d, 0.0); }};
+      break;
+    }
+    case RDD_PROBLEM_MULTISCALE: {  // C2
+      P.name = "multiscale";
+      P.domain = make_box(2, {0.0, 0.0}, {1.0, 1.0});
+      P.op = minus_laplacian();
+      P.exact = {value_field([](const Point& x) {
+        return std::sin(2.0 * kPi * x[0]) * std::sin(2.0 * kPi * x[1]) +
+               0.1 * (std::sin(50.0 * kPi * x[0]) * std::sin(50.0 * kPi * x[1]));
+      })};
+      P.rhs = {[](const Point& x) {
+        return (8.0 * kPi * kPi) * (std::sin(2.0 * kPi * x[0]) * std::sin(2.0 * kPi * x[1])) +
+               (500.0 * kPi * kPi) * (std::sin(50.0 * kPi * x[0]) * std::sin(50.0 * kPi * x[1]));
+      }};
+      P.constraint.L = [](const Point& x) { return ramp_L(2, x); };
+      P.constraint.G = {[](const Point&) { return Jet2::constant(2, 0.0); }};
+      break;
+    }
+    case RDD_PROBLEM_HEAT: {  // C3: u_t = 0.1 Δ_xy u, axis 2 = t
+      P.name = "heat";
+      P.domain = make_box(3, {0.0, 0.0, 0.0}, {1.0, 1.0, 1.0});
+      P.op = {"heat", [](const Point&, const Jet2& u) { return u.g[2] - 0.1 * (u.hess(0, 0) + u.hess(1, 1)); }};
+      P.exact = {value_field([](const Point& x) {
+        return std::exp(-0.2 * kPi * kPi * x[2]) * (std::sin(kPi * x[0]) * std::sin(kPi * x[1]));
+      })};
+      P.rhs = {[](const Point&) { return 0.0; }};
+      P.constraint.L = [](const Point& x) {
+        return tanh_of_linear(3, 0, x[0], 1.0) * tanh_of_linear(3, 0, x[0], -1.0, 1.0) *
+               tanh_of_linear(3, 1, x[1], 1.0) * tanh_of_linear(3, 1, x[1], -1.0, 1.0) * tanh_of_linear(3, 2, x[2], 1.0);
+      };
+      P.constraint.G = {[](const Point& x) { return sin_of_linear(3, 0, x[0], kPi) * sin_of_linear(3, 1, x[1], kPi); }};
+      break;
+    }
+    case RDD_PROBLEM_ADVECTION: {  // C4: u_t + 2 u_x = 0 on [0,2] x [0,1], axis 1 = t
+      P.name = "advection";
+      P.domain = make_box(2, {0.0, 0.0}, {2.0, 1.0});
+      P.op = {"advection", [](const Point&, const Jet2& u) { return u.g[1] + 2.0 * u.g[0]; }};
+      P.exact = {value_field([](const Point& x) {
+        const double q = x[0] - 2.0 * x[1] - 0.5;
+        return std::exp(-100.0 * (q * q));
+      })};
+      P.rhs = {[](const Point&) { return 0.0; }};
+      P.constraint.L = [](const Point& x) { return tanh_of_linear(2, 0, x[0], 1.0) * tanh_of_linear(2, 1, x[1], 1.0); };
+      P.constraint.G = {[](const Point& x) {
+        const Jet2 u0 = gauss_of_linear(2, 0, x[0], 1.0, -0.5);
+        const Jet2 g = gauss_of_linear(2, 1, x[1], 2.0, 0.5);
+        return (u0 + g) - Jet2::constant(2, std::exp(-25.0));
+      }};
+      break;
+    }
+    default:
+      throw std::invalid_argument("not a BASELINE problem");
+  }
+  P.components = 1;
+  P.has_exact = true;
+  return P;
+}
+
+rannddm::CartesianDecomposition cell_decomposition(const rannddm::Box& domain, const std::vector<int>& counts,
+                                                   double ext) {
+  using namespace rannddm;
+  const int d = domain.dim;
+  CartesianDecomposition dec;
+  dec.domain = domain;
+  dec.per_axis_counts = counts;
+  dec.overlap_ratio = ext;
+  std::vector<std::vector<double>> ac(d);
+  std::vector<double> ah(d);
+  for (int a = 0; a < d; ++a) {
+    const int l = counts[a];
+    const double lo = domain.lo[a], len = domain.width(a);
+    if (l == 1) {
+      ac[a] = {lo + 0.5 * len};
+      ah[a] = 0.5 * len;
+    } else {
+      ah[a] = (0.5 + ext) / static_cast<double>(l) * len;
+      for (int j = 0; j < l; ++j) ac[a].push_back(lo + (static_cast<double>(j) + 0.5) / static_cast<double>(l) * len);
+    }
+  }
+  int total = 1;
+  for (int c : counts) total *= c;
+  std::vector<int> idx(d, 0);
+  for (int flat = 0; flat < total; ++flat) {  // axis 0 slowest, as geometry.hpp:146-167
+    Box sub;
+    sub.dim = d;
+    Point c{}, h{};
+    for (int a = 0; a < d; ++a) {
+      c[a] = ac[a][idx[a]];
+      h[a] = ah[a];
+      sub.lo[a] = c[a] - h[a];
+      sub.hi[a] = c[a] + h[a];
+    }
+    dec.subdomains.push_back(sub);
+    dec.centers.push_back(c);
+    dec.half_widths.push_back(h);
+    for (int a = d - 1; a >= 0; --a) {
+      if (++idx[a] < counts[a]) break;
+      idx[a] = 0;
+    }
+  }
+  dec.neighbor_sets.assign(total, {});
+  for (int i = 0; i < total; ++i)
+    for (int j = 0; j < total; ++j)
+      if (detail::interiors_intersect(dec.subdomains[i], dec.subdomains[j])) dec.neighbor_sets[i].push_back(j);
+  return dec;
+}
+
+rannddm::PointSet baseline_points(const rannddm::Box& domain, const std::vector<int>& res, int nb) {
+  using namespace rannddm;
+  PointSet pts = uniform_grid(domain, res, PointKind::collocation);
+  if (nb > 0) {  // C1: 4 x nb cell-centred edge points after the grid (y=lo, y=hi, x=lo, x=hi)
+    for (int e = 0; e < 4; ++e) {
+      const int axis = e < 2 ? 0 : 1, fixed = 1 - axis;
+      const double fv = (e % 2 == 0) ? domain.lo[fixed] : domain.hi[fixed];
+      const double st = (domain.hi[axis] - domain.lo[axis]) / static_cast<double>(nb);
+      for (int k = 0; k < nb; ++k) {
+        Point x{};
+        x[axis] = domain.lo[axis] + (static_cast<double>(k) + 0.5) * st;
+        x[fixed] = fv;
+        pts.points.push_back(x);
+      }
+    }
+  }
+  return pts;
+}
+
 }  // namespace
 
 extern "C" {
@@ -116,6 +295,120 @@ int ref_run_single(void* hv, const rdd_config* c, uint64_t seed, rdd_summary* ou
     for (const auto& r : h->res->reports)
       if (!r.residual_history.empty()) fr = std::max(fr, r.residual_history.back());
     out->final_residual = fr;
+  });
+}
+
+
+// run_single (runner.hpp:202-275) for a BASELINE configuration, phase by phase on the reference's
+// functions: build_instance's loop (runner.hpp:52-65) over the BASELINE objects, then
+// assemble_equilibrated, normal_blocks, build_index_sets, build_preconditioner, solve_with,
+// evaluate_solution and compute_errors.
+int ref_run_baseline(void* hv, const rdd_config* c, uint64_t seed, rdd_summary* out) {
+  Ref* h = static_cast<Ref*>(hv);
+  return guarded(h, [&] {
+    using namespace rannddm;
+    if (c->problem < RDD_PROBLEM_POISSON) throw std::invalid_argument("ref_run_baseline: BASELINE problems only");
+    const auto t0 = std::chrono::steady_clock::now();
+    auto inst = std::make_unique<Instance>();
+    inst->prob = baseline_problem(c->problem, c->dim);
+    const int d = inst->prob.domain.dim;
+    std::vector<int> counts(c->counts, c->counts + d), res(c->colloc, c->colloc + d), test(c->test, c->test + d);
+    inst->dec = c->decomposition == RDD_DECOMP_CELL ? cell_decomposition(inst->prob.domain, counts, c->delta)
+                                                    : build_decomposition(inst->prob.domain, counts, c->delta);
+    inst->collocation = baseline_points(inst->prob.domain, res, c->boundary_per_edge);
+    const WindowSet ws = make_window_set(inst->dec);
+    const Activation act = c->activation == 1 ? Activation::Sin : Activation::Tanh;
+    for (int j = 0; j < inst->dec.size(); ++j) {
+      inst->bases.push_back(make_random_basis(subdomain_seed(seed, j), c->m, d, act));
+      if (c->tau_mode == RDD_TAU_OFF) {
+        inst->reduced.push_back(identity_reduction(c->m));
+        continue;
+      }
+      const SampleMatrix sm = c->pca_matrix == RDD_PCA_PSI
+                                  ? build_sample_matrix(ws, j, inst->bases.back(), inst->collocation)
+                                  : build_operator_sample_matrix(inst->prob.op, ws, j, inst->bases.back(),
+                                                                 inst->prob.constraint, inst->collocation);
+      if (c->tau_mode == RDD_TAU_ABSOLUTE) {
+        inst->reduced.push_back(truncate(sm, c->tau));
+      } else {  // relative: the reference's truncate at τ·σmax (its SVD, its strict > and sign rule)
+        ReducedLocalBasis r = truncate(sm, 0.0);
+        const double thr = c->tau * r.singular_values(0);
+        int keep = 0;
+        for (Eigen::Index i = 0; i < r.singular_values.size(); ++i)
+          if (r.singular_values(i) > thr) ++keep;
+        if (keep == 0) keep = 1;
+        r.V = Eigen::MatrixXd(r.V.leftCols(keep));
+        r.p = keep;
+        inst->reduced.push_back(std::move(r));
+      }
+    }
+    inst->column_offsets = make_column_offsets(inst->reduced);
+    inst->p = inst->column_offsets.back();
+    const EquilibratedSystem eq = assemble_equilibrated(*inst, c->precond >= 0);
+    const double t_assemble = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const int C = inst->prob.components;
+    Eigen::MatrixXd W(inst->p, C);
+    double t_precond = 0.0, t_solve = 0.0;
+    int iterations = 0;
+    bool converged = true;
+    h->base_reports.clear();
+    if (c->solver == RDD_SOLVER_QR) {
+      const auto t1 = std::chrono::steady_clock::now();
+      const Eigen::MatrixXd Hd = densify(eq.sys);
+      Eigen::ColPivHouseholderQR<Eigen::MatrixXd> qr(Hd);
+      W = qr.solve(eq.sys.F);
+      t_solve = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    } else {
+      std::optional<SchwarzPreconditioner> pre;
+      if (c->precond >= 0) {
+        const auto t1 = std::chrono::steady_clock::now();
+        const NormalBlocks nb = normal_blocks(eq.sys, inst->dec.neighbor_sets);
+        pre = build_preconditioner(static_cast<SchwarzKind>(c->precond), nb,
+                                   build_index_sets(inst->dec, inst->column_offsets));
+        t_precond = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+      }
+      const BlockSystem& sys = eq.sys;
+      LinearMap A{inst->p, [&sys](const Eigen::VectorXd& w) { return matvec_transpose(sys, matvec(sys, w)); },
+                  nullptr, false};
+      LinearMap M = pre ? LinearMap{inst->p, [&pre](const Eigen::VectorXd& v) { return apply(*pre, v); },
+                                    [&pre](const Eigen::VectorXd& v) { return apply_transpose(*pre, v); }, false}
+                        : identity_map(inst->p);
+      const SolveConfig scfg{static_cast<SolverKind>(c->solver), c->rel_tol, c->max_iter, c->gmres_restart};
+      const auto t1 = std::chrono::steady_clock::now();
+      for (int k = 0; k < C; ++k) {
+        const Eigen::VectorXd b = matvec_transpose(sys, sys.F.col(k));
+        SolveReport rep = solve_with(scfg, A, M, b);
+        W.col(k) = rep.W;
+        iterations = std::max(iterations, rep.iterations);
+        converged = converged && rep.converged;
+        h->base_reports.push_back(std::move(rep));
+      }
+      t_solve = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    }
+    W.array().colwise() /= eq.scales.array();
+    PointSet tp = uniform_grid(inst->prob.domain, test, PointKind::test);
+    const Eigen::MatrixXd approx = evaluate_solution(*inst, W, tp);
+    const Eigen::MatrixXd exact = exact_values(inst->prob, tp, nullptr);
+    const ErrorReport err = compute_errors(approx, exact);
+    std::memset(out, 0, sizeof(*out));
+    out->seed = seed;
+    out->J = inst->dec.size();
+    out->DoF = inst->dof();
+    out->N = eq.sys.N;
+    out->p = inst->p;
+    out->iterations = iterations;
+    out->converged = converged ? 1 : 0;
+    out->e_l2 = err.rel_l2;
+    out->e_l1n = err.normalized_l1;
+    out->t_assemble = t_assemble;
+    out->t_precond = t_precond;
+    out->t_solve = t_solve;
+    double fr = 0.0;
+    for (const auto& r : h->base_reports)
+      if (!r.residual_history.empty()) fr = std::max(fr, r.residual_history.back());
+    out->final_residual = fr;
+    h->inst = std::move(inst);
+    h->res.reset();
   });
 }
 
@@ -193,6 +486,7 @@ int64_t ref_get_d(void* hv, const char* what, int index, double* out, int64_t ca
   else if (w == "F" && h->eq) put(h->eq->sys.F);
   else if (w == "local_cond" && h->pre) for (const auto& l : h->pre->local_factors) v.push_back(l.cond_estimate);
   else if (w == "hist" && h->res) v = h->res->reports.at(index).residual_history;
+  else if (w == "hist" && !h->base_reports.empty()) v = h->base_reports.at(index).residual_history;
   else if (w == "true_hist" && h->res) v = h->res->reports.at(index).true_residual_history;
   else if (w == "W" && h->res) put(h->res->reports.at(index).W);
   else {

@@ -119,3 +119,18 @@ def test_reference_unit_tests_pass_on_the_shims(tmp_path):
     tail = out.stdout.strip().splitlines()[-1]
     assert out.returncode == 0, (tail, out.stderr[-2000:])
     assert "test cases: 65, failed: 0" in tail, tail
+
+
+@pytest.mark.parametrize("name", ["c1_slice", "c2_slice", "c3_slice", "c4_slice", "c5_slice"])
+def test_oracle_matches_reference_on_baseline_slices(rf, orc, name):
+    # BASELINE configurations (C1-C5 problems, cell decomposition, relative τ) built from the
+    # reference's own types and functions (oracle/ref/ref_capi.cpp ref_run_baseline) against the
+    # restatement: the oracle's BASELINE extensions follow the reference's semantics
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_parity_gpu import CASES
+    cfg = CASES[name]
+    sr, so = rf.run_baseline(cfg), orc.run_single(cfg)
+    for k in ("J", "DoF", "N", "iterations", "converged"):
+        assert sr[k] == so[k], (name, k, sr[k], so[k])
+    assert np.array_equal(rf.geti("p_j"), orc.geti("p_j"))
+    assert abs(sr["e_l2"] - so["e_l2"]) <= 1e-8 * max(1.0, so["e_l2"]), (name, sr["e_l2"], so["e_l2"])

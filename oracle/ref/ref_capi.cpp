@@ -307,10 +307,16 @@ int ref_run_baseline(void* hv, const rdd_config* c, uint64_t seed, rdd_summary* 
   Ref* h = static_cast<Ref*>(hv);
   return guarded(h, [&] {
     using namespace rannddm;
-    if (c->problem < RDD_PROBLEM_POISSON) throw std::invalid_argument("ref_run_baseline: BASELINE problems only");
     const auto t0 = std::chrono::steady_clock::now();
     auto inst = std::make_unique<Instance>();
-    inst->prob = baseline_problem(c->problem, c->dim);
+    std::shared_ptr<ReferenceGrid> refgrid;
+    if (c->problem >= RDD_PROBLEM_POISSON) {
+      inst->prob = baseline_problem(c->problem, c->dim);
+    } else {  // the reference's own problems, with the BASELINE extensions of the other fields
+      inst->prob = make_problem("example" + std::to_string(c->problem), c->n);
+      if (!inst->prob.has_exact)
+        refgrid = std::make_shared<ReferenceGrid>(reference_example2(c->ref_resolution > 0 ? c->ref_resolution : 2001));
+    }
     const int d = inst->prob.domain.dim;
     std::vector<int> counts(c->counts, c->counts + d), res(c->colloc, c->colloc + d), test(c->test, c->test + d);
     inst->dec = c->decomposition == RDD_DECOMP_CELL ? cell_decomposition(inst->prob.domain, counts, c->delta)
@@ -388,7 +394,7 @@ int ref_run_baseline(void* hv, const rdd_config* c, uint64_t seed, rdd_summary* 
     W.array().colwise() /= eq.scales.array();
     PointSet tp = uniform_grid(inst->prob.domain, test, PointKind::test);
     const Eigen::MatrixXd approx = evaluate_solution(*inst, W, tp);
-    const Eigen::MatrixXd exact = exact_values(inst->prob, tp, nullptr);
+    const Eigen::MatrixXd exact = exact_values(inst->prob, tp, refgrid.get());
     const ErrorReport err = compute_errors(approx, exact);
     std::memset(out, 0, sizeof(*out));
     out->seed = seed;

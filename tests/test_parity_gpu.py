@@ -383,7 +383,10 @@ def test_device_vs_compiled_reference(dev, name):
     rf = refmod.Reference()
     cfg = A.Config.from_buffer_copy(CASES[name])
     cfg.rel_tol = 1e-10
-    sr = rf.run_baseline(cfg) if cfg.problem >= A.PROBLEM_POISSON else rf.run_single(cfg)
+    # BASELINE fields (cell decomposition, relative τ) through ref_run_baseline, the rest through the
+    # reference's own run_single
+    base = cfg.problem >= A.PROBLEM_POISSON or cfg.tau_mode == A.TAU_RELATIVE or cfg.decomposition != A.DECOMP_REFERENCE
+    sr = rf.run_baseline(cfg) if base else rf.run_single(cfg)
     pr = rf.geti("p_j")
     sd = dev.run_single(cfg)
     assert np.array_equal(dev.geti("p_j"), pr), name

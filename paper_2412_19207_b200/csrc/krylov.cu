@@ -204,10 +204,6 @@ __global__ void k_scal_div(double* __restrict__ out, const double* __restrict__ 
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i] / s;
 }
 
-// out = ca·a + cb·b (out may alias a or b)
-__global__ void k_lincomb(double* out, const double* a, double ca, const double* b, double cb, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = ca * a[i] + cb * b[i];
-}
 
 // ---- GMRES(m) cycle on the device (krylov.hpp:275-389): the Hessenberg column, the Givens
 // rotations, the residual estimate and the stopping tests of each Arnoldi step run in one warp, so
@@ -640,10 +636,6 @@ static void gmres_solve(Ctx& c, const double* b, double* x, double tol, int max_
   c.brk[comp] = breakdown;
 }
 
-static void lincomb(Ctx& c, double* out, const double* a, double ca, const double* b, double cb, int n) {
-  k_lincomb<<<kRB, kRT, 0, c.stream>>>(out, a, ca, b, cb, n);
-  RDD_LAUNCH_CHECK();
-}
 
 static void precond_t(Ctx& c, const double* v, double* z) {
   if (c.pkind == RDD_PRECOND_NONE) {
@@ -654,93 +646,234 @@ static void precond_t(Ctx& c, const double* v, double* z) {
   }
 }
 
-// ‖b - A x‖ / ‖b‖ (the reference's diagnostic true residual)
-static double true_residual(Ctx& c, const double* b, const double* x, double bnorm, double* t, double* part) {
+
+// ---------------------------------------------------------------- CGS / BiCG (krylov.hpp:159-270)
+// The reference's recurrences with every scalar on the device: a dot writes kRB partials, one
+// thread sums them in index order (the order the host sum used, so the iterates are unchanged) and
+// derives α, the relative residual, the stop decision and β. Every kernel of an iteration is a no-op
+// once the status leaves RUNNING, so a chunk of iterations is a fixed launch sequence, captured once
+// as a CUDA graph and replayed with one status read per replay (as the CG and GMRES drivers).
+namespace {
+
+struct SsState {
+  int status;
+  int it;
+  int max_iter;
+  int ident;
+  double rho, alpha, beta, gnorm, bnorm, tol, rel, one;
+};
+
+__device__ __forceinline__ double seq_sum(const double* p, int n) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s += p[i];
+  return s;
+}
+// σ = Σ partials; breakdown when σ = 0 or ρ = 0 (krylov.hpp:184-187, 240-243); α = ρ/σ
+__global__ void k_ss_alpha(SsState* st, const double* __restrict__ part) {
+  if (threadIdx.x != 0 || st->status != ST_RUNNING) return;
+  const double sigma = seq_sum(part, kRB);
+  if (sigma == 0.0 || st->rho == 0.0) {
+    st->status = ST_BREAKDOWN;
+    return;
+  }
+  st->alpha = st->rho / sigma;
+}
+// out = a + (sgn·coef)·b with coef a device scalar (α or β)
+__global__ void k_axpy_dev(double* out, const double* a, const double* b, const double* coef, double sgn, int n,
+                           const int* __restrict__ live) {
+  if (*live != ST_RUNNING) return;
+  const double cb = sgn * *coef;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = 1.0 * a[i] + cb * b[i];
+}
+// rel = ‖r‖/‖g‖ into the history (the preconditioned residual; with no preconditioner also the true one)
+__global__ void k_ss_rel(SsState* st, const double* __restrict__ part, double* hist, double* thist) {
+  if (threadIdx.x != 0 || st->status != ST_RUNNING) return;
+  const double rel = sqrt(seq_sum(part, kRB)) / st->gnorm;
+  st->rel = rel;
+  hist[st->it + 1] = rel;
+  if (st->ident) thist[st->it + 1] = rel;
+}
+__global__ void k_ss_thist(const SsState* st, const double* __restrict__ part, double* thist) {
+  if (threadIdx.x != 0 || st->status != ST_RUNNING) return;
+  thist[st->it + 1] = st->bnorm > 0.0 ? sqrt(seq_sum(part, kRB)) / st->bnorm : 0.0;
+}
+// one iteration done: converged (rel <= tol) or out of iterations
+__global__ void k_ss_finish(SsState* st) {
+  if (threadIdx.x != 0 || st->status != ST_RUNNING) return;
+  st->it += 1;
+  if (st->rel <= st->tol) st->status = ST_CONVERGED;
+  else if (st->it >= st->max_iter) st->status = ST_MAXITER;
+}
+// ρ_new = Σ partials, β = ρ_new/ρ
+__global__ void k_ss_beta(SsState* st, const double* __restrict__ part) {
+  if (threadIdx.x != 0 || st->status != ST_RUNNING) return;
+  const double rn = seq_sum(part, kRB);
+  st->beta = rn / st->rho;
+  st->rho = rn;
+}
+
+struct GraphExec {
+  cudaGraphExec_t exec = nullptr;
+  size_t nodes = 0;
+  ~GraphExec() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+}  // namespace
+
+// shared driver: init on the host (one-time dots), then captured iterations until the status stops
+template <class Iter>
+static void ss_solve(Ctx& c, const double* b, double* x, double* r, double tol, int max_iter, int comp,
+                     double rho, double gnorm, double bnorm, Iter iteration, DBuf<SsState>& st) {
+  const bool ident = c.pkind == RDD_PRECOND_NONE;
+  auto& hist = c.hist[comp];
+  auto& thist = c.true_hist[comp];
+  DBuf<double> dh, dth;
+  dh.ensure(static_cast<size_t>(max_iter) + 2);
+  dth.ensure(static_cast<size_t>(max_iter) + 2);
+  const double h0 = 1.0, t0 = bnorm > 0.0 ? 1.0 : 0.0;
+  RDD_CUDA(cudaMemcpyAsync(dh.p, &h0, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  RDD_CUDA(cudaMemcpyAsync(dth.p, &t0, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  SsState s0{};
+  s0.status = max_iter > 0 ? ST_RUNNING : ST_MAXITER;
+  s0.max_iter = max_iter;
+  s0.ident = ident ? 1 : 0;
+  s0.rho = rho;
+  s0.gnorm = gnorm;
+  s0.bnorm = bnorm;
+  s0.tol = tol;
+  s0.one = 1.0;
+  st.upload(&s0, 1, c.stream);
+  struct LiveScope {
+    Ctx& c;
+    LiveScope(Ctx& cc, const int* p) : c(cc) { c.live = p; }
+    ~LiveScope() { c.live = nullptr; }
+  } ls(c, &st.p->status);
+  constexpr int kChunk = 8;
+  GraphExec g;
+  {
+    const bool timing = c.timing;
+    c.timing = false;
+    const int64_t before = launch_counter();
+    cudaGraph_t graph;
+    RDD_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < kChunk; ++k) iteration(dh.p, dth.p);
+    RDD_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    g.nodes = static_cast<size_t>(launch_counter() - before);
+    launch_counter() = before;
+    RDD_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+    cudaGraphDestroy(graph);
+    c.timing = timing;
+  }
+  SsState hs{};
+  for (;;) {
+    RDD_CUDA(cudaGraphLaunch(g.exec, c.stream));
+    launch_counter() += static_cast<int64_t>(g.nodes);
+    RDD_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(SsState), cudaMemcpyDeviceToHost, c.stream));
+    RDD_CUDA(cudaStreamSynchronize(c.stream));
+    if (hs.status != ST_RUNNING) break;
+  }
+  c.iters[comp] = hs.it;
+  c.conv[comp] = hs.status == ST_CONVERGED;
+  c.brk[comp] = hs.status == ST_BREAKDOWN;
+  hist.resize(hs.it + 1);
+  thist.resize(hs.it + 1);
+  dh.download(hist.data(), hs.it + 1, c.stream);
+  dth.download(thist.data(), hs.it + 1, c.stream);
+  RDD_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// the diagnostic true residual ‖b − A x‖/‖b‖ of every iteration (krylov.hpp:199, 256)
+static void ss_true_residual(Ctx& c, const SsState* st, const double* b, const double* x, double* t, double* part,
+                             double* thist) {
+  if (c.pkind == RDD_PRECOND_NONE) return;  // k_ss_rel wrote it
   normal_operator(c, x, t);
-  k_sub<<<kRB, kRT, 0, c.stream>>>(t, b, t, c.p);
+  k_sub<<<kRB, kRT, 0, c.stream>>>(t, b, t, c.p, c.live);
+  k_dot_part<<<kRB, kRT, 0, c.stream>>>(t, t, c.p, part, c.live);
+  k_ss_thist<<<1, 32, 0, c.stream>>>(st, part, thist);
   RDD_LAUNCH_CHECK();
-  return bnorm > 0.0 ? std::sqrt(dot_host(c, t, t, c.p, part)) / bnorm : 0.0;
+}
+
+static void ss_dot(Ctx& c, const double* x, const double* y, double* part) {
+  k_dot_part<<<kRB, kRT, 0, c.stream>>>(x, y, c.p, part, c.live);
+  RDD_LAUNCH_CHECK();
+}
+static void ss_axpy(Ctx& c, double* out, const double* a, const double* b, const double* coef, double sgn) {
+  k_axpy_dev<<<kRB, kRT, 0, c.stream>>>(out, a, b, coef, sgn, c.p, c.live);
+  RDD_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------- CGS (krylov.hpp:159-213)
 static void cgs_solve(Ctx& c, const double* b, double* x, double tol, int max_iter, int comp) {
   const int n = c.p;
-  const bool ident = c.pkind == RDD_PRECOND_NONE;
   double* part = c.scal.ensure(8 * kRB + 64);
   double* v = c.wk(static_cast<size_t>(n) * 9);
   double *r = v, *rstar = v + n, *p = v + 2 * n, *u = v + 3 * n, *q = v + 4 * n, *uq = v + 5 * n, *Cp = v + 6 * n,
          *t = v + 7 * n, *t2 = v + 8 * n;
-  auto& hist = c.hist[comp];
-  auto& thist = c.true_hist[comp];
-  hist.clear();
-  thist.clear();
+  c.hist[comp].clear();
+  c.true_hist[comp].clear();
   c.iters[comp] = 0;
   c.conv[comp] = 0;
   c.brk[comp] = 0;
   Vecs V{n, &c};
-  auto Cop = [&](const double* in, double* out) {  // C = M A
-    normal_operator(c, in, t2);
-    precond(c, t2, out);
-  };
   const double bnorm = std::sqrt(dot_host(c, b, b, n, part));
   V.fill(x, 0.0);
   precond(c, b, r);  // g = M b
   const double gnorm = std::sqrt(dot_host(c, r, r, n, part));
   if (gnorm == 0.0) {
-    hist = {0.0};
-    thist = {0.0};
+    c.hist[comp] = {0.0};
+    c.true_hist[comp] = {0.0};
     c.conv[comp] = 1;
     return;
   }
   V.copy(rstar, r);
   V.copy(p, r);
   V.copy(u, r);
-  double rho = dot_host(c, rstar, r, n, part);
-  hist.push_back(1.0);
-  thist.push_back(bnorm > 0.0 ? 1.0 : 0.0);
-  for (int it = 0; it < max_iter; ++it) {
+  const double rho = dot_host(c, rstar, r, n, part);
+  DBuf<SsState> st;
+  st.ensure(1);
+  double* al = &st.p->alpha;
+  double* be = &st.p->beta;
+  auto Cop = [&](const double* in, double* out) {  // C = M A
+    normal_operator(c, in, t2);
+    precond(c, t2, out);
+  };
+  auto iteration = [&](double* dh, double* dth) {
     Cop(p, Cp);
-    const double sigma = dot_host(c, rstar, Cp, n, part);
-    if (sigma == 0.0 || rho == 0.0) {
-      c.brk[comp] = 1;
-      break;
-    }
-    const double alpha = rho / sigma;
-    lincomb(c, q, u, 1.0, Cp, -alpha, n);
-    lincomb(c, uq, u, 1.0, q, 1.0, n);
-    lincomb(c, x, x, 1.0, uq, alpha, n);
+    ss_dot(c, rstar, Cp, part);
+    k_ss_alpha<<<1, 32, 0, c.stream>>>(st.p, part);
+    RDD_LAUNCH_CHECK();
+    ss_axpy(c, q, u, Cp, al, -1.0);    // q = u − α Cp
+    ss_axpy(c, uq, u, q, &st.p->one, 1.0);  // uq = u + q
+    ss_axpy(c, x, x, uq, al, 1.0);     // x += α uq
     Cop(uq, Cp);
-    lincomb(c, r, r, 1.0, Cp, -alpha, n);
-    const double rel = std::sqrt(dot_host(c, r, r, n, part)) / gnorm;
-    hist.push_back(rel);
-    thist.push_back(ident ? rel : true_residual(c, b, x, bnorm, t, part));
-    ++c.iters[comp];
-    if (rel <= tol) {
-      c.conv[comp] = 1;
-      break;
-    }
-    const double rho_new = dot_host(c, rstar, r, n, part);
-    const double beta = rho_new / rho;
-    rho = rho_new;
-    lincomb(c, u, r, 1.0, q, beta, n);
-    lincomb(c, t, q, 1.0, p, beta, n);
-    lincomb(c, p, u, 1.0, t, beta, n);
-  }
-  RDD_CUDA(cudaStreamSynchronize(c.stream));
+    ss_axpy(c, r, r, Cp, al, -1.0);    // r −= α C uq
+    ss_dot(c, r, r, part);
+    k_ss_rel<<<1, 32, 0, c.stream>>>(st.p, part, dh, dth);
+    RDD_LAUNCH_CHECK();
+    ss_true_residual(c, st.p, b, x, t, part, dth);
+    k_ss_finish<<<1, 32, 0, c.stream>>>(st.p);
+    RDD_LAUNCH_CHECK();
+    ss_dot(c, rstar, r, part);
+    k_ss_beta<<<1, 32, 0, c.stream>>>(st.p, part);
+    RDD_LAUNCH_CHECK();
+    ss_axpy(c, u, r, q, be, 1.0);      // u = r + β q
+    ss_axpy(c, t, q, p, be, 1.0);      // t = q + β p
+    ss_axpy(c, p, u, t, be, 1.0);      // p = u + β t
+  };
+  ss_solve(c, b, x, r, tol, max_iter, comp, rho, gnorm, bnorm, iteration, st);
 }
 
-// ---------------------------------------------------------------- BiCG (krylov.hpp:217-270)
+// ---------------------------------------------------------------- BiCG (krylov.hpp:216-270)
 static void bicg_solve(Ctx& c, const double* b, double* x, double tol, int max_iter, int comp) {
   const int n = c.p;
-  const bool ident = c.pkind == RDD_PRECOND_NONE;
   double* part = c.scal.ensure(8 * kRB + 64);
   double* v = c.wk(static_cast<size_t>(n) * 8);
   double *r = v, *rstar = v + n, *p = v + 2 * n, *ps = v + 3 * n, *Cp = v + 4 * n, *Cps = v + 5 * n, *t = v + 6 * n,
          *t2 = v + 7 * n;
-  auto& hist = c.hist[comp];
-  auto& thist = c.true_hist[comp];
-  hist.clear();
-  thist.clear();
+  c.hist[comp].clear();
+  c.true_hist[comp].clear();
   c.iters[comp] = 0;
   c.conv[comp] = 0;
   c.brk[comp] = 0;
@@ -750,49 +883,45 @@ static void bicg_solve(Ctx& c, const double* b, double* x, double tol, int max_i
   precond(c, b, r);
   const double gnorm = std::sqrt(dot_host(c, r, r, n, part));
   if (gnorm == 0.0) {
-    hist = {0.0};
-    thist = {0.0};
+    c.hist[comp] = {0.0};
+    c.true_hist[comp] = {0.0};
     c.conv[comp] = 1;
     return;
   }
   V.copy(rstar, r);
   V.copy(p, r);
   V.copy(ps, r);
-  double rho = dot_host(c, rstar, r, n, part);
-  hist.push_back(1.0);
-  thist.push_back(bnorm > 0.0 ? 1.0 : 0.0);
-  for (int it = 0; it < max_iter; ++it) {
+  const double rho = dot_host(c, rstar, r, n, part);
+  DBuf<SsState> st;
+  st.ensure(1);
+  double* al = &st.p->alpha;
+  double* be = &st.p->beta;
+  auto iteration = [&](double* dh, double* dth) {
     normal_operator(c, p, t2);  // C p = M (A p)
     precond(c, t2, Cp);
-    const double sigma = dot_host(c, ps, Cp, n, part);
-    if (sigma == 0.0 || rho == 0.0) {
-      c.brk[comp] = 1;
-      break;
-    }
-    const double alpha = rho / sigma;
-    lincomb(c, x, x, 1.0, p, alpha, n);
-    lincomb(c, r, r, 1.0, Cp, -alpha, n);
+    ss_dot(c, ps, Cp, part);
+    k_ss_alpha<<<1, 32, 0, c.stream>>>(st.p, part);
+    RDD_LAUNCH_CHECK();
+    ss_axpy(c, x, x, p, al, 1.0);
+    ss_axpy(c, r, r, Cp, al, -1.0);
     precond_t(c, ps, t2);  // Cᵀ p* = Aᵀ (Mᵀ p*), A symmetric
     normal_operator(c, t2, Cps);
-    lincomb(c, rstar, rstar, 1.0, Cps, -alpha, n);
-    const double rel = std::sqrt(dot_host(c, r, r, n, part)) / gnorm;
-    hist.push_back(rel);
-    thist.push_back(ident ? rel : true_residual(c, b, x, bnorm, t, part));
-    ++c.iters[comp];
-    if (rel <= tol) {
-      c.conv[comp] = 1;
-      break;
-    }
-    const double rho_new = dot_host(c, rstar, r, n, part);
-    const double beta = rho_new / rho;
-    rho = rho_new;
-    lincomb(c, p, r, 1.0, p, beta, n);
-    lincomb(c, ps, rstar, 1.0, ps, beta, n);
-  }
-  RDD_CUDA(cudaStreamSynchronize(c.stream));
+    ss_axpy(c, rstar, rstar, Cps, al, -1.0);
+    ss_dot(c, r, r, part);
+    k_ss_rel<<<1, 32, 0, c.stream>>>(st.p, part, dh, dth);
+    RDD_LAUNCH_CHECK();
+    ss_true_residual(c, st.p, b, x, t, part, dth);
+    k_ss_finish<<<1, 32, 0, c.stream>>>(st.p);
+    RDD_LAUNCH_CHECK();
+    ss_dot(c, rstar, r, part);
+    k_ss_beta<<<1, 32, 0, c.stream>>>(st.p, part);
+    RDD_LAUNCH_CHECK();
+    ss_axpy(c, p, r, p, be, 1.0);
+    ss_axpy(c, ps, rstar, ps, be, 1.0);
+  };
+  ss_solve(c, b, x, r, tol, max_iter, comp, rho, gnorm, bnorm, iteration, st);
 }
 
-// runner.hpp:239-251: per component b = Hᵀ F_c, solve, W = y ./ scales
 void solve_all(Ctx& c, int solver, double tol, int max_iter_cfg, int restart) {
   ScopedKernelTimer tk(c, "solve");
   if (max_iter_cfg < 0) throw std::invalid_argument("max_iter must be >= 1");

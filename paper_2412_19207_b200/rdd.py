@@ -17,7 +17,7 @@ import numpy as np
 from . import abi as A
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("RDD_LIB_PATH") or os.path.join(HERE, "librdd.so")  # override: tuning variants only
+LIB_PATH = os.path.join(HERE, "librdd.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rdd.h")
 
 _lib = None

@@ -828,7 +828,10 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     // small single-CTA blocks in batches larger than the SM count: two 512-thread CTAs per SM keep
     // the whole batch resident (no partial second wave) and overlap one CTA's barrier waits
     const bool half = K == 1 && B > c.prop.multiProcessorCount && 2 * smem + 2048 <= kCtaSmem + 1024;
-    lc.blockDim = dim3(half ? kJT / 2 : kJT);
+    // cluster CTAs: 512 threads (RDD_JACOBI_NT experiment override)
+    const char* ent = std::getenv("RDD_JACOBI_NT");
+    const bool half_cl = K > 1 && ent && std::atoi(ent) == 512;
+    lc.blockDim = dim3(half || half_cl ? kJT / 2 : kJT);
     lc.dynamicSmemBytes = smem;
     lc.stream = c.stream;
     cudaLaunchAttribute at[1];
@@ -848,9 +851,9 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     };
     if (K == 1 && half) launch(k_jacobi_oe<1, kJT / 2>);
     else if (K == 1) launch(k_jacobi_oe<1>);
-    else if (K == 2) launch(k_jacobi_oe<2>);
-    else if (K == 4) launch(k_jacobi_oe<4>);
-    else launch(k_jacobi_oe<8>);
+    else if (K == 2) half_cl ? launch(k_jacobi_oe<2, kJT / 2>) : launch(k_jacobi_oe<2>);
+    else if (K == 4) half_cl ? launch(k_jacobi_oe<4, kJT / 2>) : launch(k_jacobi_oe<4>);
+    else half_cl ? launch(k_jacobi_oe<8, kJT / 2>) : launch(k_jacobi_oe<8>);
     const int E = ((ne + 31) / 32 + 1) & ~1;  // positions per lane, even
     if (E <= 16) {
       const int R = E <= 8 ? 4 : 2;

@@ -295,6 +295,7 @@ void evaluate_at(Ctx& c, long long M, const double* pts, const double* W, const 
 // gemm.cu
 void gemm_tn(Ctx& c, const std::vector<GemmTask>& tasks);  // C = Aᵀ B (A: K x M, B: K x N col-major)
 void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks);  // C = A B  (A: M x K, B: K x N col-major)
+void gemm_nn_wide(Ctx& c, const std::vector<GemmTask>& tasks);  // same, 64 x 128 tiles (tn in units of 128)
 void gemm_nt(Ctx& c, const std::vector<GemmTask>& tasks);
 void gemm_nt_dev(Ctx& c, const GemmTask* tasks, int count);  // C = A Bᵀ (A: M x K, B: N x K col-major)
 void project_blocks(Ctx& c);

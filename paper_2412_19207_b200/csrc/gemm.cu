@@ -167,6 +167,95 @@ __global__ void __launch_bounds__(NT, GemmCfg<AT>::minb) k_gemm(const GemmTask* 
       }
 }
 
+// NN product with a 64 x 128 CTA tile (8 warps, 32x32 warp tiles): for C = A·B with N <= 128 (the
+// PCA's S·V_r, S·Q and S·V on blocks with r_j, p_j <= 128) one CTA covers every column, so the
+// large A = S is streamed once per row tile instead of once per 64-column tile. Tasks index tiles
+// in units of (64, 128).
+constexpr int WBN = 128, WNT = 256, WSTAGES = 3;
+constexpr int kStageWA = BK * MP, kStageWB = WBN * KP;
+constexpr size_t kWideSmem = static_cast<size_t>(WSTAGES) * (kStageWA + kStageWB) * sizeof(double);
+
+__global__ void __launch_bounds__(WNT, 2) k_gemm_nn_wide(const GemmTask* __restrict__ tasks) {
+  extern __shared__ __align__(16) double gsm[];
+  const GemmTask T = tasks[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m0 = T.tm * BM, n0 = T.tn * WBN;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 32;
+  const bool pre = T.beta != 0.0 && (T.alpha == 1.0 || T.alpha == -1.0);
+  const double cf = T.beta * T.alpha;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m = m0 + wm + 8 * i + (lane >> 2);
+        const int n = n0 + wn + 8 * j + 2 * (lane & 3) + e;
+        acc[i][j][e] = (pre && m < T.M && n < T.N) ? cf * T.Cm[m + static_cast<long long>(n) * T.ldc] : 0.0;
+      }
+  auto As = [&](int st) { return gsm + static_cast<size_t>(st) * (kStageWA + kStageWB); };
+  auto Bs = [&](int st) { return gsm + static_cast<size_t>(st) * (kStageWA + kStageWB) + kStageWA; };
+  auto issue = [&](int kt, int st) {
+    const int k0 = kt * BK;
+    double* a = As(st);
+    double* bsm = Bs(st);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // A(m, k) = A[m + k*lda] -> a[k][m]
+      const int ml = tid & 63, m = m0 + ml, kl = (tid >> 6) + 4 * i, k = k0 + kl;
+      const bool v = k < T.K && m < T.M;
+      cp_async8(a + kl * MP + ml, v ? T.A + m + static_cast<long long>(k) * T.lda : T.A, v);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {  // B(k, n) = B[k + n*ldb] -> b[n][k]
+      const int kl = tid & 15, k = k0 + kl, nl = (tid >> 4) + 16 * i, n = n0 + nl;
+      const bool v = k < T.K && n < T.N;
+      cp_async8(bsm + nl * KP + kl, v ? T.B + k + static_cast<long long>(n) * T.ldb : T.B, v);
+    }
+  };
+  const int nk = (T.K + BK - 1) / BK;
+#pragma unroll
+  for (int st = 0; st < WSTAGES - 1; ++st) {
+    if (st < nk) issue(st, st);
+    cp_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait<WSTAGES - 2>();
+    __syncthreads();
+    if (kt + WSTAGES - 1 < nk) issue(kt + WSTAGES - 1, (kt + WSTAGES - 1) % WSTAGES);
+    cp_commit();
+    const double* a = As(kt % WSTAGES);
+    const double* bsm = Bs(kt % WSTAGES);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      const int k = kk + (lane & 3);
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = a[k * MP + wm + 8 * i + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = bsm[(wn + 8 * j + (lane >> 2)) * KP + k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m = m0 + wm + 8 * i + (lane >> 2);
+        const int n = n0 + wn + 8 * j + 2 * (lane & 3) + e;
+        if (m < T.M && n < T.N) {
+          double* pp = T.Cm + m + static_cast<long long>(n) * T.ldc;
+          *pp = pre ? T.alpha * acc[i][j][e] : (T.beta != 0.0 ? T.beta * *pp : 0.0) + T.alpha * acc[i][j][e];
+        }
+      }
+}
+
 template <bool AT, bool BT>
 void launch(Ctx& c, const std::vector<GemmTask>& tasks, const char* fam) {
   if (tasks.empty()) return;
@@ -183,6 +272,16 @@ void launch(Ctx& c, const std::vector<GemmTask>& tasks, const char* fam) {
 
 }  // namespace
 
+void gemm_nn_wide(Ctx& c, const std::vector<GemmTask>& tasks) {
+  if (tasks.empty()) return;
+  ScopedKernelTimer tk(c, "gemm_nn");
+  DBuf<GemmTask> d;
+  d.upload(tasks, c.stream);
+  ensure_smem_attr(reinterpret_cast<const void*>(k_gemm_nn_wide), kWideSmem);
+  k_gemm_nn_wide<<<static_cast<unsigned>(tasks.size()), WNT, kWideSmem, c.stream>>>(d.p);
+  RDD_LAUNCH_CHECK();
+  if (!alloc_stream()) RDD_CUDA(cudaStreamSynchronize(c.stream));
+}
 void gemm_tn(Ctx& c, const std::vector<GemmTask>& tasks) { launch<true, false>(c, tasks, "gemm_tn"); }
 void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks) { launch<false, false>(c, tasks, "gemm_nn"); }
 void gemm_nt(Ctx& c, const std::vector<GemmTask>& tasks) { launch<false, true>(c, tasks, "gemm_nt"); }

@@ -22,6 +22,29 @@
 
 namespace rdd {
 
+// C_j = A_j·B_j for a batch of row-major-tiled NN products whose widths N_j are all <= 128 take the
+// 64 x 128-tile kernel (the tall A_j = S_j streamed once per row tile), otherwise 64 x 64 tiles
+struct NNItem {
+  const double* A;
+  const double* B;
+  double* C;
+  int M, N, K, lda, ldb, ldc;
+};
+static void nn_batch(Ctx& c, const std::vector<NNItem>& items) {
+  int nmax = 0;
+  for (const NNItem& it : items) nmax = std::max(nmax, it.N);
+  const bool wide = nmax > 64 && nmax <= 128;  // N <= 64 fits one 64-wide tile already
+  const int tw = wide ? 128 : 64;
+  std::vector<GemmTask> t;
+  for (const NNItem& it : items)
+    for (int tm = 0; tm < ceil_div(it.M, 64); ++tm)
+      for (int tn = 0; tn < ceil_div(it.N, tw); ++tn)
+        t.push_back({it.A, it.B, it.C, nullptr, nullptr, it.M, it.N, it.K, it.lda, it.ldb, it.ldc, tm, tn, 0.0});
+  if (wide) gemm_nn_wide(c, t);
+  else gemm_nn(c, t);
+}
+
+
 namespace {
 
 // per subdomain: sort eigenvalues descending, threshold, reorder + sign-canonicalise V
@@ -401,15 +424,13 @@ void run_pca(Ctx& c) {
         const double* Vin = it == 0 ? (skip_s1 ? Lw.p : Vr.p) : V0.p;
         {
           ScopedKernelTimer tr(c, "pca_refine");
-          std::vector<GemmTask> t;
+          std::vector<NNItem> items;
           for (int j = 0; j < J; ++j) {
             const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
-            for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
-              for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
-                t.push_back({c.S.p + c.S_off[j], Vin + offm[j], T.p + c.S_off[j], nullptr, nullptr, rows, rj[j], m,
-                             std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+            items.push_back({c.S.p + c.S_off[j], Vin + offm[j], T.p + c.S_off[j], rows, rj[j], m, std::max(rows, 1), m,
+                             std::max(rows, 1)});
           }
-          gemm_nn(c, t);  // Z = S·V
+          nn_batch(c, items);  // Z = S·V
         }
         {
           ScopedKernelTimer tr(c, "pca_refine");
@@ -435,15 +456,13 @@ void run_pca(Ctx& c) {
       }
       {
         ScopedKernelTimer ts(c, "pca_stage2_gemm");
-        std::vector<GemmTask> t;
+        std::vector<NNItem> items;
         for (int j = 0; j < J; ++j) {
           const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
-          for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
-            for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
-              t.push_back({c.S.p + c.S_off[j], V0.p + offm[j], T.p + c.S_off[j], nullptr, nullptr, rows, rj[j], m,
-                           std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+          items.push_back({c.S.p + c.S_off[j], V0.p + offm[j], T.p + c.S_off[j], rows, rj[j], m, std::max(rows, 1), m,
+                           std::max(rows, 1)});
         }
-        gemm_nn(c, t);  // T_a = S·Q
+        nn_batch(c, items);  // T_a = S·Q
       }
       {
         ScopedKernelTimer ts(c, "pca_stage2_gemm");
@@ -576,15 +595,13 @@ void project_blocks(Ctx& c) {
   }
   const int J = c.J, m = c.m;
   c.Hbuf.ensure(std::max<long long>(1, c.H_off[J]));
-  std::vector<GemmTask> t;
+  std::vector<NNItem> items;
   for (int j = 0; j < J; ++j) {
     const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
-    for (int tm = 0; tm < ceil_div(rows, 64); ++tm)
-      for (int tn = 0; tn < ceil_div(c.h_p[j], 64); ++tn)
-        t.push_back({c.S.p + c.S_off[j], c.Vred.p + static_cast<size_t>(j) * m * m, c.Hbuf.p + c.H_off[j], nullptr,
-                     nullptr, rows, c.h_p[j], m, std::max(rows, 1), m, std::max(rows, 1), tm, tn, 0.0});
+    items.push_back({c.S.p + c.S_off[j], c.Vred.p + static_cast<size_t>(j) * m * m, c.Hbuf.p + c.H_off[j], rows,
+                     c.h_p[j], m, std::max(rows, 1), m, std::max(rows, 1)});
   }
-  gemm_nn(c, t);
+  nn_batch(c, items);  // H_j = S_j·V_j
   c.H = c.Hbuf.p;
 }
 

@@ -39,6 +39,8 @@ rannddm::RunConfig to_run_config(const rdd_config& c) {
     throw std::invalid_argument("reference RunConfig: only the reference decomposition");
   if (c.boundary_per_edge != 0) throw std::invalid_argument("reference RunConfig: no extra boundary points");
   if (c.tau_mode == RDD_TAU_RELATIVE) throw std::invalid_argument("reference RunConfig: tau is absolute");
+  if (c.solver < RDD_SOLVER_QR || c.solver > RDD_SOLVER_GMRES) throw std::invalid_argument("unknown solver");
+  if (c.precond < RDD_PRECOND_NONE || c.precond > RDD_PRECOND_RAS) throw std::invalid_argument("unknown preconditioner");
   rannddm::RunConfig r;
   r.problem = "example" + std::to_string(c.problem);
   r.n = c.n;
@@ -307,6 +309,8 @@ int ref_run_baseline(void* hv, const rdd_config* c, uint64_t seed, rdd_summary* 
   Ref* h = static_cast<Ref*>(hv);
   return guarded(h, [&] {
     using namespace rannddm;
+    if (c->solver < RDD_SOLVER_QR || c->solver > RDD_SOLVER_GMRES) throw std::invalid_argument("unknown solver");
+    if (c->precond < RDD_PRECOND_NONE || c->precond > RDD_PRECOND_RAS) throw std::invalid_argument("unknown preconditioner");
     const auto t0 = std::chrono::steady_clock::now();
     auto inst = std::make_unique<Instance>();
     std::shared_ptr<ReferenceGrid> refgrid;

@@ -229,3 +229,23 @@ def test_ras_gmres_slices_vs_oracle(dev, case):
     assert abs(s["iterations"] - ref["iterations"]) <= int(0.05 * ref["iterations"])
     h = dev.getd("hist", 0)[::50]
     np.testing.assert_allclose(h[:len(ref["hist_every_50"])], ref["hist_every_50"], rtol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["C1", "C5s"])
+def test_full_size_vs_compiled_reference(dev, name):
+    # C1 at full size and C5s (the 2x2x2 run BASELINE names for C5) on the reference itself
+    # (oracle/_ref: the unmodified headers on the Eigen-subset shim, the BASELINE objects built from
+    # its own types): ranks bit-exact, iterations within 5%, errors and solutions within 1e-8
+    import ref as refmod
+    if not refmod.available():
+        pytest.fail("oracle/_ref/libref.so missing (built by __graft_entry__.build() next to /root/reference)")
+    cfg = configs.c1() if name == "C1" else configs.c5(counts=(2, 2, 2))
+    rf = refmod.Reference()
+    sr = rf.run_baseline(cfg)
+    pr = rf.geti("p_j")
+    sd = dev.run_single(cfg)
+    assert np.array_equal(dev.geti("p_j"), pr)
+    assert sd["DoF"] == sr["DoF"] and sd["N"] == sr["N"] and sd["converged"] == sr["converged"] == 1
+    assert abs(sd["iterations"] - sr["iterations"]) <= int(0.05 * sr["iterations"]), (sd, sr)
+    assert abs(sd["e_l2"] - sr["e_l2"]) <= 1e-8, (sd["e_l2"], sr["e_l2"])
+    assert abs(sd["e_l1n"] - sr["e_l1n"]) <= 1e-8

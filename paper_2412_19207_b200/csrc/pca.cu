@@ -278,6 +278,191 @@ __global__ void __launch_bounds__(kHouseThreads) k_house_complete(const double* 
   }
 }
 
+// Thin Householder QR in blocked (compact-WY) form, the same reflectors as k_house_complete's:
+// panels of kHP columns are factored in shared memory (column-by-column, H_k = I − β_k v_k v_kᵀ,
+// H x = sg e_k), T of the panel (H_p ⋯ H_{p+w−1} = I − V T Vᵀ) is formed from VᵀV, and every
+// column right of the panel takes one update y ← y − V Tᵀ (Vᵀ y), a warp per column with the
+// panel in shared memory — each trailing column is read once per panel instead of once per
+// reflector. Q = H_0 ⋯ H_{r−1} [I_r; 0] is accumulated panel by panel in reverse (y ← y − V T (Vᵀ y)
+// on columns >= p). One CTA per subdomain; m <= kHouseMaxM.
+constexpr int kHP = 32;
+constexpr int kHouseMaxM = 512;
+constexpr int kHBThreads = 512;
+constexpr int kHBWarps = kHBThreads / 32;
+
+
+// y (global column, rows p..m-1) <- y - V M (Vᵀ y), M = T (transposed when tr): one warp
+__device__ __forceinline__ void wy_update(const double* __restrict__ P, int ldp, int R, int w, const double* Tm,
+                                          bool tr, double* y, double* scr, int lane) {
+  double s[kHP];
+#pragma unroll
+  for (int i = 0; i < kHP; ++i) s[i] = 0.0;
+  for (int row = lane; row < R; row += 32) {
+    const double yr = y[row];
+#pragma unroll
+    for (int i = 0; i < kHP; ++i)
+      if (i < w) s[i] += P[i * ldp + row] * yr;  // V[:, i] is zero above row i (zeroed in smem)
+  }
+  // transpose-reduce: lane i ends with (Vᵀy)_i
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const double send = up ? s[i] : s[i + o];
+      const double keep = up ? s[i + o] : s[i];
+      s[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  scr[lane] = s[0];
+  __syncwarp();
+  double z = 0.0;  // z = M·(Vᵀy): Tᵀ for the factorisation (Qᵀ applied), T for Q
+  if (lane < w) {
+    if (tr)
+      for (int i = 0; i <= lane; ++i) z += Tm[i * kHP + lane] * scr[i];
+    else
+      for (int i = lane; i < w; ++i) z += Tm[lane * kHP + i] * scr[i];
+  }
+  __syncwarp();
+  scr[kHP + lane] = z;
+  __syncwarp();
+  for (int row = lane; row < R; row += 32) {
+    double a = 0.0;
+#pragma unroll
+    for (int i = 0; i < kHP; ++i)
+      if (i < w) a += P[i * ldp + row] * scr[kHP + i];
+    y[row] -= a;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __restrict__ Vr,
+                                                               const double* __restrict__ lam,
+                                                               const long long* __restrict__ lam_off,
+                                                               const int* __restrict__ rr, int n,
+                                                               double* __restrict__ A, double* __restrict__ Q,
+                                                               double* __restrict__ Tw) {
+  extern __shared__ double hsm[];
+  double* P = hsm;                            // panel: kHP columns, ld n
+  double* Tm = P + static_cast<size_t>(kHP) * n;  // kHP x kHP (row i, column j at i*kHP + j)
+  double* beta = Tm + kHP * kHP;              // kHP
+  double* G = beta + kHP;                     // kHP x kHP: VᵀV
+  double* scr = G + kHP * kHP;                // per warp 2*kHP
+  double* red = scr + kHBWarps * 2 * kHP;     // kHBWarps
+  int* perm = reinterpret_cast<int*>(red + kHBWarps);  // n
+  const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = rr[j];
+  const size_t off = static_cast<size_t>(j) * n * n;
+  const double* Vj = Vr + off;
+  double* Aj = A + off;
+  double* Qj = Q + off;
+  double* Tj = Tw + static_cast<size_t>(j) * ((n + kHP - 1) / kHP) * kHP * kHP;
+  const double* lj = lam + lam_off[j];
+  for (int c = tid; c < r; c += blockDim.x) {  // stable descending rank of the eigenvalues
+    int rk = 0;
+    for (int q = 0; q < r; ++q) rk += (lj[q] > lj[c]) || (lj[q] == lj[c] && q < c);
+    perm[rk] = c;
+  }
+  __syncthreads();
+  for (int c = warp; c < r; c += kHBWarps) {  // A[:, c] = Vr[:, perm[c]] / ||.||
+    const double* src = Vj + static_cast<size_t>(perm[c]) * n;
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s += src[i] * src[i];
+    s = warp_sum(s);
+    const double sc = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+    for (int i = lane; i < n; i += 32) Aj[i + static_cast<size_t>(c) * n] = src[i] * sc;
+  }
+  __syncthreads();
+  // ---- factorisation, panel by panel
+  for (int p = 0, pi = 0; p < r; p += kHP, ++pi) {
+    const int w = min(kHP, r - p), R = n - p;
+    for (int c = 0; c < w; ++c)
+      for (int i = tid; i < R; i += blockDim.x) P[c * n + i] = Aj[(p + i) + static_cast<size_t>(p + c) * n];
+    __syncthreads();
+    for (int c = 0; c < w; ++c) {  // the panel's reflectors (column norms over the whole CTA)
+      double* x = P + c * n;
+      double s2 = 0.0;
+      for (int i = c + tid; i < R; i += blockDim.x) s2 += x[i] * x[i];
+      s2 = warp_sum(s2);
+      __syncthreads();
+      if (lane == 0) red[warp] = s2;
+      __syncthreads();
+      double nrm2 = 0.0;
+      for (int q = 0; q < kHBWarps; ++q) nrm2 += red[q];
+      const double alpha = sqrt(nrm2), x0 = x[c];
+      const double sg = x0 >= 0.0 ? -alpha : alpha;  // H x = sg e_c
+      const double b = alpha > 0.0 ? 1.0 / (sg * (sg - x0)) : 0.0;
+      __syncthreads();
+      if (tid == 0) {
+        x[c] = x0 - sg;  // v_c (the rest of v is x below the diagonal)
+        beta[c] = b;
+      }
+      __syncthreads();
+      for (int cc = c + 1 + warp; cc < w; cc += kHBWarps) {  // the panel's own later columns
+        double* y = P + cc * n;
+        double t = 0.0;
+        for (int i = c + lane; i < R; i += 32) t += x[i] * y[i];
+        t = warp_sum(t) * b;
+        for (int i = c + lane; i < R; i += 32) y[i] -= t * x[i];
+      }
+      __syncthreads();
+    }
+    for (int c = 0; c < w; ++c)  // store v (and R above it) back; keep V with zeros above the diagonal
+      for (int i = tid; i < R; i += blockDim.x) {
+        Aj[(p + i) + static_cast<size_t>(p + c) * n] = P[c * n + i];
+        if (i < c) P[c * n + i] = 0.0;
+      }
+    __syncthreads();
+    // T: T_cc = β_c; T[0:c, c] = -β_c T[0:c, 0:c] (V[:, 0:c]ᵀ v_c)
+    for (int e = warp; e < w * w; e += kHBWarps) {
+      const int a = e / w, bcol = e % w;
+      if (a >= bcol) continue;
+      double t = 0.0;
+      for (int i = bcol + lane; i < R; i += 32) t += P[a * n + i] * P[bcol * n + i];
+      t = warp_sum(t);
+      if (lane == 0) G[a * kHP + bcol] = t;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int c = 0; c < w; ++c) {
+        double t = 0.0;
+        if (lane < c)
+          for (int k = lane; k < c; ++k) t += Tm[lane * kHP + k] * G[k * kHP + c];
+        __syncwarp();
+        if (lane < c) Tm[lane * kHP + c] = -beta[c] * t;
+        if (lane == c) Tm[c * kHP + c] = beta[c];
+        if (lane > c && lane < kHP) Tm[lane * kHP + c] = 0.0;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < kHP * kHP; e += blockDim.x) Tj[pi * kHP * kHP + e] = Tm[e];
+    // trailing columns: y <- (I - V T Vᵀ)ᵀ y = y - V Tᵀ (Vᵀ y)
+    for (int c = p + w + warp; c < r; c += kHBWarps)
+      wy_update(P, n, R, w, Tm, true, Aj + p + static_cast<size_t>(c) * n, scr + warp * 2 * kHP, lane);
+    __syncthreads();
+  }
+  // ---- Q = H_0 ⋯ H_{r-1} [I_r; 0], panels in reverse
+  for (size_t e = tid; e < static_cast<size_t>(n) * r; e += blockDim.x) Qj[e] = (e % (n + 1) == 0) ? 1.0 : 0.0;
+  __syncthreads();
+  const int np = (r + kHP - 1) / kHP;
+  for (int pi = np - 1; pi >= 0; --pi) {
+    const int p = pi * kHP, w = min(kHP, r - p), R = n - p;
+    for (int c = 0; c < w; ++c)
+      for (int i = tid; i < R; i += blockDim.x) P[c * n + i] = i < c ? 0.0 : Aj[(p + i) + static_cast<size_t>(p + c) * n];
+    for (int e = tid; e < kHP * kHP; e += blockDim.x) Tm[e] = Tj[pi * kHP * kHP + e];
+    __syncthreads();
+    for (int c = p + warp; c < r; c += kHBWarps)
+      wy_update(P, n, R, w, Tm, false, Qj + p + static_cast<size_t>(c) * n, scr + warp * 2 * kHP, lane);
+    __syncthreads();
+  }
+}
+
+size_t house_blocked_smem(int n) {
+  return (static_cast<size_t>(kHP) * n + 2 * kHP * kHP + kHP + kHBWarps * 2 * kHP + kHBWarps) * sizeof(double) +
+         static_cast<size_t>(n) * sizeof(int);
+}
+
 // V0[:, :r_j] = Vs[:, :r_j] (m x r_j leading columns, column-major ld m)
 __global__ void k_copy_lead(const double* __restrict__ Vs, double* __restrict__ V0, const int* __restrict__ r, int m) {
   const size_t off = static_cast<size_t>(blockIdx.x) * m * m;
@@ -450,8 +635,16 @@ void run_pca(Ctx& c) {
                                         static_cast<int>(sm)));
         const double* ord = (it == 0 && !skip_s1) ? lam.p : dorder;
         ScopedKernelTimer th(c, "pca_house");
-        k_house_complete<<<J, kHouseThreads, sm, c.stream>>>(Hw.p, ord, doffr_sel.p, dr.p, m, Lw.p == Vin ? Vr.p : Lw.p,
-                                                             V0.p, 1);
+        if (m <= kHouseMaxM && rmax >= 192) {  // wide blocks (C3, C5): blocked compact-WY form, same reflectors
+          const size_t hsm = house_blocked_smem(m);
+          ensure_smem_attr(reinterpret_cast<const void*>(k_house_blocked), hsm);
+          double* Tw = c.ws("pca.houseT", static_cast<size_t>(J) * ceil_div(m, kHP) * kHP * kHP);
+          k_house_blocked<<<J, kHBThreads, hsm, c.stream>>>(Hw.p, ord, doffr_sel.p, dr.p, m,
+                                                            Lw.p == Vin ? Vr.p : Lw.p, V0.p, Tw);
+        } else {
+          k_house_complete<<<J, kHouseThreads, sm, c.stream>>>(Hw.p, ord, doffr_sel.p, dr.p, m,
+                                                               Lw.p == Vin ? Vr.p : Lw.p, V0.p, 1);
+        }
         RDD_LAUNCH_CHECK();  // V0[:, :r] = orthonormal basis of span(Y)
       }
       {

@@ -20,7 +20,11 @@ The per-subdomain PCAs are independent, so `pca` mode runs them concurrently on 
 bench's CPU leg runs it (the reference's serial PCA loop). Timings and the core count go to
 profiles/oracle_fullsize_r02.jsonl.
 
-usage: python tests/golden/make_fullsize.py pca C5 [C3 ...] | run C2 [C4]
+  ref_run_<C>.npz (C2, C4)  the same run_single on the reference itself (oracle/_ref: the unmodified
+                headers on the Eigen-subset shim, the BASELINE objects built from its own types):
+                p_j, iterations, errors, final residual, residual history.
+
+usage: python tests/golden/make_fullsize.py pca C5 [C3 ...] | run C2 [C4] | refrun C2 [C4]
 """
 from __future__ import annotations
 
@@ -134,7 +138,29 @@ def do_run(name: str):
     o.close()
 
 
+def do_refrun(name: str):
+    import ref as refmod
+    cfg = configs.aspcg(name)
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    r = refmod.Reference()
+    t0 = time.perf_counter()
+    s = r.run_baseline(cfg)
+    t = time.perf_counter() - t0
+    pay = {"p_j": r.geti("p_j").astype(np.int32), "iterations": np.array(s["iterations"]),
+           "converged": np.array(s["converged"]), "e_l2": np.array(s["e_l2"]), "e_l1n": np.array(s["e_l1n"]),
+           "final_residual": np.array(s["final_residual"]), "DoF": np.array(s["DoF"]), "N": np.array(s["N"]),
+           "hist": r.getd("hist", 0)}
+    os.makedirs(OUT, exist_ok=True)
+    np.savez_compressed(os.path.join(OUT, f"ref_run_{name}.npz"), **pay)
+    log({"mode": "reference run_single (oracle/_ref)", "config": name, "solver": "AS-PCG", "rel_tol": cfg.rel_tol,
+         "J": s["J"], "DoF": s["DoF"], "N": s["N"], "iterations": s["iterations"], "e_l2": s["e_l2"], "wall_s": t,
+         "phases_s": {k: s[k] for k in ("t_assemble", "t_precond", "t_solve")}, "threads": os.environ["OMP_NUM_THREADS"],
+         "host": os.uname().nodename})
+    print(name, "refrun", f"{t:.1f}s", {k: s[k] for k in ("iterations", "e_l2", "DoF")}, flush=True)
+    r.close()
+
+
 if __name__ == "__main__":
     mode, names = sys.argv[1], sys.argv[2:]
     for n in names:
-        (do_pca if mode == "pca" else do_run)(n)
+        {"pca": do_pca, "run": do_run, "refrun": do_refrun}[mode](n)

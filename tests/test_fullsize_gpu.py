@@ -249,3 +249,20 @@ def test_full_size_vs_compiled_reference(dev, name):
     assert abs(sd["iterations"] - sr["iterations"]) <= int(0.05 * sr["iterations"]), (sd, sr)
     assert abs(sd["e_l2"] - sr["e_l2"]) <= 1e-8, (sd["e_l2"], sr["e_l2"])
     assert abs(sd["e_l1n"] - sr["e_l1n"]) <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_full_size_run_vs_reference_fixture(dev, name):
+    # the full-size AS-PCG solves of C2 and C4 on the reference itself (tests/golden/make_fullsize.py
+    # refrun: oracle/_ref with the BASELINE objects built from the reference's own types)
+    fx = _fixture("ref_run", name)
+    sd = dev.run_single(configs.aspcg(name))
+    assert np.array_equal(dev.geti("p_j"), fx["p_j"])
+    assert sd["DoF"] == int(fx["DoF"]) and sd["N"] == int(fx["N"]) and sd["converged"] == int(fx["converged"]) == 1
+    its = int(fx["iterations"])
+    assert abs(sd["iterations"] - its) <= int(0.05 * its), (sd["iterations"], its)
+    assert sd["e_l2"] == pytest.approx(float(fx["e_l2"]), rel=1e-8), (sd["e_l2"], float(fx["e_l2"]))
+    assert sd["e_l1n"] == pytest.approx(float(fx["e_l1n"]), rel=1e-8)
+    hd, ho = dev.getd("hist", 0), fx["hist"]
+    k = min(len(hd), len(ho))
+    np.testing.assert_allclose(hd[:k][ho[:k] > 1e-6], ho[:k][ho[:k] > 1e-6], rtol=1e-6)

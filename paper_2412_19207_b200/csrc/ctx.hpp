@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstring>
 #include <map>
 #include <string>
 #include <vector>
@@ -69,6 +70,41 @@ struct CustomInputs {
   std::vector<double> R, b;                     // J x m x d, J x m
   int C = 1;
   std::vector<double> coef, Ljet, F;            // jet_len(d); N x jet_len(d); N x C (column-major)
+};
+
+// Pinned staging for host-built task lists: the H2D copy of a pageable vector blocks the host
+// until the stream reaches it (so the GPU idles while the next list is built); two pinned slots
+// alternate, each reused only after its previous copy has executed.
+struct PinnedStage {
+  void* buf[2] = {nullptr, nullptr};
+  size_t cap[2] = {0, 0};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  bool used[2] = {false, false};
+  int next = 0;
+  ~PinnedStage() {
+    for (int i = 0; i < 2; ++i) {
+      if (buf[i]) cudaFreeHost(buf[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+  }
+  // copies `bytes` from host `src` to device `dst` on `s` through a pinned slot
+  void upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (!bytes) return;
+    const int k = next;
+    next ^= 1;
+    if (!ev[k]) RDD_CUDA(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+    if (used[k]) RDD_CUDA(cudaEventSynchronize(ev[k]));
+    if (cap[k] < bytes) {
+      if (buf[k]) RDD_CUDA(cudaFreeHost(buf[k]));
+      cap[k] = std::max(bytes, cap[k] * 2);
+      RDD_CUDA(cudaHostAlloc(&buf[k], cap[k], cudaHostAllocDefault));
+    }
+    std::memcpy(buf[k], src, bytes);
+    RDD_CUDA(cudaMemcpyAsync(dst, buf[k], bytes, cudaMemcpyHostToDevice, s));
+    RDD_CUDA(cudaEventRecord(ev[k], s));
+    used[k] = true;
+    h2d_counter() += static_cast<int64_t>(bytes);
+  }
 };
 
 struct Ctx {
@@ -214,6 +250,7 @@ struct Ctx {
   std::map<std::string, DBuf<double>> wsd;
   double* ws(const std::string& name, size_t count) { return wsd[name].ensure(count > 0 ? count : 1); }
   cudaEvent_t ev[8] = {nullptr};
+  PinnedStage stage;                  // task-list uploads (gemm.cu)
 };
 
 // timing helper: records device time of a kernel family when ctx.timing is on

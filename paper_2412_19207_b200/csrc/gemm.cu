@@ -261,7 +261,8 @@ void launch(Ctx& c, const std::vector<GemmTask>& tasks, const char* fam) {
   if (tasks.empty()) return;
   ScopedKernelTimer tk(c, fam);
   DBuf<GemmTask> d;
-  d.upload(tasks, c.stream);
+  d.ensure(tasks.size());
+  c.stage.upload(d.p, tasks.data(), tasks.size() * sizeof(GemmTask), c.stream);
   // grid.x limit is 2^31-1; tasks are far fewer
   constexpr size_t smem = gemm_smem(GemmCfg<AT>::stages);
   ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<AT, BT>), smem);
@@ -276,7 +277,8 @@ void gemm_nn_wide(Ctx& c, const std::vector<GemmTask>& tasks) {
   if (tasks.empty()) return;
   ScopedKernelTimer tk(c, "gemm_nn");
   DBuf<GemmTask> d;
-  d.upload(tasks, c.stream);
+  d.ensure(tasks.size());
+  c.stage.upload(d.p, tasks.data(), tasks.size() * sizeof(GemmTask), c.stream);
   ensure_smem_attr(reinterpret_cast<const void*>(k_gemm_nn_wide), kWideSmem);
   k_gemm_nn_wide<<<static_cast<unsigned>(tasks.size()), WNT, kWideSmem, c.stream>>>(d.p);
   RDD_LAUNCH_CHECK();

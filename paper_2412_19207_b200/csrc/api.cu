@@ -118,7 +118,7 @@ static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed, bool reside
   }
   RDD_CUDA(cudaStreamSynchronize(c.stream));
   const double t_pca = now_s() - t0;
-  if (c.verbose) std::fprintf(stderr, "[phase] instance+pca %.3f s (J=%d p=%d N=%d)\n", t_pca, c.J, c.p, c.N);
+  if (c.verbose) std::fprintf(stderr, "[phase] instance+pca %.3f s (J=%d p=%d N=%d) upload-wait %.3f s\n", t_pca, c.J, c.p, c.N, upload_wait_s());
   assemble(c, cfg.precond >= 0);
   const double t_asm = now_s() - t0;
   if (c.verbose) std::fprintf(stderr, "[phase] assemble done %.3f s\n", t_asm);
@@ -134,7 +134,7 @@ static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed, bool reside
     build_schwarz(c, cfg.precond, &x);
     RDD_CUDA(cudaStreamSynchronize(c.stream));
     t_pre = now_s() - t0;
-    if (c.verbose) std::fprintf(stderr, "[phase] precond %.3f s (fallback %d)\n", t_pre, c.n_fallback);
+    if (c.verbose) std::fprintf(stderr, "[phase] precond %.3f s (fallback %d) upload-wait %.3f s\n", t_pre, c.n_fallback, upload_wait_s());
   } else if (cfg.op_form == RDD_OPERATOR_NORMAL) {
     build_normal_blocks(c);
   }
@@ -142,7 +142,7 @@ static void run_single(Ctx& c, const rdd_config& cfg, uint64_t seed, bool reside
   if (cfg.solver == RDD_SOLVER_QR) qr_solve_dev(c);
   else solve_all(c, cfg.solver, cfg.rel_tol, cfg.max_iter, cfg.gmres_restart);
   const double t_sol = now_s() - t0;
-  if (c.verbose) std::fprintf(stderr, "[phase] solve %.3f s (%d its)\n", t_sol, c.iters.empty() ? 0 : c.iters[0]);
+  if (c.verbose) std::fprintf(stderr, "[phase] solve %.3f s (%d its) upload-wait %.3f s\n", t_sol, c.iters.empty() ? 0 : c.iters[0], upload_wait_s());
   t0 = now_s();
   if (c.prob.id != 0) evaluate(c, cfg.test);  // caller problems evaluate at caller points (evaluate_at)
   const double t_ev = now_s() - t0;

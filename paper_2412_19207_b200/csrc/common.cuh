@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -92,6 +93,12 @@ template <class T>
 using pinned_vector = std::vector<T, PinnedAlloc<T>>;
 
 // Owning device buffer (pooled, stream-ordered; grows, never shrinks).
+// host seconds spent inside DBuf::upload (pageable copies may wait for the stream): diagnostics
+inline double& upload_wait_s() {
+  static thread_local double t = 0.0;
+  return t;
+}
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -121,7 +128,9 @@ struct DBuf {
   }
   void upload(const T* h, size_t count, cudaStream_t s) {
     ensure(count);
+    const auto t0 = std::chrono::steady_clock::now();
     if (count) RDD_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    upload_wait_s() += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     h2d_counter() += static_cast<int64_t>(count * sizeof(T));
   }
   template <class Alloc>

@@ -43,7 +43,8 @@ def test_sm100a_code_only(built):
 def test_dmma_in_gemm_sass(built):
     out = subprocess.run(["cuobjdump", "-sass", built], capture_output=True, text=True).stdout
     gemm = [blk for blk in out.split("Function :") if "k_gemm" in blk.split("\n")[0]]
-    assert len(gemm) == 3 and all("DMMA" in blk for blk in gemm)
+    # NN / NT / TN at 64x64 tiles and the 64x128-tile NN variant
+    assert len(gemm) >= 3 and all("DMMA" in blk for blk in gemm)
 
 
 def test_fails_loudly_without_device(built):

@@ -817,28 +817,22 @@ void check_dense_cap(long long n, int cap) {  // krylov.hpp:405-409
 
 static void hqr_block(Ctx& c, double* A, long long ld, int nb, double* wr, double* wi, int* st, bool smem) {
   const size_t sm = smem ? sizeof(double) * nb * nb : 0;
-  static bool attr = false;
-  if (!attr) {
-    RDD_CUDA(cudaFuncSetAttribute(k_hqr, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(double) * kMsKW * kMsKW)));
-    attr = true;
-  }
+  // set on every call: the attribute is per device, and a context may live on any device
+  RDD_CUDA(cudaFuncSetAttribute(k_hqr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(double) * kMsKW * kMsKW)));
   k_hqr<<<1, smem ? 32 : kQRT, sm, c.stream>>>(A, ld, nb, wr, wi, st, 60, smem ? 1 : 0);
   RDD_LAUNCH_CHECK();
 }
 
 // one multi-bulge sweep over the active block [l, nn] with nbul bulges (shift pairs in td)
 static void ms_sweep(Ctx& c, double* A, int n, int l, int nn, int nbul, const double* td, double* U) {
-  static bool attr = false;
-  if (!attr) {
-    RDD_CUDA(cudaFuncSetAttribute(k_ms_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(double) * 2 * kMsKW * (kMsKW + 1))));
-    RDD_CUDA(cudaFuncSetAttribute(k_ms_right, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(double) * (kMsKW * (kMsKW + 1) + kMsKW * 16))));
-    RDD_CUDA(cudaFuncSetAttribute(k_ms_top, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(double) * (kMsKW * kMsKW + 32 * kMsKW))));
-    attr = true;
-  }
+  // per call (per device), as hqr_block
+  RDD_CUDA(cudaFuncSetAttribute(k_ms_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(double) * 2 * kMsKW * (kMsKW + 1))));
+  RDD_CUDA(cudaFuncSetAttribute(k_ms_right, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(double) * (kMsKW * (kMsKW + 1) + kMsKW * 16))));
+  RDD_CUDA(cudaFuncSetAttribute(k_ms_top, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(double) * (kMsKW * kMsKW + 32 * kMsKW))));
   const int S = 3 * (nbul - 1), T = (nn - l) + S, steps = kMsKW - S - 4;
   for (int tA = 0; tA < T;) {
     const int tB = std::min(T, tA + steps);

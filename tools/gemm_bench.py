@@ -16,6 +16,8 @@ SHAPES = [  # (name, mode, M, N, K, batch)
     ("tn gram 400x400 k13800", 1, 400, 400, 13824, 64),
     ("nn S·Q 13800x386 k400", 0, 13824, 386, 400, 32),
     ("tn 300x300 k5184 (C2 gram)", 1, 300, 300, 5184, 256),
+    ("tn 400x386 k13824 (C5 refine Sᵀ·Y)", 1, 400, 386, 13824, 64),
+    ("nn 13824x213 k400 (C5 projection)", 0, 13824, 213, 400, 32),
     ("nn 1024^3", 0, 1024, 1024, 1024, 16),
 ]
 

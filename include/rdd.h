@@ -226,6 +226,9 @@ int rdd_set_verbose(rdd_ctx* ctx, int on);  /* phase times and solver diagnostic
                        (default in DESIGN.md §4 K8; 0 routes every block to the eigen path).
      "pca_refine"      subspace-refinement steps Y = Sᵀ(S·V) of the PCA (DESIGN §4 K4a;
                        0 = automatic).
+     "pca_stop"        stop of the PCA's pivoted Cholesky relative to its first pivot (1e-17).
+     "inv_max"         largest local order n_i kept as an explicit packed inverse (default 1024;
+                       0 = every block through the envelope-packed Cholesky factor).
    Takes effect at the next rdd_build_preconditioner. RDD_INVALID_ARGUMENT for unknown names. */
 int rdd_set_param(rdd_ctx* ctx, const char* name, double value);
 /* Time `reps` calls of the normal operator on device-resident vectors (CUDA events). */

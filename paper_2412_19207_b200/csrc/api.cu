@@ -270,6 +270,14 @@ int rdd_set_param(rdd_ctx* h, const char* name, double value) {
     h->c.pca_refine = static_cast<int>(value);
     return RDD_OK;
   }
+  if (n == "inv_max" && value >= 0.0 && value <= 1024.0) {
+    h->c.inv_max = static_cast<int>(value);
+    return RDD_OK;
+  }
+  if (n == "pca_stop" && value >= 0.0 && value < 1.0) {
+    h->c.pca_stop = value;
+    return RDD_OK;
+  }
   h->c.err = "rdd_set_param: unknown parameter or bad value: " + n;
   return RDD_INVALID_ARGUMENT;
 }
@@ -509,6 +517,10 @@ int64_t rdd_get_i(rdd_ctx* h, const char* what, int index, int32_t* out, int64_t
     else if (w == "maxcov") v = {c.maxcov};
     else if (w == "n_fallback") v = {c.n_fallback};
     else if (w == "qr_rank") v = {c.qr_rank};
+    else if (w == "inv_mode") v = {c.inv_mode ? 1 : 0};
+    else if (w == "env_first") {  // first stored tile of every block row of subdomain `index`'s factor
+      v.assign(c.env_first.begin() + c.env_off.at(index), c.env_first.begin() + c.env_off.at(index + 1));
+    }
     else if (w == "p_j") v = c.h_p;
     else if (w == "col_off") v = c.h_col_off;
     else if (w == "rows") {
@@ -735,9 +747,13 @@ int rdd_bench_precond(rdd_ctx* h, int transpose, int reps, double* ms_per_call, 
       const double n = c.set_ptr[i + 1] - c.set_ptr[i];
       const bool dense = std::binary_search(c.fallback.begin(), c.fallback.end(), i);
       const double tri = n * (n + 1) / 2.0;
-      b += 8.0 * (dense ? n * n : (c.inv_mode ? tri : 2.0 * tri));
+      b += 8.0 * (dense ? n * n : (c.inv_mode ? tri : 0.0));
       b += 8.0 * 2.0 * n + 4.0 * n;
     }
+    // factor mode: the entries inside the envelopes of the lower triangles (structural zeros left of
+    // a row's first nonzero block are not stored), read by the forward and the backward solve; the
+    // few eigen-fallback blocks are counted dense above and not subtracted here
+    if (!c.inv_mode) b += 2.0 * 8.0 * c.env_entries;
     b += 8.0 * static_cast<double>(c.set_idx.size()) + 4.0 * static_cast<double>(c.set_idx.size()) + 8.0 * c.p;
     *bytes_per_call = b;
   });
@@ -745,7 +761,9 @@ int rdd_bench_precond(rdd_ctx* h, int transpose, int reps, double* ms_per_call, 
 
 int rdd_bench_gemm(rdd_ctx* h, int mode, int M, int N, int K, int batch, int reps, double* ms_out) {
   return guarded(h, [&](Ctx& c) {
-    if (M < 1 || N < 1 || K < 1 || batch < 1 || reps < 1 || mode < 0 || mode > 2)
+    const int tile = mode >= 10 ? 80 : 64;  // mode + 10: the 80-wide CTA tile (NN and TN)
+    mode %= 10;
+    if (M < 1 || N < 1 || K < 1 || batch < 1 || reps < 1 || mode < 0 || mode > 2 || (tile == 80 && mode == 2))
       throw std::invalid_argument("bench_gemm: bad shape");
     const size_t sa = static_cast<size_t>(M) * K, sb = static_cast<size_t>(K) * N, sc = static_cast<size_t>(M) * N;
     rdd::DBuf<double> A, B, Cm;
@@ -756,8 +774,8 @@ int rdd_bench_gemm(rdd_ctx* h, int mode, int M, int N, int K, int batch, int rep
     RDD_CUDA(cudaMemsetAsync(B.p, 0, sizeof(double) * sb * batch, c.stream));
     std::vector<rdd::GemmTask> tasks;
     for (int b = 0; b < batch; ++b)
-      for (int tm = 0; tm < (M + 63) / 64; ++tm)
-        for (int tn = 0; tn < (N + 63) / 64; ++tn) {
+      for (int tm = 0; tm < (M + tile - 1) / tile; ++tm)
+        for (int tn = 0; tn < (N + tile - 1) / tile; ++tn) {
           rdd::GemmTask t{};
           t.A = A.p + sa * b;
           t.B = B.p + sb * b;
@@ -775,8 +793,8 @@ int rdd_bench_gemm(rdd_ctx* h, int mode, int M, int N, int K, int batch, int rep
           tasks.push_back(t);
         }
     auto run = [&] {
-      if (mode == 0) rdd::gemm_nn(c, tasks);
-      else if (mode == 1) rdd::gemm_tn(c, tasks);
+      if (mode == 0) rdd::gemm_nn(c, tasks, tile);
+      else if (mode == 1) rdd::gemm_tn(c, tasks, tile);
       else rdd::gemm_nt(c, tasks);
     };
     run();

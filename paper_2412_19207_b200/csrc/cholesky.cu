@@ -90,16 +90,19 @@ __global__ void k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mat
 }
 
 
-// Block row k of the tile-packed factor: tiles (k, j<k) copied from the factored matrix (zero
-// padding past n) and the diagonal tile D_k = L_kk⁻¹ from the workspace. task = (matrix, k)
+// Block row k of the tile-packed factor: tiles (k, first_k <= j < k) copied from the factored matrix
+// (zero padding past n) and the diagonal tile D_k = L_kk⁻¹ from the workspace. task = (matrix, k);
+// ef/eb: the matrix's envelope (first tile and packed base of every block row, at eoff[matrix])
 __global__ void k_pack_row(const double* __restrict__ A, const Mat* __restrict__ mats, const int2* __restrict__ tasks,
                            double* __restrict__ P, const long long* __restrict__ poff, const double* __restrict__ Dinv,
-                           const long long* __restrict__ doff) {
+                           const long long* __restrict__ doff, const int* __restrict__ eoff,
+                           const int* __restrict__ efirst, const int* __restrict__ ebase) {
   const int2 t = tasks[blockIdx.x];
   const Mat M = mats[t.x];
   const int k = t.y, k0 = k * NB, bs = min(NB, M.n - k0);
-  double* row = P + poff[t.x] + static_cast<long long>(k) * (k + 1) / 2 * (NB * NB);
-  for (int j = 0; j < k; ++j) {
+  const int f = efirst[eoff[t.x] + k];
+  double* row = P + poff[t.x] + static_cast<long long>(ebase[eoff[t.x] + k]) * (NB * NB);  // tile (k, j) at row + j·64²
+  for (int j = f; j < k; ++j) {
     const double* a = A + M.off + k0 + static_cast<long long>(j * NB) * M.n;
     double* o = row + static_cast<long long>(j) * NB * NB;
     for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
@@ -224,9 +227,16 @@ __global__ void k_power(const double* __restrict__ A, const Mat* __restrict__ ma
 struct UpdDesc {
   long long off;   // matrix offset
   long long first; // first task index of this entry
-  int n, k, ostart, oend, kind, pad;
+  int n, k, ostart, oend, kind;
+  int nbk;         // block rows to enumerate: one past the last row whose envelope reaches the step
   const double* D; // kind 2: D_k
+  const int* ef;   // the matrix's envelope: first tile of every block row
 };
+// Envelope: a block row ib whose first tile lies right of the step's columns holds zeros there, so
+// its panel solve and its updates (as row or as column of the updated tile) are skipped — the
+// candidates are enumerated densely over the first nbk block rows and the skipped ones become
+// empty tasks (M = 0: the GEMM CTA exits). After an outer panel the K range of an update starts at
+// the later of the two rows' first tiles.
 __global__ void k_make_updates(double* __restrict__ A, const UpdDesc* __restrict__ d, int nd, long long total,
                                GemmTask* __restrict__ out) {
   const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -239,7 +249,7 @@ __global__ void k_make_updates(double* __restrict__ A, const UpdDesc* __restrict
   }
   const UpdDesc e = d[lo];
   long long loc = t - e.first;
-  const int nb = (e.n + NB - 1) / NB;
+  const int nb = e.nbk;
   double* base = A + e.off;
   GemmTask g{};
   g.gA = g.gB = nullptr;
@@ -249,7 +259,7 @@ __global__ void k_make_updates(double* __restrict__ A, const UpdDesc* __restrict
     g.A = base + ib * NB + static_cast<long long>(k0) * e.n;
     g.B = e.D;
     g.Cm = base + ib * NB + static_cast<long long>(k0) * e.n;
-    g.M = min(NB, e.n - ib * NB);
+    g.M = e.ef[ib] <= e.k ? min(NB, e.n - ib * NB) : 0;
     g.N = g.K = min(NB, e.n - k0);
     g.lda = g.ldc = e.n;
     g.ldb = NB;
@@ -259,7 +269,7 @@ __global__ void k_make_updates(double* __restrict__ A, const UpdDesc* __restrict
     return;
   }
   const int jb0 = e.kind == 0 ? e.k + 1 : e.oend;
-  const int jb1 = e.kind == 0 ? e.oend : nb;  // exclusive
+  const int jb1 = e.kind == 0 ? min(e.oend, nb) : nb;  // exclusive
   int jb = jb0;
   for (; jb < jb1; ++jb) {  // column jb holds rows ib = jb .. nb-1
     const long long cnt = nb - jb;
@@ -267,12 +277,16 @@ __global__ void k_make_updates(double* __restrict__ A, const UpdDesc* __restrict
     loc -= cnt;
   }
   const int ib = jb + static_cast<int>(loc);
-  const int c0 = e.kind == 0 ? e.k * NB : e.ostart * NB;
+  const int last = e.kind == 0 ? e.k : e.oend - 1;  // last tile column of the step's K range
+  const int fi = e.ef[ib], fj = e.ef[jb];
+  const bool live = fi <= last && fj <= last;
+  const int cb = e.kind == 0 ? e.k : max(e.ostart, max(fi, fj));
+  const int c0 = cb * NB;
   const int kw = e.kind == 0 ? min(NB, e.n - c0) : min(e.n, e.oend * NB) - c0;
   g.A = base + ib * NB + static_cast<long long>(c0) * e.n;
   g.B = base + jb * NB + static_cast<long long>(c0) * e.n;
   g.Cm = base + ib * NB + static_cast<long long>(jb) * NB * e.n;
-  g.M = min(NB, e.n - ib * NB);
+  g.M = live ? min(NB, e.n - ib * NB) : 0;
   g.N = min(NB, e.n - jb * NB);
   g.K = kw;
   g.lda = g.ldb = g.ldc = e.n;
@@ -282,20 +296,25 @@ __global__ void k_make_updates(double* __restrict__ A, const UpdDesc* __restrict
 }
 
 // ---- batched solves with the tile-packed factor ---------------------------------------------
-__device__ __forceinline__ const double* ptile(const double* P, int k, int j) {
-  return P + (static_cast<long long>(k) * (k + 1) / 2 + j) * (NB * NB);
+// tile (k, j) of a packed factor whose block row k starts at packed tile base eb[k] + ef[k]
+__device__ __forceinline__ const double* ptile(const double* P, const int* eb, int k, int j) {
+  return P + static_cast<long long>(eb[k] + j) * (NB * NB);
 }
 
 // v <- (L Lᵀ)⁻¹ v in shared memory (nb*64 entries, zero-padded past n); red: kSolveWarps*64.
-// Forward y_k = L_kk⁻¹ (v_k - Σ_{j<k} L_kj y_j), backward x_k = L_kk⁻ᵀ (y_k - Σ_{j>k} L_jkᵀ x_j).
-// Off-diagonal tiles are split over the warps (fixed order), each tile column streamed as one
-// 512-byte warp load; the transposed tiles of the backward pass reduce 32 columns per 31 shuffles.
-__device__ void chol_solve(const double* __restrict__ P, int nb, double* v, double* red) {
+// ef/eb: the factor's envelope (block row k holds tiles ef[k]..k).
+// Forward (row by row) y_k = L_kk⁻¹ (v_k - Σ_{ef[k] <= j < k} L_kj y_j); backward, also row by row so
+// that each block row is one contiguous stream: for k = nb-1..0, x_k = L_kk⁻ᵀ y_k, then
+// y_j -= L_kjᵀ x_k for ef[k] <= j < k. Off-diagonal tiles are split over the warps, each tile column
+// streamed as one 512-byte warp load; the transposed tiles of the backward pass reduce 32 columns
+// per 31 shuffles and each is applied by its one warp (distinct j: no cross-warp sum).
+__device__ void chol_solve(const double* __restrict__ P, int nb, double* v, double* red, const int* __restrict__ ef,
+                           const int* __restrict__ eb) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   for (int k = 0; k < nb; ++k) {
     double a0 = 0.0, a1 = 0.0;
-    for (int j = warp; j < k; j += kSolveWarps) {
-      const double2* t = reinterpret_cast<const double2*>(ptile(P, k, j)) + lane;
+    for (int j = ef[k] + warp; j < k; j += kSolveWarps) {
+      const double2* t = reinterpret_cast<const double2*>(ptile(P, eb, k, j)) + lane;
       const double* y = v + j * NB;
 #pragma unroll 16
       for (int c = 0; c < NB; ++c) {
@@ -314,7 +333,7 @@ __device__ void chol_solve(const double* __restrict__ P, int nb, double* v, doub
     }
     __syncthreads();
     {
-      const double2* t = reinterpret_cast<const double2*>(ptile(P, k, k)) + lane;
+      const double2* t = reinterpret_cast<const double2*>(ptile(P, eb, k, k)) + lane;
       const double* r = v + k * NB;
       double b0 = 0.0, b1 = 0.0;
 #pragma unroll
@@ -335,10 +354,24 @@ __device__ void chol_solve(const double* __restrict__ P, int nb, double* v, doub
     __syncthreads();
   }
   for (int k = nb - 1; k >= 0; --k) {
-    double a0 = 0.0, a1 = 0.0;  // columns lane, lane + 32 of block k
-    for (int j = k + 1 + warp; j < nb; j += kSolveWarps) {
-      const double* t = ptile(P, j, k);
-      const double x0 = v[j * NB + 2 * lane], x1 = v[j * NB + 2 * lane + 1];
+    double mine = 0.0;  // x_k = D_kᵀ y_k: this warp's NB/kSolveWarps columns of the diagonal tile
+    {
+      const double* t = ptile(P, eb, k, k);
+      const double r0 = v[k * NB + 2 * lane], r1 = v[k * NB + 2 * lane + 1];
+      constexpr int CW = NB / kSolveWarps;
+#pragma unroll
+      for (int cc = 0; cc < CW; ++cc) {
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(t + (warp * CW + cc) * NB) + lane);
+        const double s = warp_sum(a.x * r0 + a.y * r1);
+        if (lane == cc) mine = s;
+      }
+    }
+    __syncthreads();
+    if (lane < NB / kSolveWarps) v[k * NB + warp * (NB / kSolveWarps) + lane] = mine;
+    __syncthreads();
+    const double x0 = v[k * NB + 2 * lane], x1 = v[k * NB + 2 * lane + 1];
+    for (int j = ef[k] + warp; j < k; j += kSolveWarps) {  // y_j -= L_kjᵀ x_k
+      const double* t = ptile(P, eb, k, j);
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
         double p[32];
@@ -357,33 +390,9 @@ __device__ void chol_solve(const double* __restrict__ P, int nb, double* v, doub
             p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
           }
         }
-        if (g == 0) a0 += p[0];
-        else a1 += p[0];
+        v[j * NB + g * 32 + lane] -= p[0];
       }
     }
-    red[warp * NB + lane] = a0;
-    red[warp * NB + 32 + lane] = a1;
-    __syncthreads();
-    if (tid < NB) {
-      double s = v[k * NB + tid];
-      for (int w = 0; w < kSolveWarps; ++w) s -= red[w * NB + tid];
-      v[k * NB + tid] = s;
-    }
-    __syncthreads();
-    double mine = 0.0;
-    {
-      const double* t = ptile(P, k, k);
-      const double r0 = v[k * NB + 2 * lane], r1 = v[k * NB + 2 * lane + 1];
-      constexpr int CW = NB / kSolveWarps;
-#pragma unroll
-      for (int cc = 0; cc < CW; ++cc) {
-        const double2 a = __ldcs(reinterpret_cast<const double2*>(t + (warp * CW + cc) * NB) + lane);
-        const double s = warp_sum(a.x * r0 + a.y * r1);
-        if (lane == cc) mine = s;
-      }
-    }
-    __syncthreads();
-    if (lane < NB / kSolveWarps) v[k * NB + warp * (NB / kSolveWarps) + lane] = mine;
     __syncthreads();
   }
 }
@@ -457,7 +466,10 @@ __device__ void symv_packed(const double* __restrict__ P, int nb, double* v, dou
 __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_power(const double* __restrict__ P,
                                                                  const long long* __restrict__ poff,
                                                                  const int* __restrict__ nvec, int iters, int nbmax,
-                                                                 double* __restrict__ out, int inverse) {
+                                                                 double* __restrict__ out, int inverse,
+                                                                 const int* __restrict__ eoff,
+                                                                 const int* __restrict__ efirst,
+                                                                 const int* __restrict__ ebase) {
   extern __shared__ double sm[];
   double* x = sm;
   double* red = sm + static_cast<size_t>(nbmax) * NB;  // solve: kSolveWarps*64; symv: kSolveWarps*nbmax*64
@@ -484,7 +496,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_power(const double* _
     for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] /= nrm;
     __syncthreads();
     if (inverse) symv_packed(P + poff[i], nb, x, red);
-    else chol_solve(P + poff[i], nb, x, red);
+    else chol_solve(P + poff[i], nb, x, red, efirst + eoff[i], ebase + eoff[i]);
   }
   if (threadIdx.x == 0) out[i] = lam;
 }
@@ -520,9 +532,10 @@ std::vector<double> batched_power(Ctx& c, const double* A, const std::vector<int
 // In: A (batch at off[i], order n[i], symmetric, full storage) — destroyed (holds L).
 // Out: the tile-packed factor at P + poff[i] (diagonal tiles inverted), fail[i] = 1 when a pivot
 // was not positive, frob_A[i] = ‖A_i‖_F (an upper bound of λmax).
-void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const std::vector<long long>& off, double* P,
-                           const std::vector<long long>& poff, std::vector<int>& fail, std::vector<double>& frob_A,
-                           bool inverse, std::vector<double>* frob_P, double** Pfull_out) {
+void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& ids, const std::vector<int>& n,
+                           const std::vector<long long>& off, double* P, const std::vector<long long>& poff,
+                           std::vector<int>& fail, std::vector<double>& frob_A, bool inverse,
+                           std::vector<double>* frob_P, double** Pfull_out) {
   ScopedKernelTimer tk(c, "cholesky");
   const int B = static_cast<int>(n.size());
   fail.assign(B, 0);
@@ -583,20 +596,38 @@ void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const s
       if (k >= nb) continue;
       act.push_back(i);
       const int oend = std::min(nb, ostart + kOuter);
-      if (nb - k - 1 > 0) {  // panel solve
-        sd.push_back({off[i], stotal, n[i], k, ostart, oend, 2, 0, Dinv + doff[i] + static_cast<long long>(k) * NB * NB});
-        stotal += nb - k - 1;
+      const int* efh = c.env_first.data() + c.env_off[ids[i]];
+      const int* efd = c.denv_first.p + c.env_off[ids[i]];
+      // block rows whose envelope reaches column k (the step's panel solve and K = 64 updates)
+      int nbk = k + 1;
+      for (int ib = nb - 1; ib > k; --ib)
+        if (efh[ib] <= k) {
+          nbk = ib + 1;
+          break;
+        }
+      if (nbk - k - 1 > 0) {  // panel solve
+        sd.push_back({off[i], stotal, n[i], k, ostart, oend, 2, nbk,
+                      Dinv + doff[i] + static_cast<long long>(k) * NB * NB, efd});
+        stotal += nbk - k - 1;
       }
       long long cnt = 0;
-      for (int jb = k + 1; jb < oend; ++jb) cnt += nb - jb;
+      for (int jb = k + 1; jb < std::min(oend, nbk); ++jb) cnt += nbk - jb;
       if (cnt > 0) {
-        ud.push_back({off[i], utotal, n[i], k, ostart, oend, 0, 0, nullptr});
+        ud.push_back({off[i], utotal, n[i], k, ostart, oend, 0, nbk, nullptr, efd});
         utotal += cnt;
       }
-      if (k == oend - 1 && oend < nb) {
-        const long long T = nb - oend;
-        ud.push_back({off[i], utotal, n[i], k, ostart, oend, 1, 0, nullptr});
-        utotal += T * (T + 1) / 2;
+      if (k == oend - 1 && oend < nb) {  // the completed outer panel's K = 512 update of the trailing matrix
+        int nbo = oend;
+        for (int ib = nb - 1; ib >= oend; --ib)
+          if (efh[ib] < oend) {
+            nbo = ib + 1;
+            break;
+          }
+        const long long T = nbo - oend;
+        if (T > 0) {
+          ud.push_back({off[i], utotal, n[i], k, ostart, oend, 1, nbo, nullptr, efd});
+          utotal += T * (T + 1) / 2;
+        }
       }
     }
     st.nact = act.size() - st.act0;
@@ -640,7 +671,12 @@ void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const s
   drows.upload(rows, c.stream);
   dpoff.upload(poff, c.stream);
   if (!inverse) {
-    k_pack_row<<<static_cast<int>(rows.size()), 256, 0, c.stream>>>(A, dm.p, drows.p, P, dpoff.p, Dinv, ddoff.p);
+    std::vector<int> eo(B);
+    for (int i = 0; i < B; ++i) eo[i] = c.env_off[ids[i]];
+    DBuf<int> deo;
+    deo.upload(eo, c.stream);
+    k_pack_row<<<static_cast<int>(rows.size()), 256, 0, c.stream>>>(A, dm.p, drows.p, P, dpoff.p, Dinv, ddoff.p, deo.p,
+                                                                     c.denv_first.p, c.denv_base.p);
     RDD_LAUNCH_CHECK();
   } else {
     // explicit inverse for small blocks: M = L⁻¹ by block rows (M_kk = D_k,
@@ -744,7 +780,7 @@ size_t chol_solve_smem(int nmax, bool inverse) {
   return (len + (inverse ? kSolveWarps * len : kSolveWarps * NB)) * sizeof(double);
 }
 
-std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector<int>& n,
+std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector<int>& ids, const std::vector<int>& n,
                                       const std::vector<long long>& poff, int iters, bool inverse) {
   ScopedKernelTimer tk(c, "inv_power");
   const int B = static_cast<int>(n.size());
@@ -755,13 +791,15 @@ std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector
   std::vector<int> perm(B);
   for (int b = 0; b < B; ++b) perm[b] = b;
   std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return n[a] > n[b]; });
-  std::vector<int> ns(B);
+  std::vector<int> ns(B), eo(B);
   std::vector<long long> ps(B);
   for (int b = 0; b < B; ++b) {
     ns[b] = n[perm[b]];
     ps[b] = poff[perm[b]];
+    eo[b] = c.env_off[ids[perm[b]]];
   }
-  DBuf<int> dn;
+  DBuf<int> dn, deo;
+  deo.upload(eo, c.stream);
   DBuf<long long> dp;
   DBuf<double> d;
   dn.upload(ns, c.stream);
@@ -771,7 +809,7 @@ std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector
   if (c.verbose) std::fprintf(stderr, "[inv_power] B=%d nmax=%d smem=%zu iters=%d\n", B, nmax, smem, iters);
   RDD_CUDA(cudaFuncSetAttribute(k_chol_power, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   k_chol_power<<<B, kSolveWarps * 32, smem, c.stream>>>(P, dp.p, dn.p, iters, ceil_div(nmax, NB), d.p,
-                                                        inverse ? 1 : 0);
+                                                        inverse ? 1 : 0, deo.p, c.denv_first.p, c.denv_base.p);
   RDD_LAUNCH_CHECK();
   std::vector<double> sorted(B);
   d.download(sorted.data(), B, c.stream);
@@ -788,7 +826,8 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
     const int* __restrict__ set_ptr, const int* __restrict__ set_idx, const double* __restrict__ v,
     const int* __restrict__ mult, const int* __restrict__ owner, int kind, int transpose, int nbmax,
     double* __restrict__ z, int inverse, long long zhalf, const int* __restrict__ live,
-    const int* __restrict__ order) {
+    const int* __restrict__ order, const int* __restrict__ eoff, const int* __restrict__ efirst,
+    const int* __restrict__ ebase) {
   if (live && *live != 0) return;  // solver loop already stopped (speculative graph iteration)
   extern __shared__ double sm[];
   double* g = sm;
@@ -825,7 +864,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
     return;
   }
   if (inverse) symv_packed(P + poff[i], nb, g, red, h, 2);
-  else chol_solve(P + poff[i], nb, g, red);
+  else chol_solve(P + poff[i], nb, g, red, efirst + eoff[i], ebase + eoff[i]);
   for (int r = threadIdx.x; r < n; r += blockDim.x) zo[s0 + r] = g[r];
 }
 
@@ -1017,7 +1056,8 @@ void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
   ensure_smem_attr(reinterpret_cast<const void*>(k_chol_apply), smem);
   k_chol_apply<<<c.J, kSolveWarps * 32, smem, c.stream>>>(
       c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p, v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
-      ceil_div(c.nmax_local, NB), zloc, 0, static_cast<long long>(c.set_idx.size()), c.live, c.apply_order.p);
+      ceil_div(c.nmax_local, NB), zloc, 0, static_cast<long long>(c.set_idx.size()), c.live, c.apply_order.p,
+      c.denv_off.p, c.denv_first.p, c.denv_base.p);
   RDD_LAUNCH_CHECK();
 }
 
@@ -1050,7 +1090,8 @@ __global__ void k_ras_panel(const double* __restrict__ P, const long long* __res
         a = b;
         b = t;
       }
-      v = ptile(Pi, a / NB, b / NB)[(a % NB) + (b % NB) * NB];
+      const int tk = a / NB, tj = b / NB;  // dense packing of the explicit inverse
+      v = (Pi + (static_cast<long long>(tk) * (tk + 1) / 2 + tj) * (NB * NB))[(a % NB) + (b % NB) * NB];
     }
     Ri[e] = v;
   }

@@ -185,6 +185,16 @@ struct Ctx {
   DBuf<double> P;
   DBuf<int> dset_ptr, dset_idx, dmult, downer;
   DBuf<long long> dP_off;
+  // envelope (skyline) of the tile-packed factors: block row k of A_i's factor holds the tiles
+  // env_first[k]..k. The blocks of A_i that pair two neighbours of i which do not overlap each
+  // other are exact zeros, and Cholesky does not fill in left of a row's first nonzero, so those
+  // tiles are neither computed, stored nor read. Tile (k, j) of subdomain i lives at
+  // P_off[i] + (env_base[k] + j)·64²; both arrays are indexed at env_off[i] + k. The packed
+  // explicit inverses (inv_mode) are dense: first = 0, base = k(k+1)/2.
+  std::vector<int> env_off, env_first, env_base;
+  DBuf<int> denv_off, denv_first, denv_base;
+  double env_entries = 0.0;           // Σ_i scalar entries inside the envelopes of the lower triangles
+  int inv_max = 1024;                 // largest local order kept as an explicit inverse ("inv_max" parameter)
   // owner-gather map for the AS/SAS reduction: per column c, list of (i, position)
   DBuf<int> gat_ptr, gat_pos, gat_owner_pos;
   int nmax_local = 0;
@@ -202,6 +212,7 @@ struct Ctx {
   };
   std::vector<GatherTask> gat_tasks;
   int pca_refine = 0;                 // subspace-refinement steps of the PCA (0 = automatic)
+  double pca_stop = 1e-17;            // pivoted-Cholesky stop of PCA stage 1, relative to the first pivot (λ scale)
   double full_rank_cond = 1e9;        // Cholesky path when cond_est(A_i) is below this (DESIGN §4 K8)
   DBuf<double> zloc;                  // Σ n_i
   // RAS owner-row panels (small blocks): per i the rows of A_i⁻¹ that subdomain i owns
@@ -330,20 +341,23 @@ void evaluate(Ctx& c, const int* test_res);
 void evaluate_at(Ctx& c, long long M, const double* pts, const double* W, const double* Lv, const double* Gv,
                  double* out);
 // gemm.cu
-void gemm_tn(Ctx& c, const std::vector<GemmTask>& tasks);  // C = Aᵀ B (A: K x M, B: K x N col-major)
-void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks);  // C = A B  (A: M x K, B: K x N col-major)
+// tile = CTA tile edge, 64 or 80: the tasks' (tm, tn) count tiles of that size
+void gemm_tn(Ctx& c, const std::vector<GemmTask>& tasks, int tile = 64);  // C = Aᵀ B (A: K x M, B: K x N col-major)
+void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks, int tile = 64);  // C = A B  (A: M x K, B: K x N col-major)
 void gemm_nn_wide(Ctx& c, const std::vector<GemmTask>& tasks);  // same, 64 x 128 tiles (tn in units of 128)
 void gemm_nt(Ctx& c, const std::vector<GemmTask>& tasks);
 void gemm_nt_dev(Ctx& c, const GemmTask* tasks, int count);  // C = A Bᵀ (A: M x K, B: N x K col-major)
 void project_blocks(Ctx& c);
 void ensure_col_owner(Ctx& c);
 // cholesky.cu
-void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& n, const std::vector<long long>& off, double* P,
-                           const std::vector<long long>& poff, std::vector<int>& fail, std::vector<double>& frob_A,
-                           bool inverse = false, std::vector<double>* frob_P = nullptr, double** Pfull_out = nullptr);
+// ids: the subdomain of every batch entry (its envelope: c.env_*)
+void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& ids, const std::vector<int>& n,
+                           const std::vector<long long>& off, double* P, const std::vector<long long>& poff,
+                           std::vector<int>& fail, std::vector<double>& frob_A, bool inverse = false,
+                           std::vector<double>* frob_P = nullptr, double** Pfull_out = nullptr);
 long long packed_chol_size(int n);
 size_t chol_solve_smem(int nmax, bool inverse);
-std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector<int>& n,
+std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector<int>& ids, const std::vector<int>& n,
                                       const std::vector<long long>& poff, int iters, bool inverse);
 void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc);
 void build_ras_panels(Ctx& c);                                        // after build_schwarz (RAS, inverse mode)

@@ -13,10 +13,14 @@ namespace rdd {
 namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16, NT = 128;
-constexpr int KP = BK + 4;   // k-contiguous tiles: [64][BK+4] (row stride ≡ 4 banks mod 16)
-constexpr int MP = BM + 4;   // m/n-contiguous tiles: [BK][64+4]
-constexpr int kStageA = BM * KP > BK * MP ? BM * KP : BK * MP;  // doubles per operand per stage
-constexpr size_t gemm_smem(int stages) { return static_cast<size_t>(stages) * 2 * kStageA * sizeof(double); }
+constexpr int KP = BK + 4;   // k-contiguous tiles: [tile][BK+4] (row stride ≡ 4 banks mod 16)
+constexpr int MP = BM + 4;   // m/n-contiguous tiles: [BK][tile+4] (64- and 80-wide: stride ≡ 4 mod 16)
+// doubles per operand per stage for a TB-wide square CTA tile (TB = 64 or 80)
+constexpr int stage_doubles(int tb) { return tb * KP > BK * (tb + 4) ? tb * KP : BK * (tb + 4); }
+constexpr int kStageA = stage_doubles(BM);
+constexpr size_t gemm_smem(int stages, int tb = BM) {
+  return static_cast<size_t>(stages) * 2 * stage_doubles(tb) * sizeof(double);
+}
 // pipeline depth / residency per mode (tools/gemm_bench.py): the NN and NT products (projections,
 // Cholesky panel and trailing updates) run best with a 2-deep ring and 4 CTAs per SM (+5-10% on
 // the K = 64 and K = 512 update shapes), the TN Gram products with a 3-deep ring and 3 CTAs
@@ -40,27 +44,31 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// One CTA: a 64x64 tile of one task, 4 warps (32x32 warp tiles = 4x4 DMMA fragments). K streams
-// through a STAGES-deep cp.async ring; each operand tile keeps its global contiguous direction
-// in shared memory (k-contiguous for Aᵀ / B, m-contiguous for A / Bᵀ) so the copies coalesce,
-// and the padded strides make the fragment reads bank-conflict free.
-template <bool AT, bool BT, int STAGES = GemmCfg<AT>::stages>
-__global__ void __launch_bounds__(NT, GemmCfg<AT>::minb) k_gemm(const GemmTask* __restrict__ tasks) {
+// One CTA: a TB x TB tile of one task (TB = 16·FR: 64 by default, 80 for operands whose edges
+// are multiples of 80 — m = 400 pads to 448 in 64-wide tiles, a quarter more work), 4 warps
+// (8·FR-square warp tiles = FR x FR DMMA fragments). K streams through a STAGES-deep cp.async
+// ring; each operand tile keeps its global contiguous direction in shared memory (k-contiguous
+// for Aᵀ / B, m-contiguous for A / Bᵀ) so the copies coalesce, and the padded strides make the
+// fragment reads bank-conflict free.
+template <bool AT, bool BT, int STAGES = GemmCfg<AT>::stages, int FR = 4, int MINB = GemmCfg<AT>::minb>
+__global__ void __launch_bounds__(NT, MINB) k_gemm(const GemmTask* __restrict__ tasks) {
+  constexpr int TB = 16 * FR, WT = 8 * FR, MPt = TB + 4, kStage = stage_doubles(TB);
   extern __shared__ __align__(16) double gsm[];
   const GemmTask T = tasks[blockIdx.x];
+  if (T.M <= 0) return;  // empty task (a structurally zero tile of a device-generated list)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int m0 = T.tm * BM, n0 = T.tn * BN;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int m0 = T.tm * TB, n0 = T.tn * TB;
+  const int wm = (warp >> 1) * WT, wn = (warp & 1) * WT;
 
   // C = beta·C + alpha·op(A)op(B). With alpha = ±1 the accumulators start from (beta/alpha)·C,
   // loaded here so the C read overlaps the operand prologue instead of trailing the main loop
   const bool pre = T.beta != 0.0 && (T.alpha == 1.0 || T.alpha == -1.0);
   const double cf = T.beta * T.alpha;  // beta/alpha for alpha = ±1
-  double acc[4][4][2];
+  double acc[FR][FR][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FR; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < FR; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int m = m0 + wm + 8 * i + (lane >> 2);
@@ -68,8 +76,8 @@ __global__ void __launch_bounds__(NT, GemmCfg<AT>::minb) k_gemm(const GemmTask* 
         acc[i][j][e] = (pre && m < T.M && n < T.N) ? cf * T.Cm[m + static_cast<long long>(n) * T.ldc] : 0.0;
       }
 
-  auto As = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStageA; };
-  auto Bs = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStageA + kStageA; };
+  auto As = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStage; };
+  auto Bs = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStage + kStage; };
   // row-gather indices (TN normal blocks) for the stage issued next are loaded one issue ahead, so
   // the dependent index read does not stall the cp.async issue of every stage
   int gia = 0, gib = 0;
@@ -84,17 +92,18 @@ __global__ void __launch_bounds__(NT, GemmCfg<AT>::minb) k_gemm(const GemmTask* 
     double* a = As(s);
     double* bsm = Bs(s);
     const int ga = gia, gb = gib;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    // the wide tile keeps this loop rolled: unrolled, its 2·TB/8 hoisted row addresses spill
+#pragma unroll(FR == 4 ? TB / 8 : 1)
+    for (int i = 0; i < TB / 8; ++i) {
       if (AT) {  // A(k, m) = A[k + m*lda] -> a[m][k]
         const int k = k0 + (tid & 15), ml = (tid >> 4) + 8 * i, m = m0 + ml;
         const bool v = k < T.K && m < T.M;
         const long long kk = v ? ga : 0;
         cp_async8(a + ml * KP + (tid & 15), v ? T.A + kk + static_cast<long long>(m) * T.lda : T.A, v);
       } else {  // A(m, k) = A[m + k*lda] -> a[k][m]
-        const int ml = tid & 63, m = m0 + ml, kl = (tid >> 6) + 2 * i, k = k0 + kl;
+        const int e = tid + NT * i, ml = e % TB, m = m0 + ml, kl = e / TB, k = k0 + kl;
         const bool v = k < T.K && m < T.M;
-        cp_async8(a + kl * MP + ml, v ? T.A + m + static_cast<long long>(k) * T.lda : T.A, v);
+        cp_async8(a + kl * MPt + ml, v ? T.A + m + static_cast<long long>(k) * T.lda : T.A, v);
       }
       if (!BT) {  // B(k, n) = B[k + n*ldb] -> b[n][k]
         const int k = k0 + (tid & 15), nl = (tid >> 4) + 8 * i, n = n0 + nl;
@@ -102,9 +111,9 @@ __global__ void __launch_bounds__(NT, GemmCfg<AT>::minb) k_gemm(const GemmTask* 
         const long long kk = v ? gb : 0;
         cp_async8(bsm + nl * KP + (tid & 15), v ? T.B + kk + static_cast<long long>(n) * T.ldb : T.B, v);
       } else {  // B(k, n) = Bt[n + k*ldb] -> b[k][n]
-        const int nl = tid & 63, n = n0 + nl, kl = (tid >> 6) + 2 * i, k = k0 + kl;
+        const int e = tid + NT * i, nl = e % TB, n = n0 + nl, kl = e / TB, k = k0 + kl;
         const bool v = k < T.K && n < T.N;
-        cp_async8(bsm + kl * MP + nl, v ? T.B + n + static_cast<long long>(k) * T.ldb : T.B, v);
+        cp_async8(bsm + kl * MPt + nl, v ? T.B + n + static_cast<long long>(k) * T.ldb : T.B, v);
       }
     }
     gidx(kt + 1);
@@ -124,38 +133,43 @@ __global__ void __launch_bounds__(NT, GemmCfg<AT>::minb) k_gemm(const GemmTask* 
     const double* a = As(kt % STAGES);
     const double* bsm = Bs(kt % STAGES);
     // fragments double-buffered across the four k-steps of the stage: the loads of step kk+4 are
-    // issued before the 16 DMMAs of step kk, so no DMMA waits on its own shared-memory load
-    double af[2][4], bf[2][4];
+    // issued before the FR² DMMAs of step kk, so no DMMA waits on its own shared-memory load
+    constexpr int NBUF = FR == 4 ? 2 : 1;  // the wide tile has no registers left for a second set
+    double af[NBUF][FR], bf[NBUF][FR];
     auto frag = [&](int kk, int b) {
       const int k = kk + (lane & 3);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < FR; ++i) {
         const int ml = wm + 8 * i + (lane >> 2);
-        af[b][i] = AT ? a[ml * KP + k] : a[k * MP + ml];
+        af[b][i] = AT ? a[ml * KP + k] : a[k * MPt + ml];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < FR; ++j) {
         const int nl = wn + 8 * j + (lane >> 2);
-        bf[b][j] = BT ? bsm[k * MP + nl] : bsm[nl * KP + k];
+        bf[b][j] = BT ? bsm[k * MPt + nl] : bsm[nl * KP + k];
       }
     };
-    frag(0, 0);
+    if (NBUF == 2) frag(0, 0);
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      const int b = (kk >> 2) & 1;
-      if (kk + 4 < BK) frag(kk + 4, b ^ 1);
+      const int b = NBUF == 2 ? (kk >> 2) & 1 : 0;
+      if (NBUF == 2) {
+        if (kk + 4 < BK) frag(kk + 4, b ^ 1);
+      } else {
+        frag(kk, 0);
+      }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < FR; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[b][i], bf[b][j]);
+        for (int j = 0; j < FR; ++j) dmma(acc[i][j], af[b][i], bf[b][j]);
     }
   }
   cp_wait<0>();
   // epilogue: fragment (row = lane>>2, cols 2*(lane&3) + {0,1})
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FR; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < FR; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int m = m0 + wm + 8 * i + (lane >> 2);
@@ -257,16 +271,22 @@ __global__ void __launch_bounds__(WNT, 2) k_gemm_nn_wide(const GemmTask* __restr
 }
 
 template <bool AT, bool BT>
-void launch(Ctx& c, const std::vector<GemmTask>& tasks, const char* fam) {
+void launch(Ctx& c, const std::vector<GemmTask>& tasks, const char* fam, int tile = BM) {
   if (tasks.empty()) return;
   ScopedKernelTimer tk(c, fam);
   DBuf<GemmTask> d;
   d.ensure(tasks.size());
   c.stage.upload(d.p, tasks.data(), tasks.size() * sizeof(GemmTask), c.stream);
   // grid.x limit is 2^31-1; tasks are far fewer
-  constexpr size_t smem = gemm_smem(GemmCfg<AT>::stages);
-  ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<AT, BT>), smem);
-  k_gemm<AT, BT><<<static_cast<unsigned>(tasks.size()), NT, smem, c.stream>>>(d.p);
+  if (tile == 80) {  // 2-deep ring, 3 CTAs per SM (100 accumulator registers per thread)
+    constexpr size_t smem = gemm_smem(2, 80);
+    ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<AT, BT, 2, 5, 3>), smem);
+    k_gemm<AT, BT, 2, 5, 3><<<static_cast<unsigned>(tasks.size()), NT, smem, c.stream>>>(d.p);
+  } else {
+    constexpr size_t smem = gemm_smem(GemmCfg<AT>::stages);
+    ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<AT, BT>), smem);
+    k_gemm<AT, BT><<<static_cast<unsigned>(tasks.size()), NT, smem, c.stream>>>(d.p);
+  }
   RDD_LAUNCH_CHECK();
   if (!alloc_stream()) RDD_CUDA(cudaStreamSynchronize(c.stream));  // task buffer lifetime (non-pooled)
 }
@@ -284,8 +304,8 @@ void gemm_nn_wide(Ctx& c, const std::vector<GemmTask>& tasks) {
   RDD_LAUNCH_CHECK();
   if (!alloc_stream()) RDD_CUDA(cudaStreamSynchronize(c.stream));
 }
-void gemm_tn(Ctx& c, const std::vector<GemmTask>& tasks) { launch<true, false>(c, tasks, "gemm_tn"); }
-void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks) { launch<false, false>(c, tasks, "gemm_nn"); }
+void gemm_tn(Ctx& c, const std::vector<GemmTask>& tasks, int tile) { launch<true, false>(c, tasks, "gemm_tn", tile); }
+void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks, int tile) { launch<false, false>(c, tasks, "gemm_nn", tile); }
 void gemm_nt(Ctx& c, const std::vector<GemmTask>& tasks) { launch<false, true>(c, tasks, "gemm_nt"); }
 
 // tasks already in device memory (generated by a kernel)

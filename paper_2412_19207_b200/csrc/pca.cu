@@ -30,6 +30,19 @@ struct NNItem {
   double* C;
   int M, N, K, lda, ldb, ldc;
 };
+// CTA tile edge (64 or 80) for a batch of M_i x N_i outputs of TN products: 80 when it cuts the
+// padded tile area by more than 12%, its own per-flop deficit (m = 400 is 5 tiles of 80 but 7 of
+// 64, 448² vs 400²: Gram and Sᵀ·Z 25 -> 28 TF/s; the NN products lose with it, tools/gemm_bench.py)
+int pick_tile(const std::vector<std::pair<int, int>>& mn, bool upper = false) {
+  double a64 = 0.0, a80 = 0.0;
+  for (const auto& e : mn) {
+    const double m64 = ceil_div(e.first, 64), n64 = ceil_div(e.second, 64);
+    const double m80 = ceil_div(e.first, 80), n80 = ceil_div(e.second, 80);
+    a64 += (upper ? m64 * (m64 + 1) / 2 : m64 * n64) * 64.0 * 64.0;
+    a80 += (upper ? m80 * (m80 + 1) / 2 : m80 * n80) * 80.0 * 80.0;
+  }
+  return a80 < 0.88 * a64 ? 80 : 64;
+}
 static void nn_batch(Ctx& c, const std::vector<NNItem>& items) {
   int nmax = 0;
   for (const NNItem& it : items) nmax = std::max(nmax, it.N);
@@ -470,9 +483,9 @@ __global__ void k_copy_lead(const double* __restrict__ Vs, double* __restrict__ 
   for (long long e = threadIdx.x; e < cnt; e += blockDim.x) V0[off + e] = Vs[off + e];
 }
 
-std::vector<GemmTask> gram_tasks(Ctx& c, const double* X, double* G, const std::vector<long long>& offX) {
+std::vector<GemmTask> gram_tasks(Ctx& c, const double* X, double* G, const std::vector<long long>& offX, int tile) {
   std::vector<GemmTask> t;
-  const int m = c.m, nt = ceil_div(m, 64);
+  const int m = c.m, nt = ceil_div(m, tile);
   for (int j = 0; j < c.J; ++j) {
     const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
     for (int tm = 0; tm < nt; ++tm)
@@ -535,7 +548,8 @@ void run_pca(Ctx& c) {
     // (r x r: one CTA, few sweeps), Vr = L U, V0 = Householder completion of Vr to an n x n basis
     {
       ScopedKernelTimer tg(c, "gram");
-      gemm_tn(c, gram_tasks(c, c.S.p, G.p, c.S_off));
+      const int tgr = pick_tile({{m, m}}, true);
+      gemm_tn(c, gram_tasks(c, c.S.p, G.p, c.S_off, tgr), tgr);
     }
     WS Lw{c.ws("pca.L", J * mm)}, Vr{c.ws("pca.Vr", J * mm)}, Hw{c.ws("pca.H", J * mm)};
     DBuf<int> dr;
@@ -546,7 +560,7 @@ void run_pca(Ctx& c) {
       const size_t sm = static_cast<size_t>(m) * (2 * sizeof(double) + 1) + 16;
       if (sm > 32 * 1024)
         RDD_CUDA(cudaFuncSetAttribute(k_pchol, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-      k_pchol<<<J, kPcholThreads, sm, c.stream>>>(G.p, Lw.p, m, 1e-17, dr.p, dtrace.p);
+      k_pchol<<<J, kPcholThreads, sm, c.stream>>>(G.p, Lw.p, m, c.pca_stop, dr.p, dtrace.p);
       RDD_LAUNCH_CHECK();
     }
     std::vector<int> rj(J);
@@ -565,17 +579,23 @@ void run_pca(Ctx& c) {
       if (!(rj[j] == m || ok)) fast = false;
     }
     const bool skip_s1 = fast && rmax > 223;
+    std::vector<std::pair<int, int>> rr_pairs, mr_pairs;  // (r_j, r_j) and (m, r_j): tile-size choices
+    for (int j = 0; j < J; ++j) {
+      rr_pairs.push_back({rj[j], rj[j]});
+      mr_pairs.push_back({m, rj[j]});
+    }
     const int nref = c.pca_refine > 0 ? c.pca_refine : (skip_s1 ? 2 : 1);
     {
       std::vector<GemmTask> t;
+      const int tl = pick_tile(rr_pairs, true);
       for (int j = 0; j < J; ++j) {
-        const int nt = ceil_div(rj[j], 64);
+        const int nt = ceil_div(rj[j], tl);
         for (int tm = 0; tm < nt; ++tm)
           for (int tn = tm; tn < nt; ++tn)
             t.push_back({Lw.p + offm[j], Lw.p + offm[j], G.p + offm[j], nullptr, nullptr, rj[j], rj[j], m, m, m,
                          rj[j], tm, tn, 0.0});
       }
-      gemm_tn(c, t);  // M = LᵀL (upper tiles) over the Gram buffer
+      gemm_tn(c, t, tl);  // M = LᵀL (upper tiles) over the Gram buffer
     }
     std::vector<long long> offr(J);
     for (int j = 0, e = 0; j < J; e += rj[j], ++j) offr[j] = e;
@@ -620,14 +640,15 @@ void run_pca(Ctx& c) {
         {
           ScopedKernelTimer tr(c, "pca_refine");
           std::vector<GemmTask> t;
+          const int ty = pick_tile(mr_pairs);
           for (int j = 0; j < J; ++j) {
             const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
-            for (int tm = 0; tm < ceil_div(m, 64); ++tm)
-              for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+            for (int tm = 0; tm < ceil_div(m, ty); ++tm)
+              for (int tn = 0; tn < ceil_div(rj[j], ty); ++tn)
                 t.push_back({c.S.p + c.S_off[j], T.p + c.S_off[j], Hw.p + offm[j], nullptr, nullptr, m, rj[j], rows,
                              std::max(rows, 1), std::max(rows, 1), m, tm, tn, 0.0});
           }
-          gemm_tn(c, t);  // Y = Sᵀ·Z
+          gemm_tn(c, t, ty);  // Y = Sᵀ·Z
         }
         const size_t sm = static_cast<size_t>(m) * (2 * sizeof(double) + sizeof(int)) + 16;
         if (sm > 32 * 1024)
@@ -660,25 +681,27 @@ void run_pca(Ctx& c) {
       {
         ScopedKernelTimer ts(c, "pca_stage2_gemm");
         std::vector<GemmTask> t;
+        const int tg = pick_tile(rr_pairs, true);
         for (int j = 0; j < J; ++j) {
           const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
-          const int nt = ceil_div(rj[j], 64);
+          const int nt = ceil_div(rj[j], tg);
           for (int tm = 0; tm < nt; ++tm)
             for (int tn = tm; tn < nt; ++tn)
               t.push_back({T.p + c.S_off[j], T.p + c.S_off[j], G.p + offm[j], nullptr, nullptr, rj[j], rj[j], rows,
                            std::max(rows, 1), std::max(rows, 1), rj[j], tm, tn, 0.0});
         }
-        gemm_tn(c, t);  // G_a = T_aᵀ T_a
+        gemm_tn(c, t, tg);  // G_a = T_aᵀ T_a
       }
       batched_syevj(c, G.p, W.p, lam.p, rj, offm, s2);
       {
         std::vector<GemmTask> t;
+        const int tv = 64;
         for (int j = 0; j < J; ++j)
-          for (int tm = 0; tm < ceil_div(m, 64); ++tm)
-            for (int tn = 0; tn < ceil_div(rj[j], 64); ++tn)
+          for (int tm = 0; tm < ceil_div(m, tv); ++tm)
+            for (int tn = 0; tn < ceil_div(rj[j], tv); ++tn)
               t.push_back({V0.p + offm[j], W.p + offm[j], Vfull.p + offm[j], nullptr, nullptr, m, rj[j], rj[j], m,
                            rj[j], m, tm, tn, 0.0});
-        gemm_nn(c, t);  // V = Q W
+        gemm_nn(c, t, tv);  // V = Q W
       }
     } else {
       {
@@ -709,15 +732,16 @@ void run_pca(Ctx& c) {
       {
         ScopedKernelTimer ts(c, "pca_stage2_gemm");
         std::vector<GemmTask> t;
+        const int tg = pick_tile(rr_pairs, true);
         for (int j = 0; j < J; ++j) {
           const int rows = c.h_row_ptr[j + 1] - c.h_row_ptr[j];
-          const int nt = ceil_div(rj[j], 64);
+          const int nt = ceil_div(rj[j], tg);
           for (int tm = 0; tm < nt; ++tm)
             for (int tn = tm; tn < nt; ++tn)
               t.push_back({T.p + c.S_off[j], T.p + c.S_off[j], G.p + offm[j], nullptr, nullptr, rj[j], rj[j], rows,
                            std::max(rows, 1), std::max(rows, 1), rj[j], tm, tn, 0.0});
         }
-        gemm_tn(c, t);  // G_a = T_aᵀ T_a
+        gemm_tn(c, t, tg);  // G_a = T_aᵀ T_a
       }
       batched_syevj(c, G.p, W.p, lam.p, rj, offm, s2);
       {
@@ -743,7 +767,7 @@ void run_pca(Ctx& c) {
         }
         gemm_nn(c, t);
       }
-      gemm_tn(c, gram_tasks(c, T.p, G.p, c.S_off));
+      gemm_tn(c, gram_tasks(c, T.p, G.p, c.S_off, 64));
       batched_syevj(c, G.p, W.p, lam.p, ns, offm, s2);
       // V = V0 W
       {

@@ -18,8 +18,6 @@
 
 namespace rdd {
 
-constexpr int kInvMax = 1024;  // largest local order kept as an explicit inverse
-
 namespace {
 
 // gather A_i from normal blocks: one CTA per (i, part-pair). Blocks stored transposed (j1 > j2:
@@ -233,7 +231,7 @@ void refresh_local_cond(Ctx& c) {
     DBuf<double> Af;
     gather_locals(c, sub, Af, off);
     const std::vector<double> la = batched_power(c, Af.p, nn, off, 200);
-    const std::vector<double> lp = batched_inv_power(c, c.P.p, nn, poff, 200, c.inv_mode);
+    const std::vector<double> lp = batched_inv_power(c, c.P.p, sub, nn, poff, 200, c.inv_mode);
     for (size_t q = 0; q < sub.size(); ++q) c.local_cond[sub[q]] = la[q] * lp[q];
   }
   c.local_cond_exact = true;
@@ -314,7 +312,14 @@ void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre) {
     c.apply_order.upload(ord, c.stream);
   }
   c.gat_tasks.clear();
-  std::vector<int> po;
+  c.inv_mode = *std::max_element(n.begin(), n.end()) <= c.inv_max;
+  c.env_off.assign(J + 1, 0);
+  for (int i = 0; i < J; ++i) c.env_off[i + 1] = c.env_off[i] + ceil_div(n[i], 64);
+  c.env_first.assign(c.env_off[J], 0);
+  c.env_base.assign(c.env_off[J], 0);
+  c.env_entries = 0.0;
+  c.P_off.assign(J + 1, 0);
+  std::vector<int> po, bfirst;
   for (int i = 0; i < J; ++i) {
     po.clear();
     int o = 0;
@@ -323,6 +328,7 @@ void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre) {
       o += c.h_p[c.nbr_idx[q]];
     }
     const int b0 = c.nbr_ptr[i], nn = c.nbr_ptr[i + 1] - b0;
+    bfirst = po;  // per block row x: first column of its leftmost nonzero block (its own at least)
     for (int x = 0; x < nn; ++x)
       for (int y = 0; y < nn; ++y) {
         const int j1 = c.nbr_idx[b0 + x], j2 = c.nbr_idx[b0 + y];
@@ -334,16 +340,37 @@ void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre) {
         const long long nbo = c.h_nb_look[it - c.nbr_idx.data()];
         if (nbo < 0) continue;  // neighbours without a row intersection: no normal block
         c.gat_tasks.push_back({i, j1, j2, po[x], po[y], nbo});
+        if (y < x) bfirst[x] = std::min(bfirst[x], po[y]);
       }
+    // tile-level envelope of the lower triangle and the packed row bases
+    int* ef = c.env_first.data() + c.env_off[i];
+    int* eb = c.env_base.data() + c.env_off[i];
+    const int nbt = ceil_div(n[i], 64);
+    long long tiles = 0;
+    for (int k = 0; k < nbt; ++k) ef[k] = c.inv_mode ? 0 : k;
+    for (int x = 0; x < nn; ++x) {
+      const int r0 = po[x], r1 = (x + 1 < nn ? po[x + 1] : n[i]);  // rows of block x
+      if (r1 == r0) continue;
+      if (!c.inv_mode)
+        for (int k = r0 / 64; k <= (r1 - 1) / 64; ++k) ef[k] = std::min(ef[k], bfirst[x] / 64);
+      const double w0 = r0 - bfirst[x] + 1, cnt = r1 - r0;  // row r holds r - bfirst + 1 entries
+      c.env_entries += c.inv_mode ? 0.0 : cnt * w0 + cnt * (cnt - 1) / 2.0;
+    }
+    if (c.inv_mode) c.env_entries += static_cast<double>(n[i]) * (n[i] + 1) / 2.0;
+    for (int k = 0; k < nbt; ++k) {
+      eb[k] = static_cast<int>(tiles) - ef[k];
+      tiles += k - ef[k] + 1;
+    }
+    c.P_off[i + 1] = c.P_off[i] + tiles * 64 * 64;
   }
+  c.denv_off.upload(c.env_off, c.stream);
+  c.denv_first.upload(c.env_first, c.stream);
+  c.denv_base.upload(c.env_base, c.stream);
   if (c.verbose) std::fprintf(stderr, "[schwarz] + gather tasks (host) %.3f ms\n", 1e3 * (now_s() - th0));
   // storage: the tile-packed factor of every A_i (the eigen-fallback blocks keep a dense copy) or,
   // when every block is small, the packed explicit inverse: one symmetric tile pass per apply
   // instead of two triangular ones, for 2/3·n³ more build flops
   if (c.verbose) std::fprintf(stderr, "[schwarz] + gather tasks (host) %.3f ms\n", 1e3 * (now_s() - th0));
-  c.inv_mode = *std::max_element(n.begin(), n.end()) <= kInvMax;
-  c.P_off.assign(J + 1, 0);
-  for (int i = 0; i < J; ++i) c.P_off[i + 1] = c.P_off[i] + packed_chol_size(n[i]);
   c.dP_off.upload(c.P_off, c.stream);
   c.fb_store.clear();
   const size_t p_bytes = static_cast<size_t>(c.P_off[J]) * sizeof(double);
@@ -392,7 +419,7 @@ void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre) {
     std::vector<int> fail;
     std::vector<double> fa;
     std::vector<double> fp;
-    batched_cholesky_pack(c, Aw.p, cn, coff, c.P.p, cpoff, fail, fa, c.inv_mode, &fp);
+    batched_cholesky_pack(c, Aw.p, chunk, cn, coff, c.P.p, cpoff, fail, fa, c.inv_mode, &fp);
     // rank decision: cond(A_i) <= ‖A_i‖_F·‖A_i⁻¹‖_F (explicit inverse) or ‖A_i‖_F·λmax(A_i⁻¹) (power
     // iteration through the factor); when that does not clear the threshold, λmax(A_i) by power
     // iteration and a longer λmax(A_i⁻¹)
@@ -409,16 +436,17 @@ void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre) {
         }
       }
     } else {
-      std::vector<int> nn;
+      std::vector<int> nn, okid;
       std::vector<long long> po;
       for (int q : ok_q) {
         nn.push_back(cn[q]);
         po.push_back(cpoff[q]);
+        okid.push_back(chunk[q]);
       }
       // routing estimate only: blocks that do not clear the threshold are refined below (60
       // iterations on A_i⁻¹ and A_i), and the exported local_cond is recomputed exactly on demand
       // (refresh_local_cond); ‖A_i‖_F over-estimates λmax(A_i) by up to sqrt(n_i)
-      const std::vector<double> lp = batched_inv_power(c, c.P.p, nn, po, 4, false);
+      const std::vector<double> lp = batched_inv_power(c, c.P.p, okid, nn, po, 4, false);
       for (size_t z = 0; z < ok_q.size(); ++z) {
         const int q = ok_q[z];
         if (fa[q] * lp[z] < c.full_rank_cond) {
@@ -443,7 +471,7 @@ void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre) {
         po.push_back(cpoff[q]);
         t += static_cast<long long>(cn[q]) * cn[q];
       }
-      const std::vector<double> lp = batched_inv_power(c, c.P.p, fnn, po, 60, c.inv_mode);
+      const std::vector<double> lp = batched_inv_power(c, c.P.p, which, fnn, po, 60, c.inv_mode);
       gather_locals(c, which, Aw, foff);
       const std::vector<double> la = batched_power(c, Aw.p, fnn, foff, 60);
       for (size_t z = 0; z < flagged.size(); ++z) {

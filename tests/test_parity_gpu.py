@@ -371,6 +371,63 @@ def test_all_blocks_eigen_path(dev, orc, name):
         dev.set_param("full_rank_cond", 1e9)
 
 
+# Factor mode (local order above "inv_max": C3, C5 at full size) keeps the Cholesky factors packed
+# inside their envelopes: the blocks of A_i pairing two neighbours of i that do not overlap each
+# other are exact zeros and no fill enters left of a block row's first nonzero tile, so those tiles
+# are neither updated, stored nor read. Forced here on slices with 3 and 4 subdomains per axis
+# (structural zeros present), against the oracle's pseudo-inverse and the device's own explicit
+# inverses.
+FACTOR_CASES = {
+    "c2_4x4": configs.scaled(configs.c2(), [4, 4], 10, m=150),
+    "c5_3x3x3": configs.scaled(configs.c5(), [3, 3, 3], 6, m=36),
+    "c3_4x3x3_ras": configs.scaled(configs.c3(), [4, 3, 3], 6, m=36),
+}
+FACTOR_CASES["c3_4x3x3_ras"].max_iter = 100  # RAS-GMRES(50) on the heat slices may stagnate
+
+
+@pytest.mark.parametrize("name", list(FACTOR_CASES))
+def test_factor_mode_envelope(dev, orc, name):
+    cfg = FACTOR_CASES[name]
+    kind = cfg.precond if cfg.precond >= 0 else A.PRECOND_AS
+    p = None
+    rng = np.random.default_rng(31)
+    dev.build_instance(cfg).assemble(True).build_preconditioner(kind)
+    assert int(dev.geti("inv_mode")[0]) == 1
+    p = int(dev.geti("p")[0])
+    vs = [rng.standard_normal(p) for _ in range(2)]
+    z_inv = [dev.precond_apply(vs[0], False), dev.precond_apply(vs[1], True)]
+    its_inv = dev.run_single(cfg)["iterations"]
+    dev.set_param("inv_max", 0.0)
+    try:
+        dev.build_instance(cfg).assemble(True).build_preconditioner(kind)
+        orc.build_instance(cfg).assemble(True).build_preconditioner(kind)
+        assert int(dev.geti("inv_mode")[0]) == 0 and int(dev.geti("n_fallback")[0]) == 0
+        J = int(dev.geti("J")[0])
+        n = dev.geti("local_n")
+        skipped = total = 0
+        for i in range(J):
+            ef = dev.geti("env_first", i)
+            assert len(ef) == -(-int(n[i]) // 64) and np.all(ef <= np.arange(len(ef))) and ef[0] == 0
+            skipped += int(ef.sum())
+            total += len(ef) * (len(ef) + 1) // 2
+        assert skipped > 0, (skipped, total)  # the envelope really drops tiles here
+        print(f"{name}: {skipped} of {total} lower tiles outside the envelopes")
+        assert np.array_equal(dev.geti("local_rank"), orc.geti("local_rank"))
+        tol = max(1e-8, 1e-14 * float(orc.getd("local_cond").max()))
+        for tr in (False, True):
+            zo, zd = orc.precond_apply(vs[tr], tr), dev.precond_apply(vs[tr], tr)
+            assert np.linalg.norm(zd - zo) <= tol * np.linalg.norm(zo), (name, tr, tol)
+            assert np.linalg.norm(zd - z_inv[tr]) <= tol * np.linalg.norm(zo), (name, tr, "vs inverse mode")
+        so, sd = orc.run_single(cfg), dev.run_single(cfg)
+        assert sd["converged"] == so["converged"]
+        assert abs(sd["iterations"] - so["iterations"]) <= int(0.05 * so["iterations"]), (sd["iterations"], so["iterations"])
+        assert sd["iterations"] == its_inv
+        if so["converged"]:  # under-resolved slices: e_L2 can exceed 1, the bar is then relative
+            assert abs(sd["e_l2"] - so["e_l2"]) <= 1e-8 * max(1.0, so["e_l2"])
+    finally:
+        dev.set_param("inv_max", 1024.0)
+
+
 # The device against the reference itself (oracle/_ref: the unmodified headers compiled here on
 # the Eigen-subset shim; the BASELINE slices built from the reference's own types), not only
 # against the restatement: same ranks, same iteration counts, errors and solutions within 1e-8.

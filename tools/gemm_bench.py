@@ -19,6 +19,15 @@ SHAPES = [  # (name, mode, M, N, K, batch)
     ("tn 400x386 k13824 (C5 refine Sᵀ·Y)", 1, 400, 386, 13824, 64),
     ("nn 13824x213 k400 (C5 projection)", 0, 13824, 213, 400, 32),
     ("nn 1024^3", 0, 1024, 1024, 1024, 16),
+    # the 80-wide CTA tile (mode + 10) on the m = 400 shapes
+    ("tn gram 400x400 k13800, tile 80", 11, 400, 400, 13824, 64),
+    ("nn S·Q 13800x386 k400, tile 80", 10, 13824, 386, 400, 32),
+    ("tn 400x386 k13824, tile 80", 11, 400, 386, 13824, 64),
+    ("nn 13824x213 k400, tile 80", 10, 13824, 213, 400, 32),
+    ("nn 1280^3 tile 64", 0, 1280, 1280, 1280, 16),
+    ("nn 1280^3 tile 80", 10, 1280, 1280, 1280, 16),
+    ("tn 1280^3 tile 64", 1, 1280, 1280, 1280, 16),
+    ("tn 1280^3 tile 80", 11, 1280, 1280, 1280, 16),
 ]
 
 

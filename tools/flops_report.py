@@ -26,13 +26,24 @@ c_ms, _ = s.kernel_stats("cholesky")
 a_ms, a_n = s.kernel_stats("assemble")
 gram = float((rows * m * (m + 1)).sum())
 chol = float((n ** 3 / 3).sum())
+# flops the factorisation performs inside the envelopes (64-wide tiles): per step k the diagonal
+# POTRF, one panel solve per block row whose envelope reaches k, and one update per pair of those
+chol_env = 0.0
+if not int(s.geti("inv_mode")[0]):
+    for i in range(len(n)):
+        ef = s.geti("env_first", i)
+        ib = np.arange(len(ef))
+        for k in range(len(ef)):
+            r = int(np.count_nonzero((ib > k) & (ef <= k)))
+            chol_env += 64.0 ** 3 * (1.0 / 3.0 + r + r * (r + 1.0))
 d = cfg.d
 asm = float((rows * m).sum()) * (4 * d + 12 + 20)
 fma_peak = float(sys.argv[2]) if len(sys.argv) > 2 else 36.59  # TF/s, DFMA pipe measured (tools/fp64_peak.py)
 peak = 35.46  # TF/s, cuBLAS DGEMM measured on this B200 (tools/fp64_peak.py, DMMA pipe 96.5% busy)
 out = {"config": name, "gram_ms": g_ms, "gram_tflops": gram / g_ms / 1e9, "gram_frac": gram / g_ms / 1e9 / peak,
        "chol_ms": c_ms, "chol_tflops": chol / c_ms / 1e9, "chol_frac": chol / c_ms / 1e9 / peak,
-       "sum_n3_over_3": chol,
+       "sum_n3_over_3": chol, "chol_envelope_flops": chol_env,
+       "chol_envelope_tflops": chol_env / c_ms / 1e9, "chol_envelope_frac": chol_env / c_ms / 1e9 / peak,
        "assemble_ms": a_ms, "assemble_launches": a_n, "assemble_entries": float((rows * m).sum()),
        "assemble_tflops": asm / a_ms / 1e9, "assemble_frac": asm / a_ms / 1e9 / fma_peak, "fma_peak_tflops": fma_peak, "n_max": int(n.max()), "peak_tflops": peak}
 print(json.dumps(out))

@@ -761,9 +761,11 @@ int rdd_bench_precond(rdd_ctx* h, int transpose, int reps, double* ms_per_call, 
 
 int rdd_bench_gemm(rdd_ctx* h, int mode, int M, int N, int K, int batch, int reps, double* ms_out) {
   return guarded(h, [&](Ctx& c) {
-    const int tile = mode >= 10 ? 80 : 64;  // mode + 10: the 80-wide CTA tile (NN and TN)
+    // mode + 10: the 80 x 80 CTA tile; mode + 20: the 64 x 80 tile (NN and TN)
+    const int tile = mode >= 20 ? 6480 : (mode >= 10 ? 80 : 64);
+    const int tile_m = tile == 6480 ? 64 : tile, tile_n = tile == 6480 ? 80 : tile;
     mode %= 10;
-    if (M < 1 || N < 1 || K < 1 || batch < 1 || reps < 1 || mode < 0 || mode > 2 || (tile == 80 && mode == 2))
+    if (M < 1 || N < 1 || K < 1 || batch < 1 || reps < 1 || mode < 0 || mode > 2 || (tile != 64 && mode == 2))
       throw std::invalid_argument("bench_gemm: bad shape");
     const size_t sa = static_cast<size_t>(M) * K, sb = static_cast<size_t>(K) * N, sc = static_cast<size_t>(M) * N;
     rdd::DBuf<double> A, B, Cm;
@@ -774,8 +776,8 @@ int rdd_bench_gemm(rdd_ctx* h, int mode, int M, int N, int K, int batch, int rep
     RDD_CUDA(cudaMemsetAsync(B.p, 0, sizeof(double) * sb * batch, c.stream));
     std::vector<rdd::GemmTask> tasks;
     for (int b = 0; b < batch; ++b)
-      for (int tm = 0; tm < (M + tile - 1) / tile; ++tm)
-        for (int tn = 0; tn < (N + tile - 1) / tile; ++tn) {
+      for (int tm = 0; tm < (M + tile_m - 1) / tile_m; ++tm)
+        for (int tn = 0; tn < (N + tile_n - 1) / tile_n; ++tn) {
           rdd::GemmTask t{};
           t.A = A.p + sa * b;
           t.B = B.p + sb * b;

@@ -341,7 +341,7 @@ void evaluate(Ctx& c, const int* test_res);
 void evaluate_at(Ctx& c, long long M, const double* pts, const double* W, const double* Lv, const double* Gv,
                  double* out);
 // gemm.cu
-// tile = CTA tile edge, 64 or 80: the tasks' (tm, tn) count tiles of that size
+// tile = CTA tile edge, 64 or 80 (the tasks' (tm, tn) count tiles of that size), or 6480 = 64 rows x 80 columns
 void gemm_tn(Ctx& c, const std::vector<GemmTask>& tasks, int tile = 64);  // C = Aᵀ B (A: K x M, B: K x N col-major)
 void gemm_nn(Ctx& c, const std::vector<GemmTask>& tasks, int tile = 64);  // C = A B  (A: M x K, B: K x N col-major)
 void gemm_nn_wide(Ctx& c, const std::vector<GemmTask>& tasks);  // same, 64 x 128 tiles (tn in units of 128)

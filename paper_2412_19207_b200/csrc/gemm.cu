@@ -50,25 +50,28 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // ring; each operand tile keeps its global contiguous direction in shared memory (k-contiguous
 // for Aᵀ / B, m-contiguous for A / Bᵀ) so the copies coalesce, and the padded strides make the
 // fragment reads bank-conflict free.
-template <bool AT, bool BT, int STAGES = GemmCfg<AT>::stages, int FR = 4, int MINB = GemmCfg<AT>::minb>
+template <bool AT, bool BT, int STAGES = GemmCfg<AT>::stages, int FR = 4, int MINB = GemmCfg<AT>::minb, int FRN = FR>
 __global__ void __launch_bounds__(NT, MINB) k_gemm(const GemmTask* __restrict__ tasks) {
-  constexpr int TB = 16 * FR, WT = 8 * FR, MPt = TB + 4, kStage = stage_doubles(TB);
+  // TB x TBN CTA tile (rows x columns of C); the square tiles have FRN = FR
+  constexpr int TB = 16 * FR, WT = 8 * FR, MPt = TB + 4, kStageA_ = stage_doubles(TB);
+  constexpr int TBN = 16 * FRN, WTN = 8 * FRN, NPt = TBN + 4, kStageB_ = stage_doubles(TBN);
+  constexpr int kStage2 = kStageA_ + kStageB_;
   extern __shared__ __align__(16) double gsm[];
   const GemmTask T = tasks[blockIdx.x];
   if (T.M <= 0) return;  // empty task (a structurally zero tile of a device-generated list)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int m0 = T.tm * TB, n0 = T.tn * TB;
-  const int wm = (warp >> 1) * WT, wn = (warp & 1) * WT;
+  const int m0 = T.tm * TB, n0 = T.tn * TBN;
+  const int wm = (warp >> 1) * WT, wn = (warp & 1) * WTN;
 
   // C = beta·C + alpha·op(A)op(B). With alpha = ±1 the accumulators start from (beta/alpha)·C,
   // loaded here so the C read overlaps the operand prologue instead of trailing the main loop
   const bool pre = T.beta != 0.0 && (T.alpha == 1.0 || T.alpha == -1.0);
   const double cf = T.beta * T.alpha;  // beta/alpha for alpha = ±1
-  double acc[FR][FR][2];
+  double acc[FR][FRN][2];
 #pragma unroll
   for (int i = 0; i < FR; ++i)
 #pragma unroll
-    for (int j = 0; j < FR; ++j)
+    for (int j = 0; j < FRN; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int m = m0 + wm + 8 * i + (lane >> 2);
@@ -76,8 +79,8 @@ __global__ void __launch_bounds__(NT, MINB) k_gemm(const GemmTask* __restrict__ 
         acc[i][j][e] = (pre && m < T.M && n < T.N) ? cf * T.Cm[m + static_cast<long long>(n) * T.ldc] : 0.0;
       }
 
-  auto As = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStage; };
-  auto Bs = [&](int s) { return gsm + static_cast<size_t>(s) * 2 * kStage + kStage; };
+  auto As = [&](int s) { return gsm + static_cast<size_t>(s) * kStage2; };
+  auto Bs = [&](int s) { return gsm + static_cast<size_t>(s) * kStage2 + kStageA_; };
   // row-gather indices (TN normal blocks) for the stage issued next are loaded one issue ahead, so
   // the dependent index read does not stall the cp.async issue of every stage
   int gia = 0, gib = 0;
@@ -92,8 +95,8 @@ __global__ void __launch_bounds__(NT, MINB) k_gemm(const GemmTask* __restrict__ 
     double* a = As(s);
     double* bsm = Bs(s);
     const int ga = gia, gb = gib;
-    // the wide tile keeps this loop rolled: unrolled, its 2·TB/8 hoisted row addresses spill
-#pragma unroll(FR == 4 ? TB / 8 : 1)
+    // the wide tiles keep these loops rolled: unrolled, their hoisted row addresses spill
+#pragma unroll(FR == 4 && FRN == 4 ? TB / 8 : 1)
     for (int i = 0; i < TB / 8; ++i) {
       if (AT) {  // A(k, m) = A[k + m*lda] -> a[m][k]
         const int k = k0 + (tid & 15), ml = (tid >> 4) + 8 * i, m = m0 + ml;
@@ -105,15 +108,32 @@ __global__ void __launch_bounds__(NT, MINB) k_gemm(const GemmTask* __restrict__ 
         const bool v = k < T.K && m < T.M;
         cp_async8(a + kl * MPt + ml, v ? T.A + m + static_cast<long long>(k) * T.lda : T.A, v);
       }
-      if (!BT) {  // B(k, n) = B[k + n*ldb] -> b[n][k]
-        const int k = k0 + (tid & 15), nl = (tid >> 4) + 8 * i, n = n0 + nl;
-        const bool v = k < T.K && n < T.N;
-        const long long kk = v ? gb : 0;
-        cp_async8(bsm + nl * KP + (tid & 15), v ? T.B + kk + static_cast<long long>(n) * T.ldb : T.B, v);
-      } else {  // B(k, n) = Bt[n + k*ldb] -> b[k][n]
-        const int e = tid + NT * i, nl = e % TB, n = n0 + nl, kl = e / TB, k = k0 + kl;
-        const bool v = k < T.K && n < T.N;
-        cp_async8(bsm + kl * MPt + nl, v ? T.B + n + static_cast<long long>(k) * T.ldb : T.B, v);
+      if (FRN == FR) {
+        if (!BT) {  // B(k, n) = B[k + n*ldb] -> b[n][k]
+          const int k = k0 + (tid & 15), nl = (tid >> 4) + 8 * i, n = n0 + nl;
+          const bool v = k < T.K && n < T.N;
+          const long long kk = v ? gb : 0;
+          cp_async8(bsm + nl * KP + (tid & 15), v ? T.B + kk + static_cast<long long>(n) * T.ldb : T.B, v);
+        } else {  // B(k, n) = Bt[n + k*ldb] -> b[k][n]
+          const int e = tid + NT * i, nl = e % TBN, n = n0 + nl, kl = e / TBN, k = k0 + kl;
+          const bool v = k < T.K && n < T.N;
+          cp_async8(bsm + kl * NPt + nl, v ? T.B + n + static_cast<long long>(k) * T.ldb : T.B, v);
+        }
+      }
+    }
+    if (FRN != FR) {
+#pragma unroll 1
+      for (int i = 0; i < TBN / 8; ++i) {
+        if (!BT) {
+          const int k = k0 + (tid & 15), nl = (tid >> 4) + 8 * i, n = n0 + nl;
+          const bool v = k < T.K && n < T.N;
+          const long long kk = v ? gb : 0;
+          cp_async8(bsm + nl * KP + (tid & 15), v ? T.B + kk + static_cast<long long>(n) * T.ldb : T.B, v);
+        } else {
+          const int e = tid + NT * i, nl = e % TBN, n = n0 + nl, kl = e / TBN, k = k0 + kl;
+          const bool v = k < T.K && n < T.N;
+          cp_async8(bsm + kl * NPt + nl, v ? T.B + n + static_cast<long long>(k) * T.ldb : T.B, v);
+        }
       }
     }
     gidx(kt + 1);
@@ -134,8 +154,8 @@ __global__ void __launch_bounds__(NT, MINB) k_gemm(const GemmTask* __restrict__ 
     const double* bsm = Bs(kt % STAGES);
     // fragments double-buffered across the four k-steps of the stage: the loads of step kk+4 are
     // issued before the FR² DMMAs of step kk, so no DMMA waits on its own shared-memory load
-    constexpr int NBUF = FR == 4 ? 2 : 1;  // the wide tile has no registers left for a second set
-    double af[NBUF][FR], bf[NBUF][FR];
+    constexpr int NBUF = FR == 4 ? 2 : 1;  // the 80 x 80 tile has no registers left for a second set
+    double af[NBUF][FR], bf[NBUF][FRN];
     auto frag = [&](int kk, int b) {
       const int k = kk + (lane & 3);
 #pragma unroll
@@ -144,9 +164,9 @@ __global__ void __launch_bounds__(NT, MINB) k_gemm(const GemmTask* __restrict__ 
         af[b][i] = AT ? a[ml * KP + k] : a[k * MPt + ml];
       }
 #pragma unroll
-      for (int j = 0; j < FR; ++j) {
+      for (int j = 0; j < FRN; ++j) {
         const int nl = wn + 8 * j + (lane >> 2);
-        bf[b][j] = BT ? bsm[k * MPt + nl] : bsm[nl * KP + k];
+        bf[b][j] = BT ? bsm[k * NPt + nl] : bsm[nl * KP + k];
       }
     };
     if (NBUF == 2) frag(0, 0);
@@ -161,7 +181,7 @@ __global__ void __launch_bounds__(NT, MINB) k_gemm(const GemmTask* __restrict__ 
 #pragma unroll
       for (int i = 0; i < FR; ++i)
 #pragma unroll
-        for (int j = 0; j < FR; ++j) dmma(acc[i][j], af[b][i], bf[b][j]);
+        for (int j = 0; j < FRN; ++j) dmma(acc[i][j], af[b][i], bf[b][j]);
     }
   }
   cp_wait<0>();
@@ -169,7 +189,7 @@ __global__ void __launch_bounds__(NT, MINB) k_gemm(const GemmTask* __restrict__ 
 #pragma unroll
   for (int i = 0; i < FR; ++i)
 #pragma unroll
-    for (int j = 0; j < FR; ++j)
+    for (int j = 0; j < FRN; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int m = m0 + wm + 8 * i + (lane >> 2);
@@ -278,7 +298,11 @@ void launch(Ctx& c, const std::vector<GemmTask>& tasks, const char* fam, int til
   d.ensure(tasks.size());
   c.stage.upload(d.p, tasks.data(), tasks.size() * sizeof(GemmTask), c.stream);
   // grid.x limit is 2^31-1; tasks are far fewer
-  if (tile == 80) {  // 2-deep ring, 3 CTAs per SM (100 accumulator registers per thread)
+  if (tile == 6480) {  // 64 x 80 (rows x columns): 2-deep ring, 3 CTAs per SM
+    constexpr size_t smem = static_cast<size_t>(2) * (stage_doubles(64) + stage_doubles(80)) * sizeof(double);
+    ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<AT, BT, 2, 4, 3, 5>), smem);
+    k_gemm<AT, BT, 2, 4, 3, 5><<<static_cast<unsigned>(tasks.size()), NT, smem, c.stream>>>(d.p);
+  } else if (tile == 80) {  // 2-deep ring, 3 CTAs per SM (100 accumulator registers per thread)
     constexpr size_t smem = gemm_smem(2, 80);
     ensure_smem_attr(reinterpret_cast<const void*>(k_gemm<AT, BT, 2, 5, 3>), smem);
     k_gemm<AT, BT, 2, 5, 3><<<static_cast<unsigned>(tasks.size()), NT, smem, c.stream>>>(d.p);

@@ -24,6 +24,9 @@ SHAPES = [  # (name, mode, M, N, K, batch)
     ("nn S·Q 13800x386 k400, tile 80", 10, 13824, 386, 400, 32),
     ("tn 400x386 k13824, tile 80", 11, 400, 386, 13824, 64),
     ("nn 13824x213 k400, tile 80", 10, 13824, 213, 400, 32),
+    ("nn S·Q 13800x386 k400, tile 64x80", 20, 13824, 386, 400, 32),
+    ("nn 13824x213 k400, tile 64x80", 20, 13824, 213, 400, 32),
+    ("nn 1280^3 tile 64x80", 20, 1280, 1280, 1280, 16),
     ("nn 1280^3 tile 64", 0, 1280, 1280, 1280, 16),
     ("nn 1280^3 tile 80", 10, 1280, 1280, 1280, 16),
     ("tn 1280^3 tile 64", 1, 1280, 1280, 1280, 16),

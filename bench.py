@@ -181,25 +181,40 @@ def cpu_sample(threads: int):
 
 
 def run_reference(args, cfg, world, rank, dist):
-    """The reference arm. A full C5 solve on the CPU oracle takes hours on a host (512 serial
-    per-subdomain SVDs and dense local eigensolves of order ~5,000: profiles/oracle_fullsize_r02.jsonl),
-    and a bounded sample is not the metric (seconds for the whole C5 solve), so `value` is null
-    rather than an estimate; one real complete C5s solve is measured and reported as the sample."""
+    """The reference arm: the reference's own CPU implementation of the path (oracle/_ref when it
+    compiled, else the oracle port) on the host cores, each step a BOUNDED SAMPLE of the workload —
+    one complete run_single of C5s, BASELINE configs[4]'s own 2x2x2 run of C5 (8 of its 512
+    subdomains; same d, m, points per subdomain, operator, PCA rule and solver). A complete C5
+    solve on the host takes hours (512 serial per-subdomain SVDs and dense local eigensolves of
+    order ~5,000). `value` is the measured time of that sample, never an extrapolation to the whole
+    workload: the ratio against it understates the full-workload speed-up. The step count is
+    bounded so the run ends within a few minutes on any host."""
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    smp = cpu_sample(threads)
+    first = cpu_sample(threads)  # warm-up (page-in, thread pool) and the time budget probe
+    budget_s = 150.0
+    steps = max(1, min(args.steps, int(budget_s // max(first["value"], 1e-3))))
+    warm = 1
+    walls = []
+    smp = first
+    for _ in range(steps):
+        smp = cpu_sample(threads)
+        walls.append(smp["value"])
+    value = sum(walls) / len(walls)
+    smp["value"] = value
     line = {
-        "metric": METRIC, "value": None, "unit": "s", "n_gpus": args.gpus, "steps": 0, "warmup": 0,
-        "ms_per_step": None, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": 1e3 * value, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (formula-defined problem, SplitMix64 bases as the reference)", "impl": "reference",
         "config": {"workload": args.config, **cfg.as_dict()},
-        "reason": (f"a complete {args.config} solve on the host (the reference compiled here) takes hours (serial per-subdomain PCA and "
-                   f"dense local eigensolves); no estimate is reported. Measured instead: one complete C5s solve "
-                   f"({smp['value']:.1f} s on {smp['cores']} threads, cpu_baseline) and full-size oracle timings in "
-                   f"profiles/oracle_fullsize_r02.jsonl"),
+        "sample_note": (f"each step is a bounded sample of {args.config}: one complete run_single of C5s (8 of the 512 "
+                        f"subdomains, 1 PCG iteration instead of 81) on the host, measured; a complete {args.config} solve on "
+                        f"the host takes hours. The ratio against this value understates the full-workload speed-up "
+                        f"(the device solves the same C5s in ~0.06 s: cpu_baseline.device_same_sample_s of the repo arm; "
+                        f"full-size reference runs of C2 and C4 in profiles/oracle_fullsize_r02.jsonl and DESIGN.md §7)"),
         "cpu_baseline": {k: smp[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": None, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -341,14 +356,13 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    world, rank, local, dist = dist_setup()
     from paper_2412_19207_b200 import configs
     cfg = configs.aspcg(args.config)  # the metric: AS-PCG on every config
+    if args.impl == "reference":  # host only: rank 0 alone works, no process group is set up
+        return run_reference(args, cfg, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), None)
+    world, rank, local, dist = dist_setup()
     try:
-        if args.impl == "reference":
-            rc = run_reference(args, cfg, world, rank, dist)
-        else:
-            rc = run_device(args, cfg, world, rank, local, dist)
+        rc = run_device(args, cfg, world, rank, local, dist)
     finally:
         if dist is not None:
             dist.destroy_process_group()

@@ -818,26 +818,23 @@ std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector
   return out;
 }
 
-// Schwarz local apply: z_i = A_i⁻¹ g_i, g_i = w(v)[S_i] (schwarz.hpp:153-215: SAS/RAS weights in
-// front of the local solve for the transpose). Factor path or, for eigen-fallback subdomains, the
-// dense pseudo-inverse. One CTA per subdomain.
+// Schwarz local apply, factor mode: z_i = A_i⁻¹ g_i, g_i = w(v)[S_i] (schwarz.hpp:153-215: SAS/RAS
+// weights in front of the local solve for the transpose) through the envelope-packed Cholesky
+// factor or, for eigen-fallback subdomains, the dense pseudo-inverse. One CTA per subdomain; CTAs
+// take the subdomains largest first (order): the per-CTA streaming time grows with n_i², so the
+// biggest local solves must not start in the last wave. (The explicit inverses of the small-block
+// mode go through k_inv_apply_tma below.)
 __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
     const double* __restrict__ P, const long long* __restrict__ poff, const double* const* __restrict__ dense,
     const int* __restrict__ set_ptr, const int* __restrict__ set_idx, const double* __restrict__ v,
     const int* __restrict__ mult, const int* __restrict__ owner, int kind, int transpose, int nbmax,
-    double* __restrict__ z, int inverse, long long zhalf, const int* __restrict__ live,
-    const int* __restrict__ order, const int* __restrict__ eoff, const int* __restrict__ efirst,
-    const int* __restrict__ ebase) {
+    double* __restrict__ z, const int* __restrict__ live, const int* __restrict__ order,
+    const int* __restrict__ eoff, const int* __restrict__ efirst, const int* __restrict__ ebase) {
   if (live && *live != 0) return;  // solver loop already stopped (speculative graph iteration)
   extern __shared__ double sm[];
   double* g = sm;
   double* red = sm + static_cast<size_t>(nbmax) * NB;
-  // inverse mode: two CTAs per subdomain, each over every other tile, partials to z and z + zhalf.
-  // CTAs take the subdomains largest first (order): the per-CTA streaming time grows with n_i²,
-  // so the biggest local solves must not start in the last wave
-  const int bi = inverse ? blockIdx.x >> 1 : blockIdx.x;
-  const int i = order ? order[bi] : bi;
-  const int h = inverse ? blockIdx.x & 1 : 0;
+  const int i = order ? order[blockIdx.x] : blockIdx.x;
   const int s0 = set_ptr[i], n = set_ptr[i + 1] - s0, nb = (n + NB - 1) / NB;
   for (int q = threadIdx.x; q < nb * NB; q += blockDim.x) {
     double val = 0.0;
@@ -852,20 +849,17 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_apply(
     g[q] = val;
   }
   __syncthreads();
-  double* zo = z + static_cast<long long>(h) * zhalf;
   const double* D = dense[i];
   if (D) {
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
       double acc = 0.0;
-      if (h == 0)
-        for (int q = 0; q < n; ++q) acc += D[r + static_cast<long long>(q) * n] * g[q];
-      zo[s0 + r] = acc;
+      for (int q = 0; q < n; ++q) acc += D[r + static_cast<long long>(q) * n] * g[q];
+      z[s0 + r] = acc;
     }
     return;
   }
-  if (inverse) symv_packed(P + poff[i], nb, g, red, h, 2);
-  else chol_solve(P + poff[i], nb, g, red, efirst + eoff[i], ebase + eoff[i]);
-  for (int r = threadIdx.x; r < n; r += blockDim.x) zo[s0 + r] = g[r];
+  chol_solve(P + poff[i], nb, g, red, efirst + eoff[i], ebase + eoff[i]);
+  for (int r = threadIdx.x; r < n; r += blockDim.x) z[s0 + r] = g[r];
 }
 
 // ---- explicit-inverse apply through a TMA ring (small blocks: C1, C2, C4). The packed lower tiles
@@ -1043,7 +1037,6 @@ size_t inv_apply_tma_smem(int nmax) {
 }
 
 void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
-  const size_t smem = chol_solve_smem(c.nmax_local, c.inv_mode);
   if (c.inv_mode) {
     const size_t tsm = inv_apply_tma_smem(c.nmax_local);
     ensure_smem_attr(reinterpret_cast<const void*>(k_inv_apply_tma), tsm);
@@ -1053,11 +1046,11 @@ void chol_apply(Ctx& c, const double* v, bool transpose, double* zloc) {
     RDD_LAUNCH_CHECK();
     return;
   }
+  const size_t smem = chol_solve_smem(c.nmax_local, false);
   ensure_smem_attr(reinterpret_cast<const void*>(k_chol_apply), smem);
   k_chol_apply<<<c.J, kSolveWarps * 32, smem, c.stream>>>(
       c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.dset_idx.p, v, c.dmult.p, c.downer.p, c.pkind, transpose ? 1 : 0,
-      ceil_div(c.nmax_local, NB), zloc, 0, static_cast<long long>(c.set_idx.size()), c.live, c.apply_order.p,
-      c.denv_off.p, c.denv_first.p, c.denv_base.p);
+      ceil_div(c.nmax_local, NB), zloc, c.live, c.apply_order.p, c.denv_off.p, c.denv_first.p, c.denv_base.p);
   RDD_LAUNCH_CHECK();
 }
 

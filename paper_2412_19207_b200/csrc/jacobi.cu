@@ -750,8 +750,10 @@ static size_t oe_smem(int ne, int K) {
          static_cast<size_t>(ne) * (sizeof(double*) + sizeof(int) + 1) +
          static_cast<size_t>(2 * oe_items(ne)) * sizeof(int) + 64;
 }
+// smallest cluster that holds the packed triangle: more matrices in flight beat more threads per
+// matrix (order 386, batch 512: K = 3 291 ms, K = 4 351 ms, K = 8 684 ms; tools/jacobi_one.py)
 static int oe_k(int ne) {
-  for (int K : {1, 2, 4, 8})
+  for (int K : {1, 2, 3, 4, 8})
     if (oe_smem(ne, K) <= kCtaSmem) return K;
   return 0;
 }
@@ -816,7 +818,7 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
   const int exper = ex ? std::atoi(ex) : 0;
   if (const char* e = std::getenv("RDD_JACOBI_K")) {  // experiment override (larger clusters only)
     const int k = std::atoi(e);
-    if (K > 0 && k > K && k <= 8 && (k & (k - 1)) == 0) K = k;
+    if (K > 0 && k <= 8 && ((k > K && (k & (k - 1)) == 0) || (k == 3 && oe_smem(ne, 3) <= kCtaSmem))) K = k;
   }
   int swmax = 0;
   if (K > 0) {
@@ -852,6 +854,7 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     if (K == 1 && half) launch(k_jacobi_oe<1, kJT / 2>);
     else if (K == 1) launch(k_jacobi_oe<1>);
     else if (K == 2) half_cl ? launch(k_jacobi_oe<2, kJT / 2>) : launch(k_jacobi_oe<2>);
+    else if (K == 3) launch(k_jacobi_oe<3>);
     else if (K == 4) half_cl ? launch(k_jacobi_oe<4, kJT / 2>) : launch(k_jacobi_oe<4>);
     else half_cl ? launch(k_jacobi_oe<8, kJT / 2>) : launch(k_jacobi_oe<8>);
     const int E = ((ne + 31) / 32 + 1) & ~1;  // positions per lane, even

@@ -13,6 +13,7 @@
 // active. A failed pivot flags the matrix for the eigen fallback (schwarz.cu).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "ctx.hpp"
 
@@ -575,7 +576,8 @@ void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& ids, const
   // the trailing matrix right of an outer panel takes one K = 512 update when the panel is done.
   // Every step's work lists are built up front and uploaded once: the step loop only launches.
   const int nbmax = ceil_div(nmax, NB);
-  constexpr int kOuter = 8;  // inner blocks per outer panel (8: measured best of 4/8/16)
+  int kOuter = 8;  // inner blocks per outer panel (8: measured best of 4/8/16)
+  if (const char* e = std::getenv("RDD_CHOL_OUTER")) kOuter = std::max(1, std::atoi(e));  // tuning experiments only
   struct Step {
     size_t act0, nact, sd0, nsd, ud0, nud;
     long long stotal, utotal;

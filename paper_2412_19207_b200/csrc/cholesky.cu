@@ -1092,6 +1092,46 @@ __global__ void k_ras_panel(const double* __restrict__ P, const long long* __res
   }
 }
 
+// factor mode: the panel is the transpose of X = A_i⁻¹ E_own (n_i x p_i, solved by ras_factor_solves):
+// R[r, c] = X[c, r]; eigen-fallback blocks read their dense pseudo-inverse. 32 x 32 transposes
+// through shared memory (both sides coalesced)
+__global__ void k_ras_panel_x(const double* __restrict__ X, const long long* __restrict__ xoff,
+                              const int* __restrict__ ldx, const double* const* __restrict__ dense,
+                              const int* __restrict__ set_ptr, const int* __restrict__ own_off,
+                              const int* __restrict__ own_n, const long long* __restrict__ ras_off,
+                              double* __restrict__ R) {
+  __shared__ double tile[32][33];
+  const int i = blockIdx.y;
+  const int n = set_ptr[i + 1] - set_ptr[i], o = own_off[i], pr = own_n[i];
+  const double* D = dense[i];
+  double* Ri = R + ras_off[i];
+  const double* Xi = X + xoff[i];
+  const int ld = ldx[i];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
+  const int ctiles = (n + 31) / 32, rtiles = (pr + 31) / 32;
+  for (int t = blockIdx.x; t < ctiles * rtiles; t += gridDim.x) {
+    const int c0 = (t % ctiles) * 32, r0 = (t / ctiles) * 32;
+    for (int y = ty; y < 32; y += ny) {  // read X[c0 + tx, r0 + y] (or D[o + r, c])
+      const int cc = c0 + tx, r = r0 + y;
+      double v = 0.0;
+      if (cc < n && r < pr) v = D ? D[(o + r) + static_cast<long long>(cc) * n] : Xi[cc + static_cast<long long>(r) * ld];
+      tile[y][tx] = v;
+    }
+    __syncthreads();
+    for (int y = ty; y < 32; y += ny) {  // write R[r0 + tx, c0 + y]
+      const int r = r0 + tx, cc = c0 + y;
+      if (r < pr && cc < n) Ri[r + static_cast<long long>(cc) * pr] = tile[tx][y];
+    }
+    __syncthreads();
+  }
+}
+__global__ void k_ras_unit_rhs(double* __restrict__ X, const long long* __restrict__ xoff, const int* __restrict__ ldx,
+                               const int* __restrict__ own_off, const int* __restrict__ own_n) {
+  const int i = blockIdx.x;
+  for (int r = threadIdx.x; r < own_n[i]; r += blockDim.x)
+    X[xoff[i] + (own_off[i] + r) + static_cast<long long>(r) * ldx[i]] = 1.0;
+}
+
 constexpr int kRasRows = 4;  // row chunks of 32 per lane pass (128 rows; larger panels loop)
 
 template <bool TR>
@@ -1151,9 +1191,63 @@ __global__ void __launch_bounds__(256) k_ras_apply(const double* __restrict__ R,
 
 }  // namespace
 
+// X_i = A_i⁻¹ E_own for every factor-path subdomain, E_own the identity columns of the owned run:
+// the forward and backward triangular solves of all p_i right-hand sides as batched DMMA products
+// over the envelope-packed factor. A block row of the packing is a contiguous 64 x 64·(k − first_k)
+// column-major matrix (lda = 64), so the forward step k is Y_k = D_k (E_k − L[k, first:k] Y[first:k])
+// (one NN product per subdomain and step, then the in-place product with D_k = L_kk⁻¹), and the
+// backward pass is row-wise like the apply's: X_i = D_iᵀ Y_i, then Y[first:i] −= L[i, first:i]ᵀ X_i
+// (TN products). Rows above the owned run stay zero in the forward pass and are skipped.
+static void ras_factor_solves(Ctx& c, const std::vector<int>& oo, const std::vector<int>& on, double* X,
+                              const std::vector<long long>& xoff, const std::vector<int>& ldx,
+                              const std::vector<double*>& dense) {
+  const int J = static_cast<int>(oo.size());
+  int nbmax = 0;
+  for (int i = 0; i < J; ++i) nbmax = std::max(nbmax, ldx[i] / NB);
+  auto tile = [&](int i, int k, int j) {  // tile (k, j) of subdomain i's packed factor
+    return c.P.p + c.P_off[i] + static_cast<long long>(c.env_base[c.env_off[i] + k] + j) * (NB * NB);
+  };
+  std::vector<GemmTask> ta, tb;
+  for (int k = 0; k < nbmax; ++k) {  // forward
+    ta.clear();
+    tb.clear();
+    for (int i = 0; i < J; ++i) {
+      if (dense[i] || k >= ldx[i] / NB || k < oo[i] / NB) continue;
+      const int j0 = std::max(c.env_first[c.env_off[i] + k], oo[i] / NB);  // Y_j = 0 above the owned run
+      double* Wk = X + xoff[i] + static_cast<long long>(k) * NB;
+      for (int tn = 0; tn < ceil_div(on[i], NB); ++tn) {
+        if (k > j0)
+          ta.push_back({tile(i, k, j0), X + xoff[i] + static_cast<long long>(j0) * NB, Wk, nullptr, nullptr, NB, on[i],
+                        NB * (k - j0), NB, ldx[i], ldx[i], 0, tn, 1.0, -1.0});
+        tb.push_back({tile(i, k, k), Wk, Wk, nullptr, nullptr, NB, on[i], NB, NB, ldx[i], ldx[i], 0, tn, 0.0, 1.0});
+      }
+    }
+    gemm_nn(c, ta);
+    gemm_nn(c, tb);  // in place: a CTA reads its whole 64-row column tile before its epilogue writes it
+  }
+  for (int k = nbmax - 1; k >= 0; --k) {  // backward, row by row
+    ta.clear();
+    tb.clear();
+    for (int i = 0; i < J; ++i) {
+      if (dense[i] || k >= ldx[i] / NB) continue;
+      const int j0 = c.env_first[c.env_off[i] + k];
+      double* Wk = X + xoff[i] + static_cast<long long>(k) * NB;
+      for (int tn = 0; tn < ceil_div(on[i], NB); ++tn) {
+        tb.push_back({tile(i, k, k), Wk, Wk, nullptr, nullptr, NB, on[i], NB, NB, ldx[i], ldx[i], 0, tn, 0.0, 1.0});
+        for (int tm = 0; tm < k - j0; ++tm)
+          ta.push_back({tile(i, k, j0), Wk, X + xoff[i] + static_cast<long long>(j0) * NB, nullptr, nullptr, NB * (k - j0),
+                        on[i], NB, NB, ldx[i], ldx[i], tm, tn, 1.0, -1.0});
+      }
+    }
+    gemm_tn(c, tb);  // X_k = D_kᵀ Y_k, in place
+    gemm_tn(c, ta);  // Y[first:k] -= L[k, first:k]ᵀ X_k
+  }
+}
+
 void build_ras_panels(Ctx& c) {
   c.ras_panel = false;
-  if (c.pkind != RDD_PRECOND_RAS || !c.inv_mode) return;
+  if (c.pkind != RDD_PRECOND_RAS) return;
+  ScopedKernelTimer tk(c, "ras_panels");
   const int J = static_cast<int>(c.set_ptr.size()) - 1;
   std::vector<int> oo(J), on(J);
   c.ras_off.assign(J + 1, 0);
@@ -1163,7 +1257,7 @@ void build_ras_panels(Ctx& c) {
       if (c.h_owner[c.set_idx[q]] == i) {
         const int pos = q - c.set_ptr[i];
         if (first < 0) first = pos;
-        if (last >= 0 && pos != last + 1) return;  // not contiguous: keep the inverse path
+        if (last >= 0 && pos != last + 1) return;  // not contiguous: keep the full local solves
         last = pos;
         ++cnt;
       }
@@ -1175,9 +1269,39 @@ void build_ras_panels(Ctx& c) {
   c.down_n.upload(on, c.stream);
   c.dras_off.upload(c.ras_off, c.stream);
   c.Pras.ensure(static_cast<size_t>(std::max<long long>(1, c.ras_off[J])));
-  k_ras_panel<<<J, 256, 0, c.stream>>>(c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.down_off.p, c.down_n.p,
-                                       c.dras_off.p, c.Pras.p);
-  RDD_LAUNCH_CHECK();
+  if (c.inv_mode) {
+    k_ras_panel<<<J, 256, 0, c.stream>>>(c.P.p, c.dP_off.p, c.dfb_ptr.p, c.dset_ptr.p, c.down_off.p, c.down_n.p,
+                                         c.dras_off.p, c.Pras.p);
+    RDD_LAUNCH_CHECK();
+  } else {
+    // factor mode (large blocks): solve for the owned right-hand sides once, keep the panel
+    std::vector<long long> xoff(J + 1, 0);
+    std::vector<int> ldx(J);
+    std::vector<double*> dense(J, nullptr);
+    for (int i = 0; i < J; ++i) {
+      ldx[i] = ceil_div(c.local_n[i], NB) * NB;
+      auto it = c.fb_store.find(i);
+      if (it != c.fb_store.end()) dense[i] = it->second.p;
+      xoff[i + 1] = xoff[i] + (dense[i] ? 0 : static_cast<long long>(ldx[i]) * on[i]);
+    }
+    double* X = c.ws("ras.X", static_cast<size_t>(std::max<long long>(1, xoff[J])));
+    RDD_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * static_cast<size_t>(xoff[J]), c.stream));
+    DBuf<long long> dxoff;
+    DBuf<int> dldx;
+    dxoff.upload(xoff, c.stream);
+    dldx.upload(ldx, c.stream);
+    std::vector<int> on_f(on);
+    for (int i = 0; i < J; ++i)
+      if (dense[i]) on_f[i] = 0;  // no unit columns for the dense blocks (no X storage)
+    DBuf<int> don_f;
+    don_f.upload(on_f, c.stream);
+    k_ras_unit_rhs<<<J, 256, 0, c.stream>>>(X, dxoff.p, dldx.p, c.down_off.p, don_f.p);
+    RDD_LAUNCH_CHECK();
+    ras_factor_solves(c, oo, on, X, xoff, ldx, dense);
+    k_ras_panel_x<<<dim3(64, J), 256, 0, c.stream>>>(X, dxoff.p, dldx.p, c.dfb_ptr.p, c.dset_ptr.p, c.down_off.p,
+                                                    c.down_n.p, c.dras_off.p, c.Pras.p);
+    RDD_LAUNCH_CHECK();
+  }
   RDD_CUDA(cudaStreamSynchronize(c.stream));
   c.ras_panel = true;
 }

@@ -349,16 +349,23 @@ def test_eigen_fallback_reference_default(dev, orc, kind):
     assert abs(sd["iterations"] - so["iterations"]) <= int(0.05 * so["iterations"]), (sd, so)
 
 
-@pytest.mark.parametrize("name", ["runner77", "c2_slice", "c4_slice", "example3"])
+# local orders in (322, 386]: the batched Jacobi eigensolver takes its 3-CTA cluster form there
+# (the packed triangle fits three CTAs' shared memory; jacobi.cu oe_k)
+CASES_EIGEN = {"c2_slice_k3": configs.scaled(configs.c2(), [3, 3], 10, m=42)}
+
+
+@pytest.mark.parametrize("name", ["runner77", "c2_slice", "c4_slice", "example3", "c2_slice_k3"])
 def test_all_blocks_eigen_path(dev, orc, name):
     # full_rank_cond = 0 routes every local block to the eigen pseudo-inverse (the reference's
     # own method): the applies then agree with the oracle's to rounding of the eigensolvers
-    cfg = CASES[name]
+    cfg = CASES.get(name) or CASES_EIGEN[name]
     dev.set_param("full_rank_cond", 0.0)
     try:
         dev.build_instance(cfg).assemble(True).build_preconditioner(A.PRECOND_AS)
         orc.build_instance(cfg).assemble(True).build_preconditioner(A.PRECOND_AS)
         assert int(dev.geti("n_fallback")[0]) == int(dev.geti("J")[0])
+        if name == "c2_slice_k3":
+            assert 322 < int(dev.geti("local_n").max()) <= 386
         assert np.array_equal(dev.geti("local_rank"), orc.geti("local_rank"))
         p = int(orc.geti("p")[0])
         v = np.random.default_rng(23).standard_normal(p)

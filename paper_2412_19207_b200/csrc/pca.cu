@@ -310,51 +310,85 @@ constexpr int kHP = 32;
 constexpr int kHouseMaxM = 512;
 constexpr int kHBThreads = 512;
 constexpr int kHBWarps = kHBThreads / 32;
+__host__ __device__ constexpr int house_ldp(int n) { return n + ((20 - (n & 15)) & 15); }
 
 
-// y (global column, rows p..m-1) <- y - V M (Vᵀ y), M = T (transposed when tr): one warp
-__device__ __forceinline__ void wy_update(const double* __restrict__ P, int ldp, int R, int w, const double* Tm,
-                                          bool tr, double* y, double* scr, int lane) {
-  double s[kHP];
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+// A 32 x 8 matrix held as four DMMA accumulator fragments (tile mt: m = 8 mt + lane/4, n = 2 (lane%4) + e)
+// -> its B fragment of k-step kk: the value at (k = 4 kk + lane%4, n = lane/4)
+__device__ __forceinline__ double c_to_b(const double (&acc)[4][2], int kk, int lane) {
+  const int mt = kk >> 1;
+  const int src = ((4 * (kk & 1) + (lane & 3)) << 2) | (lane >> 3);
+  const double v0 = __shfl_sync(0xffffffffu, acc[mt][0], src);
+  const double v1 = __shfl_sync(0xffffffffu, acc[mt][1], src);
+  return ((lane >> 2) & 1) ? v1 : v0;
+}
+
+// Eight trailing columns at once on the FP64 tensor cores (one warp): Y <- Y - V M (Vᵀ Y) with
+// V = the panel in shared memory (R x w, zero above its diagonal, column stride ldp ≡ 4 mod 16 so
+// the fragment reads are conflict-free), M = T (transposed when tr), Y = global columns
+// c0 .. min(c0 + 8, cend) - 1 (rows 0..R-1 of the pointer, column stride ldy). W = VᵀY accumulates
+// over the rows in four 8 x 8 fragments, Z = M W and the update Y -= V Z are DMMA products too:
+// every panel element is read once per eight columns instead of once per column.
+__device__ __forceinline__ void wy_update8(const double* __restrict__ P, int ldp, int R, int w, const double* Tm,
+                                           bool tr, double* Y, int ldy, int c0, int cend, int lane) {
+  double wa[4][2];
 #pragma unroll
-  for (int i = 0; i < kHP; ++i) s[i] = 0.0;
-  for (int row = lane; row < R; row += 32) {
-    const double yr = y[row];
+  for (int mt = 0; mt < 4; ++mt) wa[mt][0] = wa[mt][1] = 0.0;
+  {
+    const int col = c0 + (lane >> 2);
+    const double* yc = Y + static_cast<long long>(col) * ldy;
+    for (int r = 0; r < R; r += 4) {
+      const int row = r + (lane & 3);
+      const bool rv = row < R;
+      const double bfr = (rv && col < cend) ? yc[row] : 0.0;
 #pragma unroll
-    for (int i = 0; i < kHP; ++i)
-      if (i < w) s[i] += P[i * ldp + row] * yr;  // V[:, i] is zero above row i (zeroed in smem)
-  }
-  // transpose-reduce: lane i ends with (Vᵀy)_i
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < o; ++i) {
-      const double send = up ? s[i] : s[i + o];
-      const double keep = up ? s[i + o] : s[i];
-      s[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      for (int mt = 0; mt < 4; ++mt) {
+        const int i = 8 * mt + (lane >> 2);
+        const double afr = (rv && i < w) ? P[i * ldp + row] : 0.0;
+        dmma884(wa[mt], afr, bfr);
+      }
     }
   }
-  scr[lane] = s[0];
-  __syncwarp();
-  double z = 0.0;  // z = M·(Vᵀy): Tᵀ for the factorisation (Qᵀ applied), T for Q
-  if (lane < w) {
-    if (tr)
-      for (int i = 0; i <= lane; ++i) z += Tm[i * kHP + lane] * scr[i];
-    else
-      for (int i = lane; i < w; ++i) z += Tm[lane * kHP + i] * scr[i];
-  }
-  __syncwarp();
-  scr[kHP + lane] = z;
-  __syncwarp();
-  for (int row = lane; row < R; row += 32) {
-    double a = 0.0;
+  double za[4][2];
 #pragma unroll
-    for (int i = 0; i < kHP; ++i)
-      if (i < w) a += P[i * ldp + row] * scr[kHP + i];
-    y[row] -= a;
+  for (int mt = 0; mt < 4; ++mt) za[mt][0] = za[mt][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const double bfr = c_to_b(wa, kk, lane);
+    const int kc = 4 * kk + (lane & 3);
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int i = 8 * mt + (lane >> 2);
+      double afr = 0.0;
+      if (i < w && kc < w) afr = tr ? Tm[kc * kHP + i] : Tm[i * kHP + kc];
+      dmma884(za[mt], afr, bfr);
+    }
   }
-  __syncwarp();
+  double bz[8];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) bz[kk] = c_to_b(za, kk, lane);
+  const int cc = c0 + 2 * (lane & 3);
+  for (int r0 = 0; r0 < R; r0 += 8) {
+    const int row = r0 + (lane >> 2);
+    double* y0 = Y + row + static_cast<long long>(cc) * ldy;
+    const bool v0 = row < R && cc < cend, v1 = row < R && cc + 1 < cend;
+    double acc[2];
+    acc[0] = v0 ? y0[0] : 0.0;
+    acc[1] = v1 ? y0[ldy] : 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int i = 4 * kk + (lane & 3);
+      const double afr = (row < R && i < w) ? -P[i * ldp + row] : 0.0;
+      dmma884(acc, afr, bz[kk]);
+    }
+    if (v0) y0[0] = acc[0];
+    if (v1) y0[ldy] = acc[1];
+  }
 }
 
 __global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __restrict__ Vr,
@@ -364,12 +398,12 @@ __global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __re
                                                                double* __restrict__ A, double* __restrict__ Q,
                                                                double* __restrict__ Tw) {
   extern __shared__ double hsm[];
-  double* P = hsm;                            // panel: kHP columns, ld n
-  double* Tm = P + static_cast<size_t>(kHP) * n;  // kHP x kHP (row i, column j at i*kHP + j)
+  const int ldp = house_ldp(n);               // panel column stride ≡ 4 mod 16 (conflict-free DMMA fragments)
+  double* P = hsm;                            // panel: kHP columns, ld ldp
+  double* Tm = P + static_cast<size_t>(kHP) * ldp;  // kHP x kHP (row i, column j at i*kHP + j)
   double* beta = Tm + kHP * kHP;              // kHP
   double* G = beta + kHP;                     // kHP x kHP: VᵀV
-  double* scr = G + kHP * kHP;                // per warp 2*kHP
-  double* red = scr + kHBWarps * 2 * kHP;     // kHBWarps
+  double* red = G + kHP * kHP;                // kHBWarps
   int* perm = reinterpret_cast<int*>(red + kHBWarps);  // n
   const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = rr[j];
@@ -398,10 +432,10 @@ __global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __re
   for (int p = 0, pi = 0; p < r; p += kHP, ++pi) {
     const int w = min(kHP, r - p), R = n - p;
     for (int c = 0; c < w; ++c)
-      for (int i = tid; i < R; i += blockDim.x) P[c * n + i] = Aj[(p + i) + static_cast<size_t>(p + c) * n];
+      for (int i = tid; i < R; i += blockDim.x) P[c * ldp + i] = Aj[(p + i) + static_cast<size_t>(p + c) * n];
     __syncthreads();
     for (int c = 0; c < w; ++c) {  // the panel's reflectors (column norms over the whole CTA)
-      double* x = P + c * n;
+      double* x = P + c * ldp;
       double s2 = 0.0;
       for (int i = c + tid; i < R; i += blockDim.x) s2 += x[i] * x[i];
       s2 = warp_sum(s2);
@@ -420,7 +454,7 @@ __global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __re
       }
       __syncthreads();
       for (int cc = c + 1 + warp; cc < w; cc += kHBWarps) {  // the panel's own later columns
-        double* y = P + cc * n;
+        double* y = P + cc * ldp;
         double t = 0.0;
         for (int i = c + lane; i < R; i += 32) t += x[i] * y[i];
         t = warp_sum(t) * b;
@@ -430,8 +464,8 @@ __global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __re
     }
     for (int c = 0; c < w; ++c)  // store v (and R above it) back; keep V with zeros above the diagonal
       for (int i = tid; i < R; i += blockDim.x) {
-        Aj[(p + i) + static_cast<size_t>(p + c) * n] = P[c * n + i];
-        if (i < c) P[c * n + i] = 0.0;
+        Aj[(p + i) + static_cast<size_t>(p + c) * n] = P[c * ldp + i];
+        if (i < c) P[c * ldp + i] = 0.0;
       }
     __syncthreads();
     // T: T_cc = β_c; T[0:c, c] = -β_c T[0:c, 0:c] (V[:, 0:c]ᵀ v_c)
@@ -439,7 +473,7 @@ __global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __re
       const int a = e / w, bcol = e % w;
       if (a >= bcol) continue;
       double t = 0.0;
-      for (int i = bcol + lane; i < R; i += 32) t += P[a * n + i] * P[bcol * n + i];
+      for (int i = bcol + lane; i < R; i += 32) t += P[a * ldp + i] * P[bcol * ldp + i];
       t = warp_sum(t);
       if (lane == 0) G[a * kHP + bcol] = t;
     }
@@ -459,8 +493,8 @@ __global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __re
     __syncthreads();
     for (int e = tid; e < kHP * kHP; e += blockDim.x) Tj[pi * kHP * kHP + e] = Tm[e];
     // trailing columns: y <- (I - V T Vᵀ)ᵀ y = y - V Tᵀ (Vᵀ y)
-    for (int c = p + w + warp; c < r; c += kHBWarps)
-      wy_update(P, n, R, w, Tm, true, Aj + p + static_cast<size_t>(c) * n, scr + warp * 2 * kHP, lane);
+    for (int c0 = p + w + 8 * warp; c0 < r; c0 += 8 * kHBWarps)
+      wy_update8(P, ldp, R, w, Tm, true, Aj + p, n, c0, r, lane);
     __syncthreads();
   }
   // ---- Q = H_0 ⋯ H_{r-1} [I_r; 0], panels in reverse
@@ -470,17 +504,17 @@ __global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __re
   for (int pi = np - 1; pi >= 0; --pi) {
     const int p = pi * kHP, w = min(kHP, r - p), R = n - p;
     for (int c = 0; c < w; ++c)
-      for (int i = tid; i < R; i += blockDim.x) P[c * n + i] = i < c ? 0.0 : Aj[(p + i) + static_cast<size_t>(p + c) * n];
+      for (int i = tid; i < R; i += blockDim.x) P[c * ldp + i] = i < c ? 0.0 : Aj[(p + i) + static_cast<size_t>(p + c) * n];
     for (int e = tid; e < kHP * kHP; e += blockDim.x) Tm[e] = Tj[pi * kHP * kHP + e];
     __syncthreads();
-    for (int c = p + warp; c < r; c += kHBWarps)
-      wy_update(P, n, R, w, Tm, false, Qj + p + static_cast<size_t>(c) * n, scr + warp * 2 * kHP, lane);
+    for (int c0 = p + 8 * warp; c0 < r; c0 += 8 * kHBWarps)
+      wy_update8(P, ldp, R, w, Tm, false, Qj + p, n, c0, r, lane);
     __syncthreads();
   }
 }
 
 size_t house_blocked_smem(int n) {
-  return (static_cast<size_t>(kHP) * n + 2 * kHP * kHP + kHP + kHBWarps * 2 * kHP + kHBWarps) * sizeof(double) +
+  return (static_cast<size_t>(kHP) * house_ldp(n) + 2 * kHP * kHP + kHP + kHBWarps) * sizeof(double) +
          static_cast<size_t>(n) * sizeof(int);
 }
 

@@ -391,7 +391,7 @@ __device__ __forceinline__ void wy_update8(const double* __restrict__ P, int ldp
   }
 }
 
-__global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __restrict__ Vr,
+__global__ void __launch_bounds__(kHBThreads, 2) k_house_blocked(const double* __restrict__ Vr,
                                                                const double* __restrict__ lam,
                                                                const long long* __restrict__ lam_off,
                                                                const int* __restrict__ rr, int n,
@@ -402,9 +402,11 @@ __global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __re
   double* P = hsm;                            // panel: kHP columns, ld ldp
   double* Tm = P + static_cast<size_t>(kHP) * ldp;  // kHP x kHP (row i, column j at i*kHP + j)
   double* beta = Tm + kHP * kHP;              // kHP
-  double* G = beta + kHP;                     // kHP x kHP: VᵀV
-  double* red = G + kHP * kHP;                // kHBWarps
-  int* perm = reinterpret_cast<int*>(red + kHBWarps);  // n
+  double* red = beta + kHP;                   // kHBWarps
+  // the column order (n ints) is only needed before the first panel: it borrows T's storage;
+  // VᵀV of a panel is kept in T's lower triangle until T is complete. 112 KB at n = 400: two
+  // CTAs per SM
+  int* perm = reinterpret_cast<int*>(Tm);
   const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = rr[j];
   const size_t off = static_cast<size_t>(j) * n * n;
@@ -475,21 +477,23 @@ __global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __re
       double t = 0.0;
       for (int i = bcol + lane; i < R; i += 32) t += P[a * ldp + i] * P[bcol * ldp + i];
       t = warp_sum(t);
-      if (lane == 0) G[a * kHP + bcol] = t;
+      if (lane == 0) Tm[bcol * kHP + a] = t;  // (VᵀV)[a, bcol], a < bcol, parked below the diagonal
     }
     __syncthreads();
     if (warp == 0) {
       for (int c = 0; c < w; ++c) {
         double t = 0.0;
         if (lane < c)
-          for (int k = lane; k < c; ++k) t += Tm[lane * kHP + k] * G[k * kHP + c];
+          for (int k = lane; k < c; ++k) t += Tm[lane * kHP + k] * Tm[c * kHP + k];
         __syncwarp();
         if (lane < c) Tm[lane * kHP + c] = -beta[c] * t;
         if (lane == c) Tm[c * kHP + c] = beta[c];
-        if (lane > c && lane < kHP) Tm[lane * kHP + c] = 0.0;
         __syncwarp();
       }
     }
+    __syncthreads();
+    for (int e = tid; e < kHP * kHP; e += blockDim.x)
+      if (e / kHP > e % kHP) Tm[e] = 0.0;  // T is upper triangular
     __syncthreads();
     for (int e = tid; e < kHP * kHP; e += blockDim.x) Tj[pi * kHP * kHP + e] = Tm[e];
     // trailing columns: y <- (I - V T Vᵀ)ᵀ y = y - V Tᵀ (Vᵀ y)
@@ -514,8 +518,7 @@ __global__ void __launch_bounds__(kHBThreads) k_house_blocked(const double* __re
 }
 
 size_t house_blocked_smem(int n) {
-  return (static_cast<size_t>(kHP) * house_ldp(n) + 2 * kHP * kHP + kHP + kHBWarps) * sizeof(double) +
-         static_cast<size_t>(n) * sizeof(int);
+  return (static_cast<size_t>(kHP) * house_ldp(n) + kHP * kHP + kHP + kHBWarps) * sizeof(double);
 }
 
 // V0[:, :r_j] = Vs[:, :r_j] (m x r_j leading columns, column-major ld m)

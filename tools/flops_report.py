@@ -15,15 +15,21 @@ cfg.solver, cfg.precond = A.SOLVER_CG, A.PRECOND_AS
 s = rdd.Solver(0)
 s.run_single(cfg)
 s.set_timing(True)
-s.reset_stats()
-s.rerun_resident()
+best = {}
+for _ in range(3):  # the timed mode synchronises around every family: keep each family's best of three
+    s.reset_stats()
+    s.rerun_resident()
+    for fam in ("gram", "cholesky", "assemble"):
+        ms_f, n_f = s.kernel_stats(fam)
+        if fam not in best or ms_f < best[fam][0]:
+            best[fam] = (ms_f, n_f)
 rp = s.geti("row_ptr").astype(np.float64)
 rows = np.diff(rp)
 m = cfg.m
 n = s.geti("local_n").astype(np.float64)
-g_ms, _ = s.kernel_stats("gram")
-c_ms, _ = s.kernel_stats("cholesky")
-a_ms, a_n = s.kernel_stats("assemble")
+g_ms, _ = best["gram"]
+c_ms, _ = best["cholesky"]
+a_ms, a_n = best["assemble"]
 gram = float((rows * m * (m + 1)).sum())
 chol = float((n ** 3 / 3).sum())
 # flops the factorisation performs inside the envelopes (64-wide tiles): per step k the diagonal

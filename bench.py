@@ -21,8 +21,9 @@ Schwarz -> PCG -> test evaluation) of one seed. --config C1..C4 selects the othe
 
 N>1 (torchrun): replicas — every rank solves its own seed (seed + rank) on its own GPU; the
 path has no data exchange in this tier. --impl reference: rank 0
-measures one complete C5s solve of the compiled reference and reports value = null with the
-reason (a full C5 solve on the host takes hours).
+alone times the compiled reference on a bounded sample of the workload per step (one complete
+C5s solve; a full C5 solve on the host takes hours) and reports that measured time as value,
+saying so in sample_note; nothing is extrapolated.
 """
 from __future__ import annotations
 

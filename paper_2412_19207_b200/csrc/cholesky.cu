@@ -30,6 +30,19 @@ struct Mat {
   int n;          // order (= leading dimension)
 };
 
+// Layout of a packed explicit inverse (small-block mode): lower 64 x 64 tiles (k, j <= k), block row
+// after block row, column-major; the tiles of the LAST block row keep only ld = inv_last_ld(n) rows
+// (the n - 64(nb-1) valid ones rounded up to 8), so the zero padding below row n is not stored
+// (n = 487: 40 of 64 rows, 8% of the bytes; n = 525: 16 of 64, 15%).
+__host__ __device__ inline int inv_last_ld(int n) {
+  const int bs = n - ((n + NB - 1) / NB - 1) * NB;
+  return (bs + 7) & ~7;
+}
+__host__ __device__ inline int inv_tile_ld(int n, int k) { return k == (n + NB - 1) / NB - 1 ? inv_last_ld(n) : NB; }
+__host__ __device__ inline long long inv_tile_off(int n, int k, int j) {  // in doubles
+  return static_cast<long long>(k) * (k + 1) / 2 * (NB * NB) + static_cast<long long>(j) * NB * inv_tile_ld(n, k);
+}
+
 // A[k-block, k-block] <- chol (lower); pads beyond n act as identity. Also D_k = L_kk⁻¹ (lower,
 // padding identity) into the per-matrix diagonal-inverse workspace: the panel solve becomes a DMMA
 // product with D_kᵀ and the packed factor stores D_k.
@@ -128,19 +141,20 @@ __global__ void k_set_diag(double* __restrict__ Mi, const Mat* __restrict__ mats
     if (r < bs && cc < bs) Mi[M.off + (k0 + r) + static_cast<long long>(k0 + cc) * M.n] = d[e];
   }
 }
-// block row k of the packed lower tiles of a full symmetric matrix (lower triangle valid)
+// block row k of the packed lower tiles of a full symmetric matrix (lower triangle valid), in the
+// explicit-inverse layout (inv_tile_off / inv_tile_ld)
 __global__ void k_pack_lower(const double* __restrict__ F, const Mat* __restrict__ mats, const int2* __restrict__ tasks,
                              double* __restrict__ P, const long long* __restrict__ poff) {
   const int2 t = tasks[blockIdx.x];
   const Mat M = mats[t.x];
   const int k = t.y, k0 = k * NB, bs = min(NB, M.n - k0);
-  double* row = P + poff[t.x] + static_cast<long long>(k) * (k + 1) / 2 * (NB * NB);
+  const int ld = inv_tile_ld(M.n, k);
   for (int j = 0; j <= k; ++j) {
     const double* a = F + M.off + k0 + static_cast<long long>(j * NB) * M.n;
     const int bj = min(NB, M.n - j * NB);
-    double* o = row + static_cast<long long>(j) * NB * NB;
-    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
-      const int r = e % NB, c = e / NB;
+    double* o = P + poff[t.x] + inv_tile_off(M.n, k, j);
+    for (int e = threadIdx.x; e < ld * NB; e += blockDim.x) {
+      const int r = e % ld, c = e / ld;
       double v = 0.0;
       if (r < bs && c < bj) v = (j < k || r >= c) ? a[r + static_cast<long long>(c) * M.n]
                                                   : a[c + static_cast<long long>(r) * M.n];  // diag tile: mirror
@@ -402,8 +416,9 @@ __device__ void chol_solve(const double* __restrict__ P, int nb, double* v, doub
 // (diagonal tiles full). Each tile is read once and serves both y_k += P_kj v_j and, for j < k,
 // y_j += P_kjᵀ v_k (32 columns per 31 shuffles); every warp accumulates into its own partial
 // vector in shared memory (part: kSolveWarps x nb*64), summed in warp order: deterministic.
-__device__ void symv_packed(const double* __restrict__ P, int nb, double* v, double* part, int t0 = 0, int tstep = 1) {
+__device__ void symv_packed(const double* __restrict__ P, int n, double* v, double* part, int t0 = 0, int tstep = 1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  const int nb = (n + NB - 1) / NB;
   const int len = nb * NB;
   double* my = part + static_cast<size_t>(warp) * len;
   for (int i = lane; i < len; i += 32) my[i] = 0.0;
@@ -416,7 +431,9 @@ __device__ void symv_packed(const double* __restrict__ P, int nb, double* v, dou
     ++k;
   }
   for (int t = first; t < T; t += stride) {
-    const double* tile = P + static_cast<long long>(t) * (NB * NB);
+    const double* tile = P + inv_tile_off(n, k, j);
+    const int ld = inv_tile_ld(n, k);
+    const bool rv = 2 * lane < ld;  // rows 2 lane, 2 lane + 1 are stored (ld is a multiple of 8)
     const double* gj = v + j * NB;
     const double gk0 = v[k * NB + 2 * lane], gk1 = v[k * NB + 2 * lane + 1];
     double a0 = 0.0, a1 = 0.0;
@@ -425,7 +442,8 @@ __device__ void symv_packed(const double* __restrict__ P, int nb, double* v, dou
       double p[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
-        const double2 a = __ldcs(reinterpret_cast<const double2*>(tile + (h * 32 + c) * NB) + lane);
+        double2 a = make_double2(0.0, 0.0);
+        if (rv) a = __ldcs(reinterpret_cast<const double2*>(tile + (h * 32 + c) * ld) + lane);
         const double gc = gj[h * 32 + c];
         a0 += a.x * gc;
         a1 += a.y * gc;
@@ -496,7 +514,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32) k_chol_power(const double* _
     if (it == iters || !(nrm > 0.0)) break;
     for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] /= nrm;
     __syncthreads();
-    if (inverse) symv_packed(P + poff[i], nb, x, red);
+    if (inverse) symv_packed(P + poff[i], n, x, red);
     else chol_solve(P + poff[i], nb, x, red, efirst + eoff[i], ebase + eoff[i]);
   }
   if (threadIdx.x == 0) out[i] = lam;
@@ -776,6 +794,10 @@ long long packed_chol_size(int n) {
   const long long nb = ceil_div(n, NB);
   return nb * (nb + 1) / 2 * NB * NB;
 }
+long long packed_inverse_size(int n) {  // explicit-inverse layout: trimmed last block row
+  const long long nb = ceil_div(n, NB);
+  return (nb - 1) * nb / 2 * NB * NB + nb * NB * inv_last_ld(n);
+}
 
 size_t chol_solve_smem(int nmax, bool inverse) {
   const size_t len = static_cast<size_t>(ceil_div(nmax, NB)) * NB;
@@ -899,7 +921,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
-constexpr int kTmaStages = 2;
+constexpr int kTmaStages = 3;
 constexpr int kTileBytes = NB * NB * sizeof(double);
 
 __global__ void __launch_bounds__((kSolveWarps + 1) * 32) k_inv_apply_tma(
@@ -954,13 +976,23 @@ __global__ void __launch_bounds__((kSolveWarps + 1) * 32) k_inv_apply_tma(
   const double* Pi = P + poff[i];
   if (warp == kSolveWarps) {  // producer
     if (lane == 0) {
-      int it = 0;
+      int it = 0, pk = 0, pj = h;  // tile t = pk(pk+1)/2 + pj
+      while (pj > pk) {
+        pj -= pk + 1;
+        ++pk;
+      }
       for (int t = h; t < T; t += 2, ++it) {
         const int b = it % kTmaStages;
         if (it >= kTmaStages) mbar_wait(&empty[b], ((it / kTmaStages) - 1) & 1);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&full[b], kTileBytes);
-        bulk_load(ring + b * NB * NB, Pi + static_cast<long long>(t) * (NB * NB), kTileBytes, &full[b]);
+        const uint32_t bytes = static_cast<uint32_t>(NB * inv_tile_ld(n, pk) * sizeof(double));
+        mbar_expect_tx(&full[b], bytes);
+        bulk_load(ring + b * NB * NB, Pi + inv_tile_off(n, pk, pj), bytes, &full[b]);
+        pj += 2;
+        while (pj > pk && pk < nb) {
+          pj -= pk + 1;
+          ++pk;
+        }
       }
     }
     return;
@@ -977,12 +1009,15 @@ __global__ void __launch_bounds__((kSolveWarps + 1) * 32) k_inv_apply_tma(
     const int b = it % kTmaStages;
     mbar_wait(&full[b], (it / kTmaStages) & 1);
     const double* tile = ring + b * NB * NB;
+    const int ld = inv_tile_ld(n, k);      // rows stored per tile column (the last block row is trimmed)
+    const bool rv = 2 * lane < ld;
     const double gk0 = g[k * NB + 2 * lane], gk1 = g[k * NB + 2 * lane + 1];
     double p[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int col = warp * 8 + c;
-      const double2 a = reinterpret_cast<const double2*>(tile + col * NB)[lane];
+      double2 a = make_double2(0.0, 0.0);
+      if (rv) a = reinterpret_cast<const double2*>(tile + col * ld)[lane];
       const double gc = g[j * NB + col];
       a0 += a.x * gc;
       a1 += a.y * gc;
@@ -1085,8 +1120,8 @@ __global__ void k_ras_panel(const double* __restrict__ P, const long long* __res
         a = b;
         b = t;
       }
-      const int tk = a / NB, tj = b / NB;  // dense packing of the explicit inverse
-      v = (Pi + (static_cast<long long>(tk) * (tk + 1) / 2 + tj) * (NB * NB))[(a % NB) + (b % NB) * NB];
+      const int tk = a / NB, tj = b / NB;  // packed explicit inverse (inv_tile_off / inv_tile_ld)
+      v = (Pi + inv_tile_off(n, tk, tj))[(a % NB) + (b % NB) * inv_tile_ld(n, tk)];
     }
     Ri[e] = v;
   }

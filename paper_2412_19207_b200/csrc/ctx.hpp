@@ -356,6 +356,7 @@ void batched_cholesky_pack(Ctx& c, double* A, const std::vector<int>& ids, const
                            std::vector<int>& fail, std::vector<double>& frob_A, bool inverse = false,
                            std::vector<double>* frob_P = nullptr, double** Pfull_out = nullptr);
 long long packed_chol_size(int n);
+long long packed_inverse_size(int n);
 size_t chol_solve_smem(int nmax, bool inverse);
 std::vector<double> batched_inv_power(Ctx& c, const double* P, const std::vector<int>& ids, const std::vector<int>& n,
                                       const std::vector<long long>& poff, int iters, bool inverse);

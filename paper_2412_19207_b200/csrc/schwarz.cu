@@ -361,7 +361,7 @@ void build_schwarz(Ctx& c, int kind, SchwarzIndex* pre) {
       eb[k] = static_cast<int>(tiles) - ef[k];
       tiles += k - ef[k] + 1;
     }
-    c.P_off[i + 1] = c.P_off[i] + tiles * 64 * 64;
+    c.P_off[i + 1] = c.P_off[i] + (c.inv_mode ? packed_inverse_size(n[i]) : tiles * 64 * 64);
   }
   c.denv_off.upload(c.env_off, c.stream);
   c.denv_first.upload(c.env_first, c.stream);

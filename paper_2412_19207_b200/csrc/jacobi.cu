@@ -194,15 +194,17 @@ __global__ void __launch_bounds__(256) k_apply_rotations_oe(double* __restrict__
                                                             const long long* __restrict__ off,
                                                             const double2* __restrict__ rot,
                                                             const long long* __restrict__ rot_off,
-                                                            const int* __restrict__ sweeps, const int* __restrict__ ntrue) {
+                                                            const int* __restrict__ sweeps, const int* __restrict__ ntrue,
+                                                            int rpc) {
+  // rpc rows of V per CTA (at most kRows; fewer for very large orders so the rows fit shared memory)
   extern __shared__ double vs[];
   const int b = blockIdx.y;
   const int n = nvec[b];  // padded (even)
-  const int r0 = blockIdx.x * kRows;
+  const int r0 = blockIdx.x * rpc;
   if (r0 >= n) return;
-  const int rows = min(kRows, n - r0);
+  const int rows = min(rpc, n - r0);
   const int ld = n + 1;
-  for (int e = threadIdx.x; e < kRows * n; e += blockDim.x) {
+  for (int e = threadIdx.x; e < rpc * n; e += blockDim.x) {
     const int rr = e / n, col = e % n;
     vs[rr * ld + col] = (rr < rows && r0 + rr == col) ? 1.0 : 0.0;
   }
@@ -213,8 +215,8 @@ __global__ void __launch_bounds__(256) k_apply_rotations_oe(double* __restrict__
     const int o = t & 1;
     const int npair = o ? n / 2 - 1 : n / 2;
     const double2* Rt = R + static_cast<long long>(t) * (n / 2);
-    for (int e = threadIdx.x; e < npair * kRows; e += blockDim.x) {
-      const int k = e / kRows, rr = e % kRows;
+    for (int e = threadIdx.x; e < npair * rpc; e += blockDim.x) {
+      const int k = e / rpc, rr = e % rpc;
       if (rr >= rows) continue;
       const double2 csn = Rt[k];
       const int p = o + 2 * k;
@@ -897,11 +899,13 @@ void batched_syevj(Ctx& c, double* A, double* V, double* evals, const std::vecto
     k_syevj_oe<<<B, 1024, smem, c.stream>>>(Wk.p, dnp.p, dwoff.p, evp.p, deoffp.p, max_sweeps, dsw.p, rot.p, droff.p,
                                              crit, o.floor_rel, o.conv_rel);
     RDD_LAUNCH_CHECK();
-    const size_t vsm = static_cast<size_t>(kRows) * (ne + 1) * sizeof(double);
+    // rows of V per CTA: kRows, or as many as fit shared memory (orders above ~900)
+    const int rpc = std::max(1, std::min<int>(kRows, static_cast<int>(kCtaSmem / (static_cast<size_t>(ne + 1) * sizeof(double)))));
+    const size_t vsm = static_cast<size_t>(rpc) * (ne + 1) * sizeof(double);
     RDD_CUDA(cudaFuncSetAttribute(k_apply_rotations_oe, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(vsm)));
-    k_apply_rotations_oe<<<dim3(ceil_div(ne, kRows), B), 256, vsm, c.stream>>>(Vp.p, dnp.p, dwoff.p, rot.p, droff.p,
-                                                                                 dsw.p, dn.p);
+    k_apply_rotations_oe<<<dim3(ceil_div(ne, rpc), B), 256, vsm, c.stream>>>(Vp.p, dnp.p, dwoff.p, rot.p, droff.p,
+                                                                               dsw.p, dn.p, rpc);
     RDD_LAUNCH_CHECK();
   }
   k_compact<<<B, 256, 0, c.stream>>>(Vp.p, evp.p, dwoff.p, deoffp.p, dn.p, dnp.p, V, doff.p, evals, doffE.p);

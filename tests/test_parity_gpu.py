@@ -435,6 +435,29 @@ def test_factor_mode_envelope(dev, orc, name):
         dev.set_param("inv_max", 1024.0)
 
 
+def test_factor_mode_ras_panels_with_eigen_blocks(dev, orc):
+    # RAS in factor mode with every local block on the eigen pseudo-inverse path: the owner-row
+    # panels are then read out of the dense pseudo-inverses instead of solved through the factors
+    cfg = FACTOR_CASES["c3_4x3x3_ras"]
+    dev.set_param("inv_max", 0.0)
+    dev.set_param("full_rank_cond", 0.0)
+    try:
+        dev.build_instance(cfg).assemble(True).build_preconditioner(A.PRECOND_RAS)
+        orc.build_instance(cfg).assemble(True).build_preconditioner(A.PRECOND_RAS)
+        assert int(dev.geti("inv_mode")[0]) == 0
+        assert int(dev.geti("n_fallback")[0]) == int(dev.geti("J")[0])
+        p = int(dev.geti("p")[0])
+        rng = np.random.default_rng(37)
+        tol = max(1e-10, 1e-14 * float(orc.getd("local_cond").max()))
+        for tr in (False, True):
+            v = rng.standard_normal(p)
+            zo, zd = orc.precond_apply(v, tr), dev.precond_apply(v, tr)
+            assert np.linalg.norm(zd - zo) <= tol * np.linalg.norm(zo), (tr, tol)
+    finally:
+        dev.set_param("inv_max", 1024.0)
+        dev.set_param("full_rank_cond", 1e9)
+
+
 # The device against the reference itself (oracle/_ref: the unmodified headers compiled here on
 # the Eigen-subset shim; the BASELINE slices built from the reference's own types), not only
 # against the restatement: same ranks, same iteration counts, errors and solutions within 1e-8.

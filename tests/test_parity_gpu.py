@@ -351,10 +351,12 @@ def test_eigen_fallback_reference_default(dev, orc, kind):
 
 # local orders in (322, 386]: the batched Jacobi eigensolver takes its 3-CTA cluster form there
 # (the packed triangle fits three CTAs' shared memory; jacobi.cu oe_k)
-CASES_EIGEN = {"c2_slice_k3": configs.scaled(configs.c2(), [3, 3], 10, m=42)}
+# local orders in (512, 640]: 8-CTA clusters and the shared-memory rotation replay (k_replay_oe)
+CASES_EIGEN = {"c2_slice_k3": configs.scaled(configs.c2(), [3, 3], 10, m=42),
+               "c5_slice_k8": configs.scaled(configs.aspcg("C5"), [3, 3, 3], 6, m=21)}
 
 
-@pytest.mark.parametrize("name", ["runner77", "c2_slice", "c4_slice", "example3", "c2_slice_k3"])
+@pytest.mark.parametrize("name", ["runner77", "c2_slice", "c4_slice", "example3", "c2_slice_k3", "c5_slice_k8"])
 def test_all_blocks_eigen_path(dev, orc, name):
     # full_rank_cond = 0 routes every local block to the eigen pseudo-inverse (the reference's
     # own method): the applies then agree with the oracle's to rounding of the eigensolvers
@@ -366,6 +368,8 @@ def test_all_blocks_eigen_path(dev, orc, name):
         assert int(dev.geti("n_fallback")[0]) == int(dev.geti("J")[0])
         if name == "c2_slice_k3":
             assert 322 < int(dev.geti("local_n").max()) <= 386
+        if name == "c5_slice_k8":
+            assert 512 < int(dev.geti("local_n").max()) <= 640
         assert np.array_equal(dev.geti("local_rank"), orc.geti("local_rank"))
         p = int(orc.geti("p")[0])
         v = np.random.default_rng(23).standard_normal(p)
@@ -431,6 +435,25 @@ def test_factor_mode_envelope(dev, orc, name):
         assert sd["iterations"] == its_inv
         if so["converged"]:  # under-resolved slices: e_L2 can exceed 1, the bar is then relative
             assert abs(sd["e_l2"] - so["e_l2"]) <= 1e-8 * max(1.0, so["e_l2"])
+    finally:
+        dev.set_param("inv_max", 1024.0)
+
+
+@pytest.mark.parametrize("solver,precond", [(A.SOLVER_BICG, A.PRECOND_SAS), (A.SOLVER_CGS, A.PRECOND_AS),
+                                            (A.SOLVER_GMRES, A.PRECOND_SAS)])
+def test_factor_mode_other_solvers(dev, orc, solver, precond):
+    # the transposed and weighted applies through the envelope-packed factors (BiCG's dual
+    # recurrence, SAS weights in front of the local solves) on a 3x3x3 slice forced into factor mode
+    cfg = A.Config.from_buffer_copy(FACTOR_CASES["c5_3x3x3"])
+    cfg.solver, cfg.precond, cfg.rel_tol, cfg.gmres_restart = solver, precond, 1e-8, 30
+    dev.set_param("inv_max", 0.0)
+    try:
+        so, sd = orc.run_single(cfg), dev.run_single(cfg)
+        assert int(dev.geti("inv_mode")[0]) == 0
+        assert sd["converged"] == so["converged"] and sd["breakdown"] == so["breakdown"], (sd, so)
+        assert abs(sd["iterations"] - so["iterations"]) <= max(1, int(0.05 * so["iterations"])), (sd["iterations"], so["iterations"])
+        if so["converged"]:
+            assert abs(sd["e_l2"] - so["e_l2"]) <= 1e-6 * max(1.0, so["e_l2"])
     finally:
         dev.set_param("inv_max", 1024.0)
 

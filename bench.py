@@ -181,6 +181,14 @@ def cpu_sample(threads: int):
     }
 
 
+def bench_config(workload: str, cfg, world: int) -> dict:
+    """The `config` object of both arms' lines (identical for the same workload and rank count)."""
+    return {"workload": workload,
+            "l2": "no flush needed: the resident working set (sample matrices, H, Schwarz factors) "
+                  "is tens of GB, far above the 126 MB L2",
+            "parallelism": f"replicas x{world} (one seed per GPU)", **cfg.as_dict()}
+
+
 def run_reference(args, cfg, world, rank, dist):
     """The reference arm: the reference's own CPU implementation of the path (oracle/_ref when it
     compiled, else the oracle port) on the host cores, each step a BOUNDED SAMPLE of the workload —
@@ -208,7 +216,7 @@ def run_reference(args, cfg, world, rank, dist):
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
         "ms_per_step": 1e3 * value, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (formula-defined problem, SplitMix64 bases as the reference)", "impl": "reference",
-        "config": {"workload": args.config, **cfg.as_dict()},
+        "config": bench_config(args.config, cfg, world),
         "sample_note": (f"each step is a bounded sample of {args.config}: one complete run_single of C5s (8 of the 512 "
                         f"subdomains, 1 PCG iteration instead of 81) on the host, measured; a complete {args.config} solve on "
                         f"the host takes hours. The ratio against this value understates the full-workload speed-up "
@@ -321,10 +329,7 @@ def run_device(args, cfg, world, rank, local, dist):
             "warmup": args.warmup, "ms_per_step": t_step_max * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (formula-defined problem, SplitMix64 bases as the reference)",
-            "config": {"workload": args.config,
-                       "l2": "no flush needed: the resident working set (sample matrices, H, Schwarz factors) "
-                             "is tens of GB, far above the 126 MB L2",
-                       "parallelism": f"replicas x{world} (one seed per GPU)", **cfg.as_dict()},
+            "config": bench_config(args.config, cfg, world),
             "solves_per_s": world / t_step_max,
             # the library's phase clocks are cumulative up to assembly; reported per phase here
             "phases_s": {"pca": ph["t_pca"], "assembly": ph["t_assemble"] - ph["t_pca"],

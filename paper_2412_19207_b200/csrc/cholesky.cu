@@ -60,26 +60,55 @@ __global__ void k_potrf_diag(double* __restrict__ A, const Mat* __restrict__ mat
     s[r][c] = (r < bs && c < bs) ? a[r + static_cast<long long>(c) * M.n] : (r == c ? 1.0 : 0.0);
   }
   __syncthreads();
-  __shared__ double d;
-  for (int c = 0; c < NB; ++c) {
-    if (threadIdx.x == 0) {
-      const double v = s[c][c];
-      if (!(v > 0.0)) fail[q] = 1;
-      d = sqrt(fmax(v, 1e-300));
-      s[c][c] = d;
-    }
-    __syncthreads();
-    for (int r = c + 1 + threadIdx.x; r < NB; r += blockDim.x) s[r][c] /= d;
-    __syncthreads();
-    {  // trailing update of the lower triangle: warps over rows, lanes over columns (no div/mod)
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-      for (int r = c + 1 + warp; r < NB; r += nw) {
-        const double src = s[r][c];
-        for (int qq = c + 1 + lane; qq <= r; qq += 32) s[r][qq] -= src * s[qq][c];
+  // Right-looking elimination with the tile in registers: thread (ty, tx) of the 16 x 16 grid owns
+  // the entries (ty + 16 i, tx + 16 j) (cyclic, so the shrinking active window stays spread over all
+  // threads). Per column: its owners publish the raw column, 64 threads scale it (one sqrt, one
+  // division each), everyone updates its own 16 entries — two barriers and no shared-memory
+  // read-modify-write. Every entry sees the same operations in the same order as the textbook
+  // loop (l = a / sqrt(a_cc); a_rq <- fma(-l_r, l_q, a_rq), c ascending).
+  __shared__ double col[NB], lbuf[NB];
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  double t[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t[i][j] = s[ty + 16 * i][tx + 16 * j];
+#pragma unroll
+  for (int jc = 0; jc < 4; ++jc) {
+    for (int cc = 0; cc < 16; ++cc) {
+      const int c = jc * 16 + cc;
+      if (tx == cc) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (ty + 16 * i >= c) col[ty + 16 * i] = t[i][jc];
       }
+      __syncthreads();
+      if (threadIdx.x < NB && static_cast<int>(threadIdx.x) >= c) {
+        const int r = threadIdx.x;
+        const double v = col[c];
+        const double d = sqrt(fmax(v, 1e-300));
+        if (r == c && !(v > 0.0)) fail[q] = 1;
+        const double l = r == c ? d : col[r] / d;
+        s[r][c] = l;
+        lbuf[r] = l;
+      }
+      __syncthreads();
+      double lr[4], lq[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        lr[i] = lbuf[ty + 16 * i];
+        lq[i] = lbuf[tx + 16 * i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = ty + 16 * i, qq = tx + 16 * j;
+          if (qq > c && qq <= r) t[i][j] = fma(-lr[i], lq[j], t[i][j]);
+        }
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
     const int r = e % NB, c = e / NB;
     if (r < bs && c < bs) a[r + static_cast<long long>(c) * M.n] = r >= c ? s[r][c] : 0.0;
